@@ -1,0 +1,187 @@
+/*
+ * pfg.h — C ABI of the B200-native batched LSH-forest k-NN index (PUFFINN, arXiv 1906.12211).
+ *
+ * The calls follow the paper's problem statement: the user gives only the space the index
+ * may use and the recall it must reach (PAPER.md:5 abstract, :38 §1.1, :371-374 §5
+ * "Parameter Choices"), i.e. build(data, n, d, memory budget, hash family, seed) and
+ * search(queries, k, recall target) -> ids and similarities, solving the (k, delta)-NN problem
+ * of PAPER.md:118-123 (Definition, delta = 1 - recall) on the unit sphere under angular distance
+ * (PAPER.md:133-135).
+ *
+ * Conventions (all calls):
+ *  - Every call returns a pfg_status and never aborts; pfg_last_error() returns a thread-local
+ *    message for the last non-OK status of the calling thread.
+ *  - Array arguments are plain pointers.  Unless a call says otherwise a pointer may be HOST or
+ *    DEVICE memory (of the index's device); the library inspects it with
+ *    cudaPointerGetAttributes and copies host arrays through internal device buffers.  The caller
+ *    owns every buffer it passes; the library never frees or retains caller pointers.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls enqueue work on it.
+ *    pfg_build and pfg_search synchronise `stream` before returning (they read back a small
+ *    status word to report zero rows); outputs in device memory are complete on return.
+ *  - Layouts are row-major and densely packed: data [n][d] fp32, queries [nq][d] fp32,
+ *    ids [nq][k] int64, sims [nq][k] fp32.
+ *  - Ids are global: local row r of the index is reported as r + id_offset (sharded mode).
+ */
+#ifndef PFG_H
+#define PFG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFG_ABI_VERSION 1
+
+typedef struct pfg_index pfg_index; /* opaque; owned by the library until pfg_free */
+
+typedef enum {
+    PFG_OK = 0,
+    PFG_E_ARG = 1,         /* invalid argument (n < 1, d < 1, k < 1 or k > 256, recall not in (0,1], ...) */
+    PFG_E_ZERO_VECTOR = 2, /* a data or query row has norm 0 and cannot be normalised */
+    PFG_E_BUDGET = 3,      /* memory budget below fixed cost + one repetition; message states the minimum */
+    PFG_E_CUDA = 4,        /* CUDA runtime error (message has the CUDA error string) or no device */
+    PFG_E_OOM = 5,         /* device allocation failed */
+    PFG_E_STATE = 7        /* call not valid for this index (e.g. export of a table that does not exist) */
+} pfg_status;
+
+/* LSH families (§2, 338-343 §4.3) */
+typedef enum {
+    PFG_SIMHASH = 0,               /* random hyperplane (HP): 1 bit = [<a,x> >= 0], a ~ N(0, I) */
+    PFG_CROSSPOLYTOPE_FHT = 1      /* cross-polytope via three rounds of random signs + fast Hadamard
+                                      transform: ell = 1 + log2(d') bits, d' = 2^ceil(log2 d) */
+} pfg_family;
+
+/* hash-function evaluation strategies (§3.2, App. B 841-917) */
+typedef enum {
+    PFG_INDEPENDENT = 0,  /* every repetition has its own functions (Alg. 1) */
+    PFG_POOL = 1          /* repetitions sample functions without replacement from one pool (Alg. 3) */
+} pfg_strategy;
+
+/* Build options.  Zero-initialise and set struct_size = sizeof(pfg_build_opts); a zero field
+ * takes the default in brackets.  NULL opts = all defaults. */
+typedef struct {
+    uint32_t struct_size;
+    int32_t strategy;      /* [PFG_INDEPENDENT] */
+    int32_t pool_bits;     /* [3072] pool size in bits for PFG_POOL */
+    int32_t prefix_bits;   /* [24] K: maximum prefix length in bits, 13..32 (R-7) */
+    int32_t reps_override; /* [0 = derive L from the budget] L repetitions (BASELINE config 1 uses 32) */
+    int32_t sketch_words;  /* [32] M 64-bit sketches per point; -1 = none (no filter) */
+    int32_t cp_draws;      /* [1000] Monte-Carlo draws per grid cell of the CP table */
+    int32_t max_reps;      /* [4096] cap on the derived L (R-11) */
+    int32_t reserved0;
+    int64_t id_offset;     /* [0] global id of local row 0 (sharded mode) */
+} pfg_build_opts;
+
+/* Search options.  Zero-initialise + struct_size; zero field = default.  NULL = all defaults. */
+typedef struct {
+    uint32_t struct_size;
+    int32_t rep_chunk;        /* [8] R: the filter threshold tau is refreshed once per chunk of R
+                                 repetitions (R-17); 1 = literal per-candidate-batch form */
+    int32_t segment;          /* [12] B: entries are retrieved in segments of B */
+    int32_t stop_rule;        /* [0] 0 = failure bound (1-P_i)^j <= delta;
+                                 1 = Alg. 1 line 8, j >= ln(1/delta)/P_i (independent only) */
+    int32_t stop_granularity; /* [0] 0 = check after every repetition (Alg. 1);
+                                 1 = only after all L repetitions of a level */
+    int32_t use_filter;       /* [1] 1 = sketch filter on; -1 = off */
+    float filter_eps;         /* [0] tau = (1+eps) x expected Hamming distance */
+    int32_t trace_cap;        /* [0] >0: write the ids evaluated by each query, in evaluation order,
+                                 to trace_ids[nq][trace_cap] (uint32, local row ids) */
+    int32_t reserved0;
+    uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
+} pfg_search_opts;
+
+/* per-query counters (optional output of pfg_search) */
+typedef struct {
+    int32_t i_stop;      /* prefix length at which the search stopped (0 = linear scan) */
+    int32_t j_stop;      /* 1-based repetition index at that level */
+    uint32_t emitted;    /* table positions retrieved (segments included) */
+    uint32_t filtered;   /* retrieved candidates rejected by the sketch filter */
+    uint32_t dups;       /* retrieved candidates that passed the filter but were already evaluated */
+    uint32_t evaluated;  /* distinct points whose exact inner product was computed */
+    uint32_t flags;      /* bit0: k > n (padded); bit1: zero query row; bit2: trace truncated */
+    uint32_t probes;     /* table entries read by the prefix-range searches */
+} pfg_query_stats;
+
+typedef struct {
+    int64_t n;
+    int32_t d, d_pad, family, strategy, prefix_bits, reps, ell, funcs_per_rep, sketch_words;
+    int32_t pool_funcs, fht_dim, device, reserved0;
+    uint64_t index_bytes;    /* bytes counted against the memory budget (R-11) */
+    uint64_t scratch_bytes;  /* per-query scratch currently allocated (not counted in the budget) */
+    uint64_t seed;
+    int64_t id_offset;
+} pfg_index_info_t;
+
+/* Build an index over n rows of dimension d (§4.2).
+ * data: [n][d] fp32, host or device.  Rows are normalised into index-owned
+ * memory.  memory_budget_bytes: total index size including the data and the hash functions
+ * (PAPER.md:567); L is derived from it unless opts->reps_override > 0.  family: pfg_family.
+ * seed: all hash functions derive from it (identical on every shard).
+ * Errors: PFG_E_ARG (n < 1, n >= 2^32, d < 1, d > 4096, bad option), PFG_E_ZERO_VECTOR (message
+ * names the row), PFG_E_BUDGET (message names the minimum budget), PFG_E_OOM, PFG_E_CUDA.
+ * On error *out is NULL. */
+pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t memory_budget_bytes,
+                     int32_t family, uint64_t seed, const pfg_build_opts* opts, void* stream,
+                     pfg_index** out);
+
+/* Adaptive k-NN search (Alg. 1 over the array index of PAPER.md:281-334) for
+ * nq queries.  queries: [nq][d] fp32 (normalised internally).  recall_target in (0, 1]:
+ * delta = 1 - recall (recall 1 = exhaustive).  Outputs out_ids [nq][k] int64 (global ids) and
+ * out_sims [nq][k] fp32 (inner product of the normalised vectors), sorted by similarity
+ * descending, ties by smaller id.  If k > n the last k-n entries are id -1 / sim -inf.
+ * stats: optional [nq] pfg_query_stats.  Zero query rows: that row's ids are -1, sims NaN,
+ * stats flag bit1, and the call returns PFG_E_ZERO_VECTOR naming the first such row after
+ * finishing the others.  Reentrant; concurrent calls on one index are serialised on the device. */
+pfg_status pfg_search(pfg_index* idx, const float* queries, int64_t nq, int32_t k, float recall_target,
+                      const pfg_search_opts* opts, int64_t* out_ids, float* out_sims,
+                      pfg_query_stats* stats, void* stream);
+
+/* Merge `world` per-shard top-k lists into one (sharded mode, after an all-gather):
+ * ids [world][nq][k] int64 (-1 = empty), sims [world][nq][k] fp32 -> out [nq][k] by
+ * (sim desc, id asc).  Device pointers only. */
+pfg_status pfg_merge_topk(const int64_t* ids, const float* sims, int32_t world, int64_t nq, int32_t k,
+                          int64_t* out_ids, float* out_sims, void* stream);
+
+pfg_status pfg_index_info(const pfg_index* idx, pfg_index_info_t* out);
+
+/* Host-only cost model (R-11, no GPU needed): the L that pfg_build would derive, and
+ * the minimum budget for L = 1.  Returns PFG_E_BUDGET if the budget admits no repetition. */
+pfg_status pfg_derive_reps(int64_t n, int32_t d, int32_t family, uint64_t memory_budget_bytes,
+                           const pfg_build_opts* opts, int32_t* reps_out, uint64_t* min_budget_out,
+                           uint64_t* index_bytes_out);
+
+/* ---- test hooks (parity) ---------------------------------------------------------------- */
+typedef enum {
+    PFG_EXPORT_TABLE = 1,   /* arg = rep j: uint64 [n] = (code << 32) | local id, sorted ascending */
+    PFG_EXPORT_PREFIX = 2,  /* arg = rep j: uint32 [8193] first position whose top 13 bits >= p */
+    PFG_EXPORT_SKETCH = 3,  /* uint64 [n][M] */
+    PFG_EXPORT_DATA = 4,    /* fp32 [n][d] normalised rows */
+    PFG_EXPORT_CP = 5,      /* double [ell+1][41] cleaned CP collision table (FHT family) */
+    PFG_EXPORT_SLOTS = 6,   /* int32 [L] sketch slot per repetition */
+    PFG_EXPORT_POOLSEL = 7  /* int32 [L][c] pool function indices per repetition */
+} pfg_export_what;
+
+/* copy an index array into host memory dst (dst_bytes must equal the array size) */
+pfg_status pfg_export(const pfg_index* idx, int32_t what, int32_t arg, void* dst_host, uint64_t dst_bytes);
+
+/* hash queries: out_codes [nq][L] uint32 (K-bit repetition codes), out_sketches [nq][M] uint64;
+ * either output may be NULL.  Device or host pointers. */
+pfg_status pfg_hash_queries(pfg_index* idx, const float* queries, int64_t nq, uint32_t* out_codes,
+                            uint64_t* out_sketches, void* stream);
+
+/* stop-rule and filter tables used by pfg_search for this recall target and options:
+ * thr_host [K][L] fp32: level i = 1..K row i-1: the search stops after repetition j at level i
+ * iff the k-th similarity (clamped to [-1,1]) >= thr[i-1][j-1] (+inf = never);
+ * tau_host [65] fp32: tau(ip) = min{t : ip >= tau_host[t]}.  Either may be NULL. */
+pfg_status pfg_stop_tables(pfg_index* idx, float recall_target, const pfg_search_opts* opts,
+                           float* thr_host, float* tau_host);
+
+void pfg_free(pfg_index* idx);
+const char* pfg_last_error(void);
+int32_t pfg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFG_H */

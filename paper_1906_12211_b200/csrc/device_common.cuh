@@ -1,0 +1,129 @@
+// device_common.cuh — device helpers shared by the build and query kernels (product code).
+//
+// Bit-exactness (R-2, R-6): every floating-point operation whose result decides an
+// integer (a hash bit, a cross-polytope index, a stop decision through the k-th similarity) is
+// written in a fixed order: sequential fmaf chains for inner products, the radix-2 butterfly
+// order h = 1, 2, 4, ... for the Hadamard transform, IEEE double with explicit _rn intrinsics
+// for the normalisation.  The library is compiled with --fmad=false so no other a*b+c is fused.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pfg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// orderable 32-bit image of a float (larger float -> larger unsigned); -0 is mapped to +0 so the
+// order agrees with float comparison (the oracle compares floats, where -0 == +0)
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    if (f == 0.0f) f = 0.0f;
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+    const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(u);
+}
+// top-k key: larger key = better = (similarity desc, id asc)  (R-19)
+__device__ __forceinline__ uint64_t make_key(float sim, uint32_t id) {
+    return ((uint64_t)f2ord(sim) << 32) | (uint64_t)(~id);
+}
+__device__ __forceinline__ uint32_t key_id(uint64_t k) { return ~(uint32_t)k; }
+__device__ __forceinline__ float key_sim(uint64_t k) { return ord2f((uint32_t)(k >> 32)); }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Fast Hadamard transform over one warp (§4.3; R-6).  Element u of the
+// dp-vector lives in lane u / EPL, slot u % EPL (EPL = max(1, dp/32)).  Unnormalised radix-2
+// stages h = 1, 2, ..., dp/2; the pair (u, u+h), bit h of u clear, becomes (y_u + y_{u+h},
+// y_u - y_{u+h}).  The same pairs are combined in the same stage order as the oracle, so the
+// fp32 result is bit-identical.  For dp < 32 only lanes < dp carry data.
+template <int EPL>
+__device__ __forceinline__ void fht_warp(float (&v)[EPL], int dp, int lane) {
+#pragma unroll
+    for (int h = 1; h < EPL; h <<= 1) {
+#pragma unroll
+        for (int s = 0; s < EPL; ++s)
+            if (!(s & h)) {
+                const float a = v[s], b = v[s + h];
+                v[s] = a + b;
+                v[s + h] = a - b;
+            }
+    }
+    for (int hl = 1; hl * EPL < dp; hl <<= 1) {
+        const bool upper = (lane & hl) != 0;
+#pragma unroll
+        for (int s = 0; s < EPL; ++s) {
+            const float o = __shfl_xor_sync(kFull, v[s], hl);
+            v[s] = upper ? (o - v[s]) : (v[s] + o);
+        }
+    }
+}
+
+// Cross-polytope hash with three pseudo-random rotations H D_r (§2, 340 §4.3):
+// x (d floats, zero-padded to dp) -> y = H D3 H D2 H D1 x; code = (y_a* < 0) << (ell-1) | a*,
+// a* = argmax_u |y_u| with ties to the lowest u (R-5: sign in the MSB).
+// sg: sign bits [3][W], W = max(1, dp/32); bit u of round r set = coordinate u negated.
+// All lanes of the warp must call; all return the code.
+template <int EPL>
+__device__ __forceinline__ uint32_t fhtcp_code_warp(const float* xrow, int d, int dp, int ell,
+                                                    const uint32_t* __restrict__ sg, int lane) {
+    float v[EPL];
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) {
+        const int u = lane * EPL + s;
+        v[s] = (u < d) ? xrow[u] : 0.0f;
+    }
+    const int W = (dp + 31) >> 5;
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int s = 0; s < EPL; ++s) {
+            const int u = lane * EPL + s;
+            if (u < dp) {
+                const uint32_t bit = (__ldg(sg + r * W + (u >> 5)) >> (u & 31)) & 1u;
+                v[s] = __uint_as_float(__float_as_uint(v[s]) ^ (bit << 31));  // * (-1)^bit, exact
+            }
+        }
+        fht_warp<EPL>(v, dp, lane);
+    }
+    float ba = -1.0f, bv = 0.0f;
+    int bi = 0;
+#pragma unroll
+    for (int s = 0; s < EPL; ++s) {
+        const int u = lane * EPL + s;
+        if (u < dp) {
+            const float a = fabsf(v[s]);
+            if (a > ba) { ba = a; bi = u; bv = v[s]; }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float oa = __shfl_xor_sync(kFull, ba, off);
+        const int oi = __shfl_xor_sync(kFull, bi, off);
+        const float ov = __shfl_xor_sync(kFull, bv, off);
+        if (oa > ba || (oa == ba && oi < bi)) { ba = oa; bi = oi; bv = ov; }
+    }
+    return ((uint32_t)(bv < 0.0f) << (ell - 1)) | (uint32_t)bi;
+}
+
+// warp bitonic sort of one u64 per lane, descending across lanes (lane 0 = largest)
+__device__ __forceinline__ uint64_t warp_sort_desc(uint64_t key, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t o = __shfl_xor_sync(kFull, key, j);
+            const bool desc = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            const uint64_t mx = key > o ? key : o, mn = key > o ? o : key;
+            key = (desc == lower) ? mx : mn;
+        }
+    }
+    return key;
+}
+
+}  // namespace pfg

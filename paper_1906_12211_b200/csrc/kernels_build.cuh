@@ -1,0 +1,231 @@
+// kernels_build.cuh — index-building kernels (also used to hash query batches).
+//
+//  k_normalize   a1: x <- x/|x|, double accumulation, zero-row detection
+//  k_hp_bits     a3/a4: SimHash sign bits of a batch of rows against F Gaussian functions
+//                (PAPER.md:142-146); an FP32 SIMT GEMM whose per-output accumulation is the
+//                canonical sequential fmaf chain over t (R-2), so bits equal the oracle's;
+//                also produces the 64-bit sketch words
+//  k_codes_from_bits  repetition codes from HP bits (independent or pool selection)
+//  k_fht_rep     a3: FHT cross-polytope repetition codes, warp per row
+//  k_fht_funcs   FHT-CP codes of pool functions (pool strategy)
+//  k_pool_codes  repetition codes from pooled FHT-CP function codes
+//  k_prefix      a5: 13-bit prefix tabulation of a sorted repetition
+//  k_mc_codes    Monte-Carlo CP collision counts
+#pragma once
+#include "device_common.cuh"
+
+namespace pfg {
+
+// ---------------------------------------------------------------------------------------------
+// a1: out[r][0..d) = (float)((double)x / sqrt(sum_t (double)x_t^2)), sum sequential over t;
+// out[r][d..dpad) = 0.  zflag[r] = 1 for a zero row; *zmin = smallest zero row index.
+// One thread per row (the double sum is order-dependent, so it is not split across lanes).
+__global__ void k_normalize(const float* __restrict__ x, int64_t n, int d, int ldx, float* __restrict__ out,
+                            int dpad, uint8_t* __restrict__ zflag, unsigned long long* __restrict__ zmin) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const float* row = x + r * ldx;
+    double s = 0.0;
+    for (int t = 0; t < d; ++t) {
+        const double v = (double)row[t];
+        s = __dadd_rn(s, __dmul_rn(v, v));
+    }
+    float* o = out + r * dpad;
+    const bool zero = !(s > 0.0);
+    if (zflag) zflag[r] = zero ? 1 : 0;
+    if (zero) {
+        atomicMin(zmin, (unsigned long long)r);
+        for (int t = 0; t < dpad; ++t) o[t] = 0.0f;
+        return;
+    }
+    s = __dsqrt_rn(s);
+    for (int t = 0; t < d; ++t) o[t] = __double2float_rn(__ddiv_rn((double)row[t], s));
+    for (int t = d; t < dpad; ++t) o[t] = 0.0f;
+}
+
+// ---------------------------------------------------------------------------------------------
+// SimHash bits: bit(p, f) = [sum_t X[p][t] * A[f][t] >= 0] with the sum a sequential fmaf chain
+// over t = 0..dpad-1 starting at +0 (R-2).  Padding columns are zero in both operands and
+// fmaf(0, 0, acc) == acc because the chain never holds -0 (it starts at +0 and an exact-zero
+// fma result rounds to +0), so the padded chain equals the oracle's chain over t < d.
+// Output: out[p * out_ld + f/8] byte, bit f%8 (so u64 word f/64 holds bit f%64, little endian).
+constexpr int GB_M = 128, GB_N = 128, GB_K = 16;
+__global__ void __launch_bounds__(256) k_hp_bits(const float* __restrict__ X, int64_t np, int ldx,
+                                                 const float* __restrict__ A, int nf, int lda, int kdim,
+                                                 uint8_t* __restrict__ out, int64_t out_ld) {
+    __shared__ __align__(16) float Xs[GB_K][GB_M + 4];
+    __shared__ __align__(16) float As[GB_K][GB_N + 4];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t p0 = (int64_t)blockIdx.y * GB_M;
+    const int f0 = blockIdx.x * GB_N;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int t0 = 0; t0 < kdim; t0 += GB_K) {
+#pragma unroll
+        for (int e = tid; e < GB_M * GB_K; e += 256) {
+            const int r = e >> 4, c = e & 15;
+            const int64_t p = p0 + r;
+            const int t = t0 + c;
+            Xs[c][r] = (p < np && t < kdim) ? __ldg(X + p * ldx + t) : 0.0f;
+            const int f = f0 + r;
+            As[c][r] = (f < nf && t < kdim) ? __ldg(A + (int64_t)f * lda + t) : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < GB_K; ++c) {
+            float xv[8], av[8];
+            const float4 x0 = *reinterpret_cast<const float4*>(&Xs[c][ty * 8]);
+            const float4 x1 = *reinterpret_cast<const float4*>(&Xs[c][ty * 8 + 4]);
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[c][tx * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[c][tx * 8 + 4]);
+            xv[0] = x0.x; xv[1] = x0.y; xv[2] = x0.z; xv[3] = x0.w;
+            xv[4] = x1.x; xv[5] = x1.y; xv[6] = x1.z; xv[7] = x1.w;
+            av[0] = a0.x; av[1] = a0.y; av[2] = a0.z; av[3] = a0.w;
+            av[4] = a1.x; av[5] = a1.y; av[6] = a1.z; av[7] = a1.w;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(xv[i], av[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    const int fb = f0 + tx * 8;
+    if (fb >= nf) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t p = p0 + ty * 8 + i;
+        if (p >= np) continue;
+        uint32_t b = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (fb + j < nf && acc[i][j] >= 0.0f) b |= 1u << j;
+        out[p * out_ld + (fb >> 3)] = (uint8_t)b;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// HP repetition codes from bits (ell = 1, c = K functions): code_j = bits of functions
+// f_{j,0} .. f_{j,K-1}, the first the most significant (R-7).
+// Independent: f_{j,t} = (j - fbase_rep) * K + t within the bit batch; pool: sel[j][t].
+// out: keys (u64, (code << 32) | p, layout [rep - r0][p]) or codes (u32, layout [p][ldc]).
+__global__ void k_codes_from_bits(const uint64_t* __restrict__ bits, int64_t np, int words_per_row,
+                                  int r0, int nreps, int K, const int32_t* __restrict__ sel, int rep_fbase,
+                                  uint64_t* __restrict__ keys, uint32_t* __restrict__ codes, int ldc) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (p >= np || r >= nreps) return;
+    const int j = r0 + r;
+    const uint64_t* row = bits + p * words_per_row;
+    uint32_t code = 0;
+    for (int t = 0; t < K; ++t) {
+        const int f = sel ? __ldg(sel + (int64_t)j * K + t) : (j - rep_fbase) * K + t;
+        code = (code << 1) | (uint32_t)((__ldg(row + (f >> 6)) >> (f & 63)) & 1ull);
+    }
+    if (keys) keys[(int64_t)r * np + p] = ((uint64_t)code << 32) | (uint64_t)p;
+    if (codes) codes[p * ldc + j] = code;
+}
+
+// ---------------------------------------------------------------------------------------------
+// FHT-CP repetition codes, independent strategy: rep j concatenates functions j*c .. j*c+c-1
+// (ell bits each, first most significant) and keeps the top K bits (R-7).  One warp per row;
+// the row's dp-vector lives in registers (EPL per lane).  Outputs keys [rep - r0][p] and/or
+// codes [p][ldc].
+template <int EPL>
+__global__ void __launch_bounds__(256) k_fht_rep(const float* __restrict__ X, int64_t np, int ldx, int d,
+                                                 int dp, int ell, int c, int K, const uint32_t* __restrict__ sg,
+                                                 int r0, int nreps, uint64_t* __restrict__ keys,
+                                                 uint32_t* __restrict__ codes, int ldc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int W = (dp + 31) >> 5;
+    for (int64_t p = warp; p < np; p += nwarps) {
+        const float* xr = X + p * ldx;
+        for (int r = 0; r < nreps; ++r) {
+            const int j = r0 + r;
+            uint64_t full = 0;
+            for (int t = 0; t < c; ++t) {
+                const int64_t f = (int64_t)j * c + t;
+                full = (full << ell) | fhtcp_code_warp<EPL>(xr, d, dp, ell, sg + f * 3 * W, lane);
+            }
+            const uint32_t code = (uint32_t)(full >> (c * ell - K));
+            if (lane == 0) {
+                if (keys) keys[(int64_t)r * np + p] = ((uint64_t)code << 32) | (uint64_t)p;
+                if (codes) codes[p * ldc + j] = code;
+            }
+        }
+    }
+}
+
+// FHT-CP codes of the m pool functions for every row: out [p][m] (uint16)
+template <int EPL>
+__global__ void __launch_bounds__(256) k_fht_funcs(const float* __restrict__ X, int64_t np, int ldx, int d,
+                                                   int dp, int ell, int m, const uint32_t* __restrict__ sg,
+                                                   uint16_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int W = (dp + 31) >> 5;
+    for (int64_t p = warp; p < np; p += nwarps) {
+        const float* xr = X + p * ldx;
+        for (int f = 0; f < m; ++f) {
+            const uint32_t code = fhtcp_code_warp<EPL>(xr, d, dp, ell, sg + (int64_t)f * 3 * W, lane);
+            if (lane == 0) out[p * m + f] = (uint16_t)code;
+        }
+    }
+}
+
+// repetition codes from pooled FHT-CP codes: full = concat(fc[p][sel[j][t]]), code = top K bits
+__global__ void k_pool_codes(const uint16_t* __restrict__ fc, int64_t np, int m, int r0, int nreps, int c,
+                             int ell, int K, const int32_t* __restrict__ sel, uint64_t* __restrict__ keys,
+                             uint32_t* __restrict__ codes, int ldc) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (p >= np || r >= nreps) return;
+    const int j = r0 + r;
+    uint64_t full = 0;
+    for (int t = 0; t < c; ++t) full = (full << ell) | __ldg(fc + p * m + __ldg(sel + (int64_t)j * c + t));
+    const uint32_t code = (uint32_t)(full >> (c * ell - K));
+    if (keys) keys[(int64_t)r * np + p] = ((uint64_t)code << 32) | (uint64_t)p;
+    if (codes) codes[p * ldc + j] = code;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a5: pt[q] = first position whose top-13 code bits are >= q, q = 0..8192.
+__global__ void k_prefix(const uint64_t* __restrict__ tab, int64_t n, int K, uint32_t* __restrict__ pt) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > n) return;
+    const int sh = K - 13;
+    const int64_t cur = (t < n) ? (int64_t)((uint32_t)(tab[t] >> 32) >> sh) : 8192;
+    const int64_t prev = (t == 0) ? -1 : (int64_t)((uint32_t)(tab[t - 1] >> 32) >> sh);
+    for (int64_t q = prev + 1; q <= cur; ++q) pt[q] = (uint32_t)t;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Monte-Carlo collision counts (R-14 random pairs): pair e = a*draws + t has
+// rows x = XY[2e], y = XY[2e+1] (d floats each, stride ld) and its own function signs
+// sg[e][3][W]; cnt[b*41 + a] += 1 when the first b of ell bits agree.
+template <int EPL>
+__global__ void __launch_bounds__(256) k_mc_codes(const float* __restrict__ XY, int ld, int64_t npairs, int d,
+                                                  int dp, int ell, int draws, const uint32_t* __restrict__ sg,
+                                                  unsigned long long* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int W = (dp + 31) >> 5;
+    for (int64_t e = warp; e < npairs; e += nwarps) {
+        const uint32_t* s = sg + e * 3 * W;
+        const uint32_t hx = fhtcp_code_warp<EPL>(XY + (2 * e) * ld, d, dp, ell, s, lane);
+        const uint32_t hy = fhtcp_code_warp<EPL>(XY + (2 * e + 1) * ld, d, dp, ell, s, lane);
+        const int a = (int)(e / draws);
+        if (lane >= 1 && lane <= ell) {
+            const int b = lane;
+            if ((hx >> (ell - b)) == (hy >> (ell - b))) atomicAdd(cnt + b * 41 + a, 1ull);
+        }
+    }
+}
+
+}  // namespace pfg

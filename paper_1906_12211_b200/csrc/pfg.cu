@@ -1,0 +1,1000 @@
+// pfg.cu — C-ABI implementation (include/pfg.h) of the B200-native batched LSH-forest k-NN index.
+//
+// Host side: argument checks, the budget -> L cost model (R-11), seeded hash-function
+// generation (rng.h), orchestration of the build kernels and CUB radix sorts, the host-computed
+// stop-rule / filter threshold tables (so the device does no transcendental math and its stop
+// decisions equal the oracle's, R-9/R-10/R-15), and the launch of the query kernel.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/pfg.h"
+#include "kernels_build.cuh"
+#include "kernels_query.cuh"
+#include "rng.h"
+
+namespace pfg {
+namespace {
+
+thread_local std::string g_err;
+
+pfg_status fail(pfg_status s, const std::string& m) {
+    g_err = m;
+    return s;
+}
+
+#define PFG_CUDA(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (expr);                                                                    \
+        if (e_ != cudaSuccess) {                                                                    \
+            cudaGetLastError();                                                                     \
+            return fail(e_ == cudaErrorMemoryAllocation ? PFG_E_OOM : PFG_E_CUDA,                   \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                        \
+        }                                                                                           \
+    } while (0)
+
+#define PFG_TRY(expr)                            \
+    do {                                         \
+        pfg_status s_ = (expr);                  \
+        if (s_ != PFG_OK) return s_;             \
+    } while (0)
+
+// owning device buffer
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    pfg_status alloc(size_t b, const char* what) {
+        release();
+        if (b == 0) b = 16;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return fail(e == cudaErrorMemoryAllocation ? PFG_E_OOM : PFG_E_CUDA,
+                        std::string("cudaMalloc(") + what + ", " + std::to_string(b) + " B): " + cudaGetErrorString(e));
+        }
+        bytes = b;
+        return PFG_OK;
+    }
+    pfg_status ensure(size_t b, const char* what) {  // grow-only
+        if (p && bytes >= b) return PFG_OK;
+        return alloc(b, what);
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+bool is_device_ptr(const void* ptr) {
+    if (!ptr) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+int ilog2(int v) {
+    int l = 0;
+    while ((1 << l) < v) ++l;
+    return l;
+}
+
+// ---------------------------------------------------------------------------------------------
+// index geometry and the budget -> L cost model (R-11)
+struct Geo {
+    int64_t n = 0;
+    int d = 0, dpad = 0, family = 0, strategy = 0, K = 24, M = 32, ell = 1, c = 24, dp = 1, W = 1, m = 0;
+    int pool_bits = 3072, cp_draws = 1000, max_reps = 4096, L = 0;
+    int64_t id_offset = 0;
+    uint64_t fixed_bytes = 0, per_rep_bytes = 0, index_bytes = 0;
+};
+
+pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, Geo& g) {
+    pfg_build_opts z;
+    std::memset(&z, 0, sizeof(z));
+    if (o) {
+        if (o->struct_size < sizeof(uint32_t) || o->struct_size > sizeof(pfg_build_opts))
+            return fail(PFG_E_ARG, "pfg_build_opts.struct_size must be sizeof(pfg_build_opts)");
+        std::memcpy(&z, o, o->struct_size);
+    }
+    if (n < 1 || n >= (int64_t(1) << 31)) return fail(PFG_E_ARG, "n must be in [1, 2^31)");
+    if (d < 1 || d > 4096) return fail(PFG_E_ARG, "d must be in [1, 4096]");
+    if (family != PFG_SIMHASH && family != PFG_CROSSPOLYTOPE_FHT) return fail(PFG_E_ARG, "unknown family");
+    g.n = n;
+    g.d = d;
+    g.dpad = (d + 3) & ~3;
+    g.family = family;
+    g.strategy = z.strategy;
+    if (g.strategy != PFG_INDEPENDENT && g.strategy != PFG_POOL) return fail(PFG_E_ARG, "unknown strategy");
+    g.K = z.prefix_bits ? z.prefix_bits : 24;
+    if (g.K < 13 || g.K > 32) return fail(PFG_E_ARG, "prefix_bits must be in [13, 32]");
+    g.M = z.sketch_words == 0 ? 32 : (z.sketch_words < 0 ? 0 : z.sketch_words);
+    if (g.M > 64) return fail(PFG_E_ARG, "sketch_words must be <= 64");
+    g.dp = next_pow2(d);
+    g.W = (g.dp + 31) >> 5;
+    if (family == PFG_SIMHASH) {
+        g.ell = 1;
+    } else {
+        if (g.dp > 1024) return fail(PFG_E_ARG, "cross-polytope (FHT) family supports d <= 1024");
+        g.ell = 1 + ilog2(g.dp);
+    }
+    g.c = (g.K + g.ell - 1) / g.ell;
+    g.pool_bits = z.pool_bits ? z.pool_bits : 3072;
+    g.m = g.strategy == PFG_POOL ? g.pool_bits / g.ell : 0;
+    if (g.strategy == PFG_POOL && g.m < g.c) return fail(PFG_E_ARG, "pool smaller than one repetition's functions");
+    if (g.strategy == PFG_POOL && g.family == PFG_CROSSPOLYTOPE_FHT && g.m > 65535) return fail(PFG_E_ARG, "pool too large");
+    g.cp_draws = z.cp_draws ? z.cp_draws : 1000;
+    if (g.cp_draws < 1) return fail(PFG_E_ARG, "cp_draws must be >= 1");
+    g.max_reps = z.max_reps ? z.max_reps : 4096;
+    g.id_offset = z.id_offset;
+    // bytes: data + sketches + sketch functions + pool functions + CP table (fixed);
+    // per repetition: sorted table + 13-bit prefix table + slot + its own functions / selection
+    const uint64_t N = (uint64_t)n;
+    const uint64_t fn_hp = 4ull * g.dpad, fn_fht = 3ull * g.W * 4;
+    g.fixed_bytes = 4ull * N * g.dpad + 8ull * N * g.M + 4ull * 64 * g.M * g.dpad + 8ull * (g.ell + 1) * 41;
+    if (g.strategy == PFG_POOL) g.fixed_bytes += (uint64_t)g.m * (family == PFG_SIMHASH ? fn_hp : fn_fht);
+    g.per_rep_bytes = 8ull * N + 4ull * 8193 + 1;
+    if (g.strategy == PFG_INDEPENDENT) g.per_rep_bytes += (uint64_t)g.c * (family == PFG_SIMHASH ? fn_hp : fn_fht);
+    else g.per_rep_bytes += 4ull * g.c;
+    return PFG_OK;
+}
+
+pfg_status derive_L(Geo& g, uint64_t budget, int reps_override) {
+    if (reps_override > 0) {
+        g.L = reps_override;
+    } else {
+        if (budget < g.fixed_bytes + g.per_rep_bytes) {
+            return fail(PFG_E_BUDGET, "memory budget " + std::to_string(budget) + " B admits no repetition; minimum is " +
+                                          std::to_string(g.fixed_bytes + g.per_rep_bytes) + " B");
+        }
+        const uint64_t L = (budget - g.fixed_bytes) / g.per_rep_bytes;
+        g.L = (int)std::min<uint64_t>(L, (uint64_t)g.max_reps);
+    }
+    if (g.L < 1 || g.L > 65536) return fail(PFG_E_ARG, "repetitions must be in [1, 65536]");
+    g.index_bytes = g.fixed_bytes + (uint64_t)g.L * g.per_rep_bytes;
+    return PFG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// stop rule (host, double, same formulas as the paper; R-9, R-10)
+int grid_bucket(float ip) {
+    int b = 0;
+    for (int a = 0; a <= 40; ++a)
+        if (ip >= (float)(-1.0 + 0.05 * a)) b = a;
+    return b;
+}
+
+struct StopModel {
+    int family, strategy, ell, m;
+    const double* T;  // CP table [(ell+1)][41] (FHT family)
+    double P(int i, float ip) const {
+        if (family == PFG_SIMHASH) {
+            const double p = 1.0 - std::acos((double)ip) / M_PI;
+            return std::pow(p, (double)i);
+        }
+        const int b = grid_bucket(ip);
+        return std::pow(T[ell * 41 + b], (double)(i / ell)) * T[(i % ell) * 41 + b];
+    }
+    // Lemma 1 failure bound, Alg. 1 line 8, pool Cantelli
+    bool stop(int i, int j, float ip, double delta, int rule) const {
+        const double Pi = P(i, ip);
+        if (strategy == PFG_POOL) {
+            const int ci = (i + ell - 1) / ell;
+            if (m < 2 * ci || !(Pi > 0.0)) return false;
+            const double r = (double)ci / (double)(m - ci);
+            double prod = 1.0;
+            for (int f = 0; f < ci; ++f) {
+                const int bits = (f < i / ell) ? ell : (i % ell);
+                const double pf = P(bits, ip);
+                prod *= r + (1.0 - r) * pf;
+            }
+            const double mu = (double)j * Pi;
+            const double e12 = Pi * prod;
+            const double F = 1.0 - mu * mu / (mu + (double)j * ((double)j - 1.0) * e12);
+            return F <= delta;
+        }
+        if (rule == 1) return (double)j * Pi >= std::log(1.0 / delta);
+        return (double)j * std::log1p(-Pi) <= std::log(delta);
+    }
+};
+
+uint32_t h_f2ord(float f) {
+    if (f == 0.0f) f = 0.0f;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+float h_ord2f(uint32_t o) {
+    const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+// smallest float x in [-1, 1] with pred(x) true, for pred monotone (false ... true); +inf if none
+template <class Pred>
+float smallest_true(Pred pred) {
+    if (!pred(1.0f)) return INFINITY;
+    if (pred(-1.0f)) return -1.0f;
+    uint32_t lo = h_f2ord(-1.0f), hi = h_f2ord(1.0f);  // pred(lo) false, pred(hi) true
+    while (hi - lo > 1) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (pred(h_ord2f(mid))) hi = mid; else lo = mid;
+    }
+    return h_ord2f(hi);
+}
+
+// R-15: tau = round-half-up((1+eps) * 64 * acos(ip)/pi), clamped to [0, 64]
+int tau_of(float ipk, float eps) {
+    double t = (1.0 + (double)eps) * 64.0 * std::acos((double)ipk) / M_PI;
+    double r = std::floor(t + 0.5);
+    if (r > 64.0) r = 64.0;
+    if (r < 0.0) r = 0.0;
+    return (int)r;
+}
+
+struct SearchCfg {
+    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0;
+    float eps = 0.0f;
+    uint32_t* trace_ids = nullptr;
+};
+
+pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
+    pfg_search_opts z;
+    std::memset(&z, 0, sizeof(z));
+    if (o) {
+        if (o->struct_size < sizeof(uint32_t) || o->struct_size > sizeof(pfg_search_opts))
+            return fail(PFG_E_ARG, "pfg_search_opts.struct_size must be sizeof(pfg_search_opts)");
+        std::memcpy(&z, o, o->struct_size);
+    }
+    s.R = z.rep_chunk ? z.rep_chunk : 8;
+    if (s.R < 1 || s.R > kMaxR) return fail(PFG_E_ARG, "rep_chunk must be in [1, 32]");
+    s.B = z.segment ? z.segment : 12;
+    if (s.B < 1) return fail(PFG_E_ARG, "segment must be >= 1");
+    s.rule = z.stop_rule;
+    if (s.rule != 0 && s.rule != 1) return fail(PFG_E_ARG, "stop_rule must be 0 or 1");
+    s.per_round = z.stop_granularity;
+    if (s.per_round != 0 && s.per_round != 1) return fail(PFG_E_ARG, "stop_granularity must be 0 or 1");
+    s.use_filter = z.use_filter < 0 ? 0 : 1;
+    s.eps = z.filter_eps;
+    if (!(s.eps > -1.0f) || !std::isfinite(s.eps)) return fail(PFG_E_ARG, "filter_eps must be finite and > -1");
+    s.trace_cap = z.trace_cap;
+    s.trace_ids = z.trace_ids;
+    if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
+    return PFG_OK;
+}
+
+}  // namespace
+}  // namespace pfg
+
+using namespace pfg;
+
+struct pfg_index {
+    Geo g;
+    int device = 0;
+    int num_sms = 148;
+    uint64_t seed = 0;
+    std::mutex mu;
+    // index arrays (device)
+    DBuf x, sk, tab, pt, slot, hpfn, sg, sel, skfn;
+    std::vector<double> cpT;
+    std::vector<int32_t> slot_h, sel_h;
+    // cached stop tables: key (recall bits, rule, per_round) -> device thr [K][L]; eps -> taub
+    std::map<std::tuple<uint32_t, int, int>, std::shared_ptr<DBuf>> thr_cache;
+    std::map<uint32_t, std::shared_ptr<DBuf>> tau_cache;
+    // per-call scratch (grow-only)
+    DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, outb_ids, outb_sims, outb_stats, outb_trace, work;
+    DBuf cur, bitmap, claims;
+    int64_t slots = 0;
+    int slots_L = 0;
+    int64_t slots_bm = 0;
+};
+
+namespace pfg {
+namespace {
+
+constexpr int kClaimCap = 8192;
+
+template <int EPL>
+void launch_fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps,
+                    uint64_t* keys, uint32_t* codes, int ldc, int num_sms, cudaStream_t st) {
+    int64_t warps = std::min<int64_t>(np, (int64_t)num_sms * 64);
+    const int blocks = (int)((warps * 32 + 255) / 256);
+    k_fht_rep<EPL><<<blocks, 256, 0, st>>>(X, np, ldx, g.d, g.dp, g.ell, g.c, g.K, sg, r0, nreps, keys, codes, ldc);
+}
+void fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps, uint64_t* keys,
+             uint32_t* codes, int ldc, int num_sms, cudaStream_t st) {
+    switch (std::max(1, g.dp / 32)) {
+        case 1: launch_fht_rep<1>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
+        case 2: launch_fht_rep<2>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
+        case 4: launch_fht_rep<4>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
+        case 8: launch_fht_rep<8>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
+        case 16: launch_fht_rep<16>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
+        default: launch_fht_rep<32>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
+    }
+}
+template <int EPL>
+void launch_fht_funcs(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, uint16_t* out, int num_sms,
+                      cudaStream_t st) {
+    int64_t warps = std::min<int64_t>(np, (int64_t)num_sms * 64);
+    const int blocks = (int)((warps * 32 + 255) / 256);
+    k_fht_funcs<EPL><<<blocks, 256, 0, st>>>(X, np, ldx, g.d, g.dp, g.ell, g.m, sg, out);
+}
+void fht_funcs(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, uint16_t* out, int num_sms,
+               cudaStream_t st) {
+    switch (std::max(1, g.dp / 32)) {
+        case 1: launch_fht_funcs<1>(X, np, ldx, g, sg, out, num_sms, st); break;
+        case 2: launch_fht_funcs<2>(X, np, ldx, g, sg, out, num_sms, st); break;
+        case 4: launch_fht_funcs<4>(X, np, ldx, g, sg, out, num_sms, st); break;
+        case 8: launch_fht_funcs<8>(X, np, ldx, g, sg, out, num_sms, st); break;
+        case 16: launch_fht_funcs<16>(X, np, ldx, g, sg, out, num_sms, st); break;
+        default: launch_fht_funcs<32>(X, np, ldx, g, sg, out, num_sms, st); break;
+    }
+}
+template <int EPL>
+void launch_mc(const float* XY, int ld, int64_t npairs, const Geo& g, const uint32_t* sg, unsigned long long* cnt,
+               int num_sms, cudaStream_t st) {
+    int64_t warps = std::min<int64_t>(npairs, (int64_t)num_sms * 64);
+    const int blocks = (int)((warps * 32 + 255) / 256);
+    k_mc_codes<EPL><<<blocks, 256, 0, st>>>(XY, ld, npairs, g.d, g.dp, g.ell, g.cp_draws, sg, cnt);
+}
+
+void hp_bits(const float* X, int64_t np, int ldx, const float* A, int nf, int lda, int kdim, uint8_t* out,
+             int64_t out_ld, cudaStream_t st) {
+    dim3 grid((nf + GB_N - 1) / GB_N, (unsigned)((np + GB_M - 1) / GB_M));
+    k_hp_bits<<<grid, 256, 0, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
+}
+
+// Monte-Carlo CP table (R-13 cleaning, R-14 random pairs)
+pfg_status build_cp_table(pfg_index* I, cudaStream_t st) {
+    const Geo& g = I->g;
+    const int draws = g.cp_draws, d = g.d, dp = g.dp, W = g.W;
+    const int64_t npairs = 41ll * draws;
+    std::vector<float> XY((size_t)npairs * 2 * dp, 0.0f);
+    std::vector<uint32_t> S((size_t)npairs * 3 * W, 0u);
+    const uint64_t K = stream_key(I->seed, kTagCPMC);
+    auto work = [&](int a0, int a1) {
+        std::vector<double> x(d), u(d);
+        for (int a = a0; a < a1; ++a) {
+            const double alpha = -1.0 + 0.05 * a;
+            for (int t = 0; t < draws; ++t) {
+                const int64_t e = (int64_t)a * draws + t;
+                const uint64_t kat = draw(K, (uint64_t)e);
+                const uint64_t ksg = draw(kat, 0), kx = draw(kat, 1), ku = draw(kat, 2);
+                double nx = 0.0;
+                for (int v = 0; v < d; ++v) { x[v] = gauss(kx, v); nx += x[v] * x[v]; }
+                nx = std::sqrt(nx);
+                for (int v = 0; v < d; ++v) x[v] = x[v] / nx;
+                double ux = 0.0;
+                for (int v = 0; v < d; ++v) { u[v] = gauss(ku, v); ux += u[v] * x[v]; }
+                double nu = 0.0;
+                for (int v = 0; v < d; ++v) { u[v] = u[v] - ux * x[v]; nu += u[v] * u[v]; }
+                nu = std::sqrt(nu);
+                for (int v = 0; v < d; ++v) u[v] = u[v] / nu;
+                const double s = std::sqrt(1.0 - alpha * alpha);
+                float* xr = &XY[(size_t)(2 * e) * dp];
+                float* yr = &XY[(size_t)(2 * e + 1) * dp];
+                for (int v = 0; v < d; ++v) { xr[v] = (float)x[v]; yr[v] = (float)(alpha * x[v] + s * u[v]); }
+                uint32_t* se = &S[(size_t)e * 3 * W];
+                for (int r = 0; r < 3; ++r)
+                    for (int v = 0; v < dp; ++v)
+                        if (draw(ksg, (uint64_t)(r * dp + v)) >> 63) se[r * W + (v >> 5)] |= 1u << (v & 31);
+            }
+        }
+    };
+    {
+        unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        const int per = (41 + (int)nt - 1) / (int)nt;
+        for (unsigned k = 0; k < nt; ++k) {
+            const int a0 = (int)k * per, a1 = std::min(41, a0 + per);
+            if (a0 < a1) th.emplace_back(work, a0, a1);
+        }
+        for (auto& t : th) t.join();
+    }
+    DBuf dXY, dS, dC;
+    PFG_TRY(dXY.alloc(XY.size() * 4, "cp pairs"));
+    PFG_TRY(dS.alloc(S.size() * 4, "cp signs"));
+    PFG_TRY(dC.alloc(34 * 41 * 8, "cp counts"));
+    PFG_CUDA(cudaMemcpyAsync(dXY.p, XY.data(), XY.size() * 4, cudaMemcpyHostToDevice, st));
+    PFG_CUDA(cudaMemcpyAsync(dS.p, S.data(), S.size() * 4, cudaMemcpyHostToDevice, st));
+    PFG_CUDA(cudaMemsetAsync(dC.p, 0, 34 * 41 * 8, st));
+    switch (std::max(1, dp / 32)) {
+        case 1: launch_mc<1>(dXY.as<float>(), dp, npairs, g, dS.as<uint32_t>(), dC.as<unsigned long long>(), I->num_sms, st); break;
+        case 2: launch_mc<2>(dXY.as<float>(), dp, npairs, g, dS.as<uint32_t>(), dC.as<unsigned long long>(), I->num_sms, st); break;
+        case 4: launch_mc<4>(dXY.as<float>(), dp, npairs, g, dS.as<uint32_t>(), dC.as<unsigned long long>(), I->num_sms, st); break;
+        case 8: launch_mc<8>(dXY.as<float>(), dp, npairs, g, dS.as<uint32_t>(), dC.as<unsigned long long>(), I->num_sms, st); break;
+        case 16: launch_mc<16>(dXY.as<float>(), dp, npairs, g, dS.as<uint32_t>(), dC.as<unsigned long long>(), I->num_sms, st); break;
+        default: launch_mc<32>(dXY.as<float>(), dp, npairs, g, dS.as<uint32_t>(), dC.as<unsigned long long>(), I->num_sms, st); break;
+    }
+    PFG_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> cnt(34 * 41);
+    PFG_CUDA(cudaMemcpyAsync(cnt.data(), dC.p, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
+    PFG_CUDA(cudaStreamSynchronize(st));
+    const int ell = g.ell;
+    std::vector<double>& T = I->cpT;
+    T.assign((size_t)(ell + 1) * 41, 1.0);
+    for (int b = 1; b <= ell; ++b) {
+        for (int a = 0; a < 41; ++a) T[b * 41 + a] = (double)cnt[b * 41 + a] / (double)draws;
+        T[b * 41 + 40] = 1.0;
+        for (int a = 39; a >= 0; --a)
+            if (T[b * 41 + a + 1] < T[b * 41 + a]) T[b * 41 + a] = T[b * 41 + a + 1];
+    }
+    for (int b = 2; b <= ell; ++b)
+        for (int a = 0; a < 41; ++a)
+            if (T[(b - 1) * 41 + a] < T[b * 41 + a]) T[b * 41 + a] = T[(b - 1) * 41 + a];
+    return PFG_OK;
+}
+
+pfg_status gen_functions(pfg_index* I, cudaStream_t st) {
+    const Geo& g = I->g;
+    const uint64_t seed = I->seed;
+    // sketch functions: [64M][dpad] Gaussian, stream kTagSketch, element f*d + t
+    if (g.M > 0) {
+        const int64_t F = 64ll * g.M;
+        std::vector<float> A((size_t)F * g.dpad, 0.0f);
+        const uint64_t ks = stream_key(seed, kTagSketch);
+        for (int64_t f = 0; f < F; ++f)
+            for (int t = 0; t < g.d; ++t) A[(size_t)f * g.dpad + t] = (float)gauss(ks, (uint64_t)(f * g.d + t));
+        PFG_TRY(I->skfn.alloc(A.size() * 4, "sketch functions"));
+        PFG_CUDA(cudaMemcpyAsync(I->skfn.p, A.data(), A.size() * 4, cudaMemcpyHostToDevice, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+    }
+    // slot of repetition j
+    I->slot_h.assign(g.L, 0);
+    std::vector<uint8_t> sl(g.L, 0);
+    const uint64_t kl = stream_key(seed, kTagSlot);
+    for (int j = 0; j < g.L; ++j) {
+        I->slot_h[j] = g.M > 0 ? (int32_t)(draw(kl, (uint64_t)j) % (uint64_t)g.M) : 0;
+        sl[j] = (uint8_t)I->slot_h[j];
+    }
+    PFG_TRY(I->slot.alloc(g.L, "slots"));
+    PFG_CUDA(cudaMemcpyAsync(I->slot.p, sl.data(), g.L, cudaMemcpyHostToDevice, st));
+    // LSH functions: F = L*c (independent) or m (pool)
+    const int64_t F = g.strategy == PFG_POOL ? (int64_t)g.m : (int64_t)g.L * g.c;
+    if (g.family == PFG_SIMHASH) {
+        std::vector<float> A((size_t)F * g.dpad, 0.0f);
+        const uint64_t kh = stream_key(seed, kTagHP);
+        for (int64_t f = 0; f < F; ++f)
+            for (int t = 0; t < g.d; ++t) A[(size_t)f * g.dpad + t] = (float)gauss(kh, (uint64_t)(f * g.d + t));
+        PFG_TRY(I->hpfn.alloc(A.size() * 4, "hp functions"));
+        PFG_CUDA(cudaMemcpyAsync(I->hpfn.p, A.data(), A.size() * 4, cudaMemcpyHostToDevice, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+    } else {
+        std::vector<uint32_t> S((size_t)F * 3 * g.W, 0u);
+        const uint64_t kf = stream_key(seed, kTagFHT);
+        for (int64_t f = 0; f < F; ++f)
+            for (int r = 0; r < 3; ++r)
+                for (int u = 0; u < g.dp; ++u)
+                    if (draw(kf, (uint64_t)((f * 3 + r) * g.dp + u)) >> 63)
+                        S[(size_t)(f * 3 + r) * g.W + (u >> 5)] |= 1u << (u & 31);
+        PFG_TRY(I->sg.alloc(S.size() * 4, "fht signs"));
+        PFG_CUDA(cudaMemcpyAsync(I->sg.p, S.data(), S.size() * 4, cudaMemcpyHostToDevice, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+    }
+    if (g.strategy == PFG_POOL) {
+        // PAPER.md:886 random subsets of the pool: partial Fisher-Yates per repetition
+        const uint64_t kp = stream_key(seed, kTagPool);
+        I->sel_h.assign((size_t)g.L * g.c, 0);
+        std::vector<int32_t> perm(g.m);
+        for (int j = 0; j < g.L; ++j) {
+            for (int f = 0; f < g.m; ++f) perm[f] = f;
+            for (int t = 0; t < g.c; ++t) {
+                const int64_t r = t + (int64_t)(draw(kp, (uint64_t)j * g.c + t) % (uint64_t)(g.m - t));
+                std::swap(perm[t], perm[r]);
+                I->sel_h[(size_t)j * g.c + t] = perm[t];
+            }
+        }
+        PFG_TRY(I->sel.alloc(I->sel_h.size() * 4, "pool selection"));
+        PFG_CUDA(cudaMemcpyAsync(I->sel.p, I->sel_h.data(), I->sel_h.size() * 4, cudaMemcpyHostToDevice, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+    }
+    return PFG_OK;
+}
+
+// codes of np normalised rows X for repetitions [r0, r0+nb): keys [r][p] and/or codes [p][ldc]
+// (pool strategy: pool values computed once into `poolvals`)
+pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, uint64_t* keys, uint32_t* codes, int ldc,
+                     DBuf& bits, DBuf& poolvals, bool& pool_ready, cudaStream_t st) {
+    const Geo& g = I->g;
+    const dim3 blk(256);
+    const dim3 grd((unsigned)((np + 255) / 256), (unsigned)nb);
+    if (g.family == PFG_SIMHASH) {
+        if (g.strategy == PFG_INDEPENDENT) {
+            const int nf = nb * g.K;
+            const int wpr = (nf + 63) / 64;
+            PFG_TRY(bits.ensure((size_t)np * wpr * 8, "hp bits"));
+            hp_bits(X, np, g.dpad, I->hpfn.as<float>() + (size_t)r0 * g.K * g.dpad, nf, g.dpad, g.dpad,
+                    bits.as<uint8_t>(), (int64_t)wpr * 8, st);
+            k_codes_from_bits<<<grd, blk, 0, st>>>(bits.as<uint64_t>(), np, wpr, r0, nb, g.K, nullptr, r0, keys, codes, ldc);
+        } else {
+            const int wpr = (g.m + 63) / 64;
+            if (!pool_ready) {
+                PFG_TRY(poolvals.ensure((size_t)np * wpr * 8, "pool bits"));
+                hp_bits(X, np, g.dpad, I->hpfn.as<float>(), g.m, g.dpad, g.dpad, poolvals.as<uint8_t>(), (int64_t)wpr * 8, st);
+                pool_ready = true;
+            }
+            k_codes_from_bits<<<grd, blk, 0, st>>>(poolvals.as<uint64_t>(), np, wpr, r0, nb, g.K, I->sel.as<int32_t>(), 0,
+                                                   keys, codes, ldc);
+        }
+    } else {
+        if (g.strategy == PFG_INDEPENDENT) {
+            fht_rep(X, np, g.dpad, g, I->sg.as<uint32_t>(), r0, nb, keys, codes, ldc, I->num_sms, st);
+        } else {
+            if (!pool_ready) {
+                PFG_TRY(poolvals.ensure((size_t)np * g.m * 2, "pool codes"));
+                fht_funcs(X, np, g.dpad, g, I->sg.as<uint32_t>(), poolvals.as<uint16_t>(), I->num_sms, st);
+                pool_ready = true;
+            }
+            k_pool_codes<<<grd, blk, 0, st>>>(poolvals.as<uint16_t>(), np, g.m, r0, nb, g.c, g.ell, g.K,
+                                              I->sel.as<int32_t>(), keys, codes, ldc);
+        }
+    }
+    PFG_CUDA(cudaGetLastError());
+    return PFG_OK;
+}
+
+pfg_status normalize_rows(const float* src, int64_t n, int d, float* dst, int dpad, uint8_t* zflag,
+                          unsigned long long* zmin_dev, int64_t* zrow, cudaStream_t st) {
+    PFG_CUDA(cudaMemsetAsync(zmin_dev, 0xff, 8, st));
+    k_normalize<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(src, n, d, d, dst, dpad, zflag, zmin_dev);
+    PFG_CUDA(cudaGetLastError());
+    unsigned long long z = 0;
+    PFG_CUDA(cudaMemcpyAsync(&z, zmin_dev, 8, cudaMemcpyDeviceToHost, st));
+    PFG_CUDA(cudaStreamSynchronize(st));
+    *zrow = (z == ~0ull) ? -1 : (int64_t)z;
+    return PFG_OK;
+}
+
+// stop/threshold tables for (recall, rule, granularity); cached on the index
+pfg_status get_thr(pfg_index* I, float recall, const SearchCfg& s, std::shared_ptr<DBuf>& out, std::vector<float>* host) {
+    uint32_t rb;
+    std::memcpy(&rb, &recall, 4);
+    const auto key = std::make_tuple(rb, s.rule, s.per_round);
+    auto it = I->thr_cache.find(key);
+    if (it != I->thr_cache.end() && !host) {
+        out = it->second;
+        return PFG_OK;
+    }
+    const Geo& g = I->g;
+    const double delta = 1.0 - (double)recall;
+    StopModel sm{g.family, g.strategy, g.ell, g.m, I->cpT.empty() ? nullptr : I->cpT.data()};
+    std::vector<float> thr((size_t)g.K * g.L);
+    auto work = [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i)
+            for (int j = 1; j <= g.L; ++j) {
+                float v;
+                if (s.per_round && j < g.L) v = INFINITY;
+                else v = smallest_true([&](float ip) { return sm.stop(i, j, ip, delta, s.rule); });
+                thr[(size_t)(i - 1) * g.L + (j - 1)] = v;
+            }
+    };
+    {
+        unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (unsigned k = 0; k < nt; ++k) {
+            const int i0 = 1 + (int)(k * g.K / nt), i1 = 1 + (int)((k + 1) * g.K / nt);
+            if (i0 < i1) th.emplace_back(work, i0, i1);
+        }
+        for (auto& t : th) t.join();
+    }
+    if (host) *host = thr;
+    auto buf = std::make_shared<DBuf>();
+    PFG_TRY(buf->alloc(thr.size() * 4, "stop thresholds"));
+    PFG_CUDA(cudaMemcpy(buf->p, thr.data(), thr.size() * 4, cudaMemcpyHostToDevice));
+    I->thr_cache[key] = buf;
+    out = buf;
+    return PFG_OK;
+}
+
+pfg_status get_tau(pfg_index* I, float eps, std::shared_ptr<DBuf>& out, std::vector<float>* host) {
+    uint32_t eb;
+    std::memcpy(&eb, &eps, 4);
+    auto it = I->tau_cache.find(eb);
+    if (it != I->tau_cache.end() && !host) {
+        out = it->second;
+        return PFG_OK;
+    }
+    std::vector<float> tb(65);
+    for (int t = 0; t < 65; ++t) tb[t] = smallest_true([&](float ip) { return tau_of(ip, eps) <= t; });
+    tb[64] = -1.0f;
+    if (host) *host = tb;
+    auto buf = std::make_shared<DBuf>();
+    PFG_TRY(buf->alloc(65 * 4, "tau breakpoints"));
+    PFG_CUDA(cudaMemcpy(buf->p, tb.data(), 65 * 4, cudaMemcpyHostToDevice));
+    I->tau_cache[eb] = buf;
+    out = buf;
+    return PFG_OK;
+}
+
+// normalise + sketch + (eager) code queries into index scratch; returns first zero row or -1
+pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool need_codes, bool force_codes, int64_t* zrow,
+                        bool* lazy, cudaStream_t st) {
+    const Geo& g = I->g;
+    const float* qsrc = queries;
+    if (!is_device_ptr(queries)) {
+        PFG_TRY(I->qraw.ensure((size_t)nq * g.d * 4, "query copy"));
+        PFG_CUDA(cudaMemcpyAsync(I->qraw.p, queries, (size_t)nq * g.d * 4, cudaMemcpyHostToDevice, st));
+        qsrc = I->qraw.as<float>();
+    }
+    PFG_TRY(I->qx.ensure((size_t)nq * g.dpad * 4, "queries"));
+    PFG_TRY(I->qzero.ensure((size_t)nq, "query zero flags"));
+    PFG_TRY(I->zmin.ensure(8, "zmin"));
+    PFG_TRY(normalize_rows(qsrc, nq, g.d, I->qx.as<float>(), g.dpad, I->qzero.as<uint8_t>(),
+                           I->zmin.as<unsigned long long>(), zrow, st));
+    if (g.M > 0) {
+        PFG_TRY(I->qsk.ensure((size_t)nq * g.M * 8, "query sketches"));
+        hp_bits(I->qx.as<float>(), nq, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->qsk.as<uint8_t>(),
+                (int64_t)g.M * 8, st);
+        PFG_CUDA(cudaGetLastError());
+    }
+    *lazy = (g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT && !force_codes);
+    if (need_codes && !*lazy) {
+        PFG_TRY(I->qcodes.ensure((size_t)nq * g.L * 4, "query codes"));
+        bool pool_ready = false;
+        PFG_TRY(hash_reps(I, I->qx.as<float>(), nq, 0, g.L, nullptr, I->qcodes.as<uint32_t>(), g.L, I->qbits, I->qfc,
+                          pool_ready, st));
+    }
+    return PFG_OK;
+}
+
+template <int EPL>
+pfg_status launch_query_t(const QueryParams& p, int blocks, size_t smem, cudaStream_t st) {
+    PFG_CUDA(cudaFuncSetAttribute(k_query<EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_query<EPL><<<blocks, 128, smem, st>>>(p);
+    PFG_CUDA(cudaGetLastError());
+    return PFG_OK;
+}
+template <int EPL>
+int query_occupancy(size_t smem) {
+    int nb = 0;
+    cudaFuncSetAttribute(k_query<EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_query<EPL>, 128, smem) != cudaSuccess) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    return std::max(1, nb);
+}
+
+int epl_of(const Geo& g) { return std::max(1, g.dp / 32); }
+
+}  // namespace
+}  // namespace pfg
+
+// =============================================================================================
+extern "C" {
+
+const char* pfg_last_error(void) { return g_err.c_str(); }
+int32_t pfg_abi_version(void) { return PFG_ABI_VERSION; }
+
+pfg_status pfg_derive_reps(int64_t n, int32_t d, int32_t family, uint64_t budget, const pfg_build_opts* opts,
+                           int32_t* reps_out, uint64_t* min_budget_out, uint64_t* index_bytes_out) {
+    Geo g;
+    PFG_TRY(resolve_opts(opts, n, d, family, g));
+    if (min_budget_out) *min_budget_out = g.fixed_bytes + g.per_rep_bytes;
+    pfg_status s = derive_L(g, budget, opts ? opts->reps_override : 0);
+    if (s != PFG_OK) return s;
+    if (reps_out) *reps_out = g.L;
+    if (index_bytes_out) *index_bytes_out = g.index_bytes;
+    return PFG_OK;
+}
+
+pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t budget, int32_t family, uint64_t seed,
+                     const pfg_build_opts* opts, void* stream, pfg_index** out) {
+    if (!out) return fail(PFG_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!data) return fail(PFG_E_ARG, "data is NULL");
+    std::unique_ptr<pfg_index> I(new pfg_index());
+    PFG_TRY(resolve_opts(opts, n, d, family, I->g));
+    PFG_TRY(derive_L(I->g, budget, opts ? opts->reps_override : 0));
+    Geo& g = I->g;
+    I->seed = seed;
+    cudaStream_t st = (cudaStream_t)stream;
+    PFG_CUDA(cudaGetDevice(&I->device));
+    PFG_CUDA(cudaDeviceGetAttribute(&I->num_sms, cudaDevAttrMultiProcessorCount, I->device));
+    // a1: normalise the data into index memory
+    {
+        DBuf raw;
+        const float* src = data;
+        if (!is_device_ptr(data)) {
+            PFG_TRY(raw.alloc((size_t)n * d * 4, "data copy"));
+            PFG_CUDA(cudaMemcpyAsync(raw.p, data, (size_t)n * d * 4, cudaMemcpyHostToDevice, st));
+            src = raw.as<float>();
+        }
+        PFG_TRY(I->x.alloc((size_t)n * g.dpad * 4, "data"));
+        DBuf zm;
+        PFG_TRY(zm.alloc(8, "zmin"));
+        int64_t zrow = -1;
+        PFG_TRY(normalize_rows(src, n, d, I->x.as<float>(), g.dpad, nullptr, zm.as<unsigned long long>(), &zrow, st));
+        if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "data row " + std::to_string(zrow) + " is a zero vector");
+    }
+    // a2: functions
+    PFG_TRY(gen_functions(I.get(), st));
+    // a4: sketches
+    if (g.M > 0) {
+        PFG_TRY(I->sk.alloc((size_t)n * g.M * 8, "sketches"));
+        hp_bits(I->x.as<float>(), n, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->sk.as<uint8_t>(),
+                (int64_t)g.M * 8, st);
+        PFG_CUDA(cudaGetLastError());
+    }
+    // a3 + a5: hash, sort and tabulate the repetitions in batches
+    PFG_TRY(I->tab.alloc((size_t)g.L * n * 8, "tables"));
+    PFG_TRY(I->pt.alloc((size_t)g.L * 8193 * 4, "prefix tables"));
+    {
+        const int64_t budget_keys = (int64_t)1 << 28;  // 2 GiB of keys per batch
+        const int Rb = (int)std::max<int64_t>(1, std::min<int64_t>(g.L, budget_keys / n));
+        DBuf keys, bits, poolvals, temp;
+        PFG_TRY(keys.alloc((size_t)Rb * n * 8, "build keys"));
+        size_t temp_bytes = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, temp_bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, 32,
+                                       32 + g.K, st);
+        PFG_TRY(temp.alloc(temp_bytes, "sort temp"));
+        bool pool_ready = false;
+        for (int r0 = 0; r0 < g.L; r0 += Rb) {
+            const int nb = std::min(Rb, g.L - r0);
+            PFG_TRY(hash_reps(I.get(), I->x.as<float>(), n, r0, nb, keys.as<uint64_t>(), nullptr, 0, bits, poolvals,
+                              pool_ready, st));
+            for (int r = 0; r < nb; ++r) {
+                const int j = r0 + r;
+                uint64_t* dst = I->tab.as<uint64_t>() + (size_t)j * n;
+                size_t tb = temp.bytes;
+                PFG_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, tb, keys.as<uint64_t>() + (size_t)r * n, dst, (int)n, 32,
+                                                        32 + g.K, st));
+                k_prefix<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(dst, n, g.K, I->pt.as<uint32_t>() + (size_t)j * 8193);
+                PFG_CUDA(cudaGetLastError());
+            }
+        }
+        PFG_CUDA(cudaStreamSynchronize(st));
+    }
+    if (g.family == PFG_CROSSPOLYTOPE_FHT) PFG_TRY(build_cp_table(I.get(), st));
+    PFG_CUDA(cudaStreamSynchronize(st));
+    *out = I.release();
+    return PFG_OK;
+}
+
+pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k, float recall, const pfg_search_opts* opts,
+                      int64_t* out_ids, float* out_sims, pfg_query_stats* stats, void* stream) {
+    if (!I) return fail(PFG_E_ARG, "index is NULL");
+    if (nq > 0 && (!queries || !out_ids || !out_sims)) return fail(PFG_E_ARG, "NULL queries or outputs");
+    if (nq < 0 || nq >= (int64_t(1) << 31)) return fail(PFG_E_ARG, "nq must be in [0, 2^31)");
+    if (k < 1 || k > kMaxK) return fail(PFG_E_ARG, "k must be in [1, 256]");
+    if (!(recall > 0.0f && recall <= 1.0f)) return fail(PFG_E_ARG, "recall target must be in (0, 1]");
+    SearchCfg s;
+    PFG_TRY(resolve_sopts(opts, s));
+    if (nq == 0) return PFG_OK;
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const Geo& g = I->g;
+    std::shared_ptr<DBuf> thr, taub;
+    PFG_TRY(get_thr(I, recall, s, thr, nullptr));
+    PFG_TRY(get_tau(I, s.eps, taub, nullptr));
+    int64_t zrow = -1;
+    bool lazy = false;
+    PFG_TRY(prep_queries(I, queries, nq, true, false, &zrow, &lazy, st));
+
+    const int k_eff = (int)std::min<int64_t>(k, g.n);
+    const int kt = ((k_eff + 31) / 32) * 32;
+    const int smem_warp = warp_smem_bytes(g.dpad, g.M, kt);
+    const size_t smem = (size_t)smem_warp * 4;
+    const int epl = lazy ? epl_of(g) : 1;
+    int occ = 1;
+    switch (epl) {
+        case 1: occ = query_occupancy<1>(smem); break;
+        case 2: occ = query_occupancy<2>(smem); break;
+        case 4: occ = query_occupancy<4>(smem); break;
+        case 8: occ = query_occupancy<8>(smem); break;
+        case 16: occ = query_occupancy<16>(smem); break;
+        default: occ = query_occupancy<32>(smem); break;
+    }
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * occ));
+    const int64_t slots = blocks * 4;
+    const int64_t bm_words = (g.n + 31) / 32;
+    if (slots > I->slots || g.L != I->slots_L) {
+        PFG_TRY(I->cur.alloc((size_t)slots * g.L * 16, "cursors"));
+        PFG_TRY(I->bitmap.alloc((size_t)slots * bm_words * 4, "bitmaps"));
+        PFG_TRY(I->claims.alloc((size_t)slots * kClaimCap * 4, "claims"));
+        PFG_CUDA(cudaMemsetAsync(I->bitmap.p, 0, (size_t)slots * bm_words * 4, st));
+        I->slots = slots;
+        I->slots_L = g.L;
+        I->slots_bm = bm_words;
+    }
+    PFG_TRY(I->work.ensure(8, "work counter"));
+    PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
+
+    const bool ids_dev = is_device_ptr(out_ids), sims_dev = is_device_ptr(out_sims);
+    const bool stats_dev = stats ? is_device_ptr(stats) : true;
+    const bool trace_dev = s.trace_cap > 0 ? is_device_ptr(s.trace_ids) : true;
+    int64_t* d_ids = out_ids;
+    float* d_sims = out_sims;
+    pfg_query_stats* d_stats = stats;
+    uint32_t* d_trace = s.trace_ids;
+    if (!ids_dev) { PFG_TRY(I->outb_ids.ensure((size_t)nq * k * 8, "ids")); d_ids = I->outb_ids.as<int64_t>(); }
+    if (!sims_dev) { PFG_TRY(I->outb_sims.ensure((size_t)nq * k * 4, "sims")); d_sims = I->outb_sims.as<float>(); }
+    if (stats && !stats_dev) { PFG_TRY(I->outb_stats.ensure((size_t)nq * sizeof(pfg_query_stats), "stats")); d_stats = I->outb_stats.as<pfg_query_stats>(); }
+    if (s.trace_cap > 0 && !trace_dev) { PFG_TRY(I->outb_trace.ensure((size_t)nq * s.trace_cap * 4, "trace")); d_trace = I->outb_trace.as<uint32_t>(); }
+
+    QueryParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.n = g.n; p.nq = nq; p.bm_words = bm_words; p.id_offset = g.id_offset;
+    p.d = g.d; p.dpad = g.dpad; p.K = g.K; p.L = g.L; p.M = g.M; p.B = s.B; p.R = s.R; p.k = k; p.k_eff = k_eff;
+    p.per_round = s.per_round; p.use_filter = (s.use_filter && g.M > 0) ? 1 : 0; p.c = g.c; p.ell = g.ell; p.dp = g.dp;
+    p.lazy = lazy ? 1 : 0; p.claim_cap = kClaimCap; p.trace_cap = s.trace_cap; p.kt = kt; p.smem_warp = smem_warp;
+    p.x = I->x.as<float>(); p.sk = I->sk.as<uint64_t>(); p.tab = I->tab.as<uint64_t>(); p.pt = I->pt.as<uint32_t>();
+    p.slot = I->slot.as<uint8_t>(); p.qx = I->qx.as<float>(); p.qsk = I->qsk.as<uint64_t>();
+    p.qcodes = lazy ? nullptr : I->qcodes.as<uint32_t>(); p.sg = I->sg.as<uint32_t>(); p.qzero = I->qzero.as<uint8_t>();
+    p.thr = thr->as<float>(); p.taub = taub->as<float>(); p.work = I->work.as<unsigned long long>();
+    p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
+    p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
+    switch (epl) {
+        case 1: PFG_TRY(launch_query_t<1>(p, (int)blocks, smem, st)); break;
+        case 2: PFG_TRY(launch_query_t<2>(p, (int)blocks, smem, st)); break;
+        case 4: PFG_TRY(launch_query_t<4>(p, (int)blocks, smem, st)); break;
+        case 8: PFG_TRY(launch_query_t<8>(p, (int)blocks, smem, st)); break;
+        case 16: PFG_TRY(launch_query_t<16>(p, (int)blocks, smem, st)); break;
+        default: PFG_TRY(launch_query_t<32>(p, (int)blocks, smem, st)); break;
+    }
+    if (!ids_dev) PFG_CUDA(cudaMemcpyAsync(out_ids, d_ids, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
+    if (!sims_dev) PFG_CUDA(cudaMemcpyAsync(out_sims, d_sims, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));
+    if (stats && !stats_dev)
+        PFG_CUDA(cudaMemcpyAsync(stats, d_stats, (size_t)nq * sizeof(pfg_query_stats), cudaMemcpyDeviceToHost, st));
+    if (s.trace_cap > 0 && !trace_dev)
+        PFG_CUDA(cudaMemcpyAsync(s.trace_ids, d_trace, (size_t)nq * s.trace_cap * 4, cudaMemcpyDeviceToHost, st));
+    PFG_CUDA(cudaStreamSynchronize(st));
+    if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(zrow) + " is a zero vector");
+    return PFG_OK;
+}
+
+pfg_status pfg_merge_topk(const int64_t* ids, const float* sims, int32_t world, int64_t nq, int32_t k, int64_t* out_ids,
+                          float* out_sims, void* stream) {
+    if (!ids || !sims || !out_ids || !out_sims) return fail(PFG_E_ARG, "NULL pointer");
+    if (world < 1 || k < 1 || nq < 0) return fail(PFG_E_ARG, "world, k must be >= 1");
+    if ((int64_t)world * k > 4096) return fail(PFG_E_ARG, "world * k must be <= 4096");
+    if (nq == 0) return PFG_OK;
+    if (!is_device_ptr(ids) || !is_device_ptr(sims) || !is_device_ptr(out_ids) || !is_device_ptr(out_sims))
+        return fail(PFG_E_ARG, "pfg_merge_topk takes device pointers");
+    const size_t smem = (size_t)4 * world * k * 16;
+    cudaStream_t st = (cudaStream_t)stream;
+    PFG_CUDA(cudaFuncSetAttribute(k_merge_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_merge_topk<<<(unsigned)((nq + 3) / 4), 128, smem, st>>>(ids, sims, world, nq, k, out_ids, out_sims);
+    PFG_CUDA(cudaGetLastError());
+    return PFG_OK;
+}
+
+pfg_status pfg_index_info(const pfg_index* I, pfg_index_info_t* out) {
+    if (!I || !out) return fail(PFG_E_ARG, "NULL pointer");
+    const Geo& g = I->g;
+    std::memset(out, 0, sizeof(*out));
+    out->n = g.n; out->d = g.d; out->d_pad = g.dpad; out->family = g.family; out->strategy = g.strategy;
+    out->prefix_bits = g.K; out->reps = g.L; out->ell = g.ell; out->funcs_per_rep = g.c; out->sketch_words = g.M;
+    out->pool_funcs = g.m; out->fht_dim = g.dp; out->device = I->device;
+    out->index_bytes = g.index_bytes;
+    out->scratch_bytes = I->cur.bytes + I->bitmap.bytes + I->claims.bytes;
+    out->seed = I->seed; out->id_offset = g.id_offset;
+    return PFG_OK;
+}
+
+pfg_status pfg_export(const pfg_index* Ic, int32_t what, int32_t arg, void* dst, uint64_t bytes) {
+    pfg_index* I = const_cast<pfg_index*>(Ic);
+    if (!I || !dst) return fail(PFG_E_ARG, "NULL pointer");
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    const Geo& g = I->g;
+    auto copy = [&](const void* src, uint64_t need) -> pfg_status {
+        if (bytes != need) return fail(PFG_E_ARG, "dst_bytes must be " + std::to_string(need));
+        PFG_CUDA(cudaMemcpy(dst, src, need, cudaMemcpyDeviceToHost));
+        return PFG_OK;
+    };
+    switch (what) {
+        case PFG_EXPORT_TABLE:
+            if (arg < 0 || arg >= g.L) return fail(PFG_E_ARG, "rep out of range");
+            return copy(I->tab.as<uint64_t>() + (size_t)arg * g.n, (uint64_t)g.n * 8);
+        case PFG_EXPORT_PREFIX:
+            if (arg < 0 || arg >= g.L) return fail(PFG_E_ARG, "rep out of range");
+            return copy(I->pt.as<uint32_t>() + (size_t)arg * 8193, 8193ull * 4);
+        case PFG_EXPORT_SKETCH:
+            if (g.M == 0) return fail(PFG_E_STATE, "index has no sketches");
+            return copy(I->sk.p, (uint64_t)g.n * g.M * 8);
+        case PFG_EXPORT_DATA: {
+            if (bytes != (uint64_t)g.n * g.d * 4) return fail(PFG_E_ARG, "dst_bytes must be n*d*4");
+            PFG_CUDA(cudaMemcpy2D(dst, (size_t)g.d * 4, I->x.p, (size_t)g.dpad * 4, (size_t)g.d * 4, (size_t)g.n,
+                                  cudaMemcpyDeviceToHost));
+            return PFG_OK;
+        }
+        case PFG_EXPORT_CP:
+            if (I->cpT.empty()) return fail(PFG_E_STATE, "index has no CP table (SimHash family)");
+            if (bytes != I->cpT.size() * 8) return fail(PFG_E_ARG, "dst_bytes must be (ell+1)*41*8");
+            std::memcpy(dst, I->cpT.data(), bytes);
+            return PFG_OK;
+        case PFG_EXPORT_SLOTS:
+            if (bytes != (uint64_t)g.L * 4) return fail(PFG_E_ARG, "dst_bytes must be L*4");
+            std::memcpy(dst, I->slot_h.data(), bytes);
+            return PFG_OK;
+        case PFG_EXPORT_POOLSEL:
+            if (g.strategy != PFG_POOL) return fail(PFG_E_STATE, "index is not pooled");
+            if (bytes != I->sel_h.size() * 4) return fail(PFG_E_ARG, "dst_bytes must be L*c*4");
+            std::memcpy(dst, I->sel_h.data(), bytes);
+            return PFG_OK;
+        default:
+            return fail(PFG_E_ARG, "unknown export");
+    }
+}
+
+pfg_status pfg_hash_queries(pfg_index* I, const float* queries, int64_t nq, uint32_t* out_codes, uint64_t* out_sketches,
+                            void* stream) {
+    if (!I || !queries) return fail(PFG_E_ARG, "NULL pointer");
+    if (nq < 1) return fail(PFG_E_ARG, "nq must be >= 1");
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const Geo& g = I->g;
+    int64_t zrow = -1;
+    bool lazy = false;
+    PFG_TRY(prep_queries(I, queries, nq, out_codes != nullptr, true, &zrow, &lazy, st));
+    if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(zrow) + " is a zero vector");
+    if (out_codes) {
+        const size_t b = (size_t)nq * g.L * 4;
+        PFG_CUDA(cudaMemcpyAsync(out_codes, I->qcodes.p, b, is_device_ptr(out_codes) ? cudaMemcpyDeviceToDevice
+                                                                                   : cudaMemcpyDeviceToHost, st));
+    }
+    if (out_sketches && g.M > 0) {
+        const size_t b = (size_t)nq * g.M * 8;
+        PFG_CUDA(cudaMemcpyAsync(out_sketches, I->qsk.p, b, is_device_ptr(out_sketches) ? cudaMemcpyDeviceToDevice
+                                                                                        : cudaMemcpyDeviceToHost, st));
+    }
+    PFG_CUDA(cudaStreamSynchronize(st));
+    return PFG_OK;
+}
+
+pfg_status pfg_stop_tables(pfg_index* I, float recall, const pfg_search_opts* opts, float* thr_host, float* tau_host) {
+    if (!I) return fail(PFG_E_ARG, "NULL index");
+    if (!(recall > 0.0f && recall <= 1.0f)) return fail(PFG_E_ARG, "recall target must be in (0, 1]");
+    SearchCfg s;
+    PFG_TRY(resolve_sopts(opts, s));
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    if (thr_host) {
+        std::shared_ptr<DBuf> b;
+        std::vector<float> h;
+        PFG_TRY(get_thr(I, recall, s, b, &h));
+        std::memcpy(thr_host, h.data(), h.size() * 4);
+    }
+    if (tau_host) {
+        std::shared_ptr<DBuf> b;
+        std::vector<float> h;
+        PFG_TRY(get_tau(I, s.eps, b, &h));
+        std::memcpy(tau_host, h.data(), 65 * 4);
+    }
+    return PFG_OK;
+}
+
+void pfg_free(pfg_index* I) {
+    if (!I) return;
+    cudaSetDevice(I->device);
+    delete I;
+}
+
+}  // extern "C"

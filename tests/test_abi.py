@@ -1,0 +1,78 @@
+"""Host-side checks of the C-ABI library (no GPU): it loads, exports every symbol include/pfg.h
+declares, and its host-only logic (the budget -> L cost model, R-11) behaves."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_1906_12211_b200 as pfg
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "pfg.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pfg_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = pfg.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(pfg.EXPORTED) == syms
+    assert lib.pfg_abi_version() == 1
+
+
+def test_abi_struct_sizes_match_header():
+    # the binding's ctypes mirrors must have the C sizes (struct_size versioning)
+    assert C.sizeof(pfg.BuildOpts) == 48
+    assert C.sizeof(pfg.SearchOpts) == 48
+    assert pfg.STATS_DTYPE.itemsize == 32
+    assert C.sizeof(pfg.IndexInfo) == 96
+
+
+def test_cost_model_configs():
+    # SURVEY.md Appendix B (A-11 reading): L for BASELINE configs 2-5 at their budgets (GiB)
+    assert pfg.derive_reps(1_000_000, 100, "fht_cp", 4 << 30)[0] == 452
+    assert pfg.derive_reps(1_000_000, 300, "simhash", 8 << 30)[0] == 884
+    assert pfg.derive_reps(1_000_000, 960, "simhash", 16 << 30, strategy="pool")[0] == 1626
+    assert pfg.derive_reps(12_500_000, 100, "fht_cp", 120 << 30)[0] == 1206
+
+
+def test_cost_model_arithmetic():
+    # budget = fixed + exactly 3 repetitions -> L = 3; one byte less -> 2
+    L, minb, ib = pfg.derive_reps(5000, 40, "simhash", 10 << 30, max_reps=1)
+    per_rep = 8 * 5000 + 4 * 8193 + 1 + 24 * 4 * 40
+    fixed = minb - per_rep
+    assert pfg.derive_reps(5000, 40, "simhash", fixed + 3 * per_rep)[0] == 3
+    assert pfg.derive_reps(5000, 40, "simhash", fixed + 3 * per_rep - 1)[0] == 2
+    assert pfg.derive_reps(5000, 40, "simhash", 1 << 40)[0] == 4096  # cap
+    assert pfg.derive_reps(5000, 40, "simhash", 1 << 40, max_reps=100)[0] == 100
+
+
+def test_cost_model_budget_error_names_minimum():
+    with pytest.raises(pfg.PfgError, match=r"minimum is \d+ B") as e:
+        pfg.derive_reps(1_000_000, 100, "fht_cp", 100 << 20)
+    assert e.value.status == 3
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(prefix_bits=40), "prefix_bits"), (dict(sketch_words=65), "sketch_words"),
+    (dict(strategy=7), "strategy"), (dict(cp_draws=-5), "cp_draws")])
+def test_bad_options_rejected(kw, msg):
+    with pytest.raises(pfg.PfgError, match=msg):
+        pfg.derive_reps(1000, 16, "simhash", 1 << 30, **kw)
+
+
+def test_bad_shapes_rejected():
+    with pytest.raises(pfg.PfgError, match="n must"):
+        pfg.derive_reps(0, 16, "simhash", 1 << 30)
+    with pytest.raises(pfg.PfgError, match="d must"):
+        pfg.derive_reps(10, 0, "simhash", 1 << 30)
+    with pytest.raises(pfg.PfgError, match="d <= 1024"):
+        pfg.derive_reps(10, 2000, "fht_cp", 1 << 30)

@@ -1,0 +1,288 @@
+"""GPU <-> oracle parity through the C-ABI (BASELINE north_star tolerances):
+hash codes, tables, sketches and stop points bit-exact; returned ids and evaluated sets bit-exact
+given identical tables; similarities within 1e-5 absolute (expected bit-equal under R-2)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_1906_12211_b200 as pfg  # noqa: E402
+
+DEV = torch.device("cuda:0")
+SIM_TOL = 1e-5
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+class Case:
+    def __init__(self, name, data, q, family, L, seed, strategy=O.INDEPENDENT, pool_bits=3072, M=32):
+        self.name, self.data, self.q = name, data, q
+        fam = "simhash" if family == O.HP else "fht_cp"
+        strat = "pool" if strategy == O.POOL else "independent"
+        self.gpu = pfg.Index(_cuda(data), 0, fam, seed=seed, reps=L, strategy=strat, pool_bits=pool_bits,
+                             sketch_words=M if M > 0 else -1)
+        self.orc = O.OracleIndex(data, family, L=L, seed=seed, strategy=strategy, pool_bits=pool_bits, M=M)
+
+
+@pytest.fixture(scope="module")
+def cases():
+    out = {}
+    d1, q1 = synth.config_data(1, n=3000, nq=64)
+    out["hp"] = Case("hp", d1, q1, O.HP, 16, 1)
+    d2, q2 = synth.config_data(2, n=20000, nq=100)
+    out["fht"] = Case("fht", d2, q2, O.FHTCP, 24, 3)
+    d3, q3 = synth.config_data(4, n=4000, nq=40)
+    out["hp_pool"] = Case("hp_pool", d3[:, :64].copy(), q3[:, :64].copy(), O.HP, 20, 2, O.POOL, 512)
+    out["fht_pool"] = Case("fht_pool", d2[:6000], q2[:50], O.FHTCP, 20, 5, O.POOL, 3072)
+    return out
+
+
+ALL = ["hp", "fht", "hp_pool", "fht_pool"]
+
+
+# ------------------------------------------------------------------ build-side parity
+@pytest.mark.parametrize("name", ALL)
+def test_build_arrays_bit_exact(cases, name):
+    c = cases[name]
+    g, o = c.gpu, c.orc
+    assert g.reps == o.L and g.ell == o.ell and g.funcs_per_rep == o.c
+    assert np.array_equal(g.export_data().view(np.uint32), o.data().view(np.uint32))
+    assert np.array_equal(g.export_sketches(), o.sketches())
+    assert np.array_equal(g.export_slots(), o.slots())
+    if o.strategy == O.POOL:
+        assert np.array_equal(g.export_pool_sel(), o.pool_sel())
+    for j in range(o.L):
+        tab = g.export_table(j)
+        codes, ids = o.rep(j)
+        assert np.array_equal((tab >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
+        assert np.array_equal(g.export_prefix(j), o.prefix_table(j)), j
+
+
+@pytest.mark.parametrize("name", ["fht", "fht_pool"])
+def test_cp_table_bit_exact(cases, name):
+    c = cases[name]
+    assert np.array_equal(c.gpu.export_cp(), c.orc.cp())
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_query_hashing_bit_exact(cases, name):
+    c = cases[name]
+    gc, gs = c.gpu.hash_queries(c.q)
+    oc, osk = c.orc.hash(c.q)
+    assert np.array_equal(gc, oc)
+    assert np.array_equal(gs, osk)
+
+
+@pytest.mark.parametrize("name", ["hp", "fht", "hp_pool"])
+@pytest.mark.parametrize("recall,rule,per_round", [(0.9, 0, False), (0.5, 1, False), (0.99, 0, True)])
+def test_stop_tables_match_oracle_rule(cases, name, recall, rule, per_round):
+    # the device stops iff ip_k >= thr[i][j]; thr must be the smallest float where the oracle's
+    # direct evaluation of the rule says stop (R-9/R-10)
+    c = cases[name]
+    if c.orc.strategy == O.POOL and rule == 1:
+        return
+    thr, tau = c.gpu.stop_tables(recall, stop_rule=rule, per_round=per_round)
+    delta = 1.0 - np.float64(np.float32(recall))
+    rng = np.random.default_rng(0)
+    L = c.orc.L
+    for i in rng.integers(1, 25, size=12):
+        for j in rng.integers(1, L + 1, size=6):
+            t = thr[i - 1, j - 1]
+            if per_round and j < L:
+                assert np.isinf(t)
+                continue
+            if np.isinf(t):
+                assert not c.orc.should_stop(int(i), int(j), 1.0, delta, rule)
+                continue
+            assert c.orc.should_stop(int(i), int(j), float(t), delta, rule)
+            if t > -1.0:
+                prev = np.nextafter(np.float32(t), np.float32(-2))
+                assert not c.orc.should_stop(int(i), int(j), float(prev), delta, rule)
+    for t in range(64):
+        b = tau[t]
+        assert O.tau(float(b)) <= t
+        if b > -1.0:
+            assert O.tau(float(np.nextafter(np.float32(b), np.float32(-2)))) > t
+
+
+# ------------------------------------------------------------------ search parity
+def _compare(c, k, recall, gpu_kw, orc_kw, trace=True):
+    gpu_kw = dict(gpu_kw); orc_kw = dict(orc_kw)
+    gpu_kw.setdefault("rep_chunk", 8); orc_kw.setdefault("rep_chunk", 8)
+    cap = 1 << 14
+    ids, sims, st, tr = c.gpu.search(_cuda(c.q), k, recall, stats=True, trace_cap=cap, **gpu_kw)
+    ids, sims = ids.cpu().numpy(), sims.cpu().numpy()
+    oids, osims, otr, otids = c.orc.search(c.q, k, recall, trace_cap=cap, **orc_kw)
+    assert np.array_equal(st["i_stop"], otr[:, 0]), "stop level"
+    assert np.array_equal(st["j_stop"], otr[:, 1]), "stop repetition"
+    assert np.array_equal(st["emitted"], otr[:, 2].astype(np.uint32)), "emitted"
+    assert np.array_equal(st["filtered"], otr[:, 3].astype(np.uint32)), "filtered"
+    assert np.array_equal(st["dups"], otr[:, 4].astype(np.uint32)), "dups"
+    assert np.array_equal(st["evaluated"], otr[:, 5].astype(np.uint32)), "evaluated"
+    if trace:
+        for r in range(len(c.q)):
+            n = min(cap, otr[r, 5])
+            assert set(tr[r, :n].tolist()) == set(otids[r, :n].tolist()), f"evaluated set of query {r}"
+    assert np.array_equal(ids, oids), "ids"
+    fin = np.isfinite(osims)
+    assert np.all(np.abs(sims[fin] - osims[fin]) <= SIM_TOL)
+    assert np.array_equal(np.isfinite(sims), fin)
+    return st
+
+
+@pytest.mark.parametrize("name", ALL)
+@pytest.mark.parametrize("R", [1, 8])
+@pytest.mark.parametrize("recall", [0.5, 0.9, 0.99])
+def test_search_parity(cases, name, R, recall):
+    c = cases[name]
+    _compare(c, 10, recall, dict(rep_chunk=R), dict(rep_chunk=R))
+
+
+@pytest.mark.parametrize("name", ["hp", "fht"])
+@pytest.mark.parametrize("kw", [dict(use_filter=False), dict(stop_rule=1), dict(per_round=True),
+                                dict(segment=1), dict(segment=5, rep_chunk=3), dict(eps=0.2), dict(eps=-0.2),
+                                dict(rep_chunk=32)])
+def test_search_parity_options(cases, name, kw):
+    c = cases[name]
+    okw = dict(kw)
+    _compare(c, 10, 0.9, kw, okw)
+
+
+@pytest.mark.parametrize("k", [1, 33, 100])
+def test_search_parity_k(cases, k):
+    _compare(cases["fht"], k, 0.9, dict(rep_chunk=8), dict(rep_chunk=8))
+
+
+def test_exhaustive_recall_one_is_bruteforce(cases):
+    # delta = 0: no stop above i = 0; the i = 0 scan returns the exact top-k (R-13)
+    c = cases["hp"]
+    st = _compare(c, 10, 1.0, dict(rep_chunk=8), dict(rep_chunk=8), trace=False)
+    assert np.all(st["i_stop"] == 0)
+    ids, _, _ = c.gpu.search(_cuda(c.q), 10, 1.0, stats=True)
+    bi, _ = O.bruteforce(c.orc.data(), O.normalize(c.q), 10)
+    assert np.array_equal(ids.cpu().numpy(), bi)
+
+
+def test_k_greater_than_n():
+    data, q = synth.config_data(1, n=7, nq=5)
+    g = pfg.Index(_cuda(data), 0, "simhash", seed=4, reps=3)
+    o = O.OracleIndex(data, O.HP, L=3, seed=4)
+    ids, sims, st = g.search(_cuda(q), 12, 0.9, stats=True)
+    oids, osims, otr = o.search(q, 12, 0.9, rep_chunk=8)
+    assert np.array_equal(ids.cpu().numpy(), oids)
+    assert np.all(ids.cpu().numpy()[:, 7:] == -1) and np.all(np.isneginf(sims.cpu().numpy()[:, 7:]))
+    assert np.all(st["flags"] & 1)
+
+
+def test_zero_query_row_reported_and_others_answered(cases):
+    c = cases["hp"]
+    q = c.q.copy()
+    q[3] = 0
+    with pytest.raises(pfg.PfgError, match="query row 3") as e:
+        c.gpu.search(_cuda(q), 10, 0.9)
+    assert e.value.status == 2
+    # the other rows still get answered
+    ids = torch.empty((len(q), 10), dtype=torch.int64, device=DEV)
+    sims = torch.empty((len(q), 10), dtype=torch.float32, device=DEV)
+    with pytest.raises(pfg.PfgError):
+        c.gpu.search(_cuda(q), 10, 0.9, out=(ids, sims))
+    oids, _, _ = c.orc.search(np.delete(q, 3, axis=0), 10, 0.9, rep_chunk=8)
+    assert np.array_equal(np.delete(ids.cpu().numpy(), 3, axis=0), oids)
+    assert np.all(ids.cpu().numpy()[3] == -1) and np.all(np.isnan(sims.cpu().numpy()[3]))
+
+
+def test_zero_data_row_rejected():
+    data, _ = synth.config_data(1, n=100, nq=1)
+    data[42] = 0
+    with pytest.raises(pfg.PfgError, match="row 42"):
+        pfg.Index(_cuda(data), 0, "simhash", reps=2)
+
+
+def test_bad_arguments(cases):
+    g = cases["hp"].gpu
+    q = _cuda(cases["hp"].q)
+    for kw in (dict(k=0, recall=0.9), dict(k=300, recall=0.9), dict(k=5, recall=0.0), dict(k=5, recall=1.5)):
+        with pytest.raises(pfg.PfgError) as e:
+            g.search(q, **kw)
+        assert e.value.status == 1
+    with pytest.raises(pfg.PfgError, match="rep_chunk"):
+        g.search(q, 5, 0.9, rep_chunk=64)
+
+
+def test_host_buffers_equal_device_buffers(cases):
+    # e2e path: numpy in/out goes through the library's H2D/D2H copies, same results
+    c = cases["fht"]
+    a_ids, a_sims = c.gpu.search(_cuda(c.q), 10, 0.9)
+    b_ids, b_sims = c.gpu.search(c.q, 10, 0.9)
+    assert isinstance(b_ids, np.ndarray)
+    assert np.array_equal(a_ids.cpu().numpy(), b_ids)
+    assert np.array_equal(a_sims.cpu().numpy(), b_sims)
+
+
+def test_repeat_search_is_deterministic(cases):
+    # the per-slot bitmaps are returned to zero after every query
+    c = cases["fht"]
+    r1 = c.gpu.search(_cuda(c.q), 10, 0.99, stats=True)
+    r2 = c.gpu.search(_cuda(c.q[::-1].copy()), 10, 0.99, stats=True)
+    assert np.array_equal(r1[0].cpu().numpy(), r2[0].cpu().numpy()[::-1])
+    assert np.array_equal(r1[2]["evaluated"], r2[2]["evaluated"][::-1])
+
+
+def test_single_query_and_empty_batch(cases):
+    c = cases["hp"]
+    ids, sims = c.gpu.search(_cuda(c.q[:1]), 10, 0.9)
+    oids, _, _ = c.orc.search(c.q[:1], 10, 0.9, rep_chunk=8)
+    assert np.array_equal(ids.cpu().numpy(), oids)
+    e_ids, _ = c.gpu.search(_cuda(c.q[:0]), 10, 0.9)
+    assert e_ids.shape == (0, 10)
+
+
+# ------------------------------------------------------------------ sharded mode (one GPU)
+def test_sharded_merge_equals_per_shard_oracle():
+    # each shard = an index over a contiguous id block with the same seed;
+    # merging shard-local top-k equals merging the oracle's per-shard results (P15)
+    data, q = synth.config_data(2, n=12000, nq=60)
+    world, k = 3, 10
+    per = len(data) // world
+    g_ids, g_sims, o_ids, o_sims = [], [], [], []
+    for r in range(world):
+        sl = data[r * per:(r + 1) * per]
+        g = pfg.Index(_cuda(sl), 0, "fht_cp", seed=7, reps=12, id_offset=r * per)
+        i, s = g.search(_cuda(q), k, 0.9)
+        g_ids.append(i); g_sims.append(s)
+        o = O.OracleIndex(sl, O.FHTCP, L=12, seed=7)
+        oi, os_, _ = o.search(q, k, 0.9, rep_chunk=8)
+        o_ids.append(np.where(oi >= 0, oi + r * per, -1)); o_sims.append(os_)
+    mi, ms = pfg.merge_topk(torch.stack(g_ids), torch.stack(g_sims))
+    ci = np.concatenate(o_ids, axis=1); cs = np.concatenate(o_sims, axis=1)
+    ref = np.empty((len(q), k), np.int64)
+    for t in range(len(q)):
+        order = np.lexsort((ci[t], -cs[t]))[:k]
+        ref[t] = ci[t, order]
+    assert np.array_equal(mi.cpu().numpy(), ref)
+
+
+def test_merge_of_bruteforce_shards_is_global_bruteforce():
+    # P15: merge(brute force per shard) == global brute force (exact identity)
+    rng = np.random.default_rng(5)
+    x = O.normalize(rng.standard_normal((3000, 20)))
+    q = O.normalize(rng.standard_normal((50, 20)))
+    k, world = 7, 4
+    per = 3000 // world
+    ids, sims = [], []
+    for r in range(world):
+        bi, bs = O.bruteforce(x[r * per:(r + 1) * per], q, k)
+        ids.append(bi + r * per); sims.append(bs.astype(np.float32))
+    mi, _ = pfg.merge_topk(_cuda(np.stack(ids)), _cuda(np.stack(sims)))
+    gi, _ = O.bruteforce(x, q, k)
+    assert np.array_equal(mi.cpu().numpy(), gi)
