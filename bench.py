@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the batched LSH-forest k-NN query path (BASELINE.json metric: queries/s at >= 0.9
+recall, k = 10, 1M x 100-d angular; achieved HBM GB/s).
+
+A "step" is one pass of the hot path over one batch: pfg_search over all nq queries of the
+workload (normalise, hash, sketch, adaptive query kernel with its stop rule; plus the NCCL
+all-gather and merge kernel when N > 1).  The index is built once before timing (its time is
+reported as build_s).  Inputs are resident in HBM when a timed step starts; L2 is flushed (512 MiB
+write) between timed steps.  `e2e` repeats the measurement through the same C-ABI call with
+pinned HOST query/result buffers (host<->device copies inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--recall 0.9]
+  python bench.py --impl reference ...   # the CPU oracle (test infrastructure) on the host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "queries/s at >=0.9 recall, k=10, 1Mx100-d angular; achieved HBM GB/s"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region"""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        mx = None
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- helpers
+def cfg_desc(cfg: int):
+    c = synth.CONFIGS[cfg]
+    return c
+
+
+def ground_truth(data_t, q_t, k):
+    """exact top-k by fp32 inner products of the normalised rows (torch, TF32 off; measurement
+    tool, not part of the path).  Returns (ids [nq,k], kth sims [nq])."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    x = data_t / data_t.norm(dim=1, keepdim=True)
+    q = q_t / q_t.norm(dim=1, keepdim=True)
+    ids, kth = [], []
+    for s in range(0, q.shape[0], 1024):
+        S = q[s:s + 1024] @ x.T
+        v, i = torch.topk(S, k, dim=1)
+        ids.append(i)
+        kth.append(v[:, -1])
+        del S
+    return torch.cat(ids), torch.cat(kth), x, q
+
+
+def recall_of(ids_t, truth_kth, xn, qn, k):
+    """tie-tolerant recall@k: a returned id counts if its exact sim >= true k-th sim - 1e-5"""
+    import torch
+    ids = ids_t.clamp(min=0)
+    s = torch.einsum("qd,qkd->qk", qn, xn[ids])
+    hit = (s >= truth_kth[:, None] - 1e-5) & (ids_t >= 0)
+    return float(hit.float().sum() / (k * ids_t.shape[0]))
+
+
+def alg_bytes(stats, d, M, k, use_filter=True):
+    """algorithmic bytes of the query kernel: per query
+    8 B per retrieved table entry + 8 B per sketch word read + 4d B per evaluated row
+    + 4 B per bitmap claim (evaluated + dups) + 8 B per bound-search probe + query row,
+    sketches and outputs."""
+    em = stats["emitted"].astype(np.float64)
+    ev = stats["evaluated"].astype(np.float64)
+    du = stats["dups"].astype(np.float64)
+    pr = stats["probes"].astype(np.float64)
+    b = 8 * em + (8 * em if use_filter else 0) + 4 * d * ev + 4 * (ev + du) + 8 * pr + 4 * d + 8 * M + 12 * k
+    return float(b.sum())
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The CPU oracle as it stands (test infrastructure), timed on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as O
+    c = synth.CONFIGS[args.config]
+    n, nq = c["n"], c["nq"]
+    data, q = synth.config_data(args.config)
+    import paper_1906_12211_b200 as pfg
+    L = c["reps"] or pfg.derive_reps(n, c["d"], c["family"], c["budget"],
+                                     strategy=c["strategy"])[0]
+    fam = O.HP if c["family"] == "simhash" else O.FHTCP
+    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
+    t0 = time.time()
+    X = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
+    sample = args.ref_sample
+    qs = q[:sample]
+    X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk)   # builds the touched repetitions
+    setup = time.time() - t0
+    times = []
+    for s in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        ids, sims, tr = X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk)
+        el = time.perf_counter() - t
+        if s >= args.warmup:
+            times.append(el)
+    tot = sum(times)
+    value = args.steps * sample / tot
+    bi, _ = O.bruteforce(X.data(), O.normalize(qs), c["k"])
+    rec = float(np.mean([len(set(a) & set(b)) / c["k"] for a, b in zip(ids.tolist(), bi.tolist())]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config{args.config}: {c['name']}", "n": n, "d": c["d"], "nq": nq, "k": c["k"],
+                   "recall_target": args.recall, "family": c["family"], "reps": L, "rep_chunk": args.rep_chunk},
+        "recall": rec,
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first {sample} of {nq} queries per step, single thread, lazily built "
+                                   f"oracle index ({setup:.0f} s setup untimed)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_leg(cfg, recall, rep_chunk, sample):
+    import oracle as O
+    import paper_1906_12211_b200 as pfg
+    c = synth.CONFIGS[cfg]
+    data, q = synth.config_data(cfg)
+    L = c["reps"] or pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
+    fam = O.HP if c["family"] == "simhash" else O.FHTCP
+    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
+    t0 = time.time()
+    X = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
+    qs = q[:sample]
+    X.search(qs, c["k"], recall, rep_chunk=rep_chunk)
+    setup = time.time() - t0
+    t = time.perf_counter()
+    X.search(qs, c["k"], recall, rep_chunk=rep_chunk)
+    el = time.perf_counter() - t
+    return {"value": sample / el, "unit": "queries/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {sample} of {c['nq']} queries, single thread (the paper's protocol, PAPER.md:362-363), "
+                      f"lazily built oracle index, {setup:.0f} s setup untimed"}
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--recall", type=float, default=0.9)
+    ap.add_argument("--rep-chunk", type=int, default=8)
+    ap.add_argument("--nq", type=int, default=0, help="override the query count")
+    ap.add_argument("--ref-sample", type=int, default=20)
+    ap.add_argument("--cpu-sample", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1906_12211_b200 as pfg
+    from paper_1906_12211_b200.sharded import ShardedIndex, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    c = synth.CONFIGS[args.config]
+    n, d, k = c["n"], c["d"], c["k"]
+    nq = args.nq or c["nq"]
+    lo, hi = shard_range(n, world, rank)
+    data_np, q_np = synth.config_data(args.config, n=hi - lo, nq=nq, row0=lo)
+    data = torch.from_numpy(data_np).to(dev)
+    q = torch.from_numpy(q_np).to(dev)
+    del data_np
+
+    opts = dict(strategy=c["strategy"])
+    if c["reps"]:
+        opts["reps"] = c["reps"]
+    torch.cuda.synchronize()
+    t0 = time.time()
+    idx = ShardedIndex(data, lo, c["budget"] or 0, c["family"], seed=1, **opts)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    info = idx.index.info
+
+    # ground truth (global): shard-local exact top-k, gathered and merged like the search
+    t_ids, t_kth, xn, qn = ground_truth(data, q, k)
+    if world > 1:
+        gi = torch.empty((world, nq, k), dtype=torch.int64, device=dev)
+        gs = torch.empty((world, nq, k), dtype=torch.float32, device=dev)
+        sims_local = torch.einsum("qd,qkd->qk", qn, xn[t_ids])
+        dist.all_gather_into_tensor(gi, t_ids + lo)
+        dist.all_gather_into_tensor(gs, sims_local.contiguous())
+        _, ms = pfg.merge_topk(gi, gs)
+        t_kth = ms[:, -1].contiguous()
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sopts = dict(rep_chunk=args.rep_chunk, timing=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    t_w = time.time()
+    while True:  # warm-up: at least `warmup` steps and ~1 s so the clock sampler is running
+        for _ in range(args.warmup):
+            idx.search(q, k, args.recall, **sopts)
+        torch.cuda.synchronize()
+        if time.time() - t_w > 1.0:
+            break
+    step_ms, kern_ms, prep_ms = [], [], []
+    launches = 0
+    stats = None
+    for s in range(args.steps):
+        flush.fill_(s & 0xff)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = idx.search(q, k, args.recall, stats=(s == args.steps - 1), **sopts)
+        e1.record(stream)
+        barrier()
+        step_ms.append(e0.elapsed_time(e1))
+        pm, km, _, nl = idx.index.last_timing()
+        prep_ms.append(pm)
+        kern_ms.append(km)
+        launches += nl + (1 if world > 1 else 0)
+        if s == args.steps - 1:
+            ids, sims, stats = res[0], res[1], res[2]
+    clocks = sampler.stop() if sampler else None
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    rec = recall_of(ids, t_kth, xn if world == 1 else None, qn, k) if world == 1 else None
+    if world > 1:
+        # recall against the merged global truth: check returned ids' exact sims on their owning rank
+        owned = (ids >= lo) & (ids < hi)
+        loc = (ids - lo).clamp(0, hi - lo - 1)
+        s_exact = torch.einsum("qd,qkd->qk", qn, xn[loc]) * owned
+        dist.all_reduce(s_exact)
+        hit = (s_exact >= t_kth[:, None] - 1e-5) & (ids >= 0)
+        rec = float(hit.float().sum() / (k * nq))
+
+    # e2e: same call with pinned host buffers (H2D of queries, D2H of ids + sims inside the region)
+    e2e = None
+    if not args.no_e2e:
+        qh = q.cpu().pin_memory()
+        ih = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+        sh = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+        e2e_ms = []
+        for s in range(args.warmup + args.steps):
+            flush.fill_(s & 0xff)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            idx.index.search(qh.numpy(), k, args.recall, out=(ih.numpy(), sh.numpy()), stream=stream, **sopts)
+            e1.record(stream)
+            barrier()
+            if s >= args.warmup:
+                e2e_ms.append(e0.elapsed_time(e1))
+        et = sum(e2e_ms)
+        if world > 1:
+            t = torch.tensor([et], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        e2e = {"value": args.steps * nq / (et / 1e3), "unit": "queries/s", "h2d_bytes_per_step": nq * d * 4,
+               "d2h_bytes_per_step": nq * k * 12}
+
+    if rank == 0:
+        pk = peaks()
+        ab = alg_bytes(stats, d, info["sketch_words"], k)
+        kern_s = statistics.mean(kern_ms) / 1e3
+        achieved = ab / kern_s / 1e9
+        cpu = None
+        if not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline_leg(args.config, args.recall, args.rep_chunk, args.cpu_sample)
+            except Exception as e:  # pragma: no cover
+                cpu = {"value": None, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+        line = {
+            "metric": METRIC,
+            "value": args.steps * nq / (tot_ms / 1e3),
+            "unit": "queries/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"config{args.config}: {c['name']} (Gaussian-mixture stand-in for GloVe-1M)",
+                       "n": n, "d": d, "nq": nq, "k": k, "recall_target": args.recall, "family": c["family"],
+                       "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": info["reps"],
+                       "rep_chunk": args.rep_chunk, "l2": "flushed (512 MiB write) between timed steps",
+                       "parallelism": f"data-sharded x{world}" if world > 1 else "single GPU"},
+            "recall": rec,
+            "build_s": build_s,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "kernel": "k_query", "kernel_ms": statistics.mean(kern_ms),
+                         "prep_ms": statistics.mean(prep_ms), "alg_bytes_per_query": ab / nq,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
+            "counters": {"emitted_per_q": float(np.mean(stats["emitted"])),
+                         "evaluated_per_q": float(np.mean(stats["evaluated"])),
+                         "filtered_per_q": float(np.mean(stats["filtered"])),
+                         "dups_per_q": float(np.mean(stats["dups"])),
+                         "i_stop_mean": float(np.mean(stats["i_stop"])),
+                         "j_stop_mean": float(np.mean(stats["j_stop"]))},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

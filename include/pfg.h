@@ -87,7 +87,8 @@ typedef struct {
     float filter_eps;         /* [0] tau = (1+eps) x expected Hamming distance */
     int32_t trace_cap;        /* [0] >0: write the ids evaluated by each query, in evaluation order,
                                  to trace_ids[nq][trace_cap] (uint32, local row ids) */
-    int32_t reserved0;
+    int32_t timing;           /* [0] 1: record CUDA events around the phases of this call on `stream`
+                                 (read back with pfg_last_timing) */
     uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
 } pfg_search_opts;
 
@@ -176,6 +177,11 @@ pfg_status pfg_hash_queries(pfg_index* idx, const float* queries, int64_t nq, ui
  * tau_host [65] fp32: tau(ip) = min{t : ip >= tau_host[t]}.  Either may be NULL. */
 pfg_status pfg_stop_tables(pfg_index* idx, float recall_target, const pfg_search_opts* opts,
                            float* thr_host, float* tau_host);
+
+/* phase timings of the last pfg_search on this index that set opts->timing (CUDA events on the
+ * call's stream): ms[0] = query preparation (host->device copy, normalisation, hashing, sketches),
+ * ms[1] = the query kernel, ms[2] = whole call; *launches = kernels the call launched. */
+pfg_status pfg_last_timing(const pfg_index* idx, float* ms3, int32_t* launches);
 
 void pfg_free(pfg_index* idx);
 const char* pfg_last_error(void);

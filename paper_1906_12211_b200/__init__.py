@@ -28,7 +28,8 @@ STATUS = {0: "PFG_OK", 1: "PFG_E_ARG", 2: "PFG_E_ZERO_VECTOR", 3: "PFG_E_BUDGET"
 
 # symbols include/pfg.h declares (checked by tests/test_abi.py)
 EXPORTED = ["pfg_build", "pfg_search", "pfg_merge_topk", "pfg_index_info", "pfg_derive_reps", "pfg_export",
-            "pfg_hash_queries", "pfg_stop_tables", "pfg_free", "pfg_last_error", "pfg_abi_version"]
+            "pfg_hash_queries", "pfg_stop_tables", "pfg_last_timing", "pfg_free", "pfg_last_error",
+            "pfg_abi_version"]
 
 
 class PfgError(RuntimeError):
@@ -47,7 +48,7 @@ class BuildOpts(C.Structure):
 class SearchOpts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("rep_chunk", C.c_int32), ("segment", C.c_int32),
                 ("stop_rule", C.c_int32), ("stop_granularity", C.c_int32), ("use_filter", C.c_int32),
-                ("filter_eps", C.c_float), ("trace_cap", C.c_int32), ("reserved0", C.c_int32),
+                ("filter_eps", C.c_float), ("trace_cap", C.c_int32), ("timing", C.c_int32),
                 ("trace_ids", C.c_void_p)]
 
 
@@ -91,6 +92,8 @@ def lib() -> C.CDLL:
         L.pfg_hash_queries.argtypes = [P, P, C.c_int64, P, P, P]
         L.pfg_stop_tables.restype = S
         L.pfg_stop_tables.argtypes = [P, C.c_float, P, P, P]
+        L.pfg_last_timing.restype = S
+        L.pfg_last_timing.argtypes = [P, P, P]
         L.pfg_free.restype = None
         L.pfg_free.argtypes = [P]
         L.pfg_last_error.restype = C.c_char_p
@@ -201,7 +204,7 @@ class Index:
 
     @staticmethod
     def _sopts(rep_chunk=8, segment=12, stop_rule=0, per_round=False, use_filter=True, eps=0.0,
-               trace_cap=0, trace_ptr=None) -> SearchOpts:
+               trace_cap=0, trace_ptr=None, timing=False) -> SearchOpts:
         o = SearchOpts()
         o.struct_size = C.sizeof(SearchOpts)
         o.rep_chunk, o.segment, o.stop_rule = rep_chunk, segment, stop_rule
@@ -210,7 +213,15 @@ class Index:
         o.filter_eps = eps
         o.trace_cap = trace_cap
         o.trace_ids = trace_ptr
+        o.timing = int(timing)
         return o
+
+    def last_timing(self):
+        """(prep ms, query-kernel ms, whole-call ms, kernels launched) of the last timed search"""
+        ms = (C.c_float * 3)()
+        n = C.c_int32(0)
+        _check(lib().pfg_last_timing(self._h, ms, C.byref(n)))
+        return float(ms[0]), float(ms[1]), float(ms[2]), int(n.value)
 
     def search(self, queries, k: int, recall: float, stats: bool = False, trace_cap: int = 0, out=None,
                stream=None, **sopts):

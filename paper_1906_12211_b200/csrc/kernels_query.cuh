@@ -22,7 +22,8 @@
 
 namespace pfg {
 
-constexpr int kSB = 128;      // survivor buffer per warp
+constexpr int kCB = 256;      // candidate buffer per warp (filter-passing, not yet evaluated)
+constexpr int kU = 4;         // table positions per lane per scan step (memory-level parallelism)
 constexpr int kMaxR = 32;     // max repetitions per chunk
 constexpr int kMaxK = 256;    // max k
 
@@ -58,19 +59,19 @@ struct WarpSmem {
     uint64_t* qsk;     // [M]
     uint64_t* T0;      // [kt]
     uint64_t* T1;      // [kt]
-    uint64_t* cand;    // [32]
-    uint32_t* sid;     // [kSB]
-    float* ssim;       // [kSB]
-    uint8_t* srep;     // [kSB]
+    uint64_t* cand;    // [32]   sorted merge batch
+    uint64_t* cb;      // [kCB]  candidate keys (id << 8 | rep)
+    uint32_t* sid;     // [kCB]  evaluated ids, bucketed by rep
+    float* ssim;       // [kCB]
     uint32_t* beg;     // [kMaxR + 1]
     uint32_t* lo_new;  // [kMaxR]
     uint32_t* lo_old;
     uint32_t* hi_old;
-    uint32_t* hi_new;
     uint32_t* qc;      // [kMaxR] lazily computed codes
     uint32_t* bnd;     // [2 * kMaxR] a / b bounds
     uint32_t* fcnt;    // [kMaxR] filtered per rep
     uint32_t* dcnt;    // [kMaxR] dups per rep
+    uint32_t* rcnt;    // [kMaxR + 1] survivors per rep (then bucket offsets)
 };
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
@@ -81,8 +82,8 @@ __host__ __device__ inline int warp_smem_bytes(int dpad, int M, int kt) {
     b += align16(M * 8);
     b += 2 * align16(kt * 8);
     b += 32 * 8;
-    b += kSB * 4 + kSB * 4 + align16(kSB);
-    b += align16((kMaxR + 1) * 4) + 4 * kMaxR * 4 + kMaxR * 4 + 2 * kMaxR * 4 + 2 * kMaxR * 4;
+    b += kCB * 8 + kCB * 4 + kCB * 4;
+    b += align16((kMaxR + 1) * 4) + 3 * kMaxR * 4 + kMaxR * 4 + 2 * kMaxR * 4 + 2 * kMaxR * 4 + align16((kMaxR + 1) * 4);
     return align16(b);
 }
 
@@ -94,18 +95,18 @@ __device__ inline WarpSmem carve(unsigned char* base, const QueryParams& p) {
     w.T0 = (uint64_t*)q; q += align16(p.kt * 8);
     w.T1 = (uint64_t*)q; q += align16(p.kt * 8);
     w.cand = (uint64_t*)q; q += 32 * 8;
-    w.sid = (uint32_t*)q; q += kSB * 4;
-    w.ssim = (float*)q; q += kSB * 4;
-    w.srep = (uint8_t*)q; q += align16(kSB);
+    w.cb = (uint64_t*)q; q += kCB * 8;
+    w.sid = (uint32_t*)q; q += kCB * 4;
+    w.ssim = (float*)q; q += kCB * 4;
     w.beg = (uint32_t*)q; q += align16((kMaxR + 1) * 4);
     w.lo_new = (uint32_t*)q; q += kMaxR * 4;
     w.lo_old = (uint32_t*)q; q += kMaxR * 4;
     w.hi_old = (uint32_t*)q; q += kMaxR * 4;
-    w.hi_new = (uint32_t*)q; q += kMaxR * 4;
     w.qc = (uint32_t*)q; q += kMaxR * 4;
     w.bnd = (uint32_t*)q; q += 2 * kMaxR * 4;
     w.fcnt = (uint32_t*)q; q += kMaxR * 4;
     w.dcnt = (uint32_t*)q; q += kMaxR * 4;
+    w.rcnt = (uint32_t*)q; q += align16((kMaxR + 1) * 4);
     return w;
 }
 
@@ -128,20 +129,32 @@ __device__ __forceinline__ uint32_t rep_lower_bound(const QueryParams& p, int j,
     return lo;
 }
 
+// 256-bit read-only load of 8 consecutive floats (one full 32-byte sector per lane)
+__device__ __forceinline__ void ldg256(const float* p, float (&v)[8]) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p));
+}
+
 // canonical inner product (R-2): sequential fmaf over t from +0; the zero padding of both rows
-// beyond d leaves the chain unchanged (see k_hp_bits)
+// beyond d leaves the chain unchanged (see k_hp_bits).  dpad is a multiple of 8.
 __device__ __forceinline__ float dot_row(const float* __restrict__ q, const float* __restrict__ xr, int dpad) {
     float s = 0.0f;
-    const float4* x4 = reinterpret_cast<const float4*>(xr);
-    const float4* q4 = reinterpret_cast<const float4*>(q);
-#pragma unroll 5
-    for (int t = 0; t < (dpad >> 2); ++t) {
-        const float4 v = __ldg(x4 + t);
-        const float4 w = q4[t];
-        s = fmaf(w.x, v.x, s);
-        s = fmaf(w.y, v.y, s);
-        s = fmaf(w.z, v.z, s);
-        s = fmaf(w.w, v.w, s);
+    const int nc = dpad >> 3;
+#pragma unroll 4
+    for (int c = 0; c < nc; ++c) {
+        float v[8];
+        ldg256(xr + 8 * c, v);
+        const float4 w0 = reinterpret_cast<const float4*>(q)[2 * c];
+        const float4 w1 = reinterpret_cast<const float4*>(q)[2 * c + 1];
+        s = fmaf(w0.x, v[0], s);
+        s = fmaf(w0.y, v[1], s);
+        s = fmaf(w0.z, v[2], s);
+        s = fmaf(w0.w, v[3], s);
+        s = fmaf(w1.x, v[4], s);
+        s = fmaf(w1.y, v[5], s);
+        s = fmaf(w1.z, v[6], s);
+        s = fmaf(w1.w, v[7], s);
     }
     return s;
 }
@@ -155,7 +168,7 @@ struct QState {
     uint64_t* Tn;         // scratch buffer
 };
 
-// merge survivors [e, e2) of the buffer (sims computed) into the sorted top list
+// merge survivors [e, e2) of sid/ssim into the sorted top list
 __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem& w, QState& st, int e, int e2,
                                             int64_t qi, int lane) {
     for (int b0 = e; b0 < e2; b0 += 32) {
@@ -206,11 +219,116 @@ __device__ __forceinline__ float kth_sim_clamped(const QueryParams& p, const QSt
     return fminf(fmaxf(ip, -1.0f), 1.0f);
 }
 
-// compute sims for buffer entries [nsim, nbuf)
-__device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int nsim, int nbuf, int lane) {
-    for (int e = nsim + lane; e < nbuf; e += 32)
+// compute sims for survivors [0, ns)
+__device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int ns, int lane) {
+    for (int e = lane; e < ns; e += 32)
         w.ssim[e] = dot_row(w.qrow, p.x + (int64_t)w.sid[e] * p.dpad, p.dpad);
     __syncwarp();
+}
+
+// warp-cooperative ascending bitonic sort of cb[0..P) in shared memory (P power of two)
+__device__ __forceinline__ void warp_sort_smem(uint64_t* s, int P, int lane) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t a = s[i], b = s[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) { s[i] = b; s[ixj] = a; }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Flush the candidate buffer (R-17): candidates are filter-passing positions whose id was
+// not evaluated when scanned.  Sort by (id, rep); the first occurrence of an id (its smallest
+// repetition) is evaluated, later ones count as duplicates -- the same evaluated set and repetition
+// attribution as the sequential algorithm.  Survivors are bucketed by repetition, claimed in the
+// bitmap, their inner products computed, and merged repetition by repetition; every repetition
+// < `complete` (all positions scanned) gets its stop check after its survivors are merged.
+// Returns true when the query stops (r_stop set).
+__device__ __forceinline__ bool flush_chunk(const QueryParams& p, const WarpSmem& w, QState& st, int& ncand,
+                                            int& next_check, int complete, int nr, int c0, int i, int64_t qi,
+                                            uint32_t* bm, uint32_t* claims, int& r_stop, int lane) {
+    int ns = 0;
+    if (ncand > 0) {
+        int P = 32;
+        while (P < ncand) P <<= 1;
+        for (int e = ncand + lane; e < P; e += 32) w.cb[e] = ~0ull;
+        __syncwarp();
+        warp_sort_smem(w.cb, P, lane);
+        for (int r = lane; r <= nr; r += 32) w.rcnt[r] = 0;
+        __syncwarp();
+        // dedupe + per-rep counts
+        for (int e = lane; e < ncand; e += 32) {
+            const uint64_t key = w.cb[e];
+            const bool keep = (e == 0) || ((w.cb[e - 1] >> 8) != (key >> 8));
+            const int r = (int)(key & 0xff);
+            if (keep) atomicAdd(&w.rcnt[r], 1u); else atomicAdd(&w.dcnt[r], 1u);
+        }
+        __syncwarp();
+        // exclusive prefix over reps (nr <= 32) -> bucket offsets in rcnt
+        {
+            const uint32_t v = lane < nr ? w.rcnt[lane] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off) incl += o;
+            }
+            const uint32_t tot = __shfl_sync(kFull, incl, nr - 1);
+            __syncwarp();
+            if (lane < nr) w.rcnt[lane] = incl - v;
+            if (lane == 0) w.rcnt[nr] = tot;
+            __syncwarp();
+        }
+        ns = (int)w.rcnt[nr];
+        // scatter survivors to rep buckets, claim them in the bitmap
+        for (int e = lane; e < ncand; e += 32) {
+            const uint64_t key = w.cb[e];
+            const bool keep = (e == 0) || ((w.cb[e - 1] >> 8) != (key >> 8));
+            if (keep) {
+                const uint32_t id = (uint32_t)(key >> 8);
+                const int r = (int)(key & 0xff);
+                const uint32_t dst = atomicAdd(&w.rcnt[r], 1u);
+                w.sid[dst] = id;
+                atomicOr(bm + (id >> 5), 1u << (id & 31));
+            }
+        }
+        __syncwarp();
+        // rcnt[r] is now the end of bucket r; record claims for the bitmap reset
+        for (int e = lane; e < ns; e += 32) {
+            const uint32_t cn = st.claims_n + e;
+            if (cn < (uint32_t)p.claim_cap) claims[cn] = w.sid[e];
+        }
+        st.claims_n += ns;
+        compute_sims(p, w, ns, lane);
+    }
+    ncand = 0;
+    // merge bucket by bucket in repetition order, stop check after every complete repetition
+    for (;;) {
+        if (next_check >= nr) break;
+        if (ns > 0) {
+            const int b0 = next_check == 0 ? 0 : (int)w.rcnt[next_check - 1];
+            const int b1 = (int)w.rcnt[next_check];
+            if (b1 > b0) merge_range(p, w, st, b0, b1, qi, lane);
+        }
+        if (next_check >= complete) break;
+        const int j1 = c0 + next_check + 1;
+        if (st.tn == p.k_eff && (!p.per_round || j1 == p.L)) {
+            const float ip = kth_sim_clamped(p, st);
+            if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + (j1 - 1))) {
+                r_stop = next_check;
+                return true;
+            }
+        }
+        ++next_check;
+    }
+    __syncwarp();
+    return false;
 }
 
 template <int EPL>
@@ -291,7 +409,7 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                     uint32_t nelo = elo, nehi = ehi;
                     if (a < elo) { const uint32_t s = (elo - a + B - 1) / B; nelo = (s * B >= elo) ? 0u : elo - s * B; }
                     if (b > ehi) { const uint64_t s = (b - ehi + B - 1) / B; const uint64_t v = ehi + s * B; nehi = (uint32_t)(v > (uint64_t)p.n ? p.n : v); }
-                    w.lo_new[lane] = nelo; w.lo_old[lane] = elo; w.hi_old[lane] = ehi; w.hi_new[lane] = nehi;
+                    w.lo_new[lane] = nelo; w.lo_old[lane] = elo; w.hi_old[lane] = ehi;
                     w.fcnt[lane] = 0; w.dcnt[lane] = 0;
                     em = (elo - nelo) + (nehi - ehi);
                     cur[j] = make_uint4(w.qc[lane], nelo, nehi, 0u);
@@ -308,85 +426,72 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                 __syncwarp();
                 const uint32_t total = w.beg[nr];
 
-                int nbuf = 0, nsim = 0, next_check = 0, r_stop = -1;
-                uint32_t g0 = 0;
-                // scan the chunk's emitted positions in (rep, position) order; drain the survivor
-                // buffer when it may overflow and at the end of the chunk
-                for (;;) {
-                    const bool last = g0 + 32 >= total;
+                int ncand = 0, next_check = 0, r_stop = -1;
+                // scan the chunk's emitted positions in (rep, position) order, kU per lane per step
+                for (uint32_t g0 = 0;; g0 += 32 * kU) {
+                    const bool last = g0 + 32 * kU >= total;
                     if (g0 < total) {
-                        const uint32_t g = g0 + lane;
-                        const bool act = g < total;
-                        int r = 0;
-                        uint32_t id = 0;
-                        bool pass = false;
-                        if (act) {
-                            while (r + 1 < nr && w.beg[r + 1] <= g) ++r;
-                            const uint32_t o = g - w.beg[r];
-                            const uint32_t lenA = w.lo_old[r] - w.lo_new[r];
-                            const uint32_t pos = (o < lenA) ? w.lo_new[r] + o : w.hi_old[r] + (o - lenA);
-                            const int j = c0 + r;
-                            id = (uint32_t)__ldg(p.tab + (int64_t)j * p.n + pos);
-                            pass = true;
-                            if (p.use_filter) {
-                                const int s = __ldg(p.slot + j);
-                                const uint64_t sw = __ldg(p.sk + (int64_t)id * p.M + s);
-                                pass = __popcll(sw ^ w.qsk[s]) <= tau;
-                                if (!pass) atomicAdd(&w.fcnt[r], 1u);
+                        uint32_t idv[kU];
+                        int rv[kU];
+                        bool act[kU], pass[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const uint32_t g = g0 + u * 32 + lane;
+                            act[u] = g < total;
+                            rv[u] = 0;
+                            idv[u] = 0;
+                            if (act[u]) {
+                                int r = 0;
+                                while (r + 1 < nr && w.beg[r + 1] <= g) ++r;
+                                const uint32_t o = g - w.beg[r];
+                                const uint32_t lenA = w.lo_old[r] - w.lo_new[r];
+                                const uint32_t pos = (o < lenA) ? w.lo_new[r] + o : w.hi_old[r] + (o - lenA);
+                                idv[u] = (uint32_t)__ldg(p.tab + (int64_t)(c0 + r) * p.n + pos);
+                                rv[u] = r;
                             }
                         }
-                        const uint32_t pm = __ballot_sync(kFull, act && pass);
-                        bool fresh = false;
-                        if (act && pass) {
-                            const uint32_t grp = __match_any_sync(pm, id);
-                            if ((int)(__ffs(grp) - 1) == lane) {
-                                const uint32_t bit = 1u << (id & 31);
-                                const uint32_t old = atomicOr(bm + (id >> 5), bit);
-                                fresh = !(old & bit);
-                            }
-                            if (!fresh) atomicAdd(&w.dcnt[r], 1u);
-                        }
-                        const uint32_t fm = __ballot_sync(kFull, fresh);
-                        if (fresh) {
-                            const int rank = __popc(fm & lanemask_lt());
-                            w.sid[nbuf + rank] = id;
-                            w.srep[nbuf + rank] = (uint8_t)r;
-                            const uint32_t cn = st.claims_n + rank;
-                            if (cn < (uint32_t)p.claim_cap) claims[cn] = id;
-                        }
-                        nbuf += __popc(fm);
-                        st.claims_n += __popc(fm);
-                        __syncwarp();
-                    }
-                    if (last || nbuf > kSB - 32) {
-                        // reps whose positions are all scanned
-                        int complete = nr;
-                        if (!last) { complete = 0; while (complete < nr && w.beg[complete + 1] <= g0 + 32) ++complete; }
-                        compute_sims(p, w, nsim, nbuf, lane);
-                        nsim = nbuf;
-                        int e = 0;
-                        for (;;) {
-                            int e2 = e;
-                            while (e2 < nbuf && w.srep[e2] == next_check) ++e2;
-                            if (e2 > e) merge_range(p, w, st, e, e2, qi, lane);
-                            e = e2;
-                            if (next_check >= complete) break;
-                            const int j1 = c0 + next_check + 1;
-                            if (st.tn == p.k_eff && (!p.per_round || j1 == p.L)) {
-                                const float ip = kth_sim_clamped(p, st);
-                                if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + (j1 - 1))) {
-                                    stopped = true; r_stop = next_check; i_stop = i; j_stop = j1;
-                                    break;
+                        if (p.use_filter) {
+                            uint64_t sw[kU];
+#pragma unroll
+                            for (int u = 0; u < kU; ++u)
+                                sw[u] = act[u] ? __ldg(p.sk + (int64_t)idv[u] * p.M + __ldg(p.slot + c0 + rv[u])) : 0ull;
+#pragma unroll
+                            for (int u = 0; u < kU; ++u) {
+                                pass[u] = false;
+                                if (act[u]) {
+                                    const int s = __ldg(p.slot + c0 + rv[u]);
+                                    pass[u] = __popcll(sw[u] ^ w.qsk[s]) <= tau;
+                                    if (!pass[u]) atomicAdd(&w.fcnt[rv[u]], 1u);
                                 }
                             }
-                            ++next_check;
-                            if (next_check >= nr) break;
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < kU; ++u) pass[u] = act[u];
                         }
-                        nbuf = nsim = 0;
-                        if (stopped) break;
+                        uint32_t bw[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) bw[u] = pass[u] ? __ldcg(bm + (idv[u] >> 5)) : 0u;
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            bool fresh = false;
+                            if (pass[u]) {
+                                fresh = !((bw[u] >> (idv[u] & 31)) & 1u);
+                                if (!fresh) atomicAdd(&w.dcnt[rv[u]], 1u);
+                            }
+                            const uint32_t fm = __ballot_sync(kFull, fresh);
+                            if (fresh) w.cb[ncand + __popc(fm & lanemask_lt())] = ((uint64_t)idv[u] << 8) | (uint64_t)rv[u];
+                            ncand += __popc(fm);
+                        }
+                        __syncwarp();
                     }
-                    if (last) break;
-                    g0 += 32;
+                    if (last || ncand > kCB - 32 * kU) {
+                        int complete = nr;
+                        if (!last) { complete = 0; while (complete < nr && w.beg[complete + 1] <= g0 + 32 * kU) ++complete; }
+                        if (flush_chunk(p, w, st, ncand, next_check, complete, nr, c0, i, qi, bm, claims, r_stop, lane)) {
+                            stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
+                        }
+                    }
+                    if (stopped || last) break;
                 }
                 // account the chunk's repetitions up to the stop (all of them if no stop)
                 const int rmax = stopped ? r_stop : nr - 1;
@@ -405,23 +510,19 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
             // i = 0: linear scan of every point not yet evaluated (R-13), filter off, then stop;
             // every point evaluated before the scan is retrieved again as a duplicate
             st.dups += st.nE;
-            int nbuf = 0;
+            int ns = 0;
             for (int64_t g0 = 0; g0 < p.n; g0 += 32) {
                 const int64_t id = g0 + lane;
                 bool fresh = false;
                 if (id < p.n) fresh = !((__ldcg(bm + (id >> 5)) >> (id & 31)) & 1u);
                 const uint32_t fm = __ballot_sync(kFull, fresh);
-                if (fresh) {
-                    const int rank = __popc(fm & lanemask_lt());
-                    w.sid[nbuf + rank] = (uint32_t)id;
-                    w.srep[nbuf + rank] = 0;
-                }
-                nbuf += __popc(fm);
+                if (fresh) w.sid[ns + __popc(fm & lanemask_lt())] = (uint32_t)id;
+                ns += __popc(fm);
                 __syncwarp();
-                if (nbuf > kSB - 32 || g0 + 32 >= p.n) {
-                    compute_sims(p, w, 0, nbuf, lane);
-                    if (nbuf) merge_range(p, w, st, 0, nbuf, qi, lane);
-                    nbuf = 0;
+                if (ns > kCB - 32 || g0 + 32 >= p.n) {
+                    compute_sims(p, w, ns, lane);
+                    if (ns) merge_range(p, w, st, 0, ns, qi, lane);
+                    ns = 0;
                 }
             }
             st.emitted += (uint32_t)p.n;
@@ -448,10 +549,10 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
             p.stats[qi] = s;
         }
         // return the bitmap to zero for the next query of this slot
-        const uint32_t* cl = claims;
         const uint32_t ncl = st.claims_n;
+        __syncwarp();
         if (ncl <= (uint32_t)p.claim_cap) {
-            for (uint32_t e = lane; e < ncl; e += 32) __stcg(bm + (cl[e] >> 5), 0u);
+            for (uint32_t e = lane; e < ncl; e += 32) __stcg(bm + (claims[e] >> 5), 0u);
         } else {
             for (int64_t e = lane; e < p.bm_words; e += 32) __stcg(bm + e, 0u);
         }

@@ -126,7 +126,7 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     if (family != PFG_SIMHASH && family != PFG_CROSSPOLYTOPE_FHT) return fail(PFG_E_ARG, "unknown family");
     g.n = n;
     g.d = d;
-    g.dpad = (d + 3) & ~3;
+    g.dpad = (d + 7) & ~7;  // rows 32-byte aligned for 256-bit loads
     g.family = family;
     g.strategy = z.strategy;
     if (g.strategy != PFG_INDEPENDENT && g.strategy != PFG_POOL) return fail(PFG_E_ARG, "unknown strategy");
@@ -257,7 +257,7 @@ int tau_of(float ipk, float eps) {
 }
 
 struct SearchCfg {
-    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0;
+    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0;
     float eps = 0.0f;
     uint32_t* trace_ids = nullptr;
 };
@@ -283,6 +283,7 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     if (!(s.eps > -1.0f) || !std::isfinite(s.eps)) return fail(PFG_E_ARG, "filter_eps must be finite and > -1");
     s.trace_cap = z.trace_cap;
     s.trace_ids = z.trace_ids;
+    s.timing = z.timing;
     if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
     return PFG_OK;
 }
@@ -311,6 +312,15 @@ struct pfg_index {
     int64_t slots = 0;
     int slots_L = 0;
     int64_t slots_bm = 0;
+    // launch accounting and phase timing of the last search
+    int launches = 0;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    float last_ms[3] = {0, 0, 0};
+    int last_launches = 0;
+    ~pfg_index() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
 };
 
 namespace pfg {
@@ -530,25 +540,31 @@ pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, u
             hp_bits(X, np, g.dpad, I->hpfn.as<float>() + (size_t)r0 * g.K * g.dpad, nf, g.dpad, g.dpad,
                     bits.as<uint8_t>(), (int64_t)wpr * 8, st);
             k_codes_from_bits<<<grd, blk, 0, st>>>(bits.as<uint64_t>(), np, wpr, r0, nb, g.K, nullptr, r0, keys, codes, ldc);
+            I->launches += 2;
         } else {
             const int wpr = (g.m + 63) / 64;
             if (!pool_ready) {
                 PFG_TRY(poolvals.ensure((size_t)np * wpr * 8, "pool bits"));
                 hp_bits(X, np, g.dpad, I->hpfn.as<float>(), g.m, g.dpad, g.dpad, poolvals.as<uint8_t>(), (int64_t)wpr * 8, st);
                 pool_ready = true;
+                I->launches += 1;
             }
+            I->launches += 1;
             k_codes_from_bits<<<grd, blk, 0, st>>>(poolvals.as<uint64_t>(), np, wpr, r0, nb, g.K, I->sel.as<int32_t>(), 0,
                                                    keys, codes, ldc);
         }
     } else {
         if (g.strategy == PFG_INDEPENDENT) {
             fht_rep(X, np, g.dpad, g, I->sg.as<uint32_t>(), r0, nb, keys, codes, ldc, I->num_sms, st);
+            I->launches += 1;
         } else {
             if (!pool_ready) {
                 PFG_TRY(poolvals.ensure((size_t)np * g.m * 2, "pool codes"));
                 fht_funcs(X, np, g.dpad, g, I->sg.as<uint32_t>(), poolvals.as<uint16_t>(), I->num_sms, st);
                 pool_ready = true;
+                I->launches += 1;
             }
+            I->launches += 1;
             k_pool_codes<<<grd, blk, 0, st>>>(poolvals.as<uint16_t>(), np, g.m, r0, nb, g.c, g.ell, g.K,
                                               I->sel.as<int32_t>(), keys, codes, ldc);
         }
@@ -645,11 +661,13 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     PFG_TRY(I->zmin.ensure(8, "zmin"));
     PFG_TRY(normalize_rows(qsrc, nq, g.d, I->qx.as<float>(), g.dpad, I->qzero.as<uint8_t>(),
                            I->zmin.as<unsigned long long>(), zrow, st));
+    I->launches += 1;
     if (g.M > 0) {
         PFG_TRY(I->qsk.ensure((size_t)nq * g.M * 8, "query sketches"));
         hp_bits(I->qx.as<float>(), nq, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->qsk.as<uint8_t>(),
                 (int64_t)g.M * 8, st);
         PFG_CUDA(cudaGetLastError());
+        I->launches += 1;
     }
     *lazy = (g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT && !force_codes);
     if (need_codes && !*lazy) {
@@ -792,6 +810,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     std::shared_ptr<DBuf> thr, taub;
     PFG_TRY(get_thr(I, recall, s, thr, nullptr));
     PFG_TRY(get_tau(I, s.eps, taub, nullptr));
+    if (s.timing) {
+        for (auto& e : I->ev)
+            if (!e) PFG_CUDA(cudaEventCreate(&e));
+        PFG_CUDA(cudaEventRecord(I->ev[0], st));
+    }
+    I->launches = 0;
     int64_t zrow = -1;
     bool lazy = false;
     PFG_TRY(prep_queries(I, queries, nq, true, false, &zrow, &lazy, st));
@@ -849,6 +873,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.thr = thr->as<float>(); p.taub = taub->as<float>(); p.work = I->work.as<unsigned long long>();
     p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
     p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
+    if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[1], st));
     switch (epl) {
         case 1: PFG_TRY(launch_query_t<1>(p, (int)blocks, smem, st)); break;
         case 2: PFG_TRY(launch_query_t<2>(p, (int)blocks, smem, st)); break;
@@ -857,6 +882,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         case 16: PFG_TRY(launch_query_t<16>(p, (int)blocks, smem, st)); break;
         default: PFG_TRY(launch_query_t<32>(p, (int)blocks, smem, st)); break;
     }
+    I->launches += 1;
+    if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[2], st));
     if (!ids_dev) PFG_CUDA(cudaMemcpyAsync(out_ids, d_ids, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
     if (!sims_dev) PFG_CUDA(cudaMemcpyAsync(out_sims, d_sims, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));
     if (stats && !stats_dev)
@@ -864,7 +891,20 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     if (s.trace_cap > 0 && !trace_dev)
         PFG_CUDA(cudaMemcpyAsync(s.trace_ids, d_trace, (size_t)nq * s.trace_cap * 4, cudaMemcpyDeviceToHost, st));
     PFG_CUDA(cudaStreamSynchronize(st));
+    I->last_launches = I->launches;
+    if (s.timing) {
+        PFG_CUDA(cudaEventElapsedTime(&I->last_ms[0], I->ev[0], I->ev[1]));
+        PFG_CUDA(cudaEventElapsedTime(&I->last_ms[1], I->ev[1], I->ev[2]));
+        PFG_CUDA(cudaEventElapsedTime(&I->last_ms[2], I->ev[0], I->ev[2]));
+    }
     if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(zrow) + " is a zero vector");
+    return PFG_OK;
+}
+
+pfg_status pfg_last_timing(const pfg_index* I, float* ms3, int32_t* launches) {
+    if (!I) return fail(PFG_E_ARG, "NULL index");
+    if (ms3) for (int i = 0; i < 3; ++i) ms3[i] = I->last_ms[i];
+    if (launches) *launches = I->last_launches;
     return PFG_OK;
 }
 

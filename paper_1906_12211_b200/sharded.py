@@ -1,0 +1,45 @@
+"""Data-sharded multi-GPU mode: one process per GPU, each indexing a contiguous
+block of rows under the same seed (identical hash functions on every shard), every rank answering
+every query with shard-local adaptive stopping, then an NCCL all-gather of the local top-k lists
+and the library's merge kernel.  Why the guarantee carries over: a global top-k point of shard s
+is a local top-k point of s, returned with probability >= 1 - delta; after the merge every point
+ranked above it is a true point above it, so it stays in the global top-k.
+
+Plumbing only (torch.distributed for the collective); the search and the merge are library calls.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import Index, merge_topk
+
+
+def shard_range(n: int, world: int, rank: int):
+    """contiguous row block [lo, hi) of rank `rank` (the first n % world ranks get one extra row)"""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class ShardedIndex:
+    """Build this rank's shard: `local_data` are rows [row0, row0 + len) of the global dataset."""
+
+    def __init__(self, local_data, row0: int, memory_budget: int, family, seed: int = 1, group=None, **opts):
+        self.group = group
+        self.row0 = row0
+        self.index = Index(local_data, memory_budget, family, seed=seed, id_offset=row0, **opts)
+
+    def search(self, queries, k: int, recall: float, **sopts):
+        """-> merged (ids [nq,k], sims [nq,k]) on every rank (CUDA tensors)"""
+        res = self.index.search(queries, k, recall, **sopts)
+        ids, sims = res[0], res[1]
+        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        if world == 1:
+            return (ids, sims) + tuple(res[2:])
+        g_ids = torch.empty((world,) + tuple(ids.shape), dtype=ids.dtype, device=ids.device)
+        g_sims = torch.empty((world,) + tuple(sims.shape), dtype=sims.dtype, device=sims.device)
+        dist.all_gather_into_tensor(g_ids, ids, group=self.group)
+        dist.all_gather_into_tensor(g_sims, sims, group=self.group)
+        m_ids, m_sims = merge_topk(g_ids, g_sims)
+        return (m_ids, m_sims) + tuple(res[2:])
