@@ -47,6 +47,7 @@ def lib():
         L.or_gauss_d.restype = C.c_double; L.or_gauss_d.argtypes = [C.c_uint64, C.c_uint64]
         L.or_normalize.restype = C.c_int64; L.or_normalize.argtypes = [P, C.c_int64, C.c_int, P]
         L.or_dot.restype = C.c_float; L.or_dot.argtypes = [P, P, C.c_int]
+        L.or_sim.restype = C.c_float; L.or_sim.argtypes = [P, P, C.c_int]
         L.or_hp_bit.restype = C.c_int; L.or_hp_bit.argtypes = [P, P, C.c_int]
         L.or_fht.restype = None; L.or_fht.argtypes = [P, C.c_int]
         L.or_fhtcp_code.restype = C.c_uint32; L.or_fhtcp_code.argtypes = [P, C.c_int, C.c_int, P]
@@ -118,6 +119,12 @@ def normalize(x) -> np.ndarray:
 def dot(a, b) -> float:
     a, b = _f32(a), _f32(b)
     return float(lib().or_dot(_p(a), _p(b), a.shape[0]))
+
+
+def sim(a, b) -> float:
+    """canonical similarity (32-lane tree order, R-2)"""
+    a, b = _f32(a), _f32(b)
+    return float(lib().or_sim(_p(a), _p(b), a.shape[0]))
 
 
 def hp_bit(a, x) -> int:

@@ -73,12 +73,26 @@ int64_t or_normalize(const float* x, int64_t n, int d, float* out) {
     return -1;
 }
 
-/* R-2 canonical inner product: sequential fp32 fmaf over t = 0..d-1 from +0
- * ("distance computation"; on unit vectors ip = cos) */
+/* R-2 canonical projection (hash and sketch functions): sequential fp32 fmaf over t = 0..d-1
+ * from +0 (on unit vectors the inner product is the cosine) */
 float or_dot(const float* a, const float* b, int d) {
     float s = 0.0f;
     for (int t = 0; t < d; ++t) s = fmaf(a[t], b[t], s);
     return s;
+}
+
+/* R-2 canonical similarity of two unit vectors ("distance computation"):
+ * the d products are accumulated in 32 lane sums -- element t goes to lane (t/4) mod 32 and
+ * each lane sum is a sequential fp32 fmaf chain in ascending t from +0 -- which are then added
+ * pairwise in a fixed tree: for h = 16, 8, 4, 2, 1: s[l] = s[l] + s[l+h] (l < h).  This is the
+ * order in which a warp reading a row with one 16-byte chunk per lane computes it. */
+float or_sim(const float* a, const float* b, int d) {
+    float s[32];
+    for (int l = 0; l < 32; ++l) s[l] = 0.0f;
+    for (int t = 0; t < d; ++t) s[(t / 4) % 32] = fmaf(a[t], b[t], s[(t / 4) % 32]);
+    for (int h = 16; h >= 1; h /= 2)
+        for (int l = 0; l < h; ++l) s[l] = s[l] + s[l + h];
+    return s[0];
 }
 
 /* PAPER.md:142-146 §2: HP (SimHash) bit = 1 iff <a,x> >= 0, a ~ N(0,I).
@@ -535,7 +549,7 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
                         E[id] = 1;
                         if (tids && nE < tcap) tids[nE] = id;
                         nE++;
-                        float sim = or_dot(q, X->x + (int64_t)id * d, d);
+                        float sim = or_sim(q, X->x + (int64_t)id * d, d);
                         /* insert into the sorted top list (Alg. 1 lines 6-7) */
                         if (nt < k_eff || or_better(sim, id, ts[k_eff - 1], ti[k_eff - 1])) {
                             int pos = nt < k_eff ? nt : k_eff - 1;

@@ -48,7 +48,22 @@ def test_dot_close_to_double():
     for i in range(200):
         ref = float(np.dot(a[i].astype(np.float64), b[i].astype(np.float64)))
         assert abs(O.dot(a[i], b[i]) - ref) < 1e-6
+        assert abs(O.sim(a[i], b[i]) - ref) < 1e-6
     assert O.dot(np.array([1, 2, 3], np.float32), np.array([4, 5, 6], np.float32)) == 32.0
+
+
+def test_sim_exact_on_integers_and_long_vectors():
+    # integer-valued products are exact in fp32, so any summation order gives the exact sum;
+    # covers d > 128 (several chunks per lane) and d not a multiple of 4
+    rng = np.random.default_rng(8)
+    for d in (1, 3, 7, 100, 129, 300, 960, 1030):
+        a = rng.integers(-8, 9, size=d).astype(np.float32)
+        b = rng.integers(-8, 9, size=d).astype(np.float32)
+        assert O.sim(a, b) == float(np.dot(a.astype(np.int64), b.astype(np.int64)))
+    x = O.normalize(rng.standard_normal((50, 960)))
+    for i in range(49):
+        assert abs(O.sim(x[i], x[i + 1]) - float(x[i].astype(np.float64) @ x[i + 1].astype(np.float64))) < 2e-6
+    assert abs(O.sim(x[0], x[0]) - 1.0) < 1e-6
 
 
 # ---------------------------------------------------------------- HP
@@ -342,7 +357,7 @@ def test_trace_accounting_and_lemma1():
         ev = tids[r, : tr[r, 5]]
         assert len(set(ev.tolist())) == tr[r, 5]
         # the returned list is exactly the top-10 of the evaluated set (Alg. 1 PQ)
-        s = np.array([O.dot(O.normalize(q[r:r + 1])[0], X.data()[e]) for e in ev], np.float32)
+        s = np.array([O.sim(O.normalize(q[r:r + 1])[0], X.data()[e]) for e in ev], np.float32)
         order = np.lexsort((ev, -s))[:10]
         assert np.array_equal(ids[r], ev[order].astype(np.int64))
         # Lemma 1 invariant: the found k-th similarity never exceeds the true k-th
