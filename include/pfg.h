@@ -154,9 +154,10 @@ pfg_status pfg_derive_reps(int64_t n, int32_t d, int32_t family, uint64_t memory
 
 /* ---- test hooks (parity) ---------------------------------------------------------------- */
 typedef enum {
-    PFG_EXPORT_TABLE = 1,   /* arg = rep j: uint64 [n] = (code << 32) | local id, sorted ascending */
+    PFG_EXPORT_TABLE = 1,   /* arg = rep j: uint64 [n][2] = {(code << 32) | local id, sketch word of the
+                               repetition's slot for that id}, sorted ascending by the first word */
     PFG_EXPORT_PREFIX = 2,  /* arg = rep j: uint32 [8193] first position whose top 13 bits >= p */
-    PFG_EXPORT_SKETCH = 3,  /* uint64 [n][M] */
+    PFG_EXPORT_SKETCH = 3,  /* per-point sketches are not retained (PFG_E_STATE): they live inline */
     PFG_EXPORT_DATA = 4,    /* fp32 [n][d] normalised rows */
     PFG_EXPORT_CP = 5,      /* double [ell+1][41] cleaned CP collision table (FHT family) */
     PFG_EXPORT_SLOTS = 6,   /* int32 [L] sketch slot per repetition */

@@ -271,7 +271,8 @@ class Index:
         return a
 
     def export_table(self, j: int) -> np.ndarray:
-        return self._export(EXPORT_TABLE, j, (self.info["n"],), np.uint64)
+        """[n, 2] uint64: (code << 32 | id, inline sketch word of repetition j's slot)"""
+        return self._export(EXPORT_TABLE, j, (self.info["n"], 2), np.uint64)
 
     def export_prefix(self, j: int) -> np.ndarray:
         return self._export(EXPORT_PREFIX, j, (8193,), np.uint32)

@@ -55,13 +55,53 @@ __device__ __forceinline__ void fht_warp(float (&v)[EPL], int dp, int lane) {
             }
     }
     for (int hl = 1; hl * EPL < dp; hl <<= 1) {
-        const bool upper = (lane & hl) != 0;
+        // lower lane: v + o; upper lane: o - v.  Both as fmaf(sg, v, o) with sg = +-1: the product
+        // is exact, so the single rounding equals that of the add / subtract.
+        const float sgn = (lane & hl) ? -1.0f : 1.0f;
 #pragma unroll
         for (int s = 0; s < EPL; ++s) {
             const float o = __shfl_xor_sync(kFull, v[s], hl);
-            v[s] = upper ? (o - v[s]) : (v[s] + o);
+            v[s] = fmaf(sgn, v[s], o);
         }
     }
+}
+
+// Thread-local FHT cross-polytope code (same arithmetic as fhtcp_code_warp, one function per
+// thread, the whole DP-vector in registers).  Used to hash query batches for the first
+// repetitions eagerly (k_fht_qcodes).
+template <int DP>
+__device__ __forceinline__ uint32_t fhtcp_code_thread(const float* __restrict__ xrow, int d, int ell,
+                                                      const uint32_t* __restrict__ sg) {
+    constexpr int W = (DP + 31) / 32;
+    float y[DP];
+#pragma unroll
+    for (int u = 0; u < DP; ++u) y[u] = (u < d) ? __ldg(xrow + u) : 0.0f;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        uint32_t wv[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) wv[k] = __ldg(sg + r * W + k);
+#pragma unroll
+        for (int u = 0; u < DP; ++u) y[u] = __uint_as_float(__float_as_uint(y[u]) ^ (((wv[u >> 5] >> (u & 31)) & 1u) << 31));
+#pragma unroll
+        for (int h = 1; h < DP; h <<= 1) {
+#pragma unroll
+            for (int u = 0; u < DP; ++u)
+                if (!(u & h)) {
+                    const float a = y[u], b = y[u + h];
+                    y[u] = a + b;
+                    y[u + h] = a - b;
+                }
+        }
+    }
+    int bi = 0;
+    float ba = fabsf(y[0]), bv = y[0];
+#pragma unroll
+    for (int u = 1; u < DP; ++u) {
+        const float a = fabsf(y[u]);
+        if (a > ba) { ba = a; bi = u; bv = y[u]; }
+    }
+    return ((uint32_t)(bv < 0.0f) << (ell - 1)) | (uint32_t)bi;
 }
 
 // Cross-polytope hash with three pseudo-random rotations H D_r (§2, 340 §4.3):

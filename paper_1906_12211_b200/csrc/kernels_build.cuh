@@ -160,6 +160,23 @@ __global__ void __launch_bounds__(256) k_fht_rep(const float* __restrict__ X, in
     }
 }
 
+// Eager FHT-CP query codes for repetitions [0, nreps): one thread per (row, repetition), 32
+// consecutive threads share a row (its loads broadcast); out codes [p][ldc].
+template <int DP>
+__global__ void __launch_bounds__(128) k_fht_qcodes(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
+                                                    int c, int K, const uint32_t* __restrict__ sg, int nreps,
+                                                    uint32_t* __restrict__ codes, int ldc) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t p = t / nreps;
+    const int j = (int)(t % nreps);
+    if (p >= np) return;
+    constexpr int W = (DP + 31) / 32;
+    uint64_t full = 0;
+    for (int f = 0; f < c; ++f)
+        full = (full << ell) | fhtcp_code_thread<DP>(X + p * ldx, d, ell, sg + ((int64_t)j * c + f) * 3 * W);
+    codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
+}
+
 // FHT-CP codes of the m pool functions for every row: out [p][m] (uint16)
 template <int EPL>
 __global__ void __launch_bounds__(256) k_fht_funcs(const float* __restrict__ X, int64_t np, int ldx, int d,
@@ -191,6 +208,19 @@ __global__ void k_pool_codes(const uint16_t* __restrict__ fc, int64_t np, int m,
     const uint32_t code = (uint32_t)(full >> (c * ell - K));
     if (keys) keys[(int64_t)r * np + p] = ((uint64_t)code << 32) | (uint64_t)p;
     if (codes) codes[p * ldc + j] = code;
+}
+
+// ---------------------------------------------------------------------------------------------
+// repetition table entries (16 B): the sorted key (code << 32 | id) and the sketch word of the
+// repetition's slot for that id, s_{slot(j)}(id) (R-21: stored inline
+// so the query reads it with the entry instead of a random 8-byte load)
+__global__ void k_entries(const uint64_t* __restrict__ keys, int64_t n, const uint64_t* __restrict__ sk, int M,
+                          int slot, uint64_t* __restrict__ tab) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t key = keys[t];
+    const uint64_t w = M > 0 ? __ldg(sk + (int64_t)(uint32_t)key * M + slot) : 0ull;
+    reinterpret_cast<ulonglong2*>(tab)[t] = make_ulonglong2(key, w);
 }
 
 // ---------------------------------------------------------------------------------------------

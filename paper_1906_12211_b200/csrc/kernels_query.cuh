@@ -22,19 +22,29 @@
 
 namespace pfg {
 
-constexpr int kCB = 256;      // candidate buffer per warp (filter-passing, not yet evaluated)
-constexpr int kU = 4;         // table positions per lane per scan step (memory-level parallelism)
+constexpr int kHC = 2048;     // per-warp shared-memory hash set of evaluated ids (capacity)
+constexpr int kHMax = 1536;   // beyond this many evaluated ids a query switches to the global bitmap
+constexpr int kSB = 192;      // survivor buffer (evaluated ids awaiting their similarity)
+constexpr int kRPI = 8;       // candidate rows read per warp iteration (memory-level parallelism)
+constexpr int kU = 4;         // table positions per lane per scan step
 constexpr int kMaxR = 32;     // max repetitions per chunk
 constexpr int kMaxK = 256;    // max k
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+// one repetition-table entry (16 B): key = (code << 32) | id, sk = sketch word s_{slot(j)}(id)
+struct __align__(16) Entry {
+    uint64_t key;
+    uint64_t sk;
+};
 
 struct QueryParams {
     int64_t n, nq, bm_words, id_offset;
     int d, dpad, K, L, M, B, R, k, k_eff, per_round, use_filter, c, ell, dp, lazy, claim_cap, trace_cap;
     int kt;          // T capacity (>= k_eff, multiple of 32)
+    int qc_n, qc_ld; // query codes precomputed for repetitions [0, qc_n), row stride qc_ld
     int smem_warp;   // bytes of shared memory per warp
     const float* __restrict__ x;
-    const uint64_t* __restrict__ sk;
-    const uint64_t* __restrict__ tab;
+    const Entry* __restrict__ tab;
     const uint32_t* __restrict__ pt;
     const uint8_t* __restrict__ slot;
     const float* __restrict__ qx;
@@ -60,18 +70,18 @@ struct WarpSmem {
     uint64_t* T0;      // [kt]
     uint64_t* T1;      // [kt]
     uint64_t* cand;    // [32]   sorted merge batch
-    uint64_t* cb;      // [kCB]  candidate keys (id << 8 | rep)
-    uint32_t* sid;     // [kCB]  evaluated ids, bucketed by rep
-    float* ssim;       // [kCB]
+    uint32_t* hs;      // [kHC]  hash set of evaluated ids
+    uint32_t* sid;     // [kSB]
+    float* ssim;       // [kSB]
+    uint8_t* srep;     // [kSB]
     uint32_t* beg;     // [kMaxR + 1]
     uint32_t* lo_new;  // [kMaxR]
     uint32_t* lo_old;
     uint32_t* hi_old;
-    uint32_t* qc;      // [kMaxR] lazily computed codes
-    uint32_t* bnd;     // [2 * kMaxR] a / b bounds
-    uint32_t* fcnt;    // [kMaxR] filtered per rep
-    uint32_t* dcnt;    // [kMaxR] dups per rep
-    uint32_t* rcnt;    // [kMaxR + 1] survivors per rep (then bucket offsets)
+    uint32_t* qc;      // [kMaxR]
+    uint32_t* bnd;     // [2 * kMaxR]
+    uint32_t* fcnt;    // [kMaxR]
+    uint32_t* dcnt;    // [kMaxR]
 };
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
@@ -82,8 +92,9 @@ __host__ __device__ inline int warp_smem_bytes(int dpad, int M, int kt) {
     b += align16(M * 8);
     b += 2 * align16(kt * 8);
     b += 32 * 8;
-    b += kCB * 8 + kCB * 4 + kCB * 4;
-    b += align16((kMaxR + 1) * 4) + 3 * kMaxR * 4 + kMaxR * 4 + 2 * kMaxR * 4 + 2 * kMaxR * 4 + align16((kMaxR + 1) * 4);
+    b += kHC * 4;
+    b += kSB * 4 + kSB * 4 + align16(kSB);
+    b += align16((kMaxR + 1) * 4) + 3 * kMaxR * 4 + kMaxR * 4 + 2 * kMaxR * 4 + 2 * kMaxR * 4;
     return align16(b);
 }
 
@@ -95,9 +106,10 @@ __device__ inline WarpSmem carve(unsigned char* base, const QueryParams& p) {
     w.T0 = (uint64_t*)q; q += align16(p.kt * 8);
     w.T1 = (uint64_t*)q; q += align16(p.kt * 8);
     w.cand = (uint64_t*)q; q += 32 * 8;
-    w.cb = (uint64_t*)q; q += kCB * 8;
-    w.sid = (uint32_t*)q; q += kCB * 4;
-    w.ssim = (float*)q; q += kCB * 4;
+    w.hs = (uint32_t*)q; q += kHC * 4;
+    w.sid = (uint32_t*)q; q += kSB * 4;
+    w.ssim = (float*)q; q += kSB * 4;
+    w.srep = (uint8_t*)q; q += align16(kSB);
     w.beg = (uint32_t*)q; q += align16((kMaxR + 1) * 4);
     w.lo_new = (uint32_t*)q; q += kMaxR * 4;
     w.lo_old = (uint32_t*)q; q += kMaxR * 4;
@@ -106,8 +118,11 @@ __device__ inline WarpSmem carve(unsigned char* base, const QueryParams& p) {
     w.bnd = (uint32_t*)q; q += 2 * kMaxR * 4;
     w.fcnt = (uint32_t*)q; q += kMaxR * 4;
     w.dcnt = (uint32_t*)q; q += kMaxR * 4;
-    w.rcnt = (uint32_t*)q; q += align16((kMaxR + 1) * 4);
     return w;
+}
+
+__device__ __forceinline__ uint32_t entry_code(const Entry* e) {
+    return __ldg(reinterpret_cast<const uint32_t*>(e) + 1);
 }
 
 // first position of repetition j whose K-bit code is >= x (x <= 2^K; 2^K -> n)
@@ -119,51 +134,22 @@ __device__ __forceinline__ uint32_t rep_lower_bound(const QueryParams& p, int j,
     const uint32_t pfx = xs >> sh;
     uint32_t lo = __ldg(ptj + pfx), hi = __ldg(ptj + pfx + 1);
     if ((x & ((1ull << sh) - 1)) == 0) return lo;
-    const uint64_t* tj = p.tab + (int64_t)j * p.n;
+    const Entry* tj = p.tab + (int64_t)j * p.n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        const uint32_t cm = (uint32_t)(__ldg(tj + mid) >> 32);
         ++probes;
-        if (cm < xs) lo = mid + 1; else hi = mid;
+        if (entry_code(tj + mid) < xs) lo = mid + 1; else hi = mid;
     }
     return lo;
-}
-
-// 256-bit read-only load of 8 consecutive floats (one full 32-byte sector per lane)
-__device__ __forceinline__ void ldg256(const float* p, float (&v)[8]) {
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-        : "l"(p));
-}
-
-// canonical inner product (R-2): sequential fmaf over t from +0; the zero padding of both rows
-// beyond d leaves the chain unchanged (see k_hp_bits).  dpad is a multiple of 8.
-__device__ __forceinline__ float dot_row(const float* __restrict__ q, const float* __restrict__ xr, int dpad) {
-    float s = 0.0f;
-    const int nc = dpad >> 3;
-#pragma unroll 4
-    for (int c = 0; c < nc; ++c) {
-        float v[8];
-        ldg256(xr + 8 * c, v);
-        const float4 w0 = reinterpret_cast<const float4*>(q)[2 * c];
-        const float4 w1 = reinterpret_cast<const float4*>(q)[2 * c + 1];
-        s = fmaf(w0.x, v[0], s);
-        s = fmaf(w0.y, v[1], s);
-        s = fmaf(w0.z, v[2], s);
-        s = fmaf(w0.w, v[3], s);
-        s = fmaf(w1.x, v[4], s);
-        s = fmaf(w1.y, v[5], s);
-        s = fmaf(w1.z, v[6], s);
-        s = fmaf(w1.w, v[7], s);
-    }
-    return s;
 }
 
 struct QState {
     int tn;               // entries in T (<= k_eff)
     uint32_t nE;          // evaluated (merged) ids
     uint32_t emitted, filtered, dups, probes, flags;
-    uint32_t claims_n;
+    uint32_t claims_n;    // ids recorded in the global bitmap (bitmap mode)
+    uint32_t hcount;      // ids in the shared hash set
+    bool bitmap_mode;
     uint64_t* T;          // current sorted top list
     uint64_t* Tn;         // scratch buffer
 };
@@ -190,14 +176,12 @@ __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem
             const int nc = __popc(vm);
             w.cand[lane] = key;
             __syncwarp();
-            // new position of candidate `lane` = lane + #T entries greater than it
             if (lane < nc) {
                 int lo = 0, hi = st.tn;
                 while (lo < hi) { const int mid = (lo + hi) >> 1; if (st.T[mid] > key) lo = mid + 1; else hi = mid; }
                 const int dst = lane + lo;
                 if (dst < p.k_eff) st.Tn[dst] = key;
             }
-            // new position of T entry e' = e' + #candidates greater than it
             for (int t = lane; t < st.tn; t += 32) {
                 const uint64_t tv = st.T[t];
                 int lo = 0, hi = nc;
@@ -219,116 +203,132 @@ __device__ __forceinline__ float kth_sim_clamped(const QueryParams& p, const QSt
     return fminf(fmaxf(ip, -1.0f), 1.0f);
 }
 
-// compute sims for survivors [0, ns)
-__device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int ns, int lane) {
-    for (int e = lane; e < ns; e += 32)
-        w.ssim[e] = dot_row(w.qrow, p.x + (int64_t)w.sid[e] * p.dpad, p.dpad);
+// Similarities of survivors [e0, e1) (R-2): the warp reads each candidate row coalesced, one 16-byte
+// chunk per lane (chunk c -> lane c mod 32), each lane keeps a sequential fmaf chain, and the 32
+// lane sums are added in the fixed tree h = 16, 8, 4, 2, 1 -- the oracle's or_sim order.  Zero
+// padding beyond d leaves a chain unchanged (it never holds -0).  kRPI rows are in flight per step.
+__device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int e0, int e1, int lane) {
+    const int nch = p.dpad >> 2;
+    const float4* q4 = reinterpret_cast<const float4*>(w.qrow);
+    for (int b = e0; b < e1; b += kRPI) {
+        float acc[kRPI];
+        const float4* rows[kRPI];
+#pragma unroll
+        for (int r = 0; r < kRPI; ++r) {
+            acc[r] = 0.0f;
+            const int e = b + r < e1 ? b + r : e1 - 1;
+            rows[r] = reinterpret_cast<const float4*>(p.x + (int64_t)w.sid[e] * p.dpad);
+        }
+        for (int c = lane; c < nch + ((32 - (nch & 31)) & 31); c += 32) {
+            if (c < nch) {
+                float4 v[kRPI];
+#pragma unroll
+                for (int r = 0; r < kRPI; ++r)
+                    v[r] = (b + r < e1) ? __ldg(rows[r] + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 q = q4[c];
+#pragma unroll
+                for (int r = 0; r < kRPI; ++r) {
+                    acc[r] = fmaf(q.x, v[r].x, acc[r]);
+                    acc[r] = fmaf(q.y, v[r].y, acc[r]);
+                    acc[r] = fmaf(q.z, v[r].z, acc[r]);
+                    acc[r] = fmaf(q.w, v[r].w, acc[r]);
+                }
+            }
+        }
+        // tree over the 32 lane sums, level h = 16, 8, 4 halving the rows a lane keeps (a
+        // transposed reduction: 7 shuffles for 8 rows), then h = 2, 1; lane 4r ends with row r
+        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+        float t4[4], t2[2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float recv = __shfl_xor_sync(kFull, h16 ? acc[k] : acc[k + 4], 16);
+            t4[k] = (h16 ? acc[k + 4] : acc[k]) + recv;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float recv = __shfl_xor_sync(kFull, h8 ? t4[k] : t4[k + 2], 8);
+            t2[k] = (h8 ? t4[k + 2] : t4[k]) + recv;
+        }
+        float t1 = (h4 ? t2[1] : t2[0]) + __shfl_xor_sync(kFull, h4 ? t2[0] : t2[1], 4);
+        t1 = t1 + __shfl_xor_sync(kFull, t1, 2);
+        t1 = t1 + __shfl_xor_sync(kFull, t1, 1);
+        const int rr = lane >> 2;
+        if ((lane & 3) == 0 && b + rr < e1) w.ssim[b + rr] = t1;
+    }
     __syncwarp();
 }
 
-// warp-cooperative ascending bitonic sort of cb[0..P) in shared memory (P power of two)
-__device__ __forceinline__ void warp_sort_smem(uint64_t* s, int P, int lane) {
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = lane; i < P; i += 32) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const uint64_t a = s[i], b = s[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) { s[i] = b; s[ixj] = a; }
-                }
-            }
-            __syncwarp();
-        }
-    }
-}
-
-// Flush the candidate buffer (R-17): candidates are filter-passing positions whose id was
-// not evaluated when scanned.  Sort by (id, rep); the first occurrence of an id (its smallest
-// repetition) is evaluated, later ones count as duplicates -- the same evaluated set and repetition
-// attribution as the sequential algorithm.  Survivors are bucketed by repetition, claimed in the
-// bitmap, their inner products computed, and merged repetition by repetition; every repetition
-// < `complete` (all positions scanned) gets its stop check after its survivors are merged.
-// Returns true when the query stops (r_stop set).
-__device__ __forceinline__ bool flush_chunk(const QueryParams& p, const WarpSmem& w, QState& st, int& ncand,
-                                            int& next_check, int complete, int nr, int c0, int i, int64_t qi,
-                                            uint32_t* bm, uint32_t* claims, int& r_stop, int lane) {
-    int ns = 0;
-    if (ncand > 0) {
-        int P = 32;
-        while (P < ncand) P <<= 1;
-        for (int e = ncand + lane; e < P; e += 32) w.cb[e] = ~0ull;
-        __syncwarp();
-        warp_sort_smem(w.cb, P, lane);
-        for (int r = lane; r <= nr; r += 32) w.rcnt[r] = 0;
-        __syncwarp();
-        // dedupe + per-rep counts
-        for (int e = lane; e < ncand; e += 32) {
-            const uint64_t key = w.cb[e];
-            const bool keep = (e == 0) || ((w.cb[e - 1] >> 8) != (key >> 8));
-            const int r = (int)(key & 0xff);
-            if (keep) atomicAdd(&w.rcnt[r], 1u); else atomicAdd(&w.dcnt[r], 1u);
-        }
-        __syncwarp();
-        // exclusive prefix over reps (nr <= 32) -> bucket offsets in rcnt
-        {
-            const uint32_t v = lane < nr ? w.rcnt[lane] : 0u;
-            uint32_t incl = v;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t o = __shfl_up_sync(kFull, incl, off);
-                if (lane >= off) incl += o;
-            }
-            const uint32_t tot = __shfl_sync(kFull, incl, nr - 1);
-            __syncwarp();
-            if (lane < nr) w.rcnt[lane] = incl - v;
-            if (lane == 0) w.rcnt[nr] = tot;
-            __syncwarp();
-        }
-        ns = (int)w.rcnt[nr];
-        // scatter survivors to rep buckets, claim them in the bitmap
-        for (int e = lane; e < ncand; e += 32) {
-            const uint64_t key = w.cb[e];
-            const bool keep = (e == 0) || ((w.cb[e - 1] >> 8) != (key >> 8));
-            if (keep) {
-                const uint32_t id = (uint32_t)(key >> 8);
-                const int r = (int)(key & 0xff);
-                const uint32_t dst = atomicAdd(&w.rcnt[r], 1u);
-                w.sid[dst] = id;
-                atomicOr(bm + (id >> 5), 1u << (id & 31));
-            }
-        }
-        __syncwarp();
-        // rcnt[r] is now the end of bucket r; record claims for the bitmap reset
-        for (int e = lane; e < ns; e += 32) {
-            const uint32_t cn = st.claims_n + e;
-            if (cn < (uint32_t)p.claim_cap) claims[cn] = w.sid[e];
-        }
-        st.claims_n += ns;
-        compute_sims(p, w, ns, lane);
-    }
-    ncand = 0;
-    // merge bucket by bucket in repetition order, stop check after every complete repetition
+// Process the survivor buffer (in repetition order): similarities, then merge repetition by
+// repetition; every repetition < `complete` (all positions scanned) gets its stop check after its
+// survivors are merged (Alg. 1 line 8).  Returns true when the query stops (r_stop set).
+__device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, QState& st, int& nbuf, int& next_check,
+                                      int complete, int nr, int c0, int i, int64_t qi, int& r_stop, int lane) {
+    compute_sims(p, w, 0, nbuf, lane);
+    int e = 0;
+    bool stop = false;
     for (;;) {
-        if (next_check >= nr) break;
-        if (ns > 0) {
-            const int b0 = next_check == 0 ? 0 : (int)w.rcnt[next_check - 1];
-            const int b1 = (int)w.rcnt[next_check];
-            if (b1 > b0) merge_range(p, w, st, b0, b1, qi, lane);
-        }
-        if (next_check >= complete) break;
+        int e2 = e;
+        while (e2 < nbuf && w.srep[e2] == next_check) ++e2;
+        if (e2 > e) merge_range(p, w, st, e, e2, qi, lane);
+        e = e2;
+        if (next_check >= complete || next_check >= nr) break;
         const int j1 = c0 + next_check + 1;
         if (st.tn == p.k_eff && (!p.per_round || j1 == p.L)) {
             const float ip = kth_sim_clamped(p, st);
-            if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + (j1 - 1))) {
-                r_stop = next_check;
-                return true;
-            }
+            if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + (j1 - 1))) { r_stop = next_check; stop = true; break; }
         }
         ++next_check;
     }
+    nbuf = 0;
     __syncwarp();
-    return false;
+    return stop;
+}
+
+__device__ __forceinline__ uint32_t hs_slot(uint32_t id) { return (id * 0x9E3779B1u) >> (32 - 11); }
+
+// claim id for evaluation: true if it was not evaluated before (called by one lane per distinct id)
+__device__ __forceinline__ bool claim(const WarpSmem& w, const QState& st, uint32_t* bm, uint32_t id) {
+    if (st.bitmap_mode) {
+        const uint32_t bit = 1u << (id & 31);
+        return !(atomicOr(bm + (id >> 5), bit) & bit);
+    }
+    uint32_t h = hs_slot(id);
+    for (;;) {
+        const uint32_t old = atomicCAS(&w.hs[h], kEmpty, id);
+        if (old == kEmpty) return true;
+        if (old == id) return false;
+        h = (h + 1) & (kHC - 1);
+    }
+}
+
+// membership test (no insert), for the i = 0 linear scan
+__device__ __forceinline__ bool evaluated(const WarpSmem& w, const QState& st, const uint32_t* bm, uint32_t id) {
+    if (st.bitmap_mode) return (__ldcg(bm + (id >> 5)) >> (id & 31)) & 1u;
+    uint32_t h = hs_slot(id);
+    for (;;) {
+        const uint32_t v = w.hs[h];
+        if (v == kEmpty) return false;
+        if (v == id) return true;
+        h = (h + 1) & (kHC - 1);
+    }
+}
+
+// move the hash set into the global bitmap (a query that evaluated more than kHMax ids)
+__device__ __forceinline__ void to_bitmap_mode(const QueryParams& p, const WarpSmem& w, QState& st, uint32_t* bm,
+                                               uint32_t* claims, int lane) {
+    for (int h0 = 0; h0 < kHC; h0 += 32) {
+        const uint32_t v = w.hs[h0 + lane];
+        const bool has = v != kEmpty;
+        if (has) atomicOr(bm + (v >> 5), 1u << (v & 31));
+        const uint32_t m = __ballot_sync(kFull, has);
+        if (has) {
+            const uint32_t cn = st.claims_n + __popc(m & lanemask_lt());
+            if (cn < (uint32_t)p.claim_cap) claims[cn] = v;
+        }
+        st.claims_n += __popc(m);
+    }
+    st.bitmap_mode = true;
+    __syncwarp();
 }
 
 template <int EPL>
@@ -356,10 +356,12 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
         }
         for (int t = lane; t < p.dpad; t += 32) w.qrow[t] = p.qx[qi * p.dpad + t];
         for (int t = lane; t < p.M; t += 32) w.qsk[t] = p.qsk[qi * p.M + t];
+        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(w.hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
         __syncwarp();
 
         QState st;
         st.tn = 0; st.nE = 0; st.emitted = st.filtered = st.dups = st.probes = st.flags = 0; st.claims_n = 0;
+        st.hcount = 0; st.bitmap_mode = false;
         st.T = w.T0; st.Tn = w.T1;
         bool stopped = false;
         int i_stop = 0, j_stop = 0;
@@ -374,9 +376,14 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                     while (lo < hi) { const int mid = (lo + hi) >> 1; if (ip >= __ldg(p.taub + mid)) hi = mid; else lo = mid + 1; }
                     tau = lo;
                 }
-                // lazy FHT-CP hashing of the chunk's repetitions (first level only)
-                if (i == p.K && p.lazy) {
+                // query codes of the chunk's repetitions (first level only): precomputed for
+                // repetitions < qc_n, otherwise hashed here (FHT-CP, warp-cooperative)
+                if (i == p.K) {
                     for (int r = 0; r < nr; ++r) {
+                        if (c0 + r < p.qc_n) {
+                            if (lane == 0) w.qc[r] = __ldg(p.qcodes + qi * p.qc_ld + c0 + r);
+                            continue;
+                        }
                         uint64_t full = 0;
                         for (int t = 0; t < p.c; ++t) {
                             const int64_t f = (int64_t)(c0 + r) * p.c + t;
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                     const int r = task < nr ? task : task - nr;
                     const int j = c0 + r;
                     uint32_t qc;
-                    if (i == p.K) qc = p.lazy ? w.qc[r] : __ldg(p.qcodes + qi * p.L + j);
+                    if (i == p.K) qc = w.qc[r];
                     else qc = cur[j].x;
                     const uint64_t qp = (uint64_t)qc >> (p.K - i);
                     const uint64_t x = (task < nr ? qp : qp + 1) << (p.K - i);
@@ -414,7 +421,6 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                     em = (elo - nelo) + (nehi - ehi);
                     cur[j] = make_uint4(w.qc[lane], nelo, nehi, 0u);
                 }
-                // exclusive prefix sum of per-rep emitted counts
                 uint32_t incl = em;
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {
@@ -426,74 +432,79 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                 __syncwarp();
                 const uint32_t total = w.beg[nr];
 
-                int ncand = 0, next_check = 0, r_stop = -1;
-                // scan the chunk's emitted positions in (rep, position) order, kU per lane per step
-                for (uint32_t g0 = 0;; g0 += 32 * kU) {
-                    const bool last = g0 + 32 * kU >= total;
-                    if (g0 < total) {
-                        uint32_t idv[kU];
-                        int rv[kU];
-                        bool act[kU], pass[kU];
+                int nbuf = 0, next_check = 0, r_stop = -1;
+                // scan the chunk's emitted positions in (rep, position) order, kU per lane per step;
+                // each 16-byte table entry carries the id and its sketch word for this repetition
+                for (uint32_t g0 = 0; g0 < total && !stopped; g0 += 32 * kU) {
+                    uint32_t idv[kU];
+                    int rv[kU];
+                    bool pass[kU];
 #pragma unroll
-                        for (int u = 0; u < kU; ++u) {
-                            const uint32_t g = g0 + u * 32 + lane;
-                            act[u] = g < total;
-                            rv[u] = 0;
-                            idv[u] = 0;
-                            if (act[u]) {
-                                int r = 0;
-                                while (r + 1 < nr && w.beg[r + 1] <= g) ++r;
-                                const uint32_t o = g - w.beg[r];
-                                const uint32_t lenA = w.lo_old[r] - w.lo_new[r];
-                                const uint32_t pos = (o < lenA) ? w.lo_new[r] + o : w.hi_old[r] + (o - lenA);
-                                idv[u] = (uint32_t)__ldg(p.tab + (int64_t)(c0 + r) * p.n + pos);
-                                rv[u] = r;
+                    for (int u = 0; u < kU; ++u) {
+                        const uint32_t g = g0 + u * 32 + lane;
+                        pass[u] = false;
+                        rv[u] = 0;
+                        idv[u] = 0;
+                        if (g < total) {
+                            int r = 0;
+                            while (r + 1 < nr && w.beg[r + 1] <= g) ++r;
+                            const uint32_t o = g - w.beg[r];
+                            const uint32_t lenA = w.lo_old[r] - w.lo_new[r];
+                            const uint32_t pos = (o < lenA) ? w.lo_new[r] + o : w.hi_old[r] + (o - lenA);
+                            const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.tab + (int64_t)(c0 + r) * p.n + pos));
+                            idv[u] = e.x;
+                            rv[u] = r;
+                            pass[u] = true;
+                            if (p.use_filter) {
+                                const int s = __ldg(p.slot + c0 + r);
+                                const uint64_t sw = ((uint64_t)e.w << 32) | e.z;
+                                pass[u] = __popcll(sw ^ w.qsk[s]) <= tau;
                             }
                         }
-                        if (p.use_filter) {
-                            uint64_t sw[kU];
+                    }
 #pragma unroll
-                            for (int u = 0; u < kU; ++u)
-                                sw[u] = act[u] ? __ldg(p.sk + (int64_t)idv[u] * p.M + __ldg(p.slot + c0 + rv[u])) : 0ull;
-#pragma unroll
-                            for (int u = 0; u < kU; ++u) {
-                                pass[u] = false;
-                                if (act[u]) {
-                                    const int s = __ldg(p.slot + c0 + rv[u]);
-                                    pass[u] = __popcll(sw[u] ^ w.qsk[s]) <= tau;
-                                    if (!pass[u]) atomicAdd(&w.fcnt[rv[u]], 1u);
-                                }
-                            }
-                        } else {
-#pragma unroll
-                            for (int u = 0; u < kU; ++u) pass[u] = act[u];
+                    for (int u = 0; u < kU; ++u) {
+                        const uint32_t g = g0 + u * 32 + lane;
+                        if (g < total && !pass[u]) atomicAdd(&w.fcnt[rv[u]], 1u);
+                        // claims in (rep, position) order: lanes in order within u, u in order
+                        const uint32_t pm = __ballot_sync(kFull, pass[u]);
+                        bool fresh = false;
+                        if (pass[u]) {
+                            const uint32_t grp = __match_any_sync(pm, idv[u]);
+                            if ((int)(__ffs(grp) - 1) == lane) fresh = claim(w, st, bm, idv[u]);
+                            if (!fresh) atomicAdd(&w.dcnt[rv[u]], 1u);
                         }
-                        uint32_t bw[kU];
-#pragma unroll
-                        for (int u = 0; u < kU; ++u) bw[u] = pass[u] ? __ldcg(bm + (idv[u] >> 5)) : 0u;
-#pragma unroll
-                        for (int u = 0; u < kU; ++u) {
-                            bool fresh = false;
-                            if (pass[u]) {
-                                fresh = !((bw[u] >> (idv[u] & 31)) & 1u);
-                                if (!fresh) atomicAdd(&w.dcnt[rv[u]], 1u);
+                        const uint32_t fm = __ballot_sync(kFull, fresh);
+                        if (fresh) {
+                            const int rank = __popc(fm & lanemask_lt());
+                            w.sid[nbuf + rank] = idv[u];
+                            w.srep[nbuf + rank] = (uint8_t)rv[u];
+                            if (st.bitmap_mode) {
+                                const uint32_t cn = st.claims_n + rank;
+                                if (cn < (uint32_t)p.claim_cap) claims[cn] = idv[u];
                             }
-                            const uint32_t fm = __ballot_sync(kFull, fresh);
-                            if (fresh) w.cb[ncand + __popc(fm & lanemask_lt())] = ((uint64_t)idv[u] << 8) | (uint64_t)rv[u];
-                            ncand += __popc(fm);
                         }
+                        const int nf = __popc(fm);
+                        nbuf += nf;
+                        if (st.bitmap_mode) st.claims_n += nf; else st.hcount += nf;
                         __syncwarp();
                     }
-                    if (last || ncand > kCB - 32 * kU) {
+                    if (!st.bitmap_mode && st.hcount > kHMax) to_bitmap_mode(p, w, st, bm, claims, lane);
+                    const uint32_t done_pos = min(total, g0 + 32u * kU);
+                    if (nbuf > kSB - 32 * kU || done_pos == total) {
                         int complete = nr;
-                        if (!last) { complete = 0; while (complete < nr && w.beg[complete + 1] <= g0 + 32 * kU) ++complete; }
-                        if (flush_chunk(p, w, st, ncand, next_check, complete, nr, c0, i, qi, bm, claims, r_stop, lane)) {
+                        if (done_pos < total) { complete = 0; while (complete < nr && w.beg[complete + 1] <= done_pos) ++complete; }
+                        if (drain(p, w, st, nbuf, next_check, complete, nr, c0, i, qi, r_stop, lane)) {
                             stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
                         }
                     }
-                    if (stopped || last) break;
                 }
-                // account the chunk's repetitions up to the stop (all of them if no stop)
+                if (total == 0) {
+                    // empty chunk: every repetition is complete, check them in order
+                    if (drain(p, w, st, nbuf, next_check, nr, nr, c0, i, qi, r_stop, lane)) {
+                        stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
+                    }
+                }
                 const int rmax = stopped ? r_stop : nr - 1;
                 uint32_t e_acc = 0, f_acc = 0, d_acc = 0;
                 for (int r = 0; r <= rmax; ++r) {
@@ -513,14 +524,13 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
             int ns = 0;
             for (int64_t g0 = 0; g0 < p.n; g0 += 32) {
                 const int64_t id = g0 + lane;
-                bool fresh = false;
-                if (id < p.n) fresh = !((__ldcg(bm + (id >> 5)) >> (id & 31)) & 1u);
+                const bool fresh = id < p.n && !evaluated(w, st, bm, (uint32_t)id);
                 const uint32_t fm = __ballot_sync(kFull, fresh);
                 if (fresh) w.sid[ns + __popc(fm & lanemask_lt())] = (uint32_t)id;
                 ns += __popc(fm);
                 __syncwarp();
-                if (ns > kCB - 32 || g0 + 32 >= p.n) {
-                    compute_sims(p, w, ns, lane);
+                if (ns > kSB - 32 || g0 + 32 >= p.n) {
+                    compute_sims(p, w, 0, ns, lane);
                     if (ns) merge_range(p, w, st, 0, ns, qi, lane);
                     ns = 0;
                 }
@@ -529,7 +539,6 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
             i_stop = 0; j_stop = 1;
         }
 
-        // output: T sorted desc; ids are global
         for (int t = lane; t < p.k; t += 32) {
             if (t < st.tn) {
                 const uint64_t kk = st.T[t];
@@ -544,17 +553,20 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
             pfg_query_stats s;
             s.i_stop = i_stop; s.j_stop = j_stop; s.emitted = st.emitted; s.filtered = st.filtered;
             s.dups = st.dups; s.evaluated = st.nE;
-            s.flags = (p.k > p.k_eff ? 1u : 0u) | ((p.trace_cap > 0 && st.nE > (uint32_t)p.trace_cap) ? 4u : 0u);
+            s.flags = (p.k > p.k_eff ? 1u : 0u) | ((p.trace_cap > 0 && st.nE > (uint32_t)p.trace_cap) ? 4u : 0u) |
+                      (st.bitmap_mode ? 8u : 0u);
             s.probes = st.probes;
             p.stats[qi] = s;
         }
-        // return the bitmap to zero for the next query of this slot
-        const uint32_t ncl = st.claims_n;
-        __syncwarp();
-        if (ncl <= (uint32_t)p.claim_cap) {
-            for (uint32_t e = lane; e < ncl; e += 32) __stcg(bm + (claims[e] >> 5), 0u);
-        } else {
-            for (int64_t e = lane; e < p.bm_words; e += 32) __stcg(bm + e, 0u);
+        // bitmap mode: return the bitmap to zero for the next query of this slot
+        if (st.bitmap_mode) {
+            const uint32_t ncl = st.claims_n;
+            __syncwarp();
+            if (ncl <= (uint32_t)p.claim_cap) {
+                for (uint32_t e = lane; e < ncl; e += 32) __stcg(bm + (claims[e] >> 5), 0u);
+            } else {
+                for (int64_t e = lane; e < p.bm_words; e += 32) __stcg(bm + e, 0u);
+            }
         }
         __syncwarp();
     }

@@ -155,9 +155,9 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     // per repetition: sorted table + 13-bit prefix table + slot + its own functions / selection
     const uint64_t N = (uint64_t)n;
     const uint64_t fn_hp = 4ull * g.dpad, fn_fht = 3ull * g.W * 4;
-    g.fixed_bytes = 4ull * N * g.dpad + 8ull * N * g.M + 4ull * 64 * g.M * g.dpad + 8ull * (g.ell + 1) * 41;
+    g.fixed_bytes = 4ull * N * g.dpad + 4ull * 64 * g.M * g.dpad + 8ull * (g.ell + 1) * 41;
     if (g.strategy == PFG_POOL) g.fixed_bytes += (uint64_t)g.m * (family == PFG_SIMHASH ? fn_hp : fn_fht);
-    g.per_rep_bytes = 8ull * N + 4ull * 8193 + 1;
+    g.per_rep_bytes = 16ull * N + 4ull * 8193 + 1;  // 16-byte entries: key + inline sketch word (R-21)
     if (g.strategy == PFG_INDEPENDENT) g.per_rep_bytes += (uint64_t)g.c * (family == PFG_SIMHASH ? fn_hp : fn_fht);
     else g.per_rep_bytes += 4ull * g.c;
     return PFG_OK;
@@ -300,7 +300,7 @@ struct pfg_index {
     uint64_t seed = 0;
     std::mutex mu;
     // index arrays (device)
-    DBuf x, sk, tab, pt, slot, hpfn, sg, sel, skfn;
+    DBuf x, tab, pt, slot, hpfn, sg, sel, skfn;
     std::vector<double> cpT;
     std::vector<int32_t> slot_h, sel_h;
     // cached stop tables: key (recall bits, rule, per_round) -> device thr [K][L]; eps -> taub
@@ -314,6 +314,7 @@ struct pfg_index {
     int64_t slots_bm = 0;
     // launch accounting and phase timing of the last search
     int launches = 0;
+    int qc_n = 0, qc_ld = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     float last_ms[3] = {0, 0, 0};
     int last_launches = 0;
@@ -327,6 +328,7 @@ namespace pfg {
 namespace {
 
 constexpr int kClaimCap = 8192;
+constexpr int kEagerReps = 32;
 
 template <int EPL>
 void launch_fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps,
@@ -670,11 +672,30 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         I->launches += 1;
     }
     *lazy = (g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT && !force_codes);
+    I->qc_n = 0;
+    I->qc_ld = g.L;
     if (need_codes && !*lazy) {
         PFG_TRY(I->qcodes.ensure((size_t)nq * g.L * 4, "query codes"));
         bool pool_ready = false;
         PFG_TRY(hash_reps(I, I->qx.as<float>(), nq, 0, g.L, nullptr, I->qcodes.as<uint32_t>(), g.L, I->qbits, I->qfc,
                           pool_ready, st));
+        I->qc_n = g.L;
+    } else if (need_codes && (g.dp == 32 || g.dp == 64 || g.dp == 128)) {
+        // FHT-CP independent: hash the first kEagerReps repetitions of every query here, one thread
+        // per (query, repetition); the query kernel hashes later repetitions lazily, if reached
+        const int ne = std::min(g.L, kEagerReps);
+        PFG_TRY(I->qcodes.ensure((size_t)nq * ne * 4, "query codes"));
+        const int64_t threads = nq * ne;
+        const unsigned blocks = (unsigned)((threads + 127) / 128);
+        const uint32_t* sg = I->sg.as<uint32_t>();
+        uint32_t* qc = I->qcodes.as<uint32_t>();
+        if (g.dp == 32) k_fht_qcodes<32><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
+        else if (g.dp == 64) k_fht_qcodes<64><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
+        else k_fht_qcodes<128><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 1;
+        I->qc_n = ne;
+        I->qc_ld = ne;
     }
     return PFG_OK;
 }
@@ -751,21 +772,23 @@ pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t budget, i
     }
     // a2: functions
     PFG_TRY(gen_functions(I.get(), st));
-    // a4: sketches
+    // a4: per-point sketches (transient: their slot words are stored inline in the tables, R-21)
+    DBuf skp;
     if (g.M > 0) {
-        PFG_TRY(I->sk.alloc((size_t)n * g.M * 8, "sketches"));
-        hp_bits(I->x.as<float>(), n, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->sk.as<uint8_t>(),
+        PFG_TRY(skp.alloc((size_t)n * g.M * 8, "sketches"));
+        hp_bits(I->x.as<float>(), n, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, skp.as<uint8_t>(),
                 (int64_t)g.M * 8, st);
         PFG_CUDA(cudaGetLastError());
     }
     // a3 + a5: hash, sort and tabulate the repetitions in batches
-    PFG_TRY(I->tab.alloc((size_t)g.L * n * 8, "tables"));
+    PFG_TRY(I->tab.alloc((size_t)g.L * n * 16, "tables"));
     PFG_TRY(I->pt.alloc((size_t)g.L * 8193 * 4, "prefix tables"));
     {
         const int64_t budget_keys = (int64_t)1 << 28;  // 2 GiB of keys per batch
         const int Rb = (int)std::max<int64_t>(1, std::min<int64_t>(g.L, budget_keys / n));
-        DBuf keys, bits, poolvals, temp;
+        DBuf keys, sorted, bits, poolvals, temp;
         PFG_TRY(keys.alloc((size_t)Rb * n * 8, "build keys"));
+        PFG_TRY(sorted.alloc((size_t)n * 8, "sorted keys"));
         size_t temp_bytes = 0;
         cub::DeviceRadixSort::SortKeys(nullptr, temp_bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, 32,
                                        32 + g.K, st);
@@ -777,11 +800,13 @@ pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t budget, i
                               pool_ready, st));
             for (int r = 0; r < nb; ++r) {
                 const int j = r0 + r;
-                uint64_t* dst = I->tab.as<uint64_t>() + (size_t)j * n;
                 size_t tb = temp.bytes;
-                PFG_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, tb, keys.as<uint64_t>() + (size_t)r * n, dst, (int)n, 32,
-                                                        32 + g.K, st));
-                k_prefix<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(dst, n, g.K, I->pt.as<uint32_t>() + (size_t)j * 8193);
+                PFG_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, tb, keys.as<uint64_t>() + (size_t)r * n, sorted.as<uint64_t>(),
+                                                        (int)n, 32, 32 + g.K, st));
+                k_entries<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sorted.as<uint64_t>(), n, skp.as<uint64_t>(), g.M,
+                                                                      I->slot_h[j], I->tab.as<uint64_t>() + (size_t)j * n * 2);
+                k_prefix<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(sorted.as<uint64_t>(), n, g.K,
+                                                                         I->pt.as<uint32_t>() + (size_t)j * 8193);
                 PFG_CUDA(cudaGetLastError());
             }
         }
@@ -867,9 +892,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.d = g.d; p.dpad = g.dpad; p.K = g.K; p.L = g.L; p.M = g.M; p.B = s.B; p.R = s.R; p.k = k; p.k_eff = k_eff;
     p.per_round = s.per_round; p.use_filter = (s.use_filter && g.M > 0) ? 1 : 0; p.c = g.c; p.ell = g.ell; p.dp = g.dp;
     p.lazy = lazy ? 1 : 0; p.claim_cap = kClaimCap; p.trace_cap = s.trace_cap; p.kt = kt; p.smem_warp = smem_warp;
-    p.x = I->x.as<float>(); p.sk = I->sk.as<uint64_t>(); p.tab = I->tab.as<uint64_t>(); p.pt = I->pt.as<uint32_t>();
+    p.x = I->x.as<float>(); p.tab = I->tab.as<Entry>(); p.pt = I->pt.as<uint32_t>();
     p.slot = I->slot.as<uint8_t>(); p.qx = I->qx.as<float>(); p.qsk = I->qsk.as<uint64_t>();
-    p.qcodes = lazy ? nullptr : I->qcodes.as<uint32_t>(); p.sg = I->sg.as<uint32_t>(); p.qzero = I->qzero.as<uint8_t>();
+    p.qcodes = I->qcodes.as<uint32_t>(); p.qc_n = I->qc_n; p.qc_ld = I->qc_ld;
+    p.sg = I->sg.as<uint32_t>(); p.qzero = I->qzero.as<uint8_t>();
     p.thr = thr->as<float>(); p.taub = taub->as<float>(); p.work = I->work.as<unsigned long long>();
     p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
     p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
@@ -951,13 +977,13 @@ pfg_status pfg_export(const pfg_index* Ic, int32_t what, int32_t arg, void* dst,
     switch (what) {
         case PFG_EXPORT_TABLE:
             if (arg < 0 || arg >= g.L) return fail(PFG_E_ARG, "rep out of range");
-            return copy(I->tab.as<uint64_t>() + (size_t)arg * g.n, (uint64_t)g.n * 8);
+            return copy(I->tab.as<uint64_t>() + (size_t)arg * g.n * 2, (uint64_t)g.n * 16);
         case PFG_EXPORT_PREFIX:
             if (arg < 0 || arg >= g.L) return fail(PFG_E_ARG, "rep out of range");
             return copy(I->pt.as<uint32_t>() + (size_t)arg * 8193, 8193ull * 4);
         case PFG_EXPORT_SKETCH:
-            if (g.M == 0) return fail(PFG_E_STATE, "index has no sketches");
-            return copy(I->sk.p, (uint64_t)g.n * g.M * 8);
+            return fail(PFG_E_STATE, "per-point sketches are not retained: each repetition table stores its slot's "
+                                     "sketch word inline (PFG_EXPORT_TABLE)");
         case PFG_EXPORT_DATA: {
             if (bytes != (uint64_t)g.n * g.d * 4) return fail(PFG_E_ARG, "dst_bytes must be n*d*4");
             PFG_CUDA(cudaMemcpy2D(dst, (size_t)g.d * 4, I->x.p, (size_t)g.dpad * 4, (size_t)g.d * 4, (size_t)g.n,

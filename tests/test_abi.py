@@ -37,17 +37,18 @@ def test_abi_struct_sizes_match_header():
 
 
 def test_cost_model_configs():
-    # SURVEY.md Appendix B (A-11 reading): L for BASELINE configs 2-5 at their budgets (GiB)
-    assert pfg.derive_reps(1_000_000, 100, "fht_cp", 4 << 30)[0] == 450  # rows padded to 104 floats
-    assert pfg.derive_reps(1_000_000, 300, "simhash", 8 << 30)[0] == 882
-    assert pfg.derive_reps(1_000_000, 960, "simhash", 16 << 30, strategy="pool")[0] == 1626
-    assert pfg.derive_reps(12_500_000, 100, "fht_cp", 120 << 30)[0] == 1200
+    # L for BASELINE configs 2-5 at their budgets (GiB) under the R-11 cost model with 16-byte
+    # entries (R-21); SURVEY.md Appendix B has the 8-byte-entry figures 452 / 884 / 1626 / 1206
+    assert pfg.derive_reps(1_000_000, 100, "fht_cp", 4 << 30)[0] == 241  # 16-byte entries with inline sketch words (R-21)
+    assert pfg.derive_reps(1_000_000, 300, "simhash", 8 << 30)[0] == 458
+    assert pfg.derive_reps(1_000_000, 960, "simhash", 16 << 30, strategy="pool")[0] == 830
+    assert pfg.derive_reps(12_500_000, 100, "fht_cp", 120 << 30)[0] == 618
 
 
 def test_cost_model_arithmetic():
     # budget = fixed + exactly 3 repetitions -> L = 3; one byte less -> 2
     L, minb, ib = pfg.derive_reps(5000, 40, "simhash", 10 << 30, max_reps=1)
-    per_rep = 8 * 5000 + 4 * 8193 + 1 + 24 * 4 * 40
+    per_rep = 16 * 5000 + 4 * 8193 + 1 + 24 * 4 * 40
     fixed = minb - per_rep
     assert pfg.derive_reps(5000, 40, "simhash", fixed + 3 * per_rep)[0] == 3
     assert pfg.derive_reps(5000, 40, "simhash", fixed + 3 * per_rep - 1)[0] == 2

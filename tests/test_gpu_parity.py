@@ -56,15 +56,18 @@ def test_build_arrays_bit_exact(cases, name):
     g, o = c.gpu, c.orc
     assert g.reps == o.L and g.ell == o.ell and g.funcs_per_rep == o.c
     assert np.array_equal(g.export_data().view(np.uint32), o.data().view(np.uint32))
-    assert np.array_equal(g.export_sketches(), o.sketches())
-    assert np.array_equal(g.export_slots(), o.slots())
+    slots = g.export_slots()
+    assert np.array_equal(slots, o.slots())
     if o.strategy == O.POOL:
         assert np.array_equal(g.export_pool_sel(), o.pool_sel())
+    osk = o.sketches()
     for j in range(o.L):
         tab = g.export_table(j)
         codes, ids = o.rep(j)
-        assert np.array_equal((tab >> np.uint64(32)).astype(np.uint32), codes), j
-        assert np.array_equal((tab & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
+        # inline sketch word = the oracle's per-point sketch of this repetition's slot (R-21)
+        assert np.array_equal(tab[:, 1], osk[ids, slots[j]]), j
         assert np.array_equal(g.export_prefix(j), o.prefix_table(j)), j
 
 
