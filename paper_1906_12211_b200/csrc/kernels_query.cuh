@@ -212,27 +212,25 @@ __device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSme
     const float4* q4 = reinterpret_cast<const float4*>(w.qrow);
     for (int b = e0; b < e1; b += kRPI) {
         float acc[kRPI];
-        const float4* rows[kRPI];
+        uint32_t off[kRPI];   // row offsets in float4 units (n * dpad / 4 < 2^32)
+        const int nrow = min(kRPI, e1 - b);
 #pragma unroll
         for (int r = 0; r < kRPI; ++r) {
             acc[r] = 0.0f;
-            const int e = b + r < e1 ? b + r : e1 - 1;
-            rows[r] = reinterpret_cast<const float4*>(p.x + (int64_t)w.sid[e] * p.dpad);
+            off[r] = w.sid[b + (r < nrow ? r : nrow - 1)] * (uint32_t)nch;
         }
-        for (int c = lane; c < nch + ((32 - (nch & 31)) & 31); c += 32) {
-            if (c < nch) {
-                float4 v[kRPI];
+        const float4* x4 = reinterpret_cast<const float4*>(p.x);
+        for (int c = lane; c < nch; c += 32) {
+            float4 v[kRPI];
 #pragma unroll
-                for (int r = 0; r < kRPI; ++r)
-                    v[r] = (b + r < e1) ? __ldg(rows[r] + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                const float4 q = q4[c];
+            for (int r = 0; r < kRPI; ++r) v[r] = __ldg(x4 + off[r] + c);  // rows >= nrow repeat the last
+            const float4 q = q4[c];
 #pragma unroll
-                for (int r = 0; r < kRPI; ++r) {
-                    acc[r] = fmaf(q.x, v[r].x, acc[r]);
-                    acc[r] = fmaf(q.y, v[r].y, acc[r]);
-                    acc[r] = fmaf(q.z, v[r].z, acc[r]);
-                    acc[r] = fmaf(q.w, v[r].w, acc[r]);
-                }
+            for (int r = 0; r < kRPI; ++r) {
+                acc[r] = fmaf(q.x, v[r].x, acc[r]);
+                acc[r] = fmaf(q.y, v[r].y, acc[r]);
+                acc[r] = fmaf(q.z, v[r].z, acc[r]);
+                acc[r] = fmaf(q.w, v[r].w, acc[r]);
             }
         }
         // tree over the 32 lane sums, level h = 16, 8, 4 halving the rows a lane keeps (a
@@ -267,8 +265,10 @@ __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, Q
     int e = 0;
     bool stop = false;
     for (;;) {
-        int e2 = e;
-        while (e2 < nbuf && w.srep[e2] == next_check) ++e2;
+        // survivors are in repetition order: the run of next_check ends at the first entry > it
+        int lo = e, hi = nbuf;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.srep[mid] <= next_check) lo = mid + 1; else hi = mid; }
+        const int e2 = lo;
         if (e2 > e) merge_range(p, w, st, e, e2, qi, lane);
         e = e2;
         if (next_check >= complete || next_check >= nr) break;
@@ -332,7 +332,7 @@ __device__ __forceinline__ void to_bitmap_mode(const QueryParams& p, const WarpS
 }
 
 template <int EPL>
-__global__ void __launch_bounds__(128) k_query(QueryParams p) {
+__global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t slot_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                 int nbuf = 0, next_check = 0, r_stop = -1;
                 // scan the chunk's emitted positions in (rep, position) order, kU per lane per step;
                 // each 16-byte table entry carries the id and its sketch word for this repetition
+                int rl = 0;  // this lane's current repetition (positions only increase)
                 for (uint32_t g0 = 0; g0 < total && !stopped; g0 += 32 * kU) {
                     uint32_t idv[kU];
                     int rv[kU];
@@ -446,8 +447,8 @@ __global__ void __launch_bounds__(128) k_query(QueryParams p) {
                         rv[u] = 0;
                         idv[u] = 0;
                         if (g < total) {
-                            int r = 0;
-                            while (r + 1 < nr && w.beg[r + 1] <= g) ++r;
+                            while (rl + 1 < nr && w.beg[rl + 1] <= g) ++rl;
+                            const int r = rl;
                             const uint32_t o = g - w.beg[r];
                             const uint32_t lenA = w.lo_old[r] - w.lo_new[r];
                             const uint32_t pos = (o < lenA) ? w.lo_new[r] + o : w.hi_old[r] + (o - lenA);
