@@ -392,7 +392,11 @@ def main():
                          "filtered_per_q": float(np.mean(stats["filtered"])),
                          "dups_per_q": float(np.mean(stats["dups"])),
                          "i_stop_mean": float(np.mean(stats["i_stop"])),
-                         "j_stop_mean": float(np.mean(stats["j_stop"]))},
+                         "j_stop_mean": float(np.mean(stats["j_stop"])),
+                         "j_stop_p50_p90_p99_max": [float(np.percentile(stats["j_stop"], q)) for q in (50, 90, 99, 100)],
+                         "evaluated_p99_max": [float(np.percentile(stats["evaluated"], 99)),
+                                               float(np.max(stats["evaluated"]))],
+                         "bitmap_mode_queries": int(np.sum((stats["flags"] & 8) != 0))},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -62,6 +62,7 @@ struct QueryParams {
     float* out_sims;
     pfg_query_stats* stats;
     uint32_t* trace_ids;
+    unsigned long long* prof;   // optional per-phase cycle counters (PFG_PHASE_PROF=1), [6]
 };
 
 struct WarpSmem {
@@ -261,7 +262,9 @@ __device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSme
 // survivors are merged (Alg. 1 line 8).  Returns true when the query stops (r_stop set).
 __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, QState& st, int& nbuf, int& next_check,
                                       int complete, int nr, int c0, int i, int64_t qi, int& r_stop, int lane) {
+    const long long td0 = p.prof ? clock64() : 0;
     compute_sims(p, w, 0, nbuf, lane);
+    if (p.prof && lane == 0) atomicAdd(p.prof + 5, (unsigned long long)(clock64() - td0));
     int e = 0;
     bool stop = false;
     for (;;) {
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 }
                 // query codes of the chunk's repetitions (first level only): precomputed for
                 // repetitions < qc_n, otherwise hashed here (FHT-CP, warp-cooperative)
+                const long long th0 = p.prof ? clock64() : 0;
                 if (i == p.K) {
                     for (int r = 0; r < nr; ++r) {
                         if (c0 + r < p.qc_n) {
@@ -393,6 +397,8 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                     }
                     __syncwarp();
                 }
+                if (p.prof && lane == 0) atomicAdd(p.prof + 4, (unsigned long long)(clock64() - th0));
+                long long tp0 = p.prof ? clock64() : 0;
                 // prefix match ranges [a_i, b_i): task t < nr -> a of rep t, t >= nr -> b of rep t-nr
                 for (int task = lane; task < 2 * nr; task += 32) {
                     const int r = task < nr ? task : task - nr;
@@ -431,6 +437,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 if (lane == 0) w.beg[0] = 0;
                 __syncwarp();
                 const uint32_t total = w.beg[nr];
+                if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 0, (unsigned long long)(t - tp0)); tp0 = t; }
 
                 int nbuf = 0, next_check = 0, r_stop = -1;
                 // scan the chunk's emitted positions in (rep, position) order, kU per lane per step;
@@ -463,6 +470,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                             }
                         }
                     }
+                    if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 1, (unsigned long long)(t - tp0)); tp0 = t; }
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
                         const uint32_t g = g0 + u * 32 + lane;
@@ -492,12 +500,14 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                     }
                     if (!st.bitmap_mode && st.hcount > kHMax) to_bitmap_mode(p, w, st, bm, claims, lane);
                     const uint32_t done_pos = min(total, g0 + 32u * kU);
+                    if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 2, (unsigned long long)(t - tp0)); tp0 = t; }
                     if (nbuf > kSB - 32 * kU || done_pos == total) {
                         int complete = nr;
                         if (done_pos < total) { complete = 0; while (complete < nr && w.beg[complete + 1] <= done_pos) ++complete; }
                         if (drain(p, w, st, nbuf, next_check, complete, nr, c0, i, qi, r_stop, lane)) {
                             stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
                         }
+                        if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 3, (unsigned long long)(t - tp0)); tp0 = t; }
                     }
                 }
                 if (total == 0) {

@@ -7,6 +7,8 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -901,6 +903,14 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.thr = thr->as<float>(); p.taub = taub->as<float>(); p.work = I->work.as<unsigned long long>();
     p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
     p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
+    // developer instrumentation: PFG_PHASE_PROF=1 prints per-phase warp cycles of each search to stderr
+    static const bool phase_prof = getenv("PFG_PHASE_PROF") && getenv("PFG_PHASE_PROF")[0] == '1';
+    DBuf profb;
+    if (phase_prof) {
+        PFG_TRY(profb.alloc(8 * 8, "phase profile"));
+        PFG_CUDA(cudaMemsetAsync(profb.p, 0, 64, st));
+        p.prof = profb.as<unsigned long long>();
+    }
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[1], st));
     switch (epl) {
         case 1: PFG_TRY(launch_query_t<1>(p, (int)blocks, smem, st)); break;
@@ -919,6 +929,14 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     if (s.trace_cap > 0 && !trace_dev)
         PFG_CUDA(cudaMemcpyAsync(s.trace_ids, d_trace, (size_t)nq * s.trace_cap * 4, cudaMemcpyDeviceToHost, st));
     PFG_CUDA(cudaStreamSynchronize(st));
+    if (phase_prof) {
+        unsigned long long h[8] = {0};
+        PFG_CUDA(cudaMemcpy(h, profb.p, 64, cudaMemcpyDeviceToHost));
+        const double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]);
+        fprintf(stderr, "[pfg phase] Mcycles: bounds %.1f (%.0f%%) scan-load %.1f (%.0f%%) claim %.1f (%.0f%%) drain %.1f (%.0f%%, sims %.1f) lazy-hash %.1f (%.0f%%)\n",
+                h[0] / 1e6, 100 * h[0] / tot, h[1] / 1e6, 100 * h[1] / tot, h[2] / 1e6, 100 * h[2] / tot,
+                h[3] / 1e6, 100 * h[3] / tot, h[5] / 1e6, h[4] / 1e6, 100 * h[4] / tot);
+    }
     I->last_launches = I->launches;
     if (s.timing) {
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[0], I->ev[0], I->ev[1]));
