@@ -124,17 +124,25 @@ def recall_of(ids_t, truth_kth, xn, qn, k):
     return float(hit.float().sum() / (k * ids_t.shape[0]))
 
 
-def alg_bytes(stats, d, M, k, use_filter=True):
-    """algorithmic bytes of the query kernel (DESIGN.md "Roofline"): per query
-    8 B per retrieved table entry + 8 B per sketch word read + 4d B per evaluated row
-    + 4 B per bitmap claim (evaluated + dups) + 8 B per bound-search probe + query row,
-    sketches and outputs."""
+def alg_bytes(stats, d, M, k):
+    """algorithmic bytes of the query kernel (DESIGN.md §5): per query
+    B_q = 16 E + 4d S + 8 P + 4d + 8M + 12k  (E retrieved 16-byte table entries, S evaluated rows,
+    P binary-search probes; plus the query row, its sketches and the outputs)"""
     em = stats["emitted"].astype(np.float64)
     ev = stats["evaluated"].astype(np.float64)
-    du = stats["dups"].astype(np.float64)
     pr = stats["probes"].astype(np.float64)
-    b = 8 * em + (8 * em if use_filter else 0) + 4 * d * ev + 4 * (ev + du) + 8 * pr + 4 * d + 8 * M + 12 * k
+    b = 16 * em + 4 * d * ev + 8 * pr + 4 * d + 8 * M + 12 * k
     return float(b.sum())
+
+
+def profiled_traffic():
+    """DRAM bytes per k_query launch from the committed ncu --set full summary, if present"""
+    path = os.path.join(ROOT, "profiles", "k_query_ncu.json")
+    try:
+        j = json.load(open(path))
+        return float(j["dram_bytes_read"] + j["dram_bytes_write"]), j.get("source")
+    except Exception:
+        return None, None
 
 
 # ---------------------------------------------------------------------------- reference arm
@@ -356,6 +364,7 @@ def main():
         ab = alg_bytes(stats, d, info["sketch_words"], k)
         kern_s = statistics.mean(kern_ms) / 1e3
         achieved = ab / kern_s / 1e9
+        traffic, traffic_src = profiled_traffic()
         cpu = None
         if not args.no_cpu_baseline:
             try:
@@ -383,7 +392,7 @@ def main():
             "recall": rec,
             "build_s": build_s,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "k_query", "kernel_ms": statistics.mean(kern_ms),
                          "prep_ms": statistics.mean(prep_ms), "alg_bytes_per_query": ab / nq,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
