@@ -271,12 +271,9 @@ def main():
     # ground truth (global): shard-local exact top-k, gathered and merged like the search
     t_ids, t_kth, xn, qn = ground_truth(data, q, k)
     if world > 1:
-        gi = torch.empty((world, nq, k), dtype=torch.int64, device=dev)
-        gs = torch.empty((world, nq, k), dtype=torch.float32, device=dev)
+        from paper_1906_12211_b200.sharded import gather_merge
         sims_local = torch.einsum("qd,qkd->qk", qn, xn[t_ids])
-        dist.all_gather_into_tensor(gi, t_ids + lo)
-        dist.all_gather_into_tensor(gs, sims_local.contiguous())
-        _, ms = pfg.merge_topk(gi, gs)
+        _, ms = gather_merge(t_ids + lo, sims_local.contiguous())
         t_kth = ms[:, -1].contiguous()
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)

@@ -22,6 +22,20 @@ def shard_range(n: int, world: int, rank: int):
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def gather_merge(ids, sims, group=None, merge=None):
+    """all-gather the local [nq, k] lists of every rank (NCCL in production; any backend works)
+    and merge them (default: the library's k_merge_topk).  Returns (ids, sims) [nq, k]."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return ids, sims
+    nq, k = ids.shape
+    g_ids = torch.empty((world * nq, k), dtype=ids.dtype, device=ids.device)
+    g_sims = torch.empty((world * nq, k), dtype=sims.dtype, device=sims.device)
+    dist.all_gather_into_tensor(g_ids, ids.contiguous(), group=group)
+    dist.all_gather_into_tensor(g_sims, sims.contiguous(), group=group)
+    return (merge or merge_topk)(g_ids.view(world, nq, k), g_sims.view(world, nq, k))
+
+
 class ShardedIndex:
     """Build this rank's shard: `local_data` are rows [row0, row0 + len) of the global dataset."""
 
@@ -33,13 +47,5 @@ class ShardedIndex:
     def search(self, queries, k: int, recall: float, **sopts):
         """-> merged (ids [nq,k], sims [nq,k]) on every rank (CUDA tensors)"""
         res = self.index.search(queries, k, recall, **sopts)
-        ids, sims = res[0], res[1]
-        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
-        if world == 1:
-            return (ids, sims) + tuple(res[2:])
-        g_ids = torch.empty((world,) + tuple(ids.shape), dtype=ids.dtype, device=ids.device)
-        g_sims = torch.empty((world,) + tuple(sims.shape), dtype=sims.dtype, device=sims.device)
-        dist.all_gather_into_tensor(g_ids, ids, group=self.group)
-        dist.all_gather_into_tensor(g_sims, sims, group=self.group)
-        m_ids, m_sims = merge_topk(g_ids, g_sims)
+        m_ids, m_sims = gather_merge(res[0], res[1], self.group)
         return (m_ids, m_sims) + tuple(res[2:])
