@@ -65,60 +65,46 @@ struct QueryParams {
     unsigned long long* prof;   // optional per-phase cycle counters (PFG_PHASE_PROF=1), [6]
 };
 
+// Per-warp shared memory: a fixed-size part at compile-time offsets, then the query row, its
+// sketches and the two top-k buffers (sizes known at launch).
+struct WarpFixed {
+    uint32_t hs[kHC];          // hash set of evaluated ids
+    uint32_t sid[kSB];         // survivors awaiting their similarity (repetition order)
+    float ssim[kSB];
+    uint64_t cand[32];         // sorted merge batch
+    uint32_t beg[kMaxR + 4];   // exclusive prefix of per-repetition emitted counts
+    uint32_t lo_new[kMaxR];
+    uint32_t lo_old[kMaxR];
+    uint32_t hi_old[kMaxR];
+    uint32_t qc[kMaxR];        // query codes of the chunk
+    uint32_t bnd[2 * kMaxR];   // a / b bounds
+    uint32_t fcnt[kMaxR];      // filtered per repetition
+    uint32_t dcnt[kMaxR];      // duplicates per repetition
+    uint8_t srep[kSB];
+};
+
 struct WarpSmem {
+    WarpFixed* f;
     float* qrow;       // [dpad]
     uint64_t* qsk;     // [M]
     uint64_t* T0;      // [kt]
     uint64_t* T1;      // [kt]
-    uint64_t* cand;    // [32]   sorted merge batch
-    uint32_t* hs;      // [kHC]  hash set of evaluated ids
-    uint32_t* sid;     // [kSB]
-    float* ssim;       // [kSB]
-    uint8_t* srep;     // [kSB]
-    uint32_t* beg;     // [kMaxR + 1]
-    uint32_t* lo_new;  // [kMaxR]
-    uint32_t* lo_old;
-    uint32_t* hi_old;
-    uint32_t* qc;      // [kMaxR]
-    uint32_t* bnd;     // [2 * kMaxR]
-    uint32_t* fcnt;    // [kMaxR]
-    uint32_t* dcnt;    // [kMaxR]
 };
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 
 __host__ __device__ inline int warp_smem_bytes(int dpad, int M, int kt) {
-    int b = 0;
-    b += align16(dpad * 4);
-    b += align16(M * 8);
-    b += 2 * align16(kt * 8);
-    b += 32 * 8;
-    b += kHC * 4;
-    b += kSB * 4 + kSB * 4 + align16(kSB);
-    b += align16((kMaxR + 1) * 4) + 3 * kMaxR * 4 + kMaxR * 4 + 2 * kMaxR * 4 + 2 * kMaxR * 4;
-    return align16(b);
+    return align16((int)sizeof(WarpFixed)) + align16(dpad * 4) + align16(M * 8) + 2 * align16(kt * 8);
 }
 
 __device__ inline WarpSmem carve(unsigned char* base, const QueryParams& p) {
     WarpSmem w;
     unsigned char* q = base;
+    w.f = (WarpFixed*)q; q += align16((int)sizeof(WarpFixed));
     w.qrow = (float*)q; q += align16(p.dpad * 4);
     w.qsk = (uint64_t*)q; q += align16(p.M * 8);
     w.T0 = (uint64_t*)q; q += align16(p.kt * 8);
-    w.T1 = (uint64_t*)q; q += align16(p.kt * 8);
-    w.cand = (uint64_t*)q; q += 32 * 8;
-    w.hs = (uint32_t*)q; q += kHC * 4;
-    w.sid = (uint32_t*)q; q += kSB * 4;
-    w.ssim = (float*)q; q += kSB * 4;
-    w.srep = (uint8_t*)q; q += align16(kSB);
-    w.beg = (uint32_t*)q; q += align16((kMaxR + 1) * 4);
-    w.lo_new = (uint32_t*)q; q += kMaxR * 4;
-    w.lo_old = (uint32_t*)q; q += kMaxR * 4;
-    w.hi_old = (uint32_t*)q; q += kMaxR * 4;
-    w.qc = (uint32_t*)q; q += kMaxR * 4;
-    w.bnd = (uint32_t*)q; q += 2 * kMaxR * 4;
-    w.fcnt = (uint32_t*)q; q += kMaxR * 4;
-    w.dcnt = (uint32_t*)q; q += kMaxR * 4;
+    w.T1 = (uint64_t*)q;
     return w;
 }
 
@@ -162,8 +148,8 @@ __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem
         const int idx = b0 + lane;
         uint64_t key = 0;
         if (idx < e2) {
-            const uint32_t id = w.sid[idx];
-            key = make_key(w.ssim[idx], id);
+            const uint32_t id = w.f->sid[idx];
+            key = make_key(w.f->ssim[idx], id);
             if (p.trace_cap > 0) {
                 const uint32_t pos = st.nE + (uint32_t)(idx - e);
                 if (pos < (uint32_t)p.trace_cap) p.trace_ids[qi * p.trace_cap + pos] = id;
@@ -175,7 +161,7 @@ __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem
         if (vm) {
             key = warp_sort_desc(key, lane);
             const int nc = __popc(vm);
-            w.cand[lane] = key;
+            w.f->cand[lane] = key;
             __syncwarp();
             if (lane < nc) {
                 int lo = 0, hi = st.tn;
@@ -186,7 +172,7 @@ __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem
             for (int t = lane; t < st.tn; t += 32) {
                 const uint64_t tv = st.T[t];
                 int lo = 0, hi = nc;
-                while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.cand[mid] > tv) lo = mid + 1; else hi = mid; }
+                while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.f->cand[mid] > tv) lo = mid + 1; else hi = mid; }
                 const int dst = t + lo;
                 if (dst < p.k_eff) st.Tn[dst] = tv;
             }
@@ -218,7 +204,7 @@ __device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSme
 #pragma unroll
         for (int r = 0; r < kRPI; ++r) {
             acc[r] = 0.0f;
-            off[r] = w.sid[b + (r < nrow ? r : nrow - 1)] * (uint32_t)nch;
+            off[r] = w.f->sid[b + (r < nrow ? r : nrow - 1)] * (uint32_t)nch;
         }
         const float4* x4 = reinterpret_cast<const float4*>(p.x);
         for (int c = lane; c < nch; c += 32) {
@@ -252,7 +238,7 @@ __device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSme
         t1 = t1 + __shfl_xor_sync(kFull, t1, 2);
         t1 = t1 + __shfl_xor_sync(kFull, t1, 1);
         const int rr = lane >> 2;
-        if ((lane & 3) == 0 && b + rr < e1) w.ssim[b + rr] = t1;
+        if ((lane & 3) == 0 && b + rr < e1) w.f->ssim[b + rr] = t1;
     }
     __syncwarp();
 }
@@ -270,7 +256,7 @@ __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, Q
     for (;;) {
         // survivors are in repetition order: the run of next_check ends at the first entry > it
         int lo = e, hi = nbuf;
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.srep[mid] <= next_check) lo = mid + 1; else hi = mid; }
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.f->srep[mid] <= next_check) lo = mid + 1; else hi = mid; }
         const int e2 = lo;
         if (e2 > e) merge_range(p, w, st, e, e2, qi, lane);
         e = e2;
@@ -297,7 +283,7 @@ __device__ __forceinline__ bool claim(const WarpSmem& w, const QState& st, uint3
     }
     uint32_t h = hs_slot(id);
     for (;;) {
-        const uint32_t old = atomicCAS(&w.hs[h], kEmpty, id);
+        const uint32_t old = atomicCAS(&w.f->hs[h], kEmpty, id);
         if (old == kEmpty) return true;
         if (old == id) return false;
         h = (h + 1) & (kHC - 1);
@@ -309,7 +295,7 @@ __device__ __forceinline__ bool evaluated(const WarpSmem& w, const QState& st, c
     if (st.bitmap_mode) return (__ldcg(bm + (id >> 5)) >> (id & 31)) & 1u;
     uint32_t h = hs_slot(id);
     for (;;) {
-        const uint32_t v = w.hs[h];
+        const uint32_t v = w.f->hs[h];
         if (v == kEmpty) return false;
         if (v == id) return true;
         h = (h + 1) & (kHC - 1);
@@ -320,7 +306,7 @@ __device__ __forceinline__ bool evaluated(const WarpSmem& w, const QState& st, c
 __device__ __forceinline__ void to_bitmap_mode(const QueryParams& p, const WarpSmem& w, QState& st, uint32_t* bm,
                                                uint32_t* claims, int lane) {
     for (int h0 = 0; h0 < kHC; h0 += 32) {
-        const uint32_t v = w.hs[h0 + lane];
+        const uint32_t v = w.f->hs[h0 + lane];
         const bool has = v != kEmpty;
         if (has) atomicOr(bm + (v >> 5), 1u << (v & 31));
         const uint32_t m = __ballot_sync(kFull, has);
@@ -359,7 +345,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
         }
         for (int t = lane; t < p.dpad; t += 32) w.qrow[t] = p.qx[qi * p.dpad + t];
         for (int t = lane; t < p.M; t += 32) w.qsk[t] = p.qsk[qi * p.M + t];
-        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(w.hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(w.f->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
         __syncwarp();
 
         QState st;
@@ -385,7 +371,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 if (i == p.K) {
                     for (int r = 0; r < nr; ++r) {
                         if (c0 + r < p.qc_n) {
-                            if (lane == 0) w.qc[r] = __ldg(p.qcodes + qi * p.qc_ld + c0 + r);
+                            if (lane == 0) w.f->qc[r] = __ldg(p.qcodes + qi * p.qc_ld + c0 + r);
                             continue;
                         }
                         uint64_t full = 0;
@@ -393,7 +379,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                             const int64_t f = (int64_t)(c0 + r) * p.c + t;
                             full = (full << p.ell) | fhtcp_code_warp<EPL>(w.qrow, p.d, p.dp, p.ell, p.sg + f * 3 * W, lane);
                         }
-                        if (lane == 0) w.qc[r] = (uint32_t)(full >> (p.c * p.ell - p.K));
+                        if (lane == 0) w.f->qc[r] = (uint32_t)(full >> (p.c * p.ell - p.K));
                     }
                     __syncwarp();
                 }
@@ -404,28 +390,28 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                     const int r = task < nr ? task : task - nr;
                     const int j = c0 + r;
                     uint32_t qc;
-                    if (i == p.K) qc = w.qc[r];
+                    if (i == p.K) qc = w.f->qc[r];
                     else qc = cur[j].x;
                     const uint64_t qp = (uint64_t)qc >> (p.K - i);
                     const uint64_t x = (task < nr ? qp : qp + 1) << (p.K - i);
-                    w.bnd[task] = rep_lower_bound(p, j, x, st.probes);
-                    if (task < nr) w.qc[r] = qc;
+                    w.f->bnd[task] = rep_lower_bound(p, j, x, st.probes);
+                    if (task < nr) w.f->qc[r] = qc;
                 }
                 __syncwarp();
                 uint32_t em = 0;
                 if (lane < nr) {
                     const int j = c0 + lane;
-                    const uint32_t a = w.bnd[lane], b = w.bnd[nr + lane];
+                    const uint32_t a = w.f->bnd[lane], b = w.f->bnd[nr + lane];
                     uint32_t elo, ehi;
                     if (i == p.K) { elo = ehi = a; } else { const uint4 cu = cur[j]; elo = cu.y; ehi = cu.z; }
                     const uint32_t B = (uint32_t)p.B;
                     uint32_t nelo = elo, nehi = ehi;
                     if (a < elo) { const uint32_t s = (elo - a + B - 1) / B; nelo = (s * B >= elo) ? 0u : elo - s * B; }
                     if (b > ehi) { const uint64_t s = (b - ehi + B - 1) / B; const uint64_t v = ehi + s * B; nehi = (uint32_t)(v > (uint64_t)p.n ? p.n : v); }
-                    w.lo_new[lane] = nelo; w.lo_old[lane] = elo; w.hi_old[lane] = ehi;
-                    w.fcnt[lane] = 0; w.dcnt[lane] = 0;
+                    w.f->lo_new[lane] = nelo; w.f->lo_old[lane] = elo; w.f->hi_old[lane] = ehi;
+                    w.f->fcnt[lane] = 0; w.f->dcnt[lane] = 0;
                     em = (elo - nelo) + (nehi - ehi);
-                    cur[j] = make_uint4(w.qc[lane], nelo, nehi, 0u);
+                    cur[j] = make_uint4(w.f->qc[lane], nelo, nehi, 0u);
                 }
                 uint32_t incl = em;
 #pragma unroll
@@ -433,10 +419,10 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                     const uint32_t o = __shfl_up_sync(kFull, incl, off);
                     if (lane >= off) incl += o;
                 }
-                if (lane < nr) w.beg[lane + 1] = incl;
-                if (lane == 0) w.beg[0] = 0;
+                if (lane < nr) w.f->beg[lane + 1] = incl;
+                if (lane == 0) w.f->beg[0] = 0;
                 __syncwarp();
-                const uint32_t total = w.beg[nr];
+                const uint32_t total = w.f->beg[nr];
                 if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 0, (unsigned long long)(t - tp0)); tp0 = t; }
 
                 int nbuf = 0, next_check = 0, r_stop = -1;
@@ -454,11 +440,11 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                         rv[u] = 0;
                         idv[u] = 0;
                         if (g < total) {
-                            while (rl + 1 < nr && w.beg[rl + 1] <= g) ++rl;
+                            while (rl + 1 < nr && w.f->beg[rl + 1] <= g) ++rl;
                             const int r = rl;
-                            const uint32_t o = g - w.beg[r];
-                            const uint32_t lenA = w.lo_old[r] - w.lo_new[r];
-                            const uint32_t pos = (o < lenA) ? w.lo_new[r] + o : w.hi_old[r] + (o - lenA);
+                            const uint32_t o = g - w.f->beg[r];
+                            const uint32_t lenA = w.f->lo_old[r] - w.f->lo_new[r];
+                            const uint32_t pos = (o < lenA) ? w.f->lo_new[r] + o : w.f->hi_old[r] + (o - lenA);
                             const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.tab + (int64_t)(c0 + r) * p.n + pos));
                             idv[u] = e.x;
                             rv[u] = r;
@@ -474,20 +460,20 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
                         const uint32_t g = g0 + u * 32 + lane;
-                        if (g < total && !pass[u]) atomicAdd(&w.fcnt[rv[u]], 1u);
+                        if (g < total && !pass[u]) atomicAdd(&w.f->fcnt[rv[u]], 1u);
                         // claims in (rep, position) order: lanes in order within u, u in order
                         const uint32_t pm = __ballot_sync(kFull, pass[u]);
                         bool fresh = false;
                         if (pass[u]) {
                             const uint32_t grp = __match_any_sync(pm, idv[u]);
                             if ((int)(__ffs(grp) - 1) == lane) fresh = claim(w, st, bm, idv[u]);
-                            if (!fresh) atomicAdd(&w.dcnt[rv[u]], 1u);
+                            if (!fresh) atomicAdd(&w.f->dcnt[rv[u]], 1u);
                         }
                         const uint32_t fm = __ballot_sync(kFull, fresh);
                         if (fresh) {
                             const int rank = __popc(fm & lanemask_lt());
-                            w.sid[nbuf + rank] = idv[u];
-                            w.srep[nbuf + rank] = (uint8_t)rv[u];
+                            w.f->sid[nbuf + rank] = idv[u];
+                            w.f->srep[nbuf + rank] = (uint8_t)rv[u];
                             if (st.bitmap_mode) {
                                 const uint32_t cn = st.claims_n + rank;
                                 if (cn < (uint32_t)p.claim_cap) claims[cn] = idv[u];
@@ -503,7 +489,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                     if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 2, (unsigned long long)(t - tp0)); tp0 = t; }
                     if (nbuf > kSB - 32 * kU || done_pos == total) {
                         int complete = nr;
-                        if (done_pos < total) { complete = 0; while (complete < nr && w.beg[complete + 1] <= done_pos) ++complete; }
+                        if (done_pos < total) { complete = 0; while (complete < nr && w.f->beg[complete + 1] <= done_pos) ++complete; }
                         if (drain(p, w, st, nbuf, next_check, complete, nr, c0, i, qi, r_stop, lane)) {
                             stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
                         }
@@ -519,9 +505,9 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 const int rmax = stopped ? r_stop : nr - 1;
                 uint32_t e_acc = 0, f_acc = 0, d_acc = 0;
                 for (int r = 0; r <= rmax; ++r) {
-                    e_acc += w.beg[r + 1] - w.beg[r];
-                    f_acc += w.fcnt[r];
-                    d_acc += w.dcnt[r];
+                    e_acc += w.f->beg[r + 1] - w.f->beg[r];
+                    f_acc += w.f->fcnt[r];
+                    d_acc += w.f->dcnt[r];
                 }
                 st.emitted += e_acc; st.filtered += f_acc; st.dups += d_acc;
                 __syncwarp();
@@ -537,7 +523,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 const int64_t id = g0 + lane;
                 const bool fresh = id < p.n && !evaluated(w, st, bm, (uint32_t)id);
                 const uint32_t fm = __ballot_sync(kFull, fresh);
-                if (fresh) w.sid[ns + __popc(fm & lanemask_lt())] = (uint32_t)id;
+                if (fresh) w.f->sid[ns + __popc(fm & lanemask_lt())] = (uint32_t)id;
                 ns += __popc(fm);
                 __syncwarp();
                 if (ns > kSB - 32 || g0 + 32 >= p.n) {
