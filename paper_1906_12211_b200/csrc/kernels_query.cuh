@@ -385,29 +385,60 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 }
                 if (p.prof && lane == 0) atomicAdd(p.prof + 4, (unsigned long long)(clock64() - th0));
                 long long tp0 = p.prof ? clock64() : 0;
-                // prefix match ranges [a_i, b_i): task t < nr -> a of rep t, t >= nr -> b of rep t-nr
+                // emitted-range widening (R-12), task t < nr: left side of rep t, t >= nr: right side.
+                // First level: the match range [a_K, b_K) by binary search in the 13-bit bucket (the
+                // range starts empty at lower_bound(q_j)); deeper levels: the segment loop of the
+                // paper (extend by B while the entry just outside shares the top i bits), which
+                // usually reads one boundary entry per side.
                 for (int task = lane; task < 2 * nr; task += 32) {
-                    const int r = task < nr ? task : task - nr;
+                    const bool left = task < nr;
+                    const int r = left ? task : task - nr;
                     const int j = c0 + r;
-                    uint32_t qc;
-                    if (i == p.K) qc = w.f->qc[r];
-                    else qc = cur[j].x;
-                    const uint64_t qp = (uint64_t)qc >> (p.K - i);
-                    const uint64_t x = (task < nr ? qp : qp + 1) << (p.K - i);
-                    w.f->bnd[task] = rep_lower_bound(p, j, x, st.probes);
-                    if (task < nr) w.f->qc[r] = qc;
+                    if (i == p.K) {
+                        const uint32_t qc = w.f->qc[r];
+                        w.f->bnd[task] = rep_lower_bound(p, j, left ? (uint64_t)qc : (uint64_t)qc + 1, st.probes);
+                    } else {
+                        const uint4 cu = cur[j];
+                        const uint32_t qp = cu.x >> (p.K - i);
+                        const Entry* tj = p.tab + (int64_t)j * p.n;
+                        const uint32_t B = (uint32_t)p.B;
+                        if (left) {
+                            uint32_t e = cu.y;
+                            while (e > 0) {
+                                ++st.probes;
+                                if ((entry_code(tj + e - 1) >> (p.K - i)) != qp) break;
+                                e = e > B ? e - B : 0u;
+                            }
+                            w.f->bnd[task] = e;
+                        } else {
+                            uint32_t e = cu.z;
+                            while (e < (uint32_t)p.n) {
+                                ++st.probes;
+                                if ((entry_code(tj + e) >> (p.K - i)) != qp) break;
+                                e = (uint64_t)e + B < (uint64_t)p.n ? e + B : (uint32_t)p.n;
+                            }
+                            w.f->bnd[task] = e;
+                        }
+                        if (left) w.f->qc[r] = cu.x;
+                    }
                 }
                 __syncwarp();
                 uint32_t em = 0;
                 if (lane < nr) {
                     const int j = c0 + lane;
-                    const uint32_t a = w.f->bnd[lane], b = w.f->bnd[nr + lane];
-                    uint32_t elo, ehi;
-                    if (i == p.K) { elo = ehi = a; } else { const uint4 cu = cur[j]; elo = cu.y; ehi = cu.z; }
-                    const uint32_t B = (uint32_t)p.B;
-                    uint32_t nelo = elo, nehi = ehi;
-                    if (a < elo) { const uint32_t s = (elo - a + B - 1) / B; nelo = (s * B >= elo) ? 0u : elo - s * B; }
-                    if (b > ehi) { const uint64_t s = (b - ehi + B - 1) / B; const uint64_t v = ehi + s * B; nehi = (uint32_t)(v > (uint64_t)p.n ? p.n : v); }
+                    uint32_t elo, ehi, nelo, nehi;
+                    if (i == p.K) {
+                        // closed form of the segment loop from [a, a): ehi' = a + B*ceil((b - a)/B)
+                        const uint32_t a = w.f->bnd[lane], b = w.f->bnd[nr + lane];
+                        const uint32_t B = (uint32_t)p.B;
+                        elo = ehi = nelo = a;
+                        const uint64_t v = (uint64_t)a + (uint64_t)((b - a + B - 1) / B) * B;
+                        nehi = (uint32_t)(v > (uint64_t)p.n ? p.n : v);
+                    } else {
+                        const uint4 cu = cur[j];
+                        elo = cu.y; ehi = cu.z;
+                        nelo = w.f->bnd[lane]; nehi = w.f->bnd[nr + lane];
+                    }
                     w.f->lo_new[lane] = nelo; w.f->lo_old[lane] = elo; w.f->hi_old[lane] = ehi;
                     w.f->fcnt[lane] = 0; w.f->dcnt[lane] = 0;
                     em = (elo - nelo) + (nehi - ehi);
