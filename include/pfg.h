@@ -90,6 +90,10 @@ typedef struct {
     int32_t timing;           /* [0] 1: record CUDA events around the phases of this call on `stream`
                                  (read back with pfg_last_timing) */
     uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
+    int32_t engine;           /* [0] 0 = bulk-synchronous rounds (one chunk of every active query per round,
+                                 stragglers finished by the fused kernel); 1 = fused kernel only.
+                                 Results are identical. */
+    int32_t reserved1;
 } pfg_search_opts;
 
 /* per-query counters (optional output of pfg_search) */

@@ -37,6 +37,38 @@ struct __align__(16) Entry {
     uint64_t sk;
 };
 
+// Per-query search state in global memory, shared by the round engine (kernels_rounds.cuh) and
+// the fused kernel (which can resume a query from it).
+struct RoundState {
+    int32_t* lvl;       // [nq] next level i to process (K..1); 0 = only the i = 0 scan remains
+    int32_t* c0;        // [nq] next chunk start at that level
+    int32_t* flags;     // [nq] bit0 done, bit1 hand off to the fused kernel
+    int32_t* tn;        // [nq] entries in the top list
+    uint32_t* cnt;      // [nq][8] emitted, filtered, dups, evaluated, probes
+    uint64_t* T;        // [nq][kt] top list keys
+    uint32_t* E;        // [nq][Ecap] evaluated ids in evaluation order
+    uint4* pend;        // [nq][kMaxR] cursors of the chunk in flight (committed by k_merge)
+    uint32_t* cand;     // [nq][Ccap] candidate / survivor ids of the chunk in flight
+    uint8_t* crep;      // [nq][Ccap] their repetition within the chunk
+    uint32_t* ncand;    // [nq]
+    uint32_t* repcnt;   // [nq][kMaxR][3] emitted, filtered, dups per repetition of the chunk
+    uint32_t* pool_id;  // survivor pool of the round: ids, owning query, rep, similarity
+    uint32_t* pool_q;
+    uint8_t* pool_rep;
+    float* pool_sim;
+    uint32_t* pool_top; // [1]
+    uint32_t* poff;     // [nq] first pool entry of the query
+    uint32_t* pn;       // [nq] pool entries of the query
+    uint32_t* active;   // [nq] queries of this round
+    uint32_t* next;     // [nq] queries of the next round
+    uint32_t* nnext;    // [1]
+    uint32_t* fused;    // [nq] queries handed to the fused kernel
+    uint32_t* nfused;   // [1]
+    int Ecap, Ccap;
+    uint32_t pool_cap;
+};
+constexpr int kCnt = 8;
+
 struct QueryParams {
     int64_t n, nq, bm_words, id_offset;
     int d, dpad, K, L, M, B, R, k, k_eff, per_round, use_filter, c, ell, dp, lazy, claim_cap, trace_cap;
@@ -63,6 +95,9 @@ struct QueryParams {
     pfg_query_stats* stats;
     uint32_t* trace_ids;
     unsigned long long* prof;   // optional per-phase cycle counters (PFG_PHASE_PROF=1), [6]
+    const uint32_t* qlist;      // fused kernel: query indices to process (NULL = 0..nq-1)
+    int resume;                 // fused kernel: continue each query from rs
+    RoundState rs;
 };
 
 // Per-warp shared memory: a fixed-size part at compile-time offsets, then the query row, its
@@ -326,7 +361,6 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t slot_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
     const WarpSmem w = carve(smem_raw + wib * p.smem_warp, p);
-    uint4* cur = p.cur + slot_id * p.L;
     uint32_t* bm = p.bitmap + slot_id * p.bm_words;
     uint32_t* claims = p.claims + slot_id * (int64_t)p.claim_cap;
     const int W = (p.dp + 31) >> 5;
@@ -334,8 +368,10 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
     for (;;) {
         unsigned long long qv = 0;
         if (lane == 0) qv = atomicAdd(p.work, 1ull);
-        const int64_t qi = (int64_t)__shfl_sync(kFull, qv, 0);
-        if (qi >= p.nq) break;
+        const int64_t qidx = (int64_t)__shfl_sync(kFull, qv, 0);
+        if (qidx >= p.nq) break;
+        const int64_t qi = p.qlist ? (int64_t)p.qlist[qidx] : qidx;
+        uint4* cur = p.cur + qi * p.L;   // per-query cursors (the round engine shares them)
         if (p.qzero[qi]) {
             for (int t = lane; t < p.k; t += 32) { p.out_ids[qi * p.k + t] = -1; p.out_sims[qi * p.k + t] = __int_as_float(0x7fc00000); }
             if (p.stats && lane == 0) {
@@ -354,9 +390,28 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
         st.T = w.T0; st.Tn = w.T1;
         bool stopped = false;
         int i_stop = 0, j_stop = 0;
+        int i_start = p.K, c_start = 0;
+        if (p.resume) {
+            // continue from the round engine's state: next (level, chunk), top list, counters and
+            // the evaluated ids (at most Ecap <= kHMax, so they fit the hash set)
+            i_start = p.rs.lvl[qi];
+            c_start = p.rs.c0[qi];
+            st.tn = p.rs.tn[qi];
+            for (int t = lane; t < st.tn; t += 32) w.T0[t] = p.rs.T[qi * p.kt + t];
+            const uint32_t* cn = p.rs.cnt + qi * kCnt;
+            st.emitted = cn[0]; st.filtered = cn[1]; st.dups = cn[2]; st.nE = cn[3]; st.probes = cn[4];
+            __syncwarp();
+            for (uint32_t e = lane; e < st.nE; e += 32) {
+                const uint32_t id = p.rs.E[qi * p.rs.Ecap + e];
+                uint32_t h = hs_slot(id);
+                while (atomicCAS(&w.f->hs[h], kEmpty, id) != kEmpty) h = (h + 1) & (kHC - 1);
+            }
+            st.hcount = st.nE;
+            __syncwarp();
+        }
 
-        for (int i = p.K; i >= 1 && !stopped; --i) {
-            for (int c0 = 0; c0 < p.L && !stopped; c0 += p.R) {
+        for (int i = i_start; i >= 1 && !stopped; --i) {
+            for (int c0 = (i == i_start ? c_start : 0); c0 < p.L && !stopped; c0 += p.R) {
                 const int nr = min(p.R, p.L - c0);
                 int tau = 64;
                 if (p.use_filter && st.tn == p.k_eff) {

@@ -23,6 +23,7 @@
 #include "../../include/pfg.h"
 #include "kernels_build.cuh"
 #include "kernels_query.cuh"
+#include "kernels_rounds.cuh"
 #include "rng.h"
 
 namespace pfg {
@@ -261,7 +262,7 @@ int tau_of(float ipk, float eps) {
 }
 
 struct SearchCfg {
-    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0;
+    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0, engine = 0;
     float eps = 0.0f;
     uint32_t* trace_ids = nullptr;
 };
@@ -288,6 +289,8 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     s.trace_cap = z.trace_cap;
     s.trace_ids = z.trace_ids;
     s.timing = z.timing;
+    s.engine = z.engine;
+    if (s.engine < 0 || s.engine > 1) return fail(PFG_E_ARG, "engine must be 0 (rounds + fused) or 1 (fused)");
     if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
     return PFG_OK;
 }
@@ -313,12 +316,19 @@ struct pfg_index {
     // per-call scratch (grow-only)
     DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, outb_ids, outb_sims, outb_stats, outb_trace, work;
     DBuf cur, bitmap, claims;
+    // round-engine state (per query, grow-only)
+    DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_cand, rs_crep, rs_ncand, rs_repcnt,
+        rs_pool_id, rs_pool_q, rs_pool_rep, rs_pool_sim, rs_ctr, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused;
+    int64_t rs_nq = 0;
+    int rs_kt = 0, rs_L = 0;
     int64_t slots = 0;
     int slots_L = 0;
     int64_t slots_bm = 0;
     // launch accounting and phase timing of the last search
     int launches = 0;
     int qc_n = 0, qc_ld = 0;
+    int last_rounds = 0;
+    int64_t last_fused = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     float last_ms[3] = {0, 0, 0};
     int last_launches = 0;
@@ -863,17 +873,37 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         case 16: occ = query_occupancy<16>(smem); break;
         default: occ = query_occupancy<32>(smem); break;
     }
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * occ));
-    const int64_t slots = blocks * 4;
+    const int64_t max_blocks = (int64_t)I->num_sms * occ;
+    const int64_t slots = max_blocks * 4;
     const int64_t bm_words = (g.n + 31) / 32;
-    if (slots > I->slots || g.L != I->slots_L) {
-        PFG_TRY(I->cur.alloc((size_t)slots * g.L * 16, "cursors"));
+    if (slots > I->slots || bm_words != I->slots_bm) {
         PFG_TRY(I->bitmap.alloc((size_t)slots * bm_words * 4, "bitmaps"));
         PFG_TRY(I->claims.alloc((size_t)slots * kClaimCap * 4, "claims"));
         PFG_CUDA(cudaMemsetAsync(I->bitmap.p, 0, (size_t)slots * bm_words * 4, st));
         I->slots = slots;
-        I->slots_L = g.L;
         I->slots_bm = bm_words;
+    }
+    PFG_TRY(I->cur.ensure((size_t)nq * g.L * 16, "cursors"));
+    const bool rounds = s.engine == 0;
+    // round-engine limits (developer overrides): rounds continue while at least min_active queries
+    // are active, at most max_rounds times; the rest is finished by the fused kernel
+    const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : 64;
+    const int min_active = getenv("PFG_MIN_ACTIVE") ? atoi(getenv("PFG_MIN_ACTIVE")) : 64;
+    const int ecap = kHMax, ccap = 4096;
+    const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
+    if (rounds) {
+        const size_t N = (size_t)nq;
+        PFG_TRY(I->rs_lvl.ensure(N * 4, "rs")); PFG_TRY(I->rs_c0.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_flags.ensure(N * 4, "rs")); PFG_TRY(I->rs_tn.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_cnt.ensure(N * kCnt * 4, "rs")); PFG_TRY(I->rs_T.ensure(N * kt * 8, "rs"));
+        PFG_TRY(I->rs_E.ensure(N * ecap * 4, "rs")); PFG_TRY(I->rs_pend.ensure(N * kMaxR * 16, "rs"));
+        PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs")); PFG_TRY(I->rs_crep.ensure(N * ccap, "rs"));
+        PFG_TRY(I->rs_ncand.ensure(N * 4, "rs")); PFG_TRY(I->rs_repcnt.ensure(N * kMaxR * 3 * 4, "rs"));
+        PFG_TRY(I->rs_pool_id.ensure((size_t)pool_cap * 4, "pool")); PFG_TRY(I->rs_pool_q.ensure((size_t)pool_cap * 4, "pool"));
+        PFG_TRY(I->rs_pool_rep.ensure((size_t)pool_cap, "pool")); PFG_TRY(I->rs_pool_sim.ensure((size_t)pool_cap * 4, "pool"));
+        PFG_TRY(I->rs_ctr.ensure(64, "rs counters")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_pn.ensure(N * 4, "rs")); PFG_TRY(I->rs_act0.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_act1.ensure(N * 4, "rs")); PFG_TRY(I->rs_fused.ensure(N * 4, "rs"));
     }
     PFG_TRY(I->work.ensure(8, "work counter"));
     PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
@@ -912,15 +942,82 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         p.prof = profb.as<unsigned long long>();
     }
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[1], st));
-    switch (epl) {
-        case 1: PFG_TRY(launch_query_t<1>(p, (int)blocks, smem, st)); break;
-        case 2: PFG_TRY(launch_query_t<2>(p, (int)blocks, smem, st)); break;
-        case 4: PFG_TRY(launch_query_t<4>(p, (int)blocks, smem, st)); break;
-        case 8: PFG_TRY(launch_query_t<8>(p, (int)blocks, smem, st)); break;
-        case 16: PFG_TRY(launch_query_t<16>(p, (int)blocks, smem, st)); break;
-        default: PFG_TRY(launch_query_t<32>(p, (int)blocks, smem, st)); break;
+    int64_t fused_n = nq;
+    if (rounds) {
+        RoundState& r = p.rs;
+        r.lvl = I->rs_lvl.as<int32_t>(); r.c0 = I->rs_c0.as<int32_t>(); r.flags = I->rs_flags.as<int32_t>();
+        r.tn = I->rs_tn.as<int32_t>(); r.cnt = I->rs_cnt.as<uint32_t>(); r.T = I->rs_T.as<uint64_t>();
+        r.E = I->rs_E.as<uint32_t>(); r.pend = I->rs_pend.as<uint4>(); r.cand = I->rs_cand.as<uint32_t>();
+        r.crep = I->rs_crep.as<uint8_t>(); r.ncand = I->rs_ncand.as<uint32_t>(); r.repcnt = I->rs_repcnt.as<uint32_t>();
+        r.pool_id = I->rs_pool_id.as<uint32_t>(); r.pool_q = I->rs_pool_q.as<uint32_t>();
+        r.pool_rep = I->rs_pool_rep.as<uint8_t>(); r.pool_sim = I->rs_pool_sim.as<float>();
+        uint32_t* ctr = I->rs_ctr.as<uint32_t>();  // [0] pool_top, [1] nnext, [2] nfused
+        r.pool_top = ctr; r.nnext = ctr + 1; r.nfused = ctr + 2;
+        r.poff = I->rs_poff.as<uint32_t>(); r.pn = I->rs_pn.as<uint32_t>();
+        r.active = I->rs_act0.as<uint32_t>(); r.next = I->rs_act1.as<uint32_t>(); r.fused = I->rs_fused.as<uint32_t>();
+        r.Ecap = ecap; r.Ccap = ccap; r.pool_cap = pool_cap;
+        PFG_CUDA(cudaMemsetAsync(ctr, 0, 16, st));
+        k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p);
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 1;
+        uint32_t hc[3];
+        PFG_CUDA(cudaMemcpyAsync(hc, ctr, 12, cudaMemcpyDeviceToHost, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+        uint32_t nact = hc[1];
+        std::swap(r.active, r.next);
+        const size_t csm = (size_t)collect_smem_bytes(g.dpad) * 4;
+        const size_t msm = (size_t)(align16((int)sizeof(MergeSmem)) + 2 * align16(kt * 8)) * 4;
+        PFG_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+        int round = 0;
+        while (nact >= (uint32_t)std::max(1, min_active) && round < max_rounds) {
+            PFG_CUDA(cudaMemsetAsync(ctr, 0, 8, st));  // pool_top, nnext
+            const unsigned qb = (unsigned)std::min<int64_t>(((int64_t)nact + 3) / 4, (int64_t)I->num_sms * 16);
+            switch (epl) {
+                case 1: k_collect<1><<<qb, 128, csm, st>>>(p, nact); break;
+                case 2: k_collect<2><<<qb, 128, csm, st>>>(p, nact); break;
+                case 4: k_collect<4><<<qb, 128, csm, st>>>(p, nact); break;
+                case 8: k_collect<8><<<qb, 128, csm, st>>>(p, nact); break;
+                case 16: k_collect<16><<<qb, 128, csm, st>>>(p, nact); break;
+                default: k_collect<32><<<qb, 128, csm, st>>>(p, nact); break;
+            }
+            k_dedupe<<<qb, 128, 0, st>>>(p, nact);
+            k_sims<<<(unsigned)(I->num_sms * 8), 256, 0, st>>>(p);
+            k_merge<<<qb, 128, msm, st>>>(p, nact);
+            PFG_CUDA(cudaGetLastError());
+            I->launches += 4;
+            PFG_CUDA(cudaMemcpyAsync(hc, ctr, 12, cudaMemcpyDeviceToHost, st));
+            PFG_CUDA(cudaStreamSynchronize(st));
+            nact = hc[1];
+            std::swap(r.active, r.next);
+            ++round;
+        }
+        if (nact > 0) {
+            k_handoff<<<(nact + 255) / 256, 256, 0, st>>>(p, nact);
+            PFG_CUDA(cudaGetLastError());
+            I->launches += 1;
+        }
+        PFG_CUDA(cudaMemcpyAsync(hc, ctr, 12, cudaMemcpyDeviceToHost, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+        fused_n = hc[2];
+        p.qlist = r.fused;
+        p.resume = 1;
+        p.nq = fused_n;
+        I->last_rounds = round;
     }
-    I->launches += 1;
+    if (fused_n > 0) {
+        PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((fused_n + 3) / 4, max_blocks));
+        switch (epl) {
+            case 1: PFG_TRY(launch_query_t<1>(p, (int)blocks, smem, st)); break;
+            case 2: PFG_TRY(launch_query_t<2>(p, (int)blocks, smem, st)); break;
+            case 4: PFG_TRY(launch_query_t<4>(p, (int)blocks, smem, st)); break;
+            case 8: PFG_TRY(launch_query_t<8>(p, (int)blocks, smem, st)); break;
+            case 16: PFG_TRY(launch_query_t<16>(p, (int)blocks, smem, st)); break;
+            default: PFG_TRY(launch_query_t<32>(p, (int)blocks, smem, st)); break;
+        }
+        I->launches += 1;
+    }
+    I->last_fused = fused_n;
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[2], st));
     if (!ids_dev) PFG_CUDA(cudaMemcpyAsync(out_ids, d_ids, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
     if (!sims_dev) PFG_CUDA(cudaMemcpyAsync(out_sims, d_sims, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_struct_sizes_match_header():
     # the binding's ctypes mirrors must have the C sizes (struct_size versioning)
     assert C.sizeof(pfg.BuildOpts) == 48
-    assert C.sizeof(pfg.SearchOpts) == 48
+    assert C.sizeof(pfg.SearchOpts) == 56
     assert pfg.STATS_DTYPE.itemsize == 32
     assert C.sizeof(pfg.IndexInfo) == 96
 

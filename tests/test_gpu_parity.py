@@ -1,6 +1,8 @@
 """GPU <-> oracle parity through the C-ABI (BASELINE north_star tolerances):
 hash codes, tables, sketches and stop points bit-exact; returned ids and evaluated sets bit-exact
 given identical tables; similarities within 1e-5 absolute (expected bit-equal under R-2)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -17,6 +19,8 @@ import paper_1906_12211_b200 as pfg  # noqa: E402
 
 DEV = torch.device("cuda:0")
 SIM_TOL = 1e-5
+# run the round engine even for small batches (it hands queries to the fused kernel below this)
+os.environ["PFG_MIN_ACTIVE"] = "1"
 
 
 def _cuda(a):
@@ -146,9 +150,18 @@ def _compare(c, k, recall, gpu_kw, orc_kw, trace=True):
 @pytest.mark.parametrize("name", ALL)
 @pytest.mark.parametrize("R", [1, 8])
 @pytest.mark.parametrize("recall", [0.5, 0.9, 0.99])
-def test_search_parity(cases, name, R, recall):
+@pytest.mark.parametrize("engine", [0, 1])
+def test_search_parity(cases, name, R, recall, engine):
     c = cases[name]
-    _compare(c, 10, recall, dict(rep_chunk=R), dict(rep_chunk=R))
+    _compare(c, 10, recall, dict(rep_chunk=R, engine=engine), dict(rep_chunk=R))
+
+
+@pytest.mark.parametrize("max_rounds", ["1", "3"])
+def test_round_engine_handoff_midway(cases, max_rounds, monkeypatch):
+    # queries still running after a few rounds resume in the fused kernel from the saved state
+    monkeypatch.setenv("PFG_MAX_ROUNDS", max_rounds)
+    for name in ("hp", "fht"):
+        _compare(cases[name], 10, 0.99, dict(rep_chunk=4), dict(rep_chunk=4))
 
 
 @pytest.mark.parametrize("name", ["hp", "fht"])
@@ -162,8 +175,9 @@ def test_search_parity_options(cases, name, kw):
 
 
 @pytest.mark.parametrize("k", [1, 33, 100])
-def test_search_parity_k(cases, k):
-    _compare(cases["fht"], k, 0.9, dict(rep_chunk=8), dict(rep_chunk=8))
+@pytest.mark.parametrize("engine", [0, 1])
+def test_search_parity_k(cases, k, engine):
+    _compare(cases["fht"], k, 0.9, dict(rep_chunk=8, engine=engine), dict(rep_chunk=8))
 
 
 def test_exhaustive_recall_one_is_bruteforce(cases):
