@@ -229,6 +229,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--engine", type=int, default=0, help="0 = fused kernel, 1 = rounds + fused kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -278,7 +279,7 @@ def main():
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    sopts = dict(rep_chunk=args.rep_chunk, timing=True)
+    sopts = dict(rep_chunk=args.rep_chunk, timing=True, engine=args.engine)
 
     def barrier():
         if world > 1:

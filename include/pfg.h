@@ -77,7 +77,9 @@ typedef struct {
 typedef struct {
     uint32_t struct_size;
     int32_t rep_chunk;        /* [8] R: the filter threshold tau is refreshed once per chunk of R
-                                 repetitions (R-17); 1 = literal per-candidate-batch form */
+                                 repetitions (R-17); while fewer than k points are known a
+                                 chunk is a single repetition (tau = 64 until the first k insertions,
+                                 PAPER.md:333-334) unless uniform_chunks = 1 */
     int32_t segment;          /* [12] B: entries are retrieved in segments of B */
     int32_t stop_rule;        /* [0] 0 = failure bound (1-P_i)^j <= delta;
                                  1 = Alg. 1 line 8, j >= ln(1/delta)/P_i (independent only) */
@@ -90,10 +92,11 @@ typedef struct {
     int32_t timing;           /* [0] 1: record CUDA events around the phases of this call on `stream`
                                  (read back with pfg_last_timing) */
     uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
-    int32_t engine;           /* [0] 0 = bulk-synchronous rounds (one chunk of every active query per round,
-                                 stragglers finished by the fused kernel); 1 = fused kernel only.
-                                 Results are identical. */
-    int32_t reserved1;
+    int32_t engine;           /* [0] 0 = fused kernel (one warp per query, persistent grid);
+                                 1 = bulk-synchronous rounds (one chunk of every active query per round,
+                                 stragglers finished by the fused kernel).  Results are identical. */
+    int32_t uniform_chunks;   /* [0] 1 = chunks of R repetitions from the start (tau = 64 for a whole
+                                 first chunk); 0 = single-repetition chunks until k points are known */
 } pfg_search_opts;
 
 /* per-query counters (optional output of pfg_search) */

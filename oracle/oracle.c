@@ -473,11 +473,14 @@ int64_t or_lower_bound_pub(const uint32_t* c, int64_t n, uint64_t v) { return or
 typedef struct {
     int32_t rep_chunk, stop_rule, per_round, segment, use_filter;
     float eps;
+    int32_t uniform_chunks;  /* 0: a chunk is one repetition while fewer than k points are known (R-17) */
 } or_sopts;
 
 /* ----------------------------------------------------------------------------
  * Query (Alg. 1 over the array form of PAPER.md:281-334 §4.1-4.2).
- *   levels i = K..0; at each level reps j in chunks of R (R-17: tau is frozen per chunk);
+ *   levels i = K..0; at each level reps j in chunks of R (R-17: tau is frozen per chunk; while
+ *   fewer than k points are known tau = 64 and the chunk is a single repetition, so tau is set
+ *   as soon as the first k insertions have happened, PAPER.md:333-334 -- unless uniform_chunks);
  *   per rep: widen (R-12: whole segments of B while the boundary entry shares the top i bits,
  *   PAPER.md:313-319, 934); filter popcount(s'(q) ^ s'(p)) <= tau;
  *   never re-evaluate an id; exact fp32 dot; keep the top k_eff by
@@ -514,7 +517,7 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
     int done = 0;
     for (int i = K; i >= 0 && !done; --i) {
         int Lr = (i == 0) ? 1 : L;
-        for (int c0 = 0; c0 < Lr && !done; c0 += R) {
+        for (int c0 = 0, c1 = 0; c0 < Lr && !done; c0 = c1) {
             int tau = 64;
             if (nt == k_eff && i > 0) {
                 float ip = ts[k_eff - 1];
@@ -522,7 +525,8 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
                 if (ip < -1.0f) ip = -1.0f;
                 tau = or_tau(ip, o->eps);
             }
-            int c1 = c0 + R < Lr ? c0 + R : Lr;
+            int Rc = (nt < k_eff && !o->uniform_chunks) ? 1 : R;
+            c1 = c0 + Rc < Lr ? c0 + Rc : Lr;
             for (int j = c0; j < c1 && !done; ++j) {
                 or_need_rep(X, j);
                 const uint32_t* cj = X->codes[j];

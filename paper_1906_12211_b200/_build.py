@@ -6,7 +6,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libpfg.so")
+LIB = os.environ.get("PFG_LIB") or os.path.join(HERE, "libpfg.so")  # PFG_LIB: developer A/B builds
 SRC = os.path.join(HERE, "csrc", "pfg.cu")
 DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + [
     os.path.join(ROOT, "include", "pfg.h")]

@@ -22,9 +22,18 @@
 
 namespace pfg {
 
-constexpr int kHC = 2048;     // per-warp shared-memory hash set of evaluated ids (capacity)
-constexpr int kHMax = 1536;   // beyond this many evaluated ids a query switches to the global bitmap
-constexpr int kSB = 192;      // survivor buffer (evaluated ids awaiting their similarity)
+#ifndef PFG_HC
+#define PFG_HC 2048
+#endif
+#ifndef PFG_SB
+#define PFG_SB 192
+#endif
+#ifndef PFG_MINB
+#define PFG_MINB 4
+#endif
+constexpr int kHC = PFG_HC;   // per-warp shared-memory hash set of evaluated ids (slots)
+constexpr int kHMax = kHC * 3 / 4;  // beyond this many evaluated ids a query switches to the global bitmap
+constexpr int kSB = PFG_SB;   // survivor buffer (evaluated ids awaiting their similarity)
 constexpr int kRPI = 8;       // candidate rows read per warp iteration (memory-level parallelism)
 constexpr int kU = 4;         // table positions per lane per scan step
 constexpr int kMaxR = 32;     // max repetitions per chunk
@@ -39,6 +48,12 @@ struct __align__(16) Entry {
 
 // Per-query search state in global memory, shared by the round engine (kernels_rounds.cuh) and
 // the fused kernel (which can resume a query from it).
+struct RoundCtl {
+    uint32_t nact[2];      // active-list counts (round parity)
+    uint32_t pool_top[2];  // survivor-pool fill (round parity)
+    uint32_t nfused;       // queries handed to the fused kernel
+    uint32_t pad[3];
+};
 struct RoundState {
     int32_t* lvl;       // [nq] next level i to process (K..1); 0 = only the i = 0 scan remains
     int32_t* c0;        // [nq] next chunk start at that level
@@ -48,22 +63,16 @@ struct RoundState {
     uint64_t* T;        // [nq][kt] top list keys
     uint32_t* E;        // [nq][Ecap] evaluated ids in evaluation order
     uint4* pend;        // [nq][kMaxR] cursors of the chunk in flight (committed by k_merge)
-    uint32_t* cand;     // [nq][Ccap] candidate / survivor ids of the chunk in flight
-    uint8_t* crep;      // [nq][Ccap] their repetition within the chunk
-    uint32_t* ncand;    // [nq]
+    uint32_t* cand;     // [nq][Ccap] survivors of the chunk in flight, in evaluation order
     uint32_t* repcnt;   // [nq][kMaxR][3] emitted, filtered, dups per repetition of the chunk
-    uint32_t* pool_id;  // survivor pool of the round: ids, owning query, rep, similarity
+    uint32_t* pool_id;  // survivor pool of the round: ids, owning query, (sim, id) keys
     uint32_t* pool_q;
-    uint8_t* pool_rep;
-    float* pool_sim;
-    uint32_t* pool_top; // [1]
+    uint64_t* pool_key;
     uint32_t* poff;     // [nq] first pool entry of the query
     uint32_t* pn;       // [nq] pool entries of the query
-    uint32_t* active;   // [nq] queries of this round
-    uint32_t* next;     // [nq] queries of the next round
-    uint32_t* nnext;    // [1]
+    uint32_t* act[2];   // [nq] active lists (round parity)
     uint32_t* fused;    // [nq] queries handed to the fused kernel
-    uint32_t* nfused;   // [1]
+    RoundCtl* ctl;
     int Ecap, Ccap;
     uint32_t pool_cap;
 };
@@ -74,6 +83,8 @@ struct QueryParams {
     int d, dpad, K, L, M, B, R, k, k_eff, per_round, use_filter, c, ell, dp, lazy, claim_cap, trace_cap;
     int kt;          // T capacity (>= k_eff, multiple of 32)
     int qc_n, qc_ld; // query codes precomputed for repetitions [0, qc_n), row stride qc_ld
+    int qb_n, qb_ld; // level-K match ranges precomputed for repetitions [0, qb_n) (k_qbounds)
+    int uniform;     // 1: chunks of R from the start; 0: single-repetition chunks until k are known
     int smem_warp;   // bytes of shared memory per warp
     const float* __restrict__ x;
     const Entry* __restrict__ tab;
@@ -82,6 +93,7 @@ struct QueryParams {
     const float* __restrict__ qx;
     const uint64_t* __restrict__ qsk;
     const uint32_t* __restrict__ qcodes;
+    const uint4* __restrict__ qbnd;  // [nq][qb_ld] {a_K, b_K, probes, 0} of repetition j
     const uint32_t* __restrict__ sg;
     const uint8_t* __restrict__ qzero;
     const float* __restrict__ thr;   // [K][L]
@@ -220,60 +232,96 @@ __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem
     st.nE += (uint32_t)(e2 - e);
 }
 
+// R-17: the chunk starting at c0 is one repetition while fewer than k points are known (tn < k_eff),
+// else R repetitions.  It ends early at the first repetition j whose stop threshold the current
+// k-th similarity already meets: the k-th similarity only grows, so the search stops at or before
+// j and later repetitions of the chunk are never reached (exact).  All lanes get the same value.
+__device__ __forceinline__ int chunk_reps(const QueryParams& p, int i, int c0, int tn, const uint64_t* T, int lane) {
+    int nr = min((tn < p.k_eff && !p.uniform) ? 1 : p.R, p.L - c0);
+    if (tn == p.k_eff) {
+        float ip = key_sim(T[p.k_eff - 1]);
+        ip = fminf(fmaxf(ip, -1.0f), 1.0f);
+        const bool hit = lane < nr && ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + c0 + lane);
+        const uint32_t m = __ballot_sync(kFull, hit);
+        if (m) nr = __ffs(m);
+    }
+    return nr;
+}
+
 __device__ __forceinline__ float kth_sim_clamped(const QueryParams& p, const QState& st) {
     float ip = key_sim(st.T[p.k_eff - 1]);
     return fminf(fmaxf(ip, -1.0f), 1.0f);
 }
 
+// Tree over the 32 lane sums of NR rows (R-2: level h = 16, 8, 4, 2, 1 adds lane sums l and l + h),
+// computed transposed: while a lane holds more than one row, level h halves the rows it keeps (the
+// lanes with bit h set keep the upper half) and adds the partner's value of the same row, so each
+// addition combines the same two tree nodes as the plain tree.  Lane l ends with row
+// (l >> (5 - log2 NR)) for NR <= 32.
+template <int NR>
+__device__ __forceinline__ float tree_rows(float (&a)[NR], int lane) {
+    int m = NR;
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) {
+        if (m > 1) {
+            const int half = m >> 1;
+            const bool up = lane & h;
+#pragma unroll
+            for (int k = 0; k < NR / 2; ++k) {
+                if (k < half) {
+                    const float send = up ? a[k] : a[k + half];
+                    const float keep = up ? a[k + half] : a[k];
+                    a[k] = keep + __shfl_xor_sync(kFull, send, h);
+                }
+            }
+            m = half;
+        } else {
+            a[0] = a[0] + __shfl_xor_sync(kFull, a[0], h);
+        }
+    }
+    return a[0];
+}
+
 // Similarities of survivors [e0, e1) (R-2): the warp reads each candidate row coalesced, one 16-byte
 // chunk per lane (chunk c -> lane c mod 32), each lane keeps a sequential fmaf chain, and the 32
 // lane sums are added in the fixed tree h = 16, 8, 4, 2, 1 -- the oracle's or_sim order.  Zero
-// padding beyond d leaves a chain unchanged (it never holds -0).  kRPI rows are in flight per step.
+// padding beyond d leaves a chain unchanged (it never holds -0).  kRQ rows are in flight per step.
+#ifndef PFG_KRQ
+#define PFG_KRQ 8
+#endif
+constexpr int kRQ = PFG_KRQ;
 __device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int e0, int e1, int lane) {
     const int nch = p.dpad >> 2;
     const float4* q4 = reinterpret_cast<const float4*>(w.qrow);
-    for (int b = e0; b < e1; b += kRPI) {
-        float acc[kRPI];
-        uint32_t off[kRPI];   // row offsets in float4 units (n * dpad / 4 < 2^32)
-        const int nrow = min(kRPI, e1 - b);
+    const float4* x4 = reinterpret_cast<const float4*>(p.x);
+    for (int b = e0; b < e1; b += kRQ) {
+        const int nrow = min(kRQ, e1 - b);
+        // lane r < kRQ reads survivor b + r (rows >= nrow repeat the last)
+        const uint32_t myoff = lane < kRQ ? w.f->sid[b + (lane < nrow ? lane : nrow - 1)] * (uint32_t)nch : 0u;
+        float acc[kRQ];
+        uint32_t off[kRQ];   // row offsets in float4 units (n * dpad / 4 < 2^32)
 #pragma unroll
-        for (int r = 0; r < kRPI; ++r) {
+        for (int r = 0; r < kRQ; ++r) {
             acc[r] = 0.0f;
-            off[r] = w.f->sid[b + (r < nrow ? r : nrow - 1)] * (uint32_t)nch;
+            off[r] = __shfl_sync(kFull, myoff, r);
         }
-        const float4* x4 = reinterpret_cast<const float4*>(p.x);
         for (int c = lane; c < nch; c += 32) {
-            float4 v[kRPI];
+            float4 v[kRQ];
 #pragma unroll
-            for (int r = 0; r < kRPI; ++r) v[r] = __ldg(x4 + off[r] + c);  // rows >= nrow repeat the last
+            for (int r = 0; r < kRQ; ++r) v[r] = __ldg(x4 + off[r] + c);
             const float4 q = q4[c];
 #pragma unroll
-            for (int r = 0; r < kRPI; ++r) {
+            for (int r = 0; r < kRQ; ++r) {
                 acc[r] = fmaf(q.x, v[r].x, acc[r]);
                 acc[r] = fmaf(q.y, v[r].y, acc[r]);
                 acc[r] = fmaf(q.z, v[r].z, acc[r]);
                 acc[r] = fmaf(q.w, v[r].w, acc[r]);
             }
         }
-        // tree over the 32 lane sums, level h = 16, 8, 4 halving the rows a lane keeps (a
-        // transposed reduction: 7 shuffles for 8 rows), then h = 2, 1; lane 4r ends with row r
-        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-        float t4[4], t2[2];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float recv = __shfl_xor_sync(kFull, h16 ? acc[k] : acc[k + 4], 16);
-            t4[k] = (h16 ? acc[k + 4] : acc[k]) + recv;
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const float recv = __shfl_xor_sync(kFull, h8 ? t4[k] : t4[k + 2], 8);
-            t2[k] = (h8 ? t4[k + 2] : t4[k]) + recv;
-        }
-        float t1 = (h4 ? t2[1] : t2[0]) + __shfl_xor_sync(kFull, h4 ? t2[0] : t2[1], 4);
-        t1 = t1 + __shfl_xor_sync(kFull, t1, 2);
-        t1 = t1 + __shfl_xor_sync(kFull, t1, 1);
-        const int rr = lane >> 2;
-        if ((lane & 3) == 0 && b + rr < e1) w.f->ssim[b + rr] = t1;
+        const float t = tree_rows<kRQ>(acc, lane);
+        constexpr int kSh = (kRQ == 32) ? 0 : (kRQ == 16) ? 1 : (kRQ == 8) ? 2 : 3;
+        const int rr = lane >> kSh;
+        if ((lane & ((1 << kSh) - 1)) == 0 && rr < nrow) w.f->ssim[b + rr] = t;
     }
     __syncwarp();
 }
@@ -308,7 +356,9 @@ __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, Q
     return stop;
 }
 
-__device__ __forceinline__ uint32_t hs_slot(uint32_t id) { return (id * 0x9E3779B1u) >> (32 - 11); }
+// home slot of an id: multiplicative hash scaled to [0, kHC); linear probing wraps at kHC
+__device__ __forceinline__ uint32_t hs_slot(uint32_t id) { return __umulhi(id * 0x9E3779B1u, (uint32_t)kHC); }
+__device__ __forceinline__ uint32_t hs_next(uint32_t h) { return h + 1 == (uint32_t)kHC ? 0u : h + 1; }
 
 // claim id for evaluation: true if it was not evaluated before (called by one lane per distinct id)
 __device__ __forceinline__ bool claim(const WarpSmem& w, const QState& st, uint32_t* bm, uint32_t id) {
@@ -321,7 +371,7 @@ __device__ __forceinline__ bool claim(const WarpSmem& w, const QState& st, uint3
         const uint32_t old = atomicCAS(&w.f->hs[h], kEmpty, id);
         if (old == kEmpty) return true;
         if (old == id) return false;
-        h = (h + 1) & (kHC - 1);
+        h = hs_next(h);
     }
 }
 
@@ -333,7 +383,7 @@ __device__ __forceinline__ bool evaluated(const WarpSmem& w, const QState& st, c
         const uint32_t v = w.f->hs[h];
         if (v == kEmpty) return false;
         if (v == id) return true;
-        h = (h + 1) & (kHC - 1);
+        h = hs_next(h);
     }
 }
 
@@ -356,7 +406,7 @@ __device__ __forceinline__ void to_bitmap_mode(const QueryParams& p, const WarpS
 }
 
 template <int EPL>
-__global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
+__global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t slot_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
@@ -399,20 +449,23 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
             st.tn = p.rs.tn[qi];
             for (int t = lane; t < st.tn; t += 32) w.T0[t] = p.rs.T[qi * p.kt + t];
             const uint32_t* cn = p.rs.cnt + qi * kCnt;
-            st.emitted = cn[0]; st.filtered = cn[1]; st.dups = cn[2]; st.nE = cn[3]; st.probes = cn[4];
+            st.emitted = cn[0]; st.filtered = cn[1]; st.dups = cn[2]; st.nE = cn[3];
+            st.probes = lane == 0 ? cn[4] : 0u;  // per-lane partial sums, reduced at the end
             __syncwarp();
             for (uint32_t e = lane; e < st.nE; e += 32) {
                 const uint32_t id = p.rs.E[qi * p.rs.Ecap + e];
                 uint32_t h = hs_slot(id);
-                while (atomicCAS(&w.f->hs[h], kEmpty, id) != kEmpty) h = (h + 1) & (kHC - 1);
+                while (atomicCAS(&w.f->hs[h], kEmpty, id) != kEmpty) h = hs_next(h);
             }
             st.hcount = st.nE;
             __syncwarp();
         }
 
         for (int i = i_start; i >= 1 && !stopped; --i) {
-            for (int c0 = (i == i_start ? c_start : 0); c0 < p.L && !stopped; c0 += p.R) {
-                const int nr = min(p.R, p.L - c0);
+            for (int c0 = (i == i_start ? c_start : 0), c1 = 0; c0 < p.L && !stopped; c0 = c1) {
+                // R-17: a chunk is one repetition while fewer than k points are known, else R
+                const int nr = chunk_reps(p, i, c0, st.tn, st.T, lane);
+                c1 = c0 + nr;
                 int tau = 64;
                 if (p.use_filter && st.tn == p.k_eff) {
                     const float ip = kth_sim_clamped(p, st);
@@ -424,11 +477,9 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 // repetitions < qc_n, otherwise hashed here (FHT-CP, warp-cooperative)
                 const long long th0 = p.prof ? clock64() : 0;
                 if (i == p.K) {
+                    if (lane < nr && c0 + lane < p.qc_n) w.f->qc[lane] = __ldg(p.qcodes + qi * p.qc_ld + c0 + lane);
                     for (int r = 0; r < nr; ++r) {
-                        if (c0 + r < p.qc_n) {
-                            if (lane == 0) w.f->qc[r] = __ldg(p.qcodes + qi * p.qc_ld + c0 + r);
-                            continue;
-                        }
+                        if (c0 + r < p.qc_n) continue;
                         uint64_t full = 0;
                         for (int t = 0; t < p.c; ++t) {
                             const int64_t f = (int64_t)(c0 + r) * p.c + t;
@@ -449,7 +500,11 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                     const bool left = task < nr;
                     const int r = left ? task : task - nr;
                     const int j = c0 + r;
-                    if (i == p.K) {
+                    if (i == p.K && j < p.qb_n) {
+                        const uint4 b = __ldg(p.qbnd + qi * p.qb_ld + j);
+                        w.f->bnd[task] = left ? b.x : b.y;
+                        if (left) st.probes += b.z;
+                    } else if (i == p.K) {
                         const uint32_t qc = w.f->qc[r];
                         w.f->bnd[task] = rep_lower_bound(p, j, left ? (uint64_t)qc : (uint64_t)qc + 1, st.probes);
                     } else {
@@ -509,6 +564,7 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 if (lane == 0) w.f->beg[0] = 0;
                 __syncwarp();
                 const uint32_t total = w.f->beg[nr];
+
                 if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 0, (unsigned long long)(t - tp0)); tp0 = t; }
 
                 int nbuf = 0, next_check = 0, r_stop = -1;
@@ -546,6 +602,8 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
                         const uint32_t g = g0 + u * 32 + lane;
+                        // per-repetition counters: shared-memory atomics (same-address atomics of a
+                        // warp are cheap on sm_100; measured faster than ballot aggregation)
                         if (g < total && !pass[u]) atomicAdd(&w.f->fcnt[rv[u]], 1u);
                         // claims in (rep, position) order: lanes in order within u, u in order
                         const uint32_t pm = __ballot_sync(kFull, pass[u]);
@@ -553,8 +611,8 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                         if (pass[u]) {
                             const uint32_t grp = __match_any_sync(pm, idv[u]);
                             if ((int)(__ffs(grp) - 1) == lane) fresh = claim(w, st, bm, idv[u]);
-                            if (!fresh) atomicAdd(&w.f->dcnt[rv[u]], 1u);
                         }
+                        if (pass[u] && !fresh) atomicAdd(&w.f->dcnt[rv[u]], 1u);
                         const uint32_t fm = __ballot_sync(kFull, fresh);
                         if (fresh) {
                             const int rank = __popc(fm & lanemask_lt());
@@ -632,6 +690,8 @@ __global__ void __launch_bounds__(128, 4) k_query(QueryParams p) {
                 p.out_sims[qi * p.k + t] = -__int_as_float(0x7f800000);
             }
         }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) st.probes += __shfl_xor_sync(kFull, st.probes, off);
         if (p.stats && lane == 0) {
             pfg_query_stats s;
             s.i_stop = i_stop; s.j_stop = j_stop; s.emitted = st.emitted; s.filtered = st.filtered;

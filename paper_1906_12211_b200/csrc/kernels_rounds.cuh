@@ -1,26 +1,35 @@
 // kernels_rounds.cuh — the round engine: the same adaptive query as k_query, executed one chunk
-// (R repetitions at one level) of every active query per round, split into bulk-parallel phases
-// so that the bandwidth-heavy similarity phase runs with full memory-level parallelism:
+// (the chunk's repetitions at one level) of every active query per round, split into
+// bulk-parallel phases so that each phase runs at its own best occupancy and the
+// bandwidth-heavy similarity phase has full memory-level parallelism:
 //
+//   k_qbounds  per (query, repetition < qb_n): the level-K match range [a_K, b_K) by two
+//              interleaved binary searches (once per search, before the rounds)
 //   k_rinit    per query: state init; zero query rows answered directly
 //   k_collect  warp per active query: chunk codes, widening (R-12), scan of the emitted table
-//              entries in (repetition, position) order with the sketch filter -> candidates
-//   k_dedupe   warp per active query: evaluated-id hash set rebuilt in shared memory from the query's
-//              evaluated list, claims in candidate order (R-17) -> survivors into the round's pool
-//   k_sims     grid over the pool: warp-coalesced rows, 32-lane tree (R-2)
+//              entries in (repetition, position) order with the sketch filter, and the dedupe
+//              claims against a shared-memory hash set rebuilt from the query's evaluated list
+//              (R-17/R-18) -> survivors appended to the evaluated list and to the round's pool
+//   k_sims     grid over the pool: warp-coalesced rows, 32-lane tree (R-2) -> (sim, id) keys
 //   k_merge    warp per active query: merge repetition by repetition into the top list, stop check
 //              after each repetition (Alg. 1 line 8), commit cursors / advance, or finish
 //
-// Every decision (candidate order, claims, merges, stop checks, counters) is the one k_query makes
-// for the same chunk, so results are identical.  A query whose chunk would overflow a buffer, that
-// reaches the i = 0 scan, or that is still running when the rounds end is handed to k_query, which
-// resumes it from the state (RoundState) with the chunk not yet committed.
+// Every decision (chunk boundaries, candidate order, claims, merges, stop checks, counters) is the
+// one k_query makes for the same chunk, so results are identical.  A query whose chunk would
+// overflow the evaluated list or the pool, that reaches the i = 0 scan, or that is still running
+// when the rounds end is handed to k_query, which resumes it from the state (RoundState) with the
+// chunk not yet committed.
+//
+// Round r uses parity par = r & 1: it reads active list act[par] (count ctl->nact[par]) and the
+// pool counter ctl->pool_top[par]; k_collect resets the other parity's counters, k_merge fills
+// act[par ^ 1].  No host synchronisation is needed between rounds.
 #pragma once
 #include "kernels_query.cuh"
 
 namespace pfg {
 
 constexpr int kFlagDone = 1, kFlagFused = 2;
+constexpr int kEPre = 16;  // evaluated ids loaded per lane per batch when the hash set is rebuilt
 
 __device__ __forceinline__ int tau_of_state(const QueryParams& p, int tn, const uint64_t* T) {
     if (!p.use_filter || tn != p.k_eff) return 64;
@@ -31,7 +40,42 @@ __device__ __forceinline__ int tau_of_state(const QueryParams& p, int tn, const 
     return lo;
 }
 
+
 __device__ __forceinline__ void push(uint32_t* list, uint32_t* n, uint32_t q) { list[atomicAdd(n, 1u)] = q; }
+
+// ---------------------------------------------------------------------------------------------
+// level-K match ranges: a = lower_bound(code_j), b = lower_bound(code_j + 1) in
+// repetition j's sorted table, via the 13-bit prefix table and a binary search in the bucket; the
+// two searches run interleaved so both loads are in flight together.
+__device__ __forceinline__ void bucket_of(const QueryParams& p, int j, uint64_t x, uint32_t& lo, uint32_t& hi) {
+    if (x >= (1ull << p.K)) { lo = hi = (uint32_t)p.n; return; }
+    const int sh = p.K - 13;
+    const uint32_t* ptj = p.pt + (int64_t)j * 8193;
+    const uint32_t pfx = (uint32_t)x >> sh;
+    lo = __ldg(ptj + pfx);
+    hi = ((x & ((1ull << sh) - 1)) == 0) ? lo : __ldg(ptj + pfx + 1);
+}
+
+__global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t q = t / p.qb_n;
+    const int j = (int)(t - q * p.qb_n);
+    if (q >= p.nq) return;
+    if (p.qzero[q]) { out[q * p.qb_ld + j] = make_uint4(0, 0, 0, 0); return; }
+    const uint32_t qc = __ldg(p.qcodes + q * p.qc_ld + j);
+    uint32_t lo1, hi1, lo2, hi2, probes = 0;
+    bucket_of(p, j, qc, lo1, hi1);
+    bucket_of(p, j, (uint64_t)qc + 1, lo2, hi2);
+    const Entry* tj = p.tab + (int64_t)j * p.n;
+    while (lo1 < hi1 || lo2 < hi2) {
+        const uint32_t m1 = (lo1 + hi1) >> 1, m2 = (lo2 + hi2) >> 1;
+        const uint32_t c1 = lo1 < hi1 ? entry_code(tj + m1) : 0u;
+        const uint32_t c2 = lo2 < hi2 ? entry_code(tj + m2) : 0u;
+        if (lo1 < hi1) { ++probes; if (c1 < qc) lo1 = m1 + 1; else hi1 = m1; }
+        if (lo2 < hi2) { ++probes; if ((uint64_t)c2 < (uint64_t)qc + 1) lo2 = m2 + 1; else hi2 = m2; }
+    }
+    out[q * p.qb_ld + j] = make_uint4(lo1, lo2, probes, 0u);
+}
 
 // ---------------------------------------------------------------------------------------------
 __global__ void k_rinit(QueryParams p) {
@@ -49,45 +93,69 @@ __global__ void k_rinit(QueryParams p) {
         return;
     }
     rs.flags[q] = 0;
-    push(rs.next, rs.nnext, (uint32_t)q);
+    push(rs.act[0], &rs.ctl->nact[0], (uint32_t)q);
 }
 
 // ---------------------------------------------------------------------------------------------
 struct CollectSmem {
+    uint32_t hs[kHC];          // evaluated-id hash set
     uint64_t qsk[64];
     uint32_t beg[kMaxR + 4];
-    uint32_t lo_new[kMaxR], lo_old[kMaxR], hi_old[kMaxR], qc[kMaxR], bnd[2 * kMaxR], fcnt[kMaxR];
+    uint32_t lo_new[kMaxR], lo_old[kMaxR], hi_old[kMaxR], qc[kMaxR], bnd[2 * kMaxR], fcnt[kMaxR], dcnt[kMaxR];
 };
-__host__ __device__ inline int collect_smem_bytes(int dpad) { return align16((int)sizeof(CollectSmem)) + align16(dpad * 4); }
+__host__ __device__ inline int collect_smem_bytes(int dpad, bool lazy) {
+    return align16((int)sizeof(CollectSmem)) + (lazy ? align16(dpad * 4) : 0);
+}
 
 template <int EPL>
-__global__ void __launch_bounds__(128) k_collect(QueryParams p, uint32_t nactive) {
+__global__ void __launch_bounds__(128) k_collect(QueryParams p, int par, int lazy) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int stride_b = collect_smem_bytes(p.dpad);
-    CollectSmem* c = (CollectSmem*)(smem_raw + wib * stride_b);
+    CollectSmem* c = (CollectSmem*)(smem_raw + wib * collect_smem_bytes(p.dpad, lazy));
     float* qrow = (float*)((unsigned char*)c + align16((int)sizeof(CollectSmem)));
     const RoundState& rs = p.rs;
+    const uint32_t nact = rs.ctl->nact[par];
+    if (blockIdx.x == 0 && threadIdx.x == 0) { rs.ctl->nact[par ^ 1] = 0; rs.ctl->pool_top[par ^ 1] = 0; }
+    const uint32_t* act = rs.act[par];
     const int W = (p.dp + 31) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nactive; a += nw) {
-        const int64_t q = rs.active[a];
-        const int i = rs.lvl[q], c0 = rs.c0[q];
-        const int nr = min(p.R, p.L - c0);
-        const int tau = tau_of_state(p, rs.tn[q], rs.T + q * p.kt);
+    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nact; a += nw) {
+        const int64_t q = act[a];
+        long long tq0 = p.prof ? clock64() : 0, tq = tq0;
+        const int i = rs.lvl[q], c0 = rs.c0[q], tn = rs.tn[q];
+        const int nr = chunk_reps(p, i, c0, tn, rs.T + q * p.kt, lane);
+        const int tau = tau_of_state(p, tn, rs.T + q * p.kt);
+        const uint32_t nE = rs.cnt[q * kCnt + 3];
+        uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
         uint4* cur = p.cur + q * p.L;
         for (int t = lane; t < p.M; t += 32) c->qsk[t] = p.qsk[q * p.M + t];
+        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
         const bool need_lazy = (i == p.K) && (c0 + nr > p.qc_n);
         if (need_lazy)
             for (int t = lane; t < p.dpad; t += 32) qrow[t] = p.qx[q * p.dpad + t];
+        if (lane < nr) { c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
         __syncwarp();
+        // rebuild the evaluated-id hash set (ids are distinct; kEPre loads per lane in flight)
+        for (uint32_t e0 = 0; e0 < nE; e0 += 32 * kEPre) {
+            uint32_t v[kEPre];
+#pragma unroll
+            for (int u = 0; u < kEPre; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                v[u] = e < nE ? E[e] : kEmpty;
+            }
+#pragma unroll
+            for (int u = 0; u < kEPre; ++u)
+                if (v[u] != kEmpty) {
+                    uint32_t h = hs_slot(v[u]);
+                    while (atomicCAS(&c->hs[h], kEmpty, v[u]) != kEmpty) h = hs_next(h);
+                }
+        }
+        if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 8, (unsigned long long)(t - tq)); tq = t; }
         uint32_t probes = 0;
         if (i == p.K) {
+            if (lane < nr && c0 + lane < p.qc_n) c->qc[lane] = __ldg(p.qcodes + q * p.qc_ld + c0 + lane);
             for (int r = 0; r < nr; ++r) {
-                if (c0 + r < p.qc_n) {
-                    if (lane == 0) c->qc[r] = __ldg(p.qcodes + q * p.qc_ld + c0 + r);
-                    continue;
-                }
+                if (c0 + r < p.qc_n) continue;
                 uint64_t full = 0;
                 for (int t = 0; t < p.c; ++t) {
                     const int64_t f = (int64_t)(c0 + r) * p.c + t;
@@ -97,12 +165,16 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, uint32_t nactive
             }
             __syncwarp();
         }
-        // widening, same as k_query
+        // widening, as k_query (first level: precomputed match ranges or binary search)
         for (int task = lane; task < 2 * nr; task += 32) {
             const bool left = task < nr;
             const int r = left ? task : task - nr;
             const int j = c0 + r;
-            if (i == p.K) {
+            if (i == p.K && j < p.qb_n) {
+                const uint4 b = __ldg(p.qbnd + q * p.qb_ld + j);
+                c->bnd[task] = left ? b.x : b.y;
+                if (left) probes += b.z;
+            } else if (i == p.K) {
                 const uint32_t qc = c->qc[r];
                 c->bnd[task] = rep_lower_bound(p, j, left ? (uint64_t)qc : (uint64_t)qc + 1, probes);
             } else {
@@ -147,10 +219,8 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, uint32_t nactive
                 nelo = c->bnd[lane]; nehi = c->bnd[nr + lane];
             }
             c->lo_new[lane] = nelo; c->lo_old[lane] = elo; c->hi_old[lane] = ehi;
-            c->fcnt[lane] = 0;
             em = (elo - nelo) + (nehi - ehi);
             rs.pend[q * kMaxR + lane] = make_uint4(c->qc[lane], nelo, nehi, 0u);
-            rs.repcnt[(q * kMaxR + lane) * 3 + 0] = em;
         }
         uint32_t incl = em;
 #pragma unroll
@@ -160,18 +230,16 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, uint32_t nactive
         }
         if (lane < nr) c->beg[lane + 1] = incl;
         if (lane == 0) c->beg[0] = 0;
-        probes += __shfl_xor_sync(kFull, probes, 16);
-        probes += __shfl_xor_sync(kFull, probes, 8);
-        probes += __shfl_xor_sync(kFull, probes, 4);
-        probes += __shfl_xor_sync(kFull, probes, 2);
-        probes += __shfl_xor_sync(kFull, probes, 1);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) probes += __shfl_xor_sync(kFull, probes, off);
         __syncwarp();
+        if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 9, (unsigned long long)(t - tq)); tq = t; }
         const uint32_t total = c->beg[nr];
-        // scan in (rep, position) order; filter-passing positions become candidates in that order
-        uint32_t ncand = 0;
+        // scan in (rep, position) order: filter, then claim in order through the hash set; fresh
+        // ids are appended to the evaluated list (room up to Ecap; beyond kHMax the query is
+        // handed to the fused kernel, whose bitmap mode has no limit)
+        uint32_t ns = 0;
         bool overflow = false;
-        uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
-        uint8_t* crep = rs.crep + q * (int64_t)rs.Ccap;
         int rl = 0;
         for (uint32_t g0 = 0; g0 < total; g0 += 32 * kU) {
             uint32_t idv[kU];
@@ -200,140 +268,134 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, uint32_t nactive
                 const uint32_t g = g0 + u * 32 + lane;
                 if (g < total && !pass[u]) atomicAdd(&c->fcnt[rv[u]], 1u);
                 const uint32_t pm = __ballot_sync(kFull, pass[u]);
+                bool fresh = false;
                 if (pass[u]) {
-                    const uint32_t dst = ncand + __popc(pm & lanemask_lt());
-                    if (dst < (uint32_t)rs.Ccap) { cand[dst] = idv[u]; crep[dst] = (uint8_t)rv[u]; }
-                }
-                ncand += __popc(pm);
-            }
-        }
-        if (ncand > (uint32_t)rs.Ccap) overflow = true;
-        __syncwarp();
-        if (lane < nr) rs.repcnt[(q * kMaxR + lane) * 3 + 1] = c->fcnt[lane];
-        if (lane == 0) {
-            rs.ncand[q] = overflow ? 0u : ncand;
-            rs.cnt[q * kCnt + 4] += probes;
-            if (overflow) rs.flags[q] |= kFlagFused;
-        }
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
-struct DedupeSmem {
-    uint32_t hs[kHC];
-    uint32_t dcnt[kMaxR];
-};
-
-__global__ void __launch_bounds__(128) k_dedupe(QueryParams p, uint32_t nactive) {
-    __shared__ DedupeSmem sm_all[4];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    DedupeSmem* d = &sm_all[wib];
-    const RoundState& rs = p.rs;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nactive; a += nw) {
-        const int64_t q = rs.active[a];
-        if (rs.flags[q] & kFlagFused) continue;
-        const uint32_t nE = rs.cnt[q * kCnt + 3];
-        const uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
-        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(d->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-        if (lane < kMaxR) d->dcnt[lane] = 0;
-        __syncwarp();
-        for (uint32_t e = lane; e < nE; e += 32) {
-            const uint32_t id = E[e];
-            uint32_t h = hs_slot(id);
-            while (atomicCAS(&d->hs[h], kEmpty, id) != kEmpty) h = (h + 1) & (kHC - 1);
-        }
-        __syncwarp();
-        const uint32_t n = rs.ncand[q];
-        uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
-        uint8_t* crep = rs.crep + q * (int64_t)rs.Ccap;
-        uint32_t ns = 0;
-        for (uint32_t b = 0; b < n; b += 32) {
-            const bool act = b + lane < n;
-            const uint32_t id = act ? cand[b + lane] : 0u;
-            const int r = act ? crep[b + lane] : 0;
-            const uint32_t am = __ballot_sync(kFull, act);
-            bool fresh = false;
-            if (act) {
-                const uint32_t grp = __match_any_sync(am, id);
-                if ((int)(__ffs(grp) - 1) == lane) {
-                    uint32_t h = hs_slot(id);
-                    for (;;) {
-                        const uint32_t old = atomicCAS(&d->hs[h], kEmpty, id);
-                        if (old == kEmpty) { fresh = true; break; }
-                        if (old == id) break;
-                        h = (h + 1) & (kHC - 1);
+                    const uint32_t grp = __match_any_sync(pm, idv[u]);
+                    if ((int)(__ffs(grp) - 1) == lane) {
+                        uint32_t h = hs_slot(idv[u]);
+                        for (;;) {
+                            const uint32_t old = atomicCAS(&c->hs[h], kEmpty, idv[u]);
+                            if (old == kEmpty) { fresh = true; break; }
+                            if (old == idv[u]) break;
+                            h = hs_next(h);
+                        }
                     }
+                    if (!fresh) atomicAdd(&c->dcnt[rv[u]], 1u);
                 }
-                if (!fresh) atomicAdd(&d->dcnt[r], 1u);
+                const uint32_t fm = __ballot_sync(kFull, fresh);
+                if (fresh) E[nE + ns + __popc(fm & lanemask_lt())] = idv[u];
+                ns += __popc(fm);
             }
-            const uint32_t fm = __ballot_sync(kFull, fresh);
-            __syncwarp();
-            if (fresh) {
-                const uint32_t dst = ns + __popc(fm & lanemask_lt());
-                cand[dst] = id;      // in-place compaction in order (dst <= b + lane)
-                crep[dst] = (uint8_t)r;
-            }
-            ns += __popc(fm);
-            __syncwarp();
+            if (nE + ns > (uint32_t)kHMax) { overflow = true; break; }
         }
-        bool fused = nE + ns > (uint32_t)rs.Ecap;
+        __syncwarp();
+        if (p.prof && lane == 0) {
+            const long long t = clock64(); atomicAdd(p.prof + 10, (unsigned long long)(t - tq)); tq = t;
+            atomicAdd(p.prof + 13, (unsigned long long)total);
+        }
         uint32_t base = 0;
-        if (!fused && lane == 0) base = atomicAdd(rs.pool_top, ns);
+        if (!overflow && lane == 0) base = atomicAdd(&rs.ctl->pool_top[par], ns);
         base = __shfl_sync(kFull, base, 0);
-        if (!fused && (uint64_t)base + ns > rs.pool_cap) fused = true;
-        if (fused) {
+        if (!overflow && (uint64_t)base + ns > rs.pool_cap) overflow = true;
+        if (overflow) {
             if (lane == 0) rs.flags[q] |= kFlagFused;
+            __syncwarp();
             continue;
         }
-        uint32_t* Ew = rs.E + q * (int64_t)rs.Ecap + nE;
-        for (uint32_t e = lane; e < ns; e += 32) {
-            const uint32_t id = cand[e];
-            Ew[e] = id;
-            rs.pool_id[base + e] = id;
-            rs.pool_q[base + e] = (uint32_t)q;
-            rs.pool_rep[base + e] = crep[e];
+        for (uint32_t e0 = 0; e0 < ns; e0 += 32 * kEPre) {
+            uint32_t v[kEPre];
+#pragma unroll
+            for (int u = 0; u < kEPre; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                v[u] = e < ns ? E[nE + e] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kEPre; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                if (e < ns) { rs.pool_id[base + e] = v[u]; rs.pool_q[base + e] = (uint32_t)q; }
+            }
         }
-        if (lane < kMaxR) rs.repcnt[(q * kMaxR + lane) * 3 + 2] = d->dcnt[lane];
-        if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }
+        if (lane < nr) {
+            uint32_t* rc = rs.repcnt + (q * kMaxR + lane) * 3;
+            rc[0] = c->beg[lane + 1] - c->beg[lane];
+            rc[1] = c->fcnt[lane];
+            rc[2] = c->dcnt[lane];
+        }
+        if (lane == 0) {
+            rs.poff[q] = base;
+            rs.pn[q] = ns;
+            rs.cnt[q * kCnt + 4] += probes;
+        }
         __syncwarp();
+        if (p.prof && lane == 0) {
+            const long long t = clock64(); atomicAdd(p.prof + 11, (unsigned long long)(t - tq));
+            atomicMax(p.prof + 12, (unsigned long long)(t - tq0));
+            atomicAdd(p.prof + 14, 1ull);
+            atomicMax(p.prof + 15, (unsigned long long)total);
+        }
     }
 }
 
 // ---------------------------------------------------------------------------------------------
-// similarities of the round's pool, kRPI rows per warp step (R-2 order, as compute_sims)
-__global__ void __launch_bounds__(256) k_sims(QueryParams p) {
+// similarities of the round's pool, kRPI rows per warp step (R-2 order, as compute_sims).  A
+// query's survivors are contiguous in the pool, so the kRPI rows of a step usually share one query
+// row (loaded once per chunk); otherwise each row reads its own query row.
+template <bool ONEQ>
+__device__ __forceinline__ void pool_sims_step(const float4* __restrict__ x4, const float4* __restrict__ qx4,
+                                               const uint32_t (&roff)[kRPI], const uint32_t (&qoff)[kRPI], int nch,
+                                               int lane, float (&acc)[kRPI]) {
+#pragma unroll
+    for (int r = 0; r < kRPI; ++r) acc[r] = 0.0f;
+    for (int c = lane; c < nch; c += 32) {
+        float4 v[kRPI];
+#pragma unroll
+        for (int r = 0; r < kRPI; ++r) v[r] = __ldg(x4 + roff[r] + c);
+        float4 w4 = __ldg(qx4 + qoff[0] + c);
+#pragma unroll
+        for (int r = 0; r < kRPI; ++r) {
+            if (!ONEQ && r > 0) w4 = __ldg(qx4 + qoff[r] + c);
+            acc[r] = fmaf(w4.x, v[r].x, acc[r]);
+            acc[r] = fmaf(w4.y, v[r].y, acc[r]);
+            acc[r] = fmaf(w4.z, v[r].z, acc[r]);
+            acc[r] = fmaf(w4.w, v[r].w, acc[r]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) k_sims(QueryParams p, int par) {
     const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
-    const uint32_t top = min(*rs.pool_top, rs.pool_cap);
+    const uint32_t top = min(rs.ctl->pool_top[par], rs.pool_cap);
     const int nch = p.dpad >> 2;
     const float4* x4 = reinterpret_cast<const float4*>(p.x);
     const float4* qx4 = reinterpret_cast<const float4*>(p.qx);
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRPI; b < top; b += nw * kRPI) {
+    // lane r < kRPI holds entry b + r of the current step (rows beyond the end repeat the last);
+    // the next step's entries are fetched before the current rows are read
+    auto fetch = [&](int64_t b, uint32_t& id, uint32_t& qq) {
+        if (lane < kRPI && b < top) {
+            const int64_t e1 = (int64_t)top < b + kRPI ? (int64_t)top : b + kRPI;
+            const int64_t e = b + lane < e1 ? b + lane : e1 - 1;
+            id = rs.pool_id[e];
+            qq = rs.pool_q[e];
+        }
+    };
+    int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRPI;
+    uint32_t nid = 0, nq_ = 0;
+    fetch(b, nid, nq_);
+    for (; b < top; b += nw * kRPI) {
         const int64_t e1 = (int64_t)top < b + kRPI ? (int64_t)top : b + kRPI;
+        const uint32_t myid = nid, myq = nq_;
+        fetch(b + nw * kRPI, nid, nq_);
         float acc[kRPI];
         uint32_t roff[kRPI], qoff[kRPI];
 #pragma unroll
         for (int r = 0; r < kRPI; ++r) {
-            const int64_t e = b + r < e1 ? b + r : e1 - 1;
-            acc[r] = 0.0f;
-            roff[r] = rs.pool_id[e] * (uint32_t)nch;
-            qoff[r] = rs.pool_q[e] * (uint32_t)nch;
+            roff[r] = __shfl_sync(kFull, myid, r) * (uint32_t)nch;
+            qoff[r] = __shfl_sync(kFull, myq, r) * (uint32_t)nch;
         }
-        for (int c = lane; c < nch; c += 32) {
-            float4 v[kRPI], w4[kRPI];
-#pragma unroll
-            for (int r = 0; r < kRPI; ++r) { v[r] = __ldg(x4 + roff[r] + c); w4[r] = __ldg(qx4 + qoff[r] + c); }
-#pragma unroll
-            for (int r = 0; r < kRPI; ++r) {
-                acc[r] = fmaf(w4[r].x, v[r].x, acc[r]);
-                acc[r] = fmaf(w4[r].y, v[r].y, acc[r]);
-                acc[r] = fmaf(w4[r].z, v[r].z, acc[r]);
-                acc[r] = fmaf(w4[r].w, v[r].w, acc[r]);
-            }
-        }
+        if (qoff[0] == qoff[kRPI - 1]) pool_sims_step<true>(x4, qx4, roff, qoff, nch, lane, acc);
+        else pool_sims_step<false>(x4, qx4, roff, qoff, nch, lane, acc);
         const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
         float t4[4], t2[2];
 #pragma unroll
@@ -350,18 +412,17 @@ __global__ void __launch_bounds__(256) k_sims(QueryParams p) {
         t1 = t1 + __shfl_xor_sync(kFull, t1, 2);
         t1 = t1 + __shfl_xor_sync(kFull, t1, 1);
         const int rr = lane >> 2;
-        if ((lane & 3) == 0 && b + rr < e1) rs.pool_sim[b + rr] = t1;
+        const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
+        if ((lane & 3) == 0 && b + rr < e1) rs.pool_key[b + rr] = make_key(t1, id_rr);
     }
 }
 
 // ---------------------------------------------------------------------------------------------
 struct MergeSmem {
     uint64_t cand[32];
-    uint32_t sid[32];
-    float ssim[32];
 };
 
-__global__ void __launch_bounds__(128) k_merge(QueryParams p, uint32_t nactive) {
+__global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int per_warp = align16((int)sizeof(MergeSmem)) + 2 * align16(p.kt * 8);
@@ -369,40 +430,50 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, uint32_t nactive) 
     uint64_t* T0 = (uint64_t*)((unsigned char*)m + align16((int)sizeof(MergeSmem)));
     uint64_t* T1 = T0 + align16(p.kt * 8) / 8;
     const RoundState& rs = p.rs;
+    const uint32_t nact = rs.ctl->nact[par];
+    const uint32_t* act = rs.act[par];
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nactive; a += nw) {
-        const int64_t q = rs.active[a];
+    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nact; a += nw) {
+        const int64_t q = act[a];
         if (rs.flags[q] & kFlagFused) {
-            if (lane == 0) push(rs.fused, rs.nfused, (uint32_t)q);
+            if (lane == 0) push(rs.fused, &rs.ctl->nfused, (uint32_t)q);
             continue;
         }
         const int i = rs.lvl[q], c0 = rs.c0[q];
-        const int nr = min(p.R, p.L - c0);
         int tn = rs.tn[q];
+        const int nr = chunk_reps(p, i, c0, tn, rs.T + q * p.kt, lane);
         for (int t = lane; t < tn; t += 32) T0[t] = rs.T[q * p.kt + t];
         uint64_t* T = T0;
         uint64_t* Tn = T1;
         uint32_t* cn = rs.cnt + q * kCnt;
         uint32_t nE = cn[3];
-        const uint32_t base = rs.poff[q], ns = rs.pn[q];
+        const uint32_t base = rs.poff[q];
+        // survivors of repetition r are pool entries [end_{r-1}, end_r): per repetition
+        // emitted - filtered - duplicates, in repetition order
+        uint32_t rc0 = 0, rc1 = 0, rc2 = 0;
+        if (lane < nr) {
+            const uint32_t* rc = rs.repcnt + (q * kMaxR + lane) * 3;
+            rc0 = rc[0]; rc1 = rc[1]; rc2 = rc[2];
+        }
+        uint32_t end = rc0 - rc1 - rc2;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(kFull, end, off);
+            if (lane >= off) end += o;
+        }
         __syncwarp();
         int r_stop = -1;
         uint32_t e = 0;
         for (int r = 0; r < nr; ++r) {
-            // survivors of repetition r: [e, e2) (the pool keeps the query's candidate order)
-            uint32_t lo = e, hi = ns;
-            while (lo < hi) { const uint32_t mid = (lo + hi) >> 1; if (rs.pool_rep[base + mid] <= r) lo = mid + 1; else hi = mid; }
-            const uint32_t e2 = lo;
+            const uint32_t e2 = __shfl_sync(kFull, end, r);
+            uint64_t nxt = (e + lane < e2) ? rs.pool_key[base + e + lane] : 0ull;
             for (uint32_t b0 = e; b0 < e2; b0 += 32) {
                 const uint32_t idx = b0 + lane;
-                uint64_t key = 0;
-                if (idx < e2) {
-                    const uint32_t id = rs.pool_id[base + idx];
-                    key = make_key(rs.pool_sim[base + idx], id);
-                    if (p.trace_cap > 0) {
-                        const uint32_t pos = nE + (idx - e);
-                        if (pos < (uint32_t)p.trace_cap) p.trace_ids[q * p.trace_cap + pos] = id;
-                    }
+                uint64_t key = nxt;
+                nxt = (idx + 32 < e2) ? rs.pool_key[base + idx + 32] : 0ull;  // prefetch the next batch
+                if (idx < e2 && p.trace_cap > 0) {
+                    const uint32_t pos = nE + (idx - e);
+                    if (pos < (uint32_t)p.trace_cap) p.trace_ids[q * p.trace_cap + pos] = key_id(key);
                 }
                 const uint64_t kth = (tn == p.k_eff) ? T[p.k_eff - 1] : 0ull;
                 if (key <= kth) key = 0;
@@ -439,10 +510,12 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, uint32_t nactive) 
             }
         }
         const int rmax = r_stop >= 0 ? r_stop : nr - 1;
-        uint32_t ea = 0, fa = 0, da = 0;
-        for (int r = 0; r <= rmax; ++r) {
-            const uint32_t* rc = rs.repcnt + (q * kMaxR + r) * 3;
-            ea += rc[0]; fa += rc[1]; da += rc[2];
+        uint32_t ea = lane <= rmax ? rc0 : 0u, fa = lane <= rmax ? rc1 : 0u, da = lane <= rmax ? rc2 : 0u;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            ea += __shfl_xor_sync(kFull, ea, off);
+            fa += __shfl_xor_sync(kFull, fa, off);
+            da += __shfl_xor_sync(kFull, da, off);
         }
         const uint32_t emitted = cn[0] + ea, filtered = cn[1] + fa, dups = cn[2] + da;
         __syncwarp();
@@ -475,24 +548,23 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, uint32_t nactive) 
             if (lane == 0) {
                 cn[0] = emitted; cn[1] = filtered; cn[2] = dups; cn[3] = nE;
                 rs.tn[q] = tn;
-                int ni = i, nc0 = c0 + p.R;
+                int ni = i, nc0 = c0 + nr;
                 if (nc0 >= p.L) { ni = i - 1; nc0 = 0; }
                 rs.lvl[q] = ni;
                 rs.c0[q] = nc0;
-                if (ni == 0) { rs.flags[q] |= kFlagFused; push(rs.fused, rs.nfused, (uint32_t)q); }
-                else push(rs.next, rs.nnext, (uint32_t)q);
+                if (ni == 0) { rs.flags[q] |= kFlagFused; push(rs.fused, &rs.ctl->nfused, (uint32_t)q); }
+                else push(rs.act[par ^ 1], &rs.ctl->nact[par ^ 1], (uint32_t)q);
             }
         }
         __syncwarp();
     }
 }
 
-// move the still-active queries to the fused list (rounds ended)
-__global__ void k_handoff(QueryParams p, uint32_t nactive) {
+// move the still-active queries of list `par` to the fused list (rounds ended)
+__global__ void k_handoff(QueryParams p, int par) {
     const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= nactive) return;
-    const uint32_t q = p.rs.active[a];
-    push(p.rs.fused, p.rs.nfused, q);
+    if (a >= p.rs.ctl->nact[par]) return;
+    push(p.rs.fused, &p.rs.ctl->nfused, p.rs.act[par][a]);
 }
 
 }  // namespace pfg

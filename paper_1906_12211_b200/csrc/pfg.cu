@@ -262,7 +262,7 @@ int tau_of(float ipk, float eps) {
 }
 
 struct SearchCfg {
-    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0, engine = 0;
+    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0, engine = 0, uniform = 0;
     float eps = 0.0f;
     uint32_t* trace_ids = nullptr;
 };
@@ -290,7 +290,9 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     s.trace_ids = z.trace_ids;
     s.timing = z.timing;
     s.engine = z.engine;
-    if (s.engine < 0 || s.engine > 1) return fail(PFG_E_ARG, "engine must be 0 (rounds + fused) or 1 (fused)");
+    if (s.engine < 0 || s.engine > 1) return fail(PFG_E_ARG, "engine must be 0 (fused) or 1 (rounds + fused)");
+    s.uniform = z.uniform_chunks;
+    if (s.uniform != 0 && s.uniform != 1) return fail(PFG_E_ARG, "uniform_chunks must be 0 or 1");
     if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
     return PFG_OK;
 }
@@ -317,8 +319,10 @@ struct pfg_index {
     DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, outb_ids, outb_sims, outb_stats, outb_trace, work;
     DBuf cur, bitmap, claims;
     // round-engine state (per query, grow-only)
-    DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_cand, rs_crep, rs_ncand, rs_repcnt,
-        rs_pool_id, rs_pool_q, rs_pool_rep, rs_pool_sim, rs_ctr, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused;
+    DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_repcnt, rs_pool_id, rs_pool_q, rs_pool_key,
+        rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, qbnd;
+    uint32_t* h_ctl = nullptr;   // pinned host mirror of the round control block
+    unsigned long long* h_zmin = nullptr;  // pinned host word: first zero query row
     int64_t rs_nq = 0;
     int rs_kt = 0, rs_L = 0;
     int64_t slots = 0;
@@ -335,6 +339,8 @@ struct pfg_index {
     ~pfg_index() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        if (h_ctl) cudaFreeHost(h_ctl);
+        if (h_zmin) cudaFreeHost(h_zmin);
     }
 };
 
@@ -594,6 +600,7 @@ pfg_status normalize_rows(const float* src, int64_t n, int d, float* dst, int dp
     PFG_CUDA(cudaMemsetAsync(zmin_dev, 0xff, 8, st));
     k_normalize<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(src, n, d, d, dst, dpad, zflag, zmin_dev);
     PFG_CUDA(cudaGetLastError());
+    if (!zrow) return PFG_OK;  // asynchronous: the caller reads zmin_dev later
     unsigned long long z = 0;
     PFG_CUDA(cudaMemcpyAsync(&z, zmin_dev, 8, cudaMemcpyDeviceToHost, st));
     PFG_CUDA(cudaStreamSynchronize(st));
@@ -677,6 +684,10 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     PFG_TRY(I->zmin.ensure(8, "zmin"));
     PFG_TRY(normalize_rows(qsrc, nq, g.d, I->qx.as<float>(), g.dpad, I->qzero.as<uint8_t>(),
                            I->zmin.as<unsigned long long>(), zrow, st));
+    if (!zrow) {
+        if (!I->h_zmin) PFG_CUDA(cudaMallocHost(&I->h_zmin, 8));
+        PFG_CUDA(cudaMemcpyAsync(I->h_zmin, I->zmin.p, 8, cudaMemcpyDeviceToHost, st));
+    }
     I->launches += 1;
     if (g.M > 0) {
         PFG_TRY(I->qsk.ensure((size_t)nq * g.M * 8, "query sketches"));
@@ -733,6 +744,15 @@ int query_occupancy(size_t smem) {
 }
 
 int epl_of(const Geo& g) { return std::max(1, g.dp / 32); }
+
+template <int EPL>
+pfg_status collect_setup(size_t smem, int* occ) {
+    PFG_CUDA(cudaFuncSetAttribute(k_collect<EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    PFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_collect<EPL>, 128, smem));
+    *occ = std::max(1, nb);
+    return PFG_OK;
+}
 
 }  // namespace
 }  // namespace pfg
@@ -855,9 +875,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(cudaEventRecord(I->ev[0], st));
     }
     I->launches = 0;
-    int64_t zrow = -1;
     bool lazy = false;
-    PFG_TRY(prep_queries(I, queries, nq, true, false, &zrow, &lazy, st));
+    PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st));
 
     const int k_eff = (int)std::min<int64_t>(k, g.n);
     const int kt = ((k_eff + 31) / 32) * 32;
@@ -884,12 +903,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->slots_bm = bm_words;
     }
     PFG_TRY(I->cur.ensure((size_t)nq * g.L * 16, "cursors"));
-    const bool rounds = s.engine == 0;
-    // round-engine limits (developer overrides): rounds continue while at least min_active queries
-    // are active, at most max_rounds times; the rest is finished by the fused kernel
+    const bool rounds = s.engine == 1;
+    // round-engine limits (developer overrides): at most max_rounds rounds (then the fused kernel
+    // finishes the remaining queries); the host checks the active count every sync_every rounds
     const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : 64;
-    const int min_active = getenv("PFG_MIN_ACTIVE") ? atoi(getenv("PFG_MIN_ACTIVE")) : 64;
-    const int ecap = kHMax, ccap = 4096;
+    const int sync_every = 4;
+    const int ecap = 2048;  // evaluated-list stride: kHMax committed + one scan step of slack
     const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
     if (rounds) {
         const size_t N = (size_t)nq;
@@ -897,13 +916,13 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_TRY(I->rs_flags.ensure(N * 4, "rs")); PFG_TRY(I->rs_tn.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_cnt.ensure(N * kCnt * 4, "rs")); PFG_TRY(I->rs_T.ensure(N * kt * 8, "rs"));
         PFG_TRY(I->rs_E.ensure(N * ecap * 4, "rs")); PFG_TRY(I->rs_pend.ensure(N * kMaxR * 16, "rs"));
-        PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs")); PFG_TRY(I->rs_crep.ensure(N * ccap, "rs"));
-        PFG_TRY(I->rs_ncand.ensure(N * 4, "rs")); PFG_TRY(I->rs_repcnt.ensure(N * kMaxR * 3 * 4, "rs"));
+        PFG_TRY(I->rs_repcnt.ensure(N * kMaxR * 3 * 4, "rs"));
         PFG_TRY(I->rs_pool_id.ensure((size_t)pool_cap * 4, "pool")); PFG_TRY(I->rs_pool_q.ensure((size_t)pool_cap * 4, "pool"));
-        PFG_TRY(I->rs_pool_rep.ensure((size_t)pool_cap, "pool")); PFG_TRY(I->rs_pool_sim.ensure((size_t)pool_cap * 4, "pool"));
-        PFG_TRY(I->rs_ctr.ensure(64, "rs counters")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_pool_key.ensure((size_t)pool_cap * 8, "pool"));
+        PFG_TRY(I->rs_ctl.ensure(sizeof(RoundCtl), "rs control")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_pn.ensure(N * 4, "rs")); PFG_TRY(I->rs_act0.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_act1.ensure(N * 4, "rs")); PFG_TRY(I->rs_fused.ensure(N * 4, "rs"));
+        if (!I->h_ctl) PFG_CUDA(cudaMallocHost(&I->h_ctl, sizeof(RoundCtl)));
     }
     PFG_TRY(I->work.ensure(8, "work counter"));
     PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
@@ -926,6 +945,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.d = g.d; p.dpad = g.dpad; p.K = g.K; p.L = g.L; p.M = g.M; p.B = s.B; p.R = s.R; p.k = k; p.k_eff = k_eff;
     p.per_round = s.per_round; p.use_filter = (s.use_filter && g.M > 0) ? 1 : 0; p.c = g.c; p.ell = g.ell; p.dp = g.dp;
     p.lazy = lazy ? 1 : 0; p.claim_cap = kClaimCap; p.trace_cap = s.trace_cap; p.kt = kt; p.smem_warp = smem_warp;
+    p.uniform = s.uniform;
     p.x = I->x.as<float>(); p.tab = I->tab.as<Entry>(); p.pt = I->pt.as<uint32_t>();
     p.slot = I->slot.as<uint8_t>(); p.qx = I->qx.as<float>(); p.qsk = I->qsk.as<uint64_t>();
     p.qcodes = I->qcodes.as<uint32_t>(); p.qc_n = I->qc_n; p.qc_ld = I->qc_ld;
@@ -933,12 +953,23 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.thr = thr->as<float>(); p.taub = taub->as<float>(); p.work = I->work.as<unsigned long long>();
     p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
     p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
+    // level-K match ranges of the first repetitions, one thread per (query, repetition)
+    p.qb_n = std::min(I->qc_n, kEagerReps);
+    p.qb_ld = p.qb_n;
+    if (p.qb_n > 0) {
+        PFG_TRY(I->qbnd.ensure((size_t)nq * p.qb_n * 16, "query bounds"));
+        p.qbnd = I->qbnd.as<uint4>();
+        const int64_t thr_n = nq * (int64_t)p.qb_n;
+        k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>());
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 1;
+    }
     // developer instrumentation: PFG_PHASE_PROF=1 prints per-phase warp cycles of each search to stderr
     static const bool phase_prof = getenv("PFG_PHASE_PROF") && getenv("PFG_PHASE_PROF")[0] == '1';
     DBuf profb;
     if (phase_prof) {
-        PFG_TRY(profb.alloc(8 * 8, "phase profile"));
-        PFG_CUDA(cudaMemsetAsync(profb.p, 0, 64, st));
+        PFG_TRY(profb.alloc(16 * 8, "phase profile"));
+        PFG_CUDA(cudaMemsetAsync(profb.p, 0, 128, st));
         p.prof = profb.as<unsigned long long>();
     }
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[1], st));
@@ -947,58 +978,66 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         RoundState& r = p.rs;
         r.lvl = I->rs_lvl.as<int32_t>(); r.c0 = I->rs_c0.as<int32_t>(); r.flags = I->rs_flags.as<int32_t>();
         r.tn = I->rs_tn.as<int32_t>(); r.cnt = I->rs_cnt.as<uint32_t>(); r.T = I->rs_T.as<uint64_t>();
-        r.E = I->rs_E.as<uint32_t>(); r.pend = I->rs_pend.as<uint4>(); r.cand = I->rs_cand.as<uint32_t>();
-        r.crep = I->rs_crep.as<uint8_t>(); r.ncand = I->rs_ncand.as<uint32_t>(); r.repcnt = I->rs_repcnt.as<uint32_t>();
+        r.E = I->rs_E.as<uint32_t>(); r.pend = I->rs_pend.as<uint4>(); r.repcnt = I->rs_repcnt.as<uint32_t>();
         r.pool_id = I->rs_pool_id.as<uint32_t>(); r.pool_q = I->rs_pool_q.as<uint32_t>();
-        r.pool_rep = I->rs_pool_rep.as<uint8_t>(); r.pool_sim = I->rs_pool_sim.as<float>();
-        uint32_t* ctr = I->rs_ctr.as<uint32_t>();  // [0] pool_top, [1] nnext, [2] nfused
-        r.pool_top = ctr; r.nnext = ctr + 1; r.nfused = ctr + 2;
+        r.pool_key = I->rs_pool_key.as<uint64_t>();
+        r.ctl = I->rs_ctl.as<RoundCtl>();
         r.poff = I->rs_poff.as<uint32_t>(); r.pn = I->rs_pn.as<uint32_t>();
-        r.active = I->rs_act0.as<uint32_t>(); r.next = I->rs_act1.as<uint32_t>(); r.fused = I->rs_fused.as<uint32_t>();
-        r.Ecap = ecap; r.Ccap = ccap; r.pool_cap = pool_cap;
-        PFG_CUDA(cudaMemsetAsync(ctr, 0, 16, st));
+        r.act[0] = I->rs_act0.as<uint32_t>(); r.act[1] = I->rs_act1.as<uint32_t>(); r.fused = I->rs_fused.as<uint32_t>();
+        r.Ecap = ecap; r.Ccap = ecap; r.pool_cap = pool_cap;
+        PFG_CUDA(cudaMemsetAsync(r.ctl, 0, sizeof(RoundCtl), st));
         k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p);
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
-        uint32_t hc[3];
-        PFG_CUDA(cudaMemcpyAsync(hc, ctr, 12, cudaMemcpyDeviceToHost, st));
-        PFG_CUDA(cudaStreamSynchronize(st));
-        uint32_t nact = hc[1];
-        std::swap(r.active, r.next);
-        const size_t csm = (size_t)collect_smem_bytes(g.dpad) * 4;
+        const size_t csm = (size_t)collect_smem_bytes(g.dpad, lazy) * 4;
         const size_t msm = (size_t)(align16((int)sizeof(MergeSmem)) + 2 * align16(kt * 8)) * 4;
         PFG_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+        int cocc = 1;
+        switch (epl) {
+            case 1: PFG_TRY(collect_setup<1>(csm, &cocc)); break;
+            case 2: PFG_TRY(collect_setup<2>(csm, &cocc)); break;
+            case 4: PFG_TRY(collect_setup<4>(csm, &cocc)); break;
+            case 8: PFG_TRY(collect_setup<8>(csm, &cocc)); break;
+            case 16: PFG_TRY(collect_setup<16>(csm, &cocc)); break;
+            default: PFG_TRY(collect_setup<32>(csm, &cocc)); break;
+        }
+        // grids: warp per active query, at most one resident wave (the kernels stride over the
+        // device-side active count, so no host synchronisation is needed between rounds)
+        const unsigned qb_c = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * cocc));
+        const unsigned qb_m = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * 16));
+        const unsigned sb = (unsigned)(I->num_sms * 2);
         int round = 0;
-        while (nact >= (uint32_t)std::max(1, min_active) && round < max_rounds) {
-            PFG_CUDA(cudaMemsetAsync(ctr, 0, 8, st));  // pool_top, nnext
-            const unsigned qb = (unsigned)std::min<int64_t>(((int64_t)nact + 3) / 4, (int64_t)I->num_sms * 16);
+        uint32_t nact = (uint32_t)nq;
+        while (round < max_rounds) {
+            const int par = round & 1;
             switch (epl) {
-                case 1: k_collect<1><<<qb, 128, csm, st>>>(p, nact); break;
-                case 2: k_collect<2><<<qb, 128, csm, st>>>(p, nact); break;
-                case 4: k_collect<4><<<qb, 128, csm, st>>>(p, nact); break;
-                case 8: k_collect<8><<<qb, 128, csm, st>>>(p, nact); break;
-                case 16: k_collect<16><<<qb, 128, csm, st>>>(p, nact); break;
-                default: k_collect<32><<<qb, 128, csm, st>>>(p, nact); break;
+                case 1: k_collect<1><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 2: k_collect<2><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 4: k_collect<4><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 8: k_collect<8><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 16: k_collect<16><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
+                default: k_collect<32><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
             }
-            k_dedupe<<<qb, 128, 0, st>>>(p, nact);
-            k_sims<<<(unsigned)(I->num_sms * 8), 256, 0, st>>>(p);
-            k_merge<<<qb, 128, msm, st>>>(p, nact);
+            k_sims<<<sb, 256, 0, st>>>(p, par);
+            k_merge<<<qb_m, 128, msm, st>>>(p, par);
             PFG_CUDA(cudaGetLastError());
-            I->launches += 4;
-            PFG_CUDA(cudaMemcpyAsync(hc, ctr, 12, cudaMemcpyDeviceToHost, st));
-            PFG_CUDA(cudaStreamSynchronize(st));
-            nact = hc[1];
-            std::swap(r.active, r.next);
+            I->launches += 3;
             ++round;
+            if (round % sync_every == 0 || round >= max_rounds) {
+                PFG_CUDA(cudaMemcpyAsync(I->h_ctl, r.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+                PFG_CUDA(cudaStreamSynchronize(st));
+                nact = I->h_ctl[round & 1];
+                if (nact == 0) break;
+            }
         }
         if (nact > 0) {
-            k_handoff<<<(nact + 255) / 256, 256, 0, st>>>(p, nact);
+            k_handoff<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, round & 1);
             PFG_CUDA(cudaGetLastError());
             I->launches += 1;
         }
-        PFG_CUDA(cudaMemcpyAsync(hc, ctr, 12, cudaMemcpyDeviceToHost, st));
+        PFG_CUDA(cudaMemcpyAsync(I->h_ctl, r.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
         PFG_CUDA(cudaStreamSynchronize(st));
-        fused_n = hc[2];
+        fused_n = I->h_ctl[4];
         p.qlist = r.fused;
         p.resume = 1;
         p.nq = fused_n;
@@ -1027,8 +1066,15 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(cudaMemcpyAsync(s.trace_ids, d_trace, (size_t)nq * s.trace_cap * 4, cudaMemcpyDeviceToHost, st));
     PFG_CUDA(cudaStreamSynchronize(st));
     if (phase_prof) {
-        unsigned long long h[8] = {0};
-        PFG_CUDA(cudaMemcpy(h, profb.p, 64, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[pfg phase] engine %d: rounds %d, queries finished by the fused kernel %lld of %lld\n", s.engine,
+                I->last_rounds, (long long)fused_n, (long long)nq);
+        unsigned long long h[16] = {0};
+        PFG_CUDA(cudaMemcpy(h, profb.p, 128, cudaMemcpyDeviceToHost));
+        if (h[14])
+            fprintf(stderr, "[pfg phase] collect per query-chunk: rebuild %.0f, codes+bounds %.0f, scan %.0f, epilogue %.0f cycles; "
+                    "max %.0f cycles; %.0f chunks, mean emitted %.1f, max emitted %llu\n",
+                    (double)h[8] / h[14], (double)h[9] / h[14], (double)h[10] / h[14], (double)h[11] / h[14], (double)h[12],
+                    (double)h[14], (double)h[13] / h[14], h[15]);
         const double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]);
         fprintf(stderr, "[pfg phase] Mcycles: bounds %.1f (%.0f%%) scan-load %.1f (%.0f%%) claim %.1f (%.0f%%) drain %.1f (%.0f%%, sims %.1f) lazy-hash %.1f (%.0f%%)\n",
                 h[0] / 1e6, 100 * h[0] / tot, h[1] / 1e6, 100 * h[1] / tot, h[2] / 1e6, 100 * h[2] / tot,
@@ -1040,7 +1086,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[1], I->ev[1], I->ev[2]));
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[2], I->ev[0], I->ev[2]));
     }
-    if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(zrow) + " is a zero vector");
+    if (*I->h_zmin != ~0ull)
+        return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(*I->h_zmin) + " is a zero vector");
     return PFG_OK;
 }
 

@@ -1,7 +1,6 @@
 """GPU <-> oracle parity through the C-ABI (BASELINE north_star tolerances):
 hash codes, tables, sketches and stop points bit-exact; returned ids and evaluated sets bit-exact
 given identical tables; similarities within 1e-5 absolute (expected bit-equal under R-2)."""
-import os
 
 import numpy as np
 import pytest
@@ -19,8 +18,6 @@ import paper_1906_12211_b200 as pfg  # noqa: E402
 
 DEV = torch.device("cuda:0")
 SIM_TOL = 1e-5
-# run the round engine even for small batches (it hands queries to the fused kernel below this)
-os.environ["PFG_MIN_ACTIVE"] = "1"
 
 
 def _cuda(a):
@@ -161,17 +158,19 @@ def test_round_engine_handoff_midway(cases, max_rounds, monkeypatch):
     # queries still running after a few rounds resume in the fused kernel from the saved state
     monkeypatch.setenv("PFG_MAX_ROUNDS", max_rounds)
     for name in ("hp", "fht"):
-        _compare(cases[name], 10, 0.99, dict(rep_chunk=4), dict(rep_chunk=4))
+        _compare(cases[name], 10, 0.99, dict(rep_chunk=4, engine=1), dict(rep_chunk=4))
 
 
 @pytest.mark.parametrize("name", ["hp", "fht"])
 @pytest.mark.parametrize("kw", [dict(use_filter=False), dict(stop_rule=1), dict(per_round=True),
                                 dict(segment=1), dict(segment=5, rep_chunk=3), dict(eps=0.2), dict(eps=-0.2),
-                                dict(rep_chunk=32)])
-def test_search_parity_options(cases, name, kw):
+                                dict(rep_chunk=32), dict(uniform_chunks=True),
+                                dict(uniform_chunks=True, rep_chunk=3, eps=0.1)])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_search_parity_options(cases, name, kw, engine):
     c = cases[name]
     okw = dict(kw)
-    _compare(c, 10, 0.9, kw, okw)
+    _compare(c, 10, 0.9, dict(kw, engine=engine), okw)
 
 
 @pytest.mark.parametrize("k", [1, 33, 100])
