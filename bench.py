@@ -229,7 +229,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--engine", type=int, default=0, help="0 = fused kernel, 1 = rounds + fused kernel")
+    ap.add_argument("--engine", type=int, default=0, help="0 = bulk rounds + fused kernel, 1 = fused kernel only")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -92,11 +92,14 @@ typedef struct {
     int32_t timing;           /* [0] 1: record CUDA events around the phases of this call on `stream`
                                  (read back with pfg_last_timing) */
     uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
-    int32_t engine;           /* [0] 0 = fused kernel (one warp per query, persistent grid);
-                                 1 = bulk-synchronous rounds (one chunk of every active query per round,
-                                 stragglers finished by the fused kernel).  Results are identical. */
+    int32_t engine;           /* [0] 0 = bulk rounds (one chunk of every active query per round, split
+                                 into data-parallel phases), then the fused kernel resumes the queries
+                                 still running; 1 = fused kernel only (one warp per query, persistent
+                                 grid).  Results are identical. */
     int32_t uniform_chunks;   /* [0] 1 = chunks of R repetitions from the start (tau = 64 for a whole
                                  first chunk); 0 = single-repetition chunks until k points are known */
+    int32_t rounds;           /* [4] engine 0: bulk rounds before the fused kernel resumes the rest */
+    int32_t reserved2;
 } pfg_search_opts;
 
 /* per-query counters (optional output of pfg_search) */

@@ -49,7 +49,8 @@ class SearchOpts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("rep_chunk", C.c_int32), ("segment", C.c_int32),
                 ("stop_rule", C.c_int32), ("stop_granularity", C.c_int32), ("use_filter", C.c_int32),
                 ("filter_eps", C.c_float), ("trace_cap", C.c_int32), ("timing", C.c_int32),
-                ("trace_ids", C.c_void_p), ("engine", C.c_int32), ("uniform_chunks", C.c_int32)]
+                ("trace_ids", C.c_void_p), ("engine", C.c_int32), ("uniform_chunks", C.c_int32),
+                ("rounds", C.c_int32), ("reserved2", C.c_int32)]
 
 
 class IndexInfo(C.Structure):
@@ -204,7 +205,7 @@ class Index:
 
     @staticmethod
     def _sopts(rep_chunk=8, segment=12, stop_rule=0, per_round=False, use_filter=True, eps=0.0,
-               trace_cap=0, trace_ptr=None, timing=False, engine=0, uniform_chunks=False) -> SearchOpts:
+               trace_cap=0, trace_ptr=None, timing=False, engine=0, uniform_chunks=False, rounds=0) -> SearchOpts:
         o = SearchOpts()
         o.struct_size = C.sizeof(SearchOpts)
         o.rep_chunk, o.segment, o.stop_rule = rep_chunk, segment, stop_rule
@@ -216,6 +217,7 @@ class Index:
         o.timing = int(timing)
         o.engine = int(engine)
         o.uniform_chunks = int(uniform_chunks)
+        o.rounds = int(rounds)
         return o
 
     def last_timing(self):

@@ -150,6 +150,80 @@ __device__ __forceinline__ uint32_t fhtcp_code_warp(const float* xrow, int d, in
     return ((uint32_t)(bv < 0.0f) << (ell - 1)) | (uint32_t)bi;
 }
 
+// FHT-CP repetition codes of repetitions c0 + r, r in [r0, nr), for one query row in shared memory
+// (independent strategy: repetition j concatenates functions j*c .. j*c + c - 1, MSB first, R-7).
+// The warp hashes 32/TPF repetitions at a time, one lane group per repetition: TPF = max(1, dp/32)
+// lanes per group, 32 coordinates per lane (coordinate u = sub*32 + i).  Stages h < 32 run in
+// registers; a stage h >= 32 pairs lane sub with sub ^ (h/32) (lower keeps a + b, upper a - b) --
+// the same butterflies in the same order as the oracle's radix-2 FHT, so codes are bit-identical
+// (R-6).  qc[r] receives the code of repetition c0 + r.  All lanes must call.
+template <int TPF>
+__device__ __forceinline__ void group_rep_codes(const float* qrow, int d, int dp, int ell, int c, int K,
+                                                const uint32_t* __restrict__ sg, int c0, int r0, int nr,
+                                                uint32_t* qc, int lane) {
+    constexpr int G = 32 / TPF;
+    const int g = lane / TPF, sub = lane % TPF;
+    const int hm = dp < 32 ? dp : 32;   // coordinates per lane that carry data
+    for (int rb = r0; rb < nr; rb += G) {
+        const int r = rb + g;
+        const bool valid = r < nr;
+        uint64_t full = 0;
+        for (int t = 0; t < c; ++t) {
+            const uint32_t* sf = sg + ((int64_t)(c0 + (valid ? r : r0)) * c + t) * 3 * TPF;
+            float y[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int u = sub * 32 + i;
+                y[i] = (u < d) ? qrow[u] : 0.0f;
+            }
+            for (int rr = 0; rr < 3; ++rr) {
+                const uint32_t wv = __ldg(sf + rr * TPF + sub);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) y[i] = __uint_as_float(__float_as_uint(y[i]) ^ ((wv << (31 - i)) & 0x80000000u));
+#pragma unroll
+                for (int h = 1; h < 32; h <<= 1) {
+                    if (h < hm) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (!(i & h)) {
+                                const float a = y[i], bb = y[i + h];
+                                y[i] = a + bb;
+                                y[i + h] = a - bb;
+                            }
+                    }
+                }
+#pragma unroll
+                for (int s = 1; s < TPF; s <<= 1) {
+                    const bool up = sub & s;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float o = __shfl_xor_sync(kFull, y[i], s);
+                        y[i] = up ? (o - y[i]) : (y[i] + o);
+                    }
+                }
+            }
+            int bi = 0;
+            float ba = fabsf(y[0]), bv = y[0];
+#pragma unroll
+            for (int i = 1; i < 32; ++i) {
+                const float a = fabsf(y[i]);
+                if (i < hm && a > ba) { ba = a; bi = i; bv = y[i]; }
+            }
+            bi += sub * 32;
+#pragma unroll
+            for (int s = 1; s < TPF; s <<= 1) {
+                const float oa = __shfl_xor_sync(kFull, ba, s);
+                const int oi = __shfl_xor_sync(kFull, bi, s);
+                const float ov = __shfl_xor_sync(kFull, bv, s);
+                if (oa > ba || (oa == ba && oi < bi)) { ba = oa; bi = oi; bv = ov; }
+            }
+            full = (full << ell) | (((uint32_t)(bv < 0.0f) << (ell - 1)) | (uint32_t)bi);
+        }
+        if (valid && sub == 0) qc[r] = (uint32_t)(full >> (c * ell - K));
+    }
+    __syncwarp();
+}
+
 // warp bitonic sort of one u64 per lane, descending across lanes (lane 0 = largest)
 __device__ __forceinline__ uint64_t warp_sort_desc(uint64_t key, int lane) {
 #pragma unroll

@@ -177,6 +177,83 @@ __global__ void __launch_bounds__(128) k_fht_qcodes(const float* __restrict__ X,
     codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
 }
 
+// Eager FHT-CP query codes, TPF threads per (row, repetition): the TPF consecutive lanes of a group
+// hold coordinate blocks [g*H, (g+1)*H) of the same vector (H = DP/TPF).  Stages h < H are in
+// registers; a stage h >= H pairs coordinate u of lane g with u + h of lane g + h/H (the lower lane
+// keeps a + b, the upper a - b: the oracle's butterfly, same operands, same rounding).  The argmax
+// combines the lanes' winners with ties to the lower index (R-6).
+template <int DP, int TPF>
+__global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
+                                                      int c, int K, const uint32_t* __restrict__ sg, int nreps,
+                                                      uint32_t* __restrict__ codes, int ldc) {
+    constexpr int H = DP / TPF, W = (DP + 31) / 32;
+    static_assert(H % 32 == 0 || TPF == 1, "a lane holds whole sign words");
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = (int)(t % TPF);
+    int64_t item = t / TPF;
+    const bool live = item < np * nreps;
+    if (!live) item = 0;  // keep the group's lanes in the shuffles; nothing is stored
+    const int64_t p = item / nreps;
+    const int j = (int)(item % nreps);
+    const float* xr = X + p * ldx;
+    uint64_t full = 0;
+    for (int f = 0; f < c; ++f) {
+        const uint32_t* sf = sg + ((int64_t)j * c + f) * 3 * W;
+        float y[H];
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const int u = g * H + i;
+            y[i] = (u < d) ? __ldg(xr + u) : 0.0f;
+        }
+#pragma unroll 1
+        for (int r = 0; r < 3; ++r) {
+#pragma unroll
+            for (int k = 0; k < H / 32; ++k) {
+                const uint32_t wv = __ldg(sf + r * W + g * (H / 32) + k);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    y[k * 32 + i] = __uint_as_float(__float_as_uint(y[k * 32 + i]) ^ ((wv << (31 - i)) & 0x80000000u));
+            }
+#pragma unroll
+            for (int h = 1; h < H; h <<= 1) {
+#pragma unroll
+                for (int i = 0; i < H; ++i)
+                    if (!(i & h)) {
+                        const float a = y[i], b = y[i + h];
+                        y[i] = a + b;
+                        y[i + h] = a - b;
+                    }
+            }
+#pragma unroll
+            for (int s = 1; s < TPF; s <<= 1) {
+                const bool up = g & s;
+#pragma unroll
+                for (int i = 0; i < H; ++i) {
+                    const float o = __shfl_xor_sync(kFull, y[i], s);
+                    y[i] = up ? (o - y[i]) : (y[i] + o);
+                }
+            }
+        }
+        int bi = 0;
+        float ba = fabsf(y[0]), bv = y[0];
+#pragma unroll
+        for (int i = 1; i < H; ++i) {
+            const float a = fabsf(y[i]);
+            if (a > ba) { ba = a; bi = i; bv = y[i]; }
+        }
+        bi += g * H;
+#pragma unroll
+        for (int s = 1; s < TPF; s <<= 1) {
+            const float oa = __shfl_xor_sync(kFull, ba, s);
+            const int oi = __shfl_xor_sync(kFull, bi, s);
+            const float ov = __shfl_xor_sync(kFull, bv, s);
+            if (oa > ba || (oa == ba && oi < bi)) { ba = oa; bi = oi; bv = ov; }
+        }
+        full = (full << ell) | (((uint32_t)(bv < 0.0f) << (ell - 1)) | (uint32_t)bi);
+    }
+    if (live && g == 0) codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
+}
+
 // FHT-CP codes of the m pool functions for every row: out [p][m] (uint16)
 template <int EPL>
 __global__ void __launch_bounds__(256) k_fht_funcs(const float* __restrict__ X, int64_t np, int ldx, int d,

@@ -52,7 +52,9 @@ struct RoundCtl {
     uint32_t nact[2];      // active-list counts (round parity)
     uint32_t pool_top[2];  // survivor-pool fill (round parity)
     uint32_t nfused;       // queries handed to the fused kernel
-    uint32_t pad[3];
+    uint32_t ntiles[2];    // scan tiles of the round (round parity)
+    uint32_t pad;
+    uint32_t wk[2][4];     // work counters of k_expand, k_scan, k_dedupe, k_merge (round parity)
 };
 struct RoundState {
     int32_t* lvl;       // [nq] next level i to process (K..1); 0 = only the i = 0 scan remains
@@ -63,7 +65,11 @@ struct RoundState {
     uint64_t* T;        // [nq][kt] top list keys
     uint32_t* E;        // [nq][Ecap] evaluated ids in evaluation order
     uint4* pend;        // [nq][kMaxR] cursors of the chunk in flight (committed by k_merge)
-    uint32_t* cand;     // [nq][Ccap] survivors of the chunk in flight, in evaluation order
+    uint32_t* cand;     // [nq][Ccap] candidate id per emitted position of the chunk (kEmpty = filtered)
+    uint8_t* crep;      // [nq][Ccap] repetition (within the chunk) of each emitted position
+    uint4* rseg;        // [nq][kMaxR] {lo_new, left length, hi_old, first position} per repetition
+    uint4* rinfo;       // [nq] {chunk repetitions, tau, emitted positions, 0}
+    uint2* tiles;       // scan tiles {query, tile}
     uint32_t* repcnt;   // [nq][kMaxR][3] emitted, filtered, dups per repetition of the chunk
     uint32_t* pool_id;  // survivor pool of the round: ids, owning query, (sim, id) keys
     uint32_t* pool_q;
@@ -413,8 +419,6 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
     const WarpSmem w = carve(smem_raw + wib * p.smem_warp, p);
     uint32_t* bm = p.bitmap + slot_id * p.bm_words;
     uint32_t* claims = p.claims + slot_id * (int64_t)p.claim_cap;
-    const int W = (p.dp + 31) >> 5;
-
     for (;;) {
         unsigned long long qv = 0;
         if (lane == 0) qv = atomicAdd(p.work, 1ull);
@@ -478,14 +482,10 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 const long long th0 = p.prof ? clock64() : 0;
                 if (i == p.K) {
                     if (lane < nr && c0 + lane < p.qc_n) w.f->qc[lane] = __ldg(p.qcodes + qi * p.qc_ld + c0 + lane);
-                    for (int r = 0; r < nr; ++r) {
-                        if (c0 + r < p.qc_n) continue;
-                        uint64_t full = 0;
-                        for (int t = 0; t < p.c; ++t) {
-                            const int64_t f = (int64_t)(c0 + r) * p.c + t;
-                            full = (full << p.ell) | fhtcp_code_warp<EPL>(w.qrow, p.d, p.dp, p.ell, p.sg + f * 3 * W, lane);
-                        }
-                        if (lane == 0) w.f->qc[r] = (uint32_t)(full >> (p.c * p.ell - p.K));
+                    const int r0 = max(0, p.qc_n - c0);
+                    if (r0 < nr) {
+                        __syncwarp();
+                        group_rep_codes<EPL>(w.qrow, p.d, p.dp, p.ell, p.c, p.K, p.sg, c0, r0, nr, w.f->qc, lane);
                     }
                     __syncwarp();
                 }

@@ -6,10 +6,12 @@
 //   k_qbounds  per (query, repetition < qb_n): the level-K match range [a_K, b_K) by two
 //              interleaved binary searches (once per search, before the rounds)
 //   k_rinit    per query: state init; zero query rows answered directly
-//   k_collect  warp per active query: chunk codes, widening (R-12), scan of the emitted table
-//              entries in (repetition, position) order with the sketch filter, and the dedupe
-//              claims against a shared-memory hash set rebuilt from the query's evaluated list
-//              (R-17/R-18) -> survivors appended to the evaluated list and to the round's pool
+//   k_expand   warp per active query: the chunk, its tau, chunk codes, emitted ranges (R-12),
+//              pending cursors, and the query's scan tiles of 128 positions
+//   k_scan     warp per tile (fully data-parallel): table entries + sketch filter -> candidates
+//   k_dedupe   warp per active query: claims in (repetition, position) order against a
+//              shared-memory hash set rebuilt from the query's evaluated list (R-17/R-18) ->
+//              survivors appended to the evaluated list and to the round's pool
 //   k_sims     grid over the pool: warp-coalesced rows, 32-lane tree (R-2) -> (sim, id) keys
 //   k_merge    warp per active query: merge repetition by repetition into the top list, stop check
 //              after each repetition (Alg. 1 line 8), commit cursors / advance, or finish
@@ -21,7 +23,7 @@
 // chunk not yet committed.
 //
 // Round r uses parity par = r & 1: it reads active list act[par] (count ctl->nact[par]) and the
-// pool counter ctl->pool_top[par]; k_collect resets the other parity's counters, k_merge fills
+// pool counter ctl->pool_top[par]; k_expand resets the other parity's counters, k_merge fills
 // act[par ^ 1].  No host synchronisation is needed between rounds.
 #pragma once
 #include "kernels_query.cuh"
@@ -42,6 +44,14 @@ __device__ __forceinline__ int tau_of_state(const QueryParams& p, int tn, const 
 
 
 __device__ __forceinline__ void push(uint32_t* list, uint32_t* n, uint32_t q) { list[atomicAdd(n, 1u)] = q; }
+
+// dynamic work distribution: the warp takes the next item from a counter (lane 0 draws, all
+// lanes get it), so a warp that drew expensive items does not hold the kernel's tail
+__device__ __forceinline__ uint32_t next_item(uint32_t* ctr, int lane) {
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1u);
+    return __shfl_sync(kFull, v, 0);
+}
 
 // ---------------------------------------------------------------------------------------------
 // level-K match ranges: a = lower_bound(code_j), b = lower_bound(code_j + 1) in
@@ -77,6 +87,25 @@ __global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restric
     out[q * p.qb_ld + j] = make_uint4(lo1, lo2, probes, 0u);
 }
 
+// Processing order for the fused kernel (longest first, so the persistent grid's tail is short):
+// key = (~estimated cost) << 32 | q, the cost being the number of table entries the query's level-K
+// match ranges of the first qb_n repetitions hold (the entries it will scan there).
+__global__ void k_qorder_keys(QueryParams p, uint64_t* __restrict__ keys) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= p.nq) return;
+    uint64_t cost = 0;
+    for (int j = 0; j < p.qb_n; ++j) {
+        const uint4 b = __ldg(p.qbnd + q * p.qb_ld + j);
+        cost += b.y - b.x;
+    }
+    const uint32_t c32 = cost > 0xffffffffull ? 0xffffffffu : (uint32_t)cost;
+    keys[q] = ((uint64_t)(~c32) << 32) | (uint64_t)q;
+}
+__global__ void k_qorder_list(const uint64_t* __restrict__ keys, int64_t nq, uint32_t* __restrict__ qlist) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nq) qlist[t] = (uint32_t)keys[t];
+}
+
 // ---------------------------------------------------------------------------------------------
 __global__ void k_rinit(QueryParams p) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -97,75 +126,48 @@ __global__ void k_rinit(QueryParams p) {
 }
 
 // ---------------------------------------------------------------------------------------------
-struct CollectSmem {
-    uint32_t hs[kHC];          // evaluated-id hash set
-    uint64_t qsk[64];
-    uint32_t beg[kMaxR + 4];
-    uint32_t lo_new[kMaxR], lo_old[kMaxR], hi_old[kMaxR], qc[kMaxR], bnd[2 * kMaxR], fcnt[kMaxR], dcnt[kMaxR];
+// k_expand: warp per active query.  The chunk (chunk_reps), its tau, the query codes of the chunk
+// (precomputed, or hashed here), the emitted ranges of every repetition (level K: the match range
+// rounded up to whole segments; deeper levels: the segment loop, R-12), the pending cursors, and
+// the scan tiles of 128 positions (positions in (repetition, position) order).
+struct ExpandSmem {
+    uint32_t qc[kMaxR], bnd[2 * kMaxR];
 };
-__host__ __device__ inline int collect_smem_bytes(int dpad, bool lazy) {
-    return align16((int)sizeof(CollectSmem)) + (lazy ? align16(dpad * 4) : 0);
+__host__ __device__ inline int expand_smem_bytes(int dpad, bool lazy) {
+    return align16((int)sizeof(ExpandSmem)) + (lazy ? align16(dpad * 4) : 0);
 }
+constexpr int kTile = 128;
 
 template <int EPL>
-__global__ void __launch_bounds__(128) k_collect(QueryParams p, int par, int lazy) {
+__global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    CollectSmem* c = (CollectSmem*)(smem_raw + wib * collect_smem_bytes(p.dpad, lazy));
-    float* qrow = (float*)((unsigned char*)c + align16((int)sizeof(CollectSmem)));
+    ExpandSmem* c = (ExpandSmem*)(smem_raw + wib * expand_smem_bytes(p.dpad, lazy));
+    float* qrow = (float*)((unsigned char*)c + align16((int)sizeof(ExpandSmem)));
     const RoundState& rs = p.rs;
     const uint32_t nact = rs.ctl->nact[par];
-    if (blockIdx.x == 0 && threadIdx.x == 0) { rs.ctl->nact[par ^ 1] = 0; rs.ctl->pool_top[par ^ 1] = 0; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        rs.ctl->nact[par ^ 1] = 0; rs.ctl->pool_top[par ^ 1] = 0; rs.ctl->ntiles[par ^ 1] = 0;
+        for (int t = 0; t < 4; ++t) rs.ctl->wk[par ^ 1][t] = 0;
+    }
     const uint32_t* act = rs.act[par];
-    const int W = (p.dp + 31) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nact; a += nw) {
         const int64_t q = act[a];
-        long long tq0 = p.prof ? clock64() : 0, tq = tq0;
         const int i = rs.lvl[q], c0 = rs.c0[q], tn = rs.tn[q];
         const int nr = chunk_reps(p, i, c0, tn, rs.T + q * p.kt, lane);
         const int tau = tau_of_state(p, tn, rs.T + q * p.kt);
-        const uint32_t nE = rs.cnt[q * kCnt + 3];
-        uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
         uint4* cur = p.cur + q * p.L;
-        for (int t = lane; t < p.M; t += 32) c->qsk[t] = p.qsk[q * p.M + t];
-        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-        const bool need_lazy = (i == p.K) && (c0 + nr > p.qc_n);
-        if (need_lazy)
-            for (int t = lane; t < p.dpad; t += 32) qrow[t] = p.qx[q * p.dpad + t];
-        if (lane < nr) { c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
-        __syncwarp();
-        // rebuild the evaluated-id hash set (ids are distinct; kEPre loads per lane in flight)
-        for (uint32_t e0 = 0; e0 < nE; e0 += 32 * kEPre) {
-            uint32_t v[kEPre];
-#pragma unroll
-            for (int u = 0; u < kEPre; ++u) {
-                const uint32_t e = e0 + u * 32 + lane;
-                v[u] = e < nE ? E[e] : kEmpty;
-            }
-#pragma unroll
-            for (int u = 0; u < kEPre; ++u)
-                if (v[u] != kEmpty) {
-                    uint32_t h = hs_slot(v[u]);
-                    while (atomicCAS(&c->hs[h], kEmpty, v[u]) != kEmpty) h = hs_next(h);
-                }
-        }
-        if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 8, (unsigned long long)(t - tq)); tq = t; }
         uint32_t probes = 0;
         if (i == p.K) {
             if (lane < nr && c0 + lane < p.qc_n) c->qc[lane] = __ldg(p.qcodes + q * p.qc_ld + c0 + lane);
-            for (int r = 0; r < nr; ++r) {
-                if (c0 + r < p.qc_n) continue;
-                uint64_t full = 0;
-                for (int t = 0; t < p.c; ++t) {
-                    const int64_t f = (int64_t)(c0 + r) * p.c + t;
-                    full = (full << p.ell) | fhtcp_code_warp<EPL>(qrow, p.d, p.dp, p.ell, p.sg + f * 3 * W, lane);
-                }
-                if (lane == 0) c->qc[r] = (uint32_t)(full >> (p.c * p.ell - p.K));
+            if (c0 + nr > p.qc_n) {
+                for (int t = lane; t < p.dpad; t += 32) qrow[t] = p.qx[q * p.dpad + t];
+                __syncwarp();
+                group_rep_codes<EPL>(qrow, p.d, p.dp, p.ell, p.c, p.K, p.sg, c0, max(0, p.qc_n - c0), nr, c->qc, lane);
             }
             __syncwarp();
         }
-        // widening, as k_query (first level: precomputed match ranges or binary search)
         for (int task = lane; task < 2 * nr; task += 32) {
             const bool left = task < nr;
             const int r = left ? task : task - nr;
@@ -203,10 +205,9 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, int par, int laz
             }
         }
         __syncwarp();
-        uint32_t em = 0;
+        uint32_t em = 0, nelo = 0, elo = 0, ehi = 0, nehi = 0;
         if (lane < nr) {
             const int j = c0 + lane;
-            uint32_t elo, ehi, nelo, nehi;
             if (i == p.K) {
                 const uint32_t a_ = c->bnd[lane], b_ = c->bnd[nr + lane];
                 const uint32_t B = (uint32_t)p.B;
@@ -218,7 +219,6 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, int par, int laz
                 elo = cu.y; ehi = cu.z;
                 nelo = c->bnd[lane]; nehi = c->bnd[nr + lane];
             }
-            c->lo_new[lane] = nelo; c->lo_old[lane] = elo; c->hi_old[lane] = ehi;
             em = (elo - nelo) + (nehi - ehi);
             rs.pend[q * kMaxR + lane] = make_uint4(c->qc[lane], nelo, nehi, 0u);
         }
@@ -228,71 +228,196 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, int par, int laz
             const uint32_t o = __shfl_up_sync(kFull, incl, off);
             if (lane >= off) incl += o;
         }
-        if (lane < nr) c->beg[lane + 1] = incl;
-        if (lane == 0) c->beg[0] = 0;
+        const uint32_t total = __shfl_sync(kFull, incl, nr - 1);
+        // segment r: positions [beg_r, beg_r + em_r): lenA from lo_new, the rest from hi_old
+        if (lane < nr) rs.rseg[q * kMaxR + lane] = make_uint4(nelo, elo - nelo, ehi, incl - em);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) probes += __shfl_xor_sync(kFull, probes, off);
+        const bool over = total > (uint32_t)rs.Ccap;
+        const uint32_t ntl = over ? 0u : (total + kTile - 1) / kTile;
+        uint32_t base = 0;
+        if (lane == 0) {
+            rs.rinfo[q] = make_uint4((uint32_t)nr, (uint32_t)tau, total, 0u);
+            rs.cnt[q * kCnt + 4] += probes;
+            if (over) rs.flags[q] |= kFlagFused;
+            if (ntl) base = atomicAdd(&rs.ctl->ntiles[par], ntl);
+        }
+        base = __shfl_sync(kFull, base, 0);
+        for (uint32_t t = lane; t < ntl; t += 32) rs.tiles[base + t] = make_uint2((uint32_t)q, t);
         __syncwarp();
-        if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 9, (unsigned long long)(t - tq)); tq = t; }
-        const uint32_t total = c->beg[nr];
-        // scan in (rep, position) order: filter, then claim in order through the hash set; fresh
-        // ids are appended to the evaluated list (room up to Ecap; beyond kHMax the query is
-        // handed to the fused kernel, whose bitmap mode has no limit)
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_scan: warp per tile of 128 emitted positions of one query: load the 16-byte entries, apply
+// the sketch filter with the query's chunk tau; cand[g] = id, or kEmpty if
+// the filter rejects position g.  Fully data-parallel (no order dependence).
+struct ScanSmem {
+    uint64_t qsk[64];
+    uint4 seg[kMaxR];
+};
+
+__global__ void __launch_bounds__(256) k_scan(QueryParams p, int par) {
+    __shared__ ScanSmem sm_all[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    ScanSmem* c = &sm_all[wib];
+    const RoundState& rs = p.rs;
+    const uint32_t ntiles = rs.ctl->ntiles[par];
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < ntiles; a += nw) {
+        const uint2 tl = rs.tiles[a];
+        const int64_t q = tl.x;
+        const uint4 info = rs.rinfo[q];
+        const int nr = (int)info.x, tau = (int)info.y;
+        const uint32_t total = info.z;
+        const int c0 = rs.c0[q];
+        if (lane < nr) c->seg[lane] = rs.rseg[q * kMaxR + lane];
+        if (p.use_filter)
+            for (int t = lane; t < p.M; t += 32) c->qsk[t] = p.qsk[q * p.M + t];
+        __syncwarp();
+        uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
+        uint8_t* crep = rs.crep + q * (int64_t)rs.Ccap;
+        const uint32_t g0 = tl.y * kTile;
+        int rl = 0;
+        uint4 e[kTile / 32];
+        int rv[kTile / 32];
+#pragma unroll
+        for (int u = 0; u < kTile / 32; ++u) {
+            const uint32_t g = g0 + u * 32 + lane;
+            rv[u] = 0;
+            if (g < total) {
+                while (rl + 1 < nr && c->seg[rl + 1].w <= g) ++rl;
+                const uint4 sg = c->seg[rl];
+                const uint32_t o = g - sg.w;
+                const uint32_t pos = (o < sg.y) ? sg.x + o : sg.z + (o - sg.y);
+                e[u] = __ldg(reinterpret_cast<const uint4*>(p.tab + (int64_t)(c0 + rl) * p.n + pos));
+                rv[u] = rl;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kTile / 32; ++u) {
+            const uint32_t g = g0 + u * 32 + lane;
+            if (g < total) {
+                bool pass = true;
+                if (p.use_filter) {
+                    const int s_ = __ldg(p.slot + c0 + rv[u]);
+                    pass = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ c->qsk[s_]) <= tau;
+                }
+                cand[g] = pass ? e[u].x : kEmpty;
+                crep[g] = (uint8_t)rv[u];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_dedupe: warp per active query.  Rebuild the evaluated-id hash set from the query's evaluated
+// list, then walk the chunk's candidates in (repetition, position) order: filtered positions and
+// duplicates are counted per repetition, fresh ids are claimed in order (R-17/R-18), appended to
+// the evaluated list and to the round's pool.
+struct DedupeSmem {
+    uint32_t hs[kHC];
+    uint32_t beg[kMaxR + 1];
+    uint32_t fcnt[kMaxR], dcnt[kMaxR];
+};
+constexpr int kCPre = 8;   // candidate ids loaded per lane per batch
+
+__global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    DedupeSmem* c = (DedupeSmem*)(smem_raw + wib * align16((int)sizeof(DedupeSmem)));
+    const RoundState& rs = p.rs;
+    const uint32_t nact = rs.ctl->nact[par];
+    const uint32_t* act = rs.act[par];
+    for (uint32_t a = next_item(&rs.ctl->wk[par][2], lane); a < nact; a = next_item(&rs.ctl->wk[par][2], lane)) {
+        const int64_t q = act[a];
+        if (rs.flags[q] & kFlagFused) continue;
+        const uint4 info = rs.rinfo[q];
+        const int nr = (int)info.x;
+        const uint32_t total = info.z;
+        const uint32_t nE = rs.cnt[q * kCnt + 3];
+        uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
+        const uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
+        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        if (lane < nr) { c->beg[lane] = rs.rseg[q * kMaxR + lane].w; c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
+        if (lane == 0) c->beg[nr] = total;
+        __syncwarp();
+        for (uint32_t e0 = 0; e0 < nE; e0 += 32 * kEPre) {
+            uint32_t v[kEPre];
+#pragma unroll
+            for (int u = 0; u < kEPre; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                v[u] = e < nE ? E[e] : kEmpty;
+            }
+#pragma unroll
+            for (int u = 0; u < kEPre; ++u)
+                if (v[u] != kEmpty) {
+                    uint32_t h = hs_slot(v[u]);
+                    while (atomicCAS(&c->hs[h], kEmpty, v[u]) != kEmpty) h = hs_next(h);
+                }
+        }
+        __syncwarp();
         uint32_t ns = 0;
         bool overflow = false;
-        int rl = 0;
-        for (uint32_t g0 = 0; g0 < total; g0 += 32 * kU) {
-            uint32_t idv[kU];
-            int rv[kU];
-            bool pass[kU];
+        const uint8_t* crep = rs.crep + q * (int64_t)rs.Ccap;
+        for (uint32_t g0 = 0; g0 < total && !overflow; g0 += 32 * kCPre) {
+            uint32_t v[kCPre], h[kCPre];
+            int rr[kCPre];
+            bool found[kCPre];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
+            for (int u = 0; u < kCPre; ++u) {
                 const uint32_t g = g0 + u * 32 + lane;
-                pass[u] = false; rv[u] = 0; idv[u] = 0;
-                if (g < total) {
-                    while (rl + 1 < nr && c->beg[rl + 1] <= g) ++rl;
-                    const int r = rl;
-                    const uint32_t o = g - c->beg[r];
-                    const uint32_t lenA = c->lo_old[r] - c->lo_new[r];
-                    const uint32_t pos = (o < lenA) ? c->lo_new[r] + o : c->hi_old[r] + (o - lenA);
-                    const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.tab + (int64_t)(c0 + r) * p.n + pos));
-                    idv[u] = e.x; rv[u] = r; pass[u] = true;
-                    if (p.use_filter) {
-                        const int s_ = __ldg(p.slot + c0 + r);
-                        pass[u] = __popcll((((uint64_t)e.w << 32) | e.z) ^ c->qsk[s_]) <= tau;
+                const bool live = g < total;
+                v[u] = live ? cand[g] : kEmpty;
+                rr[u] = live ? (int)crep[g] : -1;
+            }
+            // membership in the set as it stands before this batch: independent read-only probes
+#pragma unroll
+            for (int u = 0; u < kCPre; ++u) {
+                found[u] = false;
+                h[u] = hs_slot(v[u]);
+                if (v[u] != kEmpty) {
+                    for (;;) {
+                        const uint32_t x = c->hs[h[u]];
+                        if (x == v[u]) { found[u] = true; break; }
+                        if (x == kEmpty) break;
+                        h[u] = hs_next(h[u]);
                     }
                 }
             }
+            // claims of the rest in (repetition, position) order: lanes in order within u (the
+            // first lane of a group of equal ids claims), u in order; a later occurrence of an id
+            // claimed earlier in the batch finds it in the set
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const uint32_t g = g0 + u * 32 + lane;
-                if (g < total && !pass[u]) atomicAdd(&c->fcnt[rv[u]], 1u);
-                const uint32_t pm = __ballot_sync(kFull, pass[u]);
+            for (int u = 0; u < kCPre; ++u) {
+                const bool pass = v[u] != kEmpty;
+                const bool need = pass && !found[u];
+                const uint32_t nm = __ballot_sync(kFull, need);
                 bool fresh = false;
-                if (pass[u]) {
-                    const uint32_t grp = __match_any_sync(pm, idv[u]);
+                if (need) {
+                    const uint32_t grp = __match_any_sync(nm, v[u]);
                     if ((int)(__ffs(grp) - 1) == lane) {
-                        uint32_t h = hs_slot(idv[u]);
+                        uint32_t hh = h[u];
                         for (;;) {
-                            const uint32_t old = atomicCAS(&c->hs[h], kEmpty, idv[u]);
+                            const uint32_t old = atomicCAS(&c->hs[hh], kEmpty, v[u]);
                             if (old == kEmpty) { fresh = true; break; }
-                            if (old == idv[u]) break;
-                            h = hs_next(h);
+                            if (old == v[u]) break;
+                            hh = hs_next(hh);
                         }
                     }
-                    if (!fresh) atomicAdd(&c->dcnt[rv[u]], 1u);
+                }
+                if (rr[u] >= 0) {
+                    if (!pass) atomicAdd(&c->fcnt[rr[u]], 1u);
+                    else if (!fresh) atomicAdd(&c->dcnt[rr[u]], 1u);
                 }
                 const uint32_t fm = __ballot_sync(kFull, fresh);
-                if (fresh) E[nE + ns + __popc(fm & lanemask_lt())] = idv[u];
+                if (fresh) E[nE + ns + __popc(fm & lanemask_lt())] = v[u];
                 ns += __popc(fm);
             }
-            if (nE + ns > (uint32_t)kHMax) { overflow = true; break; }
+            if (nE + ns > (uint32_t)kHMax) overflow = true;
         }
         __syncwarp();
-        if (p.prof && lane == 0) {
-            const long long t = clock64(); atomicAdd(p.prof + 10, (unsigned long long)(t - tq)); tq = t;
-            atomicAdd(p.prof + 13, (unsigned long long)total);
-        }
         uint32_t base = 0;
         if (!overflow && lane == 0) base = atomicAdd(&rs.ctl->pool_top[par], ns);
         base = __shfl_sync(kFull, base, 0);
@@ -321,18 +446,8 @@ __global__ void __launch_bounds__(128) k_collect(QueryParams p, int par, int laz
             rc[1] = c->fcnt[lane];
             rc[2] = c->dcnt[lane];
         }
-        if (lane == 0) {
-            rs.poff[q] = base;
-            rs.pn[q] = ns;
-            rs.cnt[q * kCnt + 4] += probes;
-        }
+        if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }
         __syncwarp();
-        if (p.prof && lane == 0) {
-            const long long t = clock64(); atomicAdd(p.prof + 11, (unsigned long long)(t - tq));
-            atomicMax(p.prof + 12, (unsigned long long)(t - tq0));
-            atomicAdd(p.prof + 14, 1ull);
-            atomicMax(p.prof + 15, (unsigned long long)total);
-        }
     }
 }
 
@@ -441,7 +556,7 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
         }
         const int i = rs.lvl[q], c0 = rs.c0[q];
         int tn = rs.tn[q];
-        const int nr = chunk_reps(p, i, c0, tn, rs.T + q * p.kt, lane);
+        const int nr = (int)rs.rinfo[q].x;  // the chunk k_expand chose (chunk_reps)
         for (int t = lane; t < tn; t += 32) T0[t] = rs.T[q * p.kt + t];
         uint64_t* T = T0;
         uint64_t* Tn = T1;

@@ -262,7 +262,7 @@ int tau_of(float ipk, float eps) {
 }
 
 struct SearchCfg {
-    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0, engine = 0, uniform = 0;
+    int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0, engine = 0, uniform = 0, rounds = 0;
     float eps = 0.0f;
     uint32_t* trace_ids = nullptr;
 };
@@ -290,7 +290,9 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     s.trace_ids = z.trace_ids;
     s.timing = z.timing;
     s.engine = z.engine;
-    if (s.engine < 0 || s.engine > 1) return fail(PFG_E_ARG, "engine must be 0 (fused) or 1 (rounds + fused)");
+    if (s.engine < 0 || s.engine > 1) return fail(PFG_E_ARG, "engine must be 0 (rounds + fused) or 1 (fused)");
+    s.rounds = z.rounds;
+    if (s.rounds < 0 || s.rounds > 4096) return fail(PFG_E_ARG, "rounds must be in [0, 4096]");
     s.uniform = z.uniform_chunks;
     if (s.uniform != 0 && s.uniform != 1) return fail(PFG_E_ARG, "uniform_chunks must be 0 or 1");
     if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
@@ -317,11 +319,14 @@ struct pfg_index {
     std::map<uint32_t, std::shared_ptr<DBuf>> tau_cache;
     // per-call scratch (grow-only)
     DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, outb_ids, outb_sims, outb_stats, outb_trace, work;
+    DBuf qord_keys, qord_sorted, qord_list, qord_temp;  // longest-first processing order (fused engine)
     DBuf cur, bitmap, claims;
     // round-engine state (per query, grow-only)
     DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_repcnt, rs_pool_id, rs_pool_q, rs_pool_key,
-        rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, qbnd;
+        rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, rs_cand, rs_crep, rs_rseg, rs_rinfo, rs_tiles, qbnd;
     uint32_t* h_ctl = nullptr;   // pinned host mirror of the round control block
+    cudaStream_t aux = nullptr;  // second stream: query sketches run beside the query hashing
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     unsigned long long* h_zmin = nullptr;  // pinned host word: first zero query row
     int64_t rs_nq = 0;
     int rs_kt = 0, rs_L = 0;
@@ -340,6 +345,9 @@ struct pfg_index {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (h_ctl) cudaFreeHost(h_ctl);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (aux) cudaStreamDestroy(aux);
         if (h_zmin) cudaFreeHost(h_zmin);
     }
 };
@@ -349,6 +357,9 @@ namespace {
 
 constexpr int kClaimCap = 8192;
 constexpr int kEagerReps = 32;
+#ifndef PFG_QTPF
+#define PFG_QTPF 1   // threads per function of the eager FHT-CP query hashing at d' = 128
+#endif
 
 template <int EPL>
 void launch_fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps,
@@ -690,10 +701,20 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     }
     I->launches += 1;
     if (g.M > 0) {
+        // sketches (FMA pipe) on the second stream, concurrently with the hashing below; the
+        // caller joins (join_sketches) before anything reads them
         PFG_TRY(I->qsk.ensure((size_t)nq * g.M * 8, "query sketches"));
+        if (!I->aux) {
+            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
+            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
+            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
+        }
+        PFG_CUDA(cudaEventRecord(I->ev_fork, st));
+        PFG_CUDA(cudaStreamWaitEvent(I->aux, I->ev_fork, 0));
         hp_bits(I->qx.as<float>(), nq, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->qsk.as<uint8_t>(),
-                (int64_t)g.M * 8, st);
+                (int64_t)g.M * 8, I->aux);
         PFG_CUDA(cudaGetLastError());
+        PFG_CUDA(cudaEventRecord(I->ev_join, I->aux));
         I->launches += 1;
     }
     *lazy = (g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT && !force_codes);
@@ -716,12 +737,19 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         uint32_t* qc = I->qcodes.as<uint32_t>();
         if (g.dp == 32) k_fht_qcodes<32><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
         else if (g.dp == 64) k_fht_qcodes<64><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
-        else k_fht_qcodes<128><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
+        else k_fht_qcodes_g<128, PFG_QTPF><<<(unsigned)((PFG_QTPF * threads + 127) / 128), 128, 0, st>>>(
+                 I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
         I->qc_n = ne;
         I->qc_ld = ne;
     }
+    return PFG_OK;
+}
+
+// the query sketches of prep_queries are ready on `st` after this
+pfg_status join_sketches(pfg_index* I, cudaStream_t st) {
+    if (I->g.M > 0 && I->ev_join) PFG_CUDA(cudaStreamWaitEvent(st, I->ev_join, 0));
     return PFG_OK;
 }
 
@@ -745,14 +773,6 @@ int query_occupancy(size_t smem) {
 
 int epl_of(const Geo& g) { return std::max(1, g.dp / 32); }
 
-template <int EPL>
-pfg_status collect_setup(size_t smem, int* occ) {
-    PFG_CUDA(cudaFuncSetAttribute(k_collect<EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int nb = 0;
-    PFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_collect<EPL>, 128, smem));
-    *occ = std::max(1, nb);
-    return PFG_OK;
-}
 
 }  // namespace
 }  // namespace pfg
@@ -903,12 +923,16 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->slots_bm = bm_words;
     }
     PFG_TRY(I->cur.ensure((size_t)nq * g.L * 16, "cursors"));
-    const bool rounds = s.engine == 1;
-    // round-engine limits (developer overrides): at most max_rounds rounds (then the fused kernel
-    // finishes the remaining queries); the host checks the active count every sync_every rounds
-    const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : 64;
-    const int sync_every = 4;
-    const int ecap = 2048;  // evaluated-list stride: kHMax committed + one scan step of slack
+    const bool rounds = s.engine == 0;
+    // round engine: `rounds` bulk rounds (search option, default 4), then the fused kernel resumes
+    // every query still running (stragglers keep their hash set in shared memory across chunks
+    // there, instead of paying a round's fixed latency per chunk).  The rounds are enqueued
+    // without host synchronisation; the host checks the active count every sync_every rounds
+    // only to stop early when every query has finished.
+    const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : (s.rounds > 0 ? s.rounds : 4);
+    const int sync_every = 8;
+    const int ecap = 2048;  // evaluated-list stride: kHMax committed + one batch of slack
+    const int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
     const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
     if (rounds) {
         const size_t N = (size_t)nq;
@@ -922,6 +946,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_TRY(I->rs_ctl.ensure(sizeof(RoundCtl), "rs control")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_pn.ensure(N * 4, "rs")); PFG_TRY(I->rs_act0.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_act1.ensure(N * 4, "rs")); PFG_TRY(I->rs_fused.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs candidates")); PFG_TRY(I->rs_crep.ensure(N * ccap, "rs candidates")); PFG_TRY(I->rs_rseg.ensure(N * kMaxR * 16, "rs"));
+        PFG_TRY(I->rs_rinfo.ensure(N * 16, "rs")); PFG_TRY(I->rs_tiles.ensure(N * (ccap / kTile) * 8, "rs tiles"));
         if (!I->h_ctl) PFG_CUDA(cudaMallocHost(&I->h_ctl, sizeof(RoundCtl)));
     }
     PFG_TRY(I->work.ensure(8, "work counter"));
@@ -954,7 +980,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
     p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
     // level-K match ranges of the first repetitions, one thread per (query, repetition)
-    p.qb_n = std::min(I->qc_n, kEagerReps);
+    p.qb_n = getenv("PFG_NO_QB") ? 0 : std::min(I->qc_n, kEagerReps);
     p.qb_ld = p.qb_n;
     if (p.qb_n > 0) {
         PFG_TRY(I->qbnd.ensure((size_t)nq * p.qb_n * 16, "query bounds"));
@@ -972,6 +998,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(cudaMemsetAsync(profb.p, 0, 128, st));
         p.prof = profb.as<unsigned long long>();
     }
+    PFG_TRY(join_sketches(I, st));
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[1], st));
     int64_t fused_n = nq;
     if (rounds) {
@@ -984,44 +1011,45 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         r.ctl = I->rs_ctl.as<RoundCtl>();
         r.poff = I->rs_poff.as<uint32_t>(); r.pn = I->rs_pn.as<uint32_t>();
         r.act[0] = I->rs_act0.as<uint32_t>(); r.act[1] = I->rs_act1.as<uint32_t>(); r.fused = I->rs_fused.as<uint32_t>();
-        r.Ecap = ecap; r.Ccap = ecap; r.pool_cap = pool_cap;
+        r.Ecap = ecap; r.Ccap = ccap; r.pool_cap = pool_cap;
+        r.cand = I->rs_cand.as<uint32_t>(); r.crep = I->rs_crep.as<uint8_t>(); r.rseg = I->rs_rseg.as<uint4>(); r.rinfo = I->rs_rinfo.as<uint4>();
+        r.tiles = I->rs_tiles.as<uint2>();
         PFG_CUDA(cudaMemsetAsync(r.ctl, 0, sizeof(RoundCtl), st));
         k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p);
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
-        const size_t csm = (size_t)collect_smem_bytes(g.dpad, lazy) * 4;
+        const size_t esm = (size_t)expand_smem_bytes(g.dpad, lazy) * 4;
+        const size_t dsm = (size_t)align16((int)sizeof(DedupeSmem)) * 4;
         const size_t msm = (size_t)(align16((int)sizeof(MergeSmem)) + 2 * align16(kt * 8)) * 4;
         PFG_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
-        int cocc = 1;
-        switch (epl) {
-            case 1: PFG_TRY(collect_setup<1>(csm, &cocc)); break;
-            case 2: PFG_TRY(collect_setup<2>(csm, &cocc)); break;
-            case 4: PFG_TRY(collect_setup<4>(csm, &cocc)); break;
-            case 8: PFG_TRY(collect_setup<8>(csm, &cocc)); break;
-            case 16: PFG_TRY(collect_setup<16>(csm, &cocc)); break;
-            default: PFG_TRY(collect_setup<32>(csm, &cocc)); break;
-        }
-        // grids: warp per active query, at most one resident wave (the kernels stride over the
-        // device-side active count, so no host synchronisation is needed between rounds)
-        const unsigned qb_c = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * cocc));
-        const unsigned qb_m = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * 16));
+        PFG_CUDA(cudaFuncSetAttribute(k_dedupe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        int docc = 1;
+        PFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, k_dedupe, 128, dsm));
+        // grids: warp per active query (at most one resident wave; the kernels stride over the
+        // device-side counts, so no host synchronisation is needed between rounds)
+        const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * 16));
+        const unsigned qb_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * std::max(1, docc)));
+        const unsigned qb_m = qb_e;
+        const unsigned tb_s = (unsigned)(I->num_sms * 8);
         const unsigned sb = (unsigned)(I->num_sms * 2);
         int round = 0;
         uint32_t nact = (uint32_t)nq;
         while (round < max_rounds) {
             const int par = round & 1;
             switch (epl) {
-                case 1: k_collect<1><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 2: k_collect<2><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 4: k_collect<4><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 8: k_collect<8><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 16: k_collect<16><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
-                default: k_collect<32><<<qb_c, 128, csm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 1: k_expand<1><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 2: k_expand<2><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 4: k_expand<4><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 8: k_expand<8><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
+                case 16: k_expand<16><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
+                default: k_expand<32><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
             }
+            k_scan<<<tb_s, 256, 0, st>>>(p, par);
+            k_dedupe<<<qb_d, 128, dsm, st>>>(p, par);
             k_sims<<<sb, 256, 0, st>>>(p, par);
             k_merge<<<qb_m, 128, msm, st>>>(p, par);
             PFG_CUDA(cudaGetLastError());
-            I->launches += 3;
+            I->launches += 5;
             ++round;
             if (round % sync_every == 0 || round >= max_rounds) {
                 PFG_CUDA(cudaMemcpyAsync(I->h_ctl, r.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
@@ -1042,6 +1070,24 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         p.resume = 1;
         p.nq = fused_n;
         I->last_rounds = round;
+    }
+    if (!rounds && p.qb_n > 0 && nq > 1 && getenv("PFG_ORDER")) {
+        // longest-first order by the entries the first repetitions' match ranges hold
+        PFG_TRY(I->qord_keys.ensure((size_t)nq * 8, "query order"));
+        PFG_TRY(I->qord_sorted.ensure((size_t)nq * 8, "query order"));
+        PFG_TRY(I->qord_list.ensure((size_t)nq * 4, "query order"));
+        size_t tb = 0;
+        PFG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)nq, 32, 64, st));
+        PFG_TRY(I->qord_temp.ensure(tb, "query order temp"));
+        const unsigned gb = (unsigned)((nq + 255) / 256);
+        k_qorder_keys<<<gb, 256, 0, st>>>(p, I->qord_keys.as<uint64_t>());
+        tb = I->qord_temp.bytes;
+        PFG_CUDA(cub::DeviceRadixSort::SortKeys(I->qord_temp.p, tb, I->qord_keys.as<uint64_t>(), I->qord_sorted.as<uint64_t>(),
+                                                (int)nq, 32, 64, st));
+        k_qorder_list<<<gb, 256, 0, st>>>(I->qord_sorted.as<uint64_t>(), nq, I->qord_list.as<uint32_t>());
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 3;
+        p.qlist = I->qord_list.as<uint32_t>();
     }
     if (fused_n > 0) {
         PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
@@ -1184,6 +1230,7 @@ pfg_status pfg_hash_queries(pfg_index* I, const float* queries, int64_t nq, uint
     int64_t zrow = -1;
     bool lazy = false;
     PFG_TRY(prep_queries(I, queries, nq, out_codes != nullptr, true, &zrow, &lazy, st));
+    PFG_TRY(join_sketches(I, st));
     if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(zrow) + " is a zero vector");
     if (out_codes) {
         const size_t b = (size_t)nq * g.L * 4;

@@ -44,6 +44,11 @@ def cases():
     d3, q3 = synth.config_data(4, n=4000, nq=40)
     out["hp_pool"] = Case("hp_pool", d3[:, :64].copy(), q3[:, :64].copy(), O.HP, 20, 2, O.POOL, 512)
     out["fht_pool"] = Case("fht_pool", d2[:6000], q2[:50], O.FHTCP, 20, 5, O.POOL, 3072)
+    # more repetitions than the eagerly hashed 32: later repetitions are hashed in the kernels
+    # (lane groups of max(1, d'/32) lanes per repetition), d' = 128, 64 and 32
+    out["fht_long"] = Case("fht_long", d2[:8000], q2[:40], O.FHTCP, 64, 6)
+    out["fht_d40"] = Case("fht_d40", d2[:5000, :40].copy(), q2[:30, :40].copy(), O.FHTCP, 48, 7)
+    out["fht_d20"] = Case("fht_d20", d2[:5000, :20].copy(), q2[:30, :20].copy(), O.FHTCP, 40, 8)
     return out
 
 
@@ -153,12 +158,21 @@ def test_search_parity(cases, name, R, recall, engine):
     _compare(c, 10, recall, dict(rep_chunk=R, engine=engine), dict(rep_chunk=R))
 
 
-@pytest.mark.parametrize("max_rounds", ["1", "3"])
-def test_round_engine_handoff_midway(cases, max_rounds, monkeypatch):
-    # queries still running after a few rounds resume in the fused kernel from the saved state
-    monkeypatch.setenv("PFG_MAX_ROUNDS", max_rounds)
-    for name in ("hp", "fht"):
-        _compare(cases[name], 10, 0.99, dict(rep_chunk=4, engine=1), dict(rep_chunk=4))
+@pytest.mark.parametrize("name", ["fht_long", "fht_d40", "fht_d20"])
+@pytest.mark.parametrize("recall", [0.9, 0.99])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_search_parity_lazy_hashing(cases, name, recall, engine):
+    c = cases[name]
+    st = _compare(c, 10, recall, dict(rep_chunk=8, engine=engine), dict(rep_chunk=8))
+    if recall == 0.99:
+        assert np.any(st["j_stop"] > 32) or np.any(st["i_stop"] < 24), "no query reached the lazily hashed repetitions"
+
+
+@pytest.mark.parametrize("rounds", [1, 3, 64])
+def test_round_engine_handoff_midway(cases, rounds):
+    # queries still running after the bulk rounds resume in the fused kernel from the saved state
+    for name in ("hp", "fht", "fht_long"):
+        _compare(cases[name], 10, 0.99, dict(rep_chunk=4, engine=0, rounds=rounds), dict(rep_chunk=4))
 
 
 @pytest.mark.parametrize("name", ["hp", "fht"])
