@@ -28,12 +28,31 @@ def test_library_exports_every_declared_symbol():
     assert lib.pfg_abi_version() == 1
 
 
+def _c_sizes():
+    """sizeof of the header's structs as a C compiler sees them"""
+    import shutil
+    import subprocess
+    import tempfile
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if not cc:
+        pytest.skip("no C compiler")
+    src = ('#include "pfg.h"\n#include <stdio.h>\nint main(void){printf("%zu %zu %zu %zu", sizeof(pfg_build_opts), '
+           'sizeof(pfg_search_opts), sizeof(pfg_query_stats), sizeof(pfg_index_info_t)); return 0;}\n')
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "s.c")
+        open(c, "w").write(src)
+        exe = os.path.join(d, "s")
+        subprocess.check_call([cc, "-I", os.path.join(ROOT, "include"), c, "-o", exe])
+        return [int(x) for x in subprocess.check_output([exe]).split()]
+
+
 def test_abi_struct_sizes_match_header():
     # the binding's ctypes mirrors must have the C sizes (struct_size versioning)
-    assert C.sizeof(pfg.BuildOpts) == 48
-    assert C.sizeof(pfg.SearchOpts) == 56
-    assert pfg.STATS_DTYPE.itemsize == 32
-    assert C.sizeof(pfg.IndexInfo) == 96
+    b, s, q, i = _c_sizes()
+    assert C.sizeof(pfg.BuildOpts) == b
+    assert C.sizeof(pfg.SearchOpts) == s
+    assert pfg.STATS_DTYPE.itemsize == q
+    assert C.sizeof(pfg.IndexInfo) == i
 
 
 def test_cost_model_configs():
