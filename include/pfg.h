@@ -98,7 +98,7 @@ typedef struct {
                                  grid).  Results are identical. */
     int32_t uniform_chunks;   /* [0] 1 = chunks of R repetitions from the start (tau = 64 for a whole
                                  first chunk); 0 = single-repetition chunks until k points are known */
-    int32_t rounds;           /* [4] engine 0: bulk rounds before the fused kernel resumes the rest */
+    int32_t rounds;           /* [5] engine 0: bulk rounds before the fused kernel resumes the rest */
     int32_t reserved2;
 } pfg_search_opts;
 

@@ -39,6 +39,7 @@ constexpr int kU = 4;         // table positions per lane per scan step
 constexpr int kMaxR = 32;     // max repetitions per chunk
 constexpr int kMaxK = 256;    // max k
 constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr int kJHist = 256;
 
 // one repetition-table entry (16 B): key = (code << 32) | id, sk = sketch word s_{slot(j)}(id)
 struct __align__(16) Entry {
@@ -67,6 +68,7 @@ struct RoundState {
     uint4* pend;        // [nq][kMaxR] cursors of the chunk in flight (committed by k_merge)
     uint32_t* cand;     // [nq][Ccap] candidate id per emitted position of the chunk (kEmpty = filtered)
     uint8_t* crep;      // [nq][Ccap] repetition (within the chunk) of each emitted position
+    uint32_t* hsave;    // [nq][kHC] k_dedupe's hash set carried to the next round
     uint4* rseg;        // [nq][kMaxR] {lo_new, left length, hi_old, first position} per repetition
     uint4* rinfo;       // [nq] {chunk repetitions, tau, emitted positions, 0}
     uint2* tiles;       // scan tiles {query, tile}
@@ -113,6 +115,7 @@ struct QueryParams {
     pfg_query_stats* stats;
     uint32_t* trace_ids;
     unsigned long long* prof;   // optional per-phase cycle counters (PFG_PHASE_PROF=1), [6]
+    uint32_t* jhist;            // [kJHist] queries by stop repetition at level K (eager-depth tuning)
     const uint32_t* qlist;      // fused kernel: query indices to process (NULL = 0..nq-1)
     int resume;                 // fused kernel: continue each query from rs
     RoundState rs;
@@ -363,8 +366,16 @@ __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, Q
 }
 
 // home slot of an id: multiplicative hash scaled to [0, kHC); linear probing wraps at kHC
-__device__ __forceinline__ uint32_t hs_slot(uint32_t id) { return __umulhi(id * 0x9E3779B1u, (uint32_t)kHC); }
-__device__ __forceinline__ uint32_t hs_next(uint32_t h) { return h + 1 == (uint32_t)kHC ? 0u : h + 1; }
+constexpr bool kHCPow2 = (kHC & (kHC - 1)) == 0;
+constexpr int kHCLog = kHC >= 4096 ? 12 : kHC >= 2048 ? 11 : kHC >= 1024 ? 10 : 9;
+__device__ __forceinline__ uint32_t hs_slot(uint32_t id) {
+    if (kHCPow2) return (id * 0x9E3779B1u) >> (32 - kHCLog);
+    return __umulhi(id * 0x9E3779B1u, (uint32_t)kHC);
+}
+__device__ __forceinline__ uint32_t hs_next(uint32_t h) {
+    if (kHCPow2) return (h + 1) & (uint32_t)(kHC - 1);
+    return h + 1 == (uint32_t)kHC ? 0u : h + 1;
+}
 
 // claim id for evaluation: true if it was not evaluated before (called by one lane per distinct id)
 __device__ __forceinline__ bool claim(const WarpSmem& w, const QState& st, uint32_t* bm, uint32_t id) {
@@ -692,6 +703,9 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) st.probes += __shfl_xor_sync(kFull, st.probes, off);
+        // stop-depth histogram (repetitions hashed at level K), read by the host to size the
+        // next search's eager query hashing; a deeper stop counts as all L repetitions
+        if (p.jhist && lane == 0) atomicAdd(p.jhist + min(i_stop == p.K ? j_stop : p.L, kJHist - 1), 1u);
         if (p.stats && lane == 0) {
             pfg_query_stats s;
             s.i_stop = i_stop; s.j_stop = j_stop; s.emitted = st.emitted; s.filtered = st.filtered;

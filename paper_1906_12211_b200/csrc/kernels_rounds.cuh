@@ -9,9 +9,9 @@
 //   k_expand   warp per active query: the chunk, its tau, chunk codes, emitted ranges (R-12),
 //              pending cursors, and the query's scan tiles of 128 positions
 //   k_scan     warp per tile (fully data-parallel): table entries + sketch filter -> candidates
-//   k_dedupe   warp per active query: claims in (repetition, position) order against a
-//              shared-memory hash set rebuilt from the query's evaluated list (R-17/R-18) ->
-//              survivors appended to the evaluated list and to the round's pool
+//   k_dedupe   warp per active query: claims in (repetition, position) order against the query's
+//              evaluated-id hash set (shared memory; carried between rounds in global memory)
+//              (R-17/R-18) -> survivors appended to the evaluated list and to the round's pool
 //   k_sims     grid over the pool: warp-coalesced rows, 32-lane tree (R-2) -> (sim, id) keys
 //   k_merge    warp per active query: merge repetition by repetition into the top list, stop check
 //              after each repetition (Alg. 1 line 8), commit cursors / advance, or finish
@@ -136,7 +136,10 @@ struct ExpandSmem {
 __host__ __device__ inline int expand_smem_bytes(int dpad, bool lazy) {
     return align16((int)sizeof(ExpandSmem)) + (lazy ? align16(dpad * 4) : 0);
 }
-constexpr int kTile = 128;
+#ifndef PFG_TILE
+#define PFG_TILE 128
+#endif
+constexpr int kTile = PFG_TILE;   // emitted positions per scan tile
 
 template <int EPL>
 __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy) {
@@ -339,24 +342,20 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
         const uint32_t nE = rs.cnt[q * kCnt + 3];
         uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
         const uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
-        for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        // the hash set as the previous round left it (saved in global memory), or empty
+        uint4* hsv = reinterpret_cast<uint4*>(rs.hsave + q * (int64_t)kHC);
+        if (nE == 0) {
+            for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        } else {
+            uint4 tmp[kHC / 128];
+#pragma unroll
+            for (int k = 0; k < kHC / 128; ++k) tmp[k] = __ldcg(hsv + k * 32 + lane);
+#pragma unroll
+            for (int k = 0; k < kHC / 128; ++k) reinterpret_cast<uint4*>(c->hs)[k * 32 + lane] = tmp[k];
+        }
         if (lane < nr) { c->beg[lane] = rs.rseg[q * kMaxR + lane].w; c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
         if (lane == 0) c->beg[nr] = total;
         __syncwarp();
-        for (uint32_t e0 = 0; e0 < nE; e0 += 32 * kEPre) {
-            uint32_t v[kEPre];
-#pragma unroll
-            for (int u = 0; u < kEPre; ++u) {
-                const uint32_t e = e0 + u * 32 + lane;
-                v[u] = e < nE ? E[e] : kEmpty;
-            }
-#pragma unroll
-            for (int u = 0; u < kEPre; ++u)
-                if (v[u] != kEmpty) {
-                    uint32_t h = hs_slot(v[u]);
-                    while (atomicCAS(&c->hs[h], kEmpty, v[u]) != kEmpty) h = hs_next(h);
-                }
-        }
         __syncwarp();
         uint32_t ns = 0;
         bool overflow = false;
@@ -447,6 +446,9 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
             rc[2] = c->dcnt[lane];
         }
         if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }
+        // carry the set to the next round (the fused kernel rebuilds it from E instead)
+#pragma unroll
+        for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
         __syncwarp();
     }
 }
@@ -645,6 +647,7 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
                 }
             }
             if (lane == 0) {
+                if (p.jhist) atomicAdd(p.jhist + min(i == p.K ? c0 + r_stop + 1 : p.L, kJHist - 1), 1u);
                 if (p.stats) {
                     pfg_query_stats s;
                     s.i_stop = i; s.j_stop = c0 + r_stop + 1; s.emitted = emitted; s.filtered = filtered; s.dups = dups;

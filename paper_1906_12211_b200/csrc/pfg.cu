@@ -323,8 +323,11 @@ struct pfg_index {
     DBuf cur, bitmap, claims;
     // round-engine state (per query, grow-only)
     DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_repcnt, rs_pool_id, rs_pool_q, rs_pool_key,
-        rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, rs_cand, rs_crep, rs_rseg, rs_rinfo, rs_tiles, qbnd;
+        rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, rs_cand, rs_crep, rs_hsave, rs_rseg, rs_rinfo, rs_tiles, qbnd;
     uint32_t* h_ctl = nullptr;   // pinned host mirror of the round control block
+    DBuf jhist;                  // stop-depth histogram of the last search (device)
+    uint32_t* h_jhist = nullptr; // its pinned host copy
+    int eager = 32;              // repetitions hashed eagerly per query (tuned from the last search)
     cudaStream_t aux = nullptr;  // second stream: query sketches run beside the query hashing
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     unsigned long long* h_zmin = nullptr;  // pinned host word: first zero query row
@@ -345,6 +348,7 @@ struct pfg_index {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (h_ctl) cudaFreeHost(h_ctl);
+        if (h_jhist) cudaFreeHost(h_jhist);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (aux) cudaStreamDestroy(aux);
@@ -356,7 +360,7 @@ namespace pfg {
 namespace {
 
 constexpr int kClaimCap = 8192;
-constexpr int kEagerReps = 32;
+constexpr int kQBMax = 64;     // level-K match ranges precomputed for at most this many repetitions
 #ifndef PFG_QTPF
 #define PFG_QTPF 1   // threads per function of the eager FHT-CP query hashing at d' = 128
 #endif
@@ -727,9 +731,9 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
                           pool_ready, st));
         I->qc_n = g.L;
     } else if (need_codes && (g.dp == 32 || g.dp == 64 || g.dp == 128)) {
-        // FHT-CP independent: hash the first kEagerReps repetitions of every query here, one thread
+        // FHT-CP independent: hash the first I->eager repetitions of every query here, one thread
         // per (query, repetition); the query kernel hashes later repetitions lazily, if reached
-        const int ne = std::min(g.L, kEagerReps);
+        const int ne = std::min(g.L, getenv("PFG_EAGER") ? atoi(getenv("PFG_EAGER")) : I->eager);
         PFG_TRY(I->qcodes.ensure((size_t)nq * ne * 4, "query codes"));
         const int64_t threads = nq * ne;
         const unsigned blocks = (unsigned)((threads + 127) / 128);
@@ -924,12 +928,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     }
     PFG_TRY(I->cur.ensure((size_t)nq * g.L * 16, "cursors"));
     const bool rounds = s.engine == 0;
-    // round engine: `rounds` bulk rounds (search option, default 4), then the fused kernel resumes
+    // round engine: `rounds` bulk rounds (search option, default 5), then the fused kernel resumes
     // every query still running (stragglers keep their hash set in shared memory across chunks
     // there, instead of paying a round's fixed latency per chunk).  The rounds are enqueued
     // without host synchronisation; the host checks the active count every sync_every rounds
     // only to stop early when every query has finished.
-    const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : (s.rounds > 0 ? s.rounds : 4);
+    const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : (s.rounds > 0 ? s.rounds : 5);
     const int sync_every = 8;
     const int ecap = 2048;  // evaluated-list stride: kHMax committed + one batch of slack
     const int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
@@ -946,7 +950,9 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_TRY(I->rs_ctl.ensure(sizeof(RoundCtl), "rs control")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_pn.ensure(N * 4, "rs")); PFG_TRY(I->rs_act0.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_act1.ensure(N * 4, "rs")); PFG_TRY(I->rs_fused.ensure(N * 4, "rs"));
-        PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs candidates")); PFG_TRY(I->rs_crep.ensure(N * ccap, "rs candidates")); PFG_TRY(I->rs_rseg.ensure(N * kMaxR * 16, "rs"));
+        PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs candidates")); PFG_TRY(I->rs_crep.ensure(N * ccap, "rs candidates"));
+        PFG_TRY(I->rs_hsave.ensure(N * kHC * 4, "rs hash sets"));
+        PFG_TRY(I->rs_rseg.ensure(N * kMaxR * 16, "rs"));
         PFG_TRY(I->rs_rinfo.ensure(N * 16, "rs")); PFG_TRY(I->rs_tiles.ensure(N * (ccap / kTile) * 8, "rs tiles"));
         if (!I->h_ctl) PFG_CUDA(cudaMallocHost(&I->h_ctl, sizeof(RoundCtl)));
     }
@@ -980,7 +986,11 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
     p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
     // level-K match ranges of the first repetitions, one thread per (query, repetition)
-    p.qb_n = getenv("PFG_NO_QB") ? 0 : std::min(I->qc_n, kEagerReps);
+    p.qb_n = getenv("PFG_NO_QB") ? 0 : std::min(I->qc_n, kQBMax);
+    PFG_TRY(I->jhist.ensure(kJHist * 4, "stop histogram"));
+    if (!I->h_jhist) PFG_CUDA(cudaMallocHost(&I->h_jhist, kJHist * 4));
+    PFG_CUDA(cudaMemsetAsync(I->jhist.p, 0, kJHist * 4, st));
+    p.jhist = I->jhist.as<uint32_t>();
     p.qb_ld = p.qb_n;
     if (p.qb_n > 0) {
         PFG_TRY(I->qbnd.ensure((size_t)nq * p.qb_n * 16, "query bounds"));
@@ -1012,7 +1022,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         r.poff = I->rs_poff.as<uint32_t>(); r.pn = I->rs_pn.as<uint32_t>();
         r.act[0] = I->rs_act0.as<uint32_t>(); r.act[1] = I->rs_act1.as<uint32_t>(); r.fused = I->rs_fused.as<uint32_t>();
         r.Ecap = ecap; r.Ccap = ccap; r.pool_cap = pool_cap;
-        r.cand = I->rs_cand.as<uint32_t>(); r.crep = I->rs_crep.as<uint8_t>(); r.rseg = I->rs_rseg.as<uint4>(); r.rinfo = I->rs_rinfo.as<uint4>();
+        r.cand = I->rs_cand.as<uint32_t>(); r.crep = I->rs_crep.as<uint8_t>(); r.hsave = I->rs_hsave.as<uint32_t>(); r.rseg = I->rs_rseg.as<uint4>(); r.rinfo = I->rs_rinfo.as<uint4>();
         r.tiles = I->rs_tiles.as<uint2>();
         PFG_CUDA(cudaMemsetAsync(r.ctl, 0, sizeof(RoundCtl), st));
         k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p);
@@ -1127,6 +1137,19 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 h[3] / 1e6, 100 * h[3] / tot, h[5] / 1e6, h[4] / 1e6, 100 * h[4] / tot);
     }
     I->last_launches = I->launches;
+    {
+        // eager depth for the next search: the repetition count by which 99% of this batch's queries
+        // had stopped (deeper stops count as L), clamped to [8, 64]; codes are identical either way
+        PFG_CUDA(cudaMemcpy(I->h_jhist, I->jhist.p, kJHist * 4, cudaMemcpyDeviceToHost));
+        uint64_t tot = 0, cum = 0;
+        for (int j = 0; j < kJHist; ++j) tot += I->h_jhist[j];
+        int e = kJHist - 1;
+        for (int j = 0; j < kJHist; ++j) {
+            cum += I->h_jhist[j];
+            if (tot && cum * 100 >= tot * 99) { e = j; break; }
+        }
+        if (tot) I->eager = std::max(8, std::min(64, e));
+    }
     if (s.timing) {
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[0], I->ev[0], I->ev[1]));
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[1], I->ev[1], I->ev[2]));
