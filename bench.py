@@ -305,7 +305,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        res = idx.search(q, k, args.recall, stats=(s == args.steps - 1), **sopts)
+        res = idx.search(q, k, args.recall, **sopts)
         e1.record(stream)
         barrier()
         step_ms.append(e0.elapsed_time(e1))
@@ -313,9 +313,10 @@ def main():
         prep_ms.append(pm)
         kern_ms.append(km)
         launches += nl + (1 if world > 1 else 0)
-        if s == args.steps - 1:
-            ids, sims, stats = res[0], res[1], res[2]
     clocks = sampler.stop() if sampler else None
+    # per-query counters (algorithmic bytes, stop depths) from one more, untimed search of the same
+    # batch; the search is deterministic, so they are the counters of the timed steps
+    ids, sims, stats = idx.search(q, k, args.recall, stats=True, **sopts)[:3]
     tot_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([tot_ms], device=dev)

@@ -77,9 +77,9 @@ typedef struct {
 typedef struct {
     uint32_t struct_size;
     int32_t rep_chunk;        /* [8] R: the filter threshold tau is refreshed once per chunk of R
-                                 repetitions (R-17); while fewer than k points are known a
-                                 chunk is a single repetition (tau = 64 until the first k insertions,
-                                 PAPER.md:333-334) unless uniform_chunks = 1 */
+                                 repetitions (R-17); the search's first chunk is the single
+                                 repetition 0 (tau is set right after it) unless
+                                 uniform_chunks = 1 */
     int32_t segment;          /* [12] B: entries are retrieved in segments of B */
     int32_t stop_rule;        /* [0] 0 = failure bound (1-P_i)^j <= delta;
                                  1 = Alg. 1 line 8, j >= ln(1/delta)/P_i (independent only) */
@@ -97,7 +97,7 @@ typedef struct {
                                  still running; 1 = fused kernel only (one warp per query, persistent
                                  grid).  Results are identical. */
     int32_t uniform_chunks;   /* [0] 1 = chunks of R repetitions from the start (tau = 64 for a whole
-                                 first chunk); 0 = single-repetition chunks until k points are known */
+                                 first chunk); 0 = the first chunk is the single repetition 0 */
     int32_t rounds;           /* [5] engine 0: bulk rounds before the fused kernel resumes the rest */
     int32_t reserved2;
 } pfg_search_opts;

@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(128) k_fht_qcodes(const float* __restrict__ X,
 template <int DP, int TPF>
 __global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
                                                       int c, int K, const uint32_t* __restrict__ sg, int nreps,
-                                                      uint32_t* __restrict__ codes, int ldc) {
+                                                      uint32_t* __restrict__ codes, int ldc,
+                                                      const uint32_t* __restrict__ qlist, int r0) {
+    // rows: qlist[0..np) if given, else 0..np-1; repetitions r0 .. r0 + nreps - 1
     constexpr int H = DP / TPF, W = (DP + 31) / 32;
     static_assert(H % 32 == 0 || TPF == 1, "a lane holds whole sign words");
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -193,8 +195,9 @@ __global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ 
     int64_t item = t / TPF;
     const bool live = item < np * nreps;
     if (!live) item = 0;  // keep the group's lanes in the shuffles; nothing is stored
-    const int64_t p = item / nreps;
-    const int j = (int)(item % nreps);
+    const int64_t a = item / nreps;
+    const int64_t p = qlist ? (int64_t)qlist[a] : a;
+    const int j = r0 + (int)(item % nreps);
     const float* xr = X + p * ldx;
     uint64_t full = 0;
     for (int f = 0; f < c; ++f) {

@@ -241,12 +241,12 @@ __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem
     st.nE += (uint32_t)(e2 - e);
 }
 
-// R-17: the chunk starting at c0 is one repetition while fewer than k points are known (tn < k_eff),
-// else R repetitions.  It ends early at the first repetition j whose stop threshold the current
+// R-17: the search's first chunk (level K, repetition 0) is a single repetition, every other chunk
+// R repetitions.  It ends early at the first repetition j whose stop threshold the current
 // k-th similarity already meets: the k-th similarity only grows, so the search stops at or before
 // j and later repetitions of the chunk are never reached (exact).  All lanes get the same value.
 __device__ __forceinline__ int chunk_reps(const QueryParams& p, int i, int c0, int tn, const uint64_t* T, int lane) {
-    int nr = min((tn < p.k_eff && !p.uniform) ? 1 : p.R, p.L - c0);
+    int nr = min((i == p.K && c0 == 0 && !p.uniform) ? 1 : p.R, p.L - c0);
     if (tn == p.k_eff) {
         float ip = key_sim(T[p.k_eff - 1]);
         ip = fminf(fmaxf(ip, -1.0f), 1.0f);
@@ -299,36 +299,37 @@ __device__ __forceinline__ float tree_rows(float (&a)[NR], int lane) {
 #define PFG_KRQ 8
 #endif
 constexpr int kRQ = PFG_KRQ;
+template <int RQ = kRQ>
 __device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int e0, int e1, int lane) {
     const int nch = p.dpad >> 2;
     const float4* q4 = reinterpret_cast<const float4*>(w.qrow);
     const float4* x4 = reinterpret_cast<const float4*>(p.x);
-    for (int b = e0; b < e1; b += kRQ) {
-        const int nrow = min(kRQ, e1 - b);
-        // lane r < kRQ reads survivor b + r (rows >= nrow repeat the last)
-        const uint32_t myoff = lane < kRQ ? w.f->sid[b + (lane < nrow ? lane : nrow - 1)] * (uint32_t)nch : 0u;
-        float acc[kRQ];
-        uint32_t off[kRQ];   // row offsets in float4 units (n * dpad / 4 < 2^32)
+    for (int b = e0; b < e1; b += RQ) {
+        const int nrow = min(RQ, e1 - b);
+        // lane r < RQ reads survivor b + r (rows >= nrow repeat the last)
+        const uint32_t myoff = lane < RQ ? w.f->sid[b + (lane < nrow ? lane : nrow - 1)] * (uint32_t)nch : 0u;
+        float acc[RQ];
+        uint32_t off[RQ];   // row offsets in float4 units (n * dpad / 4 < 2^32)
 #pragma unroll
-        for (int r = 0; r < kRQ; ++r) {
+        for (int r = 0; r < RQ; ++r) {
             acc[r] = 0.0f;
             off[r] = __shfl_sync(kFull, myoff, r);
         }
         for (int c = lane; c < nch; c += 32) {
-            float4 v[kRQ];
+            float4 v[RQ];
 #pragma unroll
-            for (int r = 0; r < kRQ; ++r) v[r] = __ldg(x4 + off[r] + c);
+            for (int r = 0; r < RQ; ++r) v[r] = __ldg(x4 + off[r] + c);
             const float4 q = q4[c];
 #pragma unroll
-            for (int r = 0; r < kRQ; ++r) {
+            for (int r = 0; r < RQ; ++r) {
                 acc[r] = fmaf(q.x, v[r].x, acc[r]);
                 acc[r] = fmaf(q.y, v[r].y, acc[r]);
                 acc[r] = fmaf(q.z, v[r].z, acc[r]);
                 acc[r] = fmaf(q.w, v[r].w, acc[r]);
             }
         }
-        const float t = tree_rows<kRQ>(acc, lane);
-        constexpr int kSh = (kRQ == 32) ? 0 : (kRQ == 16) ? 1 : (kRQ == 8) ? 2 : 3;
+        const float t = tree_rows<RQ>(acc, lane);
+        constexpr int kSh = (RQ == 32) ? 0 : (RQ == 16) ? 1 : (RQ == 8) ? 2 : 3;
         const int rr = lane >> kSh;
         if ((lane & ((1 << kSh) - 1)) == 0 && rr < nrow) w.f->ssim[b + rr] = t;
     }
@@ -338,10 +339,11 @@ __device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSme
 // Process the survivor buffer (in repetition order): similarities, then merge repetition by
 // repetition; every repetition < `complete` (all positions scanned) gets its stop check after its
 // survivors are merged (Alg. 1 line 8).  Returns true when the query stops (r_stop set).
+template <int RQ>
 __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, QState& st, int& nbuf, int& next_check,
                                       int complete, int nr, int c0, int i, int64_t qi, int& r_stop, int lane) {
     const long long td0 = p.prof ? clock64() : 0;
-    compute_sims(p, w, 0, nbuf, lane);
+    compute_sims<RQ>(p, w, 0, nbuf, lane);
     if (p.prof && lane == 0) atomicAdd(p.prof + 5, (unsigned long long)(clock64() - td0));
     int e = 0;
     bool stop = false;
@@ -422,7 +424,7 @@ __device__ __forceinline__ void to_bitmap_mode(const QueryParams& p, const WarpS
     __syncwarp();
 }
 
-template <int EPL>
+template <int EPL, int RQ = kRQ>
 __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -645,7 +647,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                     if (nbuf > kSB - 32 * kU || done_pos == total) {
                         int complete = nr;
                         if (done_pos < total) { complete = 0; while (complete < nr && w.f->beg[complete + 1] <= done_pos) ++complete; }
-                        if (drain(p, w, st, nbuf, next_check, complete, nr, c0, i, qi, r_stop, lane)) {
+                        if (drain<RQ>(p, w, st, nbuf, next_check, complete, nr, c0, i, qi, r_stop, lane)) {
                             stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
                         }
                         if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 3, (unsigned long long)(t - tp0)); tp0 = t; }
@@ -653,7 +655,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 }
                 if (total == 0) {
                     // empty chunk: every repetition is complete, check them in order
-                    if (drain(p, w, st, nbuf, next_check, nr, nr, c0, i, qi, r_stop, lane)) {
+                    if (drain<RQ>(p, w, st, nbuf, next_check, nr, nr, c0, i, qi, r_stop, lane)) {
                         stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
                     }
                 }
@@ -682,7 +684,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 ns += __popc(fm);
                 __syncwarp();
                 if (ns > kSB - 32 || g0 + 32 >= p.n) {
-                    compute_sims(p, w, 0, ns, lane);
+                    compute_sims<RQ>(p, w, 0, ns, lane);
                     if (ns) merge_range(p, w, st, 0, ns, qi, lane);
                     ns = 0;
                 }

@@ -66,11 +66,14 @@ __device__ __forceinline__ void bucket_of(const QueryParams& p, int j, uint64_t 
     hi = ((x & ((1ull << sh) - 1)) == 0) ? lo : __ldg(ptj + pfx + 1);
 }
 
-__global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restrict__ out, const uint32_t* __restrict__ qlist,
+                                                 int64_t nlist, int r0, int nreps) {
+    // queries qlist[0..nlist) if given, else 0..nlist-1; repetitions r0 .. r0 + nreps - 1
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t q = t / p.qb_n;
-    const int j = (int)(t - q * p.qb_n);
-    if (q >= p.nq) return;
+    const int64_t a = t / nreps;
+    if (a >= nlist) return;
+    const int j = r0 + (int)(t - a * nreps);
+    const int64_t q = qlist ? (int64_t)qlist[a] : a;
     if (p.qzero[q]) { out[q * p.qb_ld + j] = make_uint4(0, 0, 0, 0); return; }
     const uint32_t qc = __ldg(p.qcodes + q * p.qc_ld + j);
     uint32_t lo1, hi1, lo2, hi2, probes = 0;

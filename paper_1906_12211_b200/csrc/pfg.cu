@@ -360,7 +360,9 @@ namespace pfg {
 namespace {
 
 constexpr int kClaimCap = 8192;
-constexpr int kQBMax = 64;     // level-K match ranges precomputed for at most this many repetitions
+constexpr int kQBMax = 96;     // level-K match ranges precomputed for at most this many repetitions
+constexpr int kExtReps = 32;   // repetitions hashed in bulk for the queries the fused kernel resumes
+pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st);
 #ifndef PFG_QTPF
 #define PFG_QTPF 1   // threads per function of the eager FHT-CP query hashing at d' = 128
 #endif
@@ -733,21 +735,34 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     } else if (need_codes && (g.dp == 32 || g.dp == 64 || g.dp == 128)) {
         // FHT-CP independent: hash the first I->eager repetitions of every query here, one thread
         // per (query, repetition); the query kernel hashes later repetitions lazily, if reached
+        // (rows are laid out with room for kExtReps more, hashed later for the queries that reach
+        // them: extend_codes)
         const int ne = std::min(g.L, getenv("PFG_EAGER") ? atoi(getenv("PFG_EAGER")) : I->eager);
-        PFG_TRY(I->qcodes.ensure((size_t)nq * ne * 4, "query codes"));
-        const int64_t threads = nq * ne;
-        const unsigned blocks = (unsigned)((threads + 127) / 128);
-        const uint32_t* sg = I->sg.as<uint32_t>();
-        uint32_t* qc = I->qcodes.as<uint32_t>();
-        if (g.dp == 32) k_fht_qcodes<32><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
-        else if (g.dp == 64) k_fht_qcodes<64><<<blocks, 128, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
-        else k_fht_qcodes_g<128, PFG_QTPF><<<(unsigned)((PFG_QTPF * threads + 127) / 128), 128, 0, st>>>(
-                 I->qx.as<float>(), nq, g.dpad, g.d, g.ell, g.c, g.K, sg, ne, qc, ne);
-        PFG_CUDA(cudaGetLastError());
-        I->launches += 1;
+        const int ld = std::min(g.L, ne + kExtReps);
+        PFG_TRY(I->qcodes.ensure((size_t)nq * ld * 4, "query codes"));
+        PFG_TRY(fht_codes(I, nq, nullptr, 0, ne, ld, st));
         I->qc_n = ne;
-        I->qc_ld = ne;
+        I->qc_ld = ld;
     }
+    return PFG_OK;
+}
+
+// FHT-CP query codes of repetitions [r0, r0 + nreps) for rows qlist[0..nrows) (or 0..nrows-1),
+// one thread per (row, repetition), into qcodes [q][ld]
+pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st) {
+    const Geo& g = I->g;
+    const int64_t threads = nrows * nreps;
+    if (threads == 0) return PFG_OK;
+    const unsigned blocks = (unsigned)((threads + 127) / 128);
+    const uint32_t* sg = I->sg.as<uint32_t>();
+    uint32_t* qc = I->qcodes.as<uint32_t>();
+    const float* X = I->qx.as<float>();
+    if (g.dp == 32) k_fht_qcodes_g<32, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0);
+    else if (g.dp == 64) k_fht_qcodes_g<64, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0);
+    else k_fht_qcodes_g<128, PFG_QTPF><<<(unsigned)((PFG_QTPF * threads + 127) / 128), 128, 0, st>>>(
+             X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0);
+    PFG_CUDA(cudaGetLastError());
+    I->launches += 1;
     return PFG_OK;
 }
 
@@ -759,6 +774,13 @@ pfg_status join_sketches(pfg_index* I, cudaStream_t st) {
 
 template <int EPL>
 pfg_status launch_query_t(const QueryParams& p, int blocks, size_t smem, cudaStream_t st) {
+    if (p.resume) {
+        // the queries resumed after the bulk rounds are few and long: more rows in flight per warp
+        PFG_CUDA(cudaFuncSetAttribute(k_query<EPL, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_query<EPL, 16><<<blocks, 128, smem, st>>>(p);
+        PFG_CUDA(cudaGetLastError());
+        return PFG_OK;
+    }
     PFG_CUDA(cudaFuncSetAttribute(k_query<EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_query<EPL><<<blocks, 128, smem, st>>>(p);
     PFG_CUDA(cudaGetLastError());
@@ -986,17 +1008,19 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.cur = I->cur.as<uint4>(); p.bitmap = I->bitmap.as<uint32_t>(); p.claims = I->claims.as<uint32_t>();
     p.out_ids = d_ids; p.out_sims = d_sims; p.stats = stats ? d_stats : nullptr; p.trace_ids = d_trace;
     // level-K match ranges of the first repetitions, one thread per (query, repetition)
-    p.qb_n = getenv("PFG_NO_QB") ? 0 : std::min(I->qc_n, kQBMax);
+    // (SimHash and pool strategies hash all L repetitions eagerly; their ranges are precomputed
+    // for the repetitions most queries reach, the tuned eager depth)
+    p.qb_n = getenv("PFG_NO_QB") ? 0 : std::min(std::min(I->qc_n, kQBMax), lazy ? I->qc_n : I->eager);
     PFG_TRY(I->jhist.ensure(kJHist * 4, "stop histogram"));
     if (!I->h_jhist) PFG_CUDA(cudaMallocHost(&I->h_jhist, kJHist * 4));
     PFG_CUDA(cudaMemsetAsync(I->jhist.p, 0, kJHist * 4, st));
     p.jhist = I->jhist.as<uint32_t>();
-    p.qb_ld = p.qb_n;
+    p.qb_ld = std::max(1, I->qc_ld);
     if (p.qb_n > 0) {
-        PFG_TRY(I->qbnd.ensure((size_t)nq * p.qb_n * 16, "query bounds"));
+        PFG_TRY(I->qbnd.ensure((size_t)nq * p.qb_ld * 16, "query bounds"));
         p.qbnd = I->qbnd.as<uint4>();
         const int64_t thr_n = nq * (int64_t)p.qb_n;
-        k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>());
+        k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, p.qb_n);
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
     }
@@ -1080,6 +1104,17 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         p.resume = 1;
         p.nq = fused_n;
         I->last_rounds = round;
+        // the queries the fused kernel resumes get codes and match ranges for kExtReps more
+        // repetitions in bulk (they would otherwise hash and search them one warp at a time)
+        if (fused_n > 0 && lazy && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+            const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
+            PFG_TRY(fht_codes(I, fused_n, r.fused, r0, nr, I->qc_ld, st));
+            const int64_t thr_n = fused_n * (int64_t)nr;
+            k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.fused, fused_n, r0, nr);
+            PFG_CUDA(cudaGetLastError());
+            I->launches += 1;
+            p.qc_n = p.qb_n = I->qc_ld;
+        }
     }
     if (!rounds && p.qb_n > 0 && nq > 1 && getenv("PFG_ORDER")) {
         // longest-first order by the entries the first repetitions' match ranges hold

@@ -347,8 +347,8 @@ def test_filter_off_equals_infinite_eps():
 
 
 def test_chunk_schedule_only_moves_tau():
-    # R-17: the chunk schedule (single repetitions while fewer than k points are known, then chunks
-    # of R; or uniform chunks of R) only decides when tau is refreshed.  With the filter off it
+    # R-17: the chunk schedule (the single repetition 0, then chunks of R; or uniform chunks of R)
+    # only decides when tau is refreshed.  With the filter off it
     # cannot change the search at all, and with R = 1 both schedules are the same chunks.
     data, q = synth.config_data(1, n=2000, nq=20)
     X = O.OracleIndex(data, O.HP, L=8, seed=4)
@@ -360,11 +360,14 @@ def test_chunk_schedule_only_moves_tau():
     a = X.search(q, 10, 0.8, rep_chunk=1)
     b = X.search(q, 10, 0.8, rep_chunk=1, uniform_chunks=True)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
-    # with the filter, the default schedule sets tau right after the top list fills, so it never
-    # evaluates more points before the stop than uniform chunks would at the first level
-    c = X.search(q, 10, 0.8, rep_chunk=8)
-    u = X.search(q, 10, 0.8, rep_chunk=8, uniform_chunks=True)
+    # with the filter, the default schedule sets tau after repetition 0 instead of after R, so the
+    # filter rejects more
+    d2, q2 = synth.config_data(2, n=4000, nq=30)
+    X2 = O.OracleIndex(d2, O.FHTCP, L=16, seed=1)
+    c = X2.search(q2, 10, 0.9, rep_chunk=8)
+    u = X2.search(q2, 10, 0.9, rep_chunk=8, uniform_chunks=True)
     assert np.sum(c[2][:, 3]) > np.sum(u[2][:, 3])  # more rejections by the filter
+    assert np.sum(c[2][:, 5]) < np.sum(u[2][:, 5])  # fewer exact evaluations
 
 
 def test_trace_accounting_and_lemma1():
