@@ -73,3 +73,94 @@ def test_config2_full_sampled():
     sub = (ids[sel], sims[sel], st[sel], tr[sel])
     orr = o.search(q[sel], c["k"], c["recall"], rep_chunk=8, trace_cap=cap, threads=1)
     _search_equal(sub, orr, cap)
+
+
+# ------------------------------------------------------------------ configs 3 and 4 at full size
+def _truth(x_dev, q_dev, k):
+    """exact top-k sims by fp32 inner products on the GPU (torch, TF32 off; test infrastructure)"""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    x_dev = x_dev / x_dev.norm(dim=1, keepdim=True)
+    q_dev = q_dev / q_dev.norm(dim=1, keepdim=True)
+    kth = []
+    for s in range(0, q_dev.shape[0], 512):
+        S = q_dev[s:s + 512] @ x_dev.T
+        kth.append(torch.topk(S, k, dim=1).values[:, -1])
+    return torch.cat(kth)
+
+
+def _properties(g, o, data_n, q, k, recall, ids, sims, st):
+    """checks that hold at any size: ids distinct and in range, order (sim desc, id asc), every
+    returned similarity equal to the oracle's R-2 similarity of that id, the stop decision equal to
+    the oracle's stop rule at the returned k-th similarity, recall against the exact top-k"""
+    xn = O.normalize(data_n)
+    qn = O.normalize(q)
+    delta = 1.0 - float(np.float32(recall))
+    for r in range(len(q)):
+        row, srow = ids[r], sims[r]
+        assert np.all(row >= 0) and np.all(row < len(xn)) and len(set(row.tolist())) == k, r
+        for t in range(k):
+            assert srow[t] == np.float32(O.sim(qn[r], xn[row[t]])), (r, t)
+            if t:
+                assert srow[t - 1] > srow[t] or (srow[t - 1] == srow[t] and row[t - 1] < row[t]), (r, t)
+        i, j = int(st["i_stop"][r]), int(st["j_stop"][r])
+        if i > 0:
+            ip = float(min(max(srow[k - 1], -1.0), 1.0))
+            assert o.should_stop(i, j, ip, delta), (r, i, j)
+
+
+def _recall(x_t, q_t, ids, k):
+    kth = _truth(x_t, q_t, k).cpu().numpy()
+    xn = x_t / x_t.norm(dim=1, keepdim=True)
+    qn = q_t / q_t.norm(dim=1, keepdim=True)
+    ex = torch.einsum("qd,qkd->qk", qn, xn[torch.from_numpy(ids).to(DEV)]).cpu().numpy()
+    return float(np.mean(ex >= kth[:, None] - 1e-5))
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_config34_full(cfg):
+    c = synth.CONFIGS[cfg]
+    data, q = synth.config_data(cfg)
+    x_t = torch.from_numpy(data).to(DEV)
+    q_t = torch.from_numpy(q).to(DEV)
+    g = pfg.Index(x_t, c["budget"], c["family"], seed=1, strategy=c["strategy"])
+    L = g.info["reps"]
+    assert L == pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
+    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
+    o = O.OracleIndex(data, O.HP, L=L, seed=1, strategy=strat, lazy=True)
+    # build side: data, slots, pool selections, two whole repetition tables with their inline
+    # sketch words, prefix tables
+    assert np.array_equal(g.export_data().view(np.uint32), o.data().view(np.uint32))
+    assert np.array_equal(g.export_slots(), o.slots())
+    if strat == O.POOL:
+        assert np.array_equal(g.export_pool_sel(), o.pool_sel())
+    osk = o.sketches()
+    slots = o.slots()
+    for j in (0, L - 1):
+        tab = g.export_table(j)
+        codes, oid = o.rep(j)
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), oid), j
+        assert np.array_equal(tab[:, 1], osk[oid, slots[j]]), j
+        assert np.array_equal(g.export_prefix(j), o.prefix_table(j)), j
+    # query side: codes and sketches of every query bit-exact
+    gc, gs = g.hash_queries(q)
+    oc, os_ = o.hash(q)
+    assert np.array_equal(gc, oc) and np.array_equal(gs, os_)
+    # the bench's launch (all queries, default engine): properties at full size
+    ids, sims, st = g.search(q_t, c["k"], c["recall"], stats=True)
+    ids, sims = ids.cpu().numpy(), sims.cpu().numpy()
+    _properties(g, o, data, q, c["k"], c["recall"], ids, sims, st)
+    assert _recall(x_t, q_t, ids, c["k"]) >= c["recall"]
+    # batch independence + the top-k is exactly the best k of the evaluated set (sampled queries)
+    sel = np.arange(0, len(q), max(1, len(q) // 16))
+    cap = 1 << 15
+    sids, ssims, sst, tr = g.search(torch.from_numpy(q[sel]).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
+    assert np.array_equal(sids.cpu().numpy(), ids[sel]) and np.array_equal(sst["j_stop"], st["j_stop"][sel])
+    xn, qn = O.normalize(data), O.normalize(q[sel])
+    for r in range(len(sel)):
+        ev = tr[r, :min(cap, int(sst["evaluated"][r]))]
+        assert len(set(ev.tolist())) == len(ev)
+        if sst["evaluated"][r] <= cap:
+            s = np.array([O.sim(qn[r], xn[e]) for e in ev], np.float32)
+            order = np.lexsort((ev, -s))[:c["k"]]
+            assert np.array_equal(ev[order].astype(np.int64), ids[sel[r]]), r
