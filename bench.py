@@ -31,6 +31,8 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 METRIC = "queries/s at >=0.9 recall, k=10, 1Mx100-d angular; achieved HBM GB/s"
+WORKLOAD_NOTE = {2: " (Gaussian-mixture stand-in for GloVe-1M)",
+                 3: " (planted-partner stand-in for the paper's SYNTHETIC set)"}
 
 
 def peaks():
@@ -100,18 +102,28 @@ def cfg_desc(cfg: int):
 
 def ground_truth(data_t, q_t, k):
     """exact top-k by fp32 inner products of the normalised rows (torch, TF32 off; measurement
-    tool, not part of the path).  Returns (ids [nq,k], kth sims [nq])."""
+    tool, not part of the path), in blocks of queries x rows.  Returns (ids [nq,k], kth sims [nq])."""
     import torch
     torch.backends.cuda.matmul.allow_tf32 = False
     x = data_t / data_t.norm(dim=1, keepdim=True)
     q = q_t / q_t.norm(dim=1, keepdim=True)
+    qb, xb = 1024, 1 << 21
     ids, kth = [], []
-    for s in range(0, q.shape[0], 1024):
-        S = q[s:s + 1024] @ x.T
-        v, i = torch.topk(S, k, dim=1)
-        ids.append(i)
-        kth.append(v[:, -1])
-        del S
+    for s in range(0, q.shape[0], qb):
+        bv = bi = None
+        for r0 in range(0, x.shape[0], xb):
+            S = q[s:s + qb] @ x[r0:r0 + xb].T
+            v, i = torch.topk(S, min(k, S.shape[1]), dim=1)
+            i = i + r0
+            if bv is not None:
+                v = torch.cat([bv, v], 1)
+                i = torch.cat([bi, i], 1)
+                v, o = torch.topk(v, k, dim=1)
+                i = torch.gather(i, 1, o)
+            bv, bi = v, i
+            del S
+        ids.append(bi)
+        kth.append(bv[:, -1])
     return torch.cat(ids), torch.cat(kth), x, q
 
 
@@ -135,12 +147,13 @@ def alg_bytes(stats, d, M, k):
     return float(b.sum())
 
 
-def profiled_traffic():
-    """DRAM bytes per k_query launch from the committed ncu --set full summary, if present"""
-    path = os.path.join(ROOT, "profiles", "k_query_ncu.json")
+def profiled_traffic(cfg):
+    """DRAM bytes (read + write) of the query phase of one search call, summed over its kernels,
+    from the committed ncu capture (tools/ncu_traffic.py), if present for this config"""
+    path = os.path.join(ROOT, "profiles", f"query_phase_traffic_config{cfg}.json")
     try:
         j = json.load(open(path))
-        return float(j["dram_bytes_read"] + j["dram_bytes_write"]), j.get("source")
+        return float(j["dram_bytes"]), os.path.relpath(path, ROOT)
     except Exception:
         return None, None
 
@@ -197,6 +210,11 @@ def cpu_baseline_leg(cfg, recall, rep_chunk, sample):
     import oracle as O
     import paper_1906_12211_b200 as pfg
     c = synth.CONFIGS[cfg]
+    if c["n"] * c["d"] > 400_000_000:
+        # the oracle's index setup alone (2048 sketch projections per point) exceeds the bounded
+        # budget of this leg; the reference arm (--impl reference) times it separately
+        return {"value": None, "unit": "queries/s", "cores": 1, "kind": "oracle",
+                "sample": f"not run: config {cfg}'s oracle setup ({c['n']} x {c['d']}) exceeds the bounded CPU budget"}
     data, q = synth.config_data(cfg)
     L = c["reps"] or pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
     fam = O.HP if c["family"] == "simhash" else O.FHTCP
@@ -251,7 +269,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     c = synth.CONFIGS[args.config]
-    n, d, k = c["n"], c["d"], c["k"]
+    d, k = c["d"], c["k"]
+    # config 5 is weak-scaled (BASELINE: 12.5M rows per GPU); the others split their n rows
+    weak = "shard_n" in c
+    n = c["shard_n"] * world if weak else c["n"]
     nq = args.nq or c["nq"]
     lo, hi = shard_range(n, world, rank)
     data_np, q_np = synth.config_data(args.config, n=hi - lo, nq=nq, row0=lo)
@@ -297,6 +318,7 @@ def main():
         if time.time() - t_w > 1.0:
             break
     step_ms, kern_ms, prep_ms = [], [], []
+    phase_ms = {}
     launches = 0
     stats = None
     for s in range(args.steps):
@@ -312,11 +334,17 @@ def main():
         pm, km, _, nl = idx.index.last_timing()
         prep_ms.append(pm)
         kern_ms.append(km)
+
         launches += nl + (1 if world > 1 else 0)
     clocks = sampler.stop() if sampler else None
     # per-query counters (algorithmic bytes, stop depths) from one more, untimed search of the same
     # batch; the search is deterministic, so they are the counters of the timed steps
     ids, sims, stats = idx.search(q, k, args.recall, stats=True, **sopts)[:3]
+    # per-phase breakdown of the query kernels from untimed searches with events between phases
+    for _ in range(3):
+        idx.search(q, k, args.recall, **dict(sopts, timing=2))
+        for key, v in idx.index.last_phases().items():
+            phase_ms[key] = phase_ms.get(key, 0.0) + v / 3
     tot_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([tot_ms], device=dev)
@@ -363,7 +391,7 @@ def main():
         ab = alg_bytes(stats, d, info["sketch_words"], k)
         kern_s = statistics.mean(kern_ms) / 1e3
         achieved = ab / kern_s / 1e9
-        traffic, traffic_src = profiled_traffic()
+        traffic, traffic_src = profiled_traffic(args.config)
         cpu = None
         if not args.no_cpu_baseline:
             try:
@@ -379,11 +407,12 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": tot_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": "weak" if weak else "strong",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"config{args.config}: {c['name']} (Gaussian-mixture stand-in for GloVe-1M)",
+            "config": {"workload": f"config{args.config}: {c['name']}" + WORKLOAD_NOTE.get(args.config, "")
+                       + (f" ({c['shard_n']} rows per GPU)" if weak else ""),
                        "n": n, "d": d, "nq": nq, "k": k, "recall_target": args.recall, "family": c["family"],
                        "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": info["reps"],
                        "rep_chunk": args.rep_chunk, "l2": "flushed (512 MiB write) between timed steps",
@@ -392,7 +421,9 @@ def main():
             "build_s": build_s,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "k_query", "kernel_ms": statistics.mean(kern_ms),
+                         "kernel": "query phase: bulk rounds (k_expand, k_scan, k_dedupe, k_sims, k_merge) "
+                                   "+ fused tail (k_query), one search call",
+                         "kernel_ms": statistics.mean(kern_ms), "phases_ms_untimed": phase_ms,
                          "prep_ms": statistics.mean(prep_ms), "alg_bytes_per_query": ab / nq,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
             "counters": {"emitted_per_q": float(np.mean(stats["emitted"])),

@@ -90,7 +90,8 @@ typedef struct {
     int32_t trace_cap;        /* [0] >0: write the ids evaluated by each query, in evaluation order,
                                  to trace_ids[nq][trace_cap] (uint32, local row ids) */
     int32_t timing;           /* [0] 1: record CUDA events around the phases of this call on `stream`
-                                 (read back with pfg_last_timing) */
+                                 (read back with pfg_last_timing); 2: also between the query-phase
+                                 kernels (pfg_last_phases; the extra events cost a few microseconds each) */
     uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
     int32_t engine;           /* [0] 0 = bulk rounds (one chunk of every active query per round, split
                                  into data-parallel phases), then the fused kernel resumes the queries
@@ -193,6 +194,12 @@ pfg_status pfg_stop_tables(pfg_index* idx, float recall_target, const pfg_search
  * call's stream): ms[0] = query preparation (host->device copy, normalisation, hashing, sketches),
  * ms[1] = the query kernel, ms[2] = whole call; *launches = kernels the call launched. */
 pfg_status pfg_last_timing(const pfg_index* idx, float* ms3, int32_t* launches);
+
+/* per-phase breakdown of the query-kernel time of the same search (CUDA events between the
+ * phases' launches): ms[0] k_expand, ms[1] k_scan, ms[2] k_dedupe, ms[3] k_sims, ms[4] k_merge
+ * (summed over the bulk rounds), ms[5] the fused kernel, ms[6] other (round control, query
+ * order, code extension for resumed queries).  n: entries to write (<= 8). */
+pfg_status pfg_last_phases(const pfg_index* idx, float* ms, int32_t n);
 
 void pfg_free(pfg_index* idx);
 const char* pfg_last_error(void);

@@ -28,7 +28,7 @@ STATUS = {0: "PFG_OK", 1: "PFG_E_ARG", 2: "PFG_E_ZERO_VECTOR", 3: "PFG_E_BUDGET"
 
 # symbols include/pfg.h declares (checked by tests/test_abi.py)
 EXPORTED = ["pfg_build", "pfg_search", "pfg_merge_topk", "pfg_index_info", "pfg_derive_reps", "pfg_export",
-            "pfg_hash_queries", "pfg_stop_tables", "pfg_last_timing", "pfg_free", "pfg_last_error",
+            "pfg_hash_queries", "pfg_stop_tables", "pfg_last_timing", "pfg_last_phases", "pfg_free", "pfg_last_error",
             "pfg_abi_version"]
 
 
@@ -95,6 +95,8 @@ def lib() -> C.CDLL:
         L.pfg_stop_tables.argtypes = [P, C.c_float, P, P, P]
         L.pfg_last_timing.restype = S
         L.pfg_last_timing.argtypes = [P, P, P]
+        L.pfg_last_phases.restype = S
+        L.pfg_last_phases.argtypes = [P, P, C.c_int32]
         L.pfg_free.restype = None
         L.pfg_free.argtypes = [P]
         L.pfg_last_error.restype = C.c_char_p
@@ -226,6 +228,14 @@ class Index:
         n = C.c_int32(0)
         _check(lib().pfg_last_timing(self._h, ms, C.byref(n)))
         return float(ms[0]), float(ms[1]), float(ms[2]), int(n.value)
+
+    PHASES = ("expand", "scan", "dedupe", "sims", "merge", "fused", "other")
+
+    def last_phases(self) -> dict:
+        """per-phase ms of the query kernels of the last timed search (see pfg_last_phases)"""
+        ms = (C.c_float * 8)()
+        _check(lib().pfg_last_phases(self._h, ms, 8))
+        return {name: float(ms[i]) for i, name in enumerate(self.PHASES)}
 
     def search(self, queries, k: int, recall: float, stats: bool = False, trace_cap: int = 0, out=None,
                stream=None, **sopts):

@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(256) k_hp_bits(const float* __restrict__ X, in
     __shared__ __align__(16) float Xs[GB_K][GB_M + 4];
     __shared__ __align__(16) float As[GB_K][GB_N + 4];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int64_t p0 = (int64_t)blockIdx.y * GB_M;
-    const int f0 = blockIdx.x * GB_N;
+    const int64_t p0 = (int64_t)blockIdx.x * GB_M;   // rows on x (up to 2^31 - 1 blocks)
+    const int f0 = blockIdx.y * GB_N;
     float acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)

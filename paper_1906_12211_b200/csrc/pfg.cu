@@ -343,9 +343,17 @@ struct pfg_index {
     int64_t last_fused = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     float last_ms[3] = {0, 0, 0};
+    // per-phase timing (opts->timing): an event before each query-phase kernel; the interval
+    // starting at event i belongs to phase pkind[i] (kPh* below)
+    std::vector<cudaEvent_t> pev;
+    std::vector<int> pkind;
+    int pev_n = 0;
+    float last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int last_launches = 0;
     ~pfg_index() {
         for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : pev)
             if (e) cudaEventDestroy(e);
         if (h_ctl) cudaFreeHost(h_ctl);
         if (h_jhist) cudaFreeHost(h_jhist);
@@ -413,7 +421,7 @@ void launch_mc(const float* XY, int ld, int64_t npairs, const Geo& g, const uint
 
 void hp_bits(const float* X, int64_t np, int ldx, const float* A, int nf, int lda, int kdim, uint8_t* out,
              int64_t out_ld, cudaStream_t st) {
-    dim3 grid((nf + GB_N - 1) / GB_N, (unsigned)((np + GB_M - 1) / GB_M));
+    dim3 grid((unsigned)((np + GB_M - 1) / GB_M), (nf + GB_N - 1) / GB_N);
     k_hp_bits<<<grid, 256, 0, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
 }
 
@@ -766,6 +774,32 @@ pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0,
     return PFG_OK;
 }
 
+// phases of pfg_last_phases: 0 expand, 1 scan, 2 dedupe, 3 sims, 4 merge, 5 fused kernel,
+// 6 other query-phase work (round control, query order, code extension)
+enum { kPhExpand = 0, kPhScan, kPhDedupe, kPhSims, kPhMerge, kPhFused, kPhOther, kPhEnd = -1 };
+pfg_status phase_mark(pfg_index* I, bool on, int kind, cudaStream_t st) {
+    if (!on) return PFG_OK;
+    if (I->pev_n == (int)I->pev.size()) {
+        cudaEvent_t e;
+        PFG_CUDA(cudaEventCreate(&e));
+        I->pev.push_back(e);
+        I->pkind.push_back(kind);
+    }
+    I->pkind[I->pev_n] = kind;
+    PFG_CUDA(cudaEventRecord(I->pev[I->pev_n++], st));
+    return PFG_OK;
+}
+pfg_status phase_collect(pfg_index* I) {
+    for (float& v : I->last_phase_ms) v = 0.0f;
+    for (int i = 0; i + 1 < I->pev_n; ++i) {
+        float ms = 0.0f;
+        PFG_CUDA(cudaEventElapsedTime(&ms, I->pev[i], I->pev[i + 1]));
+        if (I->pkind[i] >= 0) I->last_phase_ms[I->pkind[i]] += ms;
+    }
+    I->pev_n = 0;
+    return PFG_OK;
+}
+
 // the query sketches of prep_queries are ready on `st` after this
 pfg_status join_sketches(pfg_index* I, cudaStream_t st) {
     if (I->g.M > 0 && I->ev_join) PFG_CUDA(cudaStreamWaitEvent(st, I->ev_join, 0));
@@ -1068,8 +1102,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const unsigned sb = (unsigned)(I->num_sms * 2);
         int round = 0;
         uint32_t nact = (uint32_t)nq;
+        const bool tm = s.timing >= 2;
         while (round < max_rounds) {
             const int par = round & 1;
+            PFG_TRY(phase_mark(I, tm, kPhExpand, st));
             switch (epl) {
                 case 1: k_expand<1><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
                 case 2: k_expand<2><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
@@ -1078,10 +1114,15 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 case 16: k_expand<16><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
                 default: k_expand<32><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
             }
+            PFG_TRY(phase_mark(I, tm, kPhScan, st));
             k_scan<<<tb_s, 256, 0, st>>>(p, par);
+            PFG_TRY(phase_mark(I, tm, kPhDedupe, st));
             k_dedupe<<<qb_d, 128, dsm, st>>>(p, par);
+            PFG_TRY(phase_mark(I, tm, kPhSims, st));
             k_sims<<<sb, 256, 0, st>>>(p, par);
+            PFG_TRY(phase_mark(I, tm, kPhMerge, st));
             k_merge<<<qb_m, 128, msm, st>>>(p, par);
+            PFG_TRY(phase_mark(I, tm, kPhOther, st));
             PFG_CUDA(cudaGetLastError());
             I->launches += 5;
             ++round;
@@ -1135,6 +1176,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         p.qlist = I->qord_list.as<uint32_t>();
     }
     if (fused_n > 0) {
+        PFG_TRY(phase_mark(I, s.timing >= 2, kPhFused, st));
         PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((fused_n + 3) / 4, max_blocks));
         switch (epl) {
@@ -1148,6 +1190,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->launches += 1;
     }
     I->last_fused = fused_n;
+    PFG_TRY(phase_mark(I, s.timing >= 2, kPhEnd, st));
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[2], st));
     if (!ids_dev) PFG_CUDA(cudaMemcpyAsync(out_ids, d_ids, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
     if (!sims_dev) PFG_CUDA(cudaMemcpyAsync(out_sims, d_sims, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));
@@ -1186,12 +1229,19 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         if (tot) I->eager = std::max(8, std::min(64, e));
     }
     if (s.timing) {
+        if (s.timing >= 2) PFG_TRY(phase_collect(I));
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[0], I->ev[0], I->ev[1]));
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[1], I->ev[1], I->ev[2]));
         PFG_CUDA(cudaEventElapsedTime(&I->last_ms[2], I->ev[0], I->ev[2]));
     }
     if (*I->h_zmin != ~0ull)
         return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(*I->h_zmin) + " is a zero vector");
+    return PFG_OK;
+}
+
+pfg_status pfg_last_phases(const pfg_index* I, float* ms, int32_t n) {
+    if (!I || !ms || n < 0) return fail(PFG_E_ARG, "NULL index or output");
+    for (int i = 0; i < n && i < 8; ++i) ms[i] = I->last_phase_ms[i];
     return PFG_OK;
 }
 

@@ -115,7 +115,7 @@ CONFIGS = {
     4: dict(name="hidim-1Mx960", n=1_000_000, d=960, nq=1_000, k=100, recall=0.9,
             family="simhash", strategy="pool", reps=0, budget=16 << 30),
     5: dict(name="scaleout-100Mx100", n=100_000_000, d=100, nq=100_000, k=10, recall=0.9,
-            family="fht_cp", strategy="independent", reps=0, budget=120 << 30),
+            family="fht_cp", strategy="independent", reps=0, budget=120 << 30, shard_n=12_500_000),
 }
 
 
