@@ -241,7 +241,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--recall", type=float, default=0.9)
-    ap.add_argument("--rep-chunk", type=int, default=8)
+    ap.add_argument("--rep-chunk", type=int, default=16)
     ap.add_argument("--nq", type=int, default=0, help="override the query count")
     ap.add_argument("--ref-sample", type=int, default=20)
     ap.add_argument("--cpu-sample", type=int, default=200)

@@ -76,7 +76,7 @@ typedef struct {
 /* Search options.  Zero-initialise + struct_size; zero field = default.  NULL = all defaults. */
 typedef struct {
     uint32_t struct_size;
-    int32_t rep_chunk;        /* [8] R: the filter threshold tau is refreshed once per chunk of R
+    int32_t rep_chunk;        /* [16] R: the filter threshold tau is refreshed once per chunk of R
                                  repetitions (R-17); the search's first chunk is the single
                                  repetition 0 (tau is set right after it) unless
                                  uniform_chunks = 1 */

@@ -17,6 +17,7 @@ import numpy as np
 from ._build import LIB as _LIB_PATH
 
 SIMHASH, CROSSPOLYTOPE_FHT = 0, 1
+DEFAULT_REP_CHUNK = 16  # R of pfg_search_opts (R-17); measured best on config 2
 INDEPENDENT, POOL = 0, 1
 FAMILIES = {"simhash": SIMHASH, "hp": SIMHASH, "fht_cp": CROSSPOLYTOPE_FHT, "crosspolytope_fht": CROSSPOLYTOPE_FHT}
 STRATEGIES = {"independent": INDEPENDENT, "pool": POOL}
@@ -206,7 +207,7 @@ class Index:
             pass
 
     @staticmethod
-    def _sopts(rep_chunk=8, segment=12, stop_rule=0, per_round=False, use_filter=True, eps=0.0,
+    def _sopts(rep_chunk=DEFAULT_REP_CHUNK, segment=12, stop_rule=0, per_round=False, use_filter=True, eps=0.0,
                trace_cap=0, trace_ptr=None, timing=False, engine=0, uniform_chunks=False, rounds=0) -> SearchOpts:
         o = SearchOpts()
         o.struct_size = C.sizeof(SearchOpts)

@@ -275,7 +275,7 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
             return fail(PFG_E_ARG, "pfg_search_opts.struct_size must be sizeof(pfg_search_opts)");
         std::memcpy(&z, o, o->struct_size);
     }
-    s.R = z.rep_chunk ? z.rep_chunk : 8;
+    s.R = z.rep_chunk ? z.rep_chunk : 16;
     if (s.R < 1 || s.R > kMaxR) return fail(PFG_E_ARG, "rep_chunk must be in [1, 32]");
     s.B = z.segment ? z.segment : 12;
     if (s.B < 1) return fail(PFG_E_ARG, "segment must be >= 1");

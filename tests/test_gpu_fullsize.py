@@ -38,7 +38,7 @@ def test_config1_full():
     o = O.OracleIndex(data, O.HP, L=c["reps"], seed=1)
     cap = 10000
     gr = g.search(torch.from_numpy(q).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
-    orr = o.search(q, c["k"], c["recall"], rep_chunk=8, trace_cap=cap)
+    orr = o.search(q, c["k"], c["recall"], rep_chunk=pfg.DEFAULT_REP_CHUNK, trace_cap=cap)
     _search_equal(gr, orr, cap)
     for j in range(c["reps"]):
         tab = g.export_table(j)
@@ -71,7 +71,7 @@ def test_config2_full_sampled():
     ids, sims, st, tr = g.search(torch.from_numpy(q).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
     sel = np.arange(0, len(q), 50)
     sub = (ids[sel], sims[sel], st[sel], tr[sel])
-    orr = o.search(q[sel], c["k"], c["recall"], rep_chunk=8, trace_cap=cap, threads=1)
+    orr = o.search(q[sel], c["k"], c["recall"], rep_chunk=pfg.DEFAULT_REP_CHUNK, trace_cap=cap, threads=1)
     _search_equal(sub, orr, cap)
 
 

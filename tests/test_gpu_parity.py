@@ -150,7 +150,7 @@ def _compare(c, k, recall, gpu_kw, orc_kw, trace=True):
 
 
 @pytest.mark.parametrize("name", ALL)
-@pytest.mark.parametrize("R", [1, 8])
+@pytest.mark.parametrize("R", [1, 8, 16])
 @pytest.mark.parametrize("recall", [0.5, 0.9, 0.99])
 @pytest.mark.parametrize("engine", [0, 1])
 def test_search_parity(cases, name, R, recall, engine):
@@ -208,7 +208,7 @@ def test_k_greater_than_n():
     g = pfg.Index(_cuda(data), 0, "simhash", seed=4, reps=3)
     o = O.OracleIndex(data, O.HP, L=3, seed=4)
     ids, sims, st = g.search(_cuda(q), 12, 0.9, stats=True)
-    oids, osims, otr = o.search(q, 12, 0.9, rep_chunk=8)
+    oids, osims, otr = o.search(q, 12, 0.9, rep_chunk=pfg.DEFAULT_REP_CHUNK)
     assert np.array_equal(ids.cpu().numpy(), oids)
     assert np.all(ids.cpu().numpy()[:, 7:] == -1) and np.all(np.isneginf(sims.cpu().numpy()[:, 7:]))
     assert np.all(st["flags"] & 1)
@@ -226,7 +226,7 @@ def test_zero_query_row_reported_and_others_answered(cases):
     sims = torch.empty((len(q), 10), dtype=torch.float32, device=DEV)
     with pytest.raises(pfg.PfgError):
         c.gpu.search(_cuda(q), 10, 0.9, out=(ids, sims))
-    oids, _, _ = c.orc.search(np.delete(q, 3, axis=0), 10, 0.9, rep_chunk=8)
+    oids, _, _ = c.orc.search(np.delete(q, 3, axis=0), 10, 0.9, rep_chunk=pfg.DEFAULT_REP_CHUNK)
     assert np.array_equal(np.delete(ids.cpu().numpy(), 3, axis=0), oids)
     assert np.all(ids.cpu().numpy()[3] == -1) and np.all(np.isnan(sims.cpu().numpy()[3]))
 
@@ -271,7 +271,7 @@ def test_repeat_search_is_deterministic(cases):
 def test_single_query_and_empty_batch(cases):
     c = cases["hp"]
     ids, sims = c.gpu.search(_cuda(c.q[:1]), 10, 0.9)
-    oids, _, _ = c.orc.search(c.q[:1], 10, 0.9, rep_chunk=8)
+    oids, _, _ = c.orc.search(c.q[:1], 10, 0.9, rep_chunk=pfg.DEFAULT_REP_CHUNK)
     assert np.array_equal(ids.cpu().numpy(), oids)
     e_ids, _ = c.gpu.search(_cuda(c.q[:0]), 10, 0.9)
     assert e_ids.shape == (0, 10)
@@ -291,7 +291,7 @@ def test_sharded_merge_equals_per_shard_oracle():
         i, s = g.search(_cuda(q), k, 0.9)
         g_ids.append(i); g_sims.append(s)
         o = O.OracleIndex(sl, O.FHTCP, L=12, seed=7)
-        oi, os_, _ = o.search(q, k, 0.9, rep_chunk=8)
+        oi, os_, _ = o.search(q, k, 0.9, rep_chunk=pfg.DEFAULT_REP_CHUNK)
         o_ids.append(np.where(oi >= 0, oi + r * per, -1)); o_sims.append(os_)
     mi, ms = pfg.merge_topk(torch.stack(g_ids), torch.stack(g_sims))
     ci = np.concatenate(o_ids, axis=1); cs = np.concatenate(o_sims, axis=1)

@@ -20,7 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--recall", type=float, default=0.9)
-ap.add_argument("--rep-chunk", type=int, default=8)
+ap.add_argument("--rep-chunk", type=int, default=16)
 ap.add_argument("--nq", type=int, default=0)
 ap.add_argument("--warm", type=int, default=2)
 a = ap.parse_args()
