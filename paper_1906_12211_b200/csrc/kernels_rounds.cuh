@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256) k_scan(QueryParams p, int par) {
         const uint32_t total = info.z;
         const int c0 = rs.c0[q];
         if (lane < nr) c->seg[lane] = rs.rseg[q * kMaxR + lane];
-        if (p.use_filter)
+        if (p.use_filter && tau < 64)  // tau = 64 passes everything (round 0 runs before the sketches exist)
             for (int t = lane; t < p.M; t += 32) c->qsk[t] = p.qsk[q * p.M + t];
         __syncwarp();
         uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(256) k_scan(QueryParams p, int par) {
             const uint32_t g = g0 + u * 32 + lane;
             if (g < total) {
                 bool pass = true;
-                if (p.use_filter) {
+                if (p.use_filter && tau < 64) {
                     const int s_ = __ldg(p.slot + c0 + rv[u]);
                     pass = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ c->qsk[s_]) <= tau;
                 }

@@ -329,7 +329,9 @@ struct pfg_index {
     uint32_t* h_jhist = nullptr; // its pinned host copy
     int eager = 32;              // repetitions hashed eagerly per query (tuned from the last search)
     cudaStream_t aux = nullptr;  // second stream: query sketches run beside the query hashing
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t aux2 = nullptr; // third stream: codes and ranges of the later eager repetitions
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_late = nullptr;
+    bool late_pending = false;   // codes/ranges of repetitions [split, eager) still on aux2
     unsigned long long* h_zmin = nullptr;  // pinned host word: first zero query row
     int64_t rs_nq = 0;
     int rs_kt = 0, rs_L = 0;
@@ -338,7 +340,7 @@ struct pfg_index {
     int64_t slots_bm = 0;
     // launch accounting and phase timing of the last search
     int launches = 0;
-    int qc_n = 0, qc_ld = 0;
+    int qc_n = 0, qc_ld = 0, qc_split = 0;
     int last_rounds = 0;
     int64_t last_fused = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -360,6 +362,8 @@ struct pfg_index {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (aux) cudaStreamDestroy(aux);
+        if (aux2) cudaStreamDestroy(aux2);
+        if (ev_late) cudaEventDestroy(ev_late);
         if (h_zmin) cudaFreeHost(h_zmin);
     }
 };
@@ -696,7 +700,7 @@ pfg_status get_tau(pfg_index* I, float eps, std::shared_ptr<DBuf>& out, std::vec
 
 // normalise + sketch + (eager) code queries into index scratch; returns first zero row or -1
 pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool need_codes, bool force_codes, int64_t* zrow,
-                        bool* lazy, cudaStream_t st) {
+                        bool* lazy, cudaStream_t st, int split) {
     const Geo& g = I->g;
     const float* qsrc = queries;
     if (!is_device_ptr(queries)) {
@@ -720,8 +724,10 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         PFG_TRY(I->qsk.ensure((size_t)nq * g.M * 8, "query sketches"));
         if (!I->aux) {
             PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
+            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux2, cudaStreamNonBlocking));
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
+            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_late, cudaEventDisableTiming));
         }
         PFG_CUDA(cudaEventRecord(I->ev_fork, st));
         PFG_CUDA(cudaStreamWaitEvent(I->aux, I->ev_fork, 0));
@@ -748,9 +754,18 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         const int ne = std::min(g.L, getenv("PFG_EAGER") ? atoi(getenv("PFG_EAGER")) : I->eager);
         const int ld = std::min(g.L, ne + kExtReps);
         PFG_TRY(I->qcodes.ensure((size_t)nq * ld * 4, "query codes"));
-        PFG_TRY(fht_codes(I, nq, nullptr, 0, ne, ld, st));
+        // repetitions [0, split) now; [split, ne) on the third stream, joined before the round
+        // that first reaches them (the caller: late_join)
+        const int s0 = (split > 0 && split < ne && I->aux2) ? split : ne;
+        PFG_TRY(fht_codes(I, nq, nullptr, 0, s0, ld, st));
+        if (s0 < ne) {
+            PFG_CUDA(cudaStreamWaitEvent(I->aux2, I->ev_fork, 0));
+            PFG_TRY(fht_codes(I, nq, nullptr, s0, ne - s0, ld, I->aux2));
+            I->late_pending = true;
+        }
         I->qc_n = ne;
         I->qc_ld = ld;
+        I->qc_split = s0;
     }
     return PFG_OK;
 }
@@ -803,6 +818,14 @@ pfg_status phase_collect(pfg_index* I) {
 // the query sketches of prep_queries are ready on `st` after this
 pfg_status join_sketches(pfg_index* I, cudaStream_t st) {
     if (I->g.M > 0 && I->ev_join) PFG_CUDA(cudaStreamWaitEvent(st, I->ev_join, 0));
+    return PFG_OK;
+}
+// the codes (and ranges) of the later eager repetitions are ready on `st` after this
+pfg_status late_join(pfg_index* I, cudaStream_t st) {
+    if (I->late_pending) {
+        PFG_CUDA(cudaStreamWaitEvent(st, I->ev_late, 0));
+        I->late_pending = false;
+    }
     return PFG_OK;
 }
 
@@ -956,7 +979,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     }
     I->launches = 0;
     bool lazy = false;
-    PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st));
+    // rounds 0 and 1 reach repetitions [0, 1 + R) only (R-17 default schedule): the codes and
+    // ranges of the later eager repetitions are computed beside them
+    const int split = (s.engine == 0 && !s.uniform) ? 1 + s.R : 0;
+    PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st, split));
 
     const int k_eff = (int)std::min<int64_t>(k, g.n);
     const int kt = ((k_eff + 31) / 32) * 32;
@@ -1053,11 +1079,19 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     if (p.qb_n > 0) {
         PFG_TRY(I->qbnd.ensure((size_t)nq * p.qb_ld * 16, "query bounds"));
         p.qbnd = I->qbnd.as<uint4>();
-        const int64_t thr_n = nq * (int64_t)p.qb_n;
-        k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, p.qb_n);
+        const int b0 = std::min(p.qb_n, I->late_pending ? I->qc_split : p.qb_n);
+        const int64_t thr_n = nq * (int64_t)b0;
+        if (b0 > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, b0);
+        if (b0 < p.qb_n) {
+            const int64_t thr_l = nq * (int64_t)(p.qb_n - b0);
+            k_qbounds<<<(unsigned)((thr_l + 255) / 256), 256, 0, I->aux2>>>(p, I->qbnd.as<uint4>(), nullptr, nq, b0,
+                                                                          p.qb_n - b0);
+            I->launches += 1;
+        }
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
     }
+    if (I->late_pending) PFG_CUDA(cudaEventRecord(I->ev_late, I->aux2));
     // developer instrumentation: PFG_PHASE_PROF=1 prints per-phase warp cycles of each search to stderr
     static const bool phase_prof = getenv("PFG_PHASE_PROF") && getenv("PFG_PHASE_PROF")[0] == '1';
     DBuf profb;
@@ -1066,7 +1100,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(cudaMemsetAsync(profb.p, 0, 128, st));
         p.prof = profb.as<unsigned long long>();
     }
-    PFG_TRY(join_sketches(I, st));
+    if (!rounds) {
+        PFG_TRY(join_sketches(I, st));
+        PFG_TRY(late_join(I, st));
+    }
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[1], st));
     int64_t fused_n = nq;
     if (rounds) {
@@ -1105,6 +1142,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const bool tm = s.timing >= 2;
         while (round < max_rounds) {
             const int par = round & 1;
+            // round 0 is the single repetition 0 with tau = 64 (no sketches read); round 1 reaches
+            // repetitions < 1 + R; later rounds may reach every eager repetition
+            if (round == 1) PFG_TRY(join_sketches(I, st));
+            if (round == 2) PFG_TRY(late_join(I, st));
             PFG_TRY(phase_mark(I, tm, kPhExpand, st));
             switch (epl) {
                 case 1: k_expand<1><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
@@ -1175,6 +1216,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->launches += 3;
         p.qlist = I->qord_list.as<uint32_t>();
     }
+    PFG_TRY(join_sketches(I, st));
+    PFG_TRY(late_join(I, st));
     if (fused_n > 0) {
         PFG_TRY(phase_mark(I, s.timing >= 2, kPhFused, st));
         PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
@@ -1337,7 +1380,7 @@ pfg_status pfg_hash_queries(pfg_index* I, const float* queries, int64_t nq, uint
     const Geo& g = I->g;
     int64_t zrow = -1;
     bool lazy = false;
-    PFG_TRY(prep_queries(I, queries, nq, out_codes != nullptr, true, &zrow, &lazy, st));
+    PFG_TRY(prep_queries(I, queries, nq, out_codes != nullptr, true, &zrow, &lazy, st, 0));
     PFG_TRY(join_sketches(I, st));
     if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(zrow) + " is a zero vector");
     if (out_codes) {
