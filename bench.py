@@ -248,6 +248,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--engine", type=int, default=0, help="0 = bulk rounds + fused kernel, 1 = fused kernel only")
+    ap.add_argument("--uniform-chunks", action="store_true", help="first chunk R repetitions long (R-17 option)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -300,7 +301,7 @@ def main():
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    sopts = dict(rep_chunk=args.rep_chunk, timing=True, engine=args.engine)
+    sopts = dict(rep_chunk=args.rep_chunk, timing=True, engine=args.engine, uniform_chunks=args.uniform_chunks)
 
     def barrier():
         if world > 1:
@@ -415,7 +416,7 @@ def main():
                        + (f" ({c['shard_n']} rows per GPU)" if weak else ""),
                        "n": n, "d": d, "nq": nq, "k": k, "recall_target": args.recall, "family": c["family"],
                        "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": info["reps"],
-                       "rep_chunk": args.rep_chunk, "l2": "flushed (512 MiB write) between timed steps",
+                       "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"data-sharded x{world}" if world > 1 else "single GPU"},
             "recall": rec,
             "build_s": build_s,

@@ -106,6 +106,74 @@ __global__ void __launch_bounds__(256) k_hp_bits(const float* __restrict__ X, in
     }
 }
 
+// The same product as k_hp_bits with register double buffering: BK = 8 per step, each thread
+// fetches one float4 of X and one of A per step (kdim and both leading dimensions are multiples
+// of 8, rows 16-byte aligned) while the previous step is multiplied; accumulation order is the
+// canonical sequential chain over t, so the bits are identical to k_hp_bits.
+constexpr int GB2_K = 8;
+__global__ void __launch_bounds__(256, 2) k_hp_bits2(const float* __restrict__ X, int64_t np, int ldx,
+                                                     const float* __restrict__ A, int nf, int lda, int kdim,
+                                                     uint8_t* __restrict__ out, int64_t out_ld) {
+    __shared__ __align__(16) float Xs[2][GB2_K][GB_M + 4];
+    __shared__ __align__(16) float As[2][GB2_K][GB_N + 4];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t p0 = (int64_t)blockIdx.x * GB_M;
+    const int f0 = blockIdx.y * GB_N;
+    const int lr = tid >> 1, lk = (tid & 1) * 4;   // this thread's load: row lr, columns lk..lk+3
+    const bool xok = p0 + lr < np, aok = f0 + lr < nf;
+    const float4* xp = reinterpret_cast<const float4*>(X + (p0 + lr) * (int64_t)ldx + lk);
+    const float4* ap = reinterpret_cast<const float4*>(A + (int64_t)(f0 + lr) * lda + lk);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 xv = xok ? __ldg(xp) : z4, av = aok ? __ldg(ap) : z4;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    const int nk = kdim / GB2_K;
+    int buf = 0;
+    Xs[0][lk + 0][lr] = xv.x; Xs[0][lk + 1][lr] = xv.y; Xs[0][lk + 2][lr] = xv.z; Xs[0][lk + 3][lr] = xv.w;
+    As[0][lk + 0][lr] = av.x; As[0][lk + 1][lr] = av.y; As[0][lk + 2][lr] = av.z; As[0][lk + 3][lr] = av.w;
+    __syncthreads();
+    for (int s = 0; s < nk; ++s) {
+        if (s + 1 < nk) {
+            xv = xok ? __ldg(xp + (s + 1) * (GB2_K / 4)) : z4;
+            av = aok ? __ldg(ap + (s + 1) * (GB2_K / 4)) : z4;
+        }
+#pragma unroll
+        for (int c = 0; c < GB2_K; ++c) {
+            const float4 x0 = *reinterpret_cast<const float4*>(&Xs[buf][c][ty * 8]);
+            const float4 x1 = *reinterpret_cast<const float4*>(&Xs[buf][c][ty * 8 + 4]);
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][c][tx * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][c][tx * 8 + 4]);
+            const float xr[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            const float ar[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(xr[i], ar[j], acc[i][j]);
+        }
+        if (s + 1 < nk) {
+            buf ^= 1;
+            Xs[buf][lk + 0][lr] = xv.x; Xs[buf][lk + 1][lr] = xv.y; Xs[buf][lk + 2][lr] = xv.z; Xs[buf][lk + 3][lr] = xv.w;
+            As[buf][lk + 0][lr] = av.x; As[buf][lk + 1][lr] = av.y; As[buf][lk + 2][lr] = av.z; As[buf][lk + 3][lr] = av.w;
+            __syncthreads();
+        }
+    }
+    const int fb = f0 + tx * 8;
+    if (fb >= nf) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t p = p0 + ty * 8 + i;
+        if (p >= np) continue;
+        uint32_t bbits = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (fb + j < nf && acc[i][j] >= 0.0f) bbits |= 1u << j;
+        out[p * out_ld + (fb >> 3)] = (uint8_t)bbits;
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // HP repetition codes from bits (ell = 1, c = K functions): code_j = bits of functions
 // f_{j,0} .. f_{j,K-1}, the first the most significant (R-7).

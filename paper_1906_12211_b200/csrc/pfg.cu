@@ -426,7 +426,11 @@ void launch_mc(const float* XY, int ld, int64_t npairs, const Geo& g, const uint
 void hp_bits(const float* X, int64_t np, int ldx, const float* A, int nf, int lda, int kdim, uint8_t* out,
              int64_t out_ld, cudaStream_t st) {
     dim3 grid((unsigned)((np + GB_M - 1) / GB_M), (nf + GB_N - 1) / GB_N);
-    k_hp_bits<<<grid, 256, 0, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
+    // the double-buffered kernel needs kdim, ldx, lda multiples of 8 and 16-byte aligned rows
+    const bool v2 = (kdim % GB2_K) == 0 && (ldx % 4) == 0 && (lda % 4) == 0 && ((uintptr_t)X % 16) == 0 &&
+                    ((uintptr_t)A % 16) == 0 && !getenv("PFG_HP_V1");
+    if (v2) k_hp_bits2<<<grid, 256, 0, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
+    else k_hp_bits<<<grid, 256, 0, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
 }
 
 // Monte-Carlo CP table (R-13 cleaning, R-14 random pairs)
