@@ -32,6 +32,7 @@ namespace pfg {
 
 constexpr int kFlagDone = 1, kFlagFused = 2;
 constexpr int kEPre = 16;  // evaluated ids loaded per lane per batch when the hash set is rebuilt
+constexpr int kSaveMin = 512;  // k_dedupe rebuilds sets of at most this many ids instead of restoring them
 
 __device__ __forceinline__ int tau_of_state(const QueryParams& p, int tn, const uint64_t* T) {
     if (!p.use_filter || tn != p.k_eff) return 64;
@@ -345,10 +346,27 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
         const uint32_t nE = rs.cnt[q * kCnt + 3];
         uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
         const uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
-        // the hash set as the previous round left it (saved in global memory), or empty
+        // the hash set as the previous round left it: saved in global memory when it held more
+        // than kSaveMin ids, else rebuilt here from the evaluated list (cheaper than 16 KB of
+        // traffic for a small set)
         uint4* hsv = reinterpret_cast<uint4*>(rs.hsave + q * (int64_t)kHC);
-        if (nE == 0) {
+        if (nE <= (uint32_t)kSaveMin) {
             for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+            __syncwarp();
+            for (uint32_t e0 = 0; e0 < nE; e0 += 32 * kEPre) {
+                uint32_t v[kEPre];
+#pragma unroll
+                for (int u = 0; u < kEPre; ++u) {
+                    const uint32_t e = e0 + u * 32 + lane;
+                    v[u] = e < nE ? E[e] : kEmpty;
+                }
+#pragma unroll
+                for (int u = 0; u < kEPre; ++u)
+                    if (v[u] != kEmpty) {
+                        uint32_t h = hs_slot(v[u]);
+                        while (atomicCAS(&c->hs[h], kEmpty, v[u]) != kEmpty) h = hs_next(h);
+                    }
+            }
         } else {
             uint4 tmp[kHC / 128];
 #pragma unroll
@@ -449,9 +467,11 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
             rc[2] = c->dcnt[lane];
         }
         if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }
-        // carry the set to the next round (the fused kernel rebuilds it from E instead)
+        // carry a large set to the next round (the fused kernel rebuilds it from E instead)
+        if (nE + ns > (uint32_t)kSaveMin) {
 #pragma unroll
-        for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
+            for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
+        }
         __syncwarp();
     }
 }

@@ -129,7 +129,10 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     if (family != PFG_SIMHASH && family != PFG_CROSSPOLYTOPE_FHT) return fail(PFG_E_ARG, "unknown family");
     g.n = n;
     g.d = d;
-    g.dpad = (d + 7) & ~7;  // rows 32-byte aligned
+    {
+        const int al = getenv("PFG_DPAD_ALIGN") ? std::max(8, atoi(getenv("PFG_DPAD_ALIGN"))) : 8;
+        g.dpad = (d + al - 1) / al * al;  // rows 32-byte aligned (PFG_DPAD_ALIGN: developer experiments)
+    }
     if ((uint64_t)n * (uint64_t)g.dpad / 4 >= (1ull << 32))
         return fail(PFG_E_ARG, "n * d too large for one index (shard the data: n * d / 4 must be < 2^32)");
     g.family = family;
