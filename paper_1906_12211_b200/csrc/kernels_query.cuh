@@ -67,7 +67,8 @@ struct RoundState {
     uint32_t* E;        // [nq][Ecap] evaluated ids in evaluation order
     uint4* pend;        // [nq][kMaxR] cursors of the chunk in flight (committed by k_merge)
     uint32_t* cand;     // [nq][Ccap] candidate id per emitted position of the chunk (kEmpty = filtered)
-    uint8_t* crep;      // [nq][Ccap] repetition (within the chunk) of each emitted position
+    uint8_t* crep;      // [nq][Ccap] repetition (within the chunk) of each candidate
+    uint32_t* tcnt;     // [nq][Ccap/kTile] candidates (positions passing the filter) of each scan tile
     uint32_t* hsave;    // [nq][kHC] k_dedupe's hash set carried to the next round
     uint4* rseg;        // [nq][kMaxR] {lo_new, left length, hi_old, first position} per repetition
     uint4* rinfo;       // [nq] {chunk repetitions, tau, emitted positions, 0}

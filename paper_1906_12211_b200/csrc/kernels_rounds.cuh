@@ -301,19 +301,25 @@ __global__ void __launch_bounds__(256) k_scan(QueryParams p, int par) {
                 rv[u] = rl;
             }
         }
+        // the passing positions of the tile, compacted in order to the front of the tile's slots
+        uint32_t cnt = 0;
 #pragma unroll
         for (int u = 0; u < kTile / 32; ++u) {
             const uint32_t g = g0 + u * 32 + lane;
-            if (g < total) {
-                bool pass = true;
-                if (p.use_filter && tau < 64) {
-                    const int s_ = __ldg(p.slot + c0 + rv[u]);
-                    pass = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ c->qsk[s_]) <= tau;
-                }
-                cand[g] = pass ? e[u].x : kEmpty;
-                crep[g] = (uint8_t)rv[u];
+            bool pass = g < total;
+            if (pass && p.use_filter && tau < 64) {
+                const int s_ = __ldg(p.slot + c0 + rv[u]);
+                pass = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ c->qsk[s_]) <= tau;
             }
+            const uint32_t pm = __ballot_sync(kFull, pass);
+            if (pass) {
+                const uint32_t dst = g0 + cnt + __popc(pm & lanemask_lt());
+                cand[dst] = e[u].x;
+                crep[dst] = (uint8_t)rv[u];
+            }
+            cnt += __popc(pm);
         }
+        if (lane == 0) rs.tcnt[q * (int64_t)(rs.Ccap / kTile) + tl.y] = cnt;
         __syncwarp();
     }
 }
@@ -381,14 +387,24 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
         uint32_t ns = 0;
         bool overflow = false;
         const uint8_t* crep = rs.crep + q * (int64_t)rs.Ccap;
-        for (uint32_t g0 = 0; g0 < total && !overflow; g0 += 32 * kCPre) {
+        // k_scan left the passing candidates of tile t at [t*kTile, t*kTile + tcnt[t]), in order;
+        // a batch is kCPre/4 consecutive tiles
+        constexpr int kTPB = kCPre * 32 / kTile;
+        const uint32_t ntl = (total + kTile - 1) / kTile;
+        const uint32_t* tcnt = rs.tcnt + q * (int64_t)(rs.Ccap / kTile);
+        for (uint32_t t0 = 0; t0 < ntl && !overflow; t0 += kTPB) {
             uint32_t v[kCPre], h[kCPre];
             int rr[kCPre];
             bool found[kCPre];
+            uint32_t tc[kTPB];
+#pragma unroll
+            for (int b = 0; b < kTPB; ++b) tc[b] = (t0 + b < ntl) ? tcnt[t0 + b] : 0u;
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
-                const uint32_t g = g0 + u * 32 + lane;
-                const bool live = g < total;
+                const int b = u / (kTile / 32);
+                const uint32_t o = (u % (kTile / 32)) * 32 + lane;
+                const bool live = o < tc[b];
+                const uint32_t g = (t0 + b) * kTile + o;
                 v[u] = live ? cand[g] : kEmpty;
                 rr[u] = live ? (int)crep[g] : -1;
             }
@@ -396,6 +412,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
                 found[u] = false;
+                if ((uint32_t)((u % (kTile / 32)) * 32) >= tc[u / (kTile / 32)]) { h[u] = 0; continue; }  // empty step
                 h[u] = hs_slot(v[u]);
                 if (v[u] != kEmpty) {
                     for (;;) {
@@ -411,6 +428,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
             // claimed earlier in the batch finds it in the set
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
+                if ((uint32_t)((u % (kTile / 32)) * 32) >= tc[u / (kTile / 32)]) continue;  // empty step (warp-uniform)
                 const bool pass = v[u] != kEmpty;
                 const bool need = pass && !found[u];
                 const uint32_t nm = __ballot_sync(kFull, need);
@@ -428,8 +446,8 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
                     }
                 }
                 if (rr[u] >= 0) {
-                    if (!pass) atomicAdd(&c->fcnt[rr[u]], 1u);
-                    else if (!fresh) atomicAdd(&c->dcnt[rr[u]], 1u);
+                    atomicAdd(&c->fcnt[rr[u]], 1u);  // passing the filter (filtered = emitted - passing)
+                    if (!fresh) atomicAdd(&c->dcnt[rr[u]], 1u);
                 }
                 const uint32_t fm = __ballot_sync(kFull, fresh);
                 if (fresh) E[nE + ns + __popc(fm & lanemask_lt())] = v[u];
@@ -462,8 +480,9 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
         }
         if (lane < nr) {
             uint32_t* rc = rs.repcnt + (q * kMaxR + lane) * 3;
-            rc[0] = c->beg[lane + 1] - c->beg[lane];
-            rc[1] = c->fcnt[lane];
+            const uint32_t em = c->beg[lane + 1] - c->beg[lane];
+            rc[0] = em;
+            rc[1] = em - c->fcnt[lane];
             rc[2] = c->dcnt[lane];
         }
         if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }
