@@ -56,6 +56,7 @@ struct RoundCtl {
     uint32_t ntiles[2];    // scan tiles of the round (round parity)
     uint32_t pad;
     uint32_t wk[2][4];     // work counters of k_expand, k_scan, k_dedupe, k_merge (round parity)
+    uint32_t dfront[2], dback[2];  // k_dedupe's order: long chunks from the front, the rest from the back
 };
 struct RoundState {
     int32_t* lvl;       // [nq] next level i to process (K..1); 0 = only the i = 0 scan remains
@@ -80,6 +81,7 @@ struct RoundState {
     uint32_t* poff;     // [nq] first pool entry of the query
     uint32_t* pn;       // [nq] pool entries of the query
     uint32_t* act[2];   // [nq] active lists (round parity)
+    uint32_t* dord[2];  // [nq] the active list reordered for k_dedupe (long chunks first)
     uint32_t* fused;    // [nq] queries handed to the fused kernel
     RoundCtl* ctl;
     int Ecap, Ccap;

@@ -144,6 +144,10 @@ __host__ __device__ inline int expand_smem_bytes(int dpad, bool lazy) {
 #define PFG_TILE 128
 #endif
 constexpr int kTile = PFG_TILE;   // emitted positions per scan tile
+#ifndef PFG_DLONG
+#define PFG_DLONG 2048
+#endif
+constexpr int kDedupeLong = PFG_DLONG;  // emitted positions from which k_dedupe schedules a chunk first
 
 template <int EPL>
 __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy) {
@@ -156,6 +160,7 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         rs.ctl->nact[par ^ 1] = 0; rs.ctl->pool_top[par ^ 1] = 0; rs.ctl->ntiles[par ^ 1] = 0;
         for (int t = 0; t < 4; ++t) rs.ctl->wk[par ^ 1][t] = 0;
+        rs.ctl->dfront[par ^ 1] = 0; rs.ctl->dback[par ^ 1] = 0;
     }
     const uint32_t* act = rs.act[par];
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -248,6 +253,10 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
             rs.cnt[q * kCnt + 4] += probes;
             if (over) rs.flags[q] |= kFlagFused;
             if (ntl) base = atomicAdd(&rs.ctl->ntiles[par], ntl);
+            // k_dedupe takes the long chunks first (a shorter tail for its dynamic scheduler)
+            const uint32_t slot = total >= (uint32_t)kDedupeLong ? atomicAdd(&rs.ctl->dfront[par], 1u)
+                                                                  : nact - 1u - atomicAdd(&rs.ctl->dback[par], 1u);
+            rs.dord[par][slot] = (uint32_t)q;
         }
         base = __shfl_sync(kFull, base, 0);
         for (uint32_t t = lane; t < ntl; t += 32) rs.tiles[base + t] = make_uint2((uint32_t)q, t);
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
     DedupeSmem* c = (DedupeSmem*)(smem_raw + wib * align16((int)sizeof(DedupeSmem)));
     const RoundState& rs = p.rs;
     const uint32_t nact = rs.ctl->nact[par];
-    const uint32_t* act = rs.act[par];
+    const uint32_t* act = rs.dord[par];
     for (uint32_t a = next_item(&rs.ctl->wk[par][2], lane); a < nact; a = next_item(&rs.ctl->wk[par][2], lane)) {
         const int64_t q = act[a];
         if (rs.flags[q] & kFlagFused) continue;
