@@ -30,7 +30,7 @@
 
 namespace pfg {
 
-constexpr int kFlagDone = 1, kFlagFused = 2;
+constexpr int kFlagDone = 1, kFlagFused = 2, kFlagSaved = 4;  // kFlagSaved: hsave holds the set
 constexpr int kEPre = 16;  // evaluated ids loaded per lane per batch when the hash set is rebuilt
 constexpr int kSaveMin = 512;  // k_dedupe rebuilds sets of at most this many ids instead of restoring them
 
@@ -245,21 +245,38 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
         if (lane < nr) rs.rseg[q * kMaxR + lane] = make_uint4(nelo, elo - nelo, ehi, incl - em);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) probes += __shfl_xor_sync(kFull, probes, off);
-        const bool over = total > (uint32_t)rs.Ccap;
+        // a single repetition with nothing evaluated yet and tau = 64 (the search's first chunk):
+        // every emitted id is fresh (a repetition holds each id once), so k_scan writes the ids
+        // straight to the evaluated list and the round's pool and k_dedupe skips the query
+        const bool direct = nr == 1 && tau == 64 && rs.cnt[q * kCnt + 3] == 0;
+        const bool over = total > (uint32_t)(direct ? kHMax : rs.Ccap);
         const uint32_t ntl = over ? 0u : (total + kTile - 1) / kTile;
         uint32_t base = 0;
         if (lane == 0) {
-            rs.rinfo[q] = make_uint4((uint32_t)nr, (uint32_t)tau, total, 0u);
+            rs.rinfo[q] = make_uint4((uint32_t)nr, (uint32_t)tau, total, direct ? 1u : 0u);
             rs.cnt[q * kCnt + 4] += probes;
             if (over) rs.flags[q] |= kFlagFused;
-            if (ntl) base = atomicAdd(&rs.ctl->ntiles[par], ntl);
+            if (direct && !over) {
+                const uint32_t pb = atomicAdd(&rs.ctl->pool_top[par], total);
+                if ((uint64_t)pb + total > rs.pool_cap) {
+                    rs.flags[q] |= kFlagFused;
+                } else {
+                    rs.poff[q] = pb;
+                    rs.pn[q] = total;
+                    uint32_t* rc = rs.repcnt + q * kMaxR * 3;
+                    rc[0] = total; rc[1] = 0; rc[2] = 0;
+                }
+            }
+            if (ntl && !(rs.flags[q] & kFlagFused)) base = atomicAdd(&rs.ctl->ntiles[par], ntl);
             // k_dedupe takes the long chunks first (a shorter tail for its dynamic scheduler)
             const uint32_t slot = total >= (uint32_t)kDedupeLong ? atomicAdd(&rs.ctl->dfront[par], 1u)
                                                                   : nact - 1u - atomicAdd(&rs.ctl->dback[par], 1u);
             rs.dord[par][slot] = (uint32_t)q;
         }
         base = __shfl_sync(kFull, base, 0);
-        for (uint32_t t = lane; t < ntl; t += 32) rs.tiles[base + t] = make_uint2((uint32_t)q, t);
+        const bool handed = __shfl_sync(kFull, (rs.flags[q] & kFlagFused) ? 1 : 0, 0);
+        if (!handed)
+            for (uint32_t t = lane; t < ntl; t += 32) rs.tiles[base + t] = make_uint2((uint32_t)q, t);
         __syncwarp();
     }
 }
@@ -310,6 +327,22 @@ __global__ void __launch_bounds__(256) k_scan(QueryParams p, int par) {
                 rv[u] = rl;
             }
         }
+        if (info.w) {
+            // direct chunk (k_expand): every position is a fresh evaluated id
+            const uint32_t pb = rs.poff[q];
+            uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
+#pragma unroll
+            for (int u = 0; u < kTile / 32; ++u) {
+                const uint32_t g = g0 + u * 32 + lane;
+                if (g < total) {
+                    rs.pool_id[pb + g] = e[u].x;
+                    rs.pool_q[pb + g] = (uint32_t)q;
+                    E[g] = e[u].x;
+                }
+            }
+            __syncwarp();
+            continue;
+        }
         // the passing positions of the tile, compacted in order to the front of the tile's slots
         uint32_t cnt = 0;
 #pragma unroll
@@ -354,18 +387,21 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
     const uint32_t* act = rs.dord[par];
     for (uint32_t a = next_item(&rs.ctl->wk[par][2], lane); a < nact; a = next_item(&rs.ctl->wk[par][2], lane)) {
         const int64_t q = act[a];
-        if (rs.flags[q] & kFlagFused) continue;
+        const int fl = rs.flags[q];
+        if (fl & kFlagFused) continue;
         const uint4 info = rs.rinfo[q];
+        if (info.w) continue;  // direct chunk: k_scan wrote the evaluated ids and the pool
         const int nr = (int)info.x;
         const uint32_t total = info.z;
         const uint32_t nE = rs.cnt[q * kCnt + 3];
         uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
         const uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
-        // the hash set as the previous round left it: saved in global memory when it held more
-        // than kSaveMin ids, else rebuilt here from the evaluated list (cheaper than 16 KB of
-        // traffic for a small set)
+        // the hash set as the previous round left it: saved in global memory once it holds more
+        // than kSaveMin ids (kFlagSaved), else rebuilt here from the evaluated list (cheaper than
+        // 16 KB of traffic for a small set)
         uint4* hsv = reinterpret_cast<uint4*>(rs.hsave + q * (int64_t)kHC);
-        if (nE <= (uint32_t)kSaveMin) {
+        const bool saved = (fl & kFlagSaved) != 0;
+        if (!saved) {
             for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
             __syncwarp();
             for (uint32_t e0 = 0; e0 < nE; e0 += 32 * kEPre) {
@@ -497,6 +533,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
         if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }
         // carry a large set to the next round (the fused kernel rebuilds it from E instead)
         if (nE + ns > (uint32_t)kSaveMin) {
+            if (lane == 0 && !saved) rs.flags[q] |= kFlagSaved;
 #pragma unroll
             for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
         }
