@@ -666,6 +666,8 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
             const uint32_t o = __shfl_up_sync(kFull, end, off);
             if (lane >= off) end += o;
         }
+        // stop thresholds of the chunk's repetitions, lane r holds repetition c0 + r's
+        const float thr_r = lane < nr ? __ldg(p.thr + (int64_t)(i - 1) * p.L + c0 + lane) : INFINITY;
         __syncwarp();
         int r_stop = -1;
         uint32_t e = 0;
@@ -708,10 +710,11 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
             nE += e2 - e;
             e = e2;
             const int j1 = c0 + r + 1;
+            const float th = __shfl_sync(kFull, thr_r, r);
             if (tn == p.k_eff && (!p.per_round || j1 == p.L)) {
                 float ip = key_sim(T[p.k_eff - 1]);
                 ip = fminf(fmaxf(ip, -1.0f), 1.0f);
-                if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + (j1 - 1))) { r_stop = r; break; }
+                if (ip >= th) { r_stop = r; break; }
             }
         }
         const int rmax = r_stop >= 0 ? r_stop : nr - 1;
