@@ -68,12 +68,10 @@ struct RoundState {
     uint32_t* E;        // [nq][Ecap] evaluated ids in evaluation order
     uint4* pend;        // [nq][kMaxR] cursors of the chunk in flight (committed by k_merge)
     uint32_t* cand;     // [nq][Ccap] candidate id per emitted position of the chunk (kEmpty = filtered)
-    uint8_t* crep;      // [nq][Ccap] repetition (within the chunk) of each candidate
-    uint32_t* tcnt;     // [nq][Ccap/kTile] candidates (positions passing the filter) of each scan tile
+    uint32_t* tcnt;     // [nq][Ccap/kTile] per scan tile: candidates passing the filter | repetition << 16
     uint32_t* hsave;    // [nq][kHC] k_dedupe's hash set carried to the next round
-    uint4* rseg;        // [nq][kMaxR] {lo_new, left length, hi_old, first position} per repetition
-    uint4* rinfo;       // [nq] {chunk repetitions, tau, emitted positions, 0}
-    uint2* tiles;       // scan tiles {query, tile}
+    uint4* rinfo;       // [nq] {chunk repetitions, tau, scan tiles, direct}
+    uint4* tiles;       // scan tile descriptors, two uint4 each (k_expand -> k_scan)
     uint32_t* repcnt;   // [nq][kMaxR][3] emitted, filtered, dups per repetition of the chunk
     uint32_t* pool_id;  // survivor pool of the round: ids, owning query, (sim, id) keys
     uint32_t* pool_q;

@@ -241,19 +241,28 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
             if (lane >= off) incl += o;
         }
         const uint32_t total = __shfl_sync(kFull, incl, nr - 1);
-        // segment r: positions [beg_r, beg_r + em_r): lenA from lo_new, the rest from hi_old
-        if (lane < nr) rs.rseg[q * kMaxR + lane] = make_uint4(nelo, elo - nelo, ehi, incl - em);
+        // scan tiles: each repetition's left part [nelo, elo) and right part [ehi, nehi) split into
+        // pieces of at most kTile positions, in (repetition, position) order
+        const uint32_t lenA = elo - nelo, lenB = nehi - ehi;
+        const uint32_t tA = (lenA + kTile - 1) / kTile, tB = (lenB + kTile - 1) / kTile;
+        uint32_t tin = tA + tB;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(kFull, tin, off);
+            if (lane >= off) tin += o;
+        }
+        const uint32_t ntl = __shfl_sync(kFull, tin, nr - 1);
+        if (lane < nr) rs.repcnt[(q * kMaxR + lane) * 3] = em;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) probes += __shfl_xor_sync(kFull, probes, off);
         // a single repetition with nothing evaluated yet and tau = 64 (the search's first chunk):
         // every emitted id is fresh (a repetition holds each id once), so k_scan writes the ids
         // straight to the evaluated list and the round's pool and k_dedupe skips the query
         const bool direct = nr == 1 && tau == 64 && rs.cnt[q * kCnt + 3] == 0;
-        const bool over = total > (uint32_t)(direct ? kHMax : rs.Ccap);
-        const uint32_t ntl = over ? 0u : (total + kTile - 1) / kTile;
+        const bool over = direct ? total > (uint32_t)kHMax : ntl > (uint32_t)(rs.Ccap / kTile);
         uint32_t base = 0;
         if (lane == 0) {
-            rs.rinfo[q] = make_uint4((uint32_t)nr, (uint32_t)tau, total, direct ? 1u : 0u);
+            rs.rinfo[q] = make_uint4((uint32_t)nr, (uint32_t)tau, ntl, direct ? 1u : 0u);
             rs.cnt[q * kCnt + 4] += probes;
             if (over) rs.flags[q] |= kFlagFused;
             if (direct && !over) {
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
                     rs.poff[q] = pb;
                     rs.pn[q] = total;
                     uint32_t* rc = rs.repcnt + q * kMaxR * 3;
-                    rc[0] = total; rc[1] = 0; rc[2] = 0;
+                    rc[1] = 0; rc[2] = 0;
                 }
             }
             if (ntl && !(rs.flags[q] & kFlagFused)) base = atomicAdd(&rs.ctl->ntiles[par], ntl);
@@ -275,94 +284,80 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
         }
         base = __shfl_sync(kFull, base, 0);
         const bool handed = __shfl_sync(kFull, (rs.flags[q] & kFlagFused) ? 1 : 0, 0);
-        if (!handed)
-            for (uint32_t t = lane; t < ntl; t += 32) rs.tiles[base + t] = make_uint2((uint32_t)q, t);
+        if (!handed && lane < nr) {
+            // lane r writes the descriptors of repetition r's pieces: {query, table position,
+            // chunk position, count | rep << 16 | tau << 24} {sketch word, tile index | direct, j}
+            const int j = c0 + lane;
+            const uint64_t sk = (p.use_filter && tau < 64) ? __ldg(p.qsk + q * p.M + __ldg(p.slot + j)) : 0ull;
+            uint32_t t = tin - tA - tB;
+            uint32_t g = incl - em;
+            for (int part = 0; part < 2; ++part) {
+                const uint32_t len = part ? lenB : lenA, p0 = part ? ehi : nelo;
+                for (uint32_t o = 0; o < len; o += kTile, ++t) {
+                    const uint32_t cnt = min((uint32_t)kTile, len - o);
+                    rs.tiles[2 * (int64_t)(base + t)] = make_uint4((uint32_t)q, p0 + o, g + o,
+                                                                   cnt | ((uint32_t)lane << 16) | ((uint32_t)tau << 24));
+                    rs.tiles[2 * (int64_t)(base + t) + 1] = make_uint4((uint32_t)sk, (uint32_t)(sk >> 32),
+                                                                       t | (direct ? 0x80000000u : 0u), (uint32_t)j);
+                }
+                g += len;
+            }
+        }
         __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------------------------
-// k_scan: warp per tile of 128 emitted positions of one query: load the 16-byte entries, apply
-// the sketch filter with the query's chunk tau; cand[g] = id, or kEmpty if
-// the filter rejects position g.  Fully data-parallel (no order dependence).
-struct ScanSmem {
-    uint64_t qsk[64];
-    uint4 seg[kMaxR];
-};
-
+// k_scan: warp per tile -- up to kTile consecutive table positions of one repetition of one
+// query's chunk (descriptor from k_expand): load the 16-byte entries, apply the sketch filter
+// with the chunk's tau, and compact the passing ids in order to the tile's
+// candidate slots (count | repetition << 16 in tcnt).  Fully data-parallel.
 __global__ void __launch_bounds__(256) k_scan(QueryParams p, int par) {
-    __shared__ ScanSmem sm_all[8];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    ScanSmem* c = &sm_all[wib];
+    const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
     const uint32_t ntiles = rs.ctl->ntiles[par];
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < ntiles; a += nw) {
-        const uint2 tl = rs.tiles[a];
-        const int64_t q = tl.x;
-        const uint4 info = rs.rinfo[q];
-        const int nr = (int)info.x, tau = (int)info.y;
-        const uint32_t total = info.z;
-        const int c0 = rs.c0[q];
-        if (lane < nr) c->seg[lane] = rs.rseg[q * kMaxR + lane];
-        if (p.use_filter && tau < 64)  // tau = 64 passes everything (round 0 runs before the sketches exist)
-            for (int t = lane; t < p.M; t += 32) c->qsk[t] = p.qsk[q * p.M + t];
-        __syncwarp();
-        uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
-        uint8_t* crep = rs.crep + q * (int64_t)rs.Ccap;
-        const uint32_t g0 = tl.y * kTile;
-        int rl = 0;
+        const uint4 d0 = rs.tiles[2 * a], d1 = rs.tiles[2 * a + 1];
+        const int64_t q = d0.x;
+        const uint32_t cnt = d0.w & 0xffffu, rep = (d0.w >> 16) & 0xffu, tau = d0.w >> 24;
+        const uint64_t sk = ((uint64_t)d1.y << 32) | d1.x;
+        const uint32_t t = d1.z & 0x7fffffffu;
+        const bool direct = d1.z >> 31;
+        const Entry* tj = p.tab + (int64_t)d1.w * p.n + d0.y;
         uint4 e[kTile / 32];
-        int rv[kTile / 32];
 #pragma unroll
         for (int u = 0; u < kTile / 32; ++u) {
-            const uint32_t g = g0 + u * 32 + lane;
-            rv[u] = 0;
-            if (g < total) {
-                while (rl + 1 < nr && c->seg[rl + 1].w <= g) ++rl;
-                const uint4 sg = c->seg[rl];
-                const uint32_t o = g - sg.w;
-                const uint32_t pos = (o < sg.y) ? sg.x + o : sg.z + (o - sg.y);
-                e[u] = __ldg(reinterpret_cast<const uint4*>(p.tab + (int64_t)(c0 + rl) * p.n + pos));
-                rv[u] = rl;
-            }
+            const uint32_t o = u * 32 + lane;
+            if (o < cnt) e[u] = __ldg(reinterpret_cast<const uint4*>(tj + o));
         }
-        if (info.w) {
-            // direct chunk (k_expand): every position is a fresh evaluated id
-            const uint32_t pb = rs.poff[q];
-            uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
+        if (direct) {
+            // every position is a fresh evaluated id (k_expand)
+            const uint32_t pb = rs.poff[q] + d0.z;
+            uint32_t* E = rs.E + q * (int64_t)rs.Ecap + d0.z;
 #pragma unroll
             for (int u = 0; u < kTile / 32; ++u) {
-                const uint32_t g = g0 + u * 32 + lane;
-                if (g < total) {
-                    rs.pool_id[pb + g] = e[u].x;
-                    rs.pool_q[pb + g] = (uint32_t)q;
-                    E[g] = e[u].x;
+                const uint32_t o = u * 32 + lane;
+                if (o < cnt) {
+                    rs.pool_id[pb + o] = e[u].x;
+                    rs.pool_q[pb + o] = (uint32_t)q;
+                    E[o] = e[u].x;
                 }
             }
-            __syncwarp();
             continue;
         }
-        // the passing positions of the tile, compacted in order to the front of the tile's slots
-        uint32_t cnt = 0;
+        uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap + (int64_t)t * kTile;
+        uint32_t np = 0;
 #pragma unroll
         for (int u = 0; u < kTile / 32; ++u) {
-            const uint32_t g = g0 + u * 32 + lane;
-            bool pass = g < total;
-            if (pass && p.use_filter && tau < 64) {
-                const int s_ = __ldg(p.slot + c0 + rv[u]);
-                pass = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ c->qsk[s_]) <= tau;
-            }
+            const uint32_t o = u * 32 + lane;
+            bool pass = o < cnt;
+            if (pass && p.use_filter && tau < 64) pass = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ sk) <= tau;
             const uint32_t pm = __ballot_sync(kFull, pass);
-            if (pass) {
-                const uint32_t dst = g0 + cnt + __popc(pm & lanemask_lt());
-                cand[dst] = e[u].x;
-                crep[dst] = (uint8_t)rv[u];
-            }
-            cnt += __popc(pm);
+            if (pass) cand[np + __popc(pm & lanemask_lt())] = e[u].x;
+            np += __popc(pm);
         }
-        if (lane == 0) rs.tcnt[q * (int64_t)(rs.Ccap / kTile) + tl.y] = cnt;
-        __syncwarp();
+        if (lane == 0) rs.tcnt[q * (int64_t)(rs.Ccap / kTile) + t] = np | (rep << 16);
     }
 }
 
@@ -392,7 +387,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
         const uint4 info = rs.rinfo[q];
         if (info.w) continue;  // direct chunk: k_scan wrote the evaluated ids and the pool
         const int nr = (int)info.x;
-        const uint32_t total = info.z;
+        const uint32_t ntl = info.z;
         const uint32_t nE = rs.cnt[q * kCnt + 3];
         uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
         const uint32_t* cand = rs.cand + q * (int64_t)rs.Ccap;
@@ -425,25 +420,27 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
 #pragma unroll
             for (int k = 0; k < kHC / 128; ++k) reinterpret_cast<uint4*>(c->hs)[k * 32 + lane] = tmp[k];
         }
-        if (lane < nr) { c->beg[lane] = rs.rseg[q * kMaxR + lane].w; c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
-        if (lane == 0) c->beg[nr] = total;
+        if (lane < nr) { c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
         __syncwarp();
         __syncwarp();
         uint32_t ns = 0;
         bool overflow = false;
-        const uint8_t* crep = rs.crep + q * (int64_t)rs.Ccap;
         // k_scan left the passing candidates of tile t at [t*kTile, t*kTile + tcnt[t]), in order;
         // a batch is kCPre/4 consecutive tiles
         constexpr int kTPB = kCPre * 32 / kTile;
-        const uint32_t ntl = (total + kTile - 1) / kTile;
         const uint32_t* tcnt = rs.tcnt + q * (int64_t)(rs.Ccap / kTile);
         for (uint32_t t0 = 0; t0 < ntl && !overflow; t0 += kTPB) {
             uint32_t v[kCPre], h[kCPre];
             int rr[kCPre];
             bool found[kCPre];
             uint32_t tc[kTPB];
+            int trep[kTPB];
 #pragma unroll
-            for (int b = 0; b < kTPB; ++b) tc[b] = (t0 + b < ntl) ? tcnt[t0 + b] : 0u;
+            for (int b = 0; b < kTPB; ++b) {
+                const uint32_t w = (t0 + b < ntl) ? tcnt[t0 + b] : 0u;
+                tc[b] = w & 0xffffu;
+                trep[b] = (int)(w >> 16);
+            }
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
                 const int b = u / (kTile / 32);
@@ -451,7 +448,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
                 const bool live = o < tc[b];
                 const uint32_t g = (t0 + b) * kTile + o;
                 v[u] = live ? cand[g] : kEmpty;
-                rr[u] = live ? (int)crep[g] : -1;
+                rr[u] = live ? trep[b] : -1;
             }
             // membership in the set as it stands before this batch: independent read-only probes
 #pragma unroll
@@ -524,10 +521,8 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
             }
         }
         if (lane < nr) {
-            uint32_t* rc = rs.repcnt + (q * kMaxR + lane) * 3;
-            const uint32_t em = c->beg[lane + 1] - c->beg[lane];
-            rc[0] = em;
-            rc[1] = em - c->fcnt[lane];
+            uint32_t* rc = rs.repcnt + (q * kMaxR + lane) * 3;   // rc[0] = emitted (k_expand)
+            rc[1] = rc[0] - c->fcnt[lane];
             rc[2] = c->dcnt[lane];
         }
         if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }

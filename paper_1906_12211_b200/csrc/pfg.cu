@@ -326,7 +326,7 @@ struct pfg_index {
     DBuf cur, bitmap, claims;
     // round-engine state (per query, grow-only)
     DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_repcnt, rs_pool_id, rs_pool_q, rs_pool_key,
-        rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, rs_cand, rs_crep, rs_tcnt, rs_dord0, rs_dord1, rs_hsave, rs_rseg, rs_rinfo, rs_tiles, qbnd;
+        rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, rs_cand, rs_tcnt, rs_dord0, rs_dord1, rs_hsave, rs_rseg, rs_rinfo, rs_tiles, qbnd;
     uint32_t* h_ctl = nullptr;   // pinned host mirror of the round control block
     DBuf jhist;                  // stop-depth histogram of the last search (device)
     uint32_t* h_jhist = nullptr; // its pinned host copy
@@ -1039,12 +1039,11 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_TRY(I->rs_ctl.ensure(sizeof(RoundCtl), "rs control")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_pn.ensure(N * 4, "rs")); PFG_TRY(I->rs_act0.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_act1.ensure(N * 4, "rs")); PFG_TRY(I->rs_fused.ensure(N * 4, "rs"));
-        PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs candidates")); PFG_TRY(I->rs_crep.ensure(N * ccap, "rs candidates"));
+        PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs candidates"));
         PFG_TRY(I->rs_hsave.ensure(N * kHC * 4, "rs hash sets"));
         PFG_TRY(I->rs_tcnt.ensure(N * (ccap / kTile) * 4, "rs tile counts"));
         PFG_TRY(I->rs_dord0.ensure(N * 4, "rs")); PFG_TRY(I->rs_dord1.ensure(N * 4, "rs"));
-        PFG_TRY(I->rs_rseg.ensure(N * kMaxR * 16, "rs"));
-        PFG_TRY(I->rs_rinfo.ensure(N * 16, "rs")); PFG_TRY(I->rs_tiles.ensure(N * (ccap / kTile) * 8, "rs tiles"));
+        PFG_TRY(I->rs_rinfo.ensure(N * 16, "rs")); PFG_TRY(I->rs_tiles.ensure(N * (ccap / kTile) * 32, "rs tiles"));
         if (!I->h_ctl) PFG_CUDA(cudaMallocHost(&I->h_ctl, sizeof(RoundCtl)));
     }
     PFG_TRY(I->work.ensure(8, "work counter"));
@@ -1126,10 +1125,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         r.poff = I->rs_poff.as<uint32_t>(); r.pn = I->rs_pn.as<uint32_t>();
         r.act[0] = I->rs_act0.as<uint32_t>(); r.act[1] = I->rs_act1.as<uint32_t>(); r.fused = I->rs_fused.as<uint32_t>();
         r.Ecap = ecap; r.Ccap = ccap; r.pool_cap = pool_cap;
-        r.cand = I->rs_cand.as<uint32_t>(); r.crep = I->rs_crep.as<uint8_t>(); r.hsave = I->rs_hsave.as<uint32_t>();
+        r.cand = I->rs_cand.as<uint32_t>(); r.hsave = I->rs_hsave.as<uint32_t>();
         r.tcnt = I->rs_tcnt.as<uint32_t>();
-        r.dord[0] = I->rs_dord0.as<uint32_t>(); r.dord[1] = I->rs_dord1.as<uint32_t>(); r.rseg = I->rs_rseg.as<uint4>(); r.rinfo = I->rs_rinfo.as<uint4>();
-        r.tiles = I->rs_tiles.as<uint2>();
+        r.dord[0] = I->rs_dord0.as<uint32_t>(); r.dord[1] = I->rs_dord1.as<uint32_t>(); r.rinfo = I->rs_rinfo.as<uint4>();
+        r.tiles = I->rs_tiles.as<uint4>();
         PFG_CUDA(cudaMemsetAsync(r.ctl, 0, sizeof(RoundCtl), st));
         k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p);
         PFG_CUDA(cudaGetLastError());
