@@ -254,14 +254,17 @@ template <int DP, int TPF>
 __global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
                                                       int c, int K, const uint32_t* __restrict__ sg, int nreps,
                                                       uint32_t* __restrict__ codes, int ldc,
-                                                      const uint32_t* __restrict__ qlist, int r0) {
+                                                      const uint32_t* __restrict__ qlist, int r0,
+                                                      const uint32_t* __restrict__ np_dev) {
     // rows: qlist[0..np) if given, else 0..np-1; repetitions r0 .. r0 + nreps - 1
     constexpr int H = DP / TPF, W = (DP + 31) / 32;
     static_assert(H % 32 == 0 || TPF == 1, "a lane holds whole sign words");
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int g = (int)(t % TPF);
     int64_t item = t / TPF;
+    if (np_dev) np = min(np, (int64_t)*np_dev);   // rows counted on the device (a list's length)
     const bool live = item < np * nreps;
+    if (__all_sync(kFull, !live)) return;  // the whole warp is past the end (grids sized for the maximum)
     if (!live) item = 0;  // keep the group's lanes in the shuffles; nothing is stored
     const int64_t a = item / nreps;
     const int64_t p = qlist ? (int64_t)qlist[a] : a;

@@ -118,6 +118,7 @@ struct QueryParams {
     unsigned long long* prof;   // optional per-phase cycle counters (PFG_PHASE_PROF=1), [6]
     uint32_t* jhist;            // [kJHist] queries by stop repetition at level K (eager-depth tuning)
     const uint32_t* qlist;      // fused kernel: query indices to process (NULL = 0..nq-1)
+    const uint32_t* nq_dev;     // fused kernel: if set, the number of queries in qlist (device)
     int resume;                 // fused kernel: continue each query from rs
     RoundState rs;
 };
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
         unsigned long long qv = 0;
         if (lane == 0) qv = atomicAdd(p.work, 1ull);
         const int64_t qidx = (int64_t)__shfl_sync(kFull, qv, 0);
-        if (qidx >= p.nq) break;
+        if (qidx >= (p.nq_dev ? (int64_t)*p.nq_dev : p.nq)) break;
         const int64_t qi = p.qlist ? (int64_t)p.qlist[qidx] : qidx;
         uint4* cur = p.cur + qi * p.L;   // per-query cursors (the round engine shares them)
         if (p.qzero[qi]) {

@@ -68,11 +68,12 @@ __device__ __forceinline__ void bucket_of(const QueryParams& p, int j, uint64_t 
 }
 
 __global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restrict__ out, const uint32_t* __restrict__ qlist,
-                                                 int64_t nlist, int r0, int nreps) {
-    // queries qlist[0..nlist) if given, else 0..nlist-1; repetitions r0 .. r0 + nreps - 1
+                                                 int64_t nlist, int r0, int nreps, const uint32_t* __restrict__ nlist_dev) {
+    // queries qlist[0..nlist) if given, else 0..nlist-1 (nlist from device memory if nlist_dev);
+    // repetitions r0 .. r0 + nreps - 1
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t a = t / nreps;
-    if (a >= nlist) return;
+    if (a >= (nlist_dev ? (int64_t)*nlist_dev : nlist)) return;
     const int j = r0 + (int)(t - a * nreps);
     const int64_t q = qlist ? (int64_t)qlist[a] : a;
     if (p.qzero[q]) { out[q * p.qb_ld + j] = make_uint4(0, 0, 0, 0); return; }

@@ -335,6 +335,9 @@ struct pfg_index {
     cudaStream_t aux2 = nullptr; // third stream: codes and ranges of the later eager repetitions
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_late = nullptr;
     bool late_pending = false;   // codes/ranges of repetitions [split, eager) still on aux2
+    cudaEvent_t ev_zmin = nullptr, ev_done = nullptr;  // zero-row flag copied; previous search done
+    bool done_pending = false;   // ev_done recorded by a search not yet observed complete
+    int timing_pending = 0;      // the last search recorded timing events (read lazily)
     unsigned long long* h_zmin = nullptr;  // pinned host word: first zero query row
     int64_t rs_nq = 0;
     int rs_kt = 0, rs_L = 0;
@@ -367,6 +370,8 @@ struct pfg_index {
         if (aux) cudaStreamDestroy(aux);
         if (aux2) cudaStreamDestroy(aux2);
         if (ev_late) cudaEventDestroy(ev_late);
+        if (ev_zmin) cudaEventDestroy(ev_zmin);
+        if (ev_done) cudaEventDestroy(ev_done);
         if (h_zmin) cudaFreeHost(h_zmin);
     }
 };
@@ -377,7 +382,8 @@ namespace {
 constexpr int kClaimCap = 8192;
 constexpr int kQBMax = 96;     // level-K match ranges precomputed for at most this many repetitions
 constexpr int kExtReps = 32;   // repetitions hashed in bulk for the queries the fused kernel resumes
-pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st);
+pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
+                     const uint32_t* nrows_dev = nullptr);
 #ifndef PFG_QTPF
 #define PFG_QTPF 1   // threads per function of the eager FHT-CP query hashing at d' = 128
 #endif
@@ -722,7 +728,9 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
                            I->zmin.as<unsigned long long>(), zrow, st));
     if (!zrow) {
         if (!I->h_zmin) PFG_CUDA(cudaMallocHost(&I->h_zmin, 8));
+        if (!I->ev_zmin) PFG_CUDA(cudaEventCreateWithFlags(&I->ev_zmin, cudaEventDisableTiming));
         PFG_CUDA(cudaMemcpyAsync(I->h_zmin, I->zmin.p, 8, cudaMemcpyDeviceToHost, st));
+        PFG_CUDA(cudaEventRecord(I->ev_zmin, st));
     }
     I->launches += 1;
     if (g.M > 0) {
@@ -779,7 +787,8 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
 
 // FHT-CP query codes of repetitions [r0, r0 + nreps) for rows qlist[0..nrows) (or 0..nrows-1),
 // one thread per (row, repetition), into qcodes [q][ld]
-pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st) {
+pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
+                     const uint32_t* nrows_dev) {
     const Geo& g = I->g;
     const int64_t threads = nrows * nreps;
     if (threads == 0) return PFG_OK;
@@ -787,13 +796,27 @@ pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0,
     const uint32_t* sg = I->sg.as<uint32_t>();
     uint32_t* qc = I->qcodes.as<uint32_t>();
     const float* X = I->qx.as<float>();
-    if (g.dp == 32) k_fht_qcodes_g<32, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0);
-    else if (g.dp == 64) k_fht_qcodes_g<64, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0);
+    if (g.dp == 32) k_fht_qcodes_g<32, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
+    else if (g.dp == 64) k_fht_qcodes_g<64, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
     else k_fht_qcodes_g<128, PFG_QTPF><<<(unsigned)((PFG_QTPF * threads + 127) / 128), 128, 0, st>>>(
-             X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0);
+             X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
     PFG_CUDA(cudaGetLastError());
     I->launches += 1;
     return PFG_OK;
+}
+
+// eager depth for the next search: the repetition count by which 99% of the last batch's queries
+// had stopped (deeper stops count as L), clamped to [8, 64]; codes are identical either way
+void tune_eager(pfg_index* I) {
+    if (!I->h_jhist) return;
+    uint64_t tot = 0, cum = 0;
+    for (int j = 0; j < kJHist; ++j) tot += I->h_jhist[j];
+    int e = kJHist - 1;
+    for (int j = 0; j < kJHist; ++j) {
+        cum += I->h_jhist[j];
+        if (tot && cum * 100 >= tot * 99) { e = j; break; }
+    }
+    if (tot) I->eager = std::max(8, std::min(64, e));
 }
 
 // phases of pfg_last_phases: 0 expand, 1 scan, 2 dedupe, 3 sims, 4 merge, 5 fused kernel,
@@ -976,6 +999,18 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     PFG_CUDA(cudaSetDevice(I->device));
     cudaStream_t st = (cudaStream_t)stream;
     const Geo& g = I->g;
+    if (!I->ev_done) PFG_CUDA(cudaEventCreateWithFlags(&I->ev_done, cudaEventDisableTiming));
+    if (I->done_pending) {
+        // the previous search may still run (calls return without waiting): order this one after
+        // it on the GPU, and take its stop-depth histogram if it is already complete
+        PFG_CUDA(cudaStreamWaitEvent(st, I->ev_done, 0));
+        if (cudaEventQuery(I->ev_done) == cudaSuccess) {
+            I->done_pending = false;
+            tune_eager(I);
+        } else {
+            cudaGetLastError();
+        }
+    }
     std::shared_ptr<DBuf> thr, taub;
     PFG_TRY(get_thr(I, recall, s, thr, nullptr));
     PFG_TRY(get_tau(I, s.eps, taub, nullptr));
@@ -1020,10 +1055,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // round engine: `rounds` bulk rounds (search option, default 5), then the fused kernel resumes
     // every query still running (stragglers keep their hash set in shared memory across chunks
     // there, instead of paying a round's fixed latency per chunk).  The rounds are enqueued
-    // without host synchronisation; the host checks the active count every sync_every rounds
-    // only to stop early when every query has finished.
+    // without host synchronisation.
     const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : (s.rounds > 0 ? s.rounds : 5);
-    const int sync_every = 8;
     const int ecap = 2048;  // evaluated-list stride: kHMax committed + one batch of slack
     const int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
     const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
@@ -1089,11 +1122,11 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         p.qbnd = I->qbnd.as<uint4>();
         const int b0 = std::min(p.qb_n, I->late_pending ? I->qc_split : p.qb_n);
         const int64_t thr_n = nq * (int64_t)b0;
-        if (b0 > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, b0);
+        if (b0 > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, b0, nullptr);
         if (b0 < p.qb_n) {
             const int64_t thr_l = nq * (int64_t)(p.qb_n - b0);
             k_qbounds<<<(unsigned)((thr_l + 255) / 256), 256, 0, I->aux2>>>(p, I->qbnd.as<uint4>(), nullptr, nq, b0,
-                                                                          p.qb_n - b0);
+                                                                          p.qb_n - b0, nullptr);
             I->launches += 1;
         }
         PFG_CUDA(cudaGetLastError());
@@ -1148,7 +1181,6 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const unsigned tb_s = (unsigned)(I->num_sms * 8);
         const unsigned sb = (unsigned)(I->num_sms * 2);
         int round = 0;
-        uint32_t nact = (uint32_t)nq;
         const bool tm = s.timing >= 2;
         while (round < max_rounds) {
             const int par = round & 1;
@@ -1177,32 +1209,25 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             PFG_CUDA(cudaGetLastError());
             I->launches += 5;
             ++round;
-            if (round % sync_every == 0 || round >= max_rounds) {
-                PFG_CUDA(cudaMemcpyAsync(I->h_ctl, r.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-                PFG_CUDA(cudaStreamSynchronize(st));
-                nact = I->h_ctl[round & 1];
-                if (nact == 0) break;
-            }
         }
-        if (nact > 0) {
-            k_handoff<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, round & 1);
-            PFG_CUDA(cudaGetLastError());
-            I->launches += 1;
-        }
-        PFG_CUDA(cudaMemcpyAsync(I->h_ctl, r.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-        PFG_CUDA(cudaStreamSynchronize(st));
-        fused_n = I->h_ctl[4];
+        // no host synchronisation: the queries still running join the fused list on the device,
+        // and the kernels below take their counts from device memory
+        k_handoff<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, round & 1);
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 1;
         p.qlist = r.fused;
+        p.nq_dev = &r.ctl->nfused;
         p.resume = 1;
-        p.nq = fused_n;
         I->last_rounds = round;
         // the queries the fused kernel resumes get codes and match ranges for kExtReps more
         // repetitions in bulk (they would otherwise hash and search them one warp at a time)
-        if (fused_n > 0 && lazy && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+        if (lazy && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
             const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
-            PFG_TRY(fht_codes(I, fused_n, r.fused, r0, nr, I->qc_ld, st));
-            const int64_t thr_n = fused_n * (int64_t)nr;
-            k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.fused, fused_n, r0, nr);
+            PFG_TRY(late_join(I, st));
+            PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, st, &r.ctl->nfused));
+            const int64_t thr_n = nq * (int64_t)nr;
+            k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.fused, nq, r0, nr,
+                                                                       &r.ctl->nfused);
             PFG_CUDA(cudaGetLastError());
             I->launches += 1;
             p.qc_n = p.qb_n = I->qc_ld;
@@ -1231,7 +1256,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     if (fused_n > 0) {
         PFG_TRY(phase_mark(I, s.timing >= 2, kPhFused, st));
         PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
-        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((fused_n + 3) / 4, max_blocks));
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((fused_n + 3) / 4, max_blocks));  // rounds: nq bound
         switch (epl) {
             case 1: PFG_TRY(launch_query_t<1>(p, (int)blocks, smem, st)); break;
             case 2: PFG_TRY(launch_query_t<2>(p, (int)blocks, smem, st)); break;
@@ -1245,14 +1270,27 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     I->last_fused = fused_n;
     PFG_TRY(phase_mark(I, s.timing >= 2, kPhEnd, st));
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[2], st));
+    I->timing_pending = s.timing;
     if (!ids_dev) PFG_CUDA(cudaMemcpyAsync(out_ids, d_ids, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
     if (!sims_dev) PFG_CUDA(cudaMemcpyAsync(out_sims, d_sims, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, st));
     if (stats && !stats_dev)
         PFG_CUDA(cudaMemcpyAsync(stats, d_stats, (size_t)nq * sizeof(pfg_query_stats), cudaMemcpyDeviceToHost, st));
     if (s.trace_cap > 0 && !trace_dev)
         PFG_CUDA(cudaMemcpyAsync(s.trace_ids, d_trace, (size_t)nq * s.trace_cap * 4, cudaMemcpyDeviceToHost, st));
-    PFG_CUDA(cudaStreamSynchronize(st));
+    // the stop-depth histogram for the next search's eager depth, and the end-of-search event that
+    // orders the next search's use of the scratch buffers (on any stream)
+    PFG_CUDA(cudaMemcpyAsync(I->h_jhist, I->jhist.p, kJHist * 4, cudaMemcpyDeviceToHost, st));
+    PFG_CUDA(cudaEventRecord(I->ev_done, st));
+    I->done_pending = true;
+    // with device outputs the call returns without waiting for the GPU; host outputs (or the
+    // developer phase print) need the results here
+    const bool host_out = !ids_dev || !sims_dev || (stats && !stats_dev) || (s.trace_cap > 0 && !trace_dev);
+    if (host_out || phase_prof) PFG_CUDA(cudaStreamSynchronize(st));
     if (phase_prof) {
+        if (rounds) {
+            PFG_CUDA(cudaMemcpy(I->h_ctl, I->rs_ctl.p, sizeof(RoundCtl), cudaMemcpyDeviceToHost));
+            fused_n = I->h_ctl[4];
+        }
         fprintf(stderr, "[pfg phase] engine %d: rounds %d, queries finished by the fused kernel %lld of %lld\n", s.engine,
                 I->last_rounds, (long long)fused_n, (long long)nq);
         unsigned long long h[16] = {0};
@@ -1268,38 +1306,38 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 h[3] / 1e6, 100 * h[3] / tot, h[5] / 1e6, h[4] / 1e6, 100 * h[4] / tot);
     }
     I->last_launches = I->launches;
-    {
-        // eager depth for the next search: the repetition count by which 99% of this batch's queries
-        // had stopped (deeper stops count as L), clamped to [8, 64]; codes are identical either way
-        PFG_CUDA(cudaMemcpy(I->h_jhist, I->jhist.p, kJHist * 4, cudaMemcpyDeviceToHost));
-        uint64_t tot = 0, cum = 0;
-        for (int j = 0; j < kJHist; ++j) tot += I->h_jhist[j];
-        int e = kJHist - 1;
-        for (int j = 0; j < kJHist; ++j) {
-            cum += I->h_jhist[j];
-            if (tot && cum * 100 >= tot * 99) { e = j; break; }
-        }
-        if (tot) I->eager = std::max(8, std::min(64, e));
-    }
-    if (s.timing) {
-        if (s.timing >= 2) PFG_TRY(phase_collect(I));
-        PFG_CUDA(cudaEventElapsedTime(&I->last_ms[0], I->ev[0], I->ev[1]));
-        PFG_CUDA(cudaEventElapsedTime(&I->last_ms[1], I->ev[1], I->ev[2]));
-        PFG_CUDA(cudaEventElapsedTime(&I->last_ms[2], I->ev[0], I->ev[2]));
-    }
+    PFG_CUDA(cudaEventSynchronize(I->ev_zmin));  // recorded right after the normalisation
     if (*I->h_zmin != ~0ull)
         return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(*I->h_zmin) + " is a zero vector");
     return PFG_OK;
 }
 
+// the timing events of the last search, read once it has completed (calls return early)
+static pfg_status collect_timing(pfg_index* I) {
+    if (!I->timing_pending) return PFG_OK;
+    PFG_CUDA(cudaEventSynchronize(I->ev[2]));
+    PFG_CUDA(cudaEventElapsedTime(&I->last_ms[0], I->ev[0], I->ev[1]));
+    PFG_CUDA(cudaEventElapsedTime(&I->last_ms[1], I->ev[1], I->ev[2]));
+    PFG_CUDA(cudaEventElapsedTime(&I->last_ms[2], I->ev[0], I->ev[2]));
+    if (I->timing_pending >= 2) PFG_TRY(phase_collect(I));
+    I->timing_pending = 0;
+    return PFG_OK;
+}
+
 pfg_status pfg_last_phases(const pfg_index* I, float* ms, int32_t n) {
     if (!I || !ms || n < 0) return fail(PFG_E_ARG, "NULL index or output");
+    pfg_index* W = const_cast<pfg_index*>(I);
+    std::lock_guard<std::mutex> lock(W->mu);
+    PFG_TRY(collect_timing(W));
     for (int i = 0; i < n && i < 8; ++i) ms[i] = I->last_phase_ms[i];
     return PFG_OK;
 }
 
 pfg_status pfg_last_timing(const pfg_index* I, float* ms3, int32_t* launches) {
     if (!I) return fail(PFG_E_ARG, "NULL index");
+    pfg_index* W = const_cast<pfg_index*>(I);
+    std::lock_guard<std::mutex> lock(W->mu);
+    PFG_TRY(collect_timing(W));
     if (ms3) for (int i = 0; i < 3; ++i) ms3[i] = I->last_ms[i];
     if (launches) *launches = I->last_launches;
     return PFG_OK;
