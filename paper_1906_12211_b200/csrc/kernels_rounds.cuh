@@ -563,7 +563,10 @@ __device__ __forceinline__ void pool_sims_step(const float4* __restrict__ x4, co
     }
 }
 
-__global__ void __launch_bounds__(256, 2) k_sims(QueryParams p, int par) {
+#ifndef PFG_SIMS_MINB
+#define PFG_SIMS_MINB 2
+#endif
+__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(QueryParams p, int par) {
     const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
     const uint32_t top = min(rs.ctl->pool_top[par], rs.pool_cap);

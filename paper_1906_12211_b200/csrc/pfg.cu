@@ -1179,7 +1179,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const unsigned qb_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * std::max(1, docc)));
         const unsigned qb_m = qb_e;
         const unsigned tb_s = (unsigned)(I->num_sms * 8);
-        const unsigned sb = (unsigned)(I->num_sms * 2);
+        const unsigned sb = (unsigned)(I->num_sms * PFG_SIMS_MINB);
         int round = 0;
         const bool tm = s.timing >= 2;
         while (round < max_rounds) {
