@@ -22,7 +22,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 HP, FHTCP = 0, 1
-INDEPENDENT, POOL = 0, 1
+INDEPENDENT, POOL, TENSOR = 0, 1, 2
 
 
 def build_lib(force: bool = False) -> str:
@@ -190,13 +190,18 @@ class _SOpts(C.Structure):
 
 
 class OracleIndex:
-    """Oracle LSH forest.  family: HP | FHTCP; strategy: INDEPENDENT | POOL; explicit L, K, M."""
+    """Oracle LSH forest.  family: HP | FHTCP; strategy: INDEPENDENT | POOL | TENSOR; explicit L, K, M."""
 
     def __init__(self, data, family: int, L: int, seed: int = 1, K: int = 24, M: int = 32,
                  strategy: int = INDEPENDENT, pool_bits: int = 3072, lazy: bool = False,
                  cp_draws: int = 1000):
         data = _f32(data)
         self.n, self.d = data.shape
+        if strategy == TENSOR:
+            s = int(round(L ** 0.5))
+            ell = 1 if family == HP else 1 + int(np.ceil(np.log2(max(2, 1 << int(np.ceil(np.log2(self.d)))))))
+            if s * s != L or (s & (s - 1)) or (K % ell) or ((K // ell) % 2):
+                raise ValueError("tensor: L must be an even power of two and K an even number of whole functions")
         err = C.c_int64(-1)
         self._h = lib().or_build(_p(data), self.n, self.d, family, strategy, L, K, M, pool_bits,
                                  seed, int(lazy), cp_draws, C.byref(err))

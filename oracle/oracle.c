@@ -137,11 +137,11 @@ uint32_t or_fhtcp_code(const float* x, int d, int dp, const float* sg) {
  * Index (§4.2): L arrays of (hash code, pos) sorted by code.
  * -------------------------------------------------------------------------- */
 enum { OR_HP = 0, OR_FHTCP = 1 };
-enum { OR_INDEPENDENT = 0, OR_POOL = 1 };
+enum { OR_INDEPENDENT = 0, OR_POOL = 1, OR_TENSOR = 2 };
 
 typedef struct {
     int64_t n;
-    int d, dp, ell, family, strategy, K, L, M, c, m;
+    int d, dp, ell, family, strategy, K, L, M, c, m, S;  /* S = sqrt(L) for the tensor strategy */
     uint64_t seed;
     float* x;          /* normalised data [n][d] */
     uint64_t* sk;      /* sketches [n][M] */
@@ -167,11 +167,12 @@ static uint32_t or_func(const or_index* X, int64_t f, const float* x) {
 
 /* h_{<=i,j} is the concatenation of the rep's functions, earlier functions
  * more significant (a bit string); the top K bits are kept (R-7).  Independent: rep j uses
- * functions j*c..j*c+c-1.  Pool: the functions sel[j][0..c). */
+ * functions j*c..j*c+c-1.  Pool and tensor (PAPER.md:244-249,
+ * 849-858): the functions sel[j][0..c). */
 uint32_t or_rep_code(const or_index* X, int j, const float* x) {
     uint64_t full = 0;
     for (int t = 0; t < X->c; ++t) {
-        int64_t f = (X->strategy == OR_POOL) ? X->sel[j * X->c + t] : (int64_t)j * X->c + t;
+        int64_t f = (X->strategy != OR_INDEPENDENT) ? X->sel[j * X->c + t] : (int64_t)j * X->c + t;
         full = (full << X->ell) | or_func(X, f, x);
     }
     return (uint32_t)(full >> (X->c * X->ell - X->K));
@@ -291,8 +292,14 @@ or_index* or_build(const float* raw, int64_t n, int d, int family, int strategy,
     *err_row = or_normalize(raw, n, d, X->x);
     if (*err_row >= 0) { free(X->x); free(X); return NULL; }
     /* functions (R-3 streams) */
-    int64_t F = (strategy == OR_POOL) ? (int64_t)(pool_bits / X->ell) : (int64_t)L * X->c;
+    /* tensor: L an even power of two, S = sqrt(L), two collections of S
+     * tuples of c/2 functions; F = S * c functions (R-24) */
+    int S = 1;
+    while (S * S < L) ++S;
+    int64_t F = (strategy == OR_POOL) ? (int64_t)(pool_bits / X->ell)
+              : (strategy == OR_TENSOR) ? (int64_t)S * X->c : (int64_t)L * X->c;
     X->m = (strategy == OR_POOL) ? (int)F : 0;
+    X->S = (strategy == OR_TENSOR) ? S : 0;
     if (family == OR_HP) {
         uint64_t kh = or_stream_key(seed, OR_TAG_HP);
         X->hp = (float*)malloc(sizeof(float) * F * d);
@@ -317,6 +324,19 @@ or_index* or_build(const float* raw, int64_t n, int d, int family, int strategy,
             }
         }
         free(perm);
+    }
+    if (strategy == OR_TENSOR) {
+        /* trie (j1, j2), j = j1*S + j2, interleaves tuple j1 of the first collection and tuple j2
+         * of the second: position t = 2s + a holds function s of collection a's tuple
+         * ("taken by interleaving"); function (a, tuple, s) is
+         * f = (a*S + tuple)*(c/2) + s */
+        int h = X->c / 2;
+        X->sel = (int32_t*)malloc(sizeof(int32_t) * L * X->c);
+        for (int j = 0; j < L; ++j)
+            for (int t = 0; t < X->c; ++t) {
+                int a = t % 2, s = t / 2, tuple = a ? j % S : j / S;
+                X->sel[j * X->c + t] = (a * S + tuple) * h + s;
+            }
     }
     /* sketches: "M 64-bit sketches s_1(p),...,s_M(p) obtained via HP LSH";
      * slot for rep j ("pseudorandom transformation of j", R-20) */
@@ -415,6 +435,13 @@ double or_P(const or_index* X, int i, float ip) {
  *   mu = j P_i, E[X1X2] <= P_i prod_f (r + (1-r) p_f), r = c_i/(m - c_i),
  *   F = 1 - mu^2 / (mu + j(j-1) E[X1X2]);  no stop if m < 2 c_i. */
 int or_should_stop(const or_index* X, int i, int j, float ip, double delta, int rule) {
+    if (X->strategy == OR_TENSOR) {
+        /* Alg. 2: after the m = j first tuples of both collections at depth i
+         * (i/2 bits from each), fail bound 2(1 - p^{i/2})^m (union over the two collections) */
+        double Ph = or_P(X, i / 2, ip);
+        (void)rule;
+        return log(2.0) + (double)j * log1p(-Ph) <= log(delta);
+    }
     double P = or_P(X, i, ip);
     if (X->strategy == OR_POOL) {
         int ci = (i + X->ell - 1) / X->ell;
@@ -516,8 +543,16 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
     uint8_t* init = (uint8_t*)calloc(L, 1);
     int R = o->rep_chunk < 1 ? 1 : o->rep_chunk;
     int done = 0;
-    for (int i = K; i >= 0 && !done; --i) {
-        int Lr = (i == 0) ? 1 : L;
+    /* tensor (Alg. 2): depths i = K, K - 2 ell, ..., 0 (i/2 bits from each
+     * collection); at each depth the shells m = 1..S add the tries (j, m) and (m, j), j <= m, in
+     * the order (1,m), (m,1), (2,m), (m,2), ..., (m,m); tau is frozen per shell (R-17) and the stop
+     * check follows each shell */
+    const int tensor = X->strategy == OR_TENSOR;
+    const int istep = tensor ? 2 * X->ell : 1;
+    int list[256];
+    for (int i = K; i >= 0 && !done; i -= (i == 0 ? 1 : istep)) {
+        if (i < 0) break;
+        int Lr = (i == 0) ? 1 : (tensor ? X->S : L);
         for (int c0 = 0, c1 = 0; c0 < Lr && !done; c0 = c1) {
             int tau = 64;
             if (nt == k_eff && i > 0) {
@@ -526,9 +561,19 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
                 if (ip < -1.0f) ip = -1.0f;
                 tau = or_tau(ip, o->eps);
             }
-            int Rc = (i == K && c0 == 0 && !o->uniform_chunks) ? 1 : R;
-            c1 = c0 + Rc < Lr ? c0 + Rc : Lr;
-            for (int j = c0; j < c1 && !done; ++j) {
+            int nl;
+            if (i > 0 && tensor) {
+                nl = 2 * c0 + 1;
+                for (int t = 0; t < nl; ++t) list[t] = (t % 2 == 0) ? (t / 2) * X->S + c0 : c0 * X->S + (t - 1) / 2;
+                c1 = c0 + 1;
+            } else {
+                int Rc = (i == K && c0 == 0 && !o->uniform_chunks) ? 1 : R;
+                c1 = c0 + Rc < Lr ? c0 + Rc : Lr;
+                nl = c1 - c0;
+                for (int t = 0; t < nl; ++t) list[t] = c0 + t;
+            }
+            for (int tl = 0; tl < nl && !done; ++tl) {
+                const int j = list[tl];
                 or_need_rep(X, j);
                 const uint32_t* cj = X->codes[j];
                 const uint32_t* ij = X->ids[j];
@@ -565,16 +610,16 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
                             if (nt < k_eff) ++nt;
                         }
                     }
-                /* Alg. 1 line 8 */
+                /* Alg. 1 line 8 (Alg. 2: after each shell, j = m) */
                 int stop = 0;
                 if (i == 0) stop = 1;
-                else if (nt == k_eff && (!o->per_round || j == L - 1)) {
+                else if (tensor ? (tl == nl - 1 && nt == k_eff) : (nt == k_eff && (!o->per_round || j == L - 1))) {
                     float ip = ts[k_eff - 1];
                     if (ip > 1.0f) ip = 1.0f;
                     if (ip < -1.0f) ip = -1.0f;
-                    stop = or_should_stop(X, i, j + 1, ip, delta, o->stop_rule);
+                    stop = or_should_stop(X, i, tensor ? c0 + 1 : j + 1, ip, delta, o->stop_rule);
                 }
-                if (stop) { trace[0] = i; trace[1] = j + 1; done = 1; }
+                if (stop) { trace[0] = i; trace[1] = tensor ? c0 + 1 : j + 1; done = 1; }
             }
         }
     }

@@ -182,7 +182,7 @@ def tiny_hp():
 
 def test_stop_rule_golden(tiny_hp):
     for row in _rows(golden("stop_rule.txt")):
-        if row[0] == "pool":
+        if row[0] in ("pool", "tensor"):
             continue
         ip, i, delta, rule, js = float(row[0]), int(row[1]), float(row[2]), int(row[3]), int(row[4])
         assert not tiny_hp.should_stop(i, js - 1, ip, delta, rule), row
@@ -197,6 +197,58 @@ def test_pool_stop_rule_golden():
     assert X.m == m
     assert not X.should_stop(i, js - 1, ip, delta)
     assert X.should_stop(i, js, ip, delta)
+
+
+def test_tensor_stop_rule_golden():
+    data = synth.gaussian(300, 8, 2)
+    X = O.OracleIndex(data, O.HP, L=256, seed=1, M=1, strategy=O.TENSOR, lazy=True)
+    for row in [r for r in _rows(golden("stop_rule.txt")) if r[0] == "tensor"]:
+        ip, i, delta, ms = float(row[1]), int(row[2]), float(row[3]), int(row[4])
+        assert not X.should_stop(i, ms - 1, ip, delta), row
+        assert X.should_stop(i, ms, ip, delta), row
+
+
+def test_tensor_interleave():
+    # P12 / PAPER.md:247-248, 855-857: trie (j1, j2) hashes with the K/2 functions of tuple j1 of
+    # the first collection and tuple j2 of the second, interleaved (first collection first).  The
+    # functions are regenerated here from the shared seeded stream (R-3), the bits computed one by
+    # one, and the interleaved codes compared with the index's codes for every trie.
+    d, L, K = 12, 16, 4
+    S, h = 4, K // 2
+    data = synth.gaussian(50, d, 9)
+    q = synth.gaussian(20, d, 10)
+    X = O.OracleIndex(data, O.HP, L=L, K=K, seed=7, M=1, strategy=O.TENSOR)
+    codes, _ = X.hash(q)
+    key = O.stream_key(7, 1)                      # HP functions: stream tag 1 (R-3)
+    qn = O.normalize(q)
+
+    def fvec(f):
+        return np.array([O.gauss_d(key, f * d + t) for t in range(d)], np.float32)
+
+    for j1 in range(S):
+        for j2 in range(S):
+            funcs = []
+            for s in range(h):
+                funcs += [(0 * S + j1) * h + s, (1 * S + j2) * h + s]
+            for r in range(len(q)):
+                code = 0
+                for f in funcs:
+                    code = (code << 1) | O.hp_bit(fvec(f), qn[r])
+                assert code == codes[r, j1 * S + j2], (j1, j2, r)
+
+
+def test_tensor_recall_over_seeds():
+    # Alg. 2's guarantee (filter off): config 1 with L = 16 tries from 2 x 4
+    # tuples, index seeds 1..30, mean recall >= target
+    data, q = synth.config_data(1, n=3000, nq=40)
+    bi, _ = O.bruteforce(O.normalize(data), O.normalize(q), 10)
+    rec = []
+    for seed in range(1, 31):
+        X = O.OracleIndex(data, O.HP, L=16, seed=seed, strategy=O.TENSOR)
+        ids, _, tr = X.search(q, 10, 0.9, threads=8, use_filter=False)
+        rec.append(np.mean([len(set(a) & set(b)) / 10 for a, b in zip(ids.tolist(), bi.tolist())]))
+        assert np.all(tr[:, 1] <= 4)          # at most S = 4 shells per depth
+    assert np.mean(rec) >= 0.9, np.mean(rec)
 
 
 def test_failure_bound_monotone(tiny_hp):
