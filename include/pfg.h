@@ -55,7 +55,12 @@ typedef enum {
 /* hash-function evaluation strategies (§3.2, App. B 841-917) */
 typedef enum {
     PFG_INDEPENDENT = 0,  /* every repetition has its own functions (Alg. 1) */
-    PFG_POOL = 1          /* repetitions sample functions without replacement from one pool (Alg. 3) */
+    PFG_POOL = 1,         /* repetitions sample functions without replacement from one pool (Alg. 3) */
+    PFG_TENSOR = 2        /* L = S^2 tries from two collections of S tuples of K/2 functions, trie
+                             (j1, j2) interleaving tuple j1 and tuple j2; depths in steps of two
+                             functions, shells of tries per stop check (Alg. 2, PAPER.md:244-249,
+                             849-882).  L: an even power of two <= 256; K: an even number of whole
+                             functions; searched by the fused kernel */
 } pfg_strategy;
 
 /* Build options.  Zero-initialise and set struct_size = sizeof(pfg_build_opts); a zero field

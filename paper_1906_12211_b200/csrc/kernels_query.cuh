@@ -93,7 +93,9 @@ struct QueryParams {
     int kt;          // T capacity (>= k_eff, multiple of 32)
     int qc_n, qc_ld; // query codes precomputed for repetitions [0, qc_n), row stride qc_ld
     int qb_n, qb_ld; // level-K match ranges precomputed for repetitions [0, qb_n) (k_qbounds)
-    int uniform;     // 1: chunks of R from the start; 0: single-repetition chunks until k are known
+    int uniform;     // 1: chunks of R from the start; 0: the first chunk is repetition 0 alone
+    int tensor_s;    // tensor strategy: S = sqrt(L) tuples per collection (0 = not tensor)
+    int lstep;       // bits between searched depths: 1, or 2 ell for the tensor strategy
     int smem_warp;   // bytes of shared memory per warp
     const float* __restrict__ x;
     const Entry* __restrict__ tab;
@@ -247,7 +249,17 @@ __device__ __forceinline__ void merge_range(const QueryParams& p, const WarpSmem
 // R repetitions.  It ends early at the first repetition j whose stop threshold the current
 // k-th similarity already meets: the k-th similarity only grows, so the search stops at or before
 // j and later repetitions of the chunk are never reached (exact).  All lanes get the same value.
+// the table of repetition r of chunk c0: the repetitions c0 .. c0 + nr - 1, or for the tensor
+// strategy (Alg. 2) the tries of shell c0 (0-based): (j, c0) and (c0, j) for
+// j < c0 in the order (0,c0), (c0,0), (1,c0), (c0,1), ..., then (c0,c0); trie (j1, j2) = j1*S + j2
+__device__ __forceinline__ int trie_of(const QueryParams& p, int c0, int r) {
+    if (!p.tensor_s) return c0 + r;
+    return (r & 1) ? c0 * p.tensor_s + (r >> 1) : (r >> 1) * p.tensor_s + c0;
+}
+__device__ __forceinline__ int chunk_count(const QueryParams& p) { return p.tensor_s ? p.tensor_s : p.L; }
+
 __device__ __forceinline__ int chunk_reps(const QueryParams& p, int i, int c0, int tn, const uint64_t* T, int lane) {
+    if (p.tensor_s) return 2 * c0 + 1;  // a shell; the stop check follows the whole shell
     int nr = min((i == p.K && c0 == 0 && !p.uniform) ? 1 : p.R, p.L - c0);
     if (tn == p.k_eff) {
         float ip = key_sim(T[p.k_eff - 1]);
@@ -358,9 +370,11 @@ __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, Q
         e = e2;
         if (next_check >= complete || next_check >= nr) break;
         const int j1 = c0 + next_check + 1;
-        if (st.tn == p.k_eff && (!p.per_round || j1 == p.L)) {
+        const bool check = p.tensor_s ? (next_check == nr - 1) : (!p.per_round || j1 == p.L);
+        if (st.tn == p.k_eff && check) {
             const float ip = kth_sim_clamped(p, st);
-            if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + (j1 - 1))) { r_stop = next_check; stop = true; break; }
+            const int col = p.tensor_s ? c0 : j1 - 1;   // tensor: thresholds per (depth, shell)
+            if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + col)) { r_stop = next_check; stop = true; break; }
         }
         ++next_check;
     }
@@ -480,11 +494,11 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
             __syncwarp();
         }
 
-        for (int i = i_start; i >= 1 && !stopped; --i) {
-            for (int c0 = (i == i_start ? c_start : 0), c1 = 0; c0 < p.L && !stopped; c0 = c1) {
-                // R-17: a chunk is one repetition while fewer than k points are known, else R
+        for (int i = i_start; i >= 1 && !stopped; i -= p.lstep) {
+            for (int c0 = (i == i_start ? c_start : 0), c1 = 0; c0 < chunk_count(p) && !stopped; c0 = c1) {
+                // R-17 chunk (or a tensor shell)
                 const int nr = chunk_reps(p, i, c0, st.tn, st.T, lane);
-                c1 = c0 + nr;
+                c1 = p.tensor_s ? c0 + 1 : c0 + nr;
                 int tau = 64;
                 if (p.use_filter && st.tn == p.k_eff) {
                     const float ip = kth_sim_clamped(p, st);
@@ -496,7 +510,8 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 // repetitions < qc_n, otherwise hashed here (FHT-CP, warp-cooperative)
                 const long long th0 = p.prof ? clock64() : 0;
                 if (i == p.K) {
-                    if (lane < nr && c0 + lane < p.qc_n) w.f->qc[lane] = __ldg(p.qcodes + qi * p.qc_ld + c0 + lane);
+                    if (lane < nr && trie_of(p, c0, lane) < p.qc_n)
+                        w.f->qc[lane] = __ldg(p.qcodes + qi * p.qc_ld + trie_of(p, c0, lane));
                     const int r0 = max(0, p.qc_n - c0);
                     if (r0 < nr) {
                         __syncwarp();
@@ -514,7 +529,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 for (int task = lane; task < 2 * nr; task += 32) {
                     const bool left = task < nr;
                     const int r = left ? task : task - nr;
-                    const int j = c0 + r;
+                    const int j = trie_of(p, c0, r);
                     if (i == p.K && j < p.qb_n) {
                         const uint4 b = __ldg(p.qbnd + qi * p.qb_ld + j);
                         w.f->bnd[task] = left ? b.x : b.y;
@@ -550,7 +565,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 __syncwarp();
                 uint32_t em = 0;
                 if (lane < nr) {
-                    const int j = c0 + lane;
+                    const int j = trie_of(p, c0, lane);
                     uint32_t elo, ehi, nelo, nehi;
                     if (i == p.K) {
                         // closed form of the segment loop from [a, a): ehi' = a + B*ceil((b - a)/B)
@@ -602,12 +617,12 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                             const uint32_t o = g - w.f->beg[r];
                             const uint32_t lenA = w.f->lo_old[r] - w.f->lo_new[r];
                             const uint32_t pos = (o < lenA) ? w.f->lo_new[r] + o : w.f->hi_old[r] + (o - lenA);
-                            const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.tab + (int64_t)(c0 + r) * p.n + pos));
+                            const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.tab + (int64_t)trie_of(p, c0, r) * p.n + pos));
                             idv[u] = e.x;
                             rv[u] = r;
                             pass[u] = true;
                             if (p.use_filter) {
-                                const int s = __ldg(p.slot + c0 + r);
+                                const int s = __ldg(p.slot + trie_of(p, c0, r));
                                 const uint64_t sw = ((uint64_t)e.w << 32) | e.z;
                                 pass[u] = __popcll(sw ^ w.qsk[s]) <= tau;
                             }
@@ -650,7 +665,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                         int complete = nr;
                         if (done_pos < total) { complete = 0; while (complete < nr && w.f->beg[complete + 1] <= done_pos) ++complete; }
                         if (drain<RQ>(p, w, st, nbuf, next_check, complete, nr, c0, i, qi, r_stop, lane)) {
-                            stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
+                            stopped = true; i_stop = i; j_stop = p.tensor_s ? c0 + 1 : c0 + r_stop + 1;
                         }
                         if (p.prof && lane == 0) { const long long t = clock64(); atomicAdd(p.prof + 3, (unsigned long long)(t - tp0)); tp0 = t; }
                     }
@@ -658,7 +673,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 if (total == 0) {
                     // empty chunk: every repetition is complete, check them in order
                     if (drain<RQ>(p, w, st, nbuf, next_check, nr, nr, c0, i, qi, r_stop, lane)) {
-                        stopped = true; i_stop = i; j_stop = c0 + r_stop + 1;
+                        stopped = true; i_stop = i; j_stop = p.tensor_s ? c0 + 1 : c0 + r_stop + 1;
                     }
                 }
                 const int rmax = stopped ? r_stop : nr - 1;

@@ -111,7 +111,7 @@ int ilog2(int v) {
 struct Geo {
     int64_t n = 0;
     int d = 0, dpad = 0, family = 0, strategy = 0, K = 24, M = 32, ell = 1, c = 24, dp = 1, W = 1, m = 0;
-    int pool_bits = 3072, cp_draws = 1000, max_reps = 4096, L = 0;
+    int pool_bits = 3072, cp_draws = 1000, max_reps = 4096, L = 0, S = 0;  // S = sqrt(L) (tensor)
     int64_t id_offset = 0;
     uint64_t fixed_bytes = 0, per_rep_bytes = 0, index_bytes = 0;
 };
@@ -137,7 +137,8 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
         return fail(PFG_E_ARG, "n * d too large for one index (shard the data: n * d / 4 must be < 2^32)");
     g.family = family;
     g.strategy = z.strategy;
-    if (g.strategy != PFG_INDEPENDENT && g.strategy != PFG_POOL) return fail(PFG_E_ARG, "unknown strategy");
+    if (g.strategy != PFG_INDEPENDENT && g.strategy != PFG_POOL && g.strategy != PFG_TENSOR)
+        return fail(PFG_E_ARG, "unknown strategy");
     g.K = z.prefix_bits ? z.prefix_bits : 24;
     if (g.K < 13 || g.K > 32) return fail(PFG_E_ARG, "prefix_bits must be in [13, 32]");
     g.M = z.sketch_words == 0 ? 32 : (z.sketch_words < 0 ? 0 : z.sketch_words);
@@ -151,6 +152,8 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
         g.ell = 1 + ilog2(g.dp);
     }
     g.c = (g.K + g.ell - 1) / g.ell;
+    if (g.strategy == PFG_TENSOR && (g.c % 2 != 0 || g.c * g.ell != g.K))
+        return fail(PFG_E_ARG, "tensor strategy: prefix_bits must be an even number of whole functions (PAPER.md:245)");
     g.pool_bits = z.pool_bits ? z.pool_bits : 3072;
     g.m = g.strategy == PFG_POOL ? g.pool_bits / g.ell : 0;
     if (g.strategy == PFG_POOL && g.m < g.c) return fail(PFG_E_ARG, "pool smaller than one repetition's functions");
@@ -168,6 +171,9 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     g.per_rep_bytes = 16ull * N + 4ull * 8193 + 1;  // 16-byte entries: key + inline sketch word (R-21)
     if (g.strategy == PFG_INDEPENDENT) g.per_rep_bytes += (uint64_t)g.c * (family == PFG_SIMHASH ? fn_hp : fn_fht);
     else g.per_rep_bytes += 4ull * g.c;
+    // tensor: the S * c functions (S = sqrt(L)) are charged per repetition as c functions, an upper
+    // bound for S <= L
+    if (g.strategy == PFG_TENSOR) g.per_rep_bytes += (uint64_t)g.c * (family == PFG_SIMHASH ? fn_hp : fn_fht);
     return PFG_OK;
 }
 
@@ -183,6 +189,17 @@ pfg_status derive_L(Geo& g, uint64_t budget, int reps_override) {
         g.L = (int)std::min<uint64_t>(L, (uint64_t)g.max_reps);
     }
     if (g.L < 1 || g.L > 65536) return fail(PFG_E_ARG, "repetitions must be in [1, 65536]");
+    if (g.strategy == PFG_TENSOR) {
+        // L an even power of two: the largest one the budget admits, at most 4096
+        // (shells of 2S - 1 <= 32 tries per chunk need S <= 16 -> L <= 256)
+        int S = 1;
+        while ((S * 2) * (S * 2) <= g.L && S * 2 <= 16) S *= 2;
+        if (reps_override > 0 && S * S != reps_override)
+            return fail(PFG_E_ARG, "tensor strategy: reps must be an even power of two, at most 256");
+        g.S = S;
+        g.L = S * S;
+        g.m = S * g.c;   // functions: 2 collections x S tuples x c/2
+    }
     g.index_bytes = g.fixed_bytes + (uint64_t)g.L * g.per_rep_bytes;
     return PFG_OK;
 }
@@ -209,6 +226,11 @@ struct StopModel {
     }
     // Lemma 1 failure bound, Alg. 1 line 8, pool Cantelli
     bool stop(int i, int j, float ip, double delta, int rule) const {
+        if (strategy == PFG_TENSOR) {
+            // Alg. 2: after j = m shells at depth i, 2 (1 - P_{i/2})^m <= delta
+            const double Ph = P(i / 2, ip);
+            return std::log(2.0) + (double)j * std::log1p(-Ph) <= std::log(delta);
+        }
         const double Pi = P(i, ip);
         if (strategy == PFG_POOL) {
             const int ci = (i + ell - 1) / ell;
@@ -548,7 +570,7 @@ pfg_status gen_functions(pfg_index* I, cudaStream_t st) {
     PFG_TRY(I->slot.alloc(g.L, "slots"));
     PFG_CUDA(cudaMemcpyAsync(I->slot.p, sl.data(), g.L, cudaMemcpyHostToDevice, st));
     // LSH functions: F = L*c (independent) or m (pool)
-    const int64_t F = g.strategy == PFG_POOL ? (int64_t)g.m : (int64_t)g.L * g.c;
+    const int64_t F = g.strategy != PFG_INDEPENDENT ? (int64_t)g.m : (int64_t)g.L * g.c;
     if (g.family == PFG_SIMHASH) {
         std::vector<float> A((size_t)F * g.dpad, 0.0f);
         const uint64_t kh = stream_key(seed, kTagHP);
@@ -567,6 +589,21 @@ pfg_status gen_functions(pfg_index* I, cudaStream_t st) {
                         S[(size_t)(f * 3 + r) * g.W + (u >> 5)] |= 1u << (u & 31);
         PFG_TRY(I->sg.alloc(S.size() * 4, "fht signs"));
         PFG_CUDA(cudaMemcpyAsync(I->sg.p, S.data(), S.size() * 4, cudaMemcpyHostToDevice, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+    }
+    if (g.strategy == PFG_TENSOR) {
+        // trie (j1, j2), j = j1*S + j2: position t = 2s + a holds function s of collection a's tuple
+        // (j1 for a = 0, j2 for a = 1), function (a, tuple, s) = (a*S + tuple)*(c/2) + s
+        // ("taken by interleaving")
+        const int S = g.S, h = g.c / 2;
+        I->sel_h.assign((size_t)g.L * g.c, 0);
+        for (int j = 0; j < g.L; ++j)
+            for (int t = 0; t < g.c; ++t) {
+                const int a = t % 2, s = t / 2, tuple = a ? j % S : j / S;
+                I->sel_h[(size_t)j * g.c + t] = (a * S + tuple) * h + s;
+            }
+        PFG_TRY(I->sel.alloc(I->sel_h.size() * 4, "tensor selection"));
+        PFG_CUDA(cudaMemcpyAsync(I->sel.p, I->sel_h.data(), I->sel_h.size() * 4, cudaMemcpyHostToDevice, st));
         PFG_CUDA(cudaStreamSynchronize(st));
     }
     if (g.strategy == PFG_POOL) {
@@ -668,7 +705,7 @@ pfg_status get_thr(pfg_index* I, float recall, const SearchCfg& s, std::shared_p
         for (int i = i0; i < i1; ++i)
             for (int j = 1; j <= g.L; ++j) {
                 float v;
-                if (s.per_round && j < g.L) v = INFINITY;
+                if (g.strategy == PFG_TENSOR ? j > g.S : (s.per_round && j < g.L)) v = INFINITY;
                 else v = smallest_true([&](float ip) { return sm.stop(i, j, ip, delta, s.rule); });
                 thr[(size_t)(i - 1) * g.L + (j - 1)] = v;
             }
@@ -1023,7 +1060,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     bool lazy = false;
     // rounds 0 and 1 reach repetitions [0, 1 + R) only (R-17 default schedule): the codes and
     // ranges of the later eager repetitions are computed beside them
-    const int split = (s.engine == 0 && !s.uniform) ? 1 + s.R : 0;
+    const int split = (s.engine == 0 && !s.uniform && g.strategy != PFG_TENSOR) ? 1 + s.R : 0;
     PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st, split));
 
     const int k_eff = (int)std::min<int64_t>(k, g.n);
@@ -1051,7 +1088,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->slots_bm = bm_words;
     }
     PFG_TRY(I->cur.ensure((size_t)nq * g.L * 16, "cursors"));
-    const bool rounds = s.engine == 0;
+    const bool rounds = s.engine == 0 && g.strategy != PFG_TENSOR;  // tensor shells: the fused kernel
     // round engine: `rounds` bulk rounds (search option, default 5), then the fused kernel resumes
     // every query still running (stragglers keep their hash set in shared memory across chunks
     // there, instead of paying a round's fixed latency per chunk).  The rounds are enqueued
@@ -1101,6 +1138,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.per_round = s.per_round; p.use_filter = (s.use_filter && g.M > 0) ? 1 : 0; p.c = g.c; p.ell = g.ell; p.dp = g.dp;
     p.lazy = lazy ? 1 : 0; p.claim_cap = kClaimCap; p.trace_cap = s.trace_cap; p.kt = kt; p.smem_warp = smem_warp;
     p.uniform = s.uniform;
+    p.tensor_s = g.strategy == PFG_TENSOR ? g.S : 0;
+    p.lstep = g.strategy == PFG_TENSOR ? 2 * g.ell : 1;
     p.x = I->x.as<float>(); p.tab = I->tab.as<Entry>(); p.pt = I->pt.as<uint32_t>();
     p.slot = I->slot.as<uint8_t>(); p.qx = I->qx.as<float>(); p.qsk = I->qsk.as<uint64_t>();
     p.qcodes = I->qcodes.as<uint32_t>(); p.qc_n = I->qc_n; p.qc_ld = I->qc_ld;
@@ -1409,7 +1448,7 @@ pfg_status pfg_export(const pfg_index* Ic, int32_t what, int32_t arg, void* dst,
             std::memcpy(dst, I->slot_h.data(), bytes);
             return PFG_OK;
         case PFG_EXPORT_POOLSEL:
-            if (g.strategy != PFG_POOL) return fail(PFG_E_STATE, "index is not pooled");
+            if (g.strategy == PFG_INDEPENDENT) return fail(PFG_E_STATE, "index has no function selections");
             if (bytes != I->sel_h.size() * 4) return fail(PFG_E_ARG, "dst_bytes must be L*c*4");
             std::memcpy(dst, I->sel_h.data(), bytes);
             return PFG_OK;

@@ -55,6 +55,17 @@ def test_abi_struct_sizes_match_header():
     assert C.sizeof(pfg.IndexInfo) == i
 
 
+def test_cost_model_tensor():
+    # tensor: L is rounded down to an even power of two (at most 256); K must be an
+    # even number of whole functions
+    assert pfg.derive_reps(1_000_000, 100, "fht_cp", 4 << 30, strategy="tensor", prefix_bits=32)[0] == 64
+    assert pfg.derive_reps(1_000_000, 100, "simhash", 64 << 30, strategy="tensor")[0] == 256
+    with pytest.raises(pfg.PfgError):
+        pfg.derive_reps(1_000_000, 100, "fht_cp", 4 << 30, strategy="tensor")      # 3 functions of 8 bits
+    with pytest.raises(pfg.PfgError):
+        pfg.derive_reps(10_000, 32, "simhash", 0, strategy="tensor", reps=32)      # not an even power of two
+
+
 def test_cost_model_configs():
     # L for BASELINE configs 2-5 at their budgets (GiB) under the R-11 cost model with 16-byte
     # entries (R-21); SURVEY.md Appendix B has the 8-byte-entry figures 452 / 884 / 1626 / 1206

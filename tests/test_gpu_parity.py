@@ -25,13 +25,13 @@ def _cuda(a):
 
 
 class Case:
-    def __init__(self, name, data, q, family, L, seed, strategy=O.INDEPENDENT, pool_bits=3072, M=32):
+    def __init__(self, name, data, q, family, L, seed, strategy=O.INDEPENDENT, pool_bits=3072, M=32, K=24):
         self.name, self.data, self.q = name, data, q
         fam = "simhash" if family == O.HP else "fht_cp"
-        strat = "pool" if strategy == O.POOL else "independent"
+        strat = {O.POOL: "pool", O.TENSOR: "tensor"}.get(strategy, "independent")
         self.gpu = pfg.Index(_cuda(data), 0, fam, seed=seed, reps=L, strategy=strat, pool_bits=pool_bits,
-                             sketch_words=M if M > 0 else -1)
-        self.orc = O.OracleIndex(data, family, L=L, seed=seed, strategy=strategy, pool_bits=pool_bits, M=M)
+                             sketch_words=M if M > 0 else -1, prefix_bits=K)
+        self.orc = O.OracleIndex(data, family, L=L, seed=seed, strategy=strategy, pool_bits=pool_bits, M=M, K=K)
 
 
 @pytest.fixture(scope="module")
@@ -49,6 +49,10 @@ def cases():
     out["fht_long"] = Case("fht_long", d2[:8000], q2[:40], O.FHTCP, 64, 6)
     out["fht_d40"] = Case("fht_d40", d2[:5000, :40].copy(), q2[:30, :40].copy(), O.FHTCP, 48, 7)
     out["fht_d20"] = Case("fht_d20", d2[:5000, :20].copy(), q2[:30, :20].copy(), O.FHTCP, 40, 8)
+    # tensoring (Alg. 2): L = 16 tries from 2 x 4 tuples; FHT-CP with K = 32 bits = 4 functions
+    out["hp_tensor"] = Case("hp_tensor", d1, q1, O.HP, 16, 11, O.TENSOR)
+    out["fht_tensor"] = Case("fht_tensor", d2[:8000], q2[:40], O.FHTCP, 16, 12, O.TENSOR, K=32)
+    out["hp_tensor64"] = Case("hp_tensor64", d1, q1[:32], O.HP, 64, 13, O.TENSOR)
     return out
 
 
@@ -156,6 +160,28 @@ def _compare(c, k, recall, gpu_kw, orc_kw, trace=True):
 def test_search_parity(cases, name, R, recall, engine):
     c = cases[name]
     _compare(c, 10, recall, dict(rep_chunk=R, engine=engine), dict(rep_chunk=R))
+
+
+@pytest.mark.parametrize("name", ["hp_tensor", "fht_tensor", "hp_tensor64"])
+@pytest.mark.parametrize("recall", [0.5, 0.9, 0.99])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_search_parity_tensor(cases, name, recall, engine):
+    c = cases[name]
+    st = _compare(c, 10, recall, dict(engine=engine), dict())
+    assert np.all(st["j_stop"][st["i_stop"] > 0] <= int(round(c.orc.L ** 0.5)))   # shells m <= sqrt(L)
+    assert np.all((st["i_stop"] % (2 * c.orc.ell)) == 0)                          # depths in steps of two functions
+
+
+@pytest.mark.parametrize("name", ["hp_tensor", "fht_tensor"])
+def test_tensor_build_bit_exact(cases, name):
+    c = cases[name]
+    g, o = c.gpu, c.orc
+    assert np.array_equal(g.export_pool_sel(), o.pool_sel())
+    for j in range(o.L):
+        tab = g.export_table(j)
+        codes, ids = o.rep(j)
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
 
 
 @pytest.mark.parametrize("name", ["fht_long", "fht_d40", "fht_d20"])
