@@ -32,7 +32,8 @@ import synth  # noqa: E402
 
 METRIC = "queries/s at >=0.9 recall, k=10, 1Mx100-d angular; achieved HBM GB/s"
 WORKLOAD_NOTE = {2: " (Gaussian-mixture stand-in for GloVe-1M)",
-                 3: " (planted-partner stand-in for the paper's SYNTHETIC set)"}
+                 3: " (planted-partner stand-in for the paper's SYNTHETIC set)",
+                 6: " (the paper's SYNTHETIC construction, PAPER.md:424-439)"}
 
 
 def peaks():

@@ -104,8 +104,16 @@ typedef struct {
                                  grid).  Results are identical. */
     int32_t uniform_chunks;   /* [0] 1 = chunks of R repetitions from the start (tau = 64 for a whole
                                  first chunk); 0 = the first chunk is the single repetition 0 */
-    int32_t rounds;           /* [5] engine 0: bulk rounds before the fused kernel resumes the rest */
-    int32_t reserved2;
+    int32_t rounds;           /* [5] engine 0: bulk rounds before the fused kernel resumes the rest
+                                 (then a device-side loop of rounds may continue, see `wide`) */
+    int32_t wide;             /* [0] engine 0: > 0 = evaluated-id capacity of the per-query hash set
+                                 (at most 1536) before a query moves its evaluated set to a visit-tag
+                                 array of n words ("wide") and continues in the device-side round loop;
+                                 0 = automatic: capacity 1536, wide queries on iff the previous search's
+                                 queries read >= 64 MiB each (evaluated rows + table entries), and then
+                                 the loop keeps every query still running after the blind rounds;
+                                 -1 = off (a query beyond the hash set continues in the fused kernel's
+                                 global bitmap).  Results are identical in every mode. */
 } pfg_search_opts;
 
 /* per-query counters (optional output of pfg_search) */
@@ -116,7 +124,9 @@ typedef struct {
     uint32_t filtered;   /* retrieved candidates rejected by the sketch filter */
     uint32_t dups;       /* retrieved candidates that passed the filter but were already evaluated */
     uint32_t evaluated;  /* distinct points whose exact inner product was computed */
-    uint32_t flags;      /* bit0: k > n (padded); bit1: zero query row; bit2: trace truncated */
+    uint32_t flags;      /* bit0: k > n (padded); bit1: zero query row; bit2: trace truncated;
+                            bit3: fused kernel, global bitmap; bit4: wide (visit-tag array);
+                            bit5: not finished (round cap of the device-side loop; no result) */
     uint32_t probes;     /* table entries read by the prefix-range searches */
 } pfg_query_stats;
 
@@ -202,8 +212,10 @@ pfg_status pfg_last_timing(const pfg_index* idx, float* ms3, int32_t* launches);
 
 /* per-phase breakdown of the query-kernel time of the same search (CUDA events between the
  * phases' launches): ms[0] k_expand, ms[1] k_scan, ms[2] k_dedupe, ms[3] k_sims, ms[4] k_merge
- * (summed over the bulk rounds), ms[5] the fused kernel, ms[6] other (round control, query
- * order, code extension for resumed queries).  n: entries to write (<= 8). */
+ * (summed over the blind bulk rounds), ms[5] the fused kernel (both launches; the first runs
+ * beside the device-side round loop), ms[6] other (round control, query order, code extension for
+ * resumed queries), ms[7] the device-side round loop (a CUDA graph; its rounds are not split into
+ * phases).  n: entries to write (<= 8). */
 pfg_status pfg_last_phases(const pfg_index* idx, float* ms, int32_t n);
 
 void pfg_free(pfg_index* idx);

@@ -51,7 +51,7 @@ class SearchOpts(C.Structure):
                 ("stop_rule", C.c_int32), ("stop_granularity", C.c_int32), ("use_filter", C.c_int32),
                 ("filter_eps", C.c_float), ("trace_cap", C.c_int32), ("timing", C.c_int32),
                 ("trace_ids", C.c_void_p), ("engine", C.c_int32), ("uniform_chunks", C.c_int32),
-                ("rounds", C.c_int32), ("reserved2", C.c_int32)]
+                ("rounds", C.c_int32), ("wide", C.c_int32)]
 
 
 class IndexInfo(C.Structure):
@@ -208,7 +208,8 @@ class Index:
 
     @staticmethod
     def _sopts(rep_chunk=DEFAULT_REP_CHUNK, segment=12, stop_rule=0, per_round=False, use_filter=True, eps=0.0,
-               trace_cap=0, trace_ptr=None, timing=False, engine=0, uniform_chunks=False, rounds=0) -> SearchOpts:
+               trace_cap=0, trace_ptr=None, timing=False, engine=0, uniform_chunks=False, rounds=0,
+               wide=0) -> SearchOpts:
         o = SearchOpts()
         o.struct_size = C.sizeof(SearchOpts)
         o.rep_chunk, o.segment, o.stop_rule = rep_chunk, segment, stop_rule
@@ -221,6 +222,7 @@ class Index:
         o.engine = int(engine)
         o.uniform_chunks = int(uniform_chunks)
         o.rounds = int(rounds)
+        o.wide = int(wide)
         return o
 
     def last_timing(self):
@@ -230,7 +232,7 @@ class Index:
         _check(lib().pfg_last_timing(self._h, ms, C.byref(n)))
         return float(ms[0]), float(ms[1]), float(ms[2]), int(n.value)
 
-    PHASES = ("expand", "scan", "dedupe", "sims", "merge", "fused", "other")
+    PHASES = ("expand", "scan", "dedupe", "sims", "merge", "fused", "other", "loop")
 
     def last_phases(self) -> dict:
         """per-phase ms of the query kernels of the last timed search (see pfg_last_phases)"""

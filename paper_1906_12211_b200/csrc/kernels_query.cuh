@@ -57,6 +57,17 @@ struct RoundCtl {
     uint32_t pad;
     uint32_t wk[2][4];     // work counters of k_expand, k_scan, k_dedupe, k_merge (round parity)
     uint32_t dfront[2], dback[2];  // k_dedupe's order: long chunks from the front, the rest from the back
+    // wide queries (evaluated set in a visit-tag array instead of the shared-memory hash set)
+    uint32_t nwt[2];       // wide scan tiles of the round (round parity)
+    uint32_t nwide[2];     // wide queries in the active list (round parity)
+    uint32_t wnext;        // visit-tag arrays handed out in this search
+    uint32_t loop;         // 1 while the device-side round loop runs (k_merge hands off to fused2)
+    uint32_t nfused2;      // queries handed to the fused kernel during the loop
+    uint32_t round;        // rounds run by the loop
+    uint32_t wtag;         // the search's epoch tag (high half of every visit tag)
+    uint32_t wdefer;       // wide chunks deferred for want of wide tiles (the host grows the buffer)
+    uint32_t pad2;
+    unsigned long long evsum, emsum;  // evaluated ids and emitted positions of the finished queries
 };
 struct RoundState {
     int32_t* lvl;       // [nq] next level i to process (K..1); 0 = only the i = 0 scan remains
@@ -81,9 +92,23 @@ struct RoundState {
     uint32_t* act[2];   // [nq] active lists (round parity)
     uint32_t* dord[2];  // [nq] the active list reordered for k_dedupe (long chunks first)
     uint32_t* fused;    // [nq] queries handed to the fused kernel
+    uint32_t* fused2;   // [nq] queries handed to the fused kernel during the device-side loop
     RoundCtl* ctl;
     int Ecap, Ccap;
     uint32_t pool_cap;
+    // wide queries (kernels_rounds.cuh): per query a visit-tag array W[n] (slot wslot[q]); a
+    // passing candidate of visit (i, j) does atomicMin(W[id], tag(i, j)) and is fresh iff W[id]
+    // ends equal to its own tag, i.e. no earlier visit (earlier chunk, or earlier repetition of
+    // the same chunk) passed it.  Tags carry the search epoch in the high half, so no reset is
+    // needed between searches.
+    uint32_t* wv;       // [wslots][n] visit tags
+    uint32_t* wslot;    // [nq] the query's visit-tag array
+    uint4* wtiles;      // wide scan tile descriptors (two uint4 each)
+    uint32_t* wcand;    // [wcap][kTile] per wide tile: passing candidates, then the fresh ids in order
+    float* wsim;        // [wcap][kTile] similarities of the fresh ids
+    uint32_t* wtcnt;    // [wcap] fresh | passing << 8 | repetition << 16 | kept << 24
+    uint32_t* rtile;    // [nq][kMaxR + 1] first wide tile of each repetition of the chunk, then the end
+    uint32_t wslots, wcap, hmax;  // hmax: evaluated ids a query keeps in the hash set before it widens
 };
 constexpr int kCnt = 8;
 
@@ -725,6 +750,10 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
         // stop-depth histogram (repetitions hashed at level K), read by the host to size the
         // next search's eager query hashing; a deeper stop counts as all L repetitions
         if (p.jhist && lane == 0) atomicAdd(p.jhist + min(i_stop == p.K ? j_stop : p.L, kJHist - 1), 1u);
+        if (p.rs.ctl && lane == 0) {
+            atomicAdd(&p.rs.ctl->evsum, (unsigned long long)st.nE);
+            atomicAdd(&p.rs.ctl->emsum, (unsigned long long)st.emitted);
+        }
         if (p.stats && lane == 0) {
             pfg_query_stats s;
             s.i_stop = i_stop; s.j_stop = j_stop; s.emitted = st.emitted; s.filtered = st.filtered;

@@ -31,6 +31,17 @@
 namespace pfg {
 
 constexpr int kFlagDone = 1, kFlagFused = 2, kFlagSaved = 4;  // kFlagSaved: hsave holds the set
+// kFlagWide: the evaluated set lives in the query's visit-tag array (RoundState::wv); kFlagDefer:
+// the chunk found no room in the wide tile buffer and is expanded again next round; kFlagRedo: the
+// query widened while its chunk was deduplicated and runs the chunk again, wide, next round
+constexpr int kFlagWide = 8, kFlagDefer = 16, kFlagRedo = 32;
+
+// The round kernels take their parameters by value (blind rounds) or from device memory (the
+// device-side loop's graph, so that one instantiated graph serves every search: k_setp writes the
+// search's parameters there)
+__device__ __forceinline__ const QueryParams& deref(const QueryParams& p) { return p; }
+__device__ __forceinline__ const QueryParams& deref(const QueryParams* p) { return *p; }
+__global__ void k_setp(QueryParams p, QueryParams* dst) { *dst = p; }
 constexpr int kEPre = 16;  // evaluated ids loaded per lane per batch when the hash set is rebuilt
 constexpr int kSaveMin = 512;  // k_dedupe rebuilds sets of at most this many ids instead of restoring them
 
@@ -52,6 +63,32 @@ __device__ __forceinline__ uint32_t next_item(uint32_t* ctr, int lane) {
     uint32_t v = 0;
     if (lane == 0) v = atomicAdd(ctr, 1u);
     return __shfl_sync(kFull, v, 0);
+}
+
+// visit tag of (level i, repetition j): the search epoch in the high half, then the visit's place
+// s = (K - i) L + j + 1 in the query's visiting order (the host keeps (K + 1) L < 2^16); tag s = 0
+// marks the ids evaluated before the query widened
+__device__ __forceinline__ uint32_t visit_tag(const QueryParams& p, int i, int j) {
+    return p.rs.ctl->wtag | (uint32_t)((p.K - i) * p.L + j + 1);
+}
+
+// warp-collective: move the query's evaluated set into a visit-tag array of its own (false: none
+// left).  The array's stale tags are from earlier searches (larger epochs' tags are smaller, so
+// every stale tag is above the current search's tags) and no array is handed out twice per search.
+__device__ __forceinline__ bool try_widen(const QueryParams& p, int64_t q, int lane) {
+    const RoundState& rs = p.rs;
+    uint32_t slot = 0;
+    if (lane == 0) slot = atomicAdd(&rs.ctl->wnext, 1u);
+    slot = __shfl_sync(kFull, slot, 0);
+    if (slot >= rs.wslots) return false;
+    uint32_t* W = rs.wv + (int64_t)slot * p.n;
+    const uint32_t nE = rs.cnt[q * kCnt + 3];
+    const uint32_t* E = rs.E + q * (int64_t)rs.Ecap;
+    const uint32_t t0 = rs.ctl->wtag;
+    for (uint32_t e = lane; e < nE; e += 32) W[E[e]] = t0;
+    if (lane == 0) { rs.wslot[q] = slot; rs.flags[q] |= kFlagWide; }
+    __syncwarp();
+    return true;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -112,8 +149,9 @@ __global__ void k_qorder_list(const uint64_t* __restrict__ keys, int64_t nq, uin
 }
 
 // ---------------------------------------------------------------------------------------------
-__global__ void k_rinit(QueryParams p) {
+__global__ void k_rinit(QueryParams p, uint32_t wtag) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q == 0) p.rs.ctl->wtag = wtag;
     if (q >= p.nq) return;
     const RoundState& rs = p.rs;
     rs.lvl[q] = p.K;
@@ -150,8 +188,9 @@ constexpr int kTile = PFG_TILE;   // emitted positions per scan tile
 #endif
 constexpr int kDedupeLong = PFG_DLONG;  // emitted positions from which k_dedupe schedules a chunk first
 
-template <int EPL>
-__global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy) {
+template <int EPL, typename PP>
+__global__ void __launch_bounds__(128) k_expand(PP pp, int par, int lazy) {
+    const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     ExpandSmem* c = (ExpandSmem*)(smem_raw + wib * expand_smem_bytes(p.dpad, lazy));
@@ -162,14 +201,18 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
         rs.ctl->nact[par ^ 1] = 0; rs.ctl->pool_top[par ^ 1] = 0; rs.ctl->ntiles[par ^ 1] = 0;
         for (int t = 0; t < 4; ++t) rs.ctl->wk[par ^ 1][t] = 0;
         rs.ctl->dfront[par ^ 1] = 0; rs.ctl->dback[par ^ 1] = 0;
+        rs.ctl->nwt[par ^ 1] = 0; rs.ctl->nwide[par ^ 1] = 0;
     }
     const uint32_t* act = rs.act[par];
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nact; a += nw) {
         const int64_t q = act[a];
         const int i = rs.lvl[q], c0 = rs.c0[q], tn = rs.tn[q];
-        const int nr = chunk_reps(p, i, c0, tn, rs.T + q * p.kt, lane);
-        const int tau = tau_of_state(p, tn, rs.T + q * p.kt);
+        bool wide = (rs.flags[q] & kFlagWide) != 0;
+        // i = 0 (wide queries only): one repetition, the whole table of repetition 0, no filter
+        // (R-13)
+        const int nr = i == 0 ? 1 : chunk_reps(p, i, c0, tn, rs.T + q * p.kt, lane);
+        const int tau = i == 0 ? 64 : tau_of_state(p, tn, rs.T + q * p.kt);
         uint4* cur = p.cur + q * p.L;
         uint32_t probes = 0;
         if (i == p.K) {
@@ -181,7 +224,7 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
             }
             __syncwarp();
         }
-        for (int task = lane; task < 2 * nr; task += 32) {
+        for (int task = lane; i > 0 && task < 2 * nr; task += 32) {
             const bool left = task < nr;
             const int r = left ? task : task - nr;
             const int j = c0 + r;
@@ -221,7 +264,9 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
         uint32_t em = 0, nelo = 0, elo = 0, ehi = 0, nehi = 0;
         if (lane < nr) {
             const int j = c0 + lane;
-            if (i == p.K) {
+            if (i == 0) {
+                nehi = (uint32_t)p.n;
+            } else if (i == p.K) {
                 const uint32_t a_ = c->bnd[lane], b_ = c->bnd[nr + lane];
                 const uint32_t B = (uint32_t)p.B;
                 elo = ehi = nelo = a_;
@@ -233,7 +278,7 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
                 nelo = c->bnd[lane]; nehi = c->bnd[nr + lane];
             }
             em = (elo - nelo) + (nehi - ehi);
-            rs.pend[q * kMaxR + lane] = make_uint4(c->qc[lane], nelo, nehi, 0u);
+            rs.pend[q * kMaxR + lane] = make_uint4(i > 0 ? c->qc[lane] : 0u, nelo, nehi, 0u);
         }
         uint32_t incl = em;
 #pragma unroll
@@ -259,33 +304,74 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
         // a single repetition with nothing evaluated yet and tau = 64 (the search's first chunk):
         // every emitted id is fresh (a repetition holds each id once), so k_scan writes the ids
         // straight to the evaluated list and the round's pool and k_dedupe skips the query
-        const bool direct = nr == 1 && tau == 64 && rs.cnt[q * kCnt + 3] == 0;
-        const bool over = direct ? total > (uint32_t)kHMax : ntl > (uint32_t)(rs.Ccap / kTile);
+        bool direct = !wide && nr == 1 && tau == 64 && rs.cnt[q * kCnt + 3] == 0;
+        const bool over = direct ? total > rs.hmax : ntl > (uint32_t)(rs.Ccap / kTile);
+        // a chunk beyond the hash set's reach moves the query to the wide path (if an array is
+        // left; else the fused kernel takes it)
+        if (!wide && over && try_widen(p, q, lane)) { wide = true; direct = false; }
         uint32_t base = 0;
+        bool handed = false;
         if (lane == 0) {
             rs.rinfo[q] = make_uint4((uint32_t)nr, (uint32_t)tau, ntl, direct ? 1u : 0u);
             rs.cnt[q * kCnt + 4] += probes;
-            if (over) rs.flags[q] |= kFlagFused;
-            if (direct && !over) {
-                const uint32_t pb = atomicAdd(&rs.ctl->pool_top[par], total);
-                if ((uint64_t)pb + total > rs.pool_cap) {
-                    rs.flags[q] |= kFlagFused;
-                } else {
-                    rs.poff[q] = pb;
-                    rs.pn[q] = total;
-                    uint32_t* rc = rs.repcnt + q * kMaxR * 3;
-                    rc[1] = 0; rc[2] = 0;
+            if (wide) {
+                if (ntl) base = atomicAdd(&rs.ctl->nwt[par], ntl);
+                if ((uint64_t)base + ntl > rs.wcap) { rs.flags[q] |= kFlagDefer; atomicAdd(&rs.ctl->wdefer, 1u); }
+            } else {
+                if (over) rs.flags[q] |= kFlagFused;
+                if (direct && !over) {
+                    const uint32_t pb = atomicAdd(&rs.ctl->pool_top[par], total);
+                    if ((uint64_t)pb + total > rs.pool_cap) {
+                        rs.flags[q] |= kFlagFused;
+                    } else {
+                        rs.poff[q] = pb;
+                        rs.pn[q] = total;
+                        uint32_t* rc = rs.repcnt + q * kMaxR * 3;
+                        rc[1] = 0; rc[2] = 0;
+                    }
                 }
+                if (ntl && !(rs.flags[q] & kFlagFused)) base = atomicAdd(&rs.ctl->ntiles[par], ntl);
             }
-            if (ntl && !(rs.flags[q] & kFlagFused)) base = atomicAdd(&rs.ctl->ntiles[par], ntl);
+            handed = (rs.flags[q] & (kFlagFused | kFlagDefer)) != 0;
             // k_dedupe takes the long chunks first (a shorter tail for its dynamic scheduler)
             const uint32_t slot = total >= (uint32_t)kDedupeLong ? atomicAdd(&rs.ctl->dfront[par], 1u)
                                                                   : nact - 1u - atomicAdd(&rs.ctl->dback[par], 1u);
             rs.dord[par][slot] = (uint32_t)q;
         }
         base = __shfl_sync(kFull, base, 0);
-        const bool handed = __shfl_sync(kFull, (rs.flags[q] & kFlagFused) ? 1 : 0, 0);
-        if (!handed && lane < nr) {
+        handed = __shfl_sync(kFull, handed ? 1 : 0, 0) != 0;
+        if (wide) {
+            if (handed) {
+                // no room: the part of the claimed range below the capacity holds dead tiles
+                for (uint32_t t = base + lane; t < rs.wcap && t < base + ntl; t += 32)
+                    rs.wtiles[2 * (int64_t)t] = make_uint4((uint32_t)q, 0u, 0u, 0u);
+            } else {
+                // wide tiles: descriptors {query, table position, 0, count | rep << 16 | tau << 24}
+                // {sketch word, visit tag, j}, written by the whole warp one repetition at a time;
+                // rtile holds each repetition's first tile
+                uint32_t* rt = rs.rtile + q * (kMaxR + 1);
+                if (lane < nr) rt[lane] = base + tin - tA - tB;
+                if (lane == 0) rt[nr] = base + ntl;
+                for (int r = 0; r < nr; ++r) {
+                    const int j = c0 + r;
+                    const uint32_t t0 = base + __shfl_sync(kFull, tin - tA - tB, r);
+                    const uint32_t a0 = __shfl_sync(kFull, nelo, r), la = __shfl_sync(kFull, lenA, r);
+                    const uint32_t b0 = __shfl_sync(kFull, ehi, r), lb = __shfl_sync(kFull, lenB, r);
+                    const uint32_t ta = (la + kTile - 1) / kTile, tb = (lb + kTile - 1) / kTile;
+                    const uint64_t sk = (p.use_filter && tau < 64) ? __ldg(p.qsk + q * p.M + __ldg(p.slot + j)) : 0ull;
+                    const uint32_t tag = visit_tag(p, i, j);
+                    for (uint32_t t = lane; t < ta + tb; t += 32) {
+                        const bool pa = t < ta;
+                        const uint32_t o = (pa ? t : t - ta) * kTile;
+                        const uint32_t len = pa ? la : lb;
+                        const uint32_t cnt = min((uint32_t)kTile, len - o);
+                        rs.wtiles[2 * (int64_t)(t0 + t)] = make_uint4((uint32_t)q, (pa ? a0 : b0) + o, 0u,
+                                                                      cnt | ((uint32_t)r << 16) | ((uint32_t)tau << 24));
+                        rs.wtiles[2 * (int64_t)(t0 + t) + 1] = make_uint4((uint32_t)sk, (uint32_t)(sk >> 32), tag, (uint32_t)j);
+                    }
+                }
+            }
+        } else if (!handed && lane < nr) {
             // lane r writes the descriptors of repetition r's pieces: {query, table position,
             // chunk position, count | rep << 16 | tau << 24} {sketch word, tile index | direct, j}
             const int j = c0 + lane;
@@ -313,12 +399,60 @@ __global__ void __launch_bounds__(128) k_expand(QueryParams p, int par, int lazy
 // query's chunk (descriptor from k_expand): load the 16-byte entries, apply the sketch filter
 // with the chunk's tau, and compact the passing ids in order to the tile's
 // candidate slots (count | repetition << 16 in tcnt).  Fully data-parallel.
-__global__ void __launch_bounds__(256) k_scan(QueryParams p, int par) {
+//
+// Wide tiles (after the hash-set tiles): the passing ids claim their first visit in the query's
+// visit-tag array by atomicMin(W[id], tag); an id whose array already held a smaller tag was
+// evaluated before (an earlier chunk, or an earlier repetition of this chunk that got there
+// first) and is a duplicate; the others are provisional until k_sims checks that no earlier
+// repetition of the chunk lowered the tag after this claim.
+__device__ __forceinline__ void scan_wide_tile(const QueryParams& p, int64_t aw, int lane) {
+    const RoundState& rs = p.rs;
+    const uint4 d0 = rs.wtiles[2 * aw], d1 = rs.wtiles[2 * aw + 1];
+    const uint32_t cnt = d0.w & 0xffffu, rep = (d0.w >> 16) & 0xffu, tau = d0.w >> 24;
+    if (cnt == 0) { if (lane == 0) rs.wtcnt[aw] = 0; return; }
+    const int64_t q = d0.x;
+    const uint64_t sk = ((uint64_t)d1.y << 32) | d1.x;
+    const uint32_t tag = d1.z;
+    uint32_t* W = rs.wv + (int64_t)rs.wslot[q] * p.n;
+    const Entry* tj = p.tab + (int64_t)d1.w * p.n + d0.y;
+    uint4 e[kTile / 32];
+#pragma unroll
+    for (int u = 0; u < kTile / 32; ++u) {
+        const uint32_t o = u * 32 + lane;
+        if (o < cnt) e[u] = __ldg(reinterpret_cast<const uint4*>(tj + o));
+    }
+    bool pass[kTile / 32];
+    uint32_t old[kTile / 32];
+#pragma unroll
+    for (int u = 0; u < kTile / 32; ++u) {
+        const uint32_t o = u * 32 + lane;
+        pass[u] = o < cnt;
+        if (pass[u] && p.use_filter && tau < 64) pass[u] = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ sk) <= tau;
+        old[u] = pass[u] ? atomicMin(W + e[u].x, tag) : 0u;
+    }
+    uint32_t* cand = rs.wcand + aw * kTile;
+    uint32_t np = 0, npass = 0;
+#pragma unroll
+    for (int u = 0; u < kTile / 32; ++u) {
+        npass += __popc(__ballot_sync(kFull, pass[u]));
+        const bool prov = pass[u] && old[u] >= tag;
+        const uint32_t pm = __ballot_sync(kFull, prov);
+        if (prov) cand[np + __popc(pm & lanemask_lt())] = e[u].x;
+        np += __popc(pm);
+    }
+    if (lane == 0) rs.wtcnt[aw] = np | (npass << 8) | (rep << 16);
+}
+
+template <typename PP>
+__global__ void __launch_bounds__(256) k_scan(PP pp, int par) {
+    const QueryParams& p = deref(pp);
     const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
     const uint32_t ntiles = rs.ctl->ntiles[par];
+    const uint32_t nwt = min(rs.ctl->nwt[par], rs.wcap);
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < ntiles; a += nw) {
+    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < (int64_t)ntiles + nwt; a += nw) {
+        if (a >= ntiles) { scan_wide_tile(p, a - ntiles, lane); continue; }
         const uint4 d0 = rs.tiles[2 * a], d1 = rs.tiles[2 * a + 1];
         const int64_t q = d0.x;
         const uint32_t cnt = d0.w & 0xffffu, rep = (d0.w >> 16) & 0xffu, tau = d0.w >> 24;
@@ -374,7 +508,9 @@ struct DedupeSmem {
 };
 constexpr int kCPre = 8;   // candidate ids loaded per lane per batch
 
-__global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
+template <typename PP>
+__global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
+    const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     DedupeSmem* c = (DedupeSmem*)(smem_raw + wib * align16((int)sizeof(DedupeSmem)));
@@ -384,7 +520,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
     for (uint32_t a = next_item(&rs.ctl->wk[par][2], lane); a < nact; a = next_item(&rs.ctl->wk[par][2], lane)) {
         const int64_t q = act[a];
         const int fl = rs.flags[q];
-        if (fl & kFlagFused) continue;
+        if (fl & (kFlagFused | kFlagWide)) continue;
         const uint4 info = rs.rinfo[q];
         if (info.w) continue;  // direct chunk: k_scan wrote the evaluated ids and the pool
         const int nr = (int)info.x;
@@ -496,7 +632,7 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
                 if (fresh) E[nE + ns + __popc(fm & lanemask_lt())] = v[u];
                 ns += __popc(fm);
             }
-            if (nE + ns > (uint32_t)kHMax) overflow = true;
+            if (nE + ns > rs.hmax) overflow = true;
         }
         __syncwarp();
         uint32_t base = 0;
@@ -504,7 +640,10 @@ __global__ void __launch_bounds__(128) k_dedupe(QueryParams p, int par) {
         base = __shfl_sync(kFull, base, 0);
         if (!overflow && (uint64_t)base + ns > rs.pool_cap) overflow = true;
         if (overflow) {
-            if (lane == 0) rs.flags[q] |= kFlagFused;
+            // the set outgrew the hash set: widen and run the chunk again next round (the committed
+            // evaluated list E[0, nE) moves to the visit-tag array), else hand off to the fused kernel
+            if (try_widen(p, q, lane)) { if (lane == 0) rs.flags[q] |= kFlagRedo; }
+            else if (lane == 0) rs.flags[q] |= kFlagFused;
             __syncwarp();
             continue;
         }
@@ -566,7 +705,9 @@ __device__ __forceinline__ void pool_sims_step(const float4* __restrict__ x4, co
 #ifndef PFG_SIMS_MINB
 #define PFG_SIMS_MINB 2
 #endif
-__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(QueryParams p, int par) {
+template <typename PP>
+__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
+    const QueryParams& p = deref(pp);
     const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
     const uint32_t top = min(rs.ctl->pool_top[par], rs.pool_cap);
@@ -619,6 +760,56 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(QueryParams p, int 
         const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
         if ((lane & 3) == 0 && b + rr < e1) rs.pool_key[b + rr] = make_key(t1, id_rr);
     }
+    // wide tiles: a provisional id is fresh iff the query's visit-tag array still holds this
+    // visit's tag (no earlier repetition of the chunk passed it); the fresh ids are compacted in
+    // order and their similarities computed (R-2, the same tree); kept = how many of them beat the
+    // k-th key the query held at the start of the chunk (only those can enter its top list)
+    const uint32_t nwt = min(rs.ctl->nwt[par], rs.wcap);
+    for (int64_t aw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; aw < nwt; aw += nw) {
+        const uint32_t w = rs.wtcnt[aw];
+        const uint32_t np_ = w & 0xffu;
+        if (np_ == 0) continue;
+        const int64_t q = rs.wtiles[2 * aw].x;
+        const uint32_t tag = rs.wtiles[2 * aw + 1].z;
+        const uint32_t* W = rs.wv + (int64_t)rs.wslot[q] * p.n;
+        uint32_t* cand = rs.wcand + aw * kTile;
+        uint32_t v[kTile / 32];
+        bool fr[kTile / 32];
+#pragma unroll
+        for (int u = 0; u < kTile / 32; ++u) {
+            const uint32_t o = u * 32 + lane;
+            v[u] = o < np_ ? cand[o] : 0u;
+            fr[u] = o < np_ && __ldcg(W + v[u]) == tag;
+        }
+        __syncwarp();
+        uint32_t nf = 0;
+#pragma unroll
+        for (int u = 0; u < kTile / 32; ++u) {
+            const uint32_t m = __ballot_sync(kFull, fr[u]);
+            if (fr[u]) cand[nf + __popc(m & lanemask_lt())] = v[u];
+            nf += __popc(m);
+        }
+        __syncwarp();
+        const uint64_t kth = rs.tn[q] == p.k_eff ? rs.T[q * p.kt + p.k_eff - 1] : 0ull;
+        uint32_t qoff[kRPI], roff[kRPI], kept = 0;
+#pragma unroll
+        for (int r = 0; r < kRPI; ++r) qoff[r] = (uint32_t)q * (uint32_t)nch;
+        for (uint32_t b0 = 0; b0 < nf; b0 += kRPI) {
+            const uint32_t nrow = min((uint32_t)kRPI, nf - b0);
+            const uint32_t myid = lane < kRPI ? cand[b0 + min((uint32_t)lane, nrow - 1)] : 0u;
+#pragma unroll
+            for (int r = 0; r < kRPI; ++r) roff[r] = __shfl_sync(kFull, myid, r) * (uint32_t)nch;
+            float acc[kRPI];
+            pool_sims_step<true>(x4, qx4, roff, qoff, nch, lane, acc);
+            const float sim = tree_rows<kRPI>(acc, lane);  // lane l: row l >> 2
+            const uint32_t rr = lane >> 2;
+            const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
+            const bool own = (lane & 3) == 0 && rr < nrow;
+            if (own) rs.wsim[aw * kTile + b0 + rr] = sim;
+            kept += __popc(__ballot_sync(kFull, own && make_key(sim, id_rr) > kth));
+        }
+        if (lane == 0) rs.wtcnt[aw] = nf | (w & 0xffff00u) | (kept << 24);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -626,7 +817,14 @@ struct MergeSmem {
     uint64_t cand[32];
 };
 
-__global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
+__device__ __forceinline__ void push_fused(const RoundState& rs, uint32_t q) {
+    if (rs.ctl->loop) push(rs.fused2, &rs.ctl->nfused2, q);
+    else push(rs.fused, &rs.ctl->nfused, q);
+}
+
+template <typename PP>
+__global__ void __launch_bounds__(128, 8) k_merge(PP pp, int par) {
+    const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int per_warp = align16((int)sizeof(MergeSmem)) + 2 * align16(p.kt * 8);
@@ -639,8 +837,19 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nact; a += nw) {
         const int64_t q = act[a];
-        if (rs.flags[q] & kFlagFused) {
-            if (lane == 0) push(rs.fused, &rs.ctl->nfused, (uint32_t)q);
+        const int fl = rs.flags[q];
+        const bool wide = fl & kFlagWide;
+        if (fl & kFlagFused) {
+            if (lane == 0) push_fused(rs, (uint32_t)q);
+            continue;
+        }
+        if (fl & (kFlagDefer | kFlagRedo)) {
+            // the chunk runs again next round (no room for its wide tiles, or the query widened)
+            if (lane == 0) {
+                rs.flags[q] = fl & ~(kFlagDefer | kFlagRedo);
+                push(rs.act[par ^ 1], &rs.ctl->nact[par ^ 1], (uint32_t)q);
+                if (wide) atomicAdd(&rs.ctl->nwide[par ^ 1], 1u);
+            }
             continue;
         }
         const int i = rs.lvl[q], c0 = rs.c0[q];
@@ -649,16 +858,48 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
         for (int t = lane; t < tn; t += 32) T0[t] = rs.T[q * p.kt + t];
         uint64_t* T = T0;
         uint64_t* Tn = T1;
+        // merge one batch of keys (one per lane, 0 = none) into the sorted top list T (rank merge
+        // of the sorted batch, as the fused kernel's merge_range); keys at or below the k-th key
+        // are dropped
+        auto merge_batch = [&](uint64_t key) {
+            const uint64_t kth = (tn == p.k_eff) ? T[p.k_eff - 1] : 0ull;
+            if (key <= kth) key = 0;
+            const uint32_t vm = __ballot_sync(kFull, key != 0);
+            if (vm) {
+                key = warp_sort_desc(key, lane);
+                const int nc = __popc(vm);
+                m->cand[lane] = key;
+                __syncwarp();
+                if (lane < nc) {
+                    int l2 = 0, h2 = tn;
+                    while (l2 < h2) { const int mid = (l2 + h2) >> 1; if (T[mid] > key) l2 = mid + 1; else h2 = mid; }
+                    if (lane + l2 < p.k_eff) Tn[lane + l2] = key;
+                }
+                for (int t = lane; t < tn; t += 32) {
+                    const uint64_t tv = T[t];
+                    int l2 = 0, h2 = nc;
+                    while (l2 < h2) { const int mid = (l2 + h2) >> 1; if (m->cand[mid] > tv) l2 = mid + 1; else h2 = mid; }
+                    if (t + l2 < p.k_eff) Tn[t + l2] = tv;
+                }
+                __syncwarp();
+                tn = min(p.k_eff, tn + nc);
+                uint64_t* tmp = T; T = Tn; Tn = tmp;
+            }
+            __syncwarp();
+        };
         uint32_t* cn = rs.cnt + q * kCnt;
         uint32_t nE = cn[3];
         const uint32_t base = rs.poff[q];
-        // survivors of repetition r are pool entries [end_{r-1}, end_r): per repetition
-        // emitted - filtered - duplicates, in repetition order
-        uint32_t rc0 = 0, rc1 = 0, rc2 = 0;
+        // per repetition: emitted (k_expand), filtered, dups (k_dedupe; wide: counted below)
+        uint32_t rc0 = 0, rc1 = 0, rc2 = 0, rt = 0;
         if (lane < nr) {
             const uint32_t* rc = rs.repcnt + (q * kMaxR + lane) * 3;
             rc0 = rc[0]; rc1 = rc[1]; rc2 = rc[2];
         }
+        if (wide && lane < nr) rt = rs.rtile[q * (kMaxR + 1) + lane];
+        const uint32_t rend = wide ? rs.rtile[q * (kMaxR + 1) + nr] : 0u;
+        // survivors of repetition r are pool entries [end_{r-1}, end_r): per repetition
+        // emitted - filtered - duplicates, in repetition order
         uint32_t end = rc0 - rc1 - rc2;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -666,49 +907,72 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
             if (lane >= off) end += o;
         }
         // stop thresholds of the chunk's repetitions, lane r holds repetition c0 + r's
-        const float thr_r = lane < nr ? __ldg(p.thr + (int64_t)(i - 1) * p.L + c0 + lane) : INFINITY;
+        const float thr_r = (lane < nr && i > 0) ? __ldg(p.thr + (int64_t)(i - 1) * p.L + c0 + lane) : INFINITY;
         __syncwarp();
         int r_stop = -1;
         uint32_t e = 0;
         for (int r = 0; r < nr; ++r) {
-            const uint32_t e2 = __shfl_sync(kFull, end, r);
-            uint64_t nxt = (e + lane < e2) ? rs.pool_key[base + e + lane] : 0ull;
-            for (uint32_t b0 = e; b0 < e2; b0 += 32) {
-                const uint32_t idx = b0 + lane;
-                uint64_t key = nxt;
-                nxt = (idx + 32 < e2) ? rs.pool_key[base + idx + 32] : 0ull;  // prefetch the next batch
-                if (idx < e2 && p.trace_cap > 0) {
-                    const uint32_t pos = nE + (idx - e);
-                    if (pos < (uint32_t)p.trace_cap) p.trace_ids[q * p.trace_cap + pos] = key_id(key);
-                }
-                const uint64_t kth = (tn == p.k_eff) ? T[p.k_eff - 1] : 0ull;
-                if (key <= kth) key = 0;
-                const uint32_t vm = __ballot_sync(kFull, key != 0);
-                if (vm) {
-                    key = warp_sort_desc(key, lane);
-                    const int nc = __popc(vm);
-                    m->cand[lane] = key;
-                    __syncwarp();
-                    if (lane < nc) {
-                        int l2 = 0, h2 = tn;
-                        while (l2 < h2) { const int mid = (l2 + h2) >> 1; if (T[mid] > key) l2 = mid + 1; else h2 = mid; }
-                        if (lane + l2 < p.k_eff) Tn[lane + l2] = key;
+            const uint32_t rnext = __shfl_sync(kFull, rt, (r + 1) & 31);
+            if (!wide) {
+                const uint32_t e2 = __shfl_sync(kFull, end, r);
+                uint64_t nxt = (e + lane < e2) ? rs.pool_key[base + e + lane] : 0ull;
+                for (uint32_t b0 = e; b0 < e2; b0 += 32) {
+                    const uint32_t idx = b0 + lane;
+                    const uint64_t key = nxt;
+                    nxt = (idx + 32 < e2) ? rs.pool_key[base + idx + 32] : 0ull;  // prefetch the next batch
+                    if (idx < e2 && p.trace_cap > 0) {
+                        const uint32_t pos = nE + (idx - e);
+                        if (pos < (uint32_t)p.trace_cap) p.trace_ids[q * p.trace_cap + pos] = key_id(key);
                     }
-                    for (int t = lane; t < tn; t += 32) {
-                        const uint64_t tv = T[t];
-                        int l2 = 0, h2 = nc;
-                        while (l2 < h2) { const int mid = (l2 + h2) >> 1; if (m->cand[mid] > tv) l2 = mid + 1; else h2 = mid; }
-                        if (t + l2 < p.k_eff) Tn[t + l2] = tv;
-                    }
-                    __syncwarp();
-                    tn = min(p.k_eff, tn + nc);
-                    uint64_t* tmp = T; T = Tn; Tn = tmp;
+                    merge_batch(key);
                 }
-                __syncwarp();
+                nE += e2 - e;
+                e = e2;
+            } else {
+                // the repetition's wide tiles in order: fresh ids (in position order) with their
+                // similarities; a tile with nothing above the chunk-start k-th key is skipped unless
+                // the evaluated ids are traced
+                const uint32_t tb = __shfl_sync(kFull, rt, r);
+                const uint32_t te = r + 1 < nr ? rnext : rend;
+                uint32_t fr = 0, pa = 0;
+                for (uint32_t t0 = tb; t0 < te; t0 += 32) {
+                    const uint32_t w = t0 + lane < te ? rs.wtcnt[t0 + lane] : 0u;
+                    const uint32_t nf = w & 0xffu;
+                    uint32_t incl = nf;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const uint32_t o = __shfl_up_sync(kFull, incl, off);
+                        if (lane >= off) incl += o;
+                    }
+                    uint32_t need = __ballot_sync(kFull, nf > 0 && (p.trace_cap > 0 || (w >> 24) > 0));
+                    while (need) {
+                        const int l = __ffs(need) - 1;
+                        need &= need - 1;
+                        const uint32_t cntf = __shfl_sync(kFull, nf, l);
+                        const uint32_t pos0 = nE + fr + __shfl_sync(kFull, incl - nf, l);
+                        const int64_t s0 = (int64_t)(t0 + l) * kTile;
+                        for (uint32_t o = 0; o < cntf; o += 32) {
+                            const uint32_t idx = o + lane;
+                            uint64_t key = 0;
+                            if (idx < cntf) {
+                                const uint32_t id = rs.wcand[s0 + idx];
+                                key = make_key(rs.wsim[s0 + idx], id);
+                                if (p.trace_cap > 0 && pos0 + idx < (uint32_t)p.trace_cap) p.trace_ids[q * p.trace_cap + pos0 + idx] = id;
+                            }
+                            merge_batch(key);
+                        }
+                    }
+                    fr += __shfl_sync(kFull, incl, 31);
+                    uint32_t np_ = (w >> 8) & 0xffu;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) np_ += __shfl_xor_sync(kFull, np_, off);
+                    pa += np_;
+                }
+                nE += fr;
+                if (lane == r) { rc1 = rc0 - pa; rc2 = pa - fr; }
             }
-            nE += e2 - e;
-            e = e2;
             const int j1 = c0 + r + 1;
+            if (i == 0) { r_stop = r; break; }  // the linear scan ends the search (R-13)
             const float th = __shfl_sync(kFull, thr_r, r);
             if (tn == p.k_eff && (!p.per_round || j1 == p.L)) {
                 float ip = key_sim(T[p.k_eff - 1]);
@@ -738,11 +1002,14 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
             }
             if (lane == 0) {
                 if (p.jhist) atomicAdd(p.jhist + min(i == p.K ? c0 + r_stop + 1 : p.L, kJHist - 1), 1u);
+                atomicAdd(&rs.ctl->evsum, (unsigned long long)nE);
+                atomicAdd(&rs.ctl->emsum, (unsigned long long)emitted);
                 if (p.stats) {
                     pfg_query_stats s;
                     s.i_stop = i; s.j_stop = c0 + r_stop + 1; s.emitted = emitted; s.filtered = filtered; s.dups = dups;
                     s.evaluated = nE;
-                    s.flags = (p.k > p.k_eff ? 1u : 0u) | ((p.trace_cap > 0 && nE > (uint32_t)p.trace_cap) ? 4u : 0u);
+                    s.flags = (p.k > p.k_eff ? 1u : 0u) | ((p.trace_cap > 0 && nE > (uint32_t)p.trace_cap) ? 4u : 0u) |
+                              (wide ? 16u : 0u);
                     s.probes = cn[4];
                     p.stats[q] = s;
                 }
@@ -753,26 +1020,84 @@ __global__ void __launch_bounds__(128) k_merge(QueryParams p, int par) {
             uint4* cur = p.cur + q * p.L;
             if (lane < nr) cur[c0 + lane] = rs.pend[q * kMaxR + lane];
             for (int t = lane; t < tn; t += 32) rs.T[q * p.kt + t] = T[t];
+            int ni = i, nc0 = c0 + nr;
+            if (nc0 >= p.L) { ni = i - 1; nc0 = 0; }
             if (lane == 0) {
                 cn[0] = emitted; cn[1] = filtered; cn[2] = dups; cn[3] = nE;
                 rs.tn[q] = tn;
-                int ni = i, nc0 = c0 + nr;
-                if (nc0 >= p.L) { ni = i - 1; nc0 = 0; }
                 rs.lvl[q] = ni;
                 rs.c0[q] = nc0;
-                if (ni == 0) { rs.flags[q] |= kFlagFused; push(rs.fused, &rs.ctl->nfused, (uint32_t)q); }
-                else push(rs.act[par ^ 1], &rs.ctl->nact[par ^ 1], (uint32_t)q);
+            }
+            __syncwarp();
+            // the i = 0 scan runs wide (a query not yet wide widens for it, with the evaluated
+            // list just committed; else the fused kernel takes it)
+            const bool to_wide = ni == 0 && !wide && try_widen(p, q, lane);
+            if (lane == 0) {
+                if (ni == 0 && !wide && !to_wide) { rs.flags[q] |= kFlagFused; push_fused(rs, (uint32_t)q); }
+                else {
+                    push(rs.act[par ^ 1], &rs.ctl->nact[par ^ 1], (uint32_t)q);
+                    if (wide || to_wide) atomicAdd(&rs.ctl->nwide[par ^ 1], 1u);
+                }
             }
         }
         __syncwarp();
     }
 }
 
-// move the still-active queries of list `par` to the fused list (rounds ended)
-__global__ void k_handoff(QueryParams p, int par) {
+// ---------------------------------------------------------------------------------------------
+// After the blind rounds: the device-side round loop (a CUDA graph WHILE node, pfg.cu) and the
+// fused kernel split the queries still running.  The loop keeps them all when there are enough to
+// fill the bulk phases but too few to hide the fused kernel's per-warp latency
+// (lmin <= count <= lmax); otherwise it keeps only the wide queries (the fused kernel cannot resume
+// those) and the fused kernel, launched beside the loop, takes the rest.
+// k_split fills list par ^ 1, which the loop's first round consumes: reset its counters as the
+// k_expand of a round of parity par would
+__global__ void k_presplit(QueryParams p, int par) {
+    RoundCtl* c = p.rs.ctl;
+    const int o = par ^ 1;
+    c->nact[o] = 0; c->pool_top[o] = 0; c->ntiles[o] = 0;
+    for (int t = 0; t < 4; ++t) c->wk[o][t] = 0;
+    c->dfront[o] = 0; c->dback[o] = 0;
+    c->nwt[o] = 0; c->nwide[o] = 0;
+}
+__global__ void k_split(QueryParams p, int par, uint32_t lmin, uint32_t lmax) {
+    const RoundState& rs = p.rs;
+    const uint32_t n = rs.ctl->nact[par];
     const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= p.rs.ctl->nact[par]) return;
-    push(p.rs.fused, &p.rs.ctl->nfused, p.rs.act[par][a]);
+    if (a >= n) return;
+    const uint32_t q = rs.act[par][a];
+    const bool wide = rs.flags[q] & kFlagWide;
+    if ((n >= lmin && n <= lmax) || wide) {
+        push(rs.act[par ^ 1], &rs.ctl->nact[par ^ 1], q);
+        if (wide) atomicAdd(&rs.ctl->nwide[par ^ 1], 1u);
+    } else {
+        push(rs.fused, &rs.ctl->nfused, q);
+    }
+}
+// loop condition: queries left, and either a wide one among them or at least lmin
+__device__ __forceinline__ bool loop_more(const RoundCtl* c, int par, uint32_t lmin) {
+    const uint32_t n = c->nact[par];
+    return n > 0 && (c->nwide[par] > 0 || n >= lmin);
+}
+__global__ void k_loop_begin(RoundCtl* c, int par, cudaGraphConditionalHandle h, uint32_t lmin) {
+    c->loop = 1;
+    c->round = 0;
+    cudaGraphSetConditional(h, loop_more(c, par, lmin) ? 1u : 0u);
+}
+__global__ void k_loop_cond(RoundCtl* c, int par, cudaGraphConditionalHandle h, uint32_t lmin, uint32_t cap) {
+    c->round += 2;
+    cudaGraphSetConditional(h, (loop_more(c, par, lmin) && c->round < cap) ? 1u : 0u);
+}
+// the loop ended: the queries still running go to the second fused launch; a wide query left
+// here (only if the loop hit its round cap) ends with no result (stats flag bit 5)
+__global__ void k_loop_end(QueryParams p, int par) {
+    const RoundState& rs = p.rs;
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= rs.ctl->nact[par]) return;
+    const uint32_t q = rs.act[par][a];
+    if (!(rs.flags[q] & kFlagWide)) { push(rs.fused2, &rs.ctl->nfused2, q); return; }
+    for (int t = 0; t < p.k; ++t) { p.out_ids[(int64_t)q * p.k + t] = -1; p.out_sims[(int64_t)q * p.k + t] = __int_as_float(0x7fc00000); }
+    if (p.stats) { pfg_query_stats s = {}; s.flags = 32u | 16u; p.stats[q] = s; }
 }
 
 }  // namespace pfg

@@ -288,6 +288,7 @@ int tau_of(float ipk, float eps) {
 
 struct SearchCfg {
     int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0, engine = 0, uniform = 0, rounds = 0;
+    int wide = 0;
     float eps = 0.0f;
     uint32_t* trace_ids = nullptr;
 };
@@ -318,6 +319,8 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     if (s.engine < 0 || s.engine > 1) return fail(PFG_E_ARG, "engine must be 0 (rounds + fused) or 1 (fused)");
     s.rounds = z.rounds;
     if (s.rounds < 0 || s.rounds > 4096) return fail(PFG_E_ARG, "rounds must be in [0, 4096]");
+    s.wide = z.wide;
+    if (s.wide < -1 || s.wide > kHMax) return fail(PFG_E_ARG, "wide must be -1, 0 or in [1, 1536]");
     s.uniform = z.uniform_chunks;
     if (s.uniform != 0 && s.uniform != 1) return fail(PFG_E_ARG, "uniform_chunks must be 0 or 1");
     if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
@@ -349,7 +352,23 @@ struct pfg_index {
     // round-engine state (per query, grow-only)
     DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_repcnt, rs_pool_id, rs_pool_q, rs_pool_key,
         rs_ctl, rs_poff, rs_pn, rs_act0, rs_act1, rs_fused, rs_cand, rs_tcnt, rs_dord0, rs_dord1, rs_hsave, rs_rseg, rs_rinfo, rs_tiles, qbnd;
+    // wide queries: visit-tag arrays, wide scan tiles, the second fused list
+    DBuf rs_wv, rs_wslot, rs_wtiles, rs_wcand, rs_wsim, rs_wtcnt, rs_rtile, rs_fused2, rs_params;
+    int64_t wv_slots = 0, wv_n = 0, wv_want = 0;   // visit-tag arrays allocated / wanted
+    int64_t wc_cap = 0, wc_want = 0;               // wide tiles allocated / wanted
+    uint32_t wepoch = 0;         // search epoch of the visit tags (the arrays are reset on wrap)
+    // the device-side round loop: an instantiated CUDA graph with a WHILE node, rebuilt when the
+    // launch parameters change
+    cudaGraphExec_t loop_exec = nullptr;
+    std::vector<unsigned char> loop_key;
+    cudaStream_t cap_st = nullptr;
+    cudaEvent_t ev_split = nullptr, ev_f1 = nullptr, ev_f1a = nullptr, ev_f1b = nullptr;
+    bool f1_timed = false;
     uint32_t* h_ctl = nullptr;   // pinned host mirror of the round control block
+    RoundCtl* h_ctl2 = nullptr;  // [2] pinned copies of each search's final control block (by parity)
+    int64_t nsearch = 0;         // searches of the round engine so far
+    int64_t nq_prev[2] = {0, 0}; // their query counts (by parity)
+    bool loop_heavy = false;     // the last completed search's queries were heavy: keep them all in the loop
     DBuf jhist;                  // stop-depth histogram of the last search (device)
     uint32_t* h_jhist = nullptr; // its pinned host copy
     int eager = 32;              // repetitions hashed eagerly per query (tuned from the last search)
@@ -386,6 +405,7 @@ struct pfg_index {
         for (auto& e : pev)
             if (e) cudaEventDestroy(e);
         if (h_ctl) cudaFreeHost(h_ctl);
+        if (h_ctl2) cudaFreeHost(h_ctl2);
         if (h_jhist) cudaFreeHost(h_jhist);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
@@ -395,6 +415,10 @@ struct pfg_index {
         if (ev_zmin) cudaEventDestroy(ev_zmin);
         if (ev_done) cudaEventDestroy(ev_done);
         if (h_zmin) cudaFreeHost(h_zmin);
+        if (loop_exec) cudaGraphExecDestroy(loop_exec);
+        if (cap_st) cudaStreamDestroy(cap_st);
+        for (cudaEvent_t e : {ev_split, ev_f1, ev_f1a, ev_f1b})
+            if (e) cudaEventDestroy(e);
     }
 };
 
@@ -856,9 +880,18 @@ void tune_eager(pfg_index* I) {
     if (tot) I->eager = std::max(8, std::min(64, e));
 }
 
+// developer aid PFG_DBG_SYNC=1: synchronise after each launch group and name the failing one
+pfg_status dbg_sync(const char* what) {
+    static const bool on = getenv("PFG_DBG_SYNC") != nullptr;
+    if (!on) return PFG_OK;
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return fail(PFG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return PFG_OK;
+}
+
 // phases of pfg_last_phases: 0 expand, 1 scan, 2 dedupe, 3 sims, 4 merge, 5 fused kernel,
 // 6 other query-phase work (round control, query order, code extension)
-enum { kPhExpand = 0, kPhScan, kPhDedupe, kPhSims, kPhMerge, kPhFused, kPhOther, kPhEnd = -1 };
+enum { kPhExpand = 0, kPhScan, kPhDedupe, kPhSims, kPhMerge, kPhFused, kPhOther, kPhLoop, kPhEnd = -1 };
 pfg_status phase_mark(pfg_index* I, bool on, int kind, cudaStream_t st) {
     if (!on) return PFG_OK;
     if (I->pev_n == (int)I->pev.size()) {
@@ -879,6 +912,13 @@ pfg_status phase_collect(pfg_index* I) {
         if (I->pkind[i] >= 0) I->last_phase_ms[I->pkind[i]] += ms;
     }
     I->pev_n = 0;
+    if (I->f1_timed) {
+        // the first fused launch ran on the aux stream beside the loop
+        float ms = 0.0f;
+        PFG_CUDA(cudaEventElapsedTime(&ms, I->ev_f1a, I->ev_f1b));
+        I->last_phase_ms[kPhFused] += ms;
+        I->f1_timed = false;
+    }
     return PFG_OK;
 }
 
@@ -1044,6 +1084,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         if (cudaEventQuery(I->ev_done) == cudaSuccess) {
             I->done_pending = false;
             tune_eager(I);
+
         } else {
             cudaGetLastError();
         }
@@ -1097,6 +1138,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     const int ecap = 2048;  // evaluated-list stride: kHMax committed + one batch of slack
     const int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
     const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
+    int64_t wide_max = 0;   // visit-tag arrays this search may use
     if (rounds) {
         const size_t N = (size_t)nq;
         PFG_TRY(I->rs_lvl.ensure(N * 4, "rs")); PFG_TRY(I->rs_c0.ensure(N * 4, "rs"));
@@ -1114,7 +1156,54 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_TRY(I->rs_tcnt.ensure(N * (ccap / kTile) * 4, "rs tile counts"));
         PFG_TRY(I->rs_dord0.ensure(N * 4, "rs")); PFG_TRY(I->rs_dord1.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_rinfo.ensure(N * 16, "rs")); PFG_TRY(I->rs_tiles.ensure(N * (ccap / kTile) * 32, "rs tiles"));
-        if (!I->h_ctl) PFG_CUDA(cudaMallocHost(&I->h_ctl, sizeof(RoundCtl)));
+        PFG_TRY(I->rs_fused2.ensure(N * 4, "rs")); PFG_TRY(I->rs_wslot.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_rtile.ensure(N * (kMaxR + 1) * 4, "rs"));
+        if (!I->h_ctl) {
+            PFG_CUDA(cudaMallocHost(&I->h_ctl, sizeof(RoundCtl)));
+            std::memset(I->h_ctl, 0, sizeof(RoundCtl));
+        }
+        if (!I->aux) {
+            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
+            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux2, cudaStreamNonBlocking));
+        }
+        if (!I->ev_split) {
+            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_split, cudaEventDisableTiming));
+            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_f1, cudaEventDisableTiming));
+            PFG_CUDA(cudaEventCreate(&I->ev_f1a));
+            PFG_CUDA(cudaEventCreate(&I->ev_f1b));
+        }
+        // wide queries (kernels_rounds.cuh): visit-tag arrays (n words each, PFG_WIDE_MIB of them
+        // at most, default 8 GiB) and wide scan tiles, sized grow-only from what the previous
+        // search wanted; visit s = (K - i) L + j + 1 must fit 16 bits
+        const int64_t per = 4 * g.n;
+        const int64_t wmib = getenv("PFG_WIDE_MIB") ? atoll(getenv("PFG_WIDE_MIB")) : 8192;
+        wide_max = std::max<int64_t>(1, (wmib << 20) / per);
+        if (s.wide >= 0 && (int64_t)(g.K + 1) * g.L < 65536) {
+            const int64_t smax = wide_max;
+            const int64_t want = std::min<int64_t>(smax, std::max<int64_t>(I->wv_want, std::max<int64_t>(1, (512ll << 20) / per)));
+            if (want > I->wv_slots || I->wv_n != g.n) {
+                PFG_TRY(I->rs_wv.alloc((size_t)want * per, "visit tags"));
+                PFG_CUDA(cudaMemsetAsync(I->rs_wv.p, 0xff, (size_t)want * per, st));
+                I->wv_slots = want;
+                I->wv_n = g.n;
+                I->wepoch = 0;
+            }
+            const int64_t wmin = (int64_t)s.R * ((g.n + kTile - 1) / kTile + 2);
+            // (developer knob PFG_WCAP_MIN=1: the minimum, so that wide chunks compete and defer)
+            const int64_t wc0 = getenv("PFG_WCAP_MIN") ? 0 : (int64_t)1 << 18;
+            const int64_t wc = std::max<int64_t>(wmin, std::max<int64_t>(I->wc_want, wc0));
+            if (wc > I->wc_cap || (getenv("PFG_WCAP_MIN") && wc != I->wc_cap)) {
+                PFG_TRY(I->rs_wtiles.alloc((size_t)wc * 32, "wide tiles"));
+                PFG_TRY(I->rs_wcand.alloc((size_t)wc * kTile * 4, "wide candidates"));
+                PFG_TRY(I->rs_wsim.alloc((size_t)wc * kTile * 4, "wide similarities"));
+                PFG_TRY(I->rs_wtcnt.alloc((size_t)wc * 4, "wide tile counts"));
+                I->wc_cap = wc;
+            }
+            if (++I->wepoch >= 0xFFFEu) {
+                PFG_CUDA(cudaMemsetAsync(I->rs_wv.p, 0xff, (size_t)I->wv_slots * per, st));
+                I->wepoch = 1;
+            }
+        }
     }
     PFG_TRY(I->work.ensure(8, "work counter"));
     PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
@@ -1201,17 +1290,33 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         r.tcnt = I->rs_tcnt.as<uint32_t>();
         r.dord[0] = I->rs_dord0.as<uint32_t>(); r.dord[1] = I->rs_dord1.as<uint32_t>(); r.rinfo = I->rs_rinfo.as<uint4>();
         r.tiles = I->rs_tiles.as<uint4>();
+        r.fused2 = I->rs_fused2.as<uint32_t>();
+        r.wslot = I->rs_wslot.as<uint32_t>();
+        r.rtile = I->rs_rtile.as<uint32_t>();
+        // wide queries: on when asked for (wide > 0, or the developer knob PFG_LOOP_MAX), else
+        // automatic: on iff the previous search's queries were heavy (loop_heavy); off, a query
+        // beyond the hash set goes to the fused kernel's bitmap mode
+        const bool wide_on = (s.wide > 0 || (s.wide == 0 && (I->loop_heavy || getenv("PFG_LOOP_MAX")))) && I->wv_slots > 0 &&
+                             I->wv_n == g.n && (int64_t)(g.K + 1) * g.L < 65536;
+        r.wv = wide_on ? I->rs_wv.as<uint32_t>() : nullptr;
+        r.wslots = wide_on ? (uint32_t)std::min<int64_t>(I->wv_slots, wide_max) : 0u;
+        r.wtiles = I->rs_wtiles.as<uint4>(); r.wcand = I->rs_wcand.as<uint32_t>(); r.wsim = I->rs_wsim.as<float>();
+        r.wtcnt = I->rs_wtcnt.as<uint32_t>();
+        r.wcap = wide_on ? (uint32_t)I->wc_cap : 0u;
+        r.hmax = s.wide > 0 ? (uint32_t)s.wide : (uint32_t)kHMax;
         PFG_CUDA(cudaMemsetAsync(r.ctl, 0, sizeof(RoundCtl), st));
-        k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p);
+        k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, (uint32_t)(0xFFFEu - I->wepoch) << 16);
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
         const size_t esm = (size_t)expand_smem_bytes(g.dpad, lazy) * 4;
         const size_t dsm = (size_t)align16((int)sizeof(DedupeSmem)) * 4;
         const size_t msm = (size_t)(align16((int)sizeof(MergeSmem)) + 2 * align16(kt * 8)) * 4;
-        PFG_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
-        PFG_CUDA(cudaFuncSetAttribute(k_dedupe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        PFG_CUDA(cudaFuncSetAttribute(k_merge<QueryParams>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+        PFG_CUDA(cudaFuncSetAttribute(k_dedupe<QueryParams>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        PFG_CUDA(cudaFuncSetAttribute(k_merge<const QueryParams*>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+        PFG_CUDA(cudaFuncSetAttribute(k_dedupe<const QueryParams*>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         int docc = 1;
-        PFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, k_dedupe, 128, dsm));
+        PFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, k_dedupe<QueryParams>, 128, dsm));
         // grids: warp per active query (at most one resident wave; the kernels stride over the
         // device-side counts, so no host synchronisation is needed between rounds)
         const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * 16));
@@ -1221,56 +1326,167 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const unsigned sb = (unsigned)(I->num_sms * PFG_SIMS_MINB);
         int round = 0;
         const bool tm = s.timing >= 2;
+        // one round: expand, scan, dedupe, sims, merge of list `par` (phase events unless captured)
+        auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp) -> pfg_status {
+            using PP = decltype(pp);
+            PFG_TRY(phase_mark(I, marks, kPhExpand, rst));
+            switch (epl) {
+                case 1: k_expand<1, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
+                case 2: k_expand<2, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
+                case 4: k_expand<4, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
+                case 8: k_expand<8, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
+                case 16: k_expand<16, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
+                default: k_expand<32, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
+            }
+            if (rst == st) PFG_TRY(dbg_sync("k_expand"));
+            PFG_TRY(phase_mark(I, marks, kPhScan, rst));
+            k_scan<PP><<<tb_s, 256, 0, rst>>>(pp, par);
+            if (rst == st) PFG_TRY(dbg_sync("k_scan"));
+            PFG_TRY(phase_mark(I, marks, kPhDedupe, rst));
+            k_dedupe<PP><<<qb_d, 128, dsm, rst>>>(pp, par);
+            if (rst == st) PFG_TRY(dbg_sync("k_dedupe"));
+            PFG_TRY(phase_mark(I, marks, kPhSims, rst));
+            k_sims<PP><<<sb, 256, 0, rst>>>(pp, par);
+            if (rst == st) PFG_TRY(dbg_sync("k_sims"));
+            PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
+            k_merge<PP><<<qb_m, 128, msm, rst>>>(pp, par);
+            if (rst == st) PFG_TRY(dbg_sync("k_merge"));
+            PFG_TRY(phase_mark(I, marks, kPhOther, rst));
+            PFG_CUDA(cudaGetLastError());
+            return PFG_OK;
+        };
         while (round < max_rounds) {
-            const int par = round & 1;
             // round 0 is the single repetition 0 with tau = 64 (no sketches read); round 1 reaches
             // repetitions < 1 + R; later rounds may reach every eager repetition
             if (round == 1) PFG_TRY(join_sketches(I, st));
             if (round == 2) PFG_TRY(late_join(I, st));
-            PFG_TRY(phase_mark(I, tm, kPhExpand, st));
-            switch (epl) {
-                case 1: k_expand<1><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 2: k_expand<2><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 4: k_expand<4><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 8: k_expand<8><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
-                case 16: k_expand<16><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
-                default: k_expand<32><<<qb_e, 128, esm, st>>>(p, par, lazy ? 1 : 0); break;
-            }
-            PFG_TRY(phase_mark(I, tm, kPhScan, st));
-            k_scan<<<tb_s, 256, 0, st>>>(p, par);
-            PFG_TRY(phase_mark(I, tm, kPhDedupe, st));
-            k_dedupe<<<qb_d, 128, dsm, st>>>(p, par);
-            PFG_TRY(phase_mark(I, tm, kPhSims, st));
-            k_sims<<<sb, 256, 0, st>>>(p, par);
-            PFG_TRY(phase_mark(I, tm, kPhMerge, st));
-            k_merge<<<qb_m, 128, msm, st>>>(p, par);
-            PFG_TRY(phase_mark(I, tm, kPhOther, st));
-            PFG_CUDA(cudaGetLastError());
+            PFG_TRY(launch_round(round & 1, st, tm, p));
             I->launches += 5;
             ++round;
         }
-        // no host synchronisation: the queries still running join the fused list on the device,
-        // and the kernels below take their counts from device memory
-        k_handoff<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, round & 1);
+        PFG_TRY(join_sketches(I, st));
+        PFG_TRY(late_join(I, st));
+        // no host synchronisation from here on: the queries still running are split on the device
+        // between the device-side round loop and the fused kernel (k_split), whose first launch
+        // runs on the aux stream beside the loop
+        const int P = round & 1;
+        const char* e_lmin = getenv("PFG_LOOP_MIN");
+        const char* e_lmax = getenv("PFG_LOOP_MAX");
+        const uint32_t lmin = e_lmin ? (uint32_t)atol(e_lmin) : 64u;
+        // default: the loop keeps only the wide queries (a query beyond the hash set early in the
+        // search), unless the previous search's queries were heavy (loop_heavy); queries that are
+        // merely long run faster in the fused kernel (measured)
+        const uint32_t lmax = e_lmax ? (uint32_t)atol(e_lmax) : (I->loop_heavy ? 0xffffffffu : 0u);
+        const bool loop_on = r.wslots > 0 || lmax > 0;
+        const unsigned gq = (unsigned)((nq + 255) / 256);
+        k_presplit<<<1, 1, 0, st>>>(p, P);
+        k_split<<<gq, 256, 0, st>>>(p, P, lmin, lmax);
         PFG_CUDA(cudaGetLastError());
-        I->launches += 1;
-        p.qlist = r.fused;
-        p.nq_dev = &r.ctl->nfused;
-        p.resume = 1;
-        I->last_rounds = round;
-        // the queries the fused kernel resumes get codes and match ranges for kExtReps more
-        // repetitions in bulk (they would otherwise hash and search them one warp at a time)
-        if (lazy && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
-            const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
-            PFG_TRY(late_join(I, st));
-            PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, st, &r.ctl->nfused));
-            const int64_t thr_n = nq * (int64_t)nr;
-            k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.fused, nq, r0, nr,
-                                                                       &r.ctl->nfused);
-            PFG_CUDA(cudaGetLastError());
+        PFG_TRY(dbg_sync("k_split"));
+        I->launches += 2;
+        PFG_CUDA(cudaEventRecord(I->ev_split, st));
+        PFG_CUDA(cudaStreamWaitEvent(I->aux, I->ev_split, 0));
+        {
+            QueryParams p1 = p;
+            p1.qlist = r.fused;
+            p1.nq_dev = &r.ctl->nfused;
+            p1.resume = 1;
+            // the queries the fused kernel resumes get codes and match ranges for kExtReps more
+            // repetitions in bulk (they would otherwise hash and search them one warp at a time)
+            if (lazy && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+                const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
+                PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, I->aux, &r.ctl->nfused));
+                const int64_t thr_n = nq * (int64_t)nr;
+                k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, I->aux>>>(p1, I->qbnd.as<uint4>(), r.fused, nq, r0,
+                                                                              nr, &r.ctl->nfused);
+                PFG_CUDA(cudaGetLastError());
+                I->launches += 2;
+                p1.qc_n = p1.qb_n = I->qc_ld;
+            }
+            PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, I->aux));
+            const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, max_blocks));
+            switch (epl) {
+                case 1: PFG_TRY(launch_query_t<1>(p1, (int)blocks, smem, I->aux)); break;
+                case 2: PFG_TRY(launch_query_t<2>(p1, (int)blocks, smem, I->aux)); break;
+                case 4: PFG_TRY(launch_query_t<4>(p1, (int)blocks, smem, I->aux)); break;
+                case 8: PFG_TRY(launch_query_t<8>(p1, (int)blocks, smem, I->aux)); break;
+                case 16: PFG_TRY(launch_query_t<16>(p1, (int)blocks, smem, I->aux)); break;
+                default: PFG_TRY(launch_query_t<32>(p1, (int)blocks, smem, I->aux)); break;
+            }
             I->launches += 1;
-            p.qc_n = p.qb_n = I->qc_ld;
+            PFG_TRY(dbg_sync("fused 1"));
+            PFG_CUDA(cudaEventRecord(I->ev_f1, I->aux));
         }
+        // the device-side loop: a CUDA graph whose WHILE node runs two rounds per iteration
+        // (lists P^1 then P) while loop_more holds (kernels_rounds.cuh); built once per launch
+        // configuration
+        PFG_TRY(phase_mark(I, tm, kPhLoop, st));
+        if (loop_on) {
+            // the loop's kernels read the search's parameters from device memory (k_setp), so the
+            // graph depends only on the launch geometry
+            const uint32_t cap = (uint32_t)std::min<int64_t>(1 << 30, 8 * (int64_t)(g.K + 1) * g.L + 64);
+            PFG_TRY(I->rs_params.ensure(sizeof(QueryParams), "loop parameters"));
+            const QueryParams* dp = I->rs_params.as<QueryParams>();
+            k_setp<<<1, 1, 0, st>>>(p, I->rs_params.as<QueryParams>());
+            PFG_CUDA(cudaGetLastError());
+            std::vector<unsigned char> key(96);
+            const int64_t extra[12] = {P, lmin, cap, epl, (int64_t)qb_e << 32 | qb_d, (int64_t)qb_m << 32 | tb_s,
+                                       (int64_t)sb << 32 | (lazy ? 1 : 0), (int64_t)esm << 40 | (int64_t)dsm << 20 | (int64_t)msm,
+                                       (int64_t)(uintptr_t)dp, (int64_t)(uintptr_t)r.ctl, 0, 0};
+            std::memcpy(key.data(), extra, sizeof(extra));
+            if (!I->loop_exec || key != I->loop_key) {
+                if (I->loop_exec) { cudaGraphExecDestroy(I->loop_exec); I->loop_exec = nullptr; }
+                if (!I->cap_st) PFG_CUDA(cudaStreamCreateWithFlags(&I->cap_st, cudaStreamNonBlocking));
+                cudaGraph_t gr;
+                PFG_CUDA(cudaGraphCreate(&gr, 0));
+                cudaGraphConditionalHandle h;
+                PFG_CUDA(cudaGraphConditionalHandleCreate(&h, gr, 0, 0));
+                PFG_CUDA(cudaStreamBeginCaptureToGraph(I->cap_st, gr, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+                k_loop_begin<<<1, 1, 0, I->cap_st>>>(r.ctl, P ^ 1, h, lmin);
+                PFG_CUDA(cudaStreamEndCapture(I->cap_st, &gr));
+                size_t nn = 1;
+                cudaGraphNode_t n0;
+                PFG_CUDA(cudaGraphGetNodes(gr, &n0, &nn));
+                cudaGraphNodeParams cp = {};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = h;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t cn;
+                PFG_CUDA(cudaGraphAddNode(&cn, gr, &n0, 1, &cp));
+                cudaGraph_t body = cp.conditional.phGraph_out[0];
+                PFG_CUDA(cudaStreamBeginCaptureToGraph(I->cap_st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+                pfg_status ls = launch_round(P ^ 1, I->cap_st, false, dp);
+                if (ls == PFG_OK) ls = launch_round(P, I->cap_st, false, dp);
+                k_loop_cond<<<1, 1, 0, I->cap_st>>>(r.ctl, P ^ 1, h, lmin, cap);
+                cudaGraph_t body_out = body;
+                const cudaError_t ce = cudaStreamEndCapture(I->cap_st, &body_out);
+                if (ls != PFG_OK) { cudaGraphDestroy(gr); return ls; }
+                if (ce != cudaSuccess) { cudaGraphDestroy(gr); PFG_CUDA(ce); }
+                const cudaError_t ie = cudaGraphInstantiate(&I->loop_exec, gr, 0);
+                cudaGraphDestroy(gr);
+                PFG_CUDA(ie);
+                I->loop_key = key;
+            }
+            PFG_CUDA(cudaGraphLaunch(I->loop_exec, st));
+            PFG_TRY(dbg_sync("round loop graph"));
+            I->launches += 1;
+        }
+        if (loop_on) {
+            k_loop_end<<<gq, 256, 0, st>>>(p, P ^ 1);
+            PFG_CUDA(cudaGetLastError());
+            PFG_TRY(dbg_sync("k_loop_end"));
+            I->launches += 1;
+        }
+        // the fused kernel's first launch (beside the loop) ends here; a second launch takes the
+        // queries the loop handed off (only when the loop keeps non-wide queries, PFG_LOOP_MAX)
+        PFG_TRY(phase_mark(I, tm, kPhFused, st));
+        PFG_CUDA(cudaStreamWaitEvent(st, I->ev_f1, 0));
+        p.qlist = r.fused2;
+        p.nq_dev = &r.ctl->nfused2;
+        p.resume = 1;
+        if (lmax == 0) fused_n = 0;
+        I->last_rounds = round;
     }
     if (!rounds && p.qb_n > 0 && nq > 1 && getenv("PFG_ORDER")) {
         // longest-first order by the entries the first repetitions' match ranges hold
@@ -1319,6 +1535,15 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // the stop-depth histogram for the next search's eager depth, and the end-of-search event that
     // orders the next search's use of the scratch buffers (on any stream)
     PFG_CUDA(cudaMemcpyAsync(I->h_jhist, I->jhist.p, kJHist * 4, cudaMemcpyDeviceToHost, st));
+    if (rounds) {
+        if (!I->h_ctl2) {
+            PFG_CUDA(cudaMallocHost(&I->h_ctl2, 2 * sizeof(RoundCtl)));
+            std::memset(I->h_ctl2, 0, 2 * sizeof(RoundCtl));
+        }
+        PFG_CUDA(cudaMemcpyAsync(I->h_ctl2 + (I->nsearch & 1), I->rs_ctl.p, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+        I->nq_prev[I->nsearch & 1] = nq;
+        ++I->nsearch;
+    }
     PFG_CUDA(cudaEventRecord(I->ev_done, st));
     I->done_pending = true;
     // with device outputs the call returns without waiting for the GPU; host outputs (or the
@@ -1328,7 +1553,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     if (phase_prof) {
         if (rounds) {
             PFG_CUDA(cudaMemcpy(I->h_ctl, I->rs_ctl.p, sizeof(RoundCtl), cudaMemcpyDeviceToHost));
-            fused_n = I->h_ctl[4];
+            const RoundCtl* c = reinterpret_cast<const RoundCtl*>(I->h_ctl);
+            fused_n = (int64_t)c->nfused + c->nfused2;
+            fprintf(stderr, "[pfg phase] loop: %u rounds, wide arrays used %u of %lld, wide deferrals %u, fused beside the loop %u, after it %u\n",
+                    c->round, c->wnext, (long long)I->wv_slots, c->wdefer, c->nfused, c->nfused2);
         }
         fprintf(stderr, "[pfg phase] engine %d: rounds %d, queries finished by the fused kernel %lld of %lld\n", s.engine,
                 I->last_rounds, (long long)fused_n, (long long)nq);
@@ -1346,6 +1574,18 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     }
     I->last_launches = I->launches;
     PFG_CUDA(cudaEventSynchronize(I->ev_zmin));  // recorded right after the normalisation
+    if (rounds && I->nsearch >= 2) {
+        // the previous search is complete (it precedes this one's normalisation on the stream):
+        // size the wide-query scratch of the next searches from what it wanted
+        const RoundCtl* c = I->h_ctl2 + ((I->nsearch - 2) & 1);
+        if ((int64_t)c->wnext > I->wv_slots) I->wv_want = std::max<int64_t>(I->wv_want, 2 * (int64_t)c->wnext);
+        if (c->wdefer) I->wc_want = std::min<int64_t>((int64_t)1 << 22, std::max<int64_t>(I->wc_want, 2 * I->wc_cap));
+        // heavy queries (bytes a query reads: evaluated rows + emitted table entries, averaged over
+        // the previous search) run faster in the bulk rounds than one warp each in the fused kernel
+        const int64_t nprev = std::max<int64_t>(1, I->nq_prev[(I->nsearch - 2) & 1]);
+        const double bytes = ((double)c->evsum * g.dpad * 4 + (double)c->emsum * 16) / (double)nprev;
+        I->loop_heavy = bytes >= 64.0 * (1 << 20);
+    }
     if (*I->h_zmin != ~0ull)
         return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(*I->h_zmin) + " is a zero vector");
     return PFG_OK;

@@ -116,6 +116,11 @@ CONFIGS = {
             family="simhash", strategy="pool", reps=0, budget=16 << 30),
     5: dict(name="scaleout-100Mx100", n=100_000_000, d=100, nq=100_000, k=10, recall=0.9,
             family="fht_cp", strategy="independent", reps=0, budget=120 << 30, shard_n=12_500_000),
+    # the paper's own SYNTHETIC set (n = 10^6, d = 100 -> vectors in R^300; every
+    # query's nearest neighbour is the last row), with the paper's default pooled evaluation
+    # and FHT-CP; not a BASELINE config, a second workload
+    6: dict(name="paper-synthetic-1Mx300", n=1_000_000, d=300, nq=1_000, k=10, recall=0.9,
+            family="fht_cp", strategy="pool", reps=0, budget=8 << 30),
 }
 
 
@@ -138,4 +143,8 @@ def config_data(cfg: int, n: int | None = None, nq: int | None = None, row0: int
     if cfg == 5:
         return (mixture(n, 100, 10_000, 0.3, 105, row0, stream=2),
                 mixture(nq, 100, 10_000, 0.3, 105, 0, stream=3))
+    if cfg == 6:
+        if row0:
+            raise ValueError("config 6 is generated whole (its last row is the common nearest neighbour)")
+        return paper_synthetic(n, 100, nq, 106)
     raise KeyError(cfg)

@@ -116,7 +116,7 @@ def _recall(x_t, q_t, ids, k):
     return float(np.mean(ex >= kth[:, None] - 1e-5))
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("cfg", [3, 4, 6])
 def test_config34_full(cfg):
     c = synth.CONFIGS[cfg]
     data, q = synth.config_data(cfg)
@@ -126,7 +126,8 @@ def test_config34_full(cfg):
     L = g.info["reps"]
     assert L == pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
     strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
-    o = O.OracleIndex(data, O.HP, L=L, seed=1, strategy=strat, lazy=True)
+    fam = O.HP if c["family"] == "simhash" else O.FHTCP
+    o = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
     # build side: data, slots, pool selections, two whole repetition tables with their inline
     # sketch words, prefix tables
     assert np.array_equal(g.export_data().view(np.uint32), o.data().view(np.uint32))

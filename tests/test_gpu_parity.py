@@ -201,6 +201,70 @@ def test_round_engine_handoff_midway(cases, rounds):
         _compare(cases[name], 10, 0.99, dict(rep_chunk=4, engine=0, rounds=rounds), dict(rep_chunk=4))
 
 
+# ------------------------------------------------------------------ wide queries, device-side loop
+# A query whose evaluated set outgrows `wide` ids moves it to a visit-tag array and continues in the
+# device-side round loop (a CUDA graph WHILE node).  By default the loop keeps only the wide queries;
+# PFG_LOOP_MIN=1 with a large PFG_LOOP_MAX keeps every query still running after the blind rounds.
+@pytest.mark.parametrize("name", ["hp", "fht", "hp_pool", "fht_long"])
+@pytest.mark.parametrize("wide", [1, 64])
+@pytest.mark.parametrize("recall", [0.9, 0.99])
+@pytest.mark.parametrize("R", [4, 16])
+@pytest.mark.parametrize("keep_all", [False, True])
+def test_search_parity_wide(cases, name, wide, recall, R, keep_all, monkeypatch):
+    if keep_all:
+        monkeypatch.setenv("PFG_LOOP_MIN", "1")
+        monkeypatch.setenv("PFG_LOOP_MAX", "1000000")
+    st = _compare(cases[name], 10, recall, dict(rep_chunk=R, wide=wide), dict(rep_chunk=R))
+    if keep_all or wide == 1:
+        assert np.any(st["flags"] & 16), "no query went wide"
+
+
+@pytest.mark.parametrize("rounds", [1, 2, 5])
+@pytest.mark.parametrize("k", [1, 33])
+def test_search_parity_loop_and_wide_mixed(cases, rounds, k, monkeypatch):
+    # the loop keeps all queries; some widen, some stay in the hash set (and may be handed to the
+    # fused kernel's second launch)
+    monkeypatch.setenv("PFG_LOOP_MIN", "1")
+    monkeypatch.setenv("PFG_LOOP_MAX", "1000000")
+    for name in ("hp", "fht", "fht_long"):
+        _compare(cases[name], k, 0.99, dict(rep_chunk=4, rounds=rounds, wide=200), dict(rep_chunk=4))
+
+
+def test_search_parity_wide_beside_fused(cases, monkeypatch):
+    # the loop keeps only the wide queries (count above PFG_LOOP_MAX); the others run in the fused
+    # kernel launched beside it on the aux stream
+    monkeypatch.setenv("PFG_LOOP_MAX", "1")
+    st = _compare(cases["fht"], 10, 0.99, dict(rep_chunk=8, rounds=2, wide=40), dict(rep_chunk=8))
+    assert np.any(st["flags"] & 16) and np.any(~st["flags"] & 16)
+
+
+def test_search_parity_wide_deferrals(cases, monkeypatch):
+    # wide tile buffer at its minimum (one chunk's worth): chunks wait for room in later rounds
+    monkeypatch.setenv("PFG_LOOP_MIN", "1")
+    monkeypatch.setenv("PFG_LOOP_MAX", "1000000")
+    monkeypatch.setenv("PFG_WCAP_MIN", "1")
+    for name in ("hp", "fht_long"):
+        _compare(cases[name], 10, 0.99, dict(rep_chunk=8, wide=1), dict(rep_chunk=8))
+
+
+def test_search_parity_wide_arrays_exhausted(cases, monkeypatch):
+    # one visit-tag array: the first query to widen takes it, the others go to the fused kernel
+    monkeypatch.setenv("PFG_LOOP_MIN", "1")
+    monkeypatch.setenv("PFG_WIDE_MIB", "0")
+    st = _compare(cases["fht"], 10, 0.99, dict(rep_chunk=8, wide=16), dict(rep_chunk=8))
+    assert np.sum((st["flags"] & 16) != 0) == 1
+
+
+@pytest.mark.parametrize("wide", [0, 1])
+def test_exhaustive_search_in_the_loop(cases, wide, monkeypatch):
+    # recall 1: every query reaches the i = 0 linear scan, which runs as wide tiles in the loop
+    monkeypatch.setenv("PFG_LOOP_MIN", "1")
+    monkeypatch.setenv("PFG_LOOP_MAX", "1000000")
+    c = cases["hp"]
+    st = _compare(c, 10, 1.0, dict(rep_chunk=8, wide=wide), dict(rep_chunk=8))
+    assert np.all(st["i_stop"] == 0) and np.all(st["flags"] & 16)
+
+
 @pytest.mark.parametrize("name", ["hp", "fht"])
 @pytest.mark.parametrize("kw", [dict(use_filter=False), dict(stop_rule=1), dict(per_round=True),
                                 dict(segment=1), dict(segment=5, rep_chunk=3), dict(eps=0.2), dict(eps=-0.2),
