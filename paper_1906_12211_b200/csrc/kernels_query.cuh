@@ -215,6 +215,35 @@ __device__ __forceinline__ uint32_t rep_lower_bound(const QueryParams& p, int j,
     return lo;
 }
 
+// R-12 segment widening of one side of repetition j's emitted range at level i < K: the oracle's
+// loop (step B outward while the boundary entry shares the query's i-bit prefix) after its first
+// probe, which settles the common case, continues in closed form: the prefix range end a_i / b_i
+// from the prefix table and a bucket search (O(1) for i <= 13), then
+//   left  e' = e - B*ceil((e - a_i)/B), or 0 if that is <= 0
+//   right e' = min(n, e + B*ceil((b_i - e)/B))
+// -- the loop's positions, since the entries sharing the prefix are exactly [a_i, b_i).
+__device__ __forceinline__ uint32_t widen_side(const QueryParams& p, int j, int i, uint32_t code, uint32_t e, bool left,
+                                               uint32_t& probes) {
+    const Entry* tj = p.tab + (int64_t)j * p.n;
+    const int sh = p.K - i;
+    const uint32_t qp = code >> sh;
+    const uint32_t B = (uint32_t)p.B, n = (uint32_t)p.n;
+    if (left) {
+        if (e == 0) return 0u;
+        ++probes;
+        if ((entry_code(tj + e - 1) >> sh) != qp) return e;
+        const uint32_t a = rep_lower_bound(p, j, (uint64_t)qp << sh, probes);
+        const uint64_t m = (e - a + B - 1) / B;
+        return (uint64_t)B * m >= e ? 0u : e - (uint32_t)(B * m);
+    }
+    if (e >= n) return n;
+    ++probes;
+    if ((entry_code(tj + e) >> sh) != qp) return e;
+    const uint32_t b = rep_lower_bound(p, j, ((uint64_t)qp + 1) << sh, probes);
+    const uint64_t v = (uint64_t)e + (uint64_t)B * ((b - e + B - 1) / B);
+    return v > n ? n : (uint32_t)v;
+}
+
 struct QState {
     int tn;               // entries in T (<= k_eff)
     uint32_t nE;          // evaluated (merged) ids
@@ -564,26 +593,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                         w.f->bnd[task] = rep_lower_bound(p, j, left ? (uint64_t)qc : (uint64_t)qc + 1, st.probes);
                     } else {
                         const uint4 cu = cur[j];
-                        const uint32_t qp = cu.x >> (p.K - i);
-                        const Entry* tj = p.tab + (int64_t)j * p.n;
-                        const uint32_t B = (uint32_t)p.B;
-                        if (left) {
-                            uint32_t e = cu.y;
-                            while (e > 0) {
-                                ++st.probes;
-                                if ((entry_code(tj + e - 1) >> (p.K - i)) != qp) break;
-                                e = e > B ? e - B : 0u;
-                            }
-                            w.f->bnd[task] = e;
-                        } else {
-                            uint32_t e = cu.z;
-                            while (e < (uint32_t)p.n) {
-                                ++st.probes;
-                                if ((entry_code(tj + e) >> (p.K - i)) != qp) break;
-                                e = (uint64_t)e + B < (uint64_t)p.n ? e + B : (uint32_t)p.n;
-                            }
-                            w.f->bnd[task] = e;
-                        }
+                        w.f->bnd[task] = widen_side(p, j, i, cu.x, left ? cu.y : cu.z, left, st.probes);
                         if (left) w.f->qc[r] = cu.x;
                     }
                 }

@@ -171,7 +171,8 @@ __global__ void k_rinit(QueryParams p, uint32_t wtag) {
 // ---------------------------------------------------------------------------------------------
 // k_expand: warp per active query.  The chunk (chunk_reps), its tau, the query codes of the chunk
 // (precomputed, or hashed here), the emitted ranges of every repetition (level K: the match range
-// rounded up to whole segments; deeper levels: the segment loop, R-12), the pending cursors, and
+// rounded up to whole segments; deeper levels: the segment loop, R-12, in closed form after its
+// first probe, widen_side), the pending cursors, and
 // the scan tiles of 128 positions (positions in (repetition, position) order).
 struct ExpandSmem {
     uint32_t qc[kMaxR], bnd[2 * kMaxR];
@@ -237,27 +238,8 @@ __global__ void __launch_bounds__(128) k_expand(PP pp, int par, int lazy) {
                 c->bnd[task] = rep_lower_bound(p, j, left ? (uint64_t)qc : (uint64_t)qc + 1, probes);
             } else {
                 const uint4 cu = cur[j];
-                const uint32_t qp = cu.x >> (p.K - i);
-                const Entry* tj = p.tab + (int64_t)j * p.n;
-                const uint32_t B = (uint32_t)p.B;
-                uint32_t e;
-                if (left) {
-                    e = cu.y;
-                    while (e > 0) {
-                        ++probes;
-                        if ((entry_code(tj + e - 1) >> (p.K - i)) != qp) break;
-                        e = e > B ? e - B : 0u;
-                    }
-                    c->qc[r] = cu.x;
-                } else {
-                    e = cu.z;
-                    while (e < (uint32_t)p.n) {
-                        ++probes;
-                        if ((entry_code(tj + e) >> (p.K - i)) != qp) break;
-                        e = (uint64_t)e + B < (uint64_t)p.n ? e + B : (uint32_t)p.n;
-                    }
-                }
-                c->bnd[task] = e;
+                c->bnd[task] = widen_side(p, j, i, cu.x, left ? cu.y : cu.z, left, probes);
+                if (left) c->qc[r] = cu.x;
             }
         }
         __syncwarp();
@@ -428,8 +410,13 @@ __device__ __forceinline__ void scan_wide_tile(const QueryParams& p, int64_t aw,
         const uint32_t o = u * 32 + lane;
         pass[u] = o < cnt;
         if (pass[u] && p.use_filter && tau < 64) pass[u] = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ sk) <= tau;
-        old[u] = pass[u] ? atomicMin(W + e[u].x, tag) : 0u;
+        old[u] = pass[u] ? __ldcg(W + e[u].x) : 0u;
     }
+    // a smaller tag already there: a duplicate, no atomic needed (most passing ids, late in a
+    // search); else claim the visit
+#pragma unroll
+    for (int u = 0; u < kTile / 32; ++u)
+        if (pass[u] && old[u] >= tag) old[u] = atomicMin(W + e[u].x, tag);
     uint32_t* cand = rs.wcand + aw * kTile;
     uint32_t np = 0, npass = 0;
 #pragma unroll
