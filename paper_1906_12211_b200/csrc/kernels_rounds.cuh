@@ -809,8 +809,8 @@ __device__ __forceinline__ void push_fused(const RoundState& rs, uint32_t q) {
     else push(rs.fused, &rs.ctl->nfused, q);
 }
 
-template <typename PP>
-__global__ void __launch_bounds__(128, 8) k_merge(PP pp, int par) {
+template <typename PP, bool WIDE>
+__global__ void __launch_bounds__(128, WIDE ? 8 : 10) k_merge(PP pp, int par) {
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(128, 8) k_merge(PP pp, int par) {
     for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < nact; a += nw) {
         const int64_t q = act[a];
         const int fl = rs.flags[q];
-        const bool wide = fl & kFlagWide;
+        const bool wide = WIDE && (fl & kFlagWide);  // WIDE = false: no wide queries in this search
         if (fl & kFlagFused) {
             if (lane == 0) push_fused(rs, (uint32_t)q);
             continue;
@@ -1018,7 +1018,7 @@ __global__ void __launch_bounds__(128, 8) k_merge(PP pp, int par) {
             __syncwarp();
             // the i = 0 scan runs wide (a query not yet wide widens for it, with the evaluated
             // list just committed; else the fused kernel takes it)
-            const bool to_wide = ni == 0 && !wide && try_widen(p, q, lane);
+            const bool to_wide = WIDE && ni == 0 && !wide && try_widen(p, q, lane);
             if (lane == 0) {
                 if (ni == 0 && !wide && !to_wide) { rs.flags[q] |= kFlagFused; push_fused(rs, (uint32_t)q); }
                 else {

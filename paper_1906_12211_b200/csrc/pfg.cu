@@ -19,6 +19,7 @@
 #include <thread>
 #include <tuple>
 #include <vector>
+#include <type_traits>
 
 #include "../../include/pfg.h"
 #include "kernels_build.cuh"
@@ -1311,9 +1312,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const size_t esm = (size_t)expand_smem_bytes(g.dpad, lazy) * 4;
         const size_t dsm = (size_t)align16((int)sizeof(DedupeSmem)) * 4;
         const size_t msm = (size_t)(align16((int)sizeof(MergeSmem)) + 2 * align16(kt * 8)) * 4;
-        PFG_CUDA(cudaFuncSetAttribute(k_merge<QueryParams>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+        PFG_CUDA(cudaFuncSetAttribute(k_merge<QueryParams, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+        PFG_CUDA(cudaFuncSetAttribute(k_merge<QueryParams, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
         PFG_CUDA(cudaFuncSetAttribute(k_dedupe<QueryParams>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        PFG_CUDA(cudaFuncSetAttribute(k_merge<const QueryParams*>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+        PFG_CUDA(cudaFuncSetAttribute(k_merge<const QueryParams*, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
         PFG_CUDA(cudaFuncSetAttribute(k_dedupe<const QueryParams*>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         int docc = 1;
         PFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, k_dedupe<QueryParams>, 128, dsm));
@@ -1349,7 +1351,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             k_sims<PP><<<sb, 256, 0, rst>>>(pp, par);
             if (rst == st) PFG_TRY(dbg_sync("k_sims"));
             PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
-            k_merge<PP><<<qb_m, 128, msm, rst>>>(pp, par);
+            if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_merge<PP, true><<<qb_m, 128, msm, rst>>>(pp, par);
+            else k_merge<PP, false><<<qb_m, 128, msm, rst>>>(pp, par);
             if (rst == st) PFG_TRY(dbg_sync("k_merge"));
             PFG_TRY(phase_mark(I, marks, kPhOther, rst));
             PFG_CUDA(cudaGetLastError());
