@@ -216,12 +216,17 @@ __device__ __forceinline__ uint32_t rep_lower_bound(const QueryParams& p, int j,
 }
 
 // R-12 segment widening of one side of repetition j's emitted range at level i < K: the oracle's
-// loop (step B outward while the boundary entry shares the query's i-bit prefix) after its first
-// probe, which settles the common case, continues in closed form: the prefix range end a_i / b_i
-// from the prefix table and a bucket search (O(1) for i <= 13), then
+// loop (step B outward while the boundary entry shares the query's i-bit prefix), literally for
+// its first kWidenSteps probes (short ranges, the common case at high levels), then in closed
+// form: the prefix range end a_i / b_i from the prefix table and a bucket search (O(1) for
+// i <= 13), and
 //   left  e' = e - B*ceil((e - a_i)/B), or 0 if that is <= 0
 //   right e' = min(n, e + B*ceil((b_i - e)/B))
 // -- the loop's positions, since the entries sharing the prefix are exactly [a_i, b_i).
+#ifndef PFG_WIDEN_STEPS
+#define PFG_WIDEN_STEPS 4
+#endif
+constexpr int kWidenSteps = PFG_WIDEN_STEPS;
 __device__ __forceinline__ uint32_t widen_side(const QueryParams& p, int j, int i, uint32_t code, uint32_t e, bool left,
                                                uint32_t& probes) {
     const Entry* tj = p.tab + (int64_t)j * p.n;
@@ -229,17 +234,27 @@ __device__ __forceinline__ uint32_t widen_side(const QueryParams& p, int j, int 
     const uint32_t qp = code >> sh;
     const uint32_t B = (uint32_t)p.B, n = (uint32_t)p.n;
     if (left) {
+        for (int t = 0; t < kWidenSteps; ++t) {
+            if (e == 0) return 0u;
+            ++probes;
+            if ((entry_code(tj + e - 1) >> sh) != qp) return e;
+            e = e > B ? e - B : 0u;
+        }
         if (e == 0) return 0u;
-        ++probes;
-        if ((entry_code(tj + e - 1) >> sh) != qp) return e;
         const uint32_t a = rep_lower_bound(p, j, (uint64_t)qp << sh, probes);
+        if (a >= e) return e;
         const uint64_t m = (e - a + B - 1) / B;
         return (uint64_t)B * m >= e ? 0u : e - (uint32_t)(B * m);
     }
+    for (int t = 0; t < kWidenSteps; ++t) {
+        if (e >= n) return n;
+        ++probes;
+        if ((entry_code(tj + e) >> sh) != qp) return e;
+        e = (uint64_t)e + B < (uint64_t)n ? e + B : n;
+    }
     if (e >= n) return n;
-    ++probes;
-    if ((entry_code(tj + e) >> sh) != qp) return e;
     const uint32_t b = rep_lower_bound(p, j, ((uint64_t)qp + 1) << sh, probes);
+    if (b <= e) return e;
     const uint64_t v = (uint64_t)e + (uint64_t)B * ((b - e + B - 1) / B);
     return v > n ? n : (uint32_t)v;
 }

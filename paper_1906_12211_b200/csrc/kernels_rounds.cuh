@@ -43,7 +43,10 @@ __device__ __forceinline__ const QueryParams& deref(const QueryParams& p) { retu
 __device__ __forceinline__ const QueryParams& deref(const QueryParams* p) { return *p; }
 __global__ void k_setp(QueryParams p, QueryParams* dst) { *dst = p; }
 constexpr int kEPre = 16;  // evaluated ids loaded per lane per batch when the hash set is rebuilt
-constexpr int kSaveMin = 512;  // k_dedupe rebuilds sets of at most this many ids instead of restoring them
+#ifndef PFG_SAVEMIN
+#define PFG_SAVEMIN 512
+#endif
+constexpr int kSaveMin = PFG_SAVEMIN;  // k_dedupe rebuilds sets of at most this many ids instead of restoring them
 
 __device__ __forceinline__ int tau_of_state(const QueryParams& p, int tn, const uint64_t* T) {
     if (!p.use_filter || tn != p.k_eff) return 64;
