@@ -373,6 +373,7 @@ struct pfg_index {
     DBuf jhist;                  // stop-depth histogram of the last search (device)
     uint32_t* h_jhist = nullptr; // its pinned host copy
     int eager = 32;              // repetitions hashed eagerly per query (tuned from the last search)
+    int qb_depth = 64;           // level-K match ranges precomputed per query (non-lazy families; tuned)
     cudaStream_t aux = nullptr;  // second stream: query sketches run beside the query hashing
     cudaStream_t aux2 = nullptr; // third stream: codes and ranges of the later eager repetitions
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_late = nullptr;
@@ -879,6 +880,10 @@ void tune_eager(pfg_index* I) {
         if (tot && cum * 100 >= tot * 99) { e = j; break; }
     }
     if (tot) I->eager = std::max(8, std::min(64, e));
+    // level-K match ranges computed in bulk before the query kernels (k_qbounds): the depth 99 % of
+    // the queries reach at level K, all L repetitions when they go deeper (the fused kernel would
+    // otherwise binary-search them one warp at a time)
+    if (tot) I->qb_depth = e >= kJHist - 1 ? (1 << 30) : std::max(8, e);
 }
 
 // developer aid PFG_DBG_SYNC=1: synchronise after each launch group and name the failing one
@@ -1240,7 +1245,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // level-K match ranges of the first repetitions, one thread per (query, repetition)
     // (SimHash and pool strategies hash all L repetitions eagerly; their ranges are precomputed
     // for the repetitions most queries reach, the tuned eager depth)
-    p.qb_n = getenv("PFG_NO_QB") ? 0 : std::min(std::min(I->qc_n, kQBMax), lazy ? I->qc_n : I->eager);
+    p.qb_n = getenv("PFG_NO_QB") ? 0 : lazy ? std::min(I->qc_n, kQBMax) : std::min(I->qc_n, I->qb_depth);
     PFG_TRY(I->jhist.ensure(kJHist * 4, "stop histogram"));
     if (!I->h_jhist) PFG_CUDA(cudaMallocHost(&I->h_jhist, kJHist * 4));
     PFG_CUDA(cudaMemsetAsync(I->jhist.p, 0, kJHist * 4, st));
