@@ -172,6 +172,17 @@ pfg_status pfg_merge_topk(const int64_t* ids, const float* sims, int32_t world, 
 
 pfg_status pfg_index_info(const pfg_index* idx, pfg_index_info_t* out);
 
+/* Index serialisation (the paper's index is rebuilt from its seed, SPEC.md's
+ * program persists it).  pfg_save writes the geometry, the seed and every index array (normalised
+ * data, repetition tables, prefix tables, hash and sketch functions, slots, pool selections, the
+ * CP table) to `path` in a private little-endian format (magic "PFGIDX01" + ABI version); it
+ * waits for `stream` first.  pfg_load reads such a file onto the current CUDA device and returns
+ * an index equal to the saved one (searches give identical results).  Errors: PFG_E_ARG (cannot
+ * open / not an index file / other ABI version), PFG_E_STATE (short read or write),
+ * PFG_E_OOM / PFG_E_CUDA.  The caller owns `*out` (pfg_free). */
+pfg_status pfg_save(const pfg_index* idx, const char* path, void* stream);
+pfg_status pfg_load(const char* path, void* stream, pfg_index** out);
+
 /* Host-only cost model (R-11, no GPU needed): the L that pfg_build would derive, and
  * the minimum budget for L = 1.  Returns PFG_E_BUDGET if the budget admits no repetition. */
 pfg_status pfg_derive_reps(int64_t n, int32_t d, int32_t family, uint64_t memory_budget_bytes,

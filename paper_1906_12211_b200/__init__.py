@@ -30,7 +30,7 @@ STATUS = {0: "PFG_OK", 1: "PFG_E_ARG", 2: "PFG_E_ZERO_VECTOR", 3: "PFG_E_BUDGET"
 # symbols include/pfg.h declares (checked by tests/test_abi.py)
 EXPORTED = ["pfg_build", "pfg_search", "pfg_merge_topk", "pfg_index_info", "pfg_derive_reps", "pfg_export",
             "pfg_hash_queries", "pfg_stop_tables", "pfg_last_timing", "pfg_last_phases", "pfg_free", "pfg_last_error",
-            "pfg_abi_version"]
+            "pfg_abi_version", "pfg_save", "pfg_load"]
 
 
 class PfgError(RuntimeError):
@@ -104,6 +104,10 @@ def lib() -> C.CDLL:
         L.pfg_last_error.argtypes = []
         L.pfg_abi_version.restype = C.c_int32
         L.pfg_abi_version.argtypes = []
+        L.pfg_save.restype = S
+        L.pfg_save.argtypes = [P, C.c_char_p, P]
+        L.pfg_load.restype = S
+        L.pfg_load.argtypes = [C.c_char_p, P, P]
         _lib = L
     return _lib
 
@@ -182,6 +186,21 @@ class Index:
                                _stream(data, stream), C.byref(h)))
         self._h = h
         self.info = self._info()
+
+    def save(self, path: str, stream=None):
+        """write the index to `path` (pfg_save)"""
+        _check(lib().pfg_save(self._h, os.fsencode(path), _stream(None, stream)))
+
+    @classmethod
+    def load(cls, path: str, stream=None) -> "Index":
+        """an index read from a pfg_save file onto the current CUDA device (pfg_load)"""
+        self = cls.__new__(cls)
+        self._bo = None
+        h = C.c_void_p()
+        _check(lib().pfg_load(os.fsencode(path), _stream(None, stream), C.byref(h)))
+        self._h = h
+        self.info = self._info()
+        return self
 
     def _info(self) -> dict:
         inf = IndexInfo()

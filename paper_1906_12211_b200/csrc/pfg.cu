@@ -973,6 +973,34 @@ int epl_of(const Geo& g) { return std::max(1, g.dp / 32); }
 }  // namespace
 }  // namespace pfg
 
+// ---------------------------------------------------------------------------------------------
+// serialisation: magic, ABI version, sizeof(Geo), Geo, seed, the device arrays (byte count then
+// bytes, through a pinned staging buffer), the host tables
+namespace {
+const char kIdxMagic[8] = {'P', 'F', 'G', 'I', 'D', 'X', '0', '1'};
+constexpr size_t kStage = (size_t)64 << 20;
+
+struct Stage {
+    void* h = nullptr;
+    ~Stage() { if (h) cudaFreeHost(h); }
+};
+std::vector<DBuf*> index_arrays(pfg_index* I) {
+    return {&I->x, &I->tab, &I->pt, &I->slot, &I->hpfn, &I->sg, &I->sel, &I->skfn};
+}
+template <class T>
+bool put_vec(FILE* f, const std::vector<T>& v) {
+    const uint64_t n = v.size();
+    return fwrite(&n, 8, 1, f) == 1 && (n == 0 || fwrite(v.data(), sizeof(T), n, f) == n);
+}
+template <class T>
+bool get_vec(FILE* f, std::vector<T>& v) {
+    uint64_t n = 0;
+    if (fread(&n, 8, 1, f) != 1 || n > ((uint64_t)1 << 32)) return false;
+    v.resize(n);
+    return n == 0 || fread(v.data(), sizeof(T), n, f) == n;
+}
+}  // namespace
+
 // =============================================================================================
 extern "C" {
 
@@ -1145,6 +1173,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     const int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
     const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
     int64_t wide_max = 0;   // visit-tag arrays this search may use
+    bool want_wide = false;
     if (rounds) {
         const size_t N = (size_t)nq;
         PFG_TRY(I->rs_lvl.ensure(N * 4, "rs")); PFG_TRY(I->rs_c0.ensure(N * 4, "rs"));
@@ -1184,7 +1213,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const int64_t per = 4 * g.n;
         const int64_t wmib = getenv("PFG_WIDE_MIB") ? atoll(getenv("PFG_WIDE_MIB")) : 8192;
         wide_max = std::max<int64_t>(1, (wmib << 20) / per);
-        if (s.wide >= 0 && (int64_t)(g.K + 1) * g.L < 65536) {
+        // wide queries: on when asked for (wide > 0, or the developer knob PFG_LOOP_MAX), else
+        // automatic: on iff the previous search's queries were heavy (loop_heavy); off, a query
+        // beyond the hash set goes to the fused kernel's bitmap mode (and nothing is allocated)
+        want_wide = (s.wide > 0 || (s.wide == 0 && (I->loop_heavy || getenv("PFG_LOOP_MAX")))) &&
+                    (int64_t)(g.K + 1) * g.L < 65536;
+        if (want_wide) {
             const int64_t smax = wide_max;
             const int64_t want = std::min<int64_t>(smax, std::max<int64_t>(I->wv_want, std::max<int64_t>(1, (512ll << 20) / per)));
             if (want > I->wv_slots || I->wv_n != g.n) {
@@ -1299,11 +1333,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         r.fused2 = I->rs_fused2.as<uint32_t>();
         r.wslot = I->rs_wslot.as<uint32_t>();
         r.rtile = I->rs_rtile.as<uint32_t>();
-        // wide queries: on when asked for (wide > 0, or the developer knob PFG_LOOP_MAX), else
-        // automatic: on iff the previous search's queries were heavy (loop_heavy); off, a query
-        // beyond the hash set goes to the fused kernel's bitmap mode
-        const bool wide_on = (s.wide > 0 || (s.wide == 0 && (I->loop_heavy || getenv("PFG_LOOP_MAX")))) && I->wv_slots > 0 &&
-                             I->wv_n == g.n && (int64_t)(g.K + 1) * g.L < 65536;
+        const bool wide_on = want_wide && I->wv_slots > 0 && I->wv_n == g.n;
         r.wv = wide_on ? I->rs_wv.as<uint32_t>() : nullptr;
         r.wslots = wide_on ? (uint32_t)std::min<int64_t>(I->wv_slots, wide_max) : 0u;
         r.wtiles = I->rs_wtiles.as<uint4>(); r.wcand = I->rs_wcand.as<uint32_t>(); r.wsim = I->rs_wsim.as<float>();
@@ -1751,6 +1781,73 @@ pfg_status pfg_stop_tables(pfg_index* I, float recall, const pfg_search_opts* op
         PFG_TRY(get_tau(I, s.eps, b, &h));
         std::memcpy(tau_host, h.data(), 65 * 4);
     }
+    return PFG_OK;
+}
+
+pfg_status pfg_save(const pfg_index* Ic, const char* path, void* stream) {
+    if (!Ic || !path) return fail(PFG_E_ARG, "index and path are required");
+    pfg_index* I = const_cast<pfg_index*>(Ic);
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    PFG_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    std::unique_ptr<FILE, int (*)(FILE*)> f(fopen(path, "wb"), fclose);
+    if (!f) return fail(PFG_E_ARG, std::string("cannot open ") + path + " for writing");
+    const int32_t abi = PFG_ABI_VERSION;
+    const uint32_t gsz = sizeof(Geo);
+    bool ok = fwrite(kIdxMagic, 8, 1, f.get()) == 1 && fwrite(&abi, 4, 1, f.get()) == 1 &&
+              fwrite(&gsz, 4, 1, f.get()) == 1 && fwrite(&I->g, sizeof(Geo), 1, f.get()) == 1 &&
+              fwrite(&I->seed, 8, 1, f.get()) == 1;
+    Stage stg;
+    PFG_CUDA(cudaMallocHost(&stg.h, kStage));
+    for (DBuf* b : index_arrays(I)) {
+        const uint64_t nb = b->p ? (uint64_t)b->bytes : 0;
+        ok = ok && fwrite(&nb, 8, 1, f.get()) == 1;
+        for (uint64_t o = 0; ok && o < nb; o += kStage) {
+            const size_t c = (size_t)std::min<uint64_t>(kStage, nb - o);
+            PFG_CUDA(cudaMemcpy(stg.h, (char*)b->p + o, c, cudaMemcpyDeviceToHost));
+            ok = fwrite(stg.h, 1, c, f.get()) == c;
+        }
+    }
+    ok = ok && put_vec(f.get(), I->cpT) && put_vec(f.get(), I->slot_h) && put_vec(f.get(), I->sel_h);
+    if (!ok) return fail(PFG_E_STATE, std::string("short write to ") + path);
+    if (fclose(f.release()) != 0) return fail(PFG_E_STATE, std::string("cannot close ") + path);
+    return PFG_OK;
+}
+
+pfg_status pfg_load(const char* path, void* stream, pfg_index** out) {
+    if (!path || !out) return fail(PFG_E_ARG, "path and out are required");
+    *out = nullptr;
+    std::unique_ptr<FILE, int (*)(FILE*)> f(fopen(path, "rb"), fclose);
+    if (!f) return fail(PFG_E_ARG, std::string("cannot open ") + path);
+    char magic[8];
+    int32_t abi = 0;
+    uint32_t gsz = 0;
+    if (fread(magic, 8, 1, f.get()) != 1 || std::memcmp(magic, kIdxMagic, 8) != 0)
+        return fail(PFG_E_ARG, std::string(path) + " is not a pfg index file");
+    if (fread(&abi, 4, 1, f.get()) != 1 || abi != PFG_ABI_VERSION || fread(&gsz, 4, 1, f.get()) != 1 || gsz != sizeof(Geo))
+        return fail(PFG_E_ARG, std::string(path) + " was written by another ABI version");
+    std::unique_ptr<pfg_index> I(new pfg_index());
+    if (fread(&I->g, sizeof(Geo), 1, f.get()) != 1 || fread(&I->seed, 8, 1, f.get()) != 1)
+        return fail(PFG_E_STATE, std::string("short read from ") + path);
+    PFG_CUDA(cudaGetDevice(&I->device));
+    PFG_CUDA(cudaDeviceGetAttribute(&I->num_sms, cudaDevAttrMultiProcessorCount, I->device));
+    Stage stg;
+    PFG_CUDA(cudaMallocHost(&stg.h, kStage));
+    (void)stream;
+    for (DBuf* b : index_arrays(I.get())) {
+        uint64_t nb = 0;
+        if (fread(&nb, 8, 1, f.get()) != 1) return fail(PFG_E_STATE, std::string("short read from ") + path);
+        if (nb == 0) continue;
+        PFG_TRY(b->alloc((size_t)nb, "loaded index array"));
+        for (uint64_t o = 0; o < nb; o += kStage) {
+            const size_t c = (size_t)std::min<uint64_t>(kStage, nb - o);
+            if (fread(stg.h, 1, c, f.get()) != c) return fail(PFG_E_STATE, std::string("short read from ") + path);
+            PFG_CUDA(cudaMemcpy((char*)b->p + o, stg.h, c, cudaMemcpyHostToDevice));
+        }
+    }
+    if (!get_vec(f.get(), I->cpT) || !get_vec(f.get(), I->slot_h) || !get_vec(f.get(), I->sel_h))
+        return fail(PFG_E_STATE, std::string("short read from ") + path);
+    *out = I.release();
     return PFG_OK;
 }
 

@@ -406,3 +406,45 @@ def test_merge_of_bruteforce_shards_is_global_bruteforce():
     mi, _ = pfg.merge_topk(_cuda(np.stack(ids)), _cuda(np.stack(sims)))
     gi, _ = O.bruteforce(x, q, k)
     assert np.array_equal(mi.cpu().numpy(), gi)
+
+
+# ------------------------------------------------------------------ serialisation
+@pytest.mark.parametrize("name", ["hp", "fht", "hp_pool", "hp_tensor"])
+def test_save_load_roundtrip(cases, name, tmp_path):
+    c = cases[name]
+    path = str(tmp_path / f"{name}.pfg")
+    c.gpu.save(path)
+    g2 = pfg.Index.load(path)
+    assert g2.info == c.gpu.info
+    assert np.array_equal(g2.export_data().view(np.uint32), c.gpu.export_data().view(np.uint32))
+    assert np.array_equal(g2.export_slots(), c.gpu.export_slots())
+    for j in (0, c.orc.L - 1):
+        assert np.array_equal(g2.export_table(j), c.gpu.export_table(j))
+        assert np.array_equal(g2.export_prefix(j), c.gpu.export_prefix(j))
+    q = _cuda(c.q)
+    a = c.gpu.search(q, 10, 0.9, stats=True)
+    b = g2.search(q, 10, 0.9, stats=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    g2.close()
+
+
+def test_load_rejects_bad_files(tmp_path):
+    with pytest.raises(pfg.PfgError) as e:
+        pfg.Index.load(str(tmp_path / "missing.pfg"))
+    assert e.value.status == 1
+    bad = tmp_path / "bad.pfg"
+    bad.write_bytes(b"not an index file at all")
+    with pytest.raises(pfg.PfgError) as e:
+        pfg.Index.load(str(bad))
+    assert e.value.status == 1
+
+
+def test_load_truncated_file_is_a_short_read(cases, tmp_path):
+    path = tmp_path / "full.pfg"
+    cases["hp"].gpu.save(str(path))
+    raw = path.read_bytes()
+    cut = tmp_path / "cut.pfg"
+    cut.write_bytes(raw[: len(raw) // 2])
+    with pytest.raises(pfg.PfgError) as e:
+        pfg.Index.load(str(cut))
+    assert e.value.status == 7
