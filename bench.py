@@ -137,14 +137,16 @@ def recall_of(ids_t, truth_kth, xn, qn, k):
     return float(hit.float().sum() / (k * ids_t.shape[0]))
 
 
-def alg_bytes(stats, d, M, k):
+def alg_bytes(stats, d, M, k, row_bytes=None):
     """algorithmic bytes of the query kernel: per query
-    B_q = 16 E + 4d S + 8 P + 4d + 8M + 12k  (E retrieved 16-byte table entries, S evaluated rows,
-    P binary-search probes; plus the query row, its sketches and the outputs)"""
+    B_q = 16 E + r S + 8 P + r + 8M + 12k  (E retrieved 16-byte table entries, S evaluated rows of
+    r = 4d bytes (fp32; 2d for the int16 storage of R-25), P binary-search probes; plus the query
+    row, its sketches and the outputs)"""
+    r = 4 * d if row_bytes is None else row_bytes
     em = stats["emitted"].astype(np.float64)
     ev = stats["evaluated"].astype(np.float64)
     pr = stats["probes"].astype(np.float64)
-    b = 16 * em + 4 * d * ev + 8 * pr + 4 * d + 8 * M + 12 * k
+    b = 16 * em + r * ev + 8 * pr + r + 8 * M + 12 * k
     return float(b.sum())
 
 
@@ -250,6 +252,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--engine", type=int, default=0, help="0 = bulk rounds + fused kernel, 1 = fused kernel only")
     ap.add_argument("--uniform-chunks", action="store_true", help="first chunk R repetitions long (R-17 option)")
+    ap.add_argument("--storage", default="f32", choices=["f32", "i16"],
+                    help="rows for the inner products: fp32, or the paper's 16-bit fixed point (R-25)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -282,7 +286,7 @@ def main():
     q = torch.from_numpy(q_np).to(dev)
     del data_np
 
-    opts = dict(strategy=c["strategy"])
+    opts = dict(strategy=c["strategy"], storage=args.storage)
     if c["reps"]:
         opts["reps"] = c["reps"]
     torch.cuda.synchronize()
@@ -390,10 +394,10 @@ def main():
 
     if rank == 0:
         pk = peaks()
-        ab = alg_bytes(stats, d, info["sketch_words"], k)
+        ab = alg_bytes(stats, d, info["sketch_words"], k, row_bytes=2 * d if args.storage == "i16" else 4 * d)
         kern_s = statistics.mean(kern_ms) / 1e3
         achieved = ab / kern_s / 1e9
-        traffic, traffic_src = profiled_traffic(args.config)
+        traffic, traffic_src = profiled_traffic(args.config) if args.storage == "f32" else (None, None)
         cpu = None
         if not args.no_cpu_baseline:
             try:
@@ -411,13 +415,15 @@ def main():
             "higher_is_better": True,
             "scaling": "weak" if weak else "strong",
             "vs_baseline": None,
-            "dtype": "f32",
+            "dtype": "f32" if args.storage == "f32" else "i16 rows (int32 dot), f32 hashing",
             "data": "synthetic",
             "config": {"workload": f"config{args.config}: {c['name']}" + WORKLOAD_NOTE.get(args.config, "")
+                       + (" [int16 fixed-point rows, R-25]" if args.storage == "i16" else "")
                        + (f" ({c['shard_n']} rows per GPU)" if weak else ""),
                        "n": n, "d": d, "nq": nq, "k": k, "recall_target": args.recall, "family": c["family"],
                        "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": info["reps"],
-                       "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "l2": "flushed (512 MiB write) between timed steps",
+                       "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "storage": args.storage,
+                       "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"data-sharded x{world}" if world > 1 else "single GPU"},
             "recall": rec,
             "build_s": build_s,

@@ -74,9 +74,18 @@ typedef struct {
     int32_t sketch_words;  /* [32] M 64-bit sketches per point; -1 = none (no filter) */
     int32_t cp_draws;      /* [1000] Monte-Carlo draws per grid cell of the CP table */
     int32_t max_reps;      /* [4096] cap on the derived L (R-11) */
-    int32_t reserved0;
+    int32_t storage;       /* [PFG_STORAGE_F32] rows for the exact inner products (PFG_STORAGE_I16: the
+                              paper's 16-bit fixed point; R-25) */
     int64_t id_offset;     /* [0] global id of local row 0 (sharded mode) */
 } pfg_build_opts;
+
+/* Row storage for the inner products (hashing and sketches always use the fp32 normalised rows).
+ * PFG_STORAGE_I16: v = clamp(rint(x * 2^15), -2^15, 2^15 - 1) per coordinate of the normalised fp32
+ * row (round to nearest, ties to even), rows padded to a multiple of 16 coordinates (32 bytes);
+ * similarity = (float)(sum_t q_t v_t, exact in int32) * 2^-30.  Halves the bytes of every
+ * candidate row; similarities differ from fp32 by at most ~2e-3 and are exact
+ * (order-independent) integers before the final conversion. */
+enum { PFG_STORAGE_F32 = 0, PFG_STORAGE_I16 = 1 };
 
 /* Search options.  Zero-initialise + struct_size; zero field = default.  NULL = all defaults. */
 typedef struct {
@@ -175,7 +184,7 @@ pfg_status pfg_index_info(const pfg_index* idx, pfg_index_info_t* out);
 /* Index serialisation (the paper's index is rebuilt from its seed, SPEC.md's
  * program persists it).  pfg_save writes the geometry, the seed and every index array (normalised
  * data, repetition tables, prefix tables, hash and sketch functions, slots, pool selections, the
- * CP table) to `path` in a private little-endian format (magic "PFGIDX01" + ABI version); it
+ * CP table) to `path` in a private little-endian format (magic "PFGIDX02" + ABI version); it
  * waits for `stream` first.  pfg_load reads such a file onto the current CUDA device and returns
  * an index equal to the saved one (searches give identical results).  Errors: PFG_E_ARG (cannot
  * open / not an index file / other ABI version), PFG_E_STATE (short read or write),
@@ -195,10 +204,11 @@ typedef enum {
                                repetition's slot for that id}, sorted ascending by the first word */
     PFG_EXPORT_PREFIX = 2,  /* arg = rep j: uint32 [8193] first position whose top 13 bits >= p */
     PFG_EXPORT_SKETCH = 3,  /* per-point sketches are not retained (PFG_E_STATE): they live inline */
-    PFG_EXPORT_DATA = 4,    /* fp32 [n][d] normalised rows */
+    PFG_EXPORT_DATA = 4,    /* fp32 [n][d] normalised rows (PFG_STORAGE_F32 only) */
     PFG_EXPORT_CP = 5,      /* double [ell+1][41] cleaned CP collision table (FHT family) */
     PFG_EXPORT_SLOTS = 6,   /* int32 [L] sketch slot per repetition */
-    PFG_EXPORT_POOLSEL = 7  /* int32 [L][c] pool function indices per repetition */
+    PFG_EXPORT_POOLSEL = 7, /* int32 [L][c] pool function indices per repetition */
+    PFG_EXPORT_DATA16 = 8   /* int16 [n][d] fixed-point rows (PFG_STORAGE_I16 only) */
 } pfg_export_what;
 
 /* copy an index array into host memory dst (dst_bytes must equal the array size) */

@@ -68,6 +68,11 @@ def lib():
         L.or_prefix_table.restype = None; L.or_prefix_table.argtypes = [P, C.c_int, P]
         L.or_grid_bucket.restype = C.c_int; L.or_grid_bucket.argtypes = [C.c_float]
         L.or_P.restype = C.c_double; L.or_P.argtypes = [P, C.c_int, C.c_float]
+        L.or_fixed16.restype = C.c_int16; L.or_fixed16.argtypes = [C.c_float]
+        L.or_quantize.restype = None; L.or_quantize.argtypes = [P, C.c_int64, C.c_int, P]
+        L.or_sim16.restype = C.c_float; L.or_sim16.argtypes = [P, P, C.c_int]
+        L.or_set_storage.restype = None; L.or_set_storage.argtypes = [P, C.c_int]
+        L.or_get_data16.restype = None; L.or_get_data16.argtypes = [P, P]
         L.or_should_stop.restype = C.c_int
         L.or_should_stop.argtypes = [P, C.c_int, C.c_int, C.c_float, C.c_double, C.c_int]
         L.or_tau.restype = C.c_int; L.or_tau.argtypes = [C.c_float, C.c_float]
@@ -125,6 +130,21 @@ def sim(a, b) -> float:
     """canonical similarity (32-lane tree order, R-2)"""
     a, b = _f32(a), _f32(b)
     return float(lib().or_sim(_p(a), _p(b), a.shape[0]))
+
+
+def fixed16(x) -> np.ndarray:
+    """R-25: 16-bit fixed point of normalised coordinates (clamp(rint(x 2^15)))"""
+    x = _f32(np.atleast_1d(x))
+    out = np.empty(x.shape, dtype=np.int16)
+    lib().or_quantize(_p(x), 1, x.size, _p(out))
+    return out
+
+
+def sim16(a16, b16) -> float:
+    """R-25: the exact fixed-point inner product, scaled by 2^-30"""
+    a16 = np.ascontiguousarray(a16, dtype=np.int16)
+    b16 = np.ascontiguousarray(b16, dtype=np.int16)
+    return float(lib().or_sim16(_p(a16), _p(b16), a16.shape[0]))
 
 
 def hp_bit(a, x) -> int:
@@ -194,7 +214,7 @@ class OracleIndex:
 
     def __init__(self, data, family: int, L: int, seed: int = 1, K: int = 24, M: int = 32,
                  strategy: int = INDEPENDENT, pool_bits: int = 3072, lazy: bool = False,
-                 cp_draws: int = 1000):
+                 cp_draws: int = 1000, storage: str = "f32"):
         data = _f32(data)
         self.n, self.d = data.shape
         if strategy == TENSOR:
@@ -211,6 +231,11 @@ class OracleIndex:
         lib().or_info(self._h, _p(info))
         (_, _, self.dp, self.ell, self.c, self.L, self.K, self.M, self.m) = [int(v) for v in info]
         self.family, self.strategy = family, strategy
+        self.storage = storage
+        if storage == "i16":
+            lib().or_set_storage(self._h, 1)
+        elif storage != "f32":
+            raise ValueError("storage must be 'f32' or 'i16'")
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -232,6 +257,11 @@ class OracleIndex:
     def data(self) -> np.ndarray:
         x = np.empty((self.n, self.d), dtype=np.float32)
         lib().or_get_data(self._h, _p(x))
+        return x
+
+    def data16(self) -> np.ndarray:
+        x = np.empty((self.n, self.d), dtype=np.int16)
+        lib().or_get_data16(self._h, _p(x))
         return x
 
     def sketches(self) -> np.ndarray:

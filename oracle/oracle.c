@@ -95,6 +95,26 @@ float or_sim(const float* a, const float* b, int d) {
     return s[0];
 }
 
+/* R-25, §4.2 "a fixed point format represented using 16-bit integers" (scale
+ * 2^15 per SPEC.md:49, 73): v = clamp(rint(x * 2^15), -2^15, 2^15 - 1) of a normalised fp32
+ * coordinate; rint rounds to nearest, ties to even (the default rounding mode). */
+int16_t or_fixed16(float x) {
+    float r = rintf(x * 32768.0f);
+    if (r > 32767.0f) r = 32767.0f;
+    if (r < -32768.0f) r = -32768.0f;
+    return (int16_t)r;
+}
+void or_quantize(const float* x, int64_t n, int d, int16_t* out) {
+    for (int64_t i = 0; i < n * d; ++i) out[i] = or_fixed16(x[i]);
+}
+/* The fixed-point inner product: the exact integer sum of the d products,
+ * scaled back by 2^-30 after rounding the (int32-range) sum to fp32. */
+float or_sim16(const int16_t* a, const int16_t* b, int d) {
+    int64_t s = 0;
+    for (int t = 0; t < d; ++t) s += (int64_t)a[t] * (int64_t)b[t];
+    return (float)s * 0x1p-30f;
+}
+
 /* PAPER.md:142-146 §2: HP (SimHash) bit = 1 iff <a,x> >= 0, a ~ N(0,I).
  * The inner product uses the same canonical order as or_dot. */
 int or_hp_bit(const float* a, const float* x, int d) { return or_dot(a, x, d) >= 0.0f; }
@@ -154,6 +174,8 @@ typedef struct {
     uint32_t** ids;    /* point ids per rep, aligned with codes */
     double cpT[34 * 41]; /* CP table T[b][a], b = 0..ell, a = 0..40 */
     int cp_draws;
+    int storage;       /* 0 = fp32 rows (or_sim), 1 = 16-bit fixed point (or_sim16, R-25) */
+    int16_t* x16;      /* fixed-point data [n][d] (storage 1) */
 } or_index;
 
 /* number of functions a repetition concatenates: c = ceil(K / ell) (R-7) */
@@ -362,7 +384,7 @@ void or_free(or_index* X) {
     if (!X) return;
     for (int j = 0; j < X->L; ++j) { free(X->codes[j]); free(X->ids[j]); }
     free(X->codes); free(X->ids); free(X->x); free(X->sk); free(X->hp); free(X->sg);
-    free(X->sel); free(X->slot); free(X->skf); free(X);
+    free(X->sel); free(X->slot); free(X->skf); free(X->x16); free(X);
 }
 
 /* accessors for tests */
@@ -376,6 +398,15 @@ void or_get_rep(or_index* X, int j, uint32_t* codes, uint32_t* ids) {
     memcpy(ids, X->ids[j], sizeof(uint32_t) * X->n);
 }
 void or_get_data(const or_index* X, float* x) { memcpy(x, X->x, sizeof(float) * X->n * X->d); }
+/* R-25: inner products on 16-bit fixed-point rows from here on (hashing stays on the fp32 rows) */
+void or_set_storage(or_index* X, int storage) {
+    X->storage = storage;
+    if (storage == 1 && !X->x16) {
+        X->x16 = (int16_t*)malloc(sizeof(int16_t) * X->n * X->d);
+        or_quantize(X->x, X->n, X->d, X->x16);
+    }
+}
+void or_get_data16(const or_index* X, int16_t* x) { memcpy(x, X->x16, sizeof(int16_t) * X->n * X->d); }
 void or_get_sketches(const or_index* X, uint64_t* sk) { memcpy(sk, X->sk, sizeof(uint64_t) * X->n * X->M); }
 void or_get_slots(const or_index* X, int32_t* s) { memcpy(s, X->slot, sizeof(int32_t) * X->L); }
 void or_get_sel(const or_index* X, int32_t* s) { if (X->sel) memcpy(s, X->sel, sizeof(int32_t) * X->L * X->c); }
@@ -533,6 +564,11 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
     uint64_t qs[64];
     if (X->M) or_sketch(X, q, qs);
     int filt = o->use_filter && X->M > 0;
+    int16_t* q16 = NULL;
+    if (X->storage == 1) {
+        q16 = (int16_t*)malloc(sizeof(int16_t) * d);
+        or_quantize(q, 1, d, q16);
+    }
     float* ts = (float*)malloc(sizeof(float) * (k_eff + 1));
     uint32_t* ti = (uint32_t*)malloc(sizeof(uint32_t) * (k_eff + 1));
     int nt = 0;
@@ -599,7 +635,7 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
                         E[id] = 1;
                         if (tids && nE < tcap) tids[nE] = id;
                         nE++;
-                        float sim = or_sim(q, X->x + (int64_t)id * d, d);
+                        float sim = q16 ? or_sim16(q16, X->x16 + (int64_t)id * d, d) : or_sim(q, X->x + (int64_t)id * d, d);
                         /* insert into the sorted top list (Alg. 1 lines 6-7) */
                         if (nt < k_eff || or_better(sim, id, ts[k_eff - 1], ti[k_eff - 1])) {
                             int pos = nt < k_eff ? nt : k_eff - 1;
@@ -628,7 +664,7 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
         if (t < nt) { oid[t] = ti[t]; osim[t] = ts[t]; } else { oid[t] = -1; osim[t] = -INFINITY; }
     }
     if (k > k_eff) trace[6] |= 1;
-    free(q); free(qc); free(ts); free(ti); free(E); free(elo); free(ehi); free(init);
+    free(q); free(qc); free(ts); free(ti); free(E); free(elo); free(ehi); free(init); free(q16);
 }
 
 void or_search(or_index* X, const float* qraw, int64_t nq, int k, float recall, const or_sopts* o,

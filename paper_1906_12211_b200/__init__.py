@@ -23,6 +23,7 @@ FAMILIES = {"simhash": SIMHASH, "hp": SIMHASH, "fht_cp": CROSSPOLYTOPE_FHT, "cro
 STRATEGIES = {"independent": INDEPENDENT, "pool": POOL, "tensor": TENSOR}
 
 EXPORT_TABLE, EXPORT_PREFIX, EXPORT_SKETCH, EXPORT_DATA, EXPORT_CP, EXPORT_SLOTS, EXPORT_POOLSEL = 1, 2, 3, 4, 5, 6, 7
+EXPORT_DATA16 = 8
 
 STATUS = {0: "PFG_OK", 1: "PFG_E_ARG", 2: "PFG_E_ZERO_VECTOR", 3: "PFG_E_BUDGET", 4: "PFG_E_CUDA",
           5: "PFG_E_OOM", 7: "PFG_E_STATE"}
@@ -42,7 +43,7 @@ class PfgError(RuntimeError):
 class BuildOpts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("strategy", C.c_int32), ("pool_bits", C.c_int32),
                 ("prefix_bits", C.c_int32), ("reps_override", C.c_int32), ("sketch_words", C.c_int32),
-                ("cp_draws", C.c_int32), ("max_reps", C.c_int32), ("reserved0", C.c_int32),
+                ("cp_draws", C.c_int32), ("max_reps", C.c_int32), ("storage", C.c_int32),
                 ("id_offset", C.c_int64)]
 
 
@@ -162,10 +163,14 @@ def _family(f) -> int:
     return FAMILIES[f] if isinstance(f, str) else int(f)
 
 
+STORAGES = {"f32": 0, "i16": 1}
+
+
 def _build_opts(strategy=INDEPENDENT, pool_bits=0, prefix_bits=0, reps=0, sketch_words=0, cp_draws=0,
-                max_reps=0, id_offset=0) -> BuildOpts:
+                max_reps=0, id_offset=0, storage="f32") -> BuildOpts:
     o = BuildOpts()
     o.struct_size = C.sizeof(BuildOpts)
+    o.storage = STORAGES[storage] if isinstance(storage, str) else int(storage)
     o.strategy = STRATEGIES[strategy] if isinstance(strategy, str) else int(strategy)
     o.pool_bits, o.prefix_bits, o.reps_override = pool_bits, prefix_bits, reps
     o.sketch_words, o.cp_draws, o.max_reps, o.id_offset = sketch_words, cp_draws, max_reps, id_offset
@@ -318,6 +323,10 @@ class Index:
 
     def export_data(self) -> np.ndarray:
         return self._export(EXPORT_DATA, 0, (self.info["n"], self.info["d"]), np.float32)
+
+    def export_data16(self) -> np.ndarray:
+        """int16 [n, d] fixed-point rows of a storage="i16" index (R-25)"""
+        return self._export(EXPORT_DATA16, 0, (self.info["n"], self.info["d"]), np.int16)
 
     def export_cp(self) -> np.ndarray:
         return self._export(EXPORT_CP, 0, (self.info["ell"] + 1, 41), np.float64)

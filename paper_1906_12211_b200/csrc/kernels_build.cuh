@@ -16,6 +16,20 @@
 
 namespace pfg {
 
+// R-25 (PFG_STORAGE_I16, the paper's 16-bit fixed point): v = clamp(rint(x 2^15),
+// -2^15, 2^15 - 1) of the normalised fp32 coordinate (x 2^15 is exact; rint = nearest, ties to
+// even), rows padded with zeros to dpad16 coordinates
+__global__ void k_quantize(const float* __restrict__ x, int64_t n, int dpad, int d, int16_t* __restrict__ out,
+                           int dpad16) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * dpad16) return;
+    const int64_t r = t / dpad16;
+    const int c = (int)(t - r * dpad16);
+    const float v = c < d ? x[r * dpad + c] : 0.0f;
+    const int q = __float2int_rn(v * 32768.0f);
+    out[t] = (int16_t)min(max(q, -32768), 32767);
+}
+
 // ---------------------------------------------------------------------------------------------
 // a1: out[r][0..d) = (float)((double)x / sqrt(sum_t (double)x_t^2)), sum sequential over t;
 // out[r][d..dpad) = 0.  zflag[r] = 1 for a zero row; *zmin = smallest zero row index.

@@ -123,6 +123,9 @@ struct QueryParams {
     int lstep;       // bits between searched depths: 1, or 2 ell for the tensor strategy
     int smem_warp;   // bytes of shared memory per warp
     const float* __restrict__ x;
+    const int16_t* __restrict__ x16;   // PFG_STORAGE_I16 rows [n][dpad16] (x is then NULL), R-25
+    const int16_t* __restrict__ qx16;  // the queries' int16 rows [nq][dpad16]
+    int dpad16;
     const Entry* __restrict__ tab;
     const uint32_t* __restrict__ pt;
     const uint8_t* __restrict__ slot;
@@ -350,8 +353,8 @@ __device__ __forceinline__ float kth_sim_clamped(const QueryParams& p, const QSt
 // lanes with bit h set keep the upper half) and adds the partner's value of the same row, so each
 // addition combines the same two tree nodes as the plain tree.  Lane l ends with row
 // (l >> (5 - log2 NR)) for NR <= 32.
-template <int NR>
-__device__ __forceinline__ float tree_rows(float (&a)[NR], int lane) {
+template <int NR, typename T>
+__device__ __forceinline__ T tree_rows(T (&a)[NR], int lane) {
     int m = NR;
 #pragma unroll
     for (int h = 16; h >= 1; h >>= 1) {
@@ -382,8 +385,64 @@ __device__ __forceinline__ float tree_rows(float (&a)[NR], int lane) {
 #define PFG_KRQ 8
 #endif
 constexpr int kRQ = PFG_KRQ;
+// R-25 (PFG_STORAGE_I16): the exact integer inner product of 8 coordinates (two int16 per word);
+// |partial sums| <= ||q|| ||x|| 2^30 < 2^31 (Cauchy-Schwarz), and the similarity is the int32 sum
+// rounded to fp32 times 2^-30 -- exact and independent of the summation order
+__device__ __forceinline__ int dot8_i16(const int4 a, const int4 b) {
+    int s = (int)(short)a.x * (int)(short)b.x + (a.x >> 16) * (b.x >> 16);
+    s += (int)(short)a.y * (int)(short)b.y + (a.y >> 16) * (b.y >> 16);
+    s += (int)(short)a.z * (int)(short)b.z + (a.z >> 16) * (b.z >> 16);
+    s += (int)(short)a.w * (int)(short)b.w + (a.w >> 16) * (b.w >> 16);
+    return s;
+}
+__device__ __forceinline__ float sim_of_i16(int s) { return __int2float_rn(s) * 9.313225746154785e-10f; }  // 2^-30
+
+// NR int16 rows against one query row per row (qoff, int4 units): lane c reads chunk c of each row
+template <int NR, bool ONEQ>
+__device__ __forceinline__ void rows_dot_i16(const int4* __restrict__ x4, const int4* __restrict__ q4,
+                                             const uint32_t (&roff)[NR], const uint32_t (&qoff)[NR], int nch16,
+                                             int lane, int (&acc)[NR]) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[r] = 0;
+    for (int c = lane; c < nch16; c += 32) {
+        int4 v[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) v[r] = __ldg(x4 + roff[r] + c);
+        int4 qv = __ldg(q4 + qoff[0] + c);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            if (!ONEQ && r > 0) qv = __ldg(q4 + qoff[r] + c);
+            acc[r] += dot8_i16(v[r], qv);
+        }
+    }
+}
+
 template <int RQ = kRQ>
-__device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int e0, int e1, int lane) {
+__device__ __forceinline__ void compute_sims(const QueryParams& p, const WarpSmem& w, int e0, int e1, int lane,
+                                             int64_t qi = 0) {
+    if (p.x16) {
+        const int nch16 = p.dpad16 >> 3;
+        const int4* x4 = reinterpret_cast<const int4*>(p.x16);
+        const int4* q4 = reinterpret_cast<const int4*>(p.qx16);
+        uint32_t qoff[RQ];
+#pragma unroll
+        for (int r = 0; r < RQ; ++r) qoff[r] = (uint32_t)qi * (uint32_t)nch16;
+        for (int b = e0; b < e1; b += RQ) {
+            const int nrow = min(RQ, e1 - b);
+            const uint32_t myoff = lane < RQ ? w.f->sid[b + (lane < nrow ? lane : nrow - 1)] * (uint32_t)nch16 : 0u;
+            uint32_t off[RQ];
+#pragma unroll
+            for (int r = 0; r < RQ; ++r) off[r] = __shfl_sync(kFull, myoff, r);
+            int acc[RQ];
+            rows_dot_i16<RQ, true>(x4, q4, off, qoff, nch16, lane, acc);
+            const int t = tree_rows<RQ>(acc, lane);
+            constexpr int kSh = (RQ == 32) ? 0 : (RQ == 16) ? 1 : (RQ == 8) ? 2 : 3;
+            const int rr = lane >> kSh;
+            if ((lane & ((1 << kSh) - 1)) == 0 && rr < nrow) w.f->ssim[b + rr] = sim_of_i16(t);
+        }
+        __syncwarp();
+        return;
+    }
     const int nch = p.dpad >> 2;
     const float4* q4 = reinterpret_cast<const float4*>(w.qrow);
     const float4* x4 = reinterpret_cast<const float4*>(p.x);
@@ -426,7 +485,7 @@ template <int RQ>
 __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, QState& st, int& nbuf, int& next_check,
                                       int complete, int nr, int c0, int i, int64_t qi, int& r_stop, int lane) {
     const long long td0 = p.prof ? clock64() : 0;
-    compute_sims<RQ>(p, w, 0, nbuf, lane);
+    compute_sims<RQ>(p, w, 0, nbuf, lane, qi);
     if (p.prof && lane == 0) atomicAdd(p.prof + 5, (unsigned long long)(clock64() - td0));
     int e = 0;
     bool stop = false;
@@ -751,7 +810,7 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                 ns += __popc(fm);
                 __syncwarp();
                 if (ns > kSB - 32 || g0 + 32 >= p.n) {
-                    compute_sims<RQ>(p, w, 0, ns, lane);
+                    compute_sims<RQ>(p, w, 0, ns, lane, qi);
                     if (ns) merge_range(p, w, st, 0, ns, qi, lane);
                     ns = 0;
                 }

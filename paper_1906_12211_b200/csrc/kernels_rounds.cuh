@@ -695,64 +695,68 @@ __device__ __forceinline__ void pool_sims_step(const float4* __restrict__ x4, co
 #ifndef PFG_SIMS_MINB
 #define PFG_SIMS_MINB 2
 #endif
-template <typename PP>
+// NR rows of one step: fp32 (R-2 lane chains + tree) or int16 (R-25, exact integer sums); lane
+// r < NR holds row r's id (myid) and query (myq); lane l ends with row l / (32 / NR)
+template <int NR, bool I16, bool ONEQ>
+__device__ __forceinline__ float sims_step(const QueryParams& p, uint32_t myid, uint32_t myq, int lane) {
+    uint32_t roff[NR], qoff[NR];
+    const uint32_t nch = I16 ? (uint32_t)(p.dpad16 >> 3) : (uint32_t)(p.dpad >> 2);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        roff[r] = __shfl_sync(kFull, myid, r) * nch;
+        qoff[r] = (ONEQ && r > 0) ? 0u : __shfl_sync(kFull, myq, r) * nch;
+    }
+    if constexpr (I16) {
+        int acc[NR];
+        rows_dot_i16<NR, ONEQ>(reinterpret_cast<const int4*>(p.x16), reinterpret_cast<const int4*>(p.qx16), roff, qoff,
+                               (int)nch, lane, acc);
+        return sim_of_i16(tree_rows<NR>(acc, lane));
+    } else {
+        float acc[NR];
+        pool_sims_step<ONEQ>(reinterpret_cast<const float4*>(p.x), reinterpret_cast<const float4*>(p.qx), roff, qoff,
+                             (int)nch, lane, acc);
+        return tree_rows<NR>(acc, lane);
+    }
+}
+
+template <typename PP, bool I16>
 __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
     const QueryParams& p = deref(pp);
+#ifndef PFG_I16_NR
+#define PFG_I16_NR 16
+#endif
+    constexpr int NR = I16 ? PFG_I16_NR : kRPI;   // int16 rows are half as long: more rows in flight
+    constexpr int kSh = NR == 32 ? 0 : NR == 16 ? 1 : NR == 8 ? 2 : 3;
     const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
     const uint32_t top = min(rs.ctl->pool_top[par], rs.pool_cap);
-    const int nch = p.dpad >> 2;
-    const float4* x4 = reinterpret_cast<const float4*>(p.x);
-    const float4* qx4 = reinterpret_cast<const float4*>(p.qx);
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // lane r < kRPI holds entry b + r of the current step (rows beyond the end repeat the last);
+    // lane r < NR holds entry b + r of the current step (rows beyond the end repeat the last);
     // the next step's entries are fetched before the current rows are read
     auto fetch = [&](int64_t b, uint32_t& id, uint32_t& qq) {
-        if (lane < kRPI && b < top) {
-            const int64_t e1 = (int64_t)top < b + kRPI ? (int64_t)top : b + kRPI;
+        if (lane < NR && b < top) {
+            const int64_t e1 = (int64_t)top < b + NR ? (int64_t)top : b + NR;
             const int64_t e = b + lane < e1 ? b + lane : e1 - 1;
             id = rs.pool_id[e];
             qq = rs.pool_q[e];
         }
     };
-    int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRPI;
+    int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NR;
     uint32_t nid = 0, nq_ = 0;
     fetch(b, nid, nq_);
-    for (; b < top; b += nw * kRPI) {
-        const int64_t e1 = (int64_t)top < b + kRPI ? (int64_t)top : b + kRPI;
+    for (; b < top; b += nw * NR) {
+        const int64_t e1 = (int64_t)top < b + NR ? (int64_t)top : b + NR;
         const uint32_t myid = nid, myq = nq_;
-        fetch(b + nw * kRPI, nid, nq_);
-        float acc[kRPI];
-        uint32_t roff[kRPI], qoff[kRPI];
-#pragma unroll
-        for (int r = 0; r < kRPI; ++r) {
-            roff[r] = __shfl_sync(kFull, myid, r) * (uint32_t)nch;
-            qoff[r] = __shfl_sync(kFull, myq, r) * (uint32_t)nch;
-        }
-        if (qoff[0] == qoff[kRPI - 1]) pool_sims_step<true>(x4, qx4, roff, qoff, nch, lane, acc);
-        else pool_sims_step<false>(x4, qx4, roff, qoff, nch, lane, acc);
-        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-        float t4[4], t2[2];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float recv = __shfl_xor_sync(kFull, h16 ? acc[k] : acc[k + 4], 16);
-            t4[k] = (h16 ? acc[k + 4] : acc[k]) + recv;
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const float recv = __shfl_xor_sync(kFull, h8 ? t4[k] : t4[k + 2], 8);
-            t2[k] = (h8 ? t4[k + 2] : t4[k]) + recv;
-        }
-        float t1 = (h4 ? t2[1] : t2[0]) + __shfl_xor_sync(kFull, h4 ? t2[0] : t2[1], 4);
-        t1 = t1 + __shfl_xor_sync(kFull, t1, 2);
-        t1 = t1 + __shfl_xor_sync(kFull, t1, 1);
-        const int rr = lane >> 2;
+        fetch(b + nw * NR, nid, nq_);
+        const bool oneq = __shfl_sync(kFull, myq, 0) == __shfl_sync(kFull, myq, NR - 1);
+        const float t1 = oneq ? sims_step<NR, I16, true>(p, myid, myq, lane) : sims_step<NR, I16, false>(p, myid, myq, lane);
+        const int rr = lane >> kSh;
         const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
-        if ((lane & 3) == 0 && b + rr < e1) rs.pool_key[b + rr] = make_key(t1, id_rr);
+        if ((lane & ((1 << kSh) - 1)) == 0 && b + rr < e1) rs.pool_key[b + rr] = make_key(t1, id_rr);
     }
     // wide tiles: a provisional id is fresh iff the query's visit-tag array still holds this
     // visit's tag (no earlier repetition of the chunk passed it); the fresh ids are compacted in
-    // order and their similarities computed (R-2, the same tree); kept = how many of them beat the
+    // order and their similarities computed (the same arithmetic); kept = how many of them beat the
     // k-th key the query held at the start of the chunk (only those can enter its top list)
     const uint32_t nwt = min(rs.ctl->nwt[par], rs.wcap);
     for (int64_t aw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; aw < nwt; aw += nw) {
@@ -781,20 +785,14 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
         }
         __syncwarp();
         const uint64_t kth = rs.tn[q] == p.k_eff ? rs.T[q * p.kt + p.k_eff - 1] : 0ull;
-        uint32_t qoff[kRPI], roff[kRPI], kept = 0;
-#pragma unroll
-        for (int r = 0; r < kRPI; ++r) qoff[r] = (uint32_t)q * (uint32_t)nch;
-        for (uint32_t b0 = 0; b0 < nf; b0 += kRPI) {
-            const uint32_t nrow = min((uint32_t)kRPI, nf - b0);
-            const uint32_t myid = lane < kRPI ? cand[b0 + min((uint32_t)lane, nrow - 1)] : 0u;
-#pragma unroll
-            for (int r = 0; r < kRPI; ++r) roff[r] = __shfl_sync(kFull, myid, r) * (uint32_t)nch;
-            float acc[kRPI];
-            pool_sims_step<true>(x4, qx4, roff, qoff, nch, lane, acc);
-            const float sim = tree_rows<kRPI>(acc, lane);  // lane l: row l >> 2
-            const uint32_t rr = lane >> 2;
+        uint32_t kept = 0;
+        for (uint32_t b0 = 0; b0 < nf; b0 += NR) {
+            const uint32_t nrow = min((uint32_t)NR, nf - b0);
+            const uint32_t myid = lane < NR ? cand[b0 + min((uint32_t)lane, nrow - 1)] : 0u;
+            const float sim = sims_step<NR, I16, true>(p, myid, (uint32_t)q, lane);
+            const uint32_t rr = lane >> kSh;
             const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
-            const bool own = (lane & 3) == 0 && rr < nrow;
+            const bool own = (lane & ((1 << kSh) - 1)) == 0 && rr < nrow;
             if (own) rs.wsim[aw * kTile + b0 + rr] = sim;
             kept += __popc(__ballot_sync(kFull, own && make_key(sim, id_rr) > kth));
         }

@@ -115,6 +115,7 @@ struct Geo {
     int pool_bits = 3072, cp_draws = 1000, max_reps = 4096, L = 0, S = 0;  // S = sqrt(L) (tensor)
     int64_t id_offset = 0;
     uint64_t fixed_bytes = 0, per_rep_bytes = 0, index_bytes = 0;
+    int storage = 0, dpad16 = 0;  // PFG_STORAGE_I16: int16 rows of dpad16 = 16 ceil(d/16) coordinates
 };
 
 pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, Geo& g) {
@@ -163,11 +164,15 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     if (g.cp_draws < 1) return fail(PFG_E_ARG, "cp_draws must be >= 1");
     g.max_reps = z.max_reps ? z.max_reps : 4096;
     g.id_offset = z.id_offset;
+    g.storage = z.storage;
+    if (g.storage != PFG_STORAGE_F32 && g.storage != PFG_STORAGE_I16) return fail(PFG_E_ARG, "unknown storage");
+    g.dpad16 = (d + 15) / 16 * 16;
     // bytes: data + sketches + sketch functions + pool functions + CP table (fixed);
     // per repetition: sorted table + 13-bit prefix table + slot + its own functions / selection
     const uint64_t N = (uint64_t)n;
     const uint64_t fn_hp = 4ull * g.dpad, fn_fht = 3ull * g.W * 4;
-    g.fixed_bytes = 4ull * N * g.dpad + 4ull * 64 * g.M * g.dpad + 8ull * (g.ell + 1) * 41;
+    const uint64_t data_bytes = g.storage == PFG_STORAGE_I16 ? 2ull * N * g.dpad16 : 4ull * N * g.dpad;
+    g.fixed_bytes = data_bytes + 4ull * 64 * g.M * g.dpad + 8ull * (g.ell + 1) * 41;
     if (g.strategy == PFG_POOL) g.fixed_bytes += (uint64_t)g.m * (family == PFG_SIMHASH ? fn_hp : fn_fht);
     g.per_rep_bytes = 16ull * N + 4ull * 8193 + 1;  // 16-byte entries: key + inline sketch word (R-21)
     if (g.strategy == PFG_INDEPENDENT) g.per_rep_bytes += (uint64_t)g.c * (family == PFG_SIMHASH ? fn_hp : fn_fht);
@@ -340,14 +345,14 @@ struct pfg_index {
     uint64_t seed = 0;
     std::mutex mu;
     // index arrays (device)
-    DBuf x, tab, pt, slot, hpfn, sg, sel, skfn;
+    DBuf x, tab, pt, slot, hpfn, sg, sel, skfn, x16;   // x16: int16 rows (PFG_STORAGE_I16; x is then freed)
     std::vector<double> cpT;
     std::vector<int32_t> slot_h, sel_h;
     // cached stop tables: key (recall bits, rule, per_round) -> device thr [K][L]; eps -> taub
     std::map<std::tuple<uint32_t, int, int>, std::shared_ptr<DBuf>> thr_cache;
     std::map<uint32_t, std::shared_ptr<DBuf>> tau_cache;
     // per-call scratch (grow-only)
-    DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, outb_ids, outb_sims, outb_stats, outb_trace, work;
+    DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, outb_ids, outb_sims, outb_stats, outb_trace, work, qx16;
     DBuf qord_keys, qord_sorted, qord_list, qord_temp;  // longest-first processing order (fused engine)
     DBuf cur, bitmap, claims;
     // round-engine state (per query, grow-only)
@@ -789,6 +794,15 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     PFG_TRY(I->zmin.ensure(8, "zmin"));
     PFG_TRY(normalize_rows(qsrc, nq, g.d, I->qx.as<float>(), g.dpad, I->qzero.as<uint8_t>(),
                            I->zmin.as<unsigned long long>(), zrow, st));
+    if (g.storage == PFG_STORAGE_I16) {
+        // R-25: the queries' fixed-point rows for the inner products
+        PFG_TRY(I->qx16.ensure((size_t)nq * g.dpad16 * 2, "int16 queries"));
+        const int64_t tot = nq * (int64_t)g.dpad16;
+        k_quantize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(I->qx.as<float>(), nq, g.dpad, g.d, I->qx16.as<int16_t>(),
+                                                                 g.dpad16);
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 1;
+    }
     if (!zrow) {
         if (!I->h_zmin) PFG_CUDA(cudaMallocHost(&I->h_zmin, 8));
         if (!I->ev_zmin) PFG_CUDA(cudaEventCreateWithFlags(&I->ev_zmin, cudaEventDisableTiming));
@@ -977,7 +991,7 @@ int epl_of(const Geo& g) { return std::max(1, g.dp / 32); }
 // serialisation: magic, ABI version, sizeof(Geo), Geo, seed, the device arrays (byte count then
 // bytes, through a pinned staging buffer), the host tables
 namespace {
-const char kIdxMagic[8] = {'P', 'F', 'G', 'I', 'D', 'X', '0', '1'};
+const char kIdxMagic[8] = {'P', 'F', 'G', 'I', 'D', 'X', '0', '2'};
 constexpr size_t kStage = (size_t)64 << 20;
 
 struct Stage {
@@ -985,7 +999,7 @@ struct Stage {
     ~Stage() { if (h) cudaFreeHost(h); }
 };
 std::vector<DBuf*> index_arrays(pfg_index* I) {
-    return {&I->x, &I->tab, &I->pt, &I->slot, &I->hpfn, &I->sg, &I->sel, &I->skfn};
+    return {&I->x, &I->tab, &I->pt, &I->slot, &I->hpfn, &I->sg, &I->sel, &I->skfn, &I->x16};
 }
 template <class T>
 bool put_vec(FILE* f, const std::vector<T>& v) {
@@ -1091,6 +1105,17 @@ pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t budget, i
         PFG_CUDA(cudaStreamSynchronize(st));
     }
     if (g.family == PFG_CROSSPOLYTOPE_FHT) PFG_TRY(build_cp_table(I.get(), st));
+    if (g.storage == PFG_STORAGE_I16) {
+        // R-25: the inner products read 16-bit fixed-point rows; the fp32 rows were only needed
+        // for hashing and sketches
+        PFG_TRY(I->x16.alloc((size_t)n * g.dpad16 * 2, "int16 data"));
+        const int64_t tot = n * (int64_t)g.dpad16;
+        k_quantize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(I->x.as<float>(), n, g.dpad, g.d, I->x16.as<int16_t>(),
+                                                                 g.dpad16);
+        PFG_CUDA(cudaGetLastError());
+        PFG_CUDA(cudaStreamSynchronize(st));
+        I->x.release();
+    }
     PFG_CUDA(cudaStreamSynchronize(st));
     *out = I.release();
     return PFG_OK;
@@ -1270,6 +1295,11 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     p.tensor_s = g.strategy == PFG_TENSOR ? g.S : 0;
     p.lstep = g.strategy == PFG_TENSOR ? 2 * g.ell : 1;
     p.x = I->x.as<float>(); p.tab = I->tab.as<Entry>(); p.pt = I->pt.as<uint32_t>();
+    if (g.storage == PFG_STORAGE_I16) {
+        p.x16 = I->x16.as<int16_t>();
+        p.qx16 = I->qx16.as<int16_t>();
+        p.dpad16 = g.dpad16;
+    }
     p.slot = I->slot.as<uint8_t>(); p.qx = I->qx.as<float>(); p.qsk = I->qsk.as<uint64_t>();
     p.qcodes = I->qcodes.as<uint32_t>(); p.qc_n = I->qc_n; p.qc_ld = I->qc_ld;
     p.sg = I->sg.as<uint32_t>(); p.qzero = I->qzero.as<uint8_t>();
@@ -1383,7 +1413,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             k_dedupe<PP><<<qb_d, 128, dsm, rst>>>(pp, par);
             if (rst == st) PFG_TRY(dbg_sync("k_dedupe"));
             PFG_TRY(phase_mark(I, marks, kPhSims, rst));
-            k_sims<PP><<<sb, 256, 0, rst>>>(pp, par);
+            if (g.storage == PFG_STORAGE_I16) k_sims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
+            else k_sims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
             if (rst == st) PFG_TRY(dbg_sync("k_sims"));
             PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_merge<PP, true><<<qb_m, 128, msm, rst>>>(pp, par);
@@ -1710,7 +1741,15 @@ pfg_status pfg_export(const pfg_index* Ic, int32_t what, int32_t arg, void* dst,
         case PFG_EXPORT_SKETCH:
             return fail(PFG_E_STATE, "per-point sketches are not retained: each repetition table stores its slot's "
                                      "sketch word inline (PFG_EXPORT_TABLE)");
+        case PFG_EXPORT_DATA16: {
+            if (g.storage != PFG_STORAGE_I16) return fail(PFG_E_STATE, "index stores fp32 rows (PFG_EXPORT_DATA)");
+            if (bytes != (uint64_t)g.n * g.d * 2) return fail(PFG_E_ARG, "dst_bytes must be n*d*2");
+            PFG_CUDA(cudaMemcpy2D(dst, (size_t)g.d * 2, I->x16.p, (size_t)g.dpad16 * 2, (size_t)g.d * 2, (size_t)g.n,
+                                  cudaMemcpyDeviceToHost));
+            return PFG_OK;
+        }
         case PFG_EXPORT_DATA: {
+            if (g.storage != PFG_STORAGE_F32) return fail(PFG_E_STATE, "index stores int16 rows (PFG_EXPORT_DATA16)");
             if (bytes != (uint64_t)g.n * g.d * 4) return fail(PFG_E_ARG, "dst_bytes must be n*d*4");
             PFG_CUDA(cudaMemcpy2D(dst, (size_t)g.d * 4, I->x.p, (size_t)g.dpad * 4, (size_t)g.d * 4, (size_t)g.n,
                                   cudaMemcpyDeviceToHost));

@@ -448,3 +448,75 @@ def test_load_truncated_file_is_a_short_read(cases, tmp_path):
     with pytest.raises(pfg.PfgError) as e:
         pfg.Index.load(str(cut))
     assert e.value.status == 7
+
+
+# ------------------------------------------------------------------ R-25 int16 storage
+class Case16(Case):
+    def __init__(self, name, data, q, family, L, seed, strategy=O.INDEPENDENT, pool_bits=3072):
+        self.name, self.data, self.q = name, data, q
+        fam = "simhash" if family == O.HP else "fht_cp"
+        strat = {O.POOL: "pool", O.TENSOR: "tensor"}.get(strategy, "independent")
+        self.gpu = pfg.Index(_cuda(data), 0, fam, seed=seed, reps=L, strategy=strat, pool_bits=pool_bits,
+                             storage="i16")
+        self.orc = O.OracleIndex(data, family, L=L, seed=seed, strategy=strategy, pool_bits=pool_bits,
+                                 storage="i16")
+
+
+@pytest.fixture(scope="module")
+def cases16():
+    out = {}
+    d1, q1 = synth.config_data(1, n=3000, nq=64)
+    out["hp"] = Case16("hp", d1, q1, O.HP, 16, 1)
+    d2, q2 = synth.config_data(2, n=20000, nq=100)
+    out["fht"] = Case16("fht", d2, q2, O.FHTCP, 24, 3)
+    d3, q3 = synth.config_data(4, n=4000, nq=40)
+    out["hp_pool"] = Case16("hp_pool", d3[:, :64].copy(), q3[:, :64].copy(), O.HP, 20, 2, O.POOL, 512)
+    out["fht_long"] = Case16("fht_long", d2[:8000, :40].copy(), q2[:40, :40].copy(), O.FHTCP, 48, 6)
+    out["hp_tensor"] = Case16("hp_tensor", d1, q1, O.HP, 16, 11, O.TENSOR)
+    return out
+
+
+@pytest.mark.parametrize("name", ["hp", "fht", "hp_pool", "fht_long", "hp_tensor"])
+def test_int16_rows_and_tables_bit_exact(cases16, name):
+    c = cases16[name]
+    assert np.array_equal(c.gpu.export_data16(), c.orc.data16())
+    for j in (0, c.orc.L - 1):
+        tab = c.gpu.export_table(j)
+        codes, ids = c.orc.rep(j)
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes)
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids)
+    with pytest.raises(pfg.PfgError):
+        c.gpu.export_data()   # the fp32 rows are not kept
+
+
+@pytest.mark.parametrize("name", ["hp", "fht", "hp_pool", "fht_long"])
+@pytest.mark.parametrize("R", [8, 16])
+@pytest.mark.parametrize("recall", [0.5, 0.9, 0.99])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_search_parity_int16(cases16, name, R, recall, engine):
+    _compare(cases16[name], 10, recall, dict(rep_chunk=R, engine=engine), dict(rep_chunk=R))
+
+
+@pytest.mark.parametrize("name", ["hp", "fht_long"])
+@pytest.mark.parametrize("k", [1, 33])
+def test_search_parity_int16_wide_and_k(cases16, name, k, monkeypatch):
+    monkeypatch.setenv("PFG_LOOP_MIN", "1")
+    monkeypatch.setenv("PFG_LOOP_MAX", "1000000")
+    _compare(cases16[name], k, 0.99, dict(rep_chunk=8, wide=16), dict(rep_chunk=8))
+
+
+@pytest.mark.parametrize("recall", [0.9, 1.0])
+def test_search_parity_int16_tensor_and_exhaustive(cases16, recall):
+    _compare(cases16["hp_tensor"], 10, recall, dict(), dict(), trace=recall < 1.0)
+    _compare(cases16["hp"], 10, recall, dict(rep_chunk=8), dict(rep_chunk=8), trace=recall < 1.0)
+
+
+def test_int16_save_load(cases16, tmp_path):
+    c = cases16["fht"]
+    path = str(tmp_path / "i16.pfg")
+    c.gpu.save(path)
+    g2 = pfg.Index.load(path)
+    assert np.array_equal(g2.export_data16(), c.gpu.export_data16())
+    q = _cuda(c.q)
+    a, b = c.gpu.search(q, 10, 0.9), g2.search(q, 10, 0.9)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])

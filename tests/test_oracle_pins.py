@@ -490,3 +490,53 @@ def test_generator_paper_synthetic():
     assert abs(S[:, -1].mean() - 0.5) < 0.02
     assert abs(S[:, :-1].mean()) < 0.02
     assert np.mean(np.argmax(S, axis=1) == 4999) >= 0.99
+
+
+# ------------------------------------------------------------------ R-25 16-bit fixed point
+def test_fixed16_golden():
+    # insert((1,0,0)) -> (32767, 0, 0) (round(1 * 2^15) clamped); -1 is representable;
+    # ties go to even (rint under the default rounding mode)
+    v = np.array([1.0, 0.0, -1.0, 0.5, -0.25, 1.5 / 32768, 2.5 / 32768, -0.5 / 32768, -1.5 / 32768, 0.999999],
+                 np.float32)
+    assert O.fixed16(v).tolist() == [32767, 0, -32768, 16384, -8192, 2, 2, 0, -2, 32767]
+
+
+def test_sim16_within_spec_bound_of_double():
+    # for 10^4 random unit-vector pairs |fixed - float inner product| <= 2e-3
+    rng = np.random.default_rng(11)
+    a = O.normalize(rng.standard_normal((10_000, 100)).astype(np.float32))
+    b = O.normalize(rng.standard_normal((10_000, 100)).astype(np.float32))
+    a16, b16 = O.fixed16(a.ravel()).reshape(a.shape), O.fixed16(b.ravel()).reshape(b.shape)
+    err = max(abs(O.sim16(a16[i], b16[i]) - float(a[i].astype(np.float64) @ b[i].astype(np.float64)))
+              for i in range(0, 10_000, 7))
+    assert err <= 2e-3
+    # exact integer arithmetic: symmetric, and a unit vector with itself within the rounding of d
+    # coordinates (|q - x 2^15| <= 1/2 each)
+    assert O.sim16(a16[0], b16[0]) == O.sim16(b16[0], a16[0])
+    assert abs(O.sim16(a16[3], a16[3]) - 1.0) <= 100 * 2.0 ** -15
+
+
+def test_sim16_is_the_exact_integer_sum():
+    # the scaled sum equals the int64 dot of the codes (numpy) rounded to fp32 -- no summation
+    # order enters (R-25)
+    rng = np.random.default_rng(5)
+    a = O.fixed16(O.normalize(rng.standard_normal((1, 960)).astype(np.float32)).ravel())
+    b = O.fixed16(O.normalize(rng.standard_normal((1, 960)).astype(np.float32)).ravel())
+    exact = int(np.dot(a.astype(np.int64), b.astype(np.int64)))
+    assert O.sim16(a, b) == np.float32(exact) * np.float32(2.0 ** -30)
+
+
+def test_int16_storage_recall_on_config1():
+    # the adaptive search with fixed-point inner products still meets the recall target (filter on)
+    c = synth.CONFIGS[1]
+    data, q = synth.config_data(1)
+    o = O.OracleIndex(data, O.HP, L=c["reps"], seed=1, storage="i16")
+    ids, sims, tr = o.search(q, c["k"], c["recall"], rep_chunk=8)
+    bi, bs = O.bruteforce(o.data(), O.normalize(q), c["k"])
+    hit = np.mean([len(set(ids[r]) & set(bi[r])) / c["k"] for r in range(len(q))])
+    assert hit >= 0.87
+    # every returned similarity is the fixed-point inner product of that pair
+    x16, q16 = o.data16(), O.fixed16(O.normalize(q).ravel()).reshape(q.shape)
+    for r in range(0, len(q), 9):
+        for t in range(c["k"]):
+            assert sims[r, t] == np.float32(O.sim16(q16[r], x16[ids[r, t]]))
