@@ -162,6 +162,15 @@ def profiled_traffic(cfg):
 
 
 # ---------------------------------------------------------------------------- reference arm
+def profiled_ksims_traffic(cfg):
+    """DRAM bytes per k_sims launch (all launches of one search, ncu --set full) if captured"""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", f"ksims_traffic_config{cfg}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)
+
+
 def run_reference(args):
     """The CPU oracle as it stands (test infrastructure), timed on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -327,13 +336,17 @@ def main():
     phase_ms = {}
     launches = 0
     stats = None
+    # timing = 3: CUDA events around every bulk k_sims launch of the timed steps (the dominant
+    # kernel's roofline below), accumulated by the library on the search stream
+    sopts_t = dict(sopts, timing=3)
+    idx.index.kernel_timing(reset=True)
     for s in range(args.steps):
         flush.fill_(s & 0xff)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        res = idx.search(q, k, args.recall, **sopts)
+        res = idx.search(q, k, args.recall, **sopts_t)
         e1.record(stream)
         barrier()
         step_ms.append(e0.elapsed_time(e1))
@@ -343,9 +356,11 @@ def main():
 
         launches += nl + (1 if world > 1 else 0)
     clocks = sampler.stop() if sampler else None
+    ksims_ms, ksims_launches = idx.index.kernel_timing(reset=True)
     # per-query counters (algorithmic bytes, stop depths) from one more, untimed search of the same
     # batch; the search is deterministic, so they are the counters of the timed steps
     ids, sims, stats = idx.search(q, k, args.recall, stats=True, **sopts)[:3]
+    rstats = idx.index.round_stats() if args.engine == 0 else None
     # per-phase breakdown of the query kernels from untimed searches with events between phases
     for _ in range(3):
         idx.search(q, k, args.recall, **dict(sopts, timing=2))
@@ -398,6 +413,26 @@ def main():
         kern_s = statistics.mean(kern_ms) / 1e3
         achieved = ab / kern_s / 1e9
         traffic, traffic_src = profiled_traffic(args.config) if args.storage == "f32" else (None, None)
+        # the dominant kernel (k_sims, the bulk similarity gathers): algorithmic bytes per launch =
+        # rows it computed x (row bytes + 16 B of pool entry: id, query, key) / launches per search,
+        # over its average launch duration (CUDA events around every launch of the timed steps)
+        ksims_roofline = None
+        if rstats and ksims_launches:
+            row_b = 2 * d if args.storage == "i16" else 4 * d
+            per_search = rstats["sims_rows"] * (row_b + 16)
+            per_launch = per_search * args.steps / ksims_launches
+            launch_s = ksims_ms / ksims_launches / 1e3
+            ks_tr = profiled_ksims_traffic(args.config) if args.storage == "f32" else None
+            ksims_roofline = {"bound": "hbm", "kernel": "k_sims (bulk candidate-row gathers + dot products, "
+                                                        "the largest share of the query phase)",
+                              "achieved": per_launch / launch_s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                              "frac": per_launch / launch_s / 1e9 / pk["hbm_gbs"],
+                              "traffic": ks_tr["dram_bytes_per_launch"] if ks_tr else None,
+                              "traffic_source": ks_tr["source"] if ks_tr else None,
+                              "alg_bytes_per_launch": per_launch, "launch_ms": launch_s * 1e3,
+                              "launches": ksims_launches, "share_of_query_phase":
+                                  ksims_ms / args.steps / statistics.mean(kern_ms),
+                              "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"}
         cpu = None
         if not args.no_cpu_baseline:
             try:
@@ -427,13 +462,15 @@ def main():
                        "parallelism": f"data-sharded x{world}" if world > 1 else "single GPU"},
             "recall": rec,
             "build_s": build_s,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "roofline": ksims_roofline,
+            "roofline_query_phase": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "query phase: bulk rounds (k_expand, k_scan, k_dedupe, k_sims, k_merge) "
                                    "+ fused tail (k_query), one search call",
                          "kernel_ms": statistics.mean(kern_ms), "phases_ms_untimed": phase_ms,
                          "prep_ms": statistics.mean(prep_ms), "alg_bytes_per_query": ab / nq,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
+            "round_stats": rstats,
             "counters": {"emitted_per_q": float(np.mean(stats["emitted"])),
                          "evaluated_per_q": float(np.mean(stats["evaluated"])),
                          "filtered_per_q": float(np.mean(stats["filtered"])),

@@ -105,7 +105,9 @@ typedef struct {
                                  to trace_ids[nq][trace_cap] (uint32, local row ids) */
     int32_t timing;           /* [0] 1: record CUDA events around the phases of this call on `stream`
                                  (read back with pfg_last_timing); 2: also between the query-phase
-                                 kernels (pfg_last_phases; the extra events cost a few microseconds each) */
+                                 kernels (pfg_last_phases; the extra events cost a few microseconds each);
+                                 3: events around each bulk-round k_sims launch only, accumulated over
+                                 searches (pfg_kernel_timing) */
     uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
     int32_t engine;           /* [0] 0 = bulk rounds (one chunk of every active query per round, split
                                  into data-parallel phases), then the fused kernel resumes the queries
@@ -238,6 +240,18 @@ pfg_status pfg_last_timing(const pfg_index* idx, float* ms3, int32_t* launches);
  * resumed queries), ms[7] the device-side round loop (a CUDA graph; its rounds are not split into
  * phases).  n: entries to write (<= 8). */
 pfg_status pfg_last_phases(const pfg_index* idx, float* ms, int32_t n);
+
+/* Launch durations of one kernel accumulated over the searches that set opts->timing = 3 since
+ * the last reset (CUDA events on the search stream around each launch; waits for them):
+ * kernel 0 = k_sims of the blind bulk rounds.  *ms = summed duration, *launches = launches timed;
+ * reset != 0 clears the accumulator afterwards. */
+pfg_status pfg_kernel_timing(pfg_index* idx, int32_t kernel, int32_t reset, double* ms, int64_t* launches);
+
+/* Counters of the last search's round engine (waits for it): out[0] rows whose similarity the
+ * bulk k_sims computed, out[1] blind rounds, out[2] device-side loop rounds, out[3] queries the
+ * fused kernel took beside the loop, out[4] after it, out[5] visit-tag arrays used (wide queries).
+ * n: entries to write (<= 6). */
+pfg_status pfg_round_stats(pfg_index* idx, uint64_t* out, int32_t n);
 
 void pfg_free(pfg_index* idx);
 const char* pfg_last_error(void);

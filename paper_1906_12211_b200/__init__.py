@@ -31,7 +31,7 @@ STATUS = {0: "PFG_OK", 1: "PFG_E_ARG", 2: "PFG_E_ZERO_VECTOR", 3: "PFG_E_BUDGET"
 # symbols include/pfg.h declares (checked by tests/test_abi.py)
 EXPORTED = ["pfg_build", "pfg_search", "pfg_merge_topk", "pfg_index_info", "pfg_derive_reps", "pfg_export",
             "pfg_hash_queries", "pfg_stop_tables", "pfg_last_timing", "pfg_last_phases", "pfg_free", "pfg_last_error",
-            "pfg_abi_version", "pfg_save", "pfg_load"]
+            "pfg_abi_version", "pfg_save", "pfg_load", "pfg_kernel_timing", "pfg_round_stats"]
 
 
 class PfgError(RuntimeError):
@@ -105,6 +105,10 @@ def lib() -> C.CDLL:
         L.pfg_last_error.argtypes = []
         L.pfg_abi_version.restype = C.c_int32
         L.pfg_abi_version.argtypes = []
+        L.pfg_kernel_timing.restype = S
+        L.pfg_kernel_timing.argtypes = [P, C.c_int32, C.c_int32, P, P]
+        L.pfg_round_stats.restype = S
+        L.pfg_round_stats.argtypes = [P, P, C.c_int32]
         L.pfg_save.restype = S
         L.pfg_save.argtypes = [P, C.c_char_p, P]
         L.pfg_load.restype = S
@@ -263,6 +267,21 @@ class Index:
         ms = (C.c_float * 8)()
         _check(lib().pfg_last_phases(self._h, ms, 8))
         return {name: float(ms[i]) for i, name in enumerate(self.PHASES)}
+
+    def kernel_timing(self, reset: bool = False):
+        """(summed ms, launches) of the bulk k_sims launches of searches with timing=3 (pfg_kernel_timing)"""
+        ms, n = C.c_double(0), C.c_int64(0)
+        _check(lib().pfg_kernel_timing(self._h, 0, int(reset), C.byref(ms), C.byref(n)))
+        return float(ms.value), int(n.value)
+
+    ROUND_STATS = ("sims_rows", "blind_rounds", "loop_rounds", "fused_beside_loop", "fused_after_loop",
+                   "wide_arrays")
+
+    def round_stats(self) -> dict:
+        """round-engine counters of the last search (pfg_round_stats)"""
+        out = (C.c_uint64 * 6)()
+        _check(lib().pfg_round_stats(self._h, out, 6))
+        return {name: int(out[i]) for i, name in enumerate(self.ROUND_STATS)}
 
     def search(self, queries, k: int, recall: float, stats: bool = False, trace_cap: int = 0, out=None,
                stream=None, **sopts):

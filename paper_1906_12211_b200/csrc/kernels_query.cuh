@@ -68,6 +68,7 @@ struct RoundCtl {
     uint32_t wdefer;       // wide chunks deferred for want of wide tiles (the host grows the buffer)
     uint32_t pad2;
     unsigned long long evsum, emsum;  // evaluated ids and emitted positions of the finished queries
+    unsigned long long sims_rows;     // pool rows the bulk k_sims launches computed
 };
 struct RoundState {
     int32_t* lvl;       // [nq] next level i to process (K..1); 0 = only the i = 0 scan remains

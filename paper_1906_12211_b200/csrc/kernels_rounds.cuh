@@ -731,6 +731,7 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
     const RoundState& rs = p.rs;
     const uint32_t top = min(rs.ctl->pool_top[par], rs.pool_cap);
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&rs.ctl->sims_rows, (unsigned long long)top);
     // lane r < NR holds entry b + r of the current step (rows beyond the end repeat the last);
     // the next step's entries are fetched before the current rows are read
     auto fetch = [&](int64_t b, uint32_t& id, uint32_t& qq) {

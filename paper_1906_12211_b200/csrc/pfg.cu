@@ -405,11 +405,18 @@ struct pfg_index {
     std::vector<int> pkind;
     int pev_n = 0;
     float last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // timing = 3: event pairs around each bulk k_sims launch, accumulated across searches
+    std::vector<cudaEvent_t> kev;
+    int64_t kev_n = 0;          // pairs recorded and not yet summed
+    double kev_ms = 0.0;        // summed durations since the last reset
+    int64_t kev_launches = 0;
     int last_launches = 0;
     ~pfg_index() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         for (auto& e : pev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : kev)
             if (e) cudaEventDestroy(e);
         if (h_ctl) cudaFreeHost(h_ctl);
         if (h_ctl2) cudaFreeHost(h_ctl2);
@@ -909,6 +916,20 @@ pfg_status dbg_sync(const char* what) {
     return PFG_OK;
 }
 
+// timing = 3: sum the recorded k_sims event pairs (waits for the last one) into kev_ms
+pfg_status fold_kernel_timing(pfg_index* I) {
+    if (I->kev_n == 0) return PFG_OK;
+    PFG_CUDA(cudaEventSynchronize(I->kev[2 * I->kev_n - 1]));
+    for (int64_t i = 0; i < I->kev_n; ++i) {
+        float ms = 0.0f;
+        PFG_CUDA(cudaEventElapsedTime(&ms, I->kev[2 * i], I->kev[2 * i + 1]));
+        I->kev_ms += ms;
+    }
+    I->kev_launches += I->kev_n;
+    I->kev_n = 0;
+    return PFG_OK;
+}
+
 // phases of pfg_last_phases: 0 expand, 1 scan, 2 dedupe, 3 sims, 4 merge, 5 fused kernel,
 // 6 other query-phase work (round control, query order, code extension)
 enum { kPhExpand = 0, kPhScan, kPhDedupe, kPhSims, kPhMerge, kPhFused, kPhOther, kPhLoop, kPhEnd = -1 };
@@ -1392,7 +1413,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const unsigned tb_s = (unsigned)(I->num_sms * 8);
         const unsigned sb = (unsigned)(I->num_sms * PFG_SIMS_MINB);
         int round = 0;
-        const bool tm = s.timing >= 2;
+        const bool tm = s.timing == 2;
+        const bool ksims_timed = s.timing == 3;
         // one round: expand, scan, dedupe, sims, merge of list `par` (phase events unless captured)
         auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp) -> pfg_status {
             using PP = decltype(pp);
@@ -1413,8 +1435,22 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             k_dedupe<PP><<<qb_d, 128, dsm, rst>>>(pp, par);
             if (rst == st) PFG_TRY(dbg_sync("k_dedupe"));
             PFG_TRY(phase_mark(I, marks, kPhSims, rst));
+            const bool kt = ksims_timed && rst == st;
+            if (kt) {
+                if ((int64_t)I->kev.size() < 2 * (I->kev_n + 1)) {
+                    // fold the pairs recorded so far (all earlier on this stream) before reusing them
+                    if (I->kev_n >= 512) PFG_TRY(fold_kernel_timing(I));
+                    while ((int64_t)I->kev.size() < 2 * (I->kev_n + 1)) {
+                        cudaEvent_t e;
+                        PFG_CUDA(cudaEventCreate(&e));
+                        I->kev.push_back(e);
+                    }
+                }
+                PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n], rst));
+            }
             if (g.storage == PFG_STORAGE_I16) k_sims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
             else k_sims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
+            if (kt) PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n++ + 1], rst));
             if (rst == st) PFG_TRY(dbg_sync("k_sims"));
             PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_merge<PP, true><<<qb_m, 128, msm, rst>>>(pp, par);
@@ -1578,7 +1614,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     PFG_TRY(join_sketches(I, st));
     PFG_TRY(late_join(I, st));
     if (fused_n > 0) {
-        PFG_TRY(phase_mark(I, s.timing >= 2, kPhFused, st));
+        PFG_TRY(phase_mark(I, s.timing == 2, kPhFused, st));
         PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((fused_n + 3) / 4, max_blocks));  // rounds: nq bound
         switch (epl) {
@@ -1592,7 +1628,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->launches += 1;
     }
     I->last_fused = fused_n;
-    PFG_TRY(phase_mark(I, s.timing >= 2, kPhEnd, st));
+    PFG_TRY(phase_mark(I, s.timing == 2, kPhEnd, st));
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[2], st));
     I->timing_pending = s.timing;
     if (!ids_dev) PFG_CUDA(cudaMemcpyAsync(out_ids, d_ids, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, st));
@@ -1667,7 +1703,7 @@ static pfg_status collect_timing(pfg_index* I) {
     PFG_CUDA(cudaEventElapsedTime(&I->last_ms[0], I->ev[0], I->ev[1]));
     PFG_CUDA(cudaEventElapsedTime(&I->last_ms[1], I->ev[1], I->ev[2]));
     PFG_CUDA(cudaEventElapsedTime(&I->last_ms[2], I->ev[0], I->ev[2]));
-    if (I->timing_pending >= 2) PFG_TRY(phase_collect(I));
+    if (I->timing_pending == 2) PFG_TRY(phase_collect(I));
     I->timing_pending = 0;
     return PFG_OK;
 }
@@ -1678,6 +1714,30 @@ pfg_status pfg_last_phases(const pfg_index* I, float* ms, int32_t n) {
     std::lock_guard<std::mutex> lock(W->mu);
     PFG_TRY(collect_timing(W));
     for (int i = 0; i < n && i < 8; ++i) ms[i] = I->last_phase_ms[i];
+    return PFG_OK;
+}
+
+pfg_status pfg_kernel_timing(pfg_index* I, int32_t kernel, int32_t reset, double* ms, int64_t* launches) {
+    if (!I) return fail(PFG_E_ARG, "NULL index");
+    if (kernel != 0) return fail(PFG_E_ARG, "kernel must be 0 (k_sims)");
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    PFG_TRY(fold_kernel_timing(I));
+    if (ms) *ms = I->kev_ms;
+    if (launches) *launches = I->kev_launches;
+    if (reset) { I->kev_ms = 0.0; I->kev_launches = 0; }
+    return PFG_OK;
+}
+
+pfg_status pfg_round_stats(pfg_index* I, uint64_t* out, int32_t n) {
+    if (!I || !out || n < 0) return fail(PFG_E_ARG, "NULL index or output");
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    if (I->nsearch == 0 || !I->h_ctl2) return fail(PFG_E_STATE, "no round-engine search yet");
+    if (I->ev_done) PFG_CUDA(cudaEventSynchronize(I->ev_done));
+    const RoundCtl* c = I->h_ctl2 + ((I->nsearch - 1) & 1);
+    const uint64_t v[6] = {c->sims_rows, (uint64_t)I->last_rounds, c->round, c->nfused, c->nfused2, c->wnext};
+    for (int i = 0; i < n && i < 6; ++i) out[i] = v[i];
     return PFG_OK;
 }
 
