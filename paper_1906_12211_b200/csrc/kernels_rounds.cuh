@@ -656,8 +656,12 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
             rc[2] = c->dcnt[lane];
         }
         if (lane == 0) { rs.poff[q] = base; rs.pn[q] = ns; }
-        // carry a large set to the next round (the fused kernel rebuilds it from E instead)
-        if (nE + ns > (uint32_t)kSaveMin) {
+        // carry a large set to the next round (the fused kernel rebuilds it from E instead) --
+        // unless the chunk was cut short by chunk_reps: then the k-th similarity before the chunk
+        // already meets the stop threshold of its last repetition, so the query stops this round
+        const int ci = rs.lvl[q], cc0 = rs.c0[q];
+        const int nominal = min((ci == p.K && cc0 == 0 && !p.uniform) ? 1 : p.R, p.L - cc0);
+        if (nE + ns > (uint32_t)kSaveMin && nr >= nominal) {
             if (lane == 0 && !saved) rs.flags[q] |= kFlagSaved;
 #pragma unroll
             for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
