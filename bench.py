@@ -183,7 +183,7 @@ def run_reference(args):
     import paper_1906_12211_b200 as pfg
     L = c["reps"] or pfg.derive_reps(n, c["d"], c["family"], c["budget"],
                                      strategy=c["strategy"])[0]
-    fam = O.HP if c["family"] == "simhash" else O.FHTCP
+    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
     strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
     t0 = time.time()
     X = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
@@ -229,7 +229,7 @@ def cpu_baseline_leg(cfg, recall, rep_chunk, sample):
                 "sample": f"not run: config {cfg}'s oracle setup ({c['n']} x {c['d']}) exceeds the bounded CPU budget"}
     data, q = synth.config_data(cfg)
     L = c["reps"] or pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
-    fam = O.HP if c["family"] == "simhash" else O.FHTCP
+    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
     strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
     t0 = time.time()
     X = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)

@@ -48,8 +48,13 @@ typedef enum {
 /* LSH families (§2, 338-343 §4.3) */
 typedef enum {
     PFG_SIMHASH = 0,               /* random hyperplane (HP): 1 bit = [<a,x> >= 0], a ~ N(0, I) */
-    PFG_CROSSPOLYTOPE_FHT = 1      /* cross-polytope via three rounds of random signs + fast Hadamard
+    PFG_CROSSPOLYTOPE_FHT = 1,     /* cross-polytope via three rounds of random signs + fast Hadamard
                                       transform: ell = 1 + log2(d') bits, d' = 2^ceil(log2 d) */
+    PFG_CROSSPOLYTOPE = 2          /* exact cross-polytope: d Gaussian hyperplanes
+                                      a_1..a_d per function, code = index of the largest |<a_i,x>| (ties to
+                                      the lowest i) with the sign as the most significant of ell = 1 +
+                                      ceil(log2 d) bits; each <a_i,x> is the sequential fp32 fmaf chain
+                                      (R-2 projections); d <= 256; independent or pool strategy */
 } pfg_family;
 
 /* hash-function evaluation strategies (§3.2, App. B 841-917) */

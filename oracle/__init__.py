@@ -21,7 +21,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-HP, FHTCP = 0, 1
+HP, FHTCP, CP = 0, 1, 2
 INDEPENDENT, POOL, TENSOR = 0, 1, 2
 
 
@@ -51,6 +51,7 @@ def lib():
         L.or_hp_bit.restype = C.c_int; L.or_hp_bit.argtypes = [P, P, C.c_int]
         L.or_fht.restype = None; L.or_fht.argtypes = [P, C.c_int]
         L.or_fhtcp_code.restype = C.c_uint32; L.or_fhtcp_code.argtypes = [P, C.c_int, C.c_int, P]
+        L.or_cp_code.restype = C.c_uint32; L.or_cp_code.argtypes = [P, P, C.c_int, C.c_int]
         L.or_cp_table.restype = None
         L.or_cp_table.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, P, P]
         L.or_build.restype = P
@@ -161,6 +162,14 @@ def fht(y) -> np.ndarray:
 def fhtcp_code(x, dp: int, signs) -> int:
     x, s = _f32(x), _f32(signs)
     return int(lib().or_fhtcp_code(_p(x), x.shape[0], dp, _p(s)))
+
+
+def cp_code(A, x) -> int:
+    """exact cross-polytope value of x under hyperplanes A [d][d]"""
+    A, x = _f32(A), _f32(x)
+    d = x.shape[0]
+    ell = 1 + int(np.ceil(np.log2(d))) if d > 1 else 1
+    return int(lib().or_cp_code(_p(A), _p(x), d, ell))
 
 
 def cp_table(family: int, d: int, seed: int, draws: int = 1000):

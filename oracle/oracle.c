@@ -36,7 +36,7 @@
 #define OR_GAMMA 0x9E3779B97F4A7C15ULL
 
 enum { OR_TAG_HP = 1, OR_TAG_SKETCH = 2, OR_TAG_FHT = 3, OR_TAG_POOL = 4,
-       OR_TAG_SLOT = 5, OR_TAG_TENSOR = 6, OR_TAG_CPMC = 7 };
+       OR_TAG_SLOT = 5, OR_TAG_TENSOR = 6, OR_TAG_CPMC = 7, OR_TAG_CP = 8 };
 
 uint64_t or_mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -156,7 +156,7 @@ uint32_t or_fhtcp_code(const float* x, int d, int dp, const float* sg) {
 /* ----------------------------------------------------------------------------
  * Index (§4.2): L arrays of (hash code, pos) sorted by code.
  * -------------------------------------------------------------------------- */
-enum { OR_HP = 0, OR_FHTCP = 1 };
+enum { OR_HP = 0, OR_FHTCP = 1, OR_CP = 2 };
 enum { OR_INDEPENDENT = 0, OR_POOL = 1, OR_TENSOR = 2 };
 
 typedef struct {
@@ -182,8 +182,25 @@ typedef struct {
 static int or_funcs_per_rep(int K, int ell) { return (K + ell - 1) / ell; }
 
 /* value of pool/independent function f on x (ell bits) */
+/* PAPER.md:147-151 §2 exact cross-polytope: "choosing d random hyperplanes a_1..a_d and mapping x
+ * to the index of the hyperplane with the largest absolute inner product, separating the two
+ * cases that the inner product is negative or not".  A = [d][d] (row i = a_i); each <a_i, x> is
+ * or_dot (R-2 projections); ties of |y_i| go to the lowest i; the sign is the most significant of
+ * the ell = ceil(log 2d) bits (R-5). */
+uint32_t or_cp_code(const float* A, const float* x, int d, int ell) {
+    int best = 0;
+    float y0 = or_dot(A, x, d), ba = fabsf(y0);
+    int neg = y0 < 0.0f;
+    for (int i = 1; i < d; ++i) {
+        float y = or_dot(A + (int64_t)i * d, x, d);
+        if (fabsf(y) > ba) { ba = fabsf(y); best = i; neg = y < 0.0f; }
+    }
+    return ((uint32_t)neg << (ell - 1)) | (uint32_t)best;
+}
+
 static uint32_t or_func(const or_index* X, int64_t f, const float* x) {
     if (X->family == OR_HP) return (uint32_t)or_hp_bit(X->hp + f * X->d, x, X->d);
+    if (X->family == OR_CP) return or_cp_code(X->hp + f * X->d * (int64_t)X->d, x, X->d, X->ell);
     return or_fhtcp_code(x, X->d, X->dp, X->sg + f * 3 * (int64_t)X->dp);
 }
 
@@ -267,6 +284,28 @@ void or_cp_table(int family, int d, uint64_t seed, int draws, double* T /* [(ell
     for (int a = 0; a < 41; ++a) {
         double alpha = -1.0 + 0.05 * a;
         float xf[4096], yf[4096], sg[3 * 4096], hpa[4096];
+        if (family == OR_CP) {
+            /* exact CP: the paper's canonical pair x = e_0, y = (alpha, sqrt(1 - alpha^2), 0, ...)
+             * (valid by spherical symmetry); only the first two coordinates of
+             * each hyperplane enter: a_i0 = gauss(k, 2i), a_i1 = gauss(k, 2i+1) */
+            float yx = (float)alpha, yy = (float)sqrt(fmax(0.0, 1.0 - alpha * alpha));
+            for (int t = 0; t < draws; ++t) {
+                uint64_t k = or_draw(K, (uint64_t)a * draws + t);
+                float bx = -1.0f, by = -1.0f;
+                int ix = 0, iy = 0, nx = 0, ny = 0;
+                for (int i = 0; i < d; ++i) {
+                    float a0 = (float)or_gauss(k, 2 * (uint64_t)i), a1 = (float)or_gauss(k, 2 * (uint64_t)i + 1);
+                    float sx = fmaf(a0, 1.0f, 0.0f);
+                    float sy = fmaf(a1, yy, fmaf(a0, yx, 0.0f));
+                    if (fabsf(sx) > bx) { bx = fabsf(sx); ix = i; nx = sx < 0.0f; }
+                    if (fabsf(sy) > by) { by = fabsf(sy); iy = i; ny = sy < 0.0f; }
+                }
+                uint32_t hx = ((uint32_t)nx << (ell - 1)) | (uint32_t)ix, hy = ((uint32_t)ny << (ell - 1)) | (uint32_t)iy;
+                for (int b = 1; b <= ell; ++b)
+                    if ((hx >> (ell - b)) == (hy >> (ell - b))) cnt[b * 41 + a]++;
+            }
+            continue;
+        }
         for (int t = 0; t < draws; ++t) {
             uint64_t kat = or_draw(K, (uint64_t)a * draws + t);
             uint64_t ksg = or_draw(kat, 0), kx = or_draw(kat, 1), ku = or_draw(kat, 2);
@@ -326,6 +365,11 @@ or_index* or_build(const float* raw, int64_t n, int d, int family, int strategy,
         uint64_t kh = or_stream_key(seed, OR_TAG_HP);
         X->hp = (float*)malloc(sizeof(float) * F * d);
         for (int64_t i = 0; i < F * d; ++i) X->hp[i] = or_gauss(kh, (uint64_t)i);
+    } else if (family == OR_CP) {
+        /* exact CP: function f = d hyperplanes of d coordinates, element (f d + i) d + t */
+        uint64_t kc = or_stream_key(seed, OR_TAG_CP);
+        X->hp = (float*)malloc(sizeof(float) * F * d * d);
+        for (int64_t i = 0; i < F * d * d; ++i) X->hp[i] = or_gauss(kc, (uint64_t)i);
     } else {
         uint64_t kf = or_stream_key(seed, OR_TAG_FHT);
         X->sg = (float*)malloc(sizeof(float) * F * 3 * X->dp);
@@ -376,7 +420,7 @@ or_index* or_build(const float* raw, int64_t n, int d, int family, int strategy,
     X->ids = (uint32_t**)calloc(L, sizeof(uint32_t*));
     if (!lazy)
         for (int j = 0; j < L; ++j) or_build_rep(X, j);
-    if (family == OR_FHTCP) { int e; or_cp_table(OR_FHTCP, d, seed, cp_draws, X->cpT, &e); }
+    if (family == OR_FHTCP || family == OR_CP) { int e; or_cp_table(family, d, seed, cp_draws, X->cpT, &e); }
     return X;
 }
 

@@ -19,7 +19,9 @@ from ._build import LIB as _LIB_PATH
 SIMHASH, CROSSPOLYTOPE_FHT = 0, 1
 DEFAULT_REP_CHUNK = 16  # R of pfg_search_opts (R-17); measured best on config 2
 INDEPENDENT, POOL, TENSOR = 0, 1, 2
-FAMILIES = {"simhash": SIMHASH, "hp": SIMHASH, "fht_cp": CROSSPOLYTOPE_FHT, "crosspolytope_fht": CROSSPOLYTOPE_FHT}
+CROSSPOLYTOPE = 2
+FAMILIES = {"simhash": SIMHASH, "hp": SIMHASH, "fht_cp": CROSSPOLYTOPE_FHT, "crosspolytope_fht": CROSSPOLYTOPE_FHT,
+            "cp": CROSSPOLYTOPE, "crosspolytope": CROSSPOLYTOPE}
 STRATEGIES = {"independent": INDEPENDENT, "pool": POOL, "tensor": TENSOR}
 
 EXPORT_TABLE, EXPORT_PREFIX, EXPORT_SKETCH, EXPORT_DATA, EXPORT_CP, EXPORT_SLOTS, EXPORT_POOLSEL = 1, 2, 3, 4, 5, 6, 7

@@ -361,6 +361,41 @@ __global__ void __launch_bounds__(256) k_fht_funcs(const float* __restrict__ X, 
 }
 
 // repetition codes from pooled FHT-CP codes: full = concat(fc[p][sel[j][t]]), code = top K bits
+// exact cross-polytope (PFG_CROSSPOLYTOPE): function f is d Gaussian hyperplanes
+// A_f[i] (rows of lda floats); value = index of the largest |<A_f[i], x>| (ties to the lowest i),
+// sign as the most significant of ell bits; each <A_f[i], x> is the sequential fmaf chain over t
+// (R-2 projections).  Thread per (row p, function f = blockIdx.y), four hyperplanes per pass over
+// x (one load of x[t] feeds four chains; A_f's rows are the same for the whole block: broadcast).
+__global__ void __launch_bounds__(128) k_cp_funcs(const float* __restrict__ X, int64_t np, int ldx,
+                                                  const float* __restrict__ A, int nfun, int d, int lda, int ell,
+                                                  uint16_t* __restrict__ out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = blockIdx.y;
+    if (p >= np) return;
+    const float* x = X + p * ldx;
+    const float* Af = A + (int64_t)f * d * lda;
+    float best = -1.0f;
+    int bi = 0;
+    bool neg = false;
+    for (int i0 = 0; i0 < d; i0 += 4) {
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        const int nr = min(4, d - i0);
+        for (int t = 0; t < d; ++t) {
+            const float xv = __ldg(x + t);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (r < nr) s[r] = fmaf(__ldg(Af + (int64_t)(i0 + r) * lda + t), xv, s[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if (r < nr) {
+                const float a = fabsf(s[r]);
+                if (a > best) { best = a; bi = i0 + r; neg = s[r] < 0.0f; }
+            }
+    }
+    out[p * nfun + f] = (uint16_t)((neg ? 1u << (ell - 1) : 0u) | (uint32_t)bi);
+}
+
 __global__ void k_pool_codes(const uint16_t* __restrict__ fc, int64_t np, int m, int r0, int nreps, int c,
                              int ell, int K, const int32_t* __restrict__ sel, uint64_t* __restrict__ keys,
                              uint32_t* __restrict__ codes, int ldc) {

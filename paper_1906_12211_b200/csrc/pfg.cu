@@ -128,7 +128,9 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     }
     if (n < 1 || n >= (int64_t(1) << 31)) return fail(PFG_E_ARG, "n must be in [1, 2^31)");
     if (d < 1 || d > 4096) return fail(PFG_E_ARG, "d must be in [1, 4096]");
-    if (family != PFG_SIMHASH && family != PFG_CROSSPOLYTOPE_FHT) return fail(PFG_E_ARG, "unknown family");
+    if (family != PFG_SIMHASH && family != PFG_CROSSPOLYTOPE_FHT && family != PFG_CROSSPOLYTOPE)
+        return fail(PFG_E_ARG, "unknown family");
+    if (family == PFG_CROSSPOLYTOPE && d > 256) return fail(PFG_E_ARG, "exact cross-polytope family supports d <= 256");
     g.n = n;
     g.d = d;
     {
@@ -154,12 +156,14 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
         g.ell = 1 + ilog2(g.dp);
     }
     g.c = (g.K + g.ell - 1) / g.ell;
+    if (family == PFG_CROSSPOLYTOPE && g.strategy == PFG_TENSOR)
+        return fail(PFG_E_ARG, "exact cross-polytope family: independent or pool strategy");
     if (g.strategy == PFG_TENSOR && (g.c % 2 != 0 || g.c * g.ell != g.K))
         return fail(PFG_E_ARG, "tensor strategy: prefix_bits must be an even number of whole functions (PAPER.md:245)");
     g.pool_bits = z.pool_bits ? z.pool_bits : 3072;
     g.m = g.strategy == PFG_POOL ? g.pool_bits / g.ell : 0;
     if (g.strategy == PFG_POOL && g.m < g.c) return fail(PFG_E_ARG, "pool smaller than one repetition's functions");
-    if (g.strategy == PFG_POOL && g.family == PFG_CROSSPOLYTOPE_FHT && g.m > 65535) return fail(PFG_E_ARG, "pool too large");
+    if (g.strategy == PFG_POOL && g.family != PFG_SIMHASH && g.m > 65535) return fail(PFG_E_ARG, "pool too large");
     g.cp_draws = z.cp_draws ? z.cp_draws : 1000;
     if (g.cp_draws < 1) return fail(PFG_E_ARG, "cp_draws must be >= 1");
     g.max_reps = z.max_reps ? z.max_reps : 4096;
@@ -170,7 +174,7 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     // bytes: data + sketches + sketch functions + pool functions + CP table (fixed);
     // per repetition: sorted table + 13-bit prefix table + slot + its own functions / selection
     const uint64_t N = (uint64_t)n;
-    const uint64_t fn_hp = 4ull * g.dpad, fn_fht = 3ull * g.W * 4;
+    const uint64_t fn_hp = 4ull * g.dpad, fn_fht = family == PFG_CROSSPOLYTOPE ? 4ull * g.d * g.dpad : 3ull * g.W * 4;
     const uint64_t data_bytes = g.storage == PFG_STORAGE_I16 ? 2ull * N * g.dpad16 : 4ull * N * g.dpad;
     g.fixed_bytes = data_bytes + 4ull * 64 * g.M * g.dpad + 8ull * (g.ell + 1) * 41;
     if (g.strategy == PFG_POOL) g.fixed_bytes += (uint64_t)g.m * (family == PFG_SIMHASH ? fn_hp : fn_fht);
@@ -583,6 +587,69 @@ pfg_status build_cp_table(pfg_index* I, cudaStream_t st) {
     return PFG_OK;
 }
 
+// exact CP collision table with the paper's canonical pair x = e_0,
+// y = (alpha, sqrt(1 - alpha^2), 0, ...) -- valid by the spherical symmetry of exact CP
+// (PAPER.md:349 footnote): only the first two coordinates of each hyperplane enter, drawn as
+// a_i0 = gauss(k, 2i), a_i1 = gauss(k, 2i + 1) with k = draw(stream kTagCPMC, a draws + t); each
+// inner product is the fmaf chain of R-2 over the (zero-padded) pair; then the same cleaning as the
+// FHT table (running minima over alpha, then over bits)
+void cp_exact_code_pair(const float* a0, const float* a1, int d, float yx, float yy, int ell, uint32_t& hx,
+                        uint32_t& hy) {
+    float bx = -1.0f, by = -1.0f;
+    int ix = 0, iy = 0;
+    bool nx = false, ny = false;
+    for (int i = 0; i < d; ++i) {
+        const float sx = fmaf(a0[i], 1.0f, 0.0f);
+        const float sy = fmaf(a1[i], yy, fmaf(a0[i], yx, 0.0f));
+        if (std::fabs(sx) > bx) { bx = std::fabs(sx); ix = i; nx = sx < 0.0f; }
+        if (std::fabs(sy) > by) { by = std::fabs(sy); iy = i; ny = sy < 0.0f; }
+    }
+    hx = (nx ? 1u << (ell - 1) : 0u) | (uint32_t)ix;
+    hy = (ny ? 1u << (ell - 1) : 0u) | (uint32_t)iy;
+}
+void build_cp_exact_table(pfg_index* I) {
+    const Geo& g = I->g;
+    const int draws = g.cp_draws, d = g.d, ell = g.ell;
+    const uint64_t K = stream_key(I->seed, kTagCPMC);
+    std::vector<long long> cnt((size_t)(ell + 1) * 41, 0);
+    auto work = [&](int a0_, int a1_) {
+        std::vector<float> A0(d), A1(d);
+        for (int a = a0_; a < a1_; ++a) {
+            const double alpha = -1.0 + 0.05 * a;
+            const float yx = (float)alpha, yy = (float)std::sqrt(std::max(0.0, 1.0 - alpha * alpha));
+            for (int t = 0; t < draws; ++t) {
+                const uint64_t k = draw(K, (uint64_t)a * draws + t);
+                for (int i = 0; i < d; ++i) { A0[i] = (float)gauss(k, 2ull * i); A1[i] = (float)gauss(k, 2ull * i + 1); }
+                uint32_t hx, hy;
+                cp_exact_code_pair(A0.data(), A1.data(), d, yx, yy, ell, hx, hy);
+                for (int b = 1; b <= ell; ++b)
+                    if ((hx >> (ell - b)) == (hy >> (ell - b))) cnt[b * 41 + a]++;
+            }
+        }
+    };
+    {
+        unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        const int per = (41 + (int)nt - 1) / (int)nt;
+        for (unsigned k = 0; k < nt; ++k) {
+            const int a0 = (int)k * per, a1 = std::min(41, a0 + per);
+            if (a0 < a1) th.emplace_back(work, a0, a1);
+        }
+        for (auto& t : th) t.join();
+    }
+    std::vector<double>& T = I->cpT;
+    T.assign((size_t)(ell + 1) * 41, 1.0);
+    for (int b = 1; b <= ell; ++b) {
+        for (int a = 0; a < 41; ++a) T[b * 41 + a] = (double)cnt[b * 41 + a] / (double)draws;
+        T[b * 41 + 40] = 1.0;
+        for (int a = 39; a >= 0; --a)
+            if (T[b * 41 + a + 1] < T[b * 41 + a]) T[b * 41 + a] = T[b * 41 + a + 1];
+    }
+    for (int b = 2; b <= ell; ++b)
+        for (int a = 0; a < 41; ++a)
+            if (T[(b - 1) * 41 + a] < T[b * 41 + a]) T[b * 41 + a] = T[(b - 1) * 41 + a];
+}
+
 pfg_status gen_functions(pfg_index* I, cudaStream_t st) {
     const Geo& g = I->g;
     const uint64_t seed = I->seed;
@@ -617,6 +684,24 @@ pfg_status gen_functions(pfg_index* I, cudaStream_t st) {
         PFG_TRY(I->hpfn.alloc(A.size() * 4, "hp functions"));
         PFG_CUDA(cudaMemcpyAsync(I->hpfn.p, A.data(), A.size() * 4, cudaMemcpyHostToDevice, st));
         PFG_CUDA(cudaStreamSynchronize(st));
+    } else if (g.family == PFG_CROSSPOLYTOPE) {
+        // exact CP: function f = d hyperplanes, row (f d + i) of [F d][dpad], element
+        // ((f d + i) d + t) of stream kTagCP; the independent strategy reads them through the
+        // identity selection (repetition j, position t -> function j c + t)
+        std::vector<float> A((size_t)F * g.d * g.dpad, 0.0f);
+        const uint64_t kc = stream_key(seed, kTagCP);
+        for (int64_t r = 0; r < F * g.d; ++r)
+            for (int t = 0; t < g.d; ++t) A[(size_t)r * g.dpad + t] = (float)gauss(kc, (uint64_t)(r * g.d + t));
+        PFG_TRY(I->hpfn.alloc(A.size() * 4, "cp functions"));
+        PFG_CUDA(cudaMemcpyAsync(I->hpfn.p, A.data(), A.size() * 4, cudaMemcpyHostToDevice, st));
+        PFG_CUDA(cudaStreamSynchronize(st));
+        if (g.strategy == PFG_INDEPENDENT) {
+            std::vector<int32_t> id((size_t)g.L * g.c);
+            for (size_t e = 0; e < id.size(); ++e) id[e] = (int32_t)e;
+            PFG_TRY(I->sel.alloc(id.size() * 4, "cp identity selection"));
+            PFG_CUDA(cudaMemcpyAsync(I->sel.p, id.data(), id.size() * 4, cudaMemcpyHostToDevice, st));
+            PFG_CUDA(cudaStreamSynchronize(st));
+        }
     } else {
         std::vector<uint32_t> S((size_t)F * 3 * g.W, 0u);
         const uint64_t kf = stream_key(seed, kTagFHT);
@@ -692,6 +777,20 @@ pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, u
             k_codes_from_bits<<<grd, blk, 0, st>>>(poolvals.as<uint64_t>(), np, wpr, r0, nb, g.K, I->sel.as<int32_t>(), 0,
                                                    keys, codes, ldc);
         }
+    } else if (g.family == PFG_CROSSPOLYTOPE) {
+        // all function values once (uint16 [np][F]), then each repetition's concatenation
+        const int F = g.strategy == PFG_POOL ? g.m : g.L * g.c;
+        if (!pool_ready) {
+            PFG_TRY(poolvals.ensure((size_t)np * F * 2, "cp function codes"));
+            const dim3 gb((unsigned)((np + 127) / 128), (unsigned)F);
+            k_cp_funcs<<<gb, 128, 0, st>>>(X, np, g.dpad, I->hpfn.as<float>(), F, g.d, g.dpad, g.ell,
+                                           poolvals.as<uint16_t>());
+            pool_ready = true;
+            I->launches += 1;
+        }
+        I->launches += 1;
+        k_pool_codes<<<grd, blk, 0, st>>>(poolvals.as<uint16_t>(), np, F, r0, nb, g.c, g.ell, g.K, I->sel.as<int32_t>(),
+                                          keys, codes, ldc);
     } else {
         if (g.strategy == PFG_INDEPENDENT) {
             fht_rep(X, np, g.dpad, g, I->sg.as<uint32_t>(), r0, nb, keys, codes, ldc, I->num_sms, st);
@@ -1129,6 +1228,7 @@ pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t budget, i
         PFG_CUDA(cudaStreamSynchronize(st));
     }
     if (g.family == PFG_CROSSPOLYTOPE_FHT) PFG_TRY(build_cp_table(I.get(), st));
+    if (g.family == PFG_CROSSPOLYTOPE) build_cp_exact_table(I.get());
     if (g.storage == PFG_STORAGE_I16) {
         // R-25: the inner products read 16-bit fixed-point rows; the fp32 rows were only needed
         // for hashing and sketches

@@ -13,7 +13,7 @@ namespace pfg {
 
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
 enum StreamTag : uint64_t {
-    kTagHP = 1, kTagSketch = 2, kTagFHT = 3, kTagPool = 4, kTagSlot = 5, kTagTensor = 6, kTagCPMC = 7
+    kTagHP = 1, kTagSketch = 2, kTagFHT = 3, kTagPool = 4, kTagSlot = 5, kTagTensor = 6, kTagCPMC = 7, kTagCP = 8
 };
 
 inline uint64_t mix64(uint64_t z) {

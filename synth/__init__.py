@@ -121,6 +121,10 @@ CONFIGS = {
     # and FHT-CP; not a BASELINE config, a second workload
     6: dict(name="paper-synthetic-1Mx300", n=1_000_000, d=300, nq=1_000, k=10, recall=0.9,
             family="fht_cp", strategy="pool", reps=0, budget=8 << 30),
+    # config 2's workload with the exact cross-polytope family (the paper's "CP" curve, Fig. 5,
+    # PAPER.md:588, 648-652): d Gaussian hyperplanes per function instead of FHT rotations
+    7: dict(name="clustered-1Mx100-exact-cp", n=1_000_000, d=100, nq=10_000, k=10, recall=0.9,
+            family="cp", strategy="independent", reps=0, budget=4 << 30),
 }
 
 
@@ -143,6 +147,8 @@ def config_data(cfg: int, n: int | None = None, nq: int | None = None, row0: int
     if cfg == 5:
         return (mixture(n, 100, 10_000, 0.3, 105, row0, stream=2),
                 mixture(nq, 100, 10_000, 0.3, 105, 0, stream=3))
+    if cfg == 7:
+        return config_data(2, n=n, nq=nq, row0=row0)
     if cfg == 6:
         if row0:
             raise ValueError("config 6 is generated whole (its last row is the common nearest neighbour)")

@@ -126,7 +126,7 @@ def test_config34_full(cfg):
     L = g.info["reps"]
     assert L == pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
     strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
-    fam = O.HP if c["family"] == "simhash" else O.FHTCP
+    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
     o = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
     # build side: data, slots, pool selections, two whole repetition tables with their inline
     # sketch words, prefix tables

@@ -27,7 +27,7 @@ def _cuda(a):
 class Case:
     def __init__(self, name, data, q, family, L, seed, strategy=O.INDEPENDENT, pool_bits=3072, M=32, K=24):
         self.name, self.data, self.q = name, data, q
-        fam = "simhash" if family == O.HP else "fht_cp"
+        fam = {O.HP: "simhash", O.FHTCP: "fht_cp", O.CP: "cp"}[family]
         strat = {O.POOL: "pool", O.TENSOR: "tensor"}.get(strategy, "independent")
         self.gpu = pfg.Index(_cuda(data), 0, fam, seed=seed, reps=L, strategy=strat, pool_bits=pool_bits,
                              sketch_words=M if M > 0 else -1, prefix_bits=K)
@@ -53,6 +53,10 @@ def cases():
     out["hp_tensor"] = Case("hp_tensor", d1, q1, O.HP, 16, 11, O.TENSOR)
     out["fht_tensor"] = Case("fht_tensor", d2[:8000], q2[:40], O.FHTCP, 16, 12, O.TENSOR, K=32)
     out["hp_tensor64"] = Case("hp_tensor64", d1, q1[:32], O.HP, 64, 13, O.TENSOR)
+    # exact cross-polytope (d = 32: ell = 6, 4 functions per repetition; d = 100: ell = 8)
+    out["cp"] = Case("cp", d1, q1, O.CP, 16, 21)
+    out["cp_pool"] = Case("cp_pool", d1, q1[:40], O.CP, 16, 22, O.POOL, 600)
+    out["cp100"] = Case("cp100", d2[:6000], q2[:40], O.CP, 12, 23)
     return out
 
 
@@ -520,3 +524,27 @@ def test_int16_save_load(cases16, tmp_path):
     q = _cuda(c.q)
     a, b = c.gpu.search(q, 10, 0.9), g2.search(q, 10, 0.9)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+
+# ------------------------------------------------------------------ exact cross-polytope family
+@pytest.mark.parametrize("name", ["cp", "cp_pool", "cp100"])
+def test_cp_exact_build_bit_exact(cases, name):
+    c = cases[name]
+    g, o = c.gpu, c.orc
+    assert np.array_equal(g.export_cp(), o.cp())
+    for j in range(o.L):
+        tab = g.export_table(j)
+        codes, ids = o.rep(j)
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
+    gc, _ = g.hash_queries(c.q)
+    oc, _ = o.hash(c.q)
+    assert np.array_equal(gc, oc)
+
+
+@pytest.mark.parametrize("name", ["cp", "cp_pool", "cp100"])
+@pytest.mark.parametrize("recall", [0.5, 0.9, 0.99])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_search_parity_cp_exact(cases, name, recall, engine):
+    _compare(cases[name], 10, recall, dict(rep_chunk=8, engine=engine), dict(rep_chunk=8))

@@ -540,3 +540,60 @@ def test_int16_storage_recall_on_config1():
     for r in range(0, len(q), 9):
         for t in range(c["k"]):
             assert sims[r, t] == np.float32(O.sim16(q16[r], x16[ids[r, t]]))
+
+
+# ------------------------------------------------------------------ exact cross-polytope (NEXT-2)
+def test_cp_code_identity_rotation():
+    # with the identity as hyperplanes, the code is the index of the largest |coordinate| plus the
+    # sign in the most significant bit (d = 8: ell = 4); ties go to the lowest index
+    d, ell = 8, 4
+    A = np.eye(d, dtype=np.float32)
+    e = np.zeros(d, np.float32)
+    e[3] = 1.0
+    assert O.cp_code(A, e) == 3
+    assert O.cp_code(A, -e) == (1 << (ell - 1)) | 3
+    t = np.zeros(d, np.float32)
+    t[1] = t[5] = -0.5
+    assert O.cp_code(A, t) == (1 << (ell - 1)) | 1
+    # a permutation of the hyperplanes permutes the index
+    P = np.eye(d, dtype=np.float32)[[2, 0, 1, 3, 4, 5, 6, 7]]
+    assert O.cp_code(P, e) == 3 and O.cp_code(P, np.eye(d, dtype=np.float32)[2]) == 0
+
+
+def test_cp_exact_table_canonical_pair_vs_random_pairs():
+    # the table uses the paper's canonical pair (spherical symmetry); a direct Monte
+    # Carlo with full random hyperplane matrices and random pairs at the same alpha must agree
+    d, draws = 16, 3000
+    T = O.cp_table(O.CP, d, 3, draws)
+    ell = T.shape[0] - 1
+    assert ell == 1 + 4
+    assert np.all(T[:, 40] == 1.0) and np.all(T[1:, 0] == 0.0)      # alpha = 1 and alpha = -1
+    assert np.all(np.diff(T, axis=1) >= 0) and np.all(np.diff(T, axis=0) <= 0)
+    rng = np.random.default_rng(7)
+    for a in (24, 32):                                                # alpha = 0.2, 0.6
+        alpha = -1.0 + 0.05 * a
+        hits = 0
+        n = 1500
+        for _ in range(n):
+            A = rng.standard_normal((d, d)).astype(np.float32)
+            x = rng.standard_normal(d)
+            x /= np.linalg.norm(x)
+            u = rng.standard_normal(d)
+            u -= (u @ x) * x
+            u /= np.linalg.norm(u)
+            y = alpha * x + np.sqrt(1 - alpha * alpha) * u
+            hits += O.cp_code(A, x.astype(np.float32)) == O.cp_code(A, y.astype(np.float32))
+        p = hits / n
+        sd = np.sqrt(p * (1 - p) / n + T[ell, a] * (1 - T[ell, a]) / draws)
+        assert abs(p - T[ell, a]) <= 4 * sd + 1e-3, (a, p, T[ell, a])
+
+
+def test_cp_exact_index_recall():
+    data, q = synth.config_data(1, n=2000, nq=40)
+    data, q = data[:, :16].copy(), q[:, :16].copy()
+    for strat in (O.INDEPENDENT, O.POOL):
+        o = O.OracleIndex(data, O.CP, L=12, seed=2, strategy=strat, pool_bits=120, cp_draws=300)
+        ids, sims, tr = o.search(q, 10, 0.9, rep_chunk=4)
+        bi, _ = O.bruteforce(o.data(), O.normalize(q), 10)
+        hit = np.mean([len(set(ids[r]) & set(bi[r])) / 10 for r in range(len(q))])
+        assert hit >= 0.85, (strat, hit)
