@@ -362,38 +362,60 @@ __global__ void __launch_bounds__(256) k_fht_funcs(const float* __restrict__ X, 
 
 // repetition codes from pooled FHT-CP codes: full = concat(fc[p][sel[j][t]]), code = top K bits
 // exact cross-polytope (PFG_CROSSPOLYTOPE): function f is d Gaussian hyperplanes
-// A_f[i] (rows of lda floats); value = index of the largest |<A_f[i], x>| (ties to the lowest i),
-// sign as the most significant of ell bits; each <A_f[i], x> is the sequential fmaf chain over t
-// (R-2 projections).  Thread per (row p, function f = blockIdx.y), four hyperplanes per pass over
-// x (one load of x[t] feeds four chains; A_f's rows are the same for the whole block: broadcast).
+// a_i; value = index of the largest |<a_i, x>| (ties to the lowest i), sign as the most significant
+// of ell bits; each <a_i, x> is the sequential fmaf chain over t (R-2 projections).  The
+// hyperplanes are stored transposed, AT[f][t][i] (i padded to d32 = 32 ceil(d/32)), so a warp reads
+// them coalesced: lane l holds hyperplanes l, l + 32, ... (NI per lane) of 4 rows at once (x[t]
+// broadcast), 4 NI chains per step; the argmax is reduced across the warp.  Warp per (4 rows,
+// function blockIdx.y).
+template <int NI>
 __global__ void __launch_bounds__(128) k_cp_funcs(const float* __restrict__ X, int64_t np, int ldx,
-                                                  const float* __restrict__ A, int nfun, int d, int lda, int ell,
+                                                  const float* __restrict__ AT, int nfun, int d, int d32, int ell,
                                                   uint16_t* __restrict__ out) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t p0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4;
     const int f = blockIdx.y;
-    if (p >= np) return;
-    const float* x = X + p * ldx;
-    const float* Af = A + (int64_t)f * d * lda;
-    float best = -1.0f;
-    int bi = 0;
-    bool neg = false;
-    for (int i0 = 0; i0 < d; i0 += 4) {
-        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        const int nr = min(4, d - i0);
-        for (int t = 0; t < d; ++t) {
-            const float xv = __ldg(x + t);
+    if (p0 >= np) return;
+    const float* A = AT + (int64_t)f * d * d32;
+    const float* xr[4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-                if (r < nr) s[r] = fmaf(__ldg(Af + (int64_t)(i0 + r) * lda + t), xv, s[r]);
+    for (int r = 0; r < 4; ++r) xr[r] = X + min(p0 + r, np - 1) * ldx;
+    float s[4][NI];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int k = 0; k < NI; ++k) s[r][k] = 0.0f;
+    for (int t = 0; t < d; ++t) {
+        float a[NI];
+#pragma unroll
+        for (int k = 0; k < NI; ++k) a[k] = __ldg(A + (int64_t)t * d32 + k * 32 + lane);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float xv = __ldg(xr[r] + t);
+#pragma unroll
+            for (int k = 0; k < NI; ++k) s[r][k] = fmaf(a[k], xv, s[r][k]);
         }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-            if (r < nr) {
-                const float a = fabsf(s[r]);
-                if (a > best) { best = a; bi = i0 + r; neg = s[r] < 0.0f; }
-            }
     }
-    out[p * nfun + f] = (uint16_t)((neg ? 1u << (ell - 1) : 0u) | (uint32_t)bi);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        float best = -1.0f;
+        int bi = 0;
+        bool neg = false;
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {
+            const int i = k * 32 + lane;
+            if (i < d && fabsf(s[r][k]) > best) { best = fabsf(s[r][k]); bi = i; neg = s[r][k] < 0.0f; }
+        }
+        // warp argmax: larger |y|, ties to the lower index
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            const bool on = __shfl_xor_sync(0xffffffffu, neg ? 1 : 0, off) != 0;
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; neg = on; }
+        }
+        if (lane == 0 && p0 + r < np) out[(p0 + r) * nfun + f] = (uint16_t)((neg ? 1u << (ell - 1) : 0u) | (uint32_t)bi);
+    }
 }
 
 __global__ void k_pool_codes(const uint16_t* __restrict__ fc, int64_t np, int m, int r0, int nreps, int c,

@@ -688,10 +688,14 @@ pfg_status gen_functions(pfg_index* I, cudaStream_t st) {
         // exact CP: function f = d hyperplanes, row (f d + i) of [F d][dpad], element
         // ((f d + i) d + t) of stream kTagCP; the independent strategy reads them through the
         // identity selection (repetition j, position t -> function j c + t)
-        std::vector<float> A((size_t)F * g.d * g.dpad, 0.0f);
+        // stored transposed for the kernel: AT[f][t][i], i padded to d32
+        const int d32 = (g.d + 31) / 32 * 32;
+        std::vector<float> A((size_t)F * g.d * d32, 0.0f);
         const uint64_t kc = stream_key(seed, kTagCP);
-        for (int64_t r = 0; r < F * g.d; ++r)
-            for (int t = 0; t < g.d; ++t) A[(size_t)r * g.dpad + t] = (float)gauss(kc, (uint64_t)(r * g.d + t));
+        for (int64_t f = 0; f < F; ++f)
+            for (int i = 0; i < g.d; ++i)
+                for (int t = 0; t < g.d; ++t)
+                    A[((size_t)f * g.d + t) * d32 + i] = (float)gauss(kc, (uint64_t)((f * g.d + i) * g.d + t));
         PFG_TRY(I->hpfn.alloc(A.size() * 4, "cp functions"));
         PFG_CUDA(cudaMemcpyAsync(I->hpfn.p, A.data(), A.size() * 4, cudaMemcpyHostToDevice, st));
         PFG_CUDA(cudaStreamSynchronize(st));
@@ -782,9 +786,19 @@ pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, u
         const int F = g.strategy == PFG_POOL ? g.m : g.L * g.c;
         if (!pool_ready) {
             PFG_TRY(poolvals.ensure((size_t)np * F * 2, "cp function codes"));
-            const dim3 gb((unsigned)((np + 127) / 128), (unsigned)F);
-            k_cp_funcs<<<gb, 128, 0, st>>>(X, np, g.dpad, I->hpfn.as<float>(), F, g.d, g.dpad, g.ell,
-                                           poolvals.as<uint16_t>());
+            const int d32 = (g.d + 31) / 32 * 32;
+            const dim3 gb((unsigned)((np + 15) / 16), (unsigned)F);   // 4 warps x 4 rows per block
+            switch (d32 / 32) {
+#define PFG_CP_CASE(NI)                                                                                  \
+    case NI:                                                                                             \
+        k_cp_funcs<NI><<<gb, 128, 0, st>>>(X, np, g.dpad, I->hpfn.as<float>(), F, g.d, d32, g.ell,       \
+                                           poolvals.as<uint16_t>());                                    \
+        break;
+                PFG_CP_CASE(1) PFG_CP_CASE(2) PFG_CP_CASE(3) PFG_CP_CASE(4)
+                PFG_CP_CASE(5) PFG_CP_CASE(6) PFG_CP_CASE(7) PFG_CP_CASE(8)
+#undef PFG_CP_CASE
+                default: return fail(PFG_E_ARG, "exact cross-polytope family supports d <= 256");
+            }
             pool_ready = true;
             I->launches += 1;
         }
