@@ -9,9 +9,14 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
     --clock-control none --csv --log-file gpurun_out/traffic.csv python tools/prof_search.py --config 2 > /dev/null 2>&1
 python tools/ncu_traffic.py gpurun_out/traffic.csv 2 > /dev/null
+ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+    --clock-control none --kernel-name regex:k_sims --csv --log-file gpurun_out/ksims_c2.csv \
+    python tools/prof_search.py --config 2 > /dev/null 2>&1
+python tools/ksims_traffic.py gpurun_out/ksims_c2.csv gpurun_out/ksims_traffic_config2.json > /dev/null
 for k in k_sims k_dedupe k_scan k_merge; do
   ncu --profile-from-start off --set full --import-source on --clock-control none --kernel-name $k --launch-skip 1 \
       --launch-count 1 -o gpurun_out/full_$k -f python tools/prof_search.py > /dev/null 2>&1
   python tools/ncu_summary.py gpurun_out/full_$k.ncu-rep gpurun_out/full_$k.json > /dev/null 2>&1
 done
+cp profiles/query_phase_traffic_config2.json gpurun_out/ 2>/dev/null
 cat gpurun_out/pytest_gpu.log; tail -c 600 gpurun_out/bench.jsonl
