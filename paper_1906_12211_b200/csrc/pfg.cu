@@ -372,8 +372,7 @@ struct pfg_index {
     cudaGraphExec_t loop_exec = nullptr;
     std::vector<unsigned char> loop_key;
     cudaStream_t cap_st = nullptr;
-    cudaEvent_t ev_split = nullptr, ev_f1 = nullptr, ev_f1a = nullptr, ev_f1b = nullptr;
-    bool f1_timed = false;
+    cudaEvent_t ev_split = nullptr, ev_f1 = nullptr;
     uint32_t* h_ctl = nullptr;   // pinned host mirror of the round control block
     RoundCtl* h_ctl2 = nullptr;  // [2] pinned copies of each search's final control block (by parity)
     int64_t nsearch = 0;         // searches of the round engine so far
@@ -435,7 +434,7 @@ struct pfg_index {
         if (h_zmin) cudaFreeHost(h_zmin);
         if (loop_exec) cudaGraphExecDestroy(loop_exec);
         if (cap_st) cudaStreamDestroy(cap_st);
-        for (cudaEvent_t e : {ev_split, ev_f1, ev_f1a, ev_f1b})
+        for (cudaEvent_t e : {ev_split, ev_f1})
             if (e) cudaEventDestroy(e);
     }
 };
@@ -1066,13 +1065,6 @@ pfg_status phase_collect(pfg_index* I) {
         if (I->pkind[i] >= 0) I->last_phase_ms[I->pkind[i]] += ms;
     }
     I->pev_n = 0;
-    if (I->f1_timed) {
-        // the first fused launch ran on the aux stream beside the loop
-        float ms = 0.0f;
-        PFG_CUDA(cudaEventElapsedTime(&ms, I->ev_f1a, I->ev_f1b));
-        I->last_phase_ms[kPhFused] += ms;
-        I->f1_timed = false;
-    }
     return PFG_OK;
 }
 
@@ -1367,8 +1359,6 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         if (!I->ev_split) {
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_split, cudaEventDisableTiming));
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_f1, cudaEventDisableTiming));
-            PFG_CUDA(cudaEventCreate(&I->ev_f1a));
-            PFG_CUDA(cudaEventCreate(&I->ev_f1b));
         }
         // wide queries (kernels_rounds.cuh): visit-tag arrays (n words each, PFG_WIDE_MIB of them
         // at most, default 8 GiB) and wide scan tiles, sized grow-only from what the previous

@@ -46,6 +46,14 @@ res = {
     "l1_hit_pct": f("l1tex__t_sector_hit_rate.pct"),
     "l2_hit_pct": f("lts__t_sector_hit_rate.pct"),
     "instructions": f("smsp__inst_executed.sum"),
+    # FMA pipe (hashing projections: the north star asks for FMA-pipe utilisation against peak)
+    "fma_pipe_active_pct": f("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+    "fma_inst_pct": f("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+    "fp32_flops_per_s": (lambda a, b: a / b if a and b else None)(
+        (f("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum") or 0) * 2
+        + (f("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum") or 0)
+        + (f("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum") or 0),
+        scale("gpu__time_duration.sum", 1)),
     "top_stalls_share": dict(top),
 }
 res["dram_gbs"] = (res["dram_bytes_read"] + res["dram_bytes_write"]) / res["duration_s"] / 1e9
