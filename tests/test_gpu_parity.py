@@ -548,3 +548,31 @@ def test_cp_exact_build_bit_exact(cases, name):
 @pytest.mark.parametrize("engine", [0, 1])
 def test_search_parity_cp_exact(cases, name, recall, engine):
     _compare(cases[name], 10, recall, dict(rep_chunk=8, engine=engine), dict(rep_chunk=8))
+
+
+# ------------------------------------------------------------------ randomised option sweep
+def test_randomised_option_combinations(cases, cases16, monkeypatch):
+    # 40 seeded random combinations of the search options on the small cases, both engines, with
+    # and without the device-side loop / wide queries: every counter, evaluated set and result
+    # must equal the oracle's
+    import os
+    rng = np.random.default_rng(int(os.environ.get("PFG_SWEEP_SEED", 2024)))
+    names = ["hp", "fht", "hp_pool", "fht_long", "cp"]
+    for it in range(int(os.environ.get("PFG_SWEEP_N", 40))):
+        name = names[it % len(names)]
+        c = (cases16 if (it % 7 == 3 and name in cases16) else cases)[name]
+        R = int(rng.choice([1, 2, 4, 8, 16, 32]))
+        kw = dict(rep_chunk=R, segment=int(rng.choice([1, 5, 12, 30])), eps=float(rng.choice([-0.1, 0.0, 0.3])),
+                  uniform_chunks=bool(rng.random() < 0.3), use_filter=bool(rng.random() < 0.85),
+                  stop_rule=int(rng.random() < 0.2 and c.orc.strategy == O.INDEPENDENT))
+        gk = dict(kw, engine=int(rng.random() < 0.3), rounds=int(rng.choice([0, 1, 2, 7])),
+                  wide=int(rng.choice([0, 0, 1, 40])))
+        k = int(rng.choice([1, 5, 10, 33]))
+        recall = float(rng.choice([0.5, 0.8, 0.9, 0.97, 0.99]))
+        if rng.random() < 0.5:
+            monkeypatch.setenv("PFG_LOOP_MIN", "1")
+            monkeypatch.setenv("PFG_LOOP_MAX", "1000000")
+        else:
+            monkeypatch.delenv("PFG_LOOP_MIN", raising=False)
+            monkeypatch.delenv("PFG_LOOP_MAX", raising=False)
+        _compare(c, k, recall, gk, kw)
