@@ -723,12 +723,12 @@ __device__ __forceinline__ float sims_step(const QueryParams& p, uint32_t myid, 
     }
 }
 
-template <typename PP, bool I16>
-__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
-    const QueryParams& p = deref(pp);
 #ifndef PFG_I16_NR
 #define PFG_I16_NR 16
 #endif
+template <typename PP, bool I16>
+__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
+    const QueryParams& p = deref(pp);
     constexpr int NR = I16 ? PFG_I16_NR : kRPI;   // int16 rows are half as long: more rows in flight
     constexpr int kSh = NR == 32 ? 0 : NR == 16 ? 1 : NR == 8 ? 2 : 3;
     const int lane = threadIdx.x & 31;
@@ -759,49 +759,119 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
         const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
         if ((lane & ((1 << kSh) - 1)) == 0 && b + rr < e1) rs.pool_key[b + rr] = make_key(t1, id_rr);
     }
+}
+
+// Wide tiles (a separate kernel, launched only when wide queries are possible, so that k_sims keeps
+// its register budget for the pool):
+template <typename PP, bool I16>
+__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_wsims(PP pp, int par) {
+    const QueryParams& p = deref(pp);
+    constexpr int NR = I16 ? PFG_I16_NR : kRPI;
+    constexpr int kSh = NR == 32 ? 0 : NR == 16 ? 1 : NR == 8 ? 2 : 3;
+    const int lane = threadIdx.x & 31;
+    const RoundState& rs = p.rs;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     // wide tiles: a provisional id is fresh iff the query's visit-tag array still holds this
     // visit's tag (no earlier repetition of the chunk passed it); the fresh ids are compacted in
     // order and their similarities computed (the same arithmetic); kept = how many of them beat the
-    // k-th key the query held at the start of the chunk (only those can enter its top list)
+    // k-th key the query held at the start of the chunk (only those can enter its top list).
+    // A warp takes four consecutive tiles at once (their metadata, tag checks and rows in flight
+    // together): a tile holds few fresh ids late in a search, and one tile per warp step left the
+    // kernel bound by the chain of dependent loads per tile.
+    constexpr int G = 4;
     const uint32_t nwt = min(rs.ctl->nwt[par], rs.wcap);
-    for (int64_t aw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; aw < nwt; aw += nw) {
-        const uint32_t w = rs.wtcnt[aw];
-        const uint32_t np_ = w & 0xffu;
-        if (np_ == 0) continue;
-        const int64_t q = rs.wtiles[2 * aw].x;
-        const uint32_t tag = rs.wtiles[2 * aw + 1].z;
-        const uint32_t* W = rs.wv + (int64_t)rs.wslot[q] * p.n;
-        uint32_t* cand = rs.wcand + aw * kTile;
-        uint32_t v[kTile / 32];
-        bool fr[kTile / 32];
+    auto sel4 = [](uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, int t) -> uint32_t {
+        return t == 0 ? a0 : t == 1 ? a1 : t == 2 ? a2 : a3;
+    };
+    for (int64_t g0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * G; g0 < nwt; g0 += nw * G) {
+        uint32_t w = 0, q = 0, tag = 0, slot = 0;
+        uint64_t kth = 0;
+        if (lane < G && g0 + lane < nwt) {
+            w = rs.wtcnt[g0 + lane];
+            if (w & 0xffu) {
+                q = rs.wtiles[2 * (g0 + lane)].x;
+                tag = rs.wtiles[2 * (g0 + lane) + 1].z;
+            }
+        }
+        if (lane < G && (w & 0xffu)) {
+            slot = rs.wslot[q];
+            kth = rs.tn[q] == p.k_eff ? rs.T[(int64_t)q * p.kt + p.k_eff - 1] : 0ull;
+        }
+        uint32_t incl = w & 0xffu;
 #pragma unroll
-        for (int u = 0; u < kTile / 32; ++u) {
-            const uint32_t o = u * 32 + lane;
-            v[u] = o < np_ ? cand[o] : 0u;
-            fr[u] = o < np_ && __ldcg(W + v[u]) == tag;
+        for (int off = 1; off < G; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(kFull, incl, off);
+            if (lane >= off) incl += o;
+        }
+        const uint32_t i0 = __shfl_sync(kFull, incl, 0), i1 = __shfl_sync(kFull, incl, 1),
+                       i2 = __shfl_sync(kFull, incl, 2), i3 = __shfl_sync(kFull, incl, 3);
+        if (i3 == 0) continue;
+        const uint32_t q0 = __shfl_sync(kFull, q, 0), q1 = __shfl_sync(kFull, q, 1), q2 = __shfl_sync(kFull, q, 2),
+                       q3 = __shfl_sync(kFull, q, 3);
+        const uint32_t tg0 = __shfl_sync(kFull, tag, 0), tg1 = __shfl_sync(kFull, tag, 1),
+                       tg2 = __shfl_sync(kFull, tag, 2), tg3 = __shfl_sync(kFull, tag, 3);
+        const uint32_t s0 = __shfl_sync(kFull, slot, 0), s1 = __shfl_sync(kFull, slot, 1),
+                       s2 = __shfl_sync(kFull, slot, 2), s3 = __shfl_sync(kFull, slot, 3);
+        // tag checks over the tiles' provisional entries, compaction per tile in order (an entry
+        // is written at or before its own index, after every entry before it was read)
+        uint32_t fc0 = 0, fc1 = 0, fc2 = 0, fc3 = 0;
+        for (uint32_t e0 = 0; e0 < i3; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            const bool live = e < i3;
+            const int t = (int)(e >= i0) + (int)(e >= i1) + (int)(e >= i2);
+            uint32_t id = 0;
+            bool fresh = false;
+            if (live) {
+                const uint32_t o = e - sel4(0u, i0, i1, i2, t);
+                id = rs.wcand[(g0 + t) * kTile + o];
+                fresh = __ldcg(rs.wv + (int64_t)sel4(s0, s1, s2, s3, t) * p.n + id) == sel4(tg0, tg1, tg2, tg3, t);
+            }
+            const uint32_t fm = __ballot_sync(kFull, fresh);
+            __syncwarp();
+#pragma unroll
+            for (int tt = 0; tt < G; ++tt) {
+                const uint32_t m = fm & __ballot_sync(kFull, live && t == tt);
+                const uint32_t fct = sel4(fc0, fc1, fc2, fc3, tt);
+                if (fresh && t == tt) rs.wcand[(g0 + tt) * kTile + fct + __popc(m & lanemask_lt())] = id;
+                const uint32_t add = __popc(m);
+                if (tt == 0) fc0 += add; else if (tt == 1) fc1 += add; else if (tt == 2) fc2 += add; else fc3 += add;
+            }
         }
         __syncwarp();
-        uint32_t nf = 0;
-#pragma unroll
-        for (int u = 0; u < kTile / 32; ++u) {
-            const uint32_t m = __ballot_sync(kFull, fr[u]);
-            if (fr[u]) cand[nf + __popc(m & lanemask_lt())] = v[u];
-            nf += __popc(m);
-        }
-        __syncwarp();
-        const uint64_t kth = rs.tn[q] == p.k_eff ? rs.T[q * p.kt + p.k_eff - 1] : 0ull;
-        uint32_t kept = 0;
-        for (uint32_t b0 = 0; b0 < nf; b0 += NR) {
-            const uint32_t nrow = min((uint32_t)NR, nf - b0);
-            const uint32_t myid = lane < NR ? cand[b0 + min((uint32_t)lane, nrow - 1)] : 0u;
-            const float sim = sims_step<NR, I16, true>(p, myid, (uint32_t)q, lane);
+        // similarities of the fresh rows of the four tiles, NR rows per step (rows of different
+        // queries read their own query row)
+        const uint32_t f0 = fc0, f1 = f0 + fc1, f2 = f1 + fc2, f3 = f2 + fc3;
+        const uint64_t k0 = __shfl_sync(kFull, kth, 0), k1 = __shfl_sync(kFull, kth, 1), k2 = __shfl_sync(kFull, kth, 2),
+                       k3 = __shfl_sync(kFull, kth, 3);
+        uint32_t kp0 = 0, kp1 = 0, kp2 = 0, kp3 = 0;
+        for (uint32_t b0 = 0; b0 < f3; b0 += NR) {
+            const uint32_t nrow = min((uint32_t)NR, f3 - b0);
+            uint32_t myid = 0, myq = 0, mys = 0;
+            int myt = 0;
+            if (lane < NR) {
+                const uint32_t e = b0 + min((uint32_t)lane, nrow - 1);
+                myt = (int)(e >= f0) + (int)(e >= f1) + (int)(e >= f2);
+                mys = (g0 + myt) * kTile + (e - sel4(0u, f0, f1, f2, myt));
+                myid = rs.wcand[mys];
+                myq = sel4(q0, q1, q2, q3, myt);
+            }
+            const bool oneq = __shfl_sync(kFull, myq, 0) == __shfl_sync(kFull, myq, NR - 1);
+            const float sim = oneq ? sims_step<NR, I16, true>(p, myid, myq, lane) : sims_step<NR, I16, false>(p, myid, myq, lane);
             const uint32_t rr = lane >> kSh;
             const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
+            const uint32_t s_rr = __shfl_sync(kFull, mys, rr);
+            const int t_rr = __shfl_sync(kFull, myt, rr);
             const bool own = (lane & ((1 << kSh) - 1)) == 0 && rr < nrow;
-            if (own) rs.wsim[aw * kTile + b0 + rr] = sim;
-            kept += __popc(__ballot_sync(kFull, own && make_key(sim, id_rr) > kth));
+            if (own) rs.wsim[s_rr] = sim;
+            const uint64_t kt_rr = t_rr == 0 ? k0 : t_rr == 1 ? k1 : t_rr == 2 ? k2 : k3;
+            const bool kp = own && make_key(sim, id_rr) > kt_rr;
+            kp0 += __popc(__ballot_sync(kFull, kp && t_rr == 0));
+            kp1 += __popc(__ballot_sync(kFull, kp && t_rr == 1));
+            kp2 += __popc(__ballot_sync(kFull, kp && t_rr == 2));
+            kp3 += __popc(__ballot_sync(kFull, kp && t_rr == 3));
         }
-        if (lane == 0) rs.wtcnt[aw] = nf | (w & 0xffff00u) | (kept << 24);
+        if (lane < G && (w & 0xffu))
+            rs.wtcnt[g0 + lane] = sel4(fc0, fc1, fc2, fc3, lane) | (w & 0xffff00u) | (sel4(kp0, kp1, kp2, kp3, lane) << 24);
     }
 }
 

@@ -1558,6 +1558,11 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             if (g.storage == PFG_STORAGE_I16) k_sims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
             else k_sims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
             if (kt) PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n++ + 1], rst));
+            if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) {
+                // wide tiles of the round (tag checks, compaction, similarities)
+                if (g.storage == PFG_STORAGE_I16) k_wsims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
+                else k_wsims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
+            }
             if (rst == st) PFG_TRY(dbg_sync("k_sims"));
             PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_merge<PP, true><<<qb_m, 128, msm, rst>>>(pp, par);
