@@ -390,50 +390,72 @@ __global__ void __launch_bounds__(128) k_expand(PP pp, int par, int lazy) {
 // evaluated before (an earlier chunk, or an earlier repetition of this chunk that got there
 // first) and is a duplicate; the others are provisional until k_sims checks that no earlier
 // repetition of the chunk lowered the tag after this claim.
-__device__ __forceinline__ void scan_wide_tile(const QueryParams& p, int64_t aw, int lane) {
+// two tiles per call (aw1 < 0: one), their loads interleaved: late in a search a wide tile holds
+// few passing ids and its cost is the chain of dependent loads (entries, tags, claims)
+__device__ __forceinline__ void scan_wide_tiles(const QueryParams& p, int64_t aw0, int64_t aw1, int lane) {
     const RoundState& rs = p.rs;
-    const uint4 d0 = rs.wtiles[2 * aw], d1 = rs.wtiles[2 * aw + 1];
-    const uint32_t cnt = d0.w & 0xffffu, rep = (d0.w >> 16) & 0xffu, tau = d0.w >> 24;
-    if (cnt == 0) { if (lane == 0) rs.wtcnt[aw] = 0; return; }
-    const int64_t q = d0.x;
-    const uint64_t sk = ((uint64_t)d1.y << 32) | d1.x;
-    const uint32_t tag = d1.z;
-    uint32_t* W = rs.wv + (int64_t)rs.wslot[q] * p.n;
-    const Entry* tj = p.tab + (int64_t)d1.w * p.n + d0.y;
-    uint4 e[kTile / 32];
+    constexpr int U = kTile / 32;
+    int64_t aw[2] = {aw0, aw1};
+    uint32_t cnt[2], rep[2], tau[2], tag[2];
+    uint64_t sk[2];
+    const Entry* tj[2];
+    uint32_t* W[2];
 #pragma unroll
-    for (int u = 0; u < kTile / 32; ++u) {
-        const uint32_t o = u * 32 + lane;
-        if (o < cnt) e[u] = __ldg(reinterpret_cast<const uint4*>(tj + o));
+    for (int h = 0; h < 2; ++h) {
+        cnt[h] = 0; rep[h] = 0; tau[h] = 64; tag[h] = 0; sk[h] = 0; tj[h] = p.tab; W[h] = rs.wv;
+        if (aw[h] < 0) continue;
+        const uint4 d0 = rs.wtiles[2 * aw[h]], d1 = rs.wtiles[2 * aw[h] + 1];
+        cnt[h] = d0.w & 0xffffu; rep[h] = (d0.w >> 16) & 0xffu; tau[h] = d0.w >> 24;
+        sk[h] = ((uint64_t)d1.y << 32) | d1.x;
+        tag[h] = d1.z;
+        tj[h] = p.tab + (int64_t)d1.w * p.n + d0.y;
+        if (cnt[h]) W[h] = rs.wv + (int64_t)rs.wslot[d0.x] * p.n;
     }
-    bool pass[kTile / 32];
-    uint32_t old[kTile / 32];
+    uint4 e[2][U];
+    bool pass[2][U];
+    uint32_t old[2][U];
 #pragma unroll
-    for (int u = 0; u < kTile / 32; ++u) {
-        const uint32_t o = u * 32 + lane;
-        pass[u] = o < cnt;
-        if (pass[u] && p.use_filter && tau < 64) pass[u] = __popcll((((uint64_t)e[u].w << 32) | e[u].z) ^ sk) <= tau;
-        old[u] = pass[u] ? __ldcg(W + e[u].x) : 0u;
-    }
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t o = u * 32 + lane;
+            if (o < cnt[h]) e[h][u] = __ldg(reinterpret_cast<const uint4*>(tj[h] + o));
+        }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t o = u * 32 + lane;
+            pass[h][u] = o < cnt[h];
+            if (pass[h][u] && p.use_filter && tau[h] < 64)
+                pass[h][u] = __popcll((((uint64_t)e[h][u].w << 32) | e[h][u].z) ^ sk[h]) <= tau[h];
+            old[h][u] = pass[h][u] ? __ldcg(W[h] + e[h][u].x) : 0u;
+        }
     // a smaller tag already there: a duplicate, no atomic needed (most passing ids, late in a
     // search); else claim the visit
 #pragma unroll
-    for (int u = 0; u < kTile / 32; ++u)
-        if (pass[u] && old[u] >= tag) old[u] = atomicMin(W + e[u].x, tag);
-    uint32_t* cand = rs.wcand + aw * kTile;
-    uint32_t np = 0, npass = 0;
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int u = 0; u < kTile / 32; ++u) {
-        npass += __popc(__ballot_sync(kFull, pass[u]));
-        const bool prov = pass[u] && old[u] >= tag;
-        const uint32_t pm = __ballot_sync(kFull, prov);
-        if (prov) cand[np + __popc(pm & lanemask_lt())] = e[u].x;
-        np += __popc(pm);
+        for (int u = 0; u < U; ++u)
+            if (pass[h][u] && old[h][u] >= tag[h]) old[h][u] = atomicMin(W[h] + e[h][u].x, tag[h]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (aw[h] < 0) continue;
+        uint32_t* cand = rs.wcand + aw[h] * kTile;
+        uint32_t np = 0, npass = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            npass += __popc(__ballot_sync(kFull, pass[h][u]));
+            const bool prov = pass[h][u] && old[h][u] >= tag[h];
+            const uint32_t pm = __ballot_sync(kFull, prov);
+            if (prov) cand[np + __popc(pm & lanemask_lt())] = e[h][u].x;
+            np += __popc(pm);
+        }
+        if (lane == 0) rs.wtcnt[aw[h]] = cnt[h] ? (np | (npass << 8) | (rep[h] << 16)) : 0u;
     }
-    if (lane == 0) rs.wtcnt[aw] = np | (npass << 8) | (rep << 16);
 }
 
-template <typename PP>
+template <typename PP, bool WIDE>
 __global__ void __launch_bounds__(256) k_scan(PP pp, int par) {
     const QueryParams& p = deref(pp);
     const int lane = threadIdx.x & 31;
@@ -441,8 +463,10 @@ __global__ void __launch_bounds__(256) k_scan(PP pp, int par) {
     const uint32_t ntiles = rs.ctl->ntiles[par];
     const uint32_t nwt = min(rs.ctl->nwt[par], rs.wcap);
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < (int64_t)ntiles + nwt; a += nw) {
-        if (a >= ntiles) { scan_wide_tile(p, a - ntiles, lane); continue; }
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (WIDE)  // WIDE = false: no wide queries in this search (the lean variant keeps its registers)
+        for (int64_t aw = wid * 2; aw < nwt; aw += nw * 2) scan_wide_tiles(p, aw, aw + 1 < nwt ? aw + 1 : -1, lane);
+    for (int64_t a = wid; a < ntiles; a += nw) {
         const uint4 d0 = rs.tiles[2 * a], d1 = rs.tiles[2 * a + 1];
         const int64_t q = d0.x;
         const uint32_t cnt = d0.w & 0xffffu, rep = (d0.w >> 16) & 0xffu, tau = d0.w >> 24;

@@ -1536,7 +1536,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             }
             if (rst == st) PFG_TRY(dbg_sync("k_expand"));
             PFG_TRY(phase_mark(I, marks, kPhScan, rst));
-            k_scan<PP><<<tb_s, 256, 0, rst>>>(pp, par);
+            if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_scan<PP, true><<<tb_s, 256, 0, rst>>>(pp, par);
+            else k_scan<PP, false><<<tb_s, 256, 0, rst>>>(pp, par);
             if (rst == st) PFG_TRY(dbg_sync("k_scan"));
             PFG_TRY(phase_mark(I, marks, kPhDedupe, rst));
             k_dedupe<PP><<<qb_d, 128, dsm, rst>>>(pp, par);
