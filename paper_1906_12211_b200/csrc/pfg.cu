@@ -86,6 +86,29 @@ struct DBuf {
     template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and occupancy queries cost host time on every
+// search; they are cached per kernel (the attribute only grows)
+std::mutex g_attr_mu;
+cudaError_t set_smem(const void* fn, size_t bytes) {
+    static std::map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    auto it = done.find(fn);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done[fn] = bytes;
+    return e;
+}
+cudaError_t occupancy(int* nb, const void* fn, int threads, size_t smem) {
+    static std::map<std::tuple<const void*, int, size_t>, int> cache;
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    const auto key = std::make_tuple(fn, threads, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) { *nb = it->second; return cudaSuccess; }
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, fn, threads, smem);
+    if (e == cudaSuccess) cache[key] = *nb;
+    return e;
+}
+
 bool is_device_ptr(const void* ptr) {
     if (!ptr) return false;
     cudaPointerAttributes a;
@@ -1089,12 +1112,12 @@ pfg_status launch_query_t(const QueryParams& p, int blocks, size_t smem, cudaStr
     // leaner variant (measured: config 3, 10 000 resumed queries, +8 %)
     const bool few = p.nq <= (int64_t)num_sms * 16;
     if (p.resume && few) {
-        PFG_CUDA(cudaFuncSetAttribute(k_query<EPL, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PFG_CUDA(set_smem((const void*)k_query<EPL, 16>, smem));
         k_query<EPL, 16><<<blocks, 128, smem, st>>>(p);
         PFG_CUDA(cudaGetLastError());
         return PFG_OK;
     }
-    PFG_CUDA(cudaFuncSetAttribute(k_query<EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PFG_CUDA(set_smem((const void*)k_query<EPL>, smem));
     k_query<EPL><<<blocks, 128, smem, st>>>(p);
     PFG_CUDA(cudaGetLastError());
     return PFG_OK;
@@ -1102,8 +1125,8 @@ pfg_status launch_query_t(const QueryParams& p, int blocks, size_t smem, cudaStr
 template <int EPL>
 int query_occupancy(size_t smem) {
     int nb = 0;
-    cudaFuncSetAttribute(k_query<EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_query<EPL>, 128, smem) != cudaSuccess) {
+    set_smem((const void*)k_query<EPL>, smem);
+    if (occupancy(&nb, (const void*)k_query<EPL>, 128, smem) != cudaSuccess) {
         cudaGetLastError();
         nb = 1;
     }
@@ -1505,13 +1528,13 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const size_t esm = (size_t)expand_smem_bytes(g.dpad, lazy) * 4;
         const size_t dsm = (size_t)align16((int)sizeof(DedupeSmem)) * 4;
         const size_t msm = (size_t)(align16((int)sizeof(MergeSmem)) + 2 * align16(kt * 8)) * 4;
-        PFG_CUDA(cudaFuncSetAttribute(k_merge<QueryParams, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
-        PFG_CUDA(cudaFuncSetAttribute(k_merge<QueryParams, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
-        PFG_CUDA(cudaFuncSetAttribute(k_dedupe<QueryParams>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        PFG_CUDA(cudaFuncSetAttribute(k_merge<const QueryParams*, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
-        PFG_CUDA(cudaFuncSetAttribute(k_dedupe<const QueryParams*>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        PFG_CUDA(set_smem((const void*)k_merge<QueryParams, false>, msm));
+        PFG_CUDA(set_smem((const void*)k_merge<QueryParams, true>, msm));
+        PFG_CUDA(set_smem((const void*)k_dedupe<QueryParams>, dsm));
+        PFG_CUDA(set_smem((const void*)k_merge<const QueryParams*, true>, msm));
+        PFG_CUDA(set_smem((const void*)k_dedupe<const QueryParams*>, dsm));
         int docc = 1;
-        PFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&docc, k_dedupe<QueryParams>, 128, dsm));
+        PFG_CUDA(occupancy(&docc, (const void*)k_dedupe<QueryParams>, 128, dsm));
         // grids: warp per active query (at most one resident wave; the kernels stride over the
         // device-side counts, so no host synchronisation is needed between rounds)
         const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * 16));
@@ -1874,7 +1897,7 @@ pfg_status pfg_merge_topk(const int64_t* ids, const float* sims, int32_t world, 
         return fail(PFG_E_ARG, "pfg_merge_topk takes device pointers");
     const size_t smem = (size_t)4 * world * k * 16;
     cudaStream_t st = (cudaStream_t)stream;
-    PFG_CUDA(cudaFuncSetAttribute(k_merge_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PFG_CUDA(set_smem((const void*)k_merge_topk, smem));
     k_merge_topk<<<(unsigned)((nq + 3) / 4), 128, smem, st>>>(ids, sims, world, nq, k, out_ids, out_sims);
     PFG_CUDA(cudaGetLastError());
     return PFG_OK;
