@@ -409,6 +409,9 @@ struct pfg_index {
     cudaStream_t aux2 = nullptr; // third stream: codes and ranges of the later eager repetitions
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_late = nullptr;
     bool late_pending = false;   // codes/ranges of repetitions [split, eager) still on aux2
+    cudaEvent_t ev_mid = nullptr;
+    bool mid_pending = false;    // codes/ranges of repetitions [1, split) still on aux2 (round 1 joins)
+    int late_ne = 0;             // eager depth whose codes [split, late_ne) the search launches on aux2
     cudaEvent_t ev_zmin = nullptr, ev_done = nullptr;  // zero-row flag copied; previous search done
     bool done_pending = false;   // ev_done recorded by a search not yet observed complete
     int timing_pending = 0;      // the last search recorded timing events (read lazily)
@@ -452,6 +455,7 @@ struct pfg_index {
         if (aux) cudaStreamDestroy(aux);
         if (aux2) cudaStreamDestroy(aux2);
         if (ev_late) cudaEventDestroy(ev_late);
+        if (ev_mid) cudaEventDestroy(ev_mid);
         if (ev_zmin) cudaEventDestroy(ev_zmin);
         if (ev_done) cudaEventDestroy(ev_done);
         if (h_zmin) cudaFreeHost(h_zmin);
@@ -962,6 +966,7 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_late, cudaEventDisableTiming));
+            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_mid, cudaEventDisableTiming));
         }
         PFG_CUDA(cudaEventRecord(I->ev_fork, st));
         PFG_CUDA(cudaStreamWaitEvent(I->aux, I->ev_fork, 0));
@@ -990,11 +995,23 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         PFG_TRY(I->qcodes.ensure((size_t)nq * ld * 4, "query codes"));
         // repetitions [0, split) now; [split, ne) on the third stream, joined before the round
         // that first reaches them (the caller: late_join)
+        // Round 0 reaches repetition 0 only, round 1 repetitions [1, split): only repetition 0 is
+        // hashed before round 0; [1, split) runs on the third stream beside round 0 (the caller
+        // records ev_mid after its ranges, round 1 joins it) and [split, ne) after it (ev_late,
+        // round 2 joins it)
         const int s0 = (split > 0 && split < ne && I->aux2) ? split : ne;
-        PFG_TRY(fht_codes(I, nq, nullptr, 0, s0, ld, st));
+        const bool mid = s0 < ne && s0 > 1 && !getenv("PFG_NO_MID");
+        PFG_TRY(fht_codes(I, nq, nullptr, 0, mid ? 1 : s0, ld, st));
         if (s0 < ne) {
             PFG_CUDA(cudaStreamWaitEvent(I->aux2, I->ev_fork, 0));
-            PFG_TRY(fht_codes(I, nq, nullptr, s0, ne - s0, ld, I->aux2));
+            if (mid) {
+                PFG_TRY(fht_codes(I, nq, nullptr, 1, s0 - 1, ld, I->aux2));
+                I->mid_pending = true;
+                I->late_ne = ne;   // [s0, ne): launched by the caller after the ranges of [1, s0)
+            } else {
+                PFG_TRY(fht_codes(I, nq, nullptr, s0, ne - s0, ld, I->aux2));
+                I->late_ne = 0;
+            }
             I->late_pending = true;
         }
         I->qc_n = ne;
@@ -1097,7 +1114,15 @@ pfg_status join_sketches(pfg_index* I, cudaStream_t st) {
     return PFG_OK;
 }
 // the codes (and ranges) of the later eager repetitions are ready on `st` after this
+pfg_status mid_join(pfg_index* I, cudaStream_t st) {
+    if (I->mid_pending) {
+        PFG_CUDA(cudaStreamWaitEvent(st, I->ev_mid, 0));
+        I->mid_pending = false;
+    }
+    return PFG_OK;
+}
 pfg_status late_join(pfg_index* I, cudaStream_t st) {
+    PFG_TRY(mid_join(I, st));
     if (I->late_pending) {
         PFG_CUDA(cudaStreamWaitEvent(st, I->ev_late, 0));
         I->late_pending = false;
@@ -1469,9 +1494,22 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     if (p.qb_n > 0) {
         PFG_TRY(I->qbnd.ensure((size_t)nq * p.qb_ld * 16, "query bounds"));
         p.qbnd = I->qbnd.as<uint4>();
+        const int bm = I->mid_pending ? std::min(p.qb_n, 1) : -1;   // st: [0, bm); aux2: [bm, b0) (ev_mid)
         const int b0 = std::min(p.qb_n, I->late_pending ? I->qc_split : p.qb_n);
-        const int64_t thr_n = nq * (int64_t)b0;
-        if (b0 > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, b0, nullptr);
+        const int bs = bm >= 0 ? bm : b0;
+        const int64_t thr_n = nq * (int64_t)bs;
+        if (bs > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, bs, nullptr);
+        if (bm >= 0 && bm < b0) {
+            const int64_t thr_m = nq * (int64_t)(b0 - bm);
+            k_qbounds<<<(unsigned)((thr_m + 255) / 256), 256, 0, I->aux2>>>(p, I->qbnd.as<uint4>(), nullptr, nq, bm, b0 - bm,
+                                                                          nullptr);
+            I->launches += 1;
+        }
+        if (I->mid_pending) PFG_CUDA(cudaEventRecord(I->ev_mid, I->aux2));
+        if (I->late_pending && I->late_ne > I->qc_split) {
+            PFG_TRY(fht_codes(I, nq, nullptr, I->qc_split, I->late_ne - I->qc_split, I->qc_ld, I->aux2));
+            I->late_ne = 0;
+        }
         if (b0 < p.qb_n) {
             const int64_t thr_l = nq * (int64_t)(p.qb_n - b0);
             k_qbounds<<<(unsigned)((thr_l + 255) / 256), 256, 0, I->aux2>>>(p, I->qbnd.as<uint4>(), nullptr, nq, b0,
@@ -1480,6 +1518,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         }
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
+    } else if (I->mid_pending) {
+        PFG_CUDA(cudaEventRecord(I->ev_mid, I->aux2));
+    }
+    if (I->late_pending && I->late_ne > I->qc_split) {
+        PFG_TRY(fht_codes(I, nq, nullptr, I->qc_split, I->late_ne - I->qc_split, I->qc_ld, I->aux2));
+        I->late_ne = 0;
     }
     if (I->late_pending) PFG_CUDA(cudaEventRecord(I->ev_late, I->aux2));
     // developer instrumentation: PFG_PHASE_PROF=1 prints per-phase warp cycles of each search to stderr
@@ -1599,7 +1643,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         while (round < max_rounds) {
             // round 0 is the single repetition 0 with tau = 64 (no sketches read); round 1 reaches
             // repetitions < 1 + R; later rounds may reach every eager repetition
-            if (round == 1) PFG_TRY(join_sketches(I, st));
+            if (round == 1) { PFG_TRY(join_sketches(I, st)); PFG_TRY(mid_join(I, st)); }
             if (round == 2) PFG_TRY(late_join(I, st));
             PFG_TRY(launch_round(round & 1, st, tm, p));
             I->launches += 5;
