@@ -261,6 +261,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--engine", type=int, default=0, help="0 = bulk rounds + fused kernel, 1 = fused kernel only")
     ap.add_argument("--uniform-chunks", action="store_true", help="first chunk R repetitions long (R-17 option)")
+    ap.add_argument("--parallel", default="auto", choices=["auto", "data", "queries"],
+                    help="N > 1: data-sharded (each GPU indexes n/N rows, every query on every GPU, all-gather "
+                         "+ merge) or query replicas (each GPU the whole index and a query batch of its own); auto = "
+                         "data for the scale-out config 5, replicas for configs whose index fits one GPU")
     ap.add_argument("--storage", default="f32", choices=["f32", "i16"],
                     help="rows for the inner products: fp32, or the paper's 16-bit fixed point (R-25)")
     args = ap.parse_args()
@@ -273,7 +277,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1906_12211_b200 as pfg
-    from paper_1906_12211_b200.sharded import ShardedIndex, shard_range
+    from paper_1906_12211_b200.sharded import ReplicatedIndex, ShardedIndex, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -287,9 +291,12 @@ def main():
     d, k = c["d"], c["k"]
     # config 5 is weak-scaled (BASELINE: 12.5M rows per GPU); the others split their n rows
     weak = "shard_n" in c
-    n = c["shard_n"] * world if weak else c["n"]
+    mode = args.parallel if args.parallel != "auto" else ("data" if weak else "queries")
+    sharded = world > 1 and mode == "data"
+    replicas = world > 1 and mode == "queries"
+    n = c["shard_n"] * world if (weak and sharded) else c["n"] if not weak else c["shard_n"]
     nq = args.nq or c["nq"]
-    lo, hi = shard_range(n, world, rank)
+    lo, hi = shard_range(n, world, rank) if sharded else (0, n)
     data_np, q_np = synth.config_data(args.config, n=hi - lo, nq=nq, row0=lo)
     data = torch.from_numpy(data_np).to(dev)
     q = torch.from_numpy(q_np).to(dev)
@@ -300,14 +307,15 @@ def main():
         opts["reps"] = c["reps"]
     torch.cuda.synchronize()
     t0 = time.time()
-    idx = ShardedIndex(data, lo, c["budget"] or 0, c["family"], seed=1, **opts)
+    idx = (ShardedIndex(data, lo, c["budget"] or 0, c["family"], seed=1, **opts) if sharded or world == 1
+           else ReplicatedIndex(data, c["budget"] or 0, c["family"], seed=1, **opts))
     torch.cuda.synchronize()
     build_s = time.time() - t0
     info = idx.index.info
 
     # ground truth (global): shard-local exact top-k, gathered and merged like the search
     t_ids, t_kth, xn, qn = ground_truth(data, q, k)
-    if world > 1:
+    if sharded:
         from paper_1906_12211_b200.sharded import gather_merge
         sims_local = torch.einsum("qd,qkd->qk", qn, xn[t_ids])
         _, ms = gather_merge(t_ids + lo, sims_local.contiguous())
@@ -356,7 +364,7 @@ def main():
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     nl = idx.index.last_timing()[3]
-    launches = (nl + (1 if world > 1 else 0)) * args.steps
+    launches = (nl + (1 if sharded else 0)) * args.steps
     clocks = sampler.stop() if sampler else None
     # preparation / query-phase split of a search (untimed searches with events between them)
     for _ in range(3):
@@ -379,8 +387,8 @@ def main():
         t = torch.tensor([tot_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    rec = recall_of(ids, t_kth, xn if world == 1 else None, qn, k) if world == 1 else None
-    if world > 1:
+    rec = recall_of(ids, t_kth, xn, qn, k) if not sharded else None
+    if sharded:
         # recall against the merged global truth: check returned ids' exact sims on their owning rank
         owned = (ids >= lo) & (ids < hi)
         loc = (ids - lo).clamp(0, hi - lo - 1)
@@ -412,8 +420,9 @@ def main():
             t = torch.tensor([et], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             et = float(t.item())
-        e2e = {"value": args.steps * nq / (et / 1e3), "unit": "queries/s", "h2d_bytes_per_step": nq * d * 4,
-               "d2h_bytes_per_step": nq * k * 12}
+        e2e = {"value": args.steps * nq * (world if replicas else 1) / (et / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": nq * d * 4 * (world if replicas else 1),
+               "d2h_bytes_per_step": nq * k * 12 * (world if replicas else 1)}
 
     if rank == 0:
         pk = peaks()
@@ -449,14 +458,14 @@ def main():
                 cpu = {"value": None, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
         line = {
             "metric": METRIC,
-            "value": args.steps * nq / (tot_ms / 1e3),
+            "value": args.steps * nq * (world if replicas else 1) / (tot_ms / 1e3),
             "unit": "queries/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": tot_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "weak" if weak else "strong",
+            "scaling": "weak" if (weak or mode == "queries") else "strong",
             "vs_baseline": None,
             "dtype": "f32" if args.storage == "f32" else "i16 rows (int32 dot), f32 hashing",
             "data": "synthetic",
@@ -467,7 +476,10 @@ def main():
                        "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": info["reps"],
                        "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "storage": args.storage,
                        "l2": "flushed (512 MiB write) between timed steps",
-                       "parallelism": f"data-sharded x{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"data-sharded x{world}" if sharded else
+                                       f"query replicas x{world} (every GPU builds the whole index and answers a batch "
+                                       f"of {nq} queries independently; no collective on the data path)" if replicas
+                                       else "single GPU")},
             "recall": rec,
             "build_s": build_s,
             "roofline": ksims_roofline,

@@ -49,3 +49,16 @@ class ShardedIndex:
         res = self.index.search(queries, k, recall, **sopts)
         m_ids, m_sims = gather_merge(res[0], res[1], self.group)
         return (m_ids, m_sims) + tuple(res[2:])
+
+
+class ReplicatedIndex:
+    """Query-parallel mode (replicas): every rank builds the whole index under the same seed and
+    answers its own query batch; no collective on the data path (the queries are independent
+    problems, so N ranks are N independent replicas)."""
+
+    def __init__(self, data, memory_budget: int, family, seed: int = 1, **opts):
+        self.row0 = 0
+        self.index = Index(data, memory_budget, family, seed=seed, **opts)
+
+    def search(self, queries, k: int, recall: float, **sopts):
+        return self.index.search(queries, k, recall, **sopts)
