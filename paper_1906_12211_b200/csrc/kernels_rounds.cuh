@@ -193,7 +193,10 @@ constexpr int kTile = PFG_TILE;   // emitted positions per scan tile
 constexpr int kDedupeLong = PFG_DLONG;  // emitted positions from which k_dedupe schedules a chunk first
 
 template <int EPL, typename PP>
-__global__ void __launch_bounds__(128) k_expand(PP pp, int par, int lazy) {
+#ifndef PFG_EXPAND_MINB
+#define PFG_EXPAND_MINB 1
+#endif
+__global__ void __launch_bounds__(128, PFG_EXPAND_MINB) k_expand(PP pp, int par, int lazy) {
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
