@@ -205,8 +205,9 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"config{args.config}: {c['name']}", "n": n, "d": c["d"], "nq": nq, "k": c["k"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config{args.config}: {c['name']}" + WORKLOAD_NOTE.get(args.config, ""),
+                   "n": n, "d": c["d"], "nq": nq, "k": c["k"],
                    "recall_target": args.recall, "family": c["family"], "reps": L, "rep_chunk": args.rep_chunk},
         "recall": rec,
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle",
