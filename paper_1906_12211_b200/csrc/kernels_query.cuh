@@ -490,20 +490,42 @@ __device__ __forceinline__ bool drain(const QueryParams& p, const WarpSmem& w, Q
     if (p.prof && lane == 0) atomicAdd(p.prof + 5, (unsigned long long)(clock64() - td0));
     int e = 0;
     bool stop = false;
+    // survivors are in repetition order: the run of repetition r ends at the first entry > r.
+    // Lane t finds that end for repetition r0 + t and loads its stop threshold, all lanes at once
+    // (instead of one dependent search and load per repetition in the loop below)
+    const int r0 = next_check;
+    int myend = 0;
+    float mythr = INFINITY;
+    {
+        const int rt = r0 + lane;
+        int lo = 0, hi = nbuf;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.f->srep[mid] <= rt) lo = mid + 1; else hi = mid; }
+        myend = lo;
+        if (rt < nr) {
+            const int col = p.tensor_s ? c0 : c0 + rt;   // tensor: thresholds per (depth, shell)
+            mythr = __ldg(p.thr + (int64_t)(i - 1) * p.L + col);
+        }
+    }
     for (;;) {
-        // survivors are in repetition order: the run of next_check ends at the first entry > it
-        int lo = e, hi = nbuf;
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.f->srep[mid] <= next_check) lo = mid + 1; else hi = mid; }
-        const int e2 = lo;
+        const int t = next_check - r0;
+        int e2;
+        if (t < 32) {
+            e2 = __shfl_sync(kFull, myend, t);
+        } else {
+            int lo = e, hi = nbuf;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (w.f->srep[mid] <= next_check) lo = mid + 1; else hi = mid; }
+            e2 = lo;
+        }
         if (e2 > e) merge_range(p, w, st, e, e2, qi, lane);
         e = e2;
         if (next_check >= complete || next_check >= nr) break;
         const int j1 = c0 + next_check + 1;
         const bool check = p.tensor_s ? (next_check == nr - 1) : (!p.per_round || j1 == p.L);
+        const float th = t < 32 ? __shfl_sync(kFull, mythr, t)
+                                : __ldg(p.thr + (int64_t)(i - 1) * p.L + (p.tensor_s ? c0 : j1 - 1));
         if (st.tn == p.k_eff && check) {
             const float ip = kth_sim_clamped(p, st);
-            const int col = p.tensor_s ? c0 : j1 - 1;   // tensor: thresholds per (depth, shell)
-            if (ip >= __ldg(p.thr + (int64_t)(i - 1) * p.L + col)) { r_stop = next_check; stop = true; break; }
+            if (ip >= th) { r_stop = next_check; stop = true; break; }
         }
         ++next_check;
     }
