@@ -1678,7 +1678,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             p1.resume = 1;
             // the queries the fused kernel resumes get codes and match ranges for kExtReps more
             // repetitions in bulk (they would otherwise hash and search them one warp at a time)
-            if (lazy && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+            if (lazy && I->qc_n > 0 && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
                 const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
                 PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, I->aux, &r.ctl->nfused));
                 const int64_t thr_n = nq * (int64_t)nr;

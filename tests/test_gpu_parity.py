@@ -576,3 +576,23 @@ def test_randomised_option_combinations(cases, cases16, monkeypatch):
             monkeypatch.delenv("PFG_LOOP_MIN", raising=False)
             monkeypatch.delenv("PFG_LOOP_MAX", raising=False)
         _compare(c, k, recall, gk, kw)
+
+
+# ------------------------------------------------------------------ degenerate shapes
+@pytest.mark.parametrize("n,d", [(1, 4), (2, 1), (7, 3), (300, 2), (5000, 1), (3000, 300), (2000, 700)])
+@pytest.mark.parametrize("family", [O.HP, O.FHTCP])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_tiny_and_degenerate_shapes(n, d, family, engine):
+    rng = np.random.default_rng(n * 31 + d)
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    data[data == 0] = 1.0
+    q = rng.standard_normal((17, d)).astype(np.float32)
+    q[q == 0] = 1.0
+    # duplicate rows and a query equal to a data row
+    if n > 3:
+        data[3] = data[1]
+        q[0] = data[2]
+    c = Case("tiny", data, q, family, 6, 5)
+    for k in (1, 5, 12):
+        for recall in (0.5, 0.95, 1.0):
+            _compare(c, k, recall, dict(rep_chunk=4, engine=engine), dict(rep_chunk=4), trace=recall < 1.0)
