@@ -596,3 +596,54 @@ def test_tiny_and_degenerate_shapes(n, d, family, engine):
     for k in (1, 5, 12):
         for recall in (0.5, 0.95, 1.0):
             _compare(c, k, recall, dict(rep_chunk=4, engine=engine), dict(rep_chunk=4), trace=recall < 1.0)
+
+
+def test_fuzz_shapes_families_options(monkeypatch):
+    # seeded random index shapes x families x strategies x storage x search options, each against the
+    # oracle (30 cases by default; PFG_FUZZ_N / PFG_FUZZ_SEED for longer runs)
+    import os
+    rng = np.random.default_rng(int(os.environ.get("PFG_FUZZ_SEED", 99)))
+    nfuzz, compared = int(os.environ.get("PFG_FUZZ_N", 30)), 0
+    for it in range(nfuzz):
+        n = int(rng.choice([1, 3, 17, 200, 1000, 2500]))
+        d = int(rng.choice([1, 2, 5, 16, 33, 64, 100, 130]))
+        family = int(rng.choice([O.HP, O.FHTCP, O.CP])) if d <= 128 else int(rng.choice([O.HP, O.FHTCP]))
+        strategy = int(rng.choice([O.INDEPENDENT, O.POOL]))
+        L = int(rng.integers(1, 13))
+        storage = "i16" if rng.random() < 0.25 else "f32"
+        M = int(rng.choice([32, 32, 8, 0]))
+        data = rng.standard_normal((n, d)).astype(np.float32)
+        data[data == 0] = 0.5
+        q = rng.standard_normal((int(rng.integers(1, 40)), d)).astype(np.float32)
+        q[q == 0] = 0.5
+        fam = {O.HP: "simhash", O.FHTCP: "fht_cp", O.CP: "cp"}[family]
+        strat = "pool" if strategy == O.POOL else "independent"
+        ell = 1 if family == O.HP else 1 + int(np.ceil(np.log2(max(2, 1 << int(np.ceil(np.log2(max(d, 1))))))))
+        pool_bits = int(max(2 * 24, 24 * 4) * ell) if strategy == O.POOL else 3072
+        try:
+            g = pfg.Index(_cuda(data), 0, fam, seed=int(it + 1), reps=L, strategy=strat, pool_bits=pool_bits,
+                          sketch_words=M if M > 0 else -1, storage=storage, cp_draws=200)
+        except pfg.PfgError:
+            continue  # a combination the library rejects by design (e.g. FHT-CP pool too small)
+        o = O.OracleIndex(data, family, L=L, seed=int(it + 1), strategy=strategy, pool_bits=pool_bits, M=M,
+                          storage=storage, cp_draws=200)
+        c = Case.__new__(Case)
+        c.name, c.data, c.q, c.gpu, c.orc = f"fuzz{it}", data, q, g, o
+        R = int(rng.choice([1, 3, 8, 16]))
+        kw = dict(rep_chunk=R, segment=int(rng.choice([1, 12, 40])), use_filter=bool(rng.random() < 0.8),
+                  eps=float(rng.choice([0.0, 0.25])))
+        gk = dict(kw, engine=int(rng.random() < 0.3), rounds=int(rng.choice([0, 1, 3])),
+                  wide=int(rng.choice([0, 0, 2])))
+        if rng.random() < 0.5:
+            monkeypatch.setenv("PFG_LOOP_MIN", "1")
+            monkeypatch.setenv("PFG_LOOP_MAX", "1000000")
+        else:
+            monkeypatch.delenv("PFG_LOOP_MIN", raising=False)
+            monkeypatch.delenv("PFG_LOOP_MAX", raising=False)
+        k = int(rng.choice([1, 4, 10, 33]))
+        recall = float(rng.choice([0.5, 0.9, 0.99, 1.0]))
+        _compare(c, k, recall, gk, kw, trace=recall < 1.0)
+        g.close()
+        compared += 1
+    print(f"fuzz: {compared} of {nfuzz} cases compared")
+    assert compared >= nfuzz // 2
