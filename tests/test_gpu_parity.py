@@ -610,6 +610,8 @@ def test_fuzz_shapes_families_options(monkeypatch):
         family = int(rng.choice([O.HP, O.FHTCP, O.CP])) if d <= 128 else int(rng.choice([O.HP, O.FHTCP]))
         strategy = int(rng.choice([O.INDEPENDENT, O.POOL]))
         L = int(rng.integers(1, 13))
+        if family == O.HP and rng.random() < 0.2:
+            strategy, L = O.TENSOR, int(rng.choice([4, 16]))   # tensoring: L an even power of two
         storage = "i16" if rng.random() < 0.25 else "f32"
         M = int(rng.choice([32, 32, 8, 0]))
         data = rng.standard_normal((n, d)).astype(np.float32)
@@ -617,7 +619,7 @@ def test_fuzz_shapes_families_options(monkeypatch):
         q = rng.standard_normal((int(rng.integers(1, 40)), d)).astype(np.float32)
         q[q == 0] = 0.5
         fam = {O.HP: "simhash", O.FHTCP: "fht_cp", O.CP: "cp"}[family]
-        strat = "pool" if strategy == O.POOL else "independent"
+        strat = {O.POOL: "pool", O.TENSOR: "tensor"}.get(strategy, "independent")
         ell = 1 if family == O.HP else 1 + int(np.ceil(np.log2(max(2, 1 << int(np.ceil(np.log2(max(d, 1))))))))
         pool_bits = int(max(2 * 24, 24 * 4) * ell) if strategy == O.POOL else 3072
         try:
