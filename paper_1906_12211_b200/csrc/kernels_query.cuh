@@ -550,6 +550,12 @@ __device__ __forceinline__ uint32_t hs_next(uint32_t h) {
 __device__ __forceinline__ bool claim(const WarpSmem& w, const QState& st, uint32_t* bm, uint32_t id) {
     if (st.bitmap_mode) {
         const uint32_t bit = 1u << (id & 31);
+#ifndef PFG_BM_READFIRST
+#define PFG_BM_READFIRST 1
+#endif
+        // most passing ids of a long search were evaluated before: read the word first and claim
+        // only when the bit is clear (bits are only ever set during a query, so a set bit is final)
+        if (PFG_BM_READFIRST && (__ldcg(bm + (id >> 5)) & bit)) return false;
         return !(atomicOr(bm + (id >> 5), bit) & bit);
     }
     uint32_t h = hs_slot(id);
