@@ -366,23 +366,23 @@ __global__ void __launch_bounds__(256) k_fht_funcs(const float* __restrict__ X, 
 // of ell bits; each <a_i, x> is the sequential fmaf chain over t (R-2 projections).  The
 // hyperplanes are stored transposed, AT[f][t][i] (i padded to d32 = 32 ceil(d/32)), so a warp reads
 // them coalesced: lane l holds hyperplanes l, l + 32, ... (NI per lane) of 4 rows at once (x[t]
-// broadcast), 4 NI chains per step; the argmax is reduced across the warp.  Warp per (4 rows,
+// broadcast), RW NI chains per step; the argmax is reduced across the warp.  Warp per (RW rows,
 // function blockIdx.y).
-template <int NI>
+template <int NI, int RW>
 __global__ void __launch_bounds__(128) k_cp_funcs(const float* __restrict__ X, int64_t np, int ldx,
                                                   const float* __restrict__ AT, int nfun, int d, int d32, int ell,
                                                   uint16_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
-    const int64_t p0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4;
+    const int64_t p0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RW;
     const int f = blockIdx.y;
     if (p0 >= np) return;
     const float* A = AT + (int64_t)f * d * d32;
-    const float* xr[4];
+    const float* xr[RW];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) xr[r] = X + min(p0 + r, np - 1) * ldx;
-    float s[4][NI];
+    for (int r = 0; r < RW; ++r) xr[r] = X + min(p0 + r, np - 1) * ldx;
+    float s[RW][NI];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < RW; ++r)
 #pragma unroll
         for (int k = 0; k < NI; ++k) s[r][k] = 0.0f;
     for (int t = 0; t < d; ++t) {
@@ -390,14 +390,14 @@ __global__ void __launch_bounds__(128) k_cp_funcs(const float* __restrict__ X, i
 #pragma unroll
         for (int k = 0; k < NI; ++k) a[k] = __ldg(A + (int64_t)t * d32 + k * 32 + lane);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < RW; ++r) {
             const float xv = __ldg(xr[r] + t);
 #pragma unroll
             for (int k = 0; k < NI; ++k) s[r][k] = fmaf(a[k], xv, s[r][k]);
         }
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < RW; ++r) {
         float best = -1.0f;
         int bi = 0;
         bool neg = false;

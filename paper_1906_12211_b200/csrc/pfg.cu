@@ -813,12 +813,17 @@ pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, u
         if (!pool_ready) {
             PFG_TRY(poolvals.ensure((size_t)np * F * 2, "cp function codes"));
             const int d32 = (g.d + 31) / 32 * 32;
-            const dim3 gb((unsigned)((np + 15) / 16), (unsigned)F);   // 4 warps x 4 rows per block
+#ifndef PFG_CP_RW
+#define PFG_CP_RW 8
+#endif
+            constexpr int RW = PFG_CP_RW;   // rows per warp (register tile RW x NI)
             switch (d32 / 32) {
 #define PFG_CP_CASE(NI)                                                                                  \
     case NI:                                                                                             \
-        k_cp_funcs<NI><<<gb, 128, 0, st>>>(X, np, g.dpad, I->hpfn.as<float>(), F, g.d, d32, g.ell,       \
-                                           poolvals.as<uint16_t>());                                    \
+        k_cp_funcs<NI, (NI > 4 ? 4 : RW)><<<dim3((unsigned)((np + 4 * (NI > 4 ? 4 : RW) - 1) /          \
+                                                          (4 * (NI > 4 ? 4 : RW))), (unsigned)F),         \
+                                           128, 0, st>>>(X, np, g.dpad, I->hpfn.as<float>(), F, g.d, d32, \
+                                                         g.ell, poolvals.as<uint16_t>());                \
         break;
                 PFG_CP_CASE(1) PFG_CP_CASE(2) PFG_CP_CASE(3) PFG_CP_CASE(4)
                 PFG_CP_CASE(5) PFG_CP_CASE(6) PFG_CP_CASE(7) PFG_CP_CASE(8)
