@@ -369,17 +369,23 @@ __global__ void __launch_bounds__(256) k_fht_funcs(const float* __restrict__ X, 
 // broadcast), RW NI chains per step; the argmax is reduced across the warp.  Warp per (RW rows,
 // function blockIdx.y).
 template <int NI, int RW>
-__global__ void __launch_bounds__(128) k_cp_funcs(const float* __restrict__ X, int64_t np, int ldx,
+__global__ void __launch_bounds__(128) k_cp_funcs(const float* __restrict__ X, int64_t np_, int ldx,
                                                   const float* __restrict__ AT, int nfun, int d, int d32, int ell,
-                                                  uint16_t* __restrict__ out) {
+                                                  uint16_t* __restrict__ out, const uint32_t* __restrict__ qlist,
+                                                  const uint32_t* __restrict__ np_dev) {
+    // rows: 0..np-1, or qlist[0..np) (np from device memory if np_dev); output row = list index
     const int lane = threadIdx.x & 31;
+    const int64_t np = np_dev ? (int64_t)*np_dev : np_;
     const int64_t p0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RW;
     const int f = blockIdx.y;
     if (p0 >= np) return;
     const float* A = AT + (int64_t)f * d * d32;
     const float* xr[RW];
 #pragma unroll
-    for (int r = 0; r < RW; ++r) xr[r] = X + min(p0 + r, np - 1) * ldx;
+    for (int r = 0; r < RW; ++r) {
+        const int64_t pr = min(p0 + r, np - 1);
+        xr[r] = X + (qlist ? (int64_t)qlist[pr] : pr) * ldx;
+    }
     float s[RW][NI];
 #pragma unroll
     for (int r = 0; r < RW; ++r)
@@ -418,18 +424,21 @@ __global__ void __launch_bounds__(128) k_cp_funcs(const float* __restrict__ X, i
     }
 }
 
-__global__ void k_pool_codes(const uint16_t* __restrict__ fc, int64_t np, int m, int r0, int nreps, int c,
+__global__ void k_pool_codes(const uint16_t* __restrict__ fc, int64_t np_, int m, int r0, int nreps, int c,
                              int ell, int K, const int32_t* __restrict__ sel, uint64_t* __restrict__ keys,
-                             uint32_t* __restrict__ codes, int ldc) {
+                             uint32_t* __restrict__ codes, int ldc, const uint32_t* __restrict__ qlist = nullptr,
+                             const uint32_t* __restrict__ np_dev = nullptr, int fbase = 0) {
+    // fc row p holds functions [fbase, fbase + m); the codes go to row qlist[p] (or p)
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int r = blockIdx.y;
+    const int64_t np = np_dev ? (int64_t)*np_dev : np_;
     if (p >= np || r >= nreps) return;
     const int j = r0 + r;
     uint64_t full = 0;
-    for (int t = 0; t < c; ++t) full = (full << ell) | __ldg(fc + p * m + __ldg(sel + (int64_t)j * c + t));
+    for (int t = 0; t < c; ++t) full = (full << ell) | __ldg(fc + p * m + __ldg(sel + (int64_t)j * c + t) - fbase);
     const uint32_t code = (uint32_t)(full >> (c * ell - K));
     if (keys) keys[(int64_t)r * np + p] = ((uint64_t)code << 32) | (uint64_t)p;
-    if (codes) codes[p * ldc + j] = code;
+    if (codes) codes[(qlist ? (int64_t)qlist[p] : p) * ldc + j] = code;
 }
 
 // ---------------------------------------------------------------------------------------------

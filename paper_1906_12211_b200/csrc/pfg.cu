@@ -379,7 +379,7 @@ struct pfg_index {
     std::map<std::tuple<uint32_t, int, int>, std::shared_ptr<DBuf>> thr_cache;
     std::map<uint32_t, std::shared_ptr<DBuf>> tau_cache;
     // per-call scratch (grow-only)
-    DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, outb_ids, outb_sims, outb_stats, outb_trace, work, qx16;
+    DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, qfc2, outb_ids, outb_sims, outb_stats, outb_trace, work, qx16;
     DBuf qord_keys, qord_sorted, qord_list, qord_temp;  // longest-first processing order (fused engine)
     DBuf cur, bitmap, claims;
     // round-engine state (per query, grow-only)
@@ -781,6 +781,34 @@ pfg_status gen_functions(pfg_index* I, cudaStream_t st) {
 
 // codes of np normalised rows X for repetitions [r0, r0+nb): keys [r][p] and/or codes [p][ldc]
 // (pool strategy: pool values computed once into `poolvals`)
+// exact CP function values of functions [f0, f0 + nf) for rows 0..np-1 or qlist[0..np) (np_dev:
+// the count in device memory) into out [np][nf] (uint16)
+pfg_status cp_values(pfg_index* I, const float* X, int64_t np, const uint32_t* qlist, const uint32_t* np_dev, int f0, int nf,
+                     uint16_t* out, cudaStream_t st) {
+    const Geo& g = I->g;
+    const int d32 = (g.d + 31) / 32 * 32;
+    const float* AT = I->hpfn.as<float>() + (int64_t)f0 * g.d * d32;
+#ifndef PFG_CP_RW
+#define PFG_CP_RW 8
+#endif
+    constexpr int RW = PFG_CP_RW;   // rows per warp (register tile RW x NI)
+    switch (d32 / 32) {
+#define PFG_CP_CASE(NI)                                                                                        \
+    case NI: {                                                                                                 \
+        constexpr int rw = NI > 4 ? 4 : RW;                                                                    \
+        k_cp_funcs<NI, rw><<<dim3((unsigned)((np + 4 * rw - 1) / (4 * rw)), (unsigned)nf), 128, 0, st>>>(     \
+            X, np, g.dpad, AT, nf, g.d, d32, g.ell, out, qlist, np_dev);                                       \
+        break;                                                                                                 \
+    }
+        PFG_CP_CASE(1) PFG_CP_CASE(2) PFG_CP_CASE(3) PFG_CP_CASE(4)
+        PFG_CP_CASE(5) PFG_CP_CASE(6) PFG_CP_CASE(7) PFG_CP_CASE(8)
+#undef PFG_CP_CASE
+        default: return fail(PFG_E_ARG, "exact cross-polytope family supports d <= 256");
+    }
+    PFG_CUDA(cudaGetLastError());
+    return PFG_OK;
+}
+
 pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, uint64_t* keys, uint32_t* codes, int ldc,
                      DBuf& bits, DBuf& poolvals, bool& pool_ready, cudaStream_t st) {
     const Geo& g = I->g;
@@ -812,24 +840,7 @@ pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, u
         const int F = g.strategy == PFG_POOL ? g.m : g.L * g.c;
         if (!pool_ready) {
             PFG_TRY(poolvals.ensure((size_t)np * F * 2, "cp function codes"));
-            const int d32 = (g.d + 31) / 32 * 32;
-#ifndef PFG_CP_RW
-#define PFG_CP_RW 8
-#endif
-            constexpr int RW = PFG_CP_RW;   // rows per warp (register tile RW x NI)
-            switch (d32 / 32) {
-#define PFG_CP_CASE(NI)                                                                                  \
-    case NI:                                                                                             \
-        k_cp_funcs<NI, (NI > 4 ? 4 : RW)><<<dim3((unsigned)((np + 4 * (NI > 4 ? 4 : RW) - 1) /          \
-                                                          (4 * (NI > 4 ? 4 : RW))), (unsigned)F),         \
-                                           128, 0, st>>>(X, np, g.dpad, I->hpfn.as<float>(), F, g.d, d32, \
-                                                         g.ell, poolvals.as<uint16_t>());                \
-        break;
-                PFG_CP_CASE(1) PFG_CP_CASE(2) PFG_CP_CASE(3) PFG_CP_CASE(4)
-                PFG_CP_CASE(5) PFG_CP_CASE(6) PFG_CP_CASE(7) PFG_CP_CASE(8)
-#undef PFG_CP_CASE
-                default: return fail(PFG_E_ARG, "exact cross-polytope family supports d <= 256");
-            }
+            PFG_TRY(cp_values(I, X, np, nullptr, nullptr, 0, F, poolvals.as<uint16_t>(), st));
             pool_ready = true;
             I->launches += 1;
         }
@@ -932,7 +943,7 @@ pfg_status get_tau(pfg_index* I, float eps, std::shared_ptr<DBuf>& out, std::vec
 
 // normalise + sketch + (eager) code queries into index scratch; returns first zero row or -1
 pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool need_codes, bool force_codes, int64_t* zrow,
-                        bool* lazy, cudaStream_t st, int split) {
+                        bool* lazy, cudaStream_t st, int split, int cp_eager = 0) {
     const Geo& g = I->g;
     const float* qsrc = queries;
     if (!is_device_ptr(queries)) {
@@ -984,7 +995,20 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     *lazy = (g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT && !force_codes);
     I->qc_n = 0;
     I->qc_ld = g.L;
-    if (need_codes && !*lazy) {
+    if (need_codes && !*lazy && cp_eager > 0) {
+        // exact CP, independent: the repetitions the blind rounds can reach only (cp_eager); the
+        // queries still running after them get the rest in bulk (the caller)
+        PFG_TRY(I->qcodes.ensure((size_t)nq * g.L * 4, "query codes"));
+        const int F = cp_eager * g.c;
+        PFG_TRY(I->qfc.ensure((size_t)nq * F * 2, "cp function codes"));
+        PFG_TRY(cp_values(I, I->qx.as<float>(), nq, nullptr, nullptr, 0, F, I->qfc.as<uint16_t>(), st));
+        k_pool_codes<<<dim3((unsigned)((nq + 255) / 256), (unsigned)cp_eager), 256, 0, st>>>(
+            I->qfc.as<uint16_t>(), nq, F, 0, cp_eager, g.c, g.ell, g.K, I->sel.as<int32_t>(), nullptr,
+            I->qcodes.as<uint32_t>(), g.L);
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 2;
+        I->qc_n = cp_eager;
+    } else if (need_codes && !*lazy) {
         PFG_TRY(I->qcodes.ensure((size_t)nq * g.L * 4, "query codes"));
         bool pool_ready = false;
         PFG_TRY(hash_reps(I, I->qx.as<float>(), nq, 0, g.L, nullptr, I->qcodes.as<uint32_t>(), g.L, I->qbits, I->qfc,
@@ -1344,7 +1368,18 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // rounds 0 and 1 reach repetitions [0, 1 + R) only (R-17 default schedule): the codes and
     // ranges of the later eager repetitions are computed beside them
     const int split = (s.engine == 0 && !s.uniform && g.strategy != PFG_TENSOR) ? 1 + s.R : 0;
-    PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st, split));
+    // exact CP (independent): hash only the repetitions the blind rounds can reach; the fused
+    // kernel's queries get the rest in bulk after them (not with the device-side loop, which may
+    // run any query to the end)
+    int cp_eager = 0;
+    if (g.family == PFG_CROSSPOLYTOPE && g.strategy == PFG_INDEPENDENT && s.engine == 0 && s.wide <= 0 && !I->loop_heavy &&
+        !getenv("PFG_LOOP_MAX") && !getenv("PFG_NO_CP_LAZY")) {
+        const int mr = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : (s.rounds > 0 ? s.rounds : 5);
+        const int64_t reach = s.uniform ? (int64_t)s.R * mr : 1 + (int64_t)s.R * (mr - 1);
+        const int64_t e = std::min<int64_t>(g.L, std::max<int64_t>(reach, I->eager));
+        cp_eager = e < g.L ? (int)e : 0;
+    }
+    PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st, split, cp_eager));
 
     const int k_eff = (int)std::min<int64_t>(k, g.n);
     const int kt = ((k_eff + 31) / 32) * 32;
@@ -1683,6 +1718,19 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             p1.resume = 1;
             // the queries the fused kernel resumes get codes and match ranges for kExtReps more
             // repetitions in bulk (they would otherwise hash and search them one warp at a time)
+            if (cp_eager > 0) {
+                // exact CP: the codes of repetitions [cp_eager, L) for the queries the fused kernel
+                // resumes (it cannot hash CP functions itself)
+                const int f0 = cp_eager * g.c, nf = (g.L - cp_eager) * g.c;
+                PFG_TRY(I->qfc2.ensure((size_t)nq * nf * 2, "cp function codes (resumed queries)"));
+                PFG_TRY(cp_values(I, I->qx.as<float>(), nq, r.fused, &r.ctl->nfused, f0, nf, I->qfc2.as<uint16_t>(), I->aux));
+                k_pool_codes<<<dim3((unsigned)((nq + 255) / 256), (unsigned)(g.L - cp_eager)), 256, 0, I->aux>>>(
+                    I->qfc2.as<uint16_t>(), nq, nf, cp_eager, g.L - cp_eager, g.c, g.ell, g.K, I->sel.as<int32_t>(), nullptr,
+                    I->qcodes.as<uint32_t>(), g.L, r.fused, &r.ctl->nfused, f0);
+                PFG_CUDA(cudaGetLastError());
+                I->launches += 2;
+                p1.qc_n = g.L;
+            }
             if (lazy && I->qc_n > 0 && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
                 const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
                 PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, I->aux, &r.ctl->nfused));

@@ -57,6 +57,9 @@ def cases():
     out["cp"] = Case("cp", d1, q1, O.CP, 16, 21)
     out["cp_pool"] = Case("cp_pool", d1, q1[:40], O.CP, 16, 22, O.POOL, 600)
     out["cp100"] = Case("cp100", d2[:6000], q2[:40], O.CP, 12, 23)
+    # more repetitions than the blind rounds reach: only those are hashed up front, the queries
+    # the fused kernel resumes get the rest in bulk
+    out["cp48"] = Case("cp48", d1, q1, O.CP, 48, 24)
     return out
 
 
@@ -649,3 +652,12 @@ def test_fuzz_shapes_families_options(monkeypatch):
         compared += 1
     print(f"fuzz: {compared} of {nfuzz} cases compared")
     assert compared >= nfuzz // 2
+
+
+
+@pytest.mark.parametrize("rounds", [1, 2, 5])
+@pytest.mark.parametrize("recall", [0.9, 0.99, 1.0])
+def test_search_parity_cp_partial_hashing(cases, rounds, recall):
+    c = cases["cp48"]
+    _compare(c, 10, recall, dict(rep_chunk=8, rounds=rounds), dict(rep_chunk=8), trace=recall < 1.0)
+    _compare(c, 10, recall, dict(rep_chunk=2, rounds=rounds), dict(rep_chunk=2), trace=recall < 1.0)
