@@ -68,7 +68,7 @@ __device__ __forceinline__ void fht_warp(float (&v)[EPL], int dp, int lane) {
 
 // Thread-local FHT cross-polytope code (same arithmetic as fhtcp_code_warp, one function per
 // thread, the whole DP-vector in registers).  Used to hash query batches for the first
-// repetitions eagerly (k_fht_qcodes).
+// repetitions eagerly (k_fht_qcodes_g).
 template <int DP>
 __device__ __forceinline__ uint32_t fhtcp_code_thread(const float* __restrict__ xrow, int d, int ell,
                                                       const uint32_t* __restrict__ sg) {

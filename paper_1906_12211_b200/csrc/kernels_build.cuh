@@ -242,22 +242,6 @@ __global__ void __launch_bounds__(256) k_fht_rep(const float* __restrict__ X, in
     }
 }
 
-// Eager FHT-CP query codes for repetitions [0, nreps): one thread per (row, repetition), 32
-// consecutive threads share a row (its loads broadcast); out codes [p][ldc].
-template <int DP>
-__global__ void __launch_bounds__(128) k_fht_qcodes(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
-                                                    int c, int K, const uint32_t* __restrict__ sg, int nreps,
-                                                    uint32_t* __restrict__ codes, int ldc) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t p = t / nreps;
-    const int j = (int)(t % nreps);
-    if (p >= np) return;
-    constexpr int W = (DP + 31) / 32;
-    uint64_t full = 0;
-    for (int f = 0; f < c; ++f)
-        full = (full << ell) | fhtcp_code_thread<DP>(X + p * ldx, d, ell, sg + ((int64_t)j * c + f) * 3 * W);
-    codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
-}
 
 // Eager FHT-CP query codes, TPF threads per (row, repetition): the TPF consecutive lanes of a group
 // hold coordinate blocks [g*H, (g+1)*H) of the same vector (H = DP/TPF).  Stages h < H are in
