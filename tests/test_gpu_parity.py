@@ -608,7 +608,8 @@ def test_fuzz_shapes_families_options(monkeypatch):
     rng = np.random.default_rng(int(os.environ.get("PFG_FUZZ_SEED", 99)))
     nfuzz, compared = int(os.environ.get("PFG_FUZZ_N", 30)), 0
     for it in range(nfuzz):
-        n = int(rng.choice([1, 3, 17, 200, 1000, 2500]))
+        big = os.environ.get("PFG_FUZZ_BIG") is not None
+        n = int(rng.choice([1, 3, 17, 200, 1000, 2500] + ([20000, 60000] if big else [])))
         d = int(rng.choice([1, 2, 5, 16, 33, 64, 100, 130]))
         family = int(rng.choice([O.HP, O.FHTCP, O.CP])) if d <= 128 else int(rng.choice([O.HP, O.FHTCP]))
         strategy = int(rng.choice([O.INDEPENDENT, O.POOL]))
@@ -619,7 +620,7 @@ def test_fuzz_shapes_families_options(monkeypatch):
         M = int(rng.choice([32, 32, 8, 0]))
         data = rng.standard_normal((n, d)).astype(np.float32)
         data[data == 0] = 0.5
-        q = rng.standard_normal((int(rng.integers(1, 40)), d)).astype(np.float32)
+        q = rng.standard_normal((int(rng.integers(1, 400 if big else 40)), d)).astype(np.float32)
         q[q == 0] = 0.5
         fam = {O.HP: "simhash", O.FHTCP: "fht_cp", O.CP: "cp"}[family]
         strat = {O.POOL: "pool", O.TENSOR: "tensor"}.get(strategy, "independent")
