@@ -469,8 +469,12 @@ __global__ void __launch_bounds__(256) k_scan(PP pp, int par) {
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (WIDE)  // WIDE = false: no wide queries in this search (the lean variant keeps its registers)
         for (int64_t aw = wid * 2; aw < nwt; aw += nw * 2) scan_wide_tiles(p, aw, aw + 1 < nwt ? aw + 1 : -1, lane);
+    // the next tile's descriptor is fetched before this tile's entries are read
+    uint4 nd0 = make_uint4(0, 0, 0, 0), nd1 = nd0;
+    if (wid < ntiles) { nd0 = rs.tiles[2 * wid]; nd1 = rs.tiles[2 * wid + 1]; }
     for (int64_t a = wid; a < ntiles; a += nw) {
-        const uint4 d0 = rs.tiles[2 * a], d1 = rs.tiles[2 * a + 1];
+        const uint4 d0 = nd0, d1 = nd1;
+        if (a + nw < ntiles) { nd0 = rs.tiles[2 * (a + nw)]; nd1 = rs.tiles[2 * (a + nw) + 1]; }
         const int64_t q = d0.x;
         const uint32_t cnt = d0.w & 0xffffu, rep = (d0.w >> 16) & 0xffu, tau = d0.w >> 24;
         const uint64_t sk = ((uint64_t)d1.y << 32) | d1.x;
