@@ -623,26 +623,23 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                     }
                 }
             }
-            // claims of the rest in (repetition, position) order: lanes in order within u (the
-            // first lane of a group of equal ids claims), u in order; a later occurrence of an id
-            // claimed earlier in the batch finds it in the set
+            // claims of the rest in (repetition, position) order, u in order; a later occurrence
+            // of an id claimed earlier in the batch finds it in the set
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
                 if ((uint32_t)((u % (kTile / 32)) * 32) >= tc[u / (kTile / 32)]) continue;  // empty step (warp-uniform)
                 const bool pass = v[u] != kEmpty;
                 const bool need = pass && !found[u];
-                const uint32_t nm = __ballot_sync(kFull, need);
                 bool fresh = false;
+                // the 32 lanes of a step hold positions of one tile, i.e. of one repetition, whose
+                // ids are distinct: every lane claims its own id (no grouping of equal ids needed)
                 if (need) {
-                    const uint32_t grp = __match_any_sync(nm, v[u]);
-                    if ((int)(__ffs(grp) - 1) == lane) {
-                        uint32_t hh = h[u];
-                        for (;;) {
-                            const uint32_t old = atomicCAS(&c->hs[hh], kEmpty, v[u]);
-                            if (old == kEmpty) { fresh = true; break; }
-                            if (old == v[u]) break;
-                            hh = hs_next(hh);
-                        }
+                    uint32_t hh = h[u];
+                    for (;;) {
+                        const uint32_t old = atomicCAS(&c->hs[hh], kEmpty, v[u]);
+                        if (old == kEmpty) { fresh = true; break; }
+                        if (old == v[u]) break;
+                        hh = hs_next(hh);
                     }
                 }
                 if (rr[u] >= 0) {
