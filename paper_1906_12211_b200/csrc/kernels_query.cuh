@@ -775,10 +775,18 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
                         if (g < total && !pass[u]) atomicAdd(&w.f->fcnt[rv[u]], 1u);
                         // claims in (rep, position) order: lanes in order within u, u in order
                         const uint32_t pm = __ballot_sync(kFull, pass[u]);
+                        // a step inside one repetition holds distinct ids (each lane claims its
+                        // own); only a step across a repetition boundary needs equal ids grouped
+                        const int rfirst = __shfl_sync(kFull, rv[u], pm ? __ffs(pm) - 1 : 0);
+                        const bool onerep = __all_sync(kFull, !pass[u] || rv[u] == rfirst);
                         bool fresh = false;
                         if (pass[u]) {
-                            const uint32_t grp = __match_any_sync(pm, idv[u]);
-                            if ((int)(__ffs(grp) - 1) == lane) fresh = claim(w, st, bm, idv[u]);
+                            if (onerep) {
+                                fresh = claim(w, st, bm, idv[u]);
+                            } else {
+                                const uint32_t grp = __match_any_sync(pm, idv[u]);
+                                if ((int)(__ffs(grp) - 1) == lane) fresh = claim(w, st, bm, idv[u]);
+                            }
                         }
                         if (pass[u] && !fresh) atomicAdd(&w.f->dcnt[rv[u]], 1u);
                         const uint32_t fm = __ballot_sync(kFull, fresh);
