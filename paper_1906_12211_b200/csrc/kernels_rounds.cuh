@@ -194,7 +194,7 @@ constexpr int kDedupeLong = PFG_DLONG;  // emitted positions from which k_dedupe
 
 template <int EPL, typename PP>
 #ifndef PFG_EXPAND_MINB
-#define PFG_EXPAND_MINB 1
+#define PFG_EXPAND_MINB 6
 #endif
 __global__ void __launch_bounds__(128, PFG_EXPAND_MINB) k_expand(PP pp, int par, int lazy) {
     const QueryParams& p = deref(pp);
