@@ -527,7 +527,10 @@ struct DedupeSmem {
     uint32_t beg[kMaxR + 1];
     uint32_t fcnt[kMaxR], dcnt[kMaxR];
 };
-constexpr int kCPre = 8;   // candidate ids loaded per lane per batch
+#ifndef PFG_CPRE
+#define PFG_CPRE 8
+#endif
+constexpr int kCPre = PFG_CPRE;   // candidate ids loaded per lane per batch
 
 template <typename PP>
 __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
