@@ -458,8 +458,11 @@ __device__ __forceinline__ void scan_wide_tiles(const QueryParams& p, int64_t aw
     }
 }
 
+#ifndef PFG_SCAN_MINB
+#define PFG_SCAN_MINB 1
+#endif
 template <typename PP, bool WIDE>
-__global__ void __launch_bounds__(256) k_scan(PP pp, int par) {
+__global__ void __launch_bounds__(256, WIDE ? 1 : PFG_SCAN_MINB) k_scan(PP pp, int par) {
     const QueryParams& p = deref(pp);
     const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
@@ -916,8 +919,11 @@ __device__ __forceinline__ void push_fused(const RoundState& rs, uint32_t q) {
     else push(rs.fused, &rs.ctl->nfused, q);
 }
 
+#ifndef PFG_MERGE_MINB
+#define PFG_MERGE_MINB 10
+#endif
 template <typename PP, bool WIDE>
-__global__ void __launch_bounds__(128, WIDE ? 8 : 10) k_merge(PP pp, int par) {
+__global__ void __launch_bounds__(128, WIDE ? 8 : PFG_MERGE_MINB) k_merge(PP pp, int par) {
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
