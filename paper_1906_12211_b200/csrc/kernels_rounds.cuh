@@ -534,6 +534,12 @@ struct DedupeSmem {
 #define PFG_CPRE 8
 #endif
 constexpr int kCPre = PFG_CPRE;   // candidate ids loaded per lane per batch
+#ifndef PFG_DEDUPE_CPASYNC
+#define PFG_DEDUPE_CPASYNC 1
+#endif
+#ifndef PFG_DEDUPE_BULKSAVE
+#define PFG_DEDUPE_BULKSAVE 0
+#endif
 
 template <typename PP>
 __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
@@ -550,6 +556,10 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
         if (fl & (kFlagFused | kFlagWide)) continue;
         const uint4 info = rs.rinfo[q];
         if (info.w) continue;  // direct chunk: k_scan wrote the evaluated ids and the pool
+        if (PFG_DEDUPE_BULKSAVE) {  // the previous query's bulk save has read the set
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+        }
         const int nr = (int)info.x;
         const uint32_t ntl = info.z;
         const uint32_t nE = rs.cnt[q * kCnt + 3];
@@ -577,6 +587,14 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                         while (atomicCAS(&c->hs[h], kEmpty, v[u]) != kEmpty) h = hs_next(h);
                     }
             }
+        } else if (PFG_DEDUPE_CPASYNC) {
+            // global -> shared without the register round trip (LDGSTS, L2 only)
+#pragma unroll
+            for (int k = 0; k < kHC / 128; ++k) {
+                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4*>(c->hs) + k * 32 + lane);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(hsv + k * 32 + lane) : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
         } else {
             uint4 tmp[kHC / 128];
 #pragma unroll
@@ -697,11 +715,25 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
         const int nominal = min((ci == p.K && cc0 == 0 && !p.uniform) ? 1 : p.R, p.L - cc0);
         if (nE + ns > (uint32_t)kSaveMin && nr >= nominal) {
             if (lane == 0 && !saved) rs.flags[q] |= kFlagSaved;
+            if (PFG_DEDUPE_BULKSAVE) {
+                // one bulk copy (TMA engine) shared -> global, issued by lane 0 after every lane's
+                // writes are made visible to the async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(c->hs);
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(hsv), "r"(sa),
+                                 "r"((uint32_t)(kHC * 4)) : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            } else {
 #pragma unroll
-            for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
+                for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
+            }
         }
         __syncwarp();
     }
+    if (PFG_DEDUPE_BULKSAVE && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------------------------
