@@ -537,6 +537,9 @@ constexpr int kCPre = PFG_CPRE;   // candidate ids loaded per lane per batch
 #ifndef PFG_DEDUPE_CPASYNC
 #define PFG_DEDUPE_CPASYNC 1
 #endif
+#ifndef PFG_DEDUPE_LATEWAIT
+#define PFG_DEDUPE_LATEWAIT 0
+#endif
 #ifndef PFG_DEDUPE_BULKSAVE
 #define PFG_DEDUPE_BULKSAVE 0
 #endif
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                 const uint32_t sa = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4*>(c->hs) + k * 32 + lane);
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(hsv + k * 32 + lane) : "memory");
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
+            if (!PFG_DEDUPE_LATEWAIT) asm volatile("cp.async.wait_all;" ::: "memory");
         } else {
             uint4 tmp[kHC / 128];
 #pragma unroll
@@ -603,7 +606,6 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
             for (int k = 0; k < kHC / 128; ++k) reinterpret_cast<uint4*>(c->hs)[k * 32 + lane] = tmp[k];
         }
         if (lane < nr) { c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
-        __syncwarp();
         __syncwarp();
         uint32_t ns = 0;
         bool overflow = false;
@@ -631,6 +633,10 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                 const uint32_t g = (t0 + b) * kTile + o;
                 v[u] = live ? cand[g] : kEmpty;
                 rr[u] = live ? trep[b] : -1;
+            }
+            if (PFG_DEDUPE_LATEWAIT) {  // the restored set lands while the batch loads
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
             }
             // membership in the set as it stands before this batch: independent read-only probes
 #pragma unroll
@@ -675,6 +681,9 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                 ns += __popc(fm);
             }
             if (nE + ns > rs.hmax) overflow = true;
+        }
+        if (PFG_DEDUPE_LATEWAIT) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
         }
         __syncwarp();
         uint32_t base = 0;
