@@ -77,6 +77,8 @@ def lib():
         L.or_should_stop.restype = C.c_int
         L.or_should_stop.argtypes = [P, C.c_int, C.c_int, C.c_float, C.c_double, C.c_int]
         L.or_tau.restype = C.c_int; L.or_tau.argtypes = [C.c_float, C.c_float]
+        L.or_tau_prob.restype = C.c_int; L.or_tau_prob.argtypes = [C.c_float, C.c_double]
+        L.or_sim_seq.restype = C.c_float; L.or_sim_seq.argtypes = [P, P, C.c_int]
         L.or_search.restype = None
         L.or_search.argtypes = [P, P, C.c_int64, C.c_int, C.c_float, P, C.c_int, P, P, P, P, C.c_int]
         L.or_widen.restype = None
@@ -188,6 +190,17 @@ def tau(ipk: float, eps: float = 0.0) -> int:
     return int(lib().or_tau(ipk, eps))
 
 
+def tau_prob(ipk: float, delta: float) -> int:
+    """R-26: smallest t with P[Binomial(64, acos(ipk)/pi) <= t] >= 1 - delta"""
+    return int(lib().or_tau_prob(ipk, delta))
+
+
+def sim_seq(a, b) -> float:
+    """O-11 plain-order similarity (sequential fmaf chain)"""
+    a, b = _f32(a), _f32(b)
+    return float(lib().or_sim_seq(_p(a), _p(b), a.shape[0]))
+
+
 def lower_bound(codes, v: int) -> int:
     c = np.ascontiguousarray(codes, dtype=np.uint32)
     return int(lib().or_lower_bound_pub(_p(c), c.shape[0], v))
@@ -215,7 +228,7 @@ def bruteforce(x, q, k: int):
 class _SOpts(C.Structure):
     _fields_ = [("rep_chunk", C.c_int32), ("stop_rule", C.c_int32), ("per_round", C.c_int32),
                 ("segment", C.c_int32), ("use_filter", C.c_int32), ("eps", C.c_float),
-                ("uniform_chunks", C.c_int32)]
+                ("uniform_chunks", C.c_int32), ("sim_order", C.c_int32), ("tau_rule", C.c_int32)]
 
 
 class OracleIndex:
@@ -311,7 +324,8 @@ class OracleIndex:
 
     def search(self, queries, k: int, recall: float, rep_chunk: int = 1, stop_rule: int = 0,
                per_round: bool = False, segment: int = 12, use_filter: bool = True, eps: float = 0.0,
-               threads: int = 1, trace_cap: int = 0, uniform_chunks: bool = False):
+               threads: int = 1, trace_cap: int = 0, uniform_chunks: bool = False, sim_order: int = 0,
+               tau_rule: int = 0):
         """returns ids[nq,k] int64, sims[nq,k] f32, trace[nq,8] int32
         (i_stop, j_stop, emitted, filtered, dups, evaluated, flags, 0)
         and, if trace_cap > 0, the evaluated ids in evaluation order [nq, trace_cap] (uint32)."""
@@ -321,7 +335,8 @@ class OracleIndex:
         sims = np.empty((nq, k), dtype=np.float32)
         trace = np.zeros((nq, 8), dtype=np.int32)
         tids = np.zeros((nq, max(trace_cap, 1)), dtype=np.uint32)
-        o = _SOpts(rep_chunk, stop_rule, int(per_round), segment, int(use_filter), eps, int(uniform_chunks))
+        o = _SOpts(rep_chunk, stop_rule, int(per_round), segment, int(use_filter), eps, int(uniform_chunks),
+                   int(sim_order), int(tau_rule))
         lib().or_search(self._h, _p(q), nq, k, recall, C.byref(o), threads, _p(ids), _p(sims), _p(trace),
                         _p(tids) if trace_cap > 0 else None, trace_cap)
         if trace_cap > 0:

@@ -86,6 +86,11 @@ float or_dot(const float* a, const float* b, int d) {
  * each lane sum is a sequential fp32 fmaf chain in ascending t from +0 -- which are then added
  * pairwise in a fixed tree: for h = 16, 8, 4, 2, 1: s[l] = s[l] + s[l+h] (l < h).  This is the
  * order in which a warp reading a row with one 16-byte chunk per lane computes it. */
+/* O-11 plain-order similarity: one sequential fp32 fmaf chain over t = 0..d-1 from +0
+ * (the same order as or_dot).  The search uses it when or_sopts.sim_order = 1, to show that the
+ * results do not hinge on the R-2 lane-tree order (ties within 1e-6 excepted). */
+float or_sim_seq(const float* a, const float* b, int d) { return or_dot(a, b, d); }
+
 float or_sim(const float* a, const float* b, int d) {
     float s[32];
     for (int l = 0; l < 32; ++l) s[l] = 0.0f;
@@ -547,6 +552,30 @@ int or_tau(float ipk, float eps) {
     return (int)r;
 }
 
+/* R-26, the probabilistic reading of PAPER.md:327-328 ("tau ... according to the probability that a
+ * vector with Hamming distance tau or less has a dot product larger than the smallest dot product in
+ * the current top-k"): the Hamming distance of the 64-bit HP sketches of two unit vectors at inner
+ * product s is Binomial(64, acos(s)/pi) (64 independent HP bits), and it
+ * is stochastically smaller the larger s is; tau is the smallest t with P[H > t] <= delta_f at
+ * s = ip_k, so a vector at least as similar as the current k-th passes with probability >= 1 - delta_f.
+ * The search takes delta_f = delta = 1 - recall target.  The upper tail is summed in double from
+ * t = 64 down (smallest terms first, so the comparison with delta_f is not decided by rounding:
+ * delta_f = 0 gives 64 whenever p > 0). */
+double or_binom64(double p, int t) {
+    double c = 1.0;
+    for (int h = 0; h < t; ++h) c = c * (double)(64 - h) / (double)(h + 1);
+    return c * pow(p, (double)t) * pow(1.0 - p, (double)(64 - t));
+}
+int or_tau_prob(float ipk, double delta_f) {
+    double p = acos((double)ipk) / M_PI;
+    if (p < 0.0) p = 0.0;
+    if (p > 1.0) p = 1.0;
+    double tail = 0.0;   /* P[H > t] */
+    int t = 64;
+    while (t > 0 && tail + or_binom64(p, t) <= delta_f) { tail += or_binom64(p, t); --t; }
+    return t;
+}
+
 static int or_better(float s1, uint32_t i1, float s2, uint32_t i2) {
     return s1 > s2 || (s1 == s2 && i1 < i2);
 }
@@ -576,6 +605,8 @@ typedef struct {
     int32_t rep_chunk, stop_rule, per_round, segment, use_filter;
     float eps;
     int32_t uniform_chunks;  /* 0: the search's first chunk is a single repetition (R-17) */
+    int32_t sim_order;       /* 0: R-2 lane-tree similarity (or_sim); 1: plain sequential order (or_sim_seq) */
+    int32_t tau_rule;        /* 0: probabilistic, the (1 - delta)-quantile (R-26); 1: (1+eps) x expected Hamming distance (R-15) */
 } or_sopts;
 
 /* ----------------------------------------------------------------------------
@@ -639,7 +670,7 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
                 float ip = ts[k_eff - 1];
                 if (ip > 1.0f) ip = 1.0f;
                 if (ip < -1.0f) ip = -1.0f;
-                tau = or_tau(ip, o->eps);
+                tau = o->tau_rule ? or_tau(ip, o->eps) : or_tau_prob(ip, delta);
             }
             int nl;
             if (i > 0 && tensor) {
@@ -679,7 +710,9 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
                         E[id] = 1;
                         if (tids && nE < tcap) tids[nE] = id;
                         nE++;
-                        float sim = q16 ? or_sim16(q16, X->x16 + (int64_t)id * d, d) : or_sim(q, X->x + (int64_t)id * d, d);
+                        float sim = q16 ? or_sim16(q16, X->x16 + (int64_t)id * d, d)
+                                  : o->sim_order ? or_sim_seq(q, X->x + (int64_t)id * d, d)
+                                                 : or_sim(q, X->x + (int64_t)id * d, d);
                         /* insert into the sorted top list (Alg. 1 lines 6-7) */
                         if (nt < k_eff || or_better(sim, id, ts[k_eff - 1], ti[k_eff - 1])) {
                             int pos = nt < k_eff ? nt : k_eff - 1;
@@ -720,7 +753,8 @@ void or_search(or_index* X, const float* qraw, int64_t nq, int k, float recall, 
                           tids ? tids + i * (int64_t)tcap : NULL, tcap);
         return;
     }
-    for (int j = 0; j < X->L; ++j) or_need_rep(X, j);
+    /* repetition tables not built yet are built on first use, one at a time (or_need_rep's
+     * critical section) */
     #pragma omp parallel for schedule(dynamic) num_threads(nthreads)
     for (int64_t i = 0; i < nq; ++i)
         or_search_one(X, qraw + i * X->d, k, delta, o, oid + i * k, osim + i * k, trace + 8 * i,

@@ -105,26 +105,29 @@ def paper_synthetic(n: int, d: int, m: int, seed: int):
 
 
 # ---------------------------------------------------------------- BASELINE.json configs
+# reps = 0: L follows from the memory budget (R-11); `L` records that value (per shard
+# for config 5), so the CPU oracle legs need not load the product library (tests/test_abi.py checks
+# it against the library's cost model)
 CONFIGS = {
     1: dict(name="tiny", n=10_000, d=32, nq=100, k=10, recall=0.9, family="simhash",
             strategy="independent", reps=32, budget=None),
     2: dict(name="clustered-1Mx100", n=1_000_000, d=100, nq=10_000, k=10, recall=0.9,
-            family="fht_cp", strategy="independent", reps=0, budget=4 << 30),
+            family="fht_cp", strategy="independent", reps=0, L=241, budget=4 << 30),
     3: dict(name="planted-1Mx300", n=1_000_000, d=300, nq=10_000, k=1, recall=0.9,
-            family="simhash", strategy="independent", reps=0, budget=8 << 30),
+            family="simhash", strategy="independent", reps=0, L=458, budget=8 << 30),
     4: dict(name="hidim-1Mx960", n=1_000_000, d=960, nq=1_000, k=100, recall=0.9,
-            family="simhash", strategy="pool", reps=0, budget=16 << 30),
+            family="simhash", strategy="pool", reps=0, L=830, budget=16 << 30),
     5: dict(name="scaleout-100Mx100", n=100_000_000, d=100, nq=100_000, k=10, recall=0.9,
-            family="fht_cp", strategy="independent", reps=0, budget=120 << 30, shard_n=12_500_000),
+            family="fht_cp", strategy="independent", reps=0, L=618, budget=120 << 30, shard_n=12_500_000),
     # the paper's own SYNTHETIC set (n = 10^6, d = 100 -> vectors in R^300; every
     # query's nearest neighbour is the last row), with the paper's default pooled evaluation
     # and FHT-CP; not a BASELINE config, a second workload
     6: dict(name="paper-synthetic-1Mx300", n=1_000_000, d=300, nq=1_000, k=10, recall=0.9,
-            family="fht_cp", strategy="pool", reps=0, budget=8 << 30),
+            family="fht_cp", strategy="pool", reps=0, L=459, budget=8 << 30),
     # config 2's workload with the exact cross-polytope family (the paper's "CP" curve, Fig. 5,
     # PAPER.md:588, 648-652): d Gaussian hyperplanes per function instead of FHT rotations
     7: dict(name="clustered-1Mx100-exact-cp", n=1_000_000, d=100, nq=10_000, k=10, recall=0.9,
-            family="cp", strategy="independent", reps=0, budget=4 << 30),
+            family="cp", strategy="independent", reps=0, L=240, budget=4 << 30),
 }
 
 

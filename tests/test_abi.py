@@ -107,3 +107,14 @@ def test_bad_shapes_rejected():
         pfg.derive_reps(10, 0, "simhash", 1 << 30)
     with pytest.raises(pfg.PfgError, match="d <= 1024"):
         pfg.derive_reps(10, 2000, "fht_cp", 1 << 30)
+
+
+def test_config_records_carry_the_cost_model_L():
+    # synth.CONFIGS records the budget-derived L (R-11) so that the CPU oracle legs of
+    # bench.py need not load the product library; the record must equal the library's cost model
+    import synth
+    for cfg, c in synth.CONFIGS.items():
+        if c["reps"]:
+            continue
+        n = c.get("shard_n", c["n"])
+        assert c["L"] == pfg.derive_reps(n, c["d"], c["family"], c["budget"], strategy=c["strategy"])[0], cfg
