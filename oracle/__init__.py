@@ -228,7 +228,8 @@ def bruteforce(x, q, k: int):
 class _SOpts(C.Structure):
     _fields_ = [("rep_chunk", C.c_int32), ("stop_rule", C.c_int32), ("per_round", C.c_int32),
                 ("segment", C.c_int32), ("use_filter", C.c_int32), ("eps", C.c_float),
-                ("uniform_chunks", C.c_int32), ("sim_order", C.c_int32), ("tau_rule", C.c_int32)]
+                ("uniform_chunks", C.c_int32), ("sim_order", C.c_int32), ("tau_rule", C.c_int32),
+                ("rerank", C.c_int32)]
 
 
 class OracleIndex:
@@ -325,7 +326,7 @@ class OracleIndex:
     def search(self, queries, k: int, recall: float, rep_chunk: int = 1, stop_rule: int = 0,
                per_round: bool = False, segment: int = 12, use_filter: bool = True, eps: float = 0.0,
                threads: int = 1, trace_cap: int = 0, uniform_chunks: bool = False, sim_order: int = 0,
-               tau_rule: int = 0):
+               tau_rule: int = 0, rerank: bool = True):
         """returns ids[nq,k] int64, sims[nq,k] f32, trace[nq,8] int32
         (i_stop, j_stop, emitted, filtered, dups, evaluated, flags, 0)
         and, if trace_cap > 0, the evaluated ids in evaluation order [nq, trace_cap] (uint32)."""
@@ -336,7 +337,7 @@ class OracleIndex:
         trace = np.zeros((nq, 8), dtype=np.int32)
         tids = np.zeros((nq, max(trace_cap, 1)), dtype=np.uint32)
         o = _SOpts(rep_chunk, stop_rule, int(per_round), segment, int(use_filter), eps, int(uniform_chunks),
-                   int(sim_order), int(tau_rule))
+                   int(sim_order), int(tau_rule), int(rerank))
         lib().or_search(self._h, _p(q), nq, k, recall, C.byref(o), threads, _p(ids), _p(sims), _p(trace),
                         _p(tids) if trace_cap > 0 else None, trace_cap)
         if trace_cap > 0:

@@ -508,6 +508,7 @@ double or_P(const or_index* X, int i, float ip) {
 }
 
 /* Stop rule at depth i after j repetitions (1-based) with k-th similarity ip (clamped).
+ * rule 2 (independent functions): the two-level bound below, at depth i < K. 
  * rule 0 (R-9, default): the failure bound of Lemma 1's proof, (1 - P_i)^j <= delta
  *   (PAPER.md:220), evaluated as j*log1p(-P) <= log(delta).
  * rule 1: Alg. 1 line 8 literally, j >= ln(1/delta)/P_i.
@@ -539,6 +540,14 @@ int or_should_stop(const or_index* X, int i, int j, float ip, double delta, int 
         return F <= delta;
     }
     if (rule == 1) return (double)j * P >= log(1.0 / delta);
+    if (rule == 2 && i < X->K) {
+        /* two-level failure bound (the argument of Lemma 1's proof):
+         * a point at inner product >= ip_k is missed only if it collides with the query neither in
+         * the j repetitions searched at depth i nor, in the other L - j repetitions, at depth i + 1
+         * (all L were searched there before depth i): (1 - P_i)^j (1 - P_{i+1})^(L - j) <= delta */
+        double P1 = or_P(X, i + 1, ip);
+        return (double)j * log1p(-P) + (double)(X->L - j) * log1p(-P1) <= log(delta);
+    }
     return (double)j * log1p(-P) <= log(delta);
 }
 
@@ -607,6 +616,8 @@ typedef struct {
     int32_t uniform_chunks;  /* 0: the search's first chunk is a single repetition (R-17) */
     int32_t sim_order;       /* 0: R-2 lane-tree similarity (or_sim); 1: plain sequential order (or_sim_seq) */
     int32_t tau_rule;        /* 0: probabilistic, the (1 - delta)-quantile (R-26); 1: (1+eps) x expected Hamming distance (R-15) */
+    int32_t rerank;          /* storage 1 (16-bit rows): 1 = the returned top-k re-scored with or_sim on the fp32
+                                rows and re-sorted */
 } or_sopts;
 
 /* ----------------------------------------------------------------------------
@@ -737,6 +748,17 @@ static void or_search_one(or_index* X, const float* qraw, int k, double delta, c
         }
     }
     trace[5] = (int32_t)nE;
+    if (q16 && o->rerank) {
+        /* the fixed-point search's top-k, re-scored in fp32 (R-2 order) and re-sorted by
+         * (sim desc, id asc) -- insertion sort of nt <= k entries */
+        for (int t = 0; t < nt; ++t) ts[t] = or_sim(q, X->x + (int64_t)ti[t] * d, d);
+        for (int t = 1; t < nt; ++t) {
+            float sv = ts[t]; uint32_t iv = ti[t];
+            int u = t;
+            while (u > 0 && or_better(sv, iv, ts[u - 1], ti[u - 1])) { ts[u] = ts[u - 1]; ti[u] = ti[u - 1]; --u; }
+            ts[u] = sv; ti[u] = iv;
+        }
+    }
     for (int t = 0; t < k; ++t) {
         if (t < nt) { oid[t] = ti[t]; osim[t] = ts[t]; } else { oid[t] = -1; osim[t] = -INFINITY; }
     }

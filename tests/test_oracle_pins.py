@@ -182,7 +182,7 @@ def tiny_hp():
 
 def test_stop_rule_golden(tiny_hp):
     for row in _rows(golden("stop_rule.txt")):
-        if row[0] in ("pool", "tensor"):
+        if row[0] in ("pool", "tensor", "twolevel"):
             continue
         ip, i, delta, rule, js = float(row[0]), int(row[1]), float(row[2]), int(row[3]), int(row[4])
         assert not tiny_hp.should_stop(i, js - 1, ip, delta, rule), row
@@ -533,11 +533,11 @@ def test_int16_storage_recall_on_config1():
     c = synth.CONFIGS[1]
     data, q = synth.config_data(1)
     o = O.OracleIndex(data, O.HP, L=c["reps"], seed=1, storage="i16")
-    ids, sims, tr = o.search(q, c["k"], c["recall"], rep_chunk=8)
+    ids, sims, tr = o.search(q, c["k"], c["recall"], rep_chunk=8, rerank=False)
     bi, bs = O.bruteforce(o.data(), O.normalize(q), c["k"])
     hit = np.mean([len(set(ids[r]) & set(bi[r])) / c["k"] for r in range(len(q))])
     assert hit >= 0.87
-    # every returned similarity is the fixed-point inner product of that pair
+    # without the fp32 re-rank every returned similarity is the fixed-point inner product of that pair
     x16, q16 = o.data16(), O.fixed16(O.normalize(q).ravel()).reshape(q.shape)
     for r in range(0, len(q), 9):
         for t in range(c["k"]):
@@ -766,3 +766,41 @@ def test_search_results_do_not_hinge_on_the_summation_order():
         eb = np.sort(xn[b_ids[r]].astype(np.float64) @ qn[r].astype(np.float64))[::-1]
         assert np.all(np.abs(ea - eb) <= 1e-6), r
     assert exc <= 2, exc
+
+
+def test_two_level_stop_bound_golden_and_monotone():
+    # SURVEY 8(f)4 / PAPER.md:218-221: the two-level bound (stop_rule 2) against hand-derived j*, no
+    # later than the one-level bound, and never weaker after descending a level: stopping after all
+    # L repetitions at depth i + 1 implies stopping after the first repetition at depth i
+    data = synth.gaussian(300, 16, 9)
+    X = O.OracleIndex(data, O.HP, L=32, seed=3, M=2, lazy=True)
+    for row in [r for r in _rows(golden("stop_rule.txt")) if r[0] == "twolevel"]:
+        ip, i, delta, L, js = float(row[1]), int(row[2]), float(row[3]), int(row[4]), int(row[5])
+        assert X.L == L
+        if js > 1:
+            assert not X.should_stop(i, js - 1, ip, delta, 2), row
+        assert X.should_stop(i, js, ip, delta, 2), row
+    for ip in (0.3, 0.6, 0.8, 0.95):
+        for delta in (0.5, 0.1, 0.01):
+            for i in range(1, 24):
+                for j in (1, 5, 17, 32):
+                    if X.should_stop(i, j, ip, delta, 0):
+                        assert X.should_stop(i, j, ip, delta, 2), (ip, delta, i, j)
+                if X.should_stop(i + 1, 32, ip, delta, 2):
+                    assert X.should_stop(i, 1, ip, delta, 2), (ip, delta, i)
+
+
+def test_int16_rerank_scores_in_fp32():
+    # SURVEY 8(f)3 / PAPER.md:300-304: with 16-bit rows the returned top-k is re-scored with the fp32
+    # similarity (R-2 order) and re-sorted; the id set is the fixed-point search's
+    data, q = synth.config_data(1, n=4000, nq=30)
+    X = O.OracleIndex(data, O.HP, L=16, seed=2, storage="i16")
+    a_ids, a_s, _ = X.search(q, 10, 0.9, rep_chunk=8, rerank=False)
+    b_ids, b_s, _ = X.search(q, 10, 0.9, rep_chunk=8, rerank=True)
+    xn, qn = X.data(), O.normalize(q)
+    for r in range(len(q)):
+        assert set(a_ids[r].tolist()) == set(b_ids[r].tolist())
+        want = [O.sim(qn[r], xn[i]) for i in b_ids[r]]
+        assert np.array_equal(b_s[r], np.array(want, np.float32))
+        keys = [(-s, i) for s, i in zip(b_s[r].tolist(), b_ids[r].tolist())]
+        assert keys == sorted(keys)
