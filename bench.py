@@ -171,78 +171,103 @@ def profiled_ksims_traffic(cfg):
         return json.load(f)
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_index(cfg):
+    """the CPU oracle (test infrastructure) over a config's data, repetition tables built lazily;
+    L comes from the config record (the product's cost model is not loaded, R-11)"""
+    import oracle as O
+    c = synth.CONFIGS[cfg]
+    data, q = synth.config_data(cfg, n=c.get("shard_n"))
+    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
+    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
+    return O.OracleIndex(data, fam, L=c["reps"] or c["L"], seed=1, strategy=strat, lazy=True), q
+
+
+def oracle_recall(X, qs, ids, k):
+    import oracle as O
+    bi, _ = O.bruteforce(X.data(), O.normalize(qs), k)
+    return float(np.mean([len(set(a) & set(b)) / k for a, b in zip(ids.tolist(), bi.tolist())]))
+
+
 def run_reference(args):
-    """The CPU oracle as it stands (test infrastructure), timed on the host cores."""
+    """The CPU oracle as it stands (test infrastructure), timed on all host cores (OpenMP over the
+    queries), each step a bounded sample of the workload's queries."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import oracle as O
     c = synth.CONFIGS[args.config]
-    n, nq = c["n"], c["nq"]
-    data, q = synth.config_data(args.config)
-    import paper_1906_12211_b200 as pfg
-    L = c["reps"] or pfg.derive_reps(n, c["d"], c["family"], c["budget"],
-                                     strategy=c["strategy"])[0]
-    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
-    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
+    nq = c["nq"]
+    cores = os.cpu_count() or 1
     t0 = time.time()
-    X = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
+    X, q = oracle_index(args.config)
     sample = args.ref_sample
     qs = q[:sample]
-    X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk)   # builds the touched repetitions
+    X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk)   # builds the repetitions it touches
     setup = time.time() - t0
     times = []
     for s in range(args.warmup + args.steps):
         t = time.perf_counter()
-        ids, sims, tr = X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk)
+        ids, sims, tr = X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk, threads=cores)
         el = time.perf_counter() - t
         if s >= args.warmup:
             times.append(el)
     tot = sum(times)
     value = args.steps * sample / tot
-    bi, _ = O.bruteforce(X.data(), O.normalize(qs), c["k"])
-    rec = float(np.mean([len(set(a) & set(b)) / c["k"] for a, b in zip(ids.tolist(), bi.tolist())]))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"config{args.config}: {c['name']}" + WORKLOAD_NOTE.get(args.config, ""),
-                   "n": n, "d": c["d"], "nq": nq, "k": c["k"],
-                   "recall_target": args.recall, "family": c["family"], "reps": L, "rep_chunk": args.rep_chunk},
-        "recall": rec,
-        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle",
-                         "sample": f"first {sample} of {nq} queries per step, single thread, lazily built "
-                                   f"oracle index ({setup:.0f} s setup untimed)"},
+                   "n": c["n"], "d": c["d"], "nq": nq, "k": c["k"],
+                   "recall_target": args.recall, "family": c["family"], "reps": c["reps"] or c["L"],
+                   "rep_chunk": args.rep_chunk},
+        "recall": oracle_recall(X, qs, ids, c["k"]),
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": f"first {sample} of {nq} queries per step, OpenMP over the queries on {cores} "
+                                   f"host threads, lazily built oracle index ({setup:.0f} s setup untimed)"},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline_leg(cfg, recall, rep_chunk, sample):
-    import oracle as O
-    import paper_1906_12211_b200 as pfg
+def cpu_baseline_leg(cfg, recall, rep_chunk, sample1, sample_all):
+    """the oracle on the host cores: (i) one thread on the first `sample1` queries (the paper's
+    protocol), (ii) OpenMP over all cores on the first `sample_all` queries"""
     c = synth.CONFIGS[cfg]
-    if c["n"] * c["d"] > 400_000_000:
+    cores = os.cpu_count() or 1
+    if c.get("shard_n", c["n"]) * c["d"] > 400_000_000:
         # the oracle's index setup alone (2048 sketch projections per point) exceeds the bounded
         # budget of this leg; the reference arm (--impl reference) times it separately
-        return {"value": None, "unit": "queries/s", "cores": 1, "kind": "oracle",
+        return {"value": None, "unit": "queries/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                 "sample": f"not run: config {cfg}'s oracle setup ({c['n']} x {c['d']}) exceeds the bounded CPU budget"}
-    data, q = synth.config_data(cfg)
-    L = c["reps"] or pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
-    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
-    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
     t0 = time.time()
-    X = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
-    qs = q[:sample]
-    X.search(qs, c["k"], recall, rep_chunk=rep_chunk)
+    X, q = oracle_index(cfg)
+    qa = q[:sample_all]
+    X.search(qa, c["k"], recall, rep_chunk=rep_chunk)    # builds the repetitions the sample touches
     setup = time.time() - t0
     t = time.perf_counter()
-    X.search(qs, c["k"], recall, rep_chunk=rep_chunk)
-    el = time.perf_counter() - t
-    return {"value": sample / el, "unit": "queries/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {sample} of {c['nq']} queries, single thread (the paper's protocol, PAPER.md:362-363), "
-                      f"lazily built oracle index, {setup:.0f} s setup untimed"}
+    X.search(q[:sample1], c["k"], recall, rep_chunk=rep_chunk, threads=1)
+    one = sample1 / (time.perf_counter() - t)
+    t = time.perf_counter()
+    ids, _, _ = X.search(qa, c["k"], recall, rep_chunk=rep_chunk, threads=cores)
+    allc = sample_all / (time.perf_counter() - t)
+    return {"value": allc, "unit": "queries/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": f"first {sample_all} of {c['nq']} queries, OpenMP over the queries on {cores} host threads; "
+                      f"lazily built oracle index, {setup:.0f} s setup untimed",
+            "recall": oracle_recall(X, qa, ids, c["k"]),
+            "single_thread": {"value": one, "unit": "queries/s", "cores": 1,
+                              "sample": f"first {sample1} queries, one thread (the paper's protocol, PAPER.md:362-363)"}}
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -256,16 +281,22 @@ def main():
     ap.add_argument("--recall", type=float, default=0.9)
     ap.add_argument("--rep-chunk", type=int, default=16)
     ap.add_argument("--nq", type=int, default=0, help="override the query count")
-    ap.add_argument("--ref-sample", type=int, default=20)
-    ap.add_argument("--cpu-sample", type=int, default=200)
+    ap.add_argument("--ref-sample", type=int, default=500, help="queries per step of the reference arm")
+    ap.add_argument("--cpu-sample", type=int, default=1000, help="queries of the single-thread CPU leg (BASELINE.md: the first 1 000)")
+    ap.add_argument("--cpu-sample-all", type=int, default=2000, help="queries of the all-cores CPU leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--engine", type=int, default=0, help="0 = bulk rounds + fused kernel, 1 = fused kernel only")
+    ap.add_argument("--engine", type=int, default=0, help="0 = phase-split rounds + fused kernel, 1 = fused kernel only, 2 = chunk rounds + fused kernel")
     ap.add_argument("--uniform-chunks", action="store_true", help="first chunk R repetitions long (R-17 option)")
-    ap.add_argument("--parallel", default="auto", choices=["auto", "data", "queries"],
-                    help="N > 1: data-sharded (each GPU indexes n/N rows, every query on every GPU, all-gather "
-                         "+ merge) or query replicas (each GPU the whole index and a query batch of its own); auto = "
-                         "data for the scale-out config 5, replicas for configs whose index fits one GPU")
+    ap.add_argument("--rounds", type=int, default=0, help="bulk rounds before the fused kernel (0 = library default)")
+    ap.add_argument("--tau-rule", type=int, default=0, help="0 = quantile filter threshold (R-26), 1 = expected distance (R-15)")
+    ap.add_argument("--parallel", default="data", choices=["data", "queries"],
+                    help="N > 1: data-sharded (the default, SURVEY 8(e): each GPU indexes n/N rows -- 12.5M rows per GPU "
+                         "for config 5 -- every query on every GPU, distributed query hashing, NCCL all-gather + merge), "
+                         "or query replicas (each GPU the whole index and a query batch of its own; query-parallel "
+                         "throughput, no collective)")
+    ap.add_argument("--no-distributed-prep", action="store_true",
+                    help="data-sharded mode: every rank hashes every query (instead of 1/N and an all-gather)")
     ap.add_argument("--storage", default="f32", choices=["f32", "i16"],
                     help="rows for the inner products: fp32, or the paper's 16-bit fixed point (R-25)")
     args = ap.parse_args()
@@ -292,7 +323,7 @@ def main():
     d, k = c["d"], c["k"]
     # config 5 is weak-scaled (BASELINE: 12.5M rows per GPU); the others split their n rows
     weak = "shard_n" in c
-    mode = args.parallel if args.parallel != "auto" else ("data" if weak else "queries")
+    mode = args.parallel
     sharded = world > 1 and mode == "data"
     replicas = world > 1 and mode == "queries"
     n = c["shard_n"] * world if (weak and sharded) else c["n"] if not weak else c["shard_n"]
@@ -324,7 +355,10 @@ def main():
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    sopts = dict(rep_chunk=args.rep_chunk, timing=True, engine=args.engine, uniform_chunks=args.uniform_chunks)
+    sopts = dict(rep_chunk=args.rep_chunk, timing=True, engine=args.engine, uniform_chunks=args.uniform_chunks,
+                 rounds=args.rounds, tau_rule=args.tau_rule)
+    if sharded and not args.no_distributed_prep:
+        sopts["distributed_prep"] = True
 
     def barrier():
         if world > 1:
@@ -377,7 +411,7 @@ def main():
     # per-query counters (algorithmic bytes, stop depths) from one more, untimed search of the same
     # batch; the search is deterministic, so they are the counters of the timed steps
     ids, sims, stats = idx.search(q, k, args.recall, stats=True, **sopts)[:3]
-    rstats = idx.index.round_stats() if args.engine == 0 else None
+    rstats = idx.index.round_stats() if args.engine in (0, 2) else None
     # per-phase breakdown of the query kernels from untimed searches with events between phases
     for _ in range(3):
         idx.search(q, k, args.recall, **dict(sopts, timing=2))
@@ -411,7 +445,8 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            idx.index.search(qh.numpy(), k, args.recall, out=(ih.numpy(), sh.numpy()), stream=stream, **sopts)
+            idx.index.search(qh.numpy(), k, args.recall, out=(ih.numpy(), sh.numpy()), stream=stream,
+                             **{o: v for o, v in sopts.items() if o != "distributed_prep"})
             e1.record(stream)
             barrier()
             if s >= args.warmup:
@@ -432,29 +467,36 @@ def main():
         achieved = ab / kern_s / 1e9
         traffic, traffic_src = profiled_traffic(args.config) if args.storage == "f32" else (None, None)
         # the dominant kernel (k_sims, the bulk similarity gathers): algorithmic bytes per launch =
-        # rows it computed x (row bytes + 16 B of pool entry: id, query, key) / launches per search,
-        # over its average launch duration (CUDA events around every launch of the timed steps)
+        # the rows its timed launches computed (the blind rounds' launches, which timing = 3 brackets
+        # with CUDA events; rows computed inside the device-side loop are not counted) x the 4d bytes
+        # of a row (4d per evaluated row; the 16 B of pool entry per row are overhead),
+        # over the average duration of those launches
         ksims_roofline = None
         if rstats and ksims_launches:
             row_b = 2 * d if args.storage == "i16" else 4 * d
-            per_search = rstats["sims_rows"] * (row_b + 16)
-            per_launch = per_search * args.steps / ksims_launches
+            per_launch = rstats["sims_rows_blind"] * args.steps * row_b / ksims_launches
             launch_s = ksims_ms / ksims_launches / 1e3
+            frac = per_launch / launch_s / 1e9 / pk["hbm_gbs"]
             ks_tr = profiled_ksims_traffic(args.config) if args.storage == "f32" else None
             ksims_roofline = {"bound": "hbm", "kernel": "k_sims (bulk candidate-row gathers + dot products, "
                                                         "the largest share of the query phase)",
                               "achieved": per_launch / launch_s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                              "frac": per_launch / launch_s / 1e9 / pk["hbm_gbs"],
+                              "frac": frac,
                               "traffic": ks_tr["dram_bytes_per_launch"] if ks_tr else None,
                               "traffic_source": ks_tr["source"] if ks_tr else None,
-                              "alg_bytes_per_launch": per_launch, "launch_ms": launch_s * 1e3,
-                              "launches": ksims_launches, "share_of_query_phase":
-                                  ksims_ms / args.steps / statistics.mean(kern_ms),
+                              "alg_bytes_per_launch": per_launch, "alg_bytes_unit": f"{row_b} B per evaluated row",
+                              "launch_ms": launch_s * 1e3, "launches": ksims_launches,
+                              "share_of_query_phase": ksims_ms / args.steps / statistics.mean(kern_ms),
                               "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"}
+            if frac > 1.0:
+                # more algorithmic bytes than the DRAM can deliver: the accounting is wrong (or rows
+                # came from L2); flagged, never reported as a fraction of the roofline
+                print(f"bench: k_sims roofline fraction {frac:.3f} exceeds 1 (accounting error)", file=sys.stderr)
+                ksims_roofline["frac_invalid"] = True
         cpu = None
         if not args.no_cpu_baseline:
             try:
-                cpu = cpu_baseline_leg(args.config, args.recall, args.rep_chunk, args.cpu_sample)
+                cpu = cpu_baseline_leg(args.config, args.recall, args.rep_chunk, args.cpu_sample, args.cpu_sample_all)
             except Exception as e:  # pragma: no cover
                 cpu = {"value": None, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
         line = {
@@ -476,6 +518,8 @@ def main():
                        "n": n, "d": d, "nq": nq, "k": k, "recall_target": args.recall, "family": c["family"],
                        "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": info["reps"],
                        "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "storage": args.storage,
+                       "tau_rule": ["quantile (R-26)", "expected distance (R-15)"][args.tau_rule],
+                       "engine": args.engine, "rounds": args.rounds or 5,
                        "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": (f"data-sharded x{world}" if sharded else
                                        f"query replicas x{world} (every GPU builds the whole index and answers a batch "
@@ -484,6 +528,10 @@ def main():
             "recall": rec,
             "build_s": build_s,
             "roofline": ksims_roofline,
+            # the whole step (preparation included): all algorithmic bytes of the search over ms_per_step
+            "roofline_step": {"bound": "hbm", "achieved": ab / (tot_ms / args.steps / 1e3) / 1e9, "peak": pk["hbm_gbs"],
+                              "unit": "GB/s", "frac": ab / (tot_ms / args.steps / 1e3) / 1e9 / pk["hbm_gbs"],
+                              "alg_bytes_per_step": ab},
             "roofline_query_phase": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "query phase: bulk rounds (k_expand, k_scan, k_dedupe, k_sims, k_merge) "

@@ -89,7 +89,8 @@ typedef struct {
  * row (round to nearest, ties to even), rows padded to a multiple of 16 coordinates (32 bytes);
  * similarity = (float)(sum_t q_t v_t, exact in int32) * 2^-30.  Halves the bytes of every
  * candidate row; similarities differ from fp32 by at most ~2e-3 and are exact
- * (order-independent) integers before the final conversion. */
+ * (order-independent) integers before the final conversion.  The fp32 rows are kept too (and
+ * counted in the budget) for the fp32 re-rank of each query's top-k (pfg_search_opts.rerank). */
 enum { PFG_STORAGE_F32 = 0, PFG_STORAGE_I16 = 1 };
 
 /* Search options.  Zero-initialise + struct_size; zero field = default.  NULL = all defaults. */
@@ -100,24 +101,30 @@ typedef struct {
                                  repetition 0 (tau is set right after it) unless
                                  uniform_chunks = 1 */
     int32_t segment;          /* [12] B: entries are retrieved in segments of B */
-    int32_t stop_rule;        /* [0] 0 = failure bound (1-P_i)^j <= delta;
+    int32_t stop_rule;        /* [0] 0 = failure bound (1-P_i)^j <= delta; 2 = two-level bound
+                                 (1-P_i)^j (1-P_{i+1})^(L-j) <= delta below depth K (independent only; the
+                                 same argument);
                                  1 = Alg. 1 line 8, j >= ln(1/delta)/P_i (independent only) */
     int32_t stop_granularity; /* [0] 0 = check after every repetition (Alg. 1);
                                  1 = only after all L repetitions of a level */
     int32_t use_filter;       /* [1] 1 = sketch filter on; -1 = off */
-    float filter_eps;         /* [0] tau = (1+eps) x expected Hamming distance */
+    float filter_eps;         /* [0] tau_rule 1: tau = (1+eps) x expected Hamming distance */
     int32_t trace_cap;        /* [0] >0: write the ids evaluated by each query, in evaluation order,
                                  to trace_ids[nq][trace_cap] (uint32, local row ids) */
     int32_t timing;           /* [0] 1: record CUDA events around the phases of this call on `stream`
                                  (read back with pfg_last_timing); 2: also between the query-phase
                                  kernels (pfg_last_phases; the extra events cost a few microseconds each);
                                  3: events around each bulk-round k_sims launch only, accumulated over
-                                 searches (pfg_kernel_timing) */
+                                 searches (pfg_kernel_timing); 4: developer timeline, an event after
+                                 each launch group on its stream, printed to stderr when the call
+                                 completes (completion times relative to the call's first event) */
     uint32_t* trace_ids;      /* host or device pointer, required when trace_cap > 0 */
     int32_t engine;           /* [0] 0 = bulk rounds (one chunk of every active query per round, split
                                  into data-parallel phases), then the fused kernel resumes the queries
                                  still running; 1 = fused kernel only (one warp per query, persistent
-                                 grid).  Results are identical. */
+                                 grid); 2 = chunk rounds (one CTA per query fuses a round's control
+                                 phases, kernels_chunk.cuh; the phase-split engine when wide queries are
+                                 on), then the fused kernel.  Results are identical. */
     int32_t uniform_chunks;   /* [0] 1 = chunks of R repetitions from the start (tau = 64 for a whole
                                  first chunk); 0 = the first chunk is the single repetition 0 */
     int32_t rounds;           /* [5] engine 0: bulk rounds before the fused kernel resumes the rest
@@ -130,6 +137,29 @@ typedef struct {
                                  the loop keeps every query still running after the blind rounds;
                                  -1 = off (a query beyond the hash set continues in the fused kernel's
                                  global bitmap).  Results are identical in every mode. */
+    int32_t tau_rule;         /* [0] sketch-filter threshold tau at the k-th similarity ip_k (R-26,
+                                 R-15): 0 = the (1 - delta)-quantile of the sketch Hamming distance of a
+                                 pair at ip_k, i.e. the smallest t with P[Binomial(64, acos(ip_k)/pi) <= t]
+                                 >= 1 - delta, delta = 1 - recall target; 1 = (1 +
+                                 filter_eps) x the expected distance 64 acos(ip_k)/pi, rounded half up
+                                  */
+    int32_t rerank;           /* [0] PFG_STORAGE_I16: 0 = each query's top-k is re-scored with the fp32 rows
+                                 and re-sorted; -1 = returned as the fixed-point search ranked
+                                 them (fixed-point similarities) */
+    /* device-side round loop policy (engine 0 with wide queries; results are identical either way;
+       used by the tests to drive every path): */
+    int32_t loop_min;         /* [0 = 64] the loop keeps all queries still running after the blind rounds
+                                 when there are at least loop_min (and at most loop_max) of them */
+    int32_t loop_max;         /* [0 = automatic] > 0: that upper bound, and wide queries on when wide = 0 */
+    int32_t wide_arrays;      /* [0 = as many as 8 GiB holds] at most this many visit-tag arrays */
+    int32_t wide_tiles_min;   /* [0] 1 = the smallest wide-tile buffer (wide chunks compete and wait) */
+    /* precomputed query hashes (in the data-sharded mode each rank hashes a slice of the
+       queries with pfg_hash_queries_reps and the slices are all-gathered); DEVICE pointers or NULL: */
+    const uint32_t* ext_codes;     /* [nq][ext_reps] codes of repetitions [0, ext_reps): ext_reps = L, or
+                                      <= L for the FHT cross-polytope family with independent functions
+                                      (later repetitions are hashed in the kernels as usual) */
+    int32_t ext_reps;
+    const uint64_t* ext_sketches;  /* [nq][M] query sketches */
 } pfg_search_opts;
 
 /* per-query counters (optional output of pfg_search) */
@@ -226,10 +256,17 @@ pfg_status pfg_export(const pfg_index* idx, int32_t what, int32_t arg, void* dst
 pfg_status pfg_hash_queries(pfg_index* idx, const float* queries, int64_t nq, uint32_t* out_codes,
                             uint64_t* out_sketches, void* stream);
 
+/* codes of repetitions [0, nreps) (out_codes [nq][nreps] uint32) and sketches (out_sketches [nq][M]
+ * uint64, may be NULL) of nq queries, in the layout pfg_search takes as ext_codes / ext_sketches.
+ * Host or device pointers.  Errors: PFG_E_ARG (nreps not in [1, L]), PFG_E_ZERO_VECTOR. */
+pfg_status pfg_hash_queries_reps(pfg_index* idx, const float* queries, int64_t nq, int32_t nreps, uint32_t* out_codes,
+                                 uint64_t* out_sketches, void* stream);
+
 /* stop-rule and filter tables used by pfg_search for this recall target and options:
  * thr_host [K][L] fp32: level i = 1..K row i-1: the search stops after repetition j at level i
  * iff the k-th similarity (clamped to [-1,1]) >= thr[i-1][j-1] (+inf = never);
- * tau_host [65] fp32: tau(ip) = min{t : ip >= tau_host[t]}.  Either may be NULL. */
+ * tau_host [65] fp32: tau(ip) = min{t : ip >= tau_host[t]} under opts->tau_rule (and, for the
+ * quantile rule, this recall target).  Either may be NULL. */
 pfg_status pfg_stop_tables(pfg_index* idx, float recall_target, const pfg_search_opts* opts,
                            float* thr_host, float* tau_host);
 
@@ -254,8 +291,9 @@ pfg_status pfg_kernel_timing(pfg_index* idx, int32_t kernel, int32_t reset, doub
 
 /* Counters of the last search's round engine (waits for it): out[0] rows whose similarity the
  * bulk k_sims computed, out[1] blind rounds, out[2] device-side loop rounds, out[3] queries the
- * fused kernel took beside the loop, out[4] after it, out[5] visit-tag arrays used (wide queries).
- * n: entries to write (<= 6). */
+ * fused kernel took beside the loop, out[4] after it, out[5] visit-tag arrays used (wide queries),
+ * out[6] the rows of out[0] computed by the blind rounds' k_sims launches (those timed by
+ * timing = 3).  n: entries to write (<= 7). */
 pfg_status pfg_round_stats(pfg_index* idx, uint64_t* out, int32_t n);
 
 void pfg_free(pfg_index* idx);

@@ -33,7 +33,8 @@ STATUS = {0: "PFG_OK", 1: "PFG_E_ARG", 2: "PFG_E_ZERO_VECTOR", 3: "PFG_E_BUDGET"
 # symbols include/pfg.h declares (checked by tests/test_abi.py)
 EXPORTED = ["pfg_build", "pfg_search", "pfg_merge_topk", "pfg_index_info", "pfg_derive_reps", "pfg_export",
             "pfg_hash_queries", "pfg_stop_tables", "pfg_last_timing", "pfg_last_phases", "pfg_free", "pfg_last_error",
-            "pfg_abi_version", "pfg_save", "pfg_load", "pfg_kernel_timing", "pfg_round_stats"]
+            "pfg_abi_version", "pfg_save", "pfg_load", "pfg_kernel_timing", "pfg_round_stats",
+            "pfg_hash_queries_reps"]
 
 
 class PfgError(RuntimeError):
@@ -54,7 +55,10 @@ class SearchOpts(C.Structure):
                 ("stop_rule", C.c_int32), ("stop_granularity", C.c_int32), ("use_filter", C.c_int32),
                 ("filter_eps", C.c_float), ("trace_cap", C.c_int32), ("timing", C.c_int32),
                 ("trace_ids", C.c_void_p), ("engine", C.c_int32), ("uniform_chunks", C.c_int32),
-                ("rounds", C.c_int32), ("wide", C.c_int32)]
+                ("rounds", C.c_int32), ("wide", C.c_int32), ("tau_rule", C.c_int32), ("rerank", C.c_int32),
+                ("loop_min", C.c_int32), ("loop_max", C.c_int32), ("wide_arrays", C.c_int32),
+                ("wide_tiles_min", C.c_int32), ("ext_codes", C.c_void_p), ("ext_reps", C.c_int32),
+                ("ext_sketches", C.c_void_p)]
 
 
 class IndexInfo(C.Structure):
@@ -95,6 +99,8 @@ def lib() -> C.CDLL:
         L.pfg_export.argtypes = [P, C.c_int32, C.c_int32, P, C.c_uint64]
         L.pfg_hash_queries.restype = S
         L.pfg_hash_queries.argtypes = [P, P, C.c_int64, P, P, P]
+        L.pfg_hash_queries_reps.restype = S
+        L.pfg_hash_queries_reps.argtypes = [P, P, C.c_int64, C.c_int32, P, P, P]
         L.pfg_stop_tables.restype = S
         L.pfg_stop_tables.argtypes = [P, C.c_float, P, P, P]
         L.pfg_last_timing.restype = S
@@ -239,7 +245,8 @@ class Index:
     @staticmethod
     def _sopts(rep_chunk=DEFAULT_REP_CHUNK, segment=12, stop_rule=0, per_round=False, use_filter=True, eps=0.0,
                trace_cap=0, trace_ptr=None, timing=False, engine=0, uniform_chunks=False, rounds=0,
-               wide=0) -> SearchOpts:
+               wide=0, tau_rule=0, rerank=True, loop_min=0, loop_max=0, wide_arrays=0,
+               wide_tiles_min=False, ext_codes=None, ext_sketches=None) -> SearchOpts:
         o = SearchOpts()
         o.struct_size = C.sizeof(SearchOpts)
         o.rep_chunk, o.segment, o.stop_rule = rep_chunk, segment, stop_rule
@@ -253,6 +260,16 @@ class Index:
         o.uniform_chunks = int(uniform_chunks)
         o.rounds = int(rounds)
         o.wide = int(wide)
+        o.tau_rule = int(tau_rule)
+        o.rerank = 0 if rerank else -1
+        o.loop_min, o.loop_max, o.wide_arrays = int(loop_min), int(loop_max), int(wide_arrays)
+        o.wide_tiles_min = int(wide_tiles_min)
+        if ext_codes is not None:   # device tensors [nq, reps] uint32 (int32 view) / [nq, M] uint64 (int64 view)
+            assert _is_torch(ext_codes) and ext_codes.is_cuda and ext_codes.is_contiguous()
+            o.ext_codes, o.ext_reps = ext_codes.data_ptr(), int(ext_codes.shape[1])
+        if ext_sketches is not None:
+            assert _is_torch(ext_sketches) and ext_sketches.is_cuda and ext_sketches.is_contiguous()
+            o.ext_sketches = ext_sketches.data_ptr()
         return o
 
     def last_timing(self):
@@ -277,12 +294,12 @@ class Index:
         return float(ms.value), int(n.value)
 
     ROUND_STATS = ("sims_rows", "blind_rounds", "loop_rounds", "fused_beside_loop", "fused_after_loop",
-                   "wide_arrays")
+                   "wide_arrays", "sims_rows_blind")
 
     def round_stats(self) -> dict:
         """round-engine counters of the last search (pfg_round_stats)"""
-        out = (C.c_uint64 * 6)()
-        _check(lib().pfg_round_stats(self._h, out, 6))
+        out = (C.c_uint64 * 7)()
+        _check(lib().pfg_round_stats(self._h, out, 7))
         return {name: int(out[i]) for i, name in enumerate(self.ROUND_STATS)}
 
     def search(self, queries, k: int, recall: float, stats: bool = False, trace_cap: int = 0, out=None,
@@ -326,6 +343,20 @@ class Index:
         _check(lib().pfg_hash_queries(self._h, C.c_void_p(q.ctypes.data), nq, C.c_void_p(codes.ctypes.data),
                                       C.c_void_p(sk.ctypes.data), C.c_void_p(0)))
         return codes, sk[:, : self.info["sketch_words"]]
+
+    def hash_queries_reps(self, queries, nreps: int, stream=None):
+        """-> codes [nq, nreps] (int32 view of the uint32 codes), sketches [nq, M] (int64 view of the
+        uint64 words): CUDA tensors for CUDA queries (pfg_hash_queries_reps)"""
+        import torch
+        queries = _f32(queries)
+        assert _is_torch(queries) and queries.is_cuda
+        nq = queries.shape[0]
+        codes = torch.empty((nq, nreps), dtype=torch.int32, device=queries.device)
+        sk = torch.empty((nq, max(1, self.info["sketch_words"])), dtype=torch.int64, device=queries.device)
+        _check(lib().pfg_hash_queries_reps(self._h, C.c_void_p(queries.data_ptr()), nq, nreps,
+                                           C.c_void_p(codes.data_ptr()), C.c_void_p(sk.data_ptr()),
+                                           _stream(queries, stream)))
+        return codes, sk[:, : self.info["sketch_words"]].contiguous()
 
     def _export(self, what, arg, shape, dtype):
         a = np.empty(shape, dtype=dtype)

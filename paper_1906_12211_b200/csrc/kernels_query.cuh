@@ -69,6 +69,7 @@ struct RoundCtl {
     uint32_t pad2;
     unsigned long long evsum, emsum;  // evaluated ids and emitted positions of the finished queries
     unsigned long long sims_rows;     // pool rows the bulk k_sims launches computed
+    unsigned long long sims_rows_blind;  // of these, the rows of the launches outside the device-side loop
 };
 struct RoundState {
     int32_t* lvl;       // [nq] next level i to process (K..1); 0 = only the i = 0 scan remains
@@ -110,6 +111,7 @@ struct RoundState {
     uint32_t* wtcnt;    // [wcap] fresh | passing << 8 | repetition << 16 | kept << 24
     uint32_t* rtile;    // [nq][kMaxR + 1] first wide tile of each repetition of the chunk, then the end
     uint32_t wslots, wcap, hmax;  // hmax: evaluated ids a query keeps in the hash set before it widens
+    uint32_t pool_stride;         // chunk engine: the pool of round parity par starts at par * pool_stride
 };
 constexpr int kCnt = 8;
 
@@ -895,6 +897,51 @@ __global__ void __launch_bounds__(128, PFG_MINB) k_query(QueryParams p) {
             }
         }
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// with 16-bit rows (R-25) the search ranks candidates by fixed-point
+// inner products; this kernel re-scores each query's k_eff results with the fp32 rows in the R-2 order
+// (lane sums of 16-byte chunks, sequential fmaf, then the tree h = 16..1, as or_sim) and re-sorts them
+// by (sim desc, id asc).  One warp per query.
+__global__ void __launch_bounds__(128) k_rerank(const float* __restrict__ x, const float* __restrict__ qx, int dpad,
+                                                int64_t nq, int k, int k_eff, int kt, int64_t id_offset,
+                                                int64_t* __restrict__ ids, float* __restrict__ sims) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+    if (q >= nq) return;
+    uint64_t* keys = reinterpret_cast<uint64_t*>(sm + (size_t)wib * align16(kt * 8));
+    const int nch = dpad >> 2;
+    const float4* q4 = reinterpret_cast<const float4*>(qx + q * dpad);
+    int n = 0;   // results present (zero query rows and padding are -1)
+    for (int t = 0; t < k_eff; ++t) {
+        const int64_t gid = ids[q * k + t];
+        if (gid < 0) break;
+        const uint32_t id = (uint32_t)(gid - id_offset);
+        const float4* x4 = reinterpret_cast<const float4*>(x + (int64_t)id * dpad);
+        float acc = 0.0f;
+        for (int c = lane; c < nch; c += 32) {
+            const float4 v = __ldg(x4 + c), w = __ldg(q4 + c);
+            acc = fmaf(w.x, v.x, acc);
+            acc = fmaf(w.y, v.y, acc);
+            acc = fmaf(w.z, v.z, acc);
+            acc = fmaf(w.w, v.w, acc);
+        }
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) acc = acc + __shfl_xor_sync(kFull, acc, h);
+        if (lane == 0) keys[t] = make_key(acc, id);
+        n = t + 1;
+    }
+    __syncwarp();
+    // rank sort (keys are distinct: distinct ids)
+    for (int t = lane; t < n; t += 32) {
+        const uint64_t kv = keys[t];
+        int r = 0;
+        for (int u = 0; u < n; ++u) r += keys[u] > kv ? 1 : 0;
+        ids[q * k + r] = (int64_t)key_id(kv) + id_offset;
+        sims[q * k + r] = key_sim(kv);
     }
 }
 

@@ -132,25 +132,6 @@ __global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restric
     out[q * p.qb_ld + j] = make_uint4(lo1, lo2, probes, 0u);
 }
 
-// Processing order for the fused kernel (longest first, so the persistent grid's tail is short):
-// key = (~estimated cost) << 32 | q, the cost being the number of table entries the query's level-K
-// match ranges of the first qb_n repetitions hold (the entries it will scan there).
-__global__ void k_qorder_keys(QueryParams p, uint64_t* __restrict__ keys) {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= p.nq) return;
-    uint64_t cost = 0;
-    for (int j = 0; j < p.qb_n; ++j) {
-        const uint4 b = __ldg(p.qbnd + q * p.qb_ld + j);
-        cost += b.y - b.x;
-    }
-    const uint32_t c32 = cost > 0xffffffffull ? 0xffffffffu : (uint32_t)cost;
-    keys[q] = ((uint64_t)(~c32) << 32) | (uint64_t)q;
-}
-__global__ void k_qorder_list(const uint64_t* __restrict__ keys, int64_t nq, uint32_t* __restrict__ qlist) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < nq) qlist[t] = (uint32_t)keys[t];
-}
-
 // ---------------------------------------------------------------------------------------------
 __global__ void k_rinit(QueryParams p, uint32_t wtag) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -534,15 +515,8 @@ struct DedupeSmem {
 #define PFG_CPRE 8
 #endif
 constexpr int kCPre = PFG_CPRE;   // candidate ids loaded per lane per batch
-#ifndef PFG_DEDUPE_CPASYNC
-#define PFG_DEDUPE_CPASYNC 1
-#endif
-#ifndef PFG_DEDUPE_LATEWAIT
-#define PFG_DEDUPE_LATEWAIT 0
-#endif
-#ifndef PFG_DEDUPE_BULKSAVE
-#define PFG_DEDUPE_BULKSAVE 0
-#endif
+// the carried hash set is restored and saved in 16-byte pieces, 128 slots per warp step
+static_assert(kHC % 128 == 0, "k_dedupe moves the hash set in whole warp steps of 128 slots");
 
 template <typename PP>
 __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
@@ -559,10 +533,6 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
         if (fl & (kFlagFused | kFlagWide)) continue;
         const uint4 info = rs.rinfo[q];
         if (info.w) continue;  // direct chunk: k_scan wrote the evaluated ids and the pool
-        if (PFG_DEDUPE_BULKSAVE) {  // the previous query's bulk save has read the set
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncwarp();
-        }
         const int nr = (int)info.x;
         const uint32_t ntl = info.z;
         const uint32_t nE = rs.cnt[q * kCnt + 3];
@@ -590,20 +560,14 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                         while (atomicCAS(&c->hs[h], kEmpty, v[u]) != kEmpty) h = hs_next(h);
                     }
             }
-        } else if (PFG_DEDUPE_CPASYNC) {
+        } else {
             // global -> shared without the register round trip (LDGSTS, L2 only)
 #pragma unroll
             for (int k = 0; k < kHC / 128; ++k) {
                 const uint32_t sa = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4*>(c->hs) + k * 32 + lane);
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(hsv + k * 32 + lane) : "memory");
             }
-            if (!PFG_DEDUPE_LATEWAIT) asm volatile("cp.async.wait_all;" ::: "memory");
-        } else {
-            uint4 tmp[kHC / 128];
-#pragma unroll
-            for (int k = 0; k < kHC / 128; ++k) tmp[k] = __ldcg(hsv + k * 32 + lane);
-#pragma unroll
-            for (int k = 0; k < kHC / 128; ++k) reinterpret_cast<uint4*>(c->hs)[k * 32 + lane] = tmp[k];
+            asm volatile("cp.async.wait_all;" ::: "memory");
         }
         if (lane < nr) { c->fcnt[lane] = 0; c->dcnt[lane] = 0; }
         __syncwarp();
@@ -633,10 +597,6 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                 const uint32_t g = (t0 + b) * kTile + o;
                 v[u] = live ? cand[g] : kEmpty;
                 rr[u] = live ? trep[b] : -1;
-            }
-            if (PFG_DEDUPE_LATEWAIT) {  // the restored set lands while the batch loads
-                asm volatile("cp.async.wait_all;" ::: "memory");
-                __syncwarp();
             }
             // membership in the set as it stands before this batch: independent read-only probes
 #pragma unroll
@@ -682,9 +642,6 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
             }
             if (nE + ns > rs.hmax) overflow = true;
         }
-        if (PFG_DEDUPE_LATEWAIT) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-        }
         __syncwarp();
         uint32_t base = 0;
         if (!overflow && lane == 0) base = atomicAdd(&rs.ctl->pool_top[par], ns);
@@ -724,25 +681,11 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
         const int nominal = min((ci == p.K && cc0 == 0 && !p.uniform) ? 1 : p.R, p.L - cc0);
         if (nE + ns > (uint32_t)kSaveMin && nr >= nominal) {
             if (lane == 0 && !saved) rs.flags[q] |= kFlagSaved;
-            if (PFG_DEDUPE_BULKSAVE) {
-                // one bulk copy (TMA engine) shared -> global, issued by lane 0 after every lane's
-                // writes are made visible to the async proxy
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(c->hs);
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(hsv), "r"(sa),
-                                 "r"((uint32_t)(kHC * 4)) : "memory");
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
-            } else {
 #pragma unroll
-                for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
-            }
+            for (int k = 0; k < kHC / 128; ++k) __stcg(hsv + k * 32 + lane, reinterpret_cast<const uint4*>(c->hs)[k * 32 + lane]);
         }
         __syncwarp();
     }
-    if (PFG_DEDUPE_BULKSAVE && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -801,8 +744,13 @@ __device__ __forceinline__ float sims_step(const QueryParams& p, uint32_t myid, 
 #ifndef PFG_I16_NR
 #define PFG_I16_NR 16
 #endif
+// flags bit 0 (the chunk engine, kernels_chunk.cuh): the pool of parity par starts at
+// par * pool_stride, and the kernel resets the counters the next round's k_chunk starts from (its
+// active list's successor, its pool, its work counter), none of which this launch reads;
+// bit 1: a launch outside the device-side loop (its rows are also counted in sims_rows_blind)
 template <typename PP, bool I16>
-__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
+__global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par, int flags) {
+    const int chunk = flags & 1;
     const QueryParams& p = deref(pp);
     constexpr int NR = I16 ? PFG_I16_NR : kRPI;   // int16 rows are half as long: more rows in flight
     constexpr int kSh = NR == 32 ? 0 : NR == 16 ? 1 : NR == 8 ? 2 : 3;
@@ -810,15 +758,23 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
     const RoundState& rs = p.rs;
     const uint32_t top = min(rs.ctl->pool_top[par], rs.pool_cap);
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&rs.ctl->sims_rows, (unsigned long long)top);
+    const size_t po = chunk ? (size_t)par * rs.pool_stride : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicAdd(&rs.ctl->sims_rows, (unsigned long long)top);
+        if (flags & 2) atomicAdd(&rs.ctl->sims_rows_blind, (unsigned long long)top);
+        if (chunk) { rs.ctl->nact[par] = 0; rs.ctl->pool_top[par ^ 1] = 0; rs.ctl->wk[par ^ 1][0] = 0; }
+    }
+    const uint32_t* pool_id = rs.pool_id + po;
+    const uint32_t* pool_q = rs.pool_q + po;
+    uint64_t* pool_key = rs.pool_key + po;
     // lane r < NR holds entry b + r of the current step (rows beyond the end repeat the last);
     // the next step's entries are fetched before the current rows are read
     auto fetch = [&](int64_t b, uint32_t& id, uint32_t& qq) {
         if (lane < NR && b < top) {
             const int64_t e1 = (int64_t)top < b + NR ? (int64_t)top : b + NR;
             const int64_t e = b + lane < e1 ? b + lane : e1 - 1;
-            id = rs.pool_id[e];
-            qq = rs.pool_q[e];
+            id = pool_id[e];
+            qq = pool_q[e];
         }
     };
     int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NR;
@@ -832,7 +788,7 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par) {
         const float t1 = oneq ? sims_step<NR, I16, true>(p, myid, myq, lane) : sims_step<NR, I16, false>(p, myid, myq, lane);
         const int rr = lane >> kSh;
         const uint32_t id_rr = __shfl_sync(kFull, myid, rr);
-        if ((lane & ((1 << kSh) - 1)) == 0 && b + rr < e1) rs.pool_key[b + rr] = make_key(t1, id_rr);
+        if ((lane & ((1 << kSh) - 1)) == 0 && b + rr < e1) pool_key[b + rr] = make_key(t1, id_rr);
     }
 }
 

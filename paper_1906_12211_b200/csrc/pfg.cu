@@ -25,6 +25,7 @@
 #include "kernels_build.cuh"
 #include "kernels_query.cuh"
 #include "kernels_rounds.cuh"
+#include "kernels_chunk.cuh"
 #include "rng.h"
 
 namespace pfg {
@@ -156,10 +157,7 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     if (family == PFG_CROSSPOLYTOPE && d > 256) return fail(PFG_E_ARG, "exact cross-polytope family supports d <= 256");
     g.n = n;
     g.d = d;
-    {
-        const int al = getenv("PFG_DPAD_ALIGN") ? std::max(8, atoi(getenv("PFG_DPAD_ALIGN"))) : 8;
-        g.dpad = (d + al - 1) / al * al;  // rows 32-byte aligned (PFG_DPAD_ALIGN: developer experiments)
-    }
+    g.dpad = (d + 7) / 8 * 8;  // rows 32-byte aligned
     if ((uint64_t)n * (uint64_t)g.dpad / 4 >= (1ull << 32))
         return fail(PFG_E_ARG, "n * d too large for one index (shard the data: n * d / 4 must be < 2^32)");
     g.family = family;
@@ -198,7 +196,8 @@ pfg_status resolve_opts(const pfg_build_opts* o, int64_t n, int d, int family, G
     // per repetition: sorted table + 13-bit prefix table + slot + its own functions / selection
     const uint64_t N = (uint64_t)n;
     const uint64_t fn_hp = 4ull * g.dpad, fn_fht = family == PFG_CROSSPOLYTOPE ? 4ull * g.d * g.dpad : 3ull * g.W * 4;
-    const uint64_t data_bytes = g.storage == PFG_STORAGE_I16 ? 2ull * N * g.dpad16 : 4ull * N * g.dpad;
+    // PFG_STORAGE_I16 keeps the fp32 rows too (hashing at build, the fp32 re-rank of each query's top-k)
+    const uint64_t data_bytes = g.storage == PFG_STORAGE_I16 ? 2ull * N * g.dpad16 + 4ull * N * g.dpad : 4ull * N * g.dpad;
     g.fixed_bytes = data_bytes + 4ull * 64 * g.M * g.dpad + 8ull * (g.ell + 1) * 41;
     if (g.strategy == PFG_POOL) g.fixed_bytes += (uint64_t)g.m * (family == PFG_SIMHASH ? fn_hp : fn_fht);
     g.per_rep_bytes = 16ull * N + 4ull * 8193 + 1;  // 16-byte entries: key + inline sketch word (R-21)
@@ -249,6 +248,7 @@ int grid_bucket(float ip) {
 struct StopModel {
     int family, strategy, ell, m;
     const double* T;  // CP table [(ell+1)][41] (FHT family)
+    int K, L;
     double P(int i, float ip) const {
         if (family == PFG_SIMHASH) {
             const double p = 1.0 - std::acos((double)ip) / M_PI;
@@ -281,6 +281,12 @@ struct StopModel {
             return F <= delta;
         }
         if (rule == 1) return (double)j * Pi >= std::log(1.0 / delta);
+        if (rule == 2 && i < K) {
+            // two-level bound: the L - j repetitions not yet searched
+            // at depth i were searched at depth i + 1: (1 - P_i)^j (1 - P_{i+1})^(L - j) <= delta
+            const double P1 = P(i + 1, ip);
+            return (double)j * std::log1p(-Pi) + (double)(L - j) * std::log1p(-P1) <= std::log(delta);
+        }
         return (double)j * std::log1p(-Pi) <= std::log(delta);
     }
 };
@@ -319,9 +325,39 @@ int tau_of(float ipk, float eps) {
     return (int)r;
 }
 
+// R-26: tau = the smallest t with P[H > t] <= delta for H ~ Binomial(64, acos(ip)/pi),
+// the (1 - delta)-quantile of the sketch Hamming distance of a pair at the k-th similarity; the upper
+// tail summed in double from t = 64 down (smallest terms first)
+double binom64(double p, int t) {
+    double c = 1.0;
+    for (int h = 0; h < t; ++h) c = c * (double)(64 - h) / (double)(h + 1);
+    return c * std::pow(p, (double)t) * std::pow(1.0 - p, (double)(64 - t));
+}
+int tau_quantile(float ipk, double delta) {
+    double p = std::acos((double)ipk) / M_PI;
+    if (p < 0.0) p = 0.0;
+    if (p > 1.0) p = 1.0;
+    double tail = 0.0;
+    int t = 64;
+    while (t > 0 && tail + binom64(p, t) <= delta) { tail += binom64(p, t); --t; }
+    return t;
+}
+
+// query codes of repetitions [0, reps) and sketches computed elsewhere (device pointers; SURVEY 8(e):
+// each rank of the data-sharded mode hashes a slice of the queries, the slices are all-gathered)
+struct ExtHash {
+    const uint32_t* codes = nullptr;  // [nq][reps]
+    int reps = 0;
+    const uint64_t* sk = nullptr;     // [nq][M]
+};
+
 struct SearchCfg {
     int R = 8, B = 12, rule = 0, per_round = 0, use_filter = 1, trace_cap = 0, timing = 0, engine = 0, uniform = 0, rounds = 0;
     int wide = 0;
+    int tau_rule = 0;   // 0: binomial quantile (R-26), 1: (1 + eps) x expected distance (R-15)
+    int rerank = 1;     // PFG_STORAGE_I16: re-score each query's top-k in fp32
+    int loop_min = 0, loop_max = 0, wide_arrays = 0, wide_tiles_min = 0;  // device-side loop policy (tests)
+    ExtHash ext;        // precomputed query codes / sketches (SURVEY 8(e) distributed preparation)
     float eps = 0.0f;
     uint32_t* trace_ids = nullptr;
 };
@@ -339,7 +375,7 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     s.B = z.segment ? z.segment : 12;
     if (s.B < 1) return fail(PFG_E_ARG, "segment must be >= 1");
     s.rule = z.stop_rule;
-    if (s.rule != 0 && s.rule != 1) return fail(PFG_E_ARG, "stop_rule must be 0 or 1");
+    if (s.rule < 0 || s.rule > 2) return fail(PFG_E_ARG, "stop_rule must be 0, 1 or 2");
     s.per_round = z.stop_granularity;
     if (s.per_round != 0 && s.per_round != 1) return fail(PFG_E_ARG, "stop_granularity must be 0 or 1");
     s.use_filter = z.use_filter < 0 ? 0 : 1;
@@ -349,11 +385,24 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     s.trace_ids = z.trace_ids;
     s.timing = z.timing;
     s.engine = z.engine;
-    if (s.engine < 0 || s.engine > 1) return fail(PFG_E_ARG, "engine must be 0 (rounds + fused) or 1 (fused)");
+    if (s.engine < 0 || s.engine > 2)
+        return fail(PFG_E_ARG, "engine must be 0 (phase-split rounds + fused), 1 (fused) or 2 (chunk rounds + fused)");
     s.rounds = z.rounds;
     if (s.rounds < 0 || s.rounds > 4096) return fail(PFG_E_ARG, "rounds must be in [0, 4096]");
     s.wide = z.wide;
     if (s.wide < -1 || s.wide > kHMax) return fail(PFG_E_ARG, "wide must be -1, 0 or in [1, 1536]");
+    s.rerank = z.rerank < 0 ? 0 : 1;
+    s.loop_min = z.loop_min;
+    s.loop_max = z.loop_max;
+    s.wide_arrays = z.wide_arrays;
+    s.wide_tiles_min = z.wide_tiles_min;
+    s.ext.codes = z.ext_codes;
+    s.ext.reps = z.ext_reps;
+    s.ext.sk = z.ext_sketches;
+    if (s.ext.codes && s.ext.reps < 1) return fail(PFG_E_ARG, "ext_codes needs ext_reps >= 1");
+    if (s.loop_min < 0 || s.loop_max < 0 || s.wide_arrays < 0) return fail(PFG_E_ARG, "loop_min, loop_max, wide_arrays must be >= 0");
+    s.tau_rule = z.tau_rule;
+    if (s.tau_rule != 0 && s.tau_rule != 1) return fail(PFG_E_ARG, "tau_rule must be 0 (quantile) or 1 (expected distance)");
     s.uniform = z.uniform_chunks;
     if (s.uniform != 0 && s.uniform != 1) return fail(PFG_E_ARG, "uniform_chunks must be 0 or 1");
     if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
@@ -372,15 +421,14 @@ struct pfg_index {
     uint64_t seed = 0;
     std::mutex mu;
     // index arrays (device)
-    DBuf x, tab, pt, slot, hpfn, sg, sel, skfn, x16;   // x16: int16 rows (PFG_STORAGE_I16; x is then freed)
+    DBuf x, tab, pt, slot, hpfn, sg, sel, skfn, x16;   // x16: int16 rows (PFG_STORAGE_I16, beside the fp32 rows)
     std::vector<double> cpT;
     std::vector<int32_t> slot_h, sel_h;
     // cached stop tables: key (recall bits, rule, per_round) -> device thr [K][L]; eps -> taub
     std::map<std::tuple<uint32_t, int, int>, std::shared_ptr<DBuf>> thr_cache;
-    std::map<uint32_t, std::shared_ptr<DBuf>> tau_cache;
+    std::map<std::tuple<int, uint32_t, uint32_t>, std::shared_ptr<DBuf>> tau_cache;  // (rule, eps, recall)
     // per-call scratch (grow-only)
     DBuf qraw, qx, qzero, zmin, qsk, qcodes, qbits, qfc, qfc2, outb_ids, outb_sims, outb_stats, outb_trace, work, qx16;
-    DBuf qord_keys, qord_sorted, qord_list, qord_temp;  // longest-first processing order (fused engine)
     DBuf cur, bitmap, claims;
     // round-engine state (per query, grow-only)
     DBuf rs_lvl, rs_c0, rs_flags, rs_tn, rs_cnt, rs_T, rs_E, rs_pend, rs_repcnt, rs_pool_id, rs_pool_q, rs_pool_key,
@@ -436,6 +484,12 @@ struct pfg_index {
     float last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // timing = 3: event pairs around each bulk k_sims launch, accumulated across searches
     std::vector<cudaEvent_t> kev;
+    // timing = 4 (developer timeline): an event after each launch group on its stream, printed to
+    // stderr as completion times relative to the search's first event
+    std::vector<cudaEvent_t> tlev;
+    std::vector<std::string> tlname;
+    int tl_n = 0;
+    bool tl_on = false;
     int64_t kev_n = 0;          // pairs recorded and not yet summed
     double kev_ms = 0.0;        // summed durations since the last reset
     int64_t kev_launches = 0;
@@ -446,6 +500,8 @@ struct pfg_index {
         for (auto& e : pev)
             if (e) cudaEventDestroy(e);
         for (auto& e : kev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : tlev)
             if (e) cudaEventDestroy(e);
         if (h_ctl) cudaFreeHost(h_ctl);
         if (h_ctl2) cudaFreeHost(h_ctl2);
@@ -470,6 +526,7 @@ namespace pfg {
 namespace {
 
 constexpr int kClaimCap = 8192;
+void tl_mark(pfg_index* I, const char* name, cudaStream_t st);
 constexpr int kQBMax = 96;     // level-K match ranges precomputed for at most this many repetitions
 constexpr int kExtReps = 32;   // repetitions hashed in bulk for the queries the fused kernel resumes
 pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
@@ -527,7 +584,7 @@ void hp_bits(const float* X, int64_t np, int ldx, const float* A, int nf, int ld
     dim3 grid((unsigned)((np + GB_M - 1) / GB_M), (nf + GB_N - 1) / GB_N);
     // the double-buffered kernel needs kdim, ldx, lda multiples of 8 and 16-byte aligned rows
     const bool v2 = (kdim % GB2_K) == 0 && (ldx % 4) == 0 && (lda % 4) == 0 && ((uintptr_t)X % 16) == 0 &&
-                    ((uintptr_t)A % 16) == 0 && !getenv("PFG_HP_V1");
+                    ((uintptr_t)A % 16) == 0;
     if (v2) k_hp_bits2<<<grid, 256, 0, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
     else k_hp_bits<<<grid, 256, 0, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
 }
@@ -892,7 +949,7 @@ pfg_status get_thr(pfg_index* I, float recall, const SearchCfg& s, std::shared_p
     }
     const Geo& g = I->g;
     const double delta = 1.0 - (double)recall;
-    StopModel sm{g.family, g.strategy, g.ell, g.m, I->cpT.empty() ? nullptr : I->cpT.data()};
+    StopModel sm{g.family, g.strategy, g.ell, g.m, I->cpT.empty() ? nullptr : I->cpT.data(), g.K, g.L};
     std::vector<float> thr((size_t)g.K * g.L);
     auto work = [&](int i0, int i1) {
         for (int i = i0; i < i1; ++i)
@@ -921,30 +978,48 @@ pfg_status get_thr(pfg_index* I, float recall, const SearchCfg& s, std::shared_p
     return PFG_OK;
 }
 
-pfg_status get_tau(pfg_index* I, float eps, std::shared_ptr<DBuf>& out, std::vector<float>* host) {
-    uint32_t eb;
+pfg_status get_tau(pfg_index* I, int rule, float eps, float recall, std::shared_ptr<DBuf>& out, std::vector<float>* host) {
+    uint32_t eb, rb;
     std::memcpy(&eb, &eps, 4);
-    auto it = I->tau_cache.find(eb);
+    std::memcpy(&rb, &recall, 4);
+    const auto key = rule ? std::make_tuple(rule, eb, 0u) : std::make_tuple(rule, 0u, rb);
+    auto it = I->tau_cache.find(key);
     if (it != I->tau_cache.end() && !host) {
         out = it->second;
         return PFG_OK;
     }
+    const double delta = 1.0 - (double)recall;
     std::vector<float> tb(65);
-    for (int t = 0; t < 65; ++t) tb[t] = smallest_true([&](float ip) { return tau_of(ip, eps) <= t; });
+    for (int t = 0; t < 65; ++t)
+        tb[t] = smallest_true([&](float ip) { return (rule ? tau_of(ip, eps) : tau_quantile(ip, delta)) <= t; });
     tb[64] = -1.0f;
     if (host) *host = tb;
     auto buf = std::make_shared<DBuf>();
     PFG_TRY(buf->alloc(65 * 4, "tau breakpoints"));
     PFG_CUDA(cudaMemcpy(buf->p, tb.data(), 65 * 4, cudaMemcpyHostToDevice));
-    I->tau_cache[eb] = buf;
+    I->tau_cache[key] = buf;
     out = buf;
+    return PFG_OK;
+}
+
+// the side streams and the events that order them against the search stream, created together
+// (every later use may assume all of them exist, whatever the index's sketch or family settings)
+pfg_status ensure_streams(pfg_index* I) {
+    if (I->aux) return PFG_OK;
+    PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
+    PFG_CUDA(cudaStreamCreateWithFlags(&I->aux2, cudaStreamNonBlocking));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_late, cudaEventDisableTiming));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_mid, cudaEventDisableTiming));
     return PFG_OK;
 }
 
 // normalise + sketch + (eager) code queries into index scratch; returns first zero row or -1
 pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool need_codes, bool force_codes, int64_t* zrow,
-                        bool* lazy, cudaStream_t st, int split, int cp_eager = 0) {
+                        bool* lazy, cudaStream_t st, int split, int cp_eager = 0, const ExtHash* ext = nullptr) {
     const Geo& g = I->g;
+    PFG_TRY(ensure_streams(I));
     const float* qsrc = queries;
     if (!is_device_ptr(queries)) {
         PFG_TRY(I->qraw.ensure((size_t)nq * g.d * 4, "query copy"));
@@ -956,6 +1031,7 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     PFG_TRY(I->zmin.ensure(8, "zmin"));
     PFG_TRY(normalize_rows(qsrc, nq, g.d, I->qx.as<float>(), g.dpad, I->qzero.as<uint8_t>(),
                            I->zmin.as<unsigned long long>(), zrow, st));
+    tl_mark(I, "normalize", st);
     if (g.storage == PFG_STORAGE_I16) {
         // R-25: the queries' fixed-point rows for the inner products
         PFG_TRY(I->qx16.ensure((size_t)nq * g.dpad16 * 2, "int16 queries"));
@@ -972,30 +1048,39 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         PFG_CUDA(cudaEventRecord(I->ev_zmin, st));
     }
     I->launches += 1;
+    // the normalised (and quantised) queries are ready: the side streams start from here
+    PFG_CUDA(cudaEventRecord(I->ev_fork, st));
     if (g.M > 0) {
         // sketches (FMA pipe) on the second stream, concurrently with the hashing below; the
         // caller joins (join_sketches) before anything reads them
         PFG_TRY(I->qsk.ensure((size_t)nq * g.M * 8, "query sketches"));
-        if (!I->aux) {
-            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
-            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux2, cudaStreamNonBlocking));
-            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
-            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
-            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_late, cudaEventDisableTiming));
-            PFG_CUDA(cudaEventCreateWithFlags(&I->ev_mid, cudaEventDisableTiming));
+        if (ext && ext->sk) {
+            PFG_CUDA(cudaMemcpyAsync(I->qsk.p, ext->sk, (size_t)nq * g.M * 8, cudaMemcpyDeviceToDevice, st));
+            PFG_CUDA(cudaEventRecord(I->ev_join, st));
+        } else {
+            PFG_CUDA(cudaStreamWaitEvent(I->aux, I->ev_fork, 0));
+            hp_bits(I->qx.as<float>(), nq, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->qsk.as<uint8_t>(),
+                    (int64_t)g.M * 8, I->aux);
+            PFG_CUDA(cudaGetLastError());
+            tl_mark(I, "query sketches (k_hp_bits2)", I->aux);
+            PFG_CUDA(cudaEventRecord(I->ev_join, I->aux));
+            I->launches += 1;
         }
-        PFG_CUDA(cudaEventRecord(I->ev_fork, st));
-        PFG_CUDA(cudaStreamWaitEvent(I->aux, I->ev_fork, 0));
-        hp_bits(I->qx.as<float>(), nq, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->qsk.as<uint8_t>(),
-                (int64_t)g.M * 8, I->aux);
-        PFG_CUDA(cudaGetLastError());
-        PFG_CUDA(cudaEventRecord(I->ev_join, I->aux));
-        I->launches += 1;
     }
     *lazy = (g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT && !force_codes);
     I->qc_n = 0;
     I->qc_ld = g.L;
-    if (need_codes && !*lazy && cp_eager > 0) {
+    if (need_codes && ext && ext->codes) {
+        // precomputed codes of repetitions [0, reps) (all L unless the family hashes lazily); rows
+        // laid out with room for kExtReps more for the queries the fused kernel resumes
+        const int ld = *lazy ? std::min(g.L, ext->reps + kExtReps) : g.L;
+        PFG_TRY(I->qcodes.ensure((size_t)nq * ld * 4, "query codes"));
+        PFG_CUDA(cudaMemcpy2DAsync(I->qcodes.p, (size_t)ld * 4, ext->codes, (size_t)ext->reps * 4, (size_t)ext->reps * 4,
+                                   (size_t)nq, cudaMemcpyDeviceToDevice, st));
+        I->qc_n = ext->reps;
+        I->qc_ld = ld;
+        I->qc_split = ext->reps;
+    } else if (need_codes && !*lazy && cp_eager > 0) {
         // exact CP, independent: the repetitions the blind rounds can reach only (cp_eager); the
         // queries still running after them get the rest in bulk (the caller)
         PFG_TRY(I->qcodes.ensure((size_t)nq * g.L * 4, "query codes"));
@@ -1019,7 +1104,7 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         // per (query, repetition); the query kernel hashes later repetitions lazily, if reached
         // (rows are laid out with room for kExtReps more, hashed later for the queries that reach
         // them: extend_codes)
-        const int ne = std::min(g.L, getenv("PFG_EAGER") ? atoi(getenv("PFG_EAGER")) : I->eager);
+        const int ne = std::min(g.L, I->eager);
         const int ld = std::min(g.L, ne + kExtReps);
         PFG_TRY(I->qcodes.ensure((size_t)nq * ld * 4, "query codes"));
         // repetitions [0, split) now; [split, ne) on the third stream, joined before the round
@@ -1029,7 +1114,7 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         // records ev_mid after its ranges, round 1 joins it) and [split, ne) after it (ev_late,
         // round 2 joins it)
         const int s0 = (split > 0 && split < ne && I->aux2) ? split : ne;
-        const bool mid = s0 < ne && s0 > 1 && !getenv("PFG_NO_MID");
+        const bool mid = s0 < ne && s0 > 1;
         PFG_TRY(fht_codes(I, nq, nullptr, 0, mid ? 1 : s0, ld, st));
         if (s0 < ne) {
             PFG_CUDA(cudaStreamWaitEvent(I->aux2, I->ev_fork, 0));
@@ -1067,6 +1152,7 @@ pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0,
              X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
     PFG_CUDA(cudaGetLastError());
     I->launches += 1;
+    tl_mark(I, (std::string("fht codes reps ") + std::to_string(r0) + "+" + std::to_string(nreps)).c_str(), st);
     return PFG_OK;
 }
 
@@ -1088,10 +1174,12 @@ void tune_eager(pfg_index* I) {
     if (tot) I->qb_depth = e >= kJHist - 1 ? (1 << 30) : std::max(8, e);
 }
 
-// developer aid PFG_DBG_SYNC=1: synchronise after each launch group and name the failing one
+// developer aid (a -DPFG_DEBUG_SYNC=1 build): synchronise after each launch group and name the failing one
+#ifndef PFG_DEBUG_SYNC
+#define PFG_DEBUG_SYNC 0
+#endif
 pfg_status dbg_sync(const char* what) {
-    static const bool on = getenv("PFG_DBG_SYNC") != nullptr;
-    if (!on) return PFG_OK;
+    if (!PFG_DEBUG_SYNC) return PFG_OK;
     const cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return fail(PFG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     return PFG_OK;
@@ -1135,6 +1223,31 @@ pfg_status phase_collect(pfg_index* I) {
     }
     I->pev_n = 0;
     return PFG_OK;
+}
+
+// timing = 4: timeline mark (completion of everything enqueued on `st` so far)
+void tl_mark(pfg_index* I, const char* name, cudaStream_t st) {
+    if (!I->tl_on) return;
+    if (I->tl_n == (int)I->tlev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return; }
+        I->tlev.push_back(e);
+        I->tlname.emplace_back();
+    }
+    const char* sn = st == I->aux ? "aux" : st == I->aux2 ? "aux2" : "main";
+    I->tlname[I->tl_n] = std::string(sn) + " " + name;
+    cudaEventRecord(I->tlev[I->tl_n++], st);
+}
+void tl_print(pfg_index* I) {
+    if (!I->tl_on || I->tl_n == 0) return;
+    cudaEventSynchronize(I->tlev[I->tl_n - 1]);
+    cudaDeviceSynchronize();
+    for (int i = 0; i < I->tl_n; ++i) {
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, I->tlev[0], I->tlev[i]);
+        fprintf(stderr, "[pfg timeline] %8.1f us  %s\n", 1e3 * ms, I->tlname[i].c_str());
+    }
+    I->tl_n = 0;
 }
 
 // the query sketches of prep_queries are ready on `st` after this
@@ -1313,15 +1426,14 @@ pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t budget, i
     if (g.family == PFG_CROSSPOLYTOPE_FHT) PFG_TRY(build_cp_table(I.get(), st));
     if (g.family == PFG_CROSSPOLYTOPE) build_cp_exact_table(I.get());
     if (g.storage == PFG_STORAGE_I16) {
-        // R-25: the inner products read 16-bit fixed-point rows; the fp32 rows were only needed
-        // for hashing and sketches
+        // R-25: the search's inner products read 16-bit fixed-point rows; the fp32 rows stay for
+        // the fp32 re-rank of each query's top-k
         PFG_TRY(I->x16.alloc((size_t)n * g.dpad16 * 2, "int16 data"));
         const int64_t tot = n * (int64_t)g.dpad16;
         k_quantize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(I->x.as<float>(), n, g.dpad, g.d, I->x16.as<int16_t>(),
                                                                  g.dpad16);
         PFG_CUDA(cudaGetLastError());
         PFG_CUDA(cudaStreamSynchronize(st));
-        I->x.release();
     }
     PFG_CUDA(cudaStreamSynchronize(st));
     *out = I.release();
@@ -1357,12 +1469,15 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     }
     std::shared_ptr<DBuf> thr, taub;
     PFG_TRY(get_thr(I, recall, s, thr, nullptr));
-    PFG_TRY(get_tau(I, s.eps, taub, nullptr));
+    PFG_TRY(get_tau(I, s.tau_rule, s.eps, recall, taub, nullptr));
     if (s.timing) {
         for (auto& e : I->ev)
             if (!e) PFG_CUDA(cudaEventCreate(&e));
         PFG_CUDA(cudaEventRecord(I->ev[0], st));
     }
+    I->tl_on = s.timing == 4;
+    I->tl_n = 0;
+    tl_mark(I, "start", st);
     I->launches = 0;
     bool lazy = false;
     // rounds 0 and 1 reach repetitions [0, 1 + R) only (R-17 default schedule): the codes and
@@ -1373,13 +1488,23 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // run any query to the end)
     int cp_eager = 0;
     if (g.family == PFG_CROSSPOLYTOPE && g.strategy == PFG_INDEPENDENT && s.engine == 0 && s.wide <= 0 && !I->loop_heavy &&
-        !getenv("PFG_LOOP_MAX") && !getenv("PFG_NO_CP_LAZY")) {
-        const int mr = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : (s.rounds > 0 ? s.rounds : 5);
+        s.loop_max == 0) {
+        const int mr = s.rounds > 0 ? s.rounds : 5;
         const int64_t reach = s.uniform ? (int64_t)s.R * mr : 1 + (int64_t)s.R * (mr - 1);
         const int64_t e = std::min<int64_t>(g.L, std::max<int64_t>(reach, I->eager));
         cp_eager = e < g.L ? (int)e : 0;
     }
-    PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st, split, cp_eager));
+    if (s.ext.codes) {
+        const bool lz = g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT;
+        if (s.ext.reps > g.L || (!lz && s.ext.reps != g.L))
+            return fail(PFG_E_ARG, "ext_reps must be L (<= L for the FHT cross-polytope family, independent functions)");
+        if (!is_device_ptr(s.ext.codes) || (s.ext.sk && !is_device_ptr(s.ext.sk)))
+            return fail(PFG_E_ARG, "ext_codes / ext_sketches must be device pointers");
+        cp_eager = 0;
+    }
+    if (s.ext.sk && g.M == 0) return fail(PFG_E_ARG, "ext_sketches given for an index without sketches");
+    PFG_TRY(prep_queries(I, queries, nq, true, false, nullptr, &lazy, st, s.ext.codes ? 0 : split, cp_eager,
+                         s.ext.codes || s.ext.sk ? &s.ext : nullptr));
 
     const int k_eff = (int)std::min<int64_t>(k, g.n);
     const int kt = ((k_eff + 31) / 32) * 32;
@@ -1406,17 +1531,18 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->slots_bm = bm_words;
     }
     PFG_TRY(I->cur.ensure((size_t)nq * g.L * 16, "cursors"));
-    const bool rounds = s.engine == 0 && g.strategy != PFG_TENSOR;  // tensor shells: the fused kernel
+    const bool rounds = (s.engine == 0 || s.engine == 2) && g.strategy != PFG_TENSOR;  // tensor shells: the fused kernel
     // round engine: `rounds` bulk rounds (search option, default 5), then the fused kernel resumes
     // every query still running (stragglers keep their hash set in shared memory across chunks
     // there, instead of paying a round's fixed latency per chunk).  The rounds are enqueued
     // without host synchronisation.
-    const int max_rounds = getenv("PFG_MAX_ROUNDS") ? atoi(getenv("PFG_MAX_ROUNDS")) : (s.rounds > 0 ? s.rounds : 5);
+    const int max_rounds = s.rounds > 0 ? s.rounds : 5;
     const int ecap = 2048;  // evaluated-list stride: kHMax committed + one batch of slack
     const int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
     const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
     int64_t wide_max = 0;   // visit-tag arrays this search may use
     bool want_wide = false;
+    bool chunk_eng = false; // the chunk engine (kernels_chunk.cuh): engine 2, unless wide queries are on
     if (rounds) {
         const size_t N = (size_t)nq;
         PFG_TRY(I->rs_lvl.ensure(N * 4, "rs")); PFG_TRY(I->rs_c0.ensure(N * 4, "rs"));
@@ -1424,8 +1550,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_TRY(I->rs_cnt.ensure(N * kCnt * 4, "rs")); PFG_TRY(I->rs_T.ensure(N * kt * 8, "rs"));
         PFG_TRY(I->rs_E.ensure(N * ecap * 4, "rs")); PFG_TRY(I->rs_pend.ensure(N * kMaxR * 16, "rs"));
         PFG_TRY(I->rs_repcnt.ensure(N * kMaxR * 3 * 4, "rs"));
-        PFG_TRY(I->rs_pool_id.ensure((size_t)pool_cap * 4, "pool")); PFG_TRY(I->rs_pool_q.ensure((size_t)pool_cap * 4, "pool"));
-        PFG_TRY(I->rs_pool_key.ensure((size_t)pool_cap * 8, "pool"));
+        // two pools (one per round parity: the chunk engine merges the previous round's pool while
+        // it fills the next)
+        PFG_TRY(I->rs_pool_id.ensure((size_t)pool_cap * 8, "pool")); PFG_TRY(I->rs_pool_q.ensure((size_t)pool_cap * 8, "pool"));
+        PFG_TRY(I->rs_pool_key.ensure((size_t)pool_cap * 16, "pool"));
         PFG_TRY(I->rs_ctl.ensure(sizeof(RoundCtl), "rs control")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_pn.ensure(N * 4, "rs")); PFG_TRY(I->rs_act0.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_act1.ensure(N * 4, "rs")); PFG_TRY(I->rs_fused.ensure(N * 4, "rs"));
@@ -1440,10 +1568,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             PFG_CUDA(cudaMallocHost(&I->h_ctl, sizeof(RoundCtl)));
             std::memset(I->h_ctl, 0, sizeof(RoundCtl));
         }
-        if (!I->aux) {
-            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
-            PFG_CUDA(cudaStreamCreateWithFlags(&I->aux2, cudaStreamNonBlocking));
-        }
+        PFG_TRY(ensure_streams(I));
         if (!I->ev_split) {
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_split, cudaEventDisableTiming));
             PFG_CUDA(cudaEventCreateWithFlags(&I->ev_f1, cudaEventDisableTiming));
@@ -1452,13 +1577,14 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         // at most, default 8 GiB) and wide scan tiles, sized grow-only from what the previous
         // search wanted; visit s = (K - i) L + j + 1 must fit 16 bits
         const int64_t per = 4 * g.n;
-        const int64_t wmib = getenv("PFG_WIDE_MIB") ? atoll(getenv("PFG_WIDE_MIB")) : 8192;
-        wide_max = std::max<int64_t>(1, (wmib << 20) / per);
+        wide_max = std::max<int64_t>(1, ((int64_t)8192 << 20) / per);
+        if (s.wide_arrays > 0) wide_max = std::min<int64_t>(wide_max, s.wide_arrays);
         // wide queries: on when asked for (wide > 0, or the developer knob PFG_LOOP_MAX), else
         // automatic: on iff the previous search's queries were heavy (loop_heavy); off, a query
         // beyond the hash set goes to the fused kernel's bitmap mode (and nothing is allocated)
-        want_wide = (s.wide > 0 || (s.wide == 0 && (I->loop_heavy || getenv("PFG_LOOP_MAX")))) &&
+        want_wide = (s.wide > 0 || (s.wide == 0 && (I->loop_heavy || s.loop_max > 0))) &&
                     (int64_t)(g.K + 1) * g.L < 65536;
+        if (s.engine == 2 && !want_wide) chunk_eng = true;
         if (want_wide) {
             const int64_t smax = wide_max;
             const int64_t want = std::min<int64_t>(smax, std::max<int64_t>(I->wv_want, std::max<int64_t>(1, (512ll << 20) / per)));
@@ -1470,10 +1596,10 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 I->wepoch = 0;
             }
             const int64_t wmin = (int64_t)s.R * ((g.n + kTile - 1) / kTile + 2);
-            // (developer knob PFG_WCAP_MIN=1: the minimum, so that wide chunks compete and defer)
-            const int64_t wc0 = getenv("PFG_WCAP_MIN") ? 0 : (int64_t)1 << 18;
+            // (wide_tiles_min: the minimum, so that wide chunks compete and defer)
+            const int64_t wc0 = s.wide_tiles_min ? 0 : (int64_t)1 << 18;
             const int64_t wc = std::max<int64_t>(wmin, std::max<int64_t>(I->wc_want, wc0));
-            if (wc > I->wc_cap || (getenv("PFG_WCAP_MIN") && wc != I->wc_cap)) {
+            if (wc > I->wc_cap || (s.wide_tiles_min && wc != I->wc_cap)) {
                 PFG_TRY(I->rs_wtiles.alloc((size_t)wc * 32, "wide tiles"));
                 PFG_TRY(I->rs_wcand.alloc((size_t)wc * kTile * 4, "wide candidates"));
                 PFG_TRY(I->rs_wsim.alloc((size_t)wc * kTile * 4, "wide similarities"));
@@ -1525,7 +1651,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // level-K match ranges of the first repetitions, one thread per (query, repetition)
     // (SimHash and pool strategies hash all L repetitions eagerly; their ranges are precomputed
     // for the repetitions most queries reach, the tuned eager depth)
-    p.qb_n = getenv("PFG_NO_QB") ? 0 : lazy ? std::min(I->qc_n, kQBMax) : std::min(I->qc_n, I->qb_depth);
+    p.qb_n = lazy ? std::min(I->qc_n, kQBMax) : std::min(I->qc_n, I->qb_depth);
     PFG_TRY(I->jhist.ensure(kJHist * 4, "stop histogram"));
     if (!I->h_jhist) PFG_CUDA(cudaMallocHost(&I->h_jhist, kJHist * 4));
     PFG_CUDA(cudaMemsetAsync(I->jhist.p, 0, kJHist * 4, st));
@@ -1539,11 +1665,13 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const int bs = bm >= 0 ? bm : b0;
         const int64_t thr_n = nq * (int64_t)bs;
         if (bs > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, bs, nullptr);
+        tl_mark(I, "k_qbounds", st);
         if (bm >= 0 && bm < b0) {
             const int64_t thr_m = nq * (int64_t)(b0 - bm);
             k_qbounds<<<(unsigned)((thr_m + 255) / 256), 256, 0, I->aux2>>>(p, I->qbnd.as<uint4>(), nullptr, nq, bm, b0 - bm,
                                                                           nullptr);
             I->launches += 1;
+            tl_mark(I, "k_qbounds (mid)", I->aux2);
         }
         if (I->mid_pending) PFG_CUDA(cudaEventRecord(I->ev_mid, I->aux2));
         if (I->late_pending && I->late_ne > I->qc_split) {
@@ -1555,6 +1683,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             k_qbounds<<<(unsigned)((thr_l + 255) / 256), 256, 0, I->aux2>>>(p, I->qbnd.as<uint4>(), nullptr, nq, b0,
                                                                           p.qb_n - b0, nullptr);
             I->launches += 1;
+            tl_mark(I, "k_qbounds (late)", I->aux2);
         }
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
@@ -1567,11 +1696,13 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     }
     if (I->late_pending) PFG_CUDA(cudaEventRecord(I->ev_late, I->aux2));
     // developer instrumentation: PFG_PHASE_PROF=1 prints per-phase warp cycles of each search to stderr
-    static const bool phase_prof = getenv("PFG_PHASE_PROF") && getenv("PFG_PHASE_PROF")[0] == '1';
+    // timing = 5 (developer): per-phase cycle counters of the fused kernel (and of k_chunk in a
+    // -DPFG_CHUNK_PROF=1 build), printed to stderr
+    const bool phase_prof = s.timing == 5;
     DBuf profb;
     if (phase_prof) {
-        PFG_TRY(profb.alloc(16 * 8, "phase profile"));
-        PFG_CUDA(cudaMemsetAsync(profb.p, 0, 128, st));
+        PFG_TRY(profb.alloc(32 * 8, "phase profile"));
+        PFG_CUDA(cudaMemsetAsync(profb.p, 0, 256, st));
         p.prof = profb.as<unsigned long long>();
     }
     if (!rounds) {
@@ -1605,10 +1736,105 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         r.wtcnt = I->rs_wtcnt.as<uint32_t>();
         r.wcap = wide_on ? (uint32_t)I->wc_cap : 0u;
         r.hmax = s.wide > 0 ? (uint32_t)s.wide : (uint32_t)kHMax;
+        r.pool_stride = chunk_eng ? pool_cap : 0u;
         PFG_CUDA(cudaMemsetAsync(r.ctl, 0, sizeof(RoundCtl), st));
         k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, (uint32_t)(0xFFFEu - I->wepoch) << 16);
         PFG_CUDA(cudaGetLastError());
         I->launches += 1;
+    }
+    if (chunk_eng) {
+        // the chunk engine: per round k_chunk (CTA per query: merge, expand, scan, dedupe) and
+        // k_sims; a merge-only pass; the fused kernel for the queries still running
+        RoundState& r = p.rs;
+        const size_t csm = (size_t)chunk_smem_bytes(kt, g.dpad, lazy);
+        const void* kfn = epl == 1 ? (const void*)k_chunk<1> : epl == 2 ? (const void*)k_chunk<2> : epl == 4 ? (const void*)k_chunk<4>
+                        : epl == 8 ? (const void*)k_chunk<8> : epl == 16 ? (const void*)k_chunk<16> : (const void*)k_chunk<32>;
+        PFG_CUDA(set_smem(kfn, csm));
+        int cocc = 1;
+        PFG_CUDA(occupancy(&cocc, kfn, kCT, csm));
+        const unsigned cb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)I->num_sms * std::max(1, cocc)));
+        const unsigned sb = (unsigned)(I->num_sms * PFG_SIMS_MINB);
+        const bool tm = s.timing == 2;
+        const bool ksims_timed = s.timing == 3;
+        auto launch_chunk = [&](int par, int mode) -> pfg_status {
+            switch (epl) {
+                case 1: k_chunk<1><<<cb, kCT, csm, st>>>(p, par, mode); break;
+                case 2: k_chunk<2><<<cb, kCT, csm, st>>>(p, par, mode); break;
+                case 4: k_chunk<4><<<cb, kCT, csm, st>>>(p, par, mode); break;
+                case 8: k_chunk<8><<<cb, kCT, csm, st>>>(p, par, mode); break;
+                case 16: k_chunk<16><<<cb, kCT, csm, st>>>(p, par, mode); break;
+                default: k_chunk<32><<<cb, kCT, csm, st>>>(p, par, mode); break;
+            }
+            PFG_CUDA(cudaGetLastError());
+            PFG_TRY(dbg_sync("k_chunk"));
+            tl_mark(I, mode ? "k_chunk (merge only)" : "k_chunk", st);
+            I->launches += 1;
+            return PFG_OK;
+        };
+        int round = 0;
+        for (; round < max_rounds; ++round) {
+            // round 0 is the single repetition 0 with tau = 64 (no sketches read); round 1 reaches
+            // repetitions < 1 + R; later rounds may reach every eager repetition
+            if (round == 1) { PFG_TRY(join_sketches(I, st)); PFG_TRY(mid_join(I, st)); }
+            if (round == 2) PFG_TRY(late_join(I, st));
+            const int par = round & 1;
+            PFG_TRY(phase_mark(I, tm, kPhExpand, st));
+            PFG_TRY(launch_chunk(par, 0));
+            PFG_TRY(phase_mark(I, tm, kPhSims, st));
+            const bool kt_ = ksims_timed;
+            if (kt_) {
+                if ((int64_t)I->kev.size() < 2 * (I->kev_n + 1)) {
+                    if (I->kev_n >= 512) PFG_TRY(fold_kernel_timing(I));
+                    while ((int64_t)I->kev.size() < 2 * (I->kev_n + 1)) {
+                        cudaEvent_t e;
+                        PFG_CUDA(cudaEventCreate(&e));
+                        I->kev.push_back(e);
+                    }
+                }
+                PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n], st));
+            }
+            if (g.storage == PFG_STORAGE_I16) k_sims<QueryParams, true><<<sb, 256, 0, st>>>(p, par, 3);
+            else k_sims<QueryParams, false><<<sb, 256, 0, st>>>(p, par, 3);
+            PFG_CUDA(cudaGetLastError());
+            if (kt_) PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n++ + 1], st));
+            PFG_TRY(dbg_sync("k_sims"));
+            tl_mark(I, "k_sims", st);
+            I->launches += 1;
+        }
+        PFG_TRY(join_sketches(I, st));
+        PFG_TRY(late_join(I, st));
+        PFG_TRY(phase_mark(I, tm, kPhMerge, st));
+        PFG_TRY(launch_chunk(round & 1, 1));
+        PFG_TRY(phase_mark(I, tm, kPhOther, st));
+        p.qlist = r.fused;
+        p.nq_dev = &r.ctl->nfused;
+        p.resume = 1;
+        // the queries the fused kernel resumes get codes and match ranges for kExtReps more
+        // repetitions in bulk (they would otherwise hash and search them one warp at a time)
+        if (cp_eager > 0) {
+            const int f0 = cp_eager * g.c, nf = (g.L - cp_eager) * g.c;
+            PFG_TRY(I->qfc2.ensure((size_t)nq * nf * 2, "cp function codes (resumed queries)"));
+            PFG_TRY(cp_values(I, I->qx.as<float>(), nq, r.fused, &r.ctl->nfused, f0, nf, I->qfc2.as<uint16_t>(), st));
+            k_pool_codes<<<dim3((unsigned)((nq + 255) / 256), (unsigned)(g.L - cp_eager)), 256, 0, st>>>(
+                I->qfc2.as<uint16_t>(), nq, nf, cp_eager, g.L - cp_eager, g.c, g.ell, g.K, I->sel.as<int32_t>(), nullptr,
+                I->qcodes.as<uint32_t>(), g.L, r.fused, &r.ctl->nfused, f0);
+            PFG_CUDA(cudaGetLastError());
+            I->launches += 2;
+            p.qc_n = g.L;
+        }
+        if (lazy && I->qc_n > 0 && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+            const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
+            PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, st, &r.ctl->nfused));
+            const int64_t thr_n = nq * (int64_t)nr;
+            k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.fused, nq, r0, nr,
+                                                                     &r.ctl->nfused);
+            PFG_CUDA(cudaGetLastError());
+            I->launches += 2;
+            p.qc_n = p.qb_n = I->qc_ld;
+        }
+        I->last_rounds = round;
+    } else if (rounds) {
+        RoundState& r = p.rs;
         const size_t esm = (size_t)expand_smem_bytes(g.dpad, lazy) * 4;
         const size_t dsm = (size_t)align16((int)sizeof(DedupeSmem)) * 4;
         const size_t msm = (size_t)(align16((int)sizeof(MergeSmem)) + 2 * align16(kt * 8)) * 4;
@@ -1641,14 +1867,14 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 case 16: k_expand<16, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
                 default: k_expand<32, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
             }
-            if (rst == st) PFG_TRY(dbg_sync("k_expand"));
+            if (rst == st) { PFG_TRY(dbg_sync("k_expand")); tl_mark(I, "k_expand", st); }
             PFG_TRY(phase_mark(I, marks, kPhScan, rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_scan<PP, true><<<tb_s, 256, 0, rst>>>(pp, par);
             else k_scan<PP, false><<<tb_s, 256, 0, rst>>>(pp, par);
-            if (rst == st) PFG_TRY(dbg_sync("k_scan"));
+            if (rst == st) { PFG_TRY(dbg_sync("k_scan")); tl_mark(I, "k_scan", st); }
             PFG_TRY(phase_mark(I, marks, kPhDedupe, rst));
             k_dedupe<PP><<<qb_d, 128, dsm, rst>>>(pp, par);
-            if (rst == st) PFG_TRY(dbg_sync("k_dedupe"));
+            if (rst == st) { PFG_TRY(dbg_sync("k_dedupe")); tl_mark(I, "k_dedupe", st); }
             PFG_TRY(phase_mark(I, marks, kPhSims, rst));
             const bool kt = ksims_timed && rst == st;
             if (kt) {
@@ -1663,19 +1889,20 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 }
                 PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n], rst));
             }
-            if (g.storage == PFG_STORAGE_I16) k_sims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
-            else k_sims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
+            const int sflags = rst == st ? 2 : 0;   // blind rounds (outside the captured loop)
+            if (g.storage == PFG_STORAGE_I16) k_sims<PP, true><<<sb, 256, 0, rst>>>(pp, par, sflags);
+            else k_sims<PP, false><<<sb, 256, 0, rst>>>(pp, par, sflags);
             if (kt) PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n++ + 1], rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) {
                 // wide tiles of the round (tag checks, compaction, similarities)
                 if (g.storage == PFG_STORAGE_I16) k_wsims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
                 else k_wsims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
             }
-            if (rst == st) PFG_TRY(dbg_sync("k_sims"));
+            if (rst == st) { PFG_TRY(dbg_sync("k_sims")); tl_mark(I, "k_sims", st); }
             PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_merge<PP, true><<<qb_m, 128, msm, rst>>>(pp, par);
             else k_merge<PP, false><<<qb_m, 128, msm, rst>>>(pp, par);
-            if (rst == st) PFG_TRY(dbg_sync("k_merge"));
+            if (rst == st) { PFG_TRY(dbg_sync("k_merge")); tl_mark(I, "k_merge", st); }
             PFG_TRY(phase_mark(I, marks, kPhOther, rst));
             PFG_CUDA(cudaGetLastError());
             return PFG_OK;
@@ -1695,13 +1922,11 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         // between the device-side round loop and the fused kernel (k_split), whose first launch
         // runs on the aux stream beside the loop
         const int P = round & 1;
-        const char* e_lmin = getenv("PFG_LOOP_MIN");
-        const char* e_lmax = getenv("PFG_LOOP_MAX");
-        const uint32_t lmin = e_lmin ? (uint32_t)atol(e_lmin) : 64u;
+        const uint32_t lmin = s.loop_min > 0 ? (uint32_t)s.loop_min : 64u;
         // default: the loop keeps only the wide queries (a query beyond the hash set early in the
         // search), unless the previous search's queries were heavy (loop_heavy); queries that are
         // merely long run faster in the fused kernel (measured)
-        const uint32_t lmax = e_lmax ? (uint32_t)atol(e_lmax) : (I->loop_heavy ? 0xffffffffu : 0u);
+        const uint32_t lmax = s.loop_max > 0 ? (uint32_t)s.loop_max : (I->loop_heavy ? 0xffffffffu : 0u);
         const bool loop_on = r.wslots > 0 || lmax > 0;
         const unsigned gq = (unsigned)((nq + 255) / 256);
         k_presplit<<<1, 1, 0, st>>>(p, P);
@@ -1753,6 +1978,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             }
             I->launches += 1;
             PFG_TRY(dbg_sync("fused 1"));
+            tl_mark(I, "k_query (fused, beside the loop)", I->aux);
             PFG_CUDA(cudaEventRecord(I->ev_f1, I->aux));
         }
         // the device-side loop: a CUDA graph whose WHILE node runs two rounds per iteration
@@ -1826,24 +2052,6 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         if (lmax == 0) fused_n = 0;
         I->last_rounds = round;
     }
-    if (!rounds && p.qb_n > 0 && nq > 1 && getenv("PFG_ORDER")) {
-        // longest-first order by the entries the first repetitions' match ranges hold
-        PFG_TRY(I->qord_keys.ensure((size_t)nq * 8, "query order"));
-        PFG_TRY(I->qord_sorted.ensure((size_t)nq * 8, "query order"));
-        PFG_TRY(I->qord_list.ensure((size_t)nq * 4, "query order"));
-        size_t tb = 0;
-        PFG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)nq, 32, 64, st));
-        PFG_TRY(I->qord_temp.ensure(tb, "query order temp"));
-        const unsigned gb = (unsigned)((nq + 255) / 256);
-        k_qorder_keys<<<gb, 256, 0, st>>>(p, I->qord_keys.as<uint64_t>());
-        tb = I->qord_temp.bytes;
-        PFG_CUDA(cub::DeviceRadixSort::SortKeys(I->qord_temp.p, tb, I->qord_keys.as<uint64_t>(), I->qord_sorted.as<uint64_t>(),
-                                                (int)nq, 32, 64, st));
-        k_qorder_list<<<gb, 256, 0, st>>>(I->qord_sorted.as<uint64_t>(), nq, I->qord_list.as<uint32_t>());
-        PFG_CUDA(cudaGetLastError());
-        I->launches += 3;
-        p.qlist = I->qord_list.as<uint32_t>();
-    }
     PFG_TRY(join_sketches(I, st));
     PFG_TRY(late_join(I, st));
     if (fused_n > 0) {
@@ -1861,6 +2069,16 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->launches += 1;
     }
     I->last_fused = fused_n;
+    if (g.storage == PFG_STORAGE_I16 && s.rerank) {
+        // the fixed-point search's top-k re-scored with fp32 rows (R-2 order), re-sorted
+        const size_t rsm = (size_t)4 * align16(kt * 8);
+        PFG_CUDA(set_smem((const void*)k_rerank, rsm));
+        k_rerank<<<(unsigned)((nq + 3) / 4), 128, rsm, st>>>(p.x, p.qx, g.dpad, nq, k, k_eff, kt, g.id_offset, d_ids, d_sims);
+        PFG_CUDA(cudaGetLastError());
+        I->launches += 1;
+        tl_mark(I, "k_rerank", st);
+    }
+    tl_mark(I, "end", st);
     PFG_TRY(phase_mark(I, s.timing == 2, kPhEnd, st));
     if (s.timing) PFG_CUDA(cudaEventRecord(I->ev[2], st));
     I->timing_pending = s.timing;
@@ -1888,6 +2106,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // developer phase print) need the results here
     const bool host_out = !ids_dev || !sims_dev || (stats && !stats_dev) || (s.trace_cap > 0 && !trace_dev);
     if (host_out || phase_prof) PFG_CUDA(cudaStreamSynchronize(st));
+    tl_print(I);
     if (phase_prof) {
         if (rounds) {
             PFG_CUDA(cudaMemcpy(I->h_ctl, I->rs_ctl.p, sizeof(RoundCtl), cudaMemcpyDeviceToHost));
@@ -1898,8 +2117,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         }
         fprintf(stderr, "[pfg phase] engine %d: rounds %d, queries finished by the fused kernel %lld of %lld\n", s.engine,
                 I->last_rounds, (long long)fused_n, (long long)nq);
-        unsigned long long h[16] = {0};
-        PFG_CUDA(cudaMemcpy(h, profb.p, 128, cudaMemcpyDeviceToHost));
+        unsigned long long h[32] = {0};
+        PFG_CUDA(cudaMemcpy(h, profb.p, 256, cudaMemcpyDeviceToHost));
+        if (h[22])
+            fprintf(stderr, "[pfg phase] k_chunk per query (thread-0 cycles): merge %.0f, expand %.0f, scan+dedupe %.0f, "
+                    "pool %.0f, scheduling %.0f; %.0f query-rounds\n", (double)h[16] / h[22], (double)h[17] / h[22],
+                    (double)h[18] / h[22], (double)h[19] / h[22], (double)h[23] / h[22], (double)h[22]);
         if (h[14])
             fprintf(stderr, "[pfg phase] collect per query-chunk: rebuild %.0f, codes+bounds %.0f, scan %.0f, epilogue %.0f cycles; "
                     "max %.0f cycles; %.0f chunks, mean emitted %.1f, max emitted %llu\n",
@@ -1969,8 +2192,9 @@ pfg_status pfg_round_stats(pfg_index* I, uint64_t* out, int32_t n) {
     if (I->nsearch == 0 || !I->h_ctl2) return fail(PFG_E_STATE, "no round-engine search yet");
     if (I->ev_done) PFG_CUDA(cudaEventSynchronize(I->ev_done));
     const RoundCtl* c = I->h_ctl2 + ((I->nsearch - 1) & 1);
-    const uint64_t v[6] = {c->sims_rows, (uint64_t)I->last_rounds, c->round, c->nfused, c->nfused2, c->wnext};
-    for (int i = 0; i < n && i < 6; ++i) out[i] = v[i];
+    const uint64_t v[7] = {c->sims_rows, (uint64_t)I->last_rounds, c->round, c->nfused, c->nfused2, c->wnext,
+                           c->sims_rows_blind};
+    for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
     return PFG_OK;
 }
 
@@ -2042,7 +2266,7 @@ pfg_status pfg_export(const pfg_index* Ic, int32_t what, int32_t arg, void* dst,
             return PFG_OK;
         }
         case PFG_EXPORT_DATA: {
-            if (g.storage != PFG_STORAGE_F32) return fail(PFG_E_STATE, "index stores int16 rows (PFG_EXPORT_DATA16)");
+            if (!I->x.p) return fail(PFG_E_STATE, "index holds no fp32 rows");
             if (bytes != (uint64_t)g.n * g.d * 4) return fail(PFG_E_ARG, "dst_bytes must be n*d*4");
             PFG_CUDA(cudaMemcpy2D(dst, (size_t)g.d * 4, I->x.p, (size_t)g.dpad * 4, (size_t)g.d * 4, (size_t)g.n,
                                   cudaMemcpyDeviceToHost));
@@ -2094,6 +2318,37 @@ pfg_status pfg_hash_queries(pfg_index* I, const float* queries, int64_t nq, uint
     return PFG_OK;
 }
 
+pfg_status pfg_hash_queries_reps(pfg_index* I, const float* queries, int64_t nq, int32_t nreps, uint32_t* out_codes,
+                                 uint64_t* out_sketches, void* stream) {
+    if (!I || !queries || !out_codes) return fail(PFG_E_ARG, "NULL pointer");
+    if (nq < 1) return fail(PFG_E_ARG, "nq must be >= 1");
+    if (nreps < 1 || nreps > I->g.L) return fail(PFG_E_ARG, "nreps must be in [1, L]");
+    std::lock_guard<std::mutex> lock(I->mu);
+    PFG_CUDA(cudaSetDevice(I->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const Geo& g = I->g;
+    int64_t zrow = -1;
+    bool lazy = false;
+    PFG_TRY(prep_queries(I, queries, nq, false, true, &zrow, &lazy, st, 0));
+    PFG_TRY(join_sketches(I, st));
+    if (zrow >= 0) return fail(PFG_E_ZERO_VECTOR, "query row " + std::to_string(zrow) + " is a zero vector");
+    PFG_TRY(I->qcodes.ensure((size_t)nq * nreps * 4, "query codes"));
+    if (g.family == PFG_CROSSPOLYTOPE_FHT && g.strategy == PFG_INDEPENDENT && (g.dp == 32 || g.dp == 64 || g.dp == 128)) {
+        PFG_TRY(fht_codes(I, nq, nullptr, 0, nreps, nreps, st));
+    } else {
+        bool pool_ready = false;
+        PFG_TRY(hash_reps(I, I->qx.as<float>(), nq, 0, nreps, nullptr, I->qcodes.as<uint32_t>(), nreps, I->qbits, I->qfc,
+                          pool_ready, st));
+    }
+    PFG_CUDA(cudaMemcpyAsync(out_codes, I->qcodes.p, (size_t)nq * nreps * 4,
+                             is_device_ptr(out_codes) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (out_sketches && g.M > 0)
+        PFG_CUDA(cudaMemcpyAsync(out_sketches, I->qsk.p, (size_t)nq * g.M * 8,
+                                 is_device_ptr(out_sketches) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    PFG_CUDA(cudaStreamSynchronize(st));
+    return PFG_OK;
+}
+
 pfg_status pfg_stop_tables(pfg_index* I, float recall, const pfg_search_opts* opts, float* thr_host, float* tau_host) {
     if (!I) return fail(PFG_E_ARG, "NULL index");
     if (!(recall > 0.0f && recall <= 1.0f)) return fail(PFG_E_ARG, "recall target must be in (0, 1]");
@@ -2110,7 +2365,7 @@ pfg_status pfg_stop_tables(pfg_index* I, float recall, const pfg_search_opts* op
     if (tau_host) {
         std::shared_ptr<DBuf> b;
         std::vector<float> h;
-        PFG_TRY(get_tau(I, s.eps, b, &h));
+        PFG_TRY(get_tau(I, s.tau_rule, s.eps, recall, b, &h));
         std::memcpy(tau_host, h.data(), 65 * 4);
     }
     return PFG_OK;

@@ -36,6 +36,36 @@ def gather_merge(ids, sims, group=None, merge=None):
     return (merge or merge_topk)(g_ids.view(world, nq, k), g_sims.view(world, nq, k))
 
 
+def gather_rows(local, nrows: int, group=None):
+    """all-gather row slices [shard_range(nrows, world, r)] of a [rows, w] tensor from every rank into
+    the full [nrows, w] tensor (slices padded to equal length for all_gather_into_tensor)"""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return local
+    rank = dist.get_rank(group)
+    per = shard_range(nrows, world, 0)[1]        # the largest slice
+    buf = torch.zeros((per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    lo, hi = shard_range(nrows, world, rank)
+    buf[: hi - lo] = local
+    out = torch.empty((world * per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    parts = [out[r * per: r * per + (shard_range(nrows, world, r)[1] - shard_range(nrows, world, r)[0])]
+             for r in range(world)]
+    return torch.cat(parts).contiguous()
+
+
+def distributed_query_hashes(hash_slice, queries, group=None):
+    """SURVEY 8(e) (identical functions on every shard): rank r hashes only its slice of the queries,
+    hash_slice(q_slice) -> (codes [s, reps], sketches [s, M]); the slices are all-gathered so every
+    rank holds every query's codes and sketches without hashing them all"""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    nq = queries.shape[0]
+    lo, hi = shard_range(nq, world, rank)
+    codes, sk = hash_slice(queries[lo:hi])
+    return gather_rows(codes, nq, group), gather_rows(sk, nq, group)
+
+
 class ShardedIndex:
     """Build this rank's shard: `local_data` are rows [row0, row0 + len) of the global dataset."""
 
@@ -44,8 +74,21 @@ class ShardedIndex:
         self.row0 = row0
         self.index = Index(local_data, memory_budget, family, seed=seed, id_offset=row0, **opts)
 
-    def search(self, queries, k: int, recall: float, **sopts):
-        """-> merged (ids [nq,k], sims [nq,k]) on every rank (CUDA tensors)"""
+    def prep_reps(self) -> int:
+        """repetitions whose codes the distributed preparation computes (all L unless the family
+        hashes later repetitions lazily in the kernels: FHT cross-polytope, independent functions)"""
+        inf = self.index.info
+        lazy = inf["family"] == 1 and inf["strategy"] == 0 and inf["fht_dim"] in (32, 64, 128)
+        return min(inf["reps"], 64) if lazy else inf["reps"]
+
+    def search(self, queries, k: int, recall: float, distributed_prep: bool = False, **sopts):
+        """-> merged (ids [nq,k], sims [nq,k]) on every rank (CUDA tensors).  distributed_prep: each rank
+        hashes 1/world of the queries and the codes and sketches are all-gathered"""
+        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        if distributed_prep and world > 1:
+            reps = self.prep_reps()
+            codes, sk = distributed_query_hashes(lambda qs: self.index.hash_queries_reps(qs, reps), queries, self.group)
+            sopts = dict(sopts, ext_codes=codes, ext_sketches=sk if self.index.info["sketch_words"] > 0 else None)
         res = self.index.search(queries, k, recall, **sopts)
         m_ids, m_sims = gather_merge(res[0], res[1], self.group)
         return (m_ids, m_sims) + tuple(res[2:])

@@ -156,6 +156,13 @@ def test_config34_full(cfg):
     sel = np.arange(0, len(q), max(1, len(q) // 16))
     cap = 1 << 15
     sids, ssims, sst, tr = g.search(torch.from_numpy(q[sel]).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
+    if cfg == 3:
+        # element by element against the oracle on the sampled queries (independent SimHash: the
+        # oracle builds the repetitions they touch; every query descends several levels)
+        for j in range(L):
+            o.prefix_table(j)   # builds repetition j (hashing in parallel over the points)
+        orr = o.search(q[sel], c["k"], c["recall"], rep_chunk=pfg.DEFAULT_REP_CHUNK, trace_cap=cap, threads=8)
+        _search_equal((sids, ssims, sst, tr), orr, cap)
     assert np.array_equal(sids.cpu().numpy(), ids[sel]) and np.array_equal(sst["j_stop"], st["j_stop"][sel])
     xn, qn = O.normalize(data), O.normalize(q[sel])
     for r in range(len(sel)):

@@ -70,3 +70,35 @@ def test_gloo_world2_gather_merge_equals_global_bruteforce():
     mp.spawn(_worker, args=(2, _free_port(), x, q, k, out), nprocs=2, join=True)
     gi, _ = O.bruteforce(x, q, k)
     assert np.array_equal(out[0], gi) and np.array_equal(out[1], gi)
+
+
+def _prep_worker(rank, world, port, data, q, out):
+    # every rank hashes only its slice of the queries (here with the oracle, CPU) and the
+    # slices are all-gathered; the result must equal hashing every query on one rank
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1906_12211_b200.sharded import distributed_query_hashes
+    X = O.OracleIndex(data, O.FHTCP, L=6, seed=4, M=3)
+
+    def hash_slice(qs):
+        codes, sk = X.hash(qs.numpy())
+        return torch.from_numpy(codes.view(np.int32)), torch.from_numpy(sk.view(np.int64))
+
+    codes, sk = distributed_query_hashes(hash_slice, torch.from_numpy(q))
+    out[rank] = (codes.numpy().view(np.uint32), sk.numpy().view(np.uint64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nq", [7, 40])
+def test_gloo_world2_distributed_query_hashing(nq):
+    rng = np.random.default_rng(5)
+    data = rng.standard_normal((500, 20)).astype(np.float32)
+    q = rng.standard_normal((nq, 20)).astype(np.float32)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_prep_worker, args=(2, _free_port(), data, q, out), nprocs=2, join=True)
+    codes, sk = O.OracleIndex(data, O.FHTCP, L=6, seed=4, M=3).hash(q)
+    for r in (0, 1):
+        assert np.array_equal(out[r][0], codes) and np.array_equal(out[r][1], sk)

@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Per-phase times of one search (timing = 2: CUDA events between the phases' launches) after a few
-warm-up searches, for a config; PFG_MAX_ROUNDS makes every round a blind (phase-timed) round.
+warm-up searches, for a config; --rounds 200 makes every round a blind (phase-timed) round.
 
-  PFG_MAX_ROUNDS=200 python tools/phase_breakdown.py --config 4
+  python tools/phase_breakdown.py --config 4 --rounds 200
 """
 import argparse
 import json
@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--warm", type=int, default=3)
 ap.add_argument("--wide", type=int, default=0)
+ap.add_argument("--rounds", type=int, default=0)
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 dev = torch.device("cuda:0")
@@ -32,9 +33,9 @@ if c["reps"]:
     opts["reps"] = c["reps"]
 idx = pfg.Index(X, c["budget"] or 0, c["family"], seed=1, **opts)
 for _ in range(a.warm):
-    idx.search(Q, c["k"], c["recall"], wide=a.wide)
+    idx.search(Q, c["k"], c["recall"], wide=a.wide, rounds=a.rounds)
 torch.cuda.synchronize()
-idx.search(Q, c["k"], c["recall"], timing=2, wide=a.wide)
+idx.search(Q, c["k"], c["recall"], timing=2, wide=a.wide, rounds=a.rounds)
 torch.cuda.synchronize()
 t = idx.last_timing()
 print(json.dumps({"config": a.config, "prep_ms": t[0], "kernel_ms": t[1], "launches": t[3],

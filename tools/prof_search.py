@@ -23,6 +23,7 @@ ap.add_argument("--recall", type=float, default=0.9)
 ap.add_argument("--rep-chunk", type=int, default=16)
 ap.add_argument("--nq", type=int, default=0)
 ap.add_argument("--warm", type=int, default=2)
+ap.add_argument("--timing", type=int, default=1, help="5: the fused kernel's per-phase cycle counters (stderr)")
 a = ap.parse_args()
 
 c = synth.CONFIGS[a.config]
@@ -39,7 +40,7 @@ for _ in range(a.warm):
     idx.search(Q, c["k"], a.recall, **so)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-idx.search(Q, c["k"], a.recall, **so)
+idx.search(Q, c["k"], a.recall, **dict(so, timing=a.timing))
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("timing (prep_ms, kernel_ms, ?, launches):", idx.last_timing())
