@@ -34,27 +34,42 @@ __global__ void k_quantize(const float* __restrict__ x, int64_t n, int dpad, int
 // a1: out[r][0..d) = (float)((double)x / sqrt(sum_t (double)x_t^2)), sum sequential over t;
 // out[r][d..dpad) = 0.  zflag[r] = 1 for a zero row; *zmin = smallest zero row index.
 // One thread per row (the double sum is order-dependent, so it is not split across lanes).
-__global__ void k_normalize(const float* __restrict__ x, int64_t n, int d, int ldx, float* __restrict__ out,
-                            int dpad, uint8_t* __restrict__ zflag, unsigned long long* __restrict__ zmin) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const float* row = x + r * ldx;
-    double s = 0.0;
-    for (int t = 0; t < d; ++t) {
-        const double v = (double)row[t];
-        s = __dadd_rn(s, __dmul_rn(v, v));
+__global__ void __launch_bounds__(128) k_normalize(const float* __restrict__ x, int64_t n, int d, int ldx,
+                                                  float* __restrict__ out, int dpad, uint8_t* __restrict__ zflag,
+                                                  unsigned long long* __restrict__ zmin, int rb) {
+    // rb rows per block, staged through shared memory so that the block reads and writes them
+    // coalesced; thread r < rb sums its row sequentially in double (the oracle's order)
+    extern __shared__ float srow[];   // [rb][d]
+    __shared__ double sinv[32];
+    __shared__ int szero[32];
+    const int64_t r0 = (int64_t)blockIdx.x * rb;
+    const int nr = (int)(n - r0 < (int64_t)rb ? n - r0 : (int64_t)rb);
+    if (nr <= 0) return;
+    for (int e = threadIdx.x; e < nr * d; e += blockDim.x) {
+        const int rr = e / d, t = e - rr * d;
+        srow[e] = x[(r0 + rr) * ldx + t];
     }
-    float* o = out + r * dpad;
-    const bool zero = !(s > 0.0);
-    if (zflag) zflag[r] = zero ? 1 : 0;
-    if (zero) {
-        atomicMin(zmin, (unsigned long long)r);
-        for (int t = 0; t < dpad; ++t) o[t] = 0.0f;
-        return;
+    __syncthreads();
+    if ((int)threadIdx.x < nr) {
+        const float* row = srow + threadIdx.x * d;
+        double s = 0.0;
+        for (int t = 0; t < d; ++t) {
+            const double v = (double)row[t];
+            s = __dadd_rn(s, __dmul_rn(v, v));
+        }
+        const int64_t r = r0 + threadIdx.x;
+        const bool zero = !(s > 0.0);
+        if (zflag) zflag[r] = zero ? 1 : 0;
+        if (zero) atomicMin(zmin, (unsigned long long)r);
+        szero[threadIdx.x] = zero ? 1 : 0;
+        sinv[threadIdx.x] = zero ? 1.0 : __dsqrt_rn(s);
     }
-    s = __dsqrt_rn(s);
-    for (int t = 0; t < d; ++t) o[t] = __double2float_rn(__ddiv_rn((double)row[t], s));
-    for (int t = d; t < dpad; ++t) o[t] = 0.0f;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * dpad; e += blockDim.x) {
+        const int rr = e / dpad, t = e - rr * dpad;
+        out[(r0 + rr) * dpad + t] = (t < d && !szero[rr]) ? __double2float_rn(__ddiv_rn((double)srow[rr * d + t], sinv[rr]))
+                                                          : 0.0f;
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -272,10 +287,12 @@ __global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ 
     for (int f = 0; f < c; ++f) {
         const uint32_t* sf = sg + ((int64_t)j * c + f) * 3 * W;
         float y[H];
+        // rows are ldx floats, zero beyond d (k_normalize), 16-byte aligned: 128-bit loads
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
+        for (int i = 0; i < H; i += 4) {
             const int u = g * H + i;
-            y[i] = (u < d) ? __ldg(xr + u) : 0.0f;
+            const float4 v = (u < ldx) ? __ldg(reinterpret_cast<const float4*>(xr + u)) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            y[i] = v.x; y[i + 1] = v.y; y[i + 2] = v.z; y[i + 3] = v.w;
         }
 #pragma unroll 1
         for (int r = 0; r < 3; ++r) {

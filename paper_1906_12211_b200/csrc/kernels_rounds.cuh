@@ -1008,7 +1008,63 @@ __global__ void __launch_bounds__(128, WIDE ? 8 : PFG_MERGE_MINB) k_merge(PP pp,
         __syncwarp();
         int r_stop = -1;
         uint32_t e = 0;
-        for (int r = 0; r < nr; ++r) {
+        // k_eff <= 32, not wide: the top list lives in registers (lane t holds T[t]) and each key above
+        // the k-th is inserted where it ranks (a ballot); the chunk's keys are read two batches ahead
+        // across repetition boundaries; the stop check follows each repetition as below
+        const bool regs = !wide && p.kt == 32;
+        if (regs) {
+            uint64_t tv = lane < tn ? T0[lane] : 0ull;
+            const uint32_t pn = __shfl_sync(kFull, end, nr - 1);
+            const uint64_t* keys = rs.pool_key + base;
+            uint64_t cur = lane < pn ? keys[lane] : 0ull;
+            uint64_t nxt = 32 + lane < pn ? keys[32 + lane] : 0ull;
+            int r = 0;
+            uint32_t rend = __shfl_sync(kFull, end, 0), done = 0;
+            bool fin = false;
+            for (uint32_t b0 = 0; !fin; b0 += 32) {
+                for (;;) {
+                    const uint32_t lim = min(b0 + 32, rend);
+                    const uint32_t idx = b0 + lane;
+                    const bool mine = idx >= done && idx < lim;
+                    if (mine && p.trace_cap > 0 && nE + idx < (uint32_t)p.trace_cap)
+                        p.trace_ids[q * p.trace_cap + nE + idx] = key_id(cur);
+                    uint64_t kth = (tn == p.k_eff) ? __shfl_sync(kFull, tv, p.k_eff - 1) : 0ull;
+                    uint32_t mk = __ballot_sync(kFull, mine && cur > kth);
+                    while (mk) {
+                        const int l = __ffs(mk) - 1;
+                        mk &= mk - 1;
+                        const uint64_t kk = __shfl_sync(kFull, cur, l);
+                        if (kk <= kth) continue;   // the k-th grew since the ballot
+                        const int pos = __popc(__ballot_sync(kFull, tv > kk));
+                        const uint64_t up = __shfl_up_sync(kFull, tv, 1);
+                        if (lane > pos) tv = up;
+                        else if (lane == pos) tv = kk;
+                        if (lane >= p.k_eff) tv = 0ull;
+                        tn = min(p.k_eff, tn + 1);
+                        kth = (tn == p.k_eff) ? __shfl_sync(kFull, tv, p.k_eff - 1) : 0ull;
+                    }
+                    done = lim;
+                    if (rend > b0 + 32) break;   // repetition r continues in the next batch
+                    const int j1 = c0 + r + 1;
+                    const float th = __shfl_sync(kFull, thr_r, r);
+                    if (i == 0) { r_stop = r; fin = true; break; }
+                    if (tn == p.k_eff && (!p.per_round || j1 == p.L)) {
+                        float ip = key_sim(__shfl_sync(kFull, tv, p.k_eff - 1));
+                        ip = fminf(fmaxf(ip, -1.0f), 1.0f);
+                        if (ip >= th) { r_stop = r; fin = true; break; }
+                    }
+                    if (++r >= nr) { fin = true; break; }
+                    rend = __shfl_sync(kFull, end, r);
+                }
+                if (fin) break;
+                cur = nxt;
+                nxt = b0 + 64 + lane < pn ? keys[b0 + 64 + lane] : 0ull;
+            }
+            nE += __shfl_sync(kFull, end, r_stop >= 0 ? r_stop : nr - 1);
+            if (lane < p.k_eff) T0[lane] = tv;
+            __syncwarp();
+        }
+        for (int r = 0; r < nr && !regs; ++r) {
             const uint32_t rnext = __shfl_sync(kFull, rt, (r + 1) & 31);
             if (!wide) {
                 const uint32_t e2 = __shfl_sync(kFull, end, r);

@@ -1,0 +1,229 @@
+// kernels_tc.cuh — SimHash bits (a3) and sketch words (a4) on the 5th-generation tensor cores.
+//
+// bit(p, f) = [<x_p, a_f> >= 0] is decided by the sequential fp32 fmaf chain over
+// t = 0..d-1 (R-2).  This kernel computes <x_p, a_f> as a 3xTF32 product on tcgen05 (x = x_hi + x_lo,
+// a = a_hi + a_lo with tf32 parts; x_hi a_hi + x_hi a_lo + x_lo a_hi accumulated in fp32 in TMEM) and
+// takes the sign from it wherever |value| >= B_f, a bound on the difference between the 3xTF32
+// value and the fmaf chain; inside the band the chain itself is evaluated (rare: |<x,a>| < B_f).
+// So every bit equals the chain's, i.e. the oracle's, by construction:
+//   |3xTF32 - exact| <= (2 * 2^-22 + 2^-22 + kdim * 2^-23) * sum_t |x_t a_t|   (split residuals, the
+//                                                                               dropped lo*lo term,
+//                                                                               fp32 accumulation)
+//   |chain - exact|  <= kdim * 2^-24 * sum_t |x_t a_t|
+//   sum_t |x_t a_t|  <= ||x||_2 ||a_f||_2 <= (1 + 2^-20) ||a_f||_2   (rows are normalised)
+// B_f = 4 * (kdim + 8) * 2^-22 * ||a_f||_2 covers both with a margin of more than 2x.
+//
+// CTA: 128 rows x 128 functions, K in chunks of 32 floats staged in shared memory (tf32 hi/lo parts
+// of both operands, canonical K-major SWIZZLE_NONE layout: 8-row x 16-byte core matrices), one
+// elected thread issues 3 x 4 tcgen05.mma.kind::tf32 (M = 128, N = 128, K = 8) per chunk and commits
+// them to an mbarrier; the accumulator (128 lanes x 128 fp32 columns) lives in TMEM and is read back
+// with tcgen05.ld (32x32b.x32) by the four warps (warp w: rows 32w .. 32w + 31).
+#pragma once
+#include "device_common.cuh"
+
+namespace pfg {
+
+constexpr int TC_M = 128, TC_N = 128, TC_KC = 32;
+constexpr int kTcSmem = (2 * TC_M * TC_KC + 2 * TC_N * TC_KC) * 4;   // 64 KB of operand tiles
+constexpr int kTcFallback = 512;   // band entries listed per CTA (more: evaluated in place)
+
+__device__ __forceinline__ uint32_t tc_smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// byte offset of element (r, k) of an [R][TC_KC] tile in the canonical K-major SWIZZLE_NONE layout
+__device__ __forceinline__ uint32_t tc_off(int r, int k, int R) {
+    return ((uint32_t)(((k >> 2) * (R >> 3) + (r >> 3)) << 7)) + ((r & 7) << 4) + ((k & 3) << 2);
+}
+
+// shared-memory matrix descriptor: start address, leading (K-direction) and stride (8-row group)
+// byte offsets in 16-byte units, descriptor version 1 (sm_100), SWIZZLE_NONE
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, int R) {
+    const uint64_t lbo = (uint64_t)((R >> 3) * 128) >> 4;
+    const uint64_t sbo = 128 >> 4;
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | (lbo << 16) | (sbo << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tc_mbar_wait(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+        "r"(phase)
+        : "memory");
+}
+
+// the four float tf32 hi / lo parts of a float4 into the two tiles at byte offset `off`
+__device__ __forceinline__ void tc_split_store(unsigned char* hi, unsigned char* lo, uint32_t off, float4 v) {
+    float4 h, l;
+    h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
+    h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
+    h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
+    h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
+    *reinterpret_cast<float4*>(hi + off) = h;
+    *reinterpret_cast<float4*>(lo + off) = l;
+}
+
+// bits of rows X[np][ldx] against functions A[nf][lda] over kdim (a multiple of 8, rows and
+// functions zero beyond d) into out[p * out_ld + f / 8] (bit f % 8), the same output as k_hp_bits
+__global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__ X, int64_t np, int ldx,
+                                                      const float* __restrict__ A, int nf, int lda, int kdim,
+                                                      uint8_t* __restrict__ out, int64_t out_ld) {
+    extern __shared__ __align__(1024) unsigned char tc_sm[];
+    unsigned char* Xhi = tc_sm;
+    unsigned char* Xlo = Xhi + TC_M * TC_KC * 4;
+    unsigned char* Ahi = Xlo + TC_M * TC_KC * 4;
+    unsigned char* Alo = Ahi + TC_N * TC_KC * 4;
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    __shared__ float fsq[TC_N];              // ||a_f||^2 of the CTA's functions, then the band B_f
+    __shared__ uint32_t obits[TC_M][TC_N / 32];
+    __shared__ uint32_t nfb;                 // entries inside the band (evaluated by the chain)
+    __shared__ uint32_t fbl[kTcFallback];    // their (row << 16 | function) indices
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t p0 = (int64_t)blockIdx.x * TC_M;
+    const int f0 = blockIdx.y * TC_N;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem_addr(&tmem_base)),
+                     "r"(TC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem_addr(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fsq[tid] = 0.0f;
+    if (tid == 0) nfb = 0;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+    uint32_t phase = 0;
+    const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    for (int k0 = 0; k0 < kdim; k0 += TC_KC) {
+        const int kc = min(TC_KC, kdim - k0);
+        // operand tiles: tf32 hi / lo parts in the canonical layout (a 16-byte core-matrix row holds
+        // 4 consecutive k of one row); columns beyond kc are zero
+#pragma unroll 2
+        for (int e = tid; e < TC_M * (TC_KC / 4); e += 128) {
+            const int r = e / (TC_KC / 4), k = (e % (TC_KC / 4)) * 4;
+            const float4 v = (p0 + r < np && k < kc) ? __ldg(reinterpret_cast<const float4*>(X + (p0 + r) * ldx + k0 + k)) : z4;
+            tc_split_store(Xhi, Xlo, tc_off(r, k, TC_M), v);
+        }
+#pragma unroll 2
+        for (int e = tid; e < TC_N * (TC_KC / 4); e += 128) {
+            const int r = e / (TC_KC / 4), k = (e % (TC_KC / 4)) * 4;
+            const float4 v = (f0 + r < nf && k < kc) ? __ldg(reinterpret_cast<const float4*>(A + (int64_t)(f0 + r) * lda + k0 + k)) : z4;
+            tc_split_store(Ahi, Alo, tc_off(r, k, TC_N), v);
+            // the 8 lanes holding row r's chunk sum its squares; one of them adds (each row has one
+            // writer per chunk)
+            float sq = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+            sq += __shfl_xor_sync(kFull, sq, 1);
+            sq += __shfl_xor_sync(kFull, sq, 2);
+            sq += __shfl_xor_sync(kFull, sq, 4);
+            if ((e & 7) == 0) fsq[r] += sq;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the tiles, to the tensor core
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t xh = tc_smem_addr(Xhi), xl = tc_smem_addr(Xlo), ah = tc_smem_addr(Ahi), al = tc_smem_addr(Alo);
+            for (int s = 0; s < kc / 8; ++s) {
+                const uint32_t ox = s * 2 * (TC_M / 8) * 128, oa = s * 2 * (TC_N / 8) * 128;
+                const uint64_t dxh = tc_desc(xh + ox, TC_M), dxl = tc_desc(xl + ox, TC_M);
+                const uint64_t dah = tc_desc(ah + oa, TC_N), dal = tc_desc(al + oa, TC_N);
+                tc_mma(tmem, dxh, dah, idesc, (k0 > 0 || s > 0) ? 1u : 0u);
+                tc_mma(tmem, dxh, dal, idesc, 1u);
+                tc_mma(tmem, dxl, dah, idesc, 1u);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             tc_smem_addr(&mbar))
+                         : "memory");
+        }
+        // the MMAs read the tiles: wait for them before the next chunk overwrites them
+        tc_mbar_wait(tc_smem_addr(&mbar), phase);
+        phase ^= 1;
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // B_f = 4 (kdim + 8) 2^-22 ||a_f||_2 (header)
+    fsq[tid] = 4.0f * (float)(kdim + 8) * 2.384185791015625e-07f * sqrtf(fsq[tid]);
+    __syncthreads();
+    // epilogue: thread = row 32 warp + lane; 32 columns (functions) per TMEM load; entries inside
+    // the band are listed and evaluated afterwards by the canonical chain, one per thread
+    const int rl = 32 * warp + lane;
+    const int64_t p = p0 + rl;
+#pragma unroll
+    for (int cb = 0; cb < TC_N; cb += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+            "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+              "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+              "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)cb));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t bits = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float a = __uint_as_float(v[j]);
+            const float band = fsq[cb + j];
+            if (a >= 0.0f) bits |= 1u << j;
+            if (fabsf(a) < band && p < np && f0 + cb + j < nf) {
+                const uint32_t slot = atomicAdd(&nfb, 1u);
+                if (slot < (uint32_t)kTcFallback) {
+                    fbl[slot] = ((uint32_t)rl << 16) | (uint32_t)(cb + j);
+                } else {
+                    const float* xr = X + p * ldx;
+                    const float* ar = A + (int64_t)(f0 + cb + j) * lda;
+                    float acc = 0.0f;
+                    for (int t = 0; t < kdim; ++t) acc = fmaf(__ldg(xr + t), __ldg(ar + t), acc);
+                    bits = (bits & ~(1u << j)) | ((acc >= 0.0f ? 1u : 0u) << j);
+                }
+            }
+        }
+        obits[rl][cb >> 5] = bits;
+    }
+    __syncthreads();
+    const uint32_t nl = min(nfb, (uint32_t)kTcFallback);
+    for (uint32_t e = tid; e < nl; e += 128) {
+        const uint32_t r = fbl[e] >> 16, j = fbl[e] & 0xffffu;
+        const float* xr = X + (p0 + r) * ldx;
+        const float* ar = A + (int64_t)(f0 + j) * lda;
+        float acc = 0.0f;
+        for (int t = 0; t < kdim; ++t) acc = fmaf(__ldg(xr + t), __ldg(ar + t), acc);   // the canonical chain (R-2)
+        if (acc >= 0.0f) atomicOr(&obits[r][j >> 5], 1u << (j & 31));
+        else atomicAnd(&obits[r][j >> 5], ~(1u << (j & 31)));
+    }
+    __syncthreads();
+    if (p < np) {
+#pragma unroll
+        for (int w = 0; w < TC_N / 32; ++w) {
+            const uint32_t bits = obits[rl][w];
+            const int fb = f0 + 32 * w;
+#pragma unroll
+            for (int by = 0; by < 4; ++by)
+                if (fb + 8 * by < nf) out[p * out_ld + ((fb >> 3) + by)] = (uint8_t)(bits >> (8 * by));
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_N));
+}
+
+}  // namespace pfg

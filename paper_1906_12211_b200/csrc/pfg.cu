@@ -26,6 +26,7 @@
 #include "kernels_query.cuh"
 #include "kernels_rounds.cuh"
 #include "kernels_chunk.cuh"
+#include "kernels_tc.cuh"
 #include "rng.h"
 
 namespace pfg {
@@ -579,8 +580,17 @@ void launch_mc(const float* XY, int ld, int64_t npairs, const Geo& g, const uint
     k_mc_codes<EPL><<<blocks, 256, 0, st>>>(XY, ld, npairs, g.d, g.dp, g.ell, g.cp_draws, sg, cnt);
 }
 
+#ifndef PFG_HP_TC
+#define PFG_HP_TC 0   // 1: SimHash bits / sketches on tcgen05 (3xTF32 + exact band, kernels_tc.cuh)
+#endif
 void hp_bits(const float* X, int64_t np, int ldx, const float* A, int nf, int lda, int kdim, uint8_t* out,
              int64_t out_ld, cudaStream_t st) {
+    if (PFG_HP_TC && (kdim % 8) == 0 && (ldx % 4) == 0 && (lda % 4) == 0 && ((uintptr_t)X % 16) == 0 &&
+        ((uintptr_t)A % 16) == 0 && set_smem((const void*)k_hp_bits_tc, kTcSmem) == cudaSuccess) {
+        dim3 tg((unsigned)((np + TC_M - 1) / TC_M), (unsigned)((nf + TC_N - 1) / TC_N));
+        k_hp_bits_tc<<<tg, 128, kTcSmem, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
+        return;
+    }
     dim3 grid((unsigned)((np + GB_M - 1) / GB_M), (nf + GB_N - 1) / GB_N);
     // the double-buffered kernel needs kdim, ldx, lda multiples of 8 and 16-byte aligned rows
     const bool v2 = (kdim % GB2_K) == 0 && (ldx % 4) == 0 && (lda % 4) == 0 && ((uintptr_t)X % 16) == 0 &&
@@ -927,7 +937,8 @@ pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, u
 pfg_status normalize_rows(const float* src, int64_t n, int d, float* dst, int dpad, uint8_t* zflag,
                           unsigned long long* zmin_dev, int64_t* zrow, cudaStream_t st) {
     PFG_CUDA(cudaMemsetAsync(zmin_dev, 0xff, 8, st));
-    k_normalize<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(src, n, d, d, dst, dpad, zflag, zmin_dev);
+    const int rb = std::max(1, std::min(32, 12288 / d));   // rows per block staged in shared memory
+    k_normalize<<<(unsigned)((n + rb - 1) / rb), 128, (size_t)rb * d * 4, st>>>(src, n, d, d, dst, dpad, zflag, zmin_dev, rb);
     PFG_CUDA(cudaGetLastError());
     if (!zrow) return PFG_OK;  // asynchronous: the caller reads zmin_dev later
     unsigned long long z = 0;

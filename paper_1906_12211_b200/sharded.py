@@ -79,7 +79,7 @@ class ShardedIndex:
         hashes later repetitions lazily in the kernels: FHT cross-polytope, independent functions)"""
         inf = self.index.info
         lazy = inf["family"] == 1 and inf["strategy"] == 0 and inf["fht_dim"] in (32, 64, 128)
-        return min(inf["reps"], 64) if lazy else inf["reps"]
+        return min(inf["reps"], 32) if lazy else inf["reps"]
 
     def search(self, queries, k: int, recall: float, distributed_prep: bool = False, **sopts):
         """-> merged (ids [nq,k], sims [nq,k]) on every rank (CUDA tensors).  distributed_prep: each rank
