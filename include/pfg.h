@@ -191,7 +191,7 @@ typedef struct {
  * memory.  memory_budget_bytes: total index size including the data and the hash functions
  * (PAPER.md:567); L is derived from it unless opts->reps_override > 0.  family: pfg_family.
  * seed: all hash functions derive from it (identical on every shard).
- * Errors: PFG_E_ARG (n < 1, n >= 2^32, d < 1, d > 4096, bad option), PFG_E_ZERO_VECTOR (message
+ * Errors: PFG_E_ARG (n < 1, n >= 2^31, d < 1, d > 4096, bad option), PFG_E_ZERO_VECTOR (message
  * names the row), PFG_E_BUDGET (message names the minimum budget), PFG_E_OOM, PFG_E_CUDA.
  * On error *out is NULL. */
 pfg_status pfg_build(const float* data, int64_t n, int32_t d, uint64_t memory_budget_bytes,

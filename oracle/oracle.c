@@ -177,6 +177,8 @@ typedef struct {
     float* skf;        /* sketch functions [64M][d] */
     uint32_t** codes;  /* sorted codes per rep (NULL = not built yet; lazy mode) */
     uint32_t** ids;    /* point ids per rep, aligned with codes */
+    uint16_t* fcache;  /* pool strategy: or_func of every pool function on every data point [n][m],
+                          computed once on the first table build (memoised values, same arithmetic) */
     double cpT[34 * 41]; /* CP table T[b][a], b = 0..ell, a = 0..40 */
     int cp_draws;
     int storage;       /* 0 = fp32 rows (or_sim), 1 = 16-bit fixed point (or_sim16, R-25) */
@@ -233,6 +235,22 @@ void or_sketch(const or_index* X, const float* x, uint64_t* out) {
     }
 }
 
+/* pool strategy: the values of all m pool functions on every data point, computed once (a table
+ * build reads c of them per point; the rep code is the same concatenation as or_rep_code) */
+static void or_need_fcache(or_index* X) {
+    if (X->fcache) return;
+    uint16_t* fc = (uint16_t*)malloc(sizeof(uint16_t) * X->n * (int64_t)X->m);
+    #pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < X->n; ++p)
+        for (int f = 0; f < X->m; ++f) fc[p * X->m + f] = (uint16_t)or_func(X, f, X->x + p * X->d);
+    X->fcache = fc;
+}
+static uint32_t or_rep_code_cached(const or_index* X, int j, int64_t p) {
+    uint64_t full = 0;
+    for (int t = 0; t < X->c; ++t) full = (full << X->ell) | X->fcache[p * X->m + X->sel[j * X->c + t]];
+    return (uint32_t)(full >> (X->c * X->ell - X->K));
+}
+
 /* build one repetition: hash all points, sort (code, id) ascending */
 static int or_cmp_pair(const void* a, const void* b) {
     const uint64_t* x = (const uint64_t*)a; const uint64_t* y = (const uint64_t*)b;
@@ -241,9 +259,15 @@ static int or_cmp_pair(const void* a, const void* b) {
 static void or_build_rep(or_index* X, int j) {
     int64_t n = X->n;
     uint64_t* pr = (uint64_t*)malloc(sizeof(uint64_t) * n);
-    #pragma omp parallel for schedule(static)
-    for (int64_t p = 0; p < n; ++p)
-        pr[p] = ((uint64_t)or_rep_code(X, j, X->x + p * X->d) << 32) | (uint64_t)p;
+    if (X->strategy == OR_POOL) {
+        or_need_fcache(X);
+        #pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < n; ++p) pr[p] = ((uint64_t)or_rep_code_cached(X, j, p) << 32) | (uint64_t)p;
+    } else {
+        #pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < n; ++p)
+            pr[p] = ((uint64_t)or_rep_code(X, j, X->x + p * X->d) << 32) | (uint64_t)p;
+    }
     qsort(pr, n, sizeof(uint64_t), or_cmp_pair);
     X->codes[j] = (uint32_t*)malloc(sizeof(uint32_t) * n);
     X->ids[j] = (uint32_t*)malloc(sizeof(uint32_t) * n);
@@ -433,7 +457,7 @@ void or_free(or_index* X) {
     if (!X) return;
     for (int j = 0; j < X->L; ++j) { free(X->codes[j]); free(X->ids[j]); }
     free(X->codes); free(X->ids); free(X->x); free(X->sk); free(X->hp); free(X->sg);
-    free(X->sel); free(X->slot); free(X->skf); free(X->x16); free(X);
+    free(X->sel); free(X->slot); free(X->skf); free(X->x16); free(X->fcache); free(X);
 }
 
 /* accessors for tests */

@@ -117,26 +117,28 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
     for (int k0 = 0; k0 < kdim; k0 += TC_KC) {
         const int kc = min(TC_KC, kdim - k0);
         // operand tiles: tf32 hi / lo parts in the canonical layout (a 16-byte core-matrix row holds
-        // 4 consecutive k of one row); columns beyond kc are zero
-#pragma unroll 2
-        for (int e = tid; e < TC_M * (TC_KC / 4); e += 128) {
-            const int r = e / (TC_KC / 4), k = (e % (TC_KC / 4)) * 4;
-            const float4 v = (p0 + r < np && k < kc) ? __ldg(reinterpret_cast<const float4*>(X + (p0 + r) * ldx + k0 + k)) : z4;
-            tc_split_store(Xhi, Xlo, tc_off(r, k, TC_M), v);
+        // 4 consecutive k of one row); columns beyond kc are zero.  Thread t stages row t of both
+        // tiles (8 chunks of 4 k), so the 8 lanes of a quarter warp write one contiguous 128-byte
+        // core matrix (no bank conflicts); all 16 loads are issued before any is converted.
+        static_assert(TC_M == 128 && TC_N == 128, "thread t stages row t");
+        constexpr int kIt = TC_KC / 4;
+        float4 xv[kIt], av[kIt];
+        const bool xr_ok = p0 + tid < np, ar_ok = f0 + tid < nf;
+        const float* xrow = X + (p0 + tid) * ldx + k0;
+        const float* arow = A + (int64_t)(f0 + tid) * lda + k0;
+#pragma unroll
+        for (int u = 0; u < kIt; ++u) {
+            xv[u] = (xr_ok && 4 * u < kc) ? __ldg(reinterpret_cast<const float4*>(xrow + 4 * u)) : z4;
+            av[u] = (ar_ok && 4 * u < kc) ? __ldg(reinterpret_cast<const float4*>(arow + 4 * u)) : z4;
         }
-#pragma unroll 2
-        for (int e = tid; e < TC_N * (TC_KC / 4); e += 128) {
-            const int r = e / (TC_KC / 4), k = (e % (TC_KC / 4)) * 4;
-            const float4 v = (f0 + r < nf && k < kc) ? __ldg(reinterpret_cast<const float4*>(A + (int64_t)(f0 + r) * lda + k0 + k)) : z4;
-            tc_split_store(Ahi, Alo, tc_off(r, k, TC_N), v);
-            // the 8 lanes holding row r's chunk sum its squares; one of them adds (each row has one
-            // writer per chunk)
-            float sq = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-            sq += __shfl_xor_sync(kFull, sq, 1);
-            sq += __shfl_xor_sync(kFull, sq, 2);
-            sq += __shfl_xor_sync(kFull, sq, 4);
-            if ((e & 7) == 0) fsq[r] += sq;
+        float sq = 0.0f;
+#pragma unroll
+        for (int u = 0; u < kIt; ++u) {
+            tc_split_store(Xhi, Xlo, tc_off(tid, 4 * u, TC_M), xv[u]);
+            tc_split_store(Ahi, Alo, tc_off(tid, 4 * u, TC_N), av[u]);
+            sq += av[u].x * av[u].x + av[u].y * av[u].y + av[u].z * av[u].z + av[u].w * av[u].w;
         }
+        fsq[tid] += sq;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the tiles, to the tensor core
         __syncthreads();
         if (tid == 0) {
@@ -178,23 +180,27 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
               "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)cb));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        uint32_t bits = 0;
+        uint32_t bits = 0, inband = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             const float a = __uint_as_float(v[j]);
-            const float band = fsq[cb + j];
-            if (a >= 0.0f) bits |= 1u << j;
-            if (fabsf(a) < band && p < np && f0 + cb + j < nf) {
-                const uint32_t slot = atomicAdd(&nfb, 1u);
-                if (slot < (uint32_t)kTcFallback) {
-                    fbl[slot] = ((uint32_t)rl << 16) | (uint32_t)(cb + j);
-                } else {
-                    const float* xr = X + p * ldx;
-                    const float* ar = A + (int64_t)(f0 + cb + j) * lda;
-                    float acc = 0.0f;
-                    for (int t = 0; t < kdim; ++t) acc = fmaf(__ldg(xr + t), __ldg(ar + t), acc);
-                    bits = (bits & ~(1u << j)) | ((acc >= 0.0f ? 1u : 0u) << j);
-                }
+            bits |= (a >= 0.0f ? 1u : 0u) << j;
+            inband |= (fabsf(a) < fsq[cb + j] ? 1u : 0u) << j;
+        }
+        if (p >= np) inband = 0;
+        if (f0 + cb + 32 > nf) inband &= (f0 + cb >= nf) ? 0u : ((1u << (nf - f0 - cb)) - 1u);
+        while (inband) {   // rare: listed for the chain pass below (evaluated here if the list is full)
+            const int j = __ffs(inband) - 1;
+            inband &= inband - 1;
+            const uint32_t slot = atomicAdd(&nfb, 1u);
+            if (slot < (uint32_t)kTcFallback) {
+                fbl[slot] = ((uint32_t)rl << 16) | (uint32_t)(cb + j);
+            } else {
+                const float* xr = X + p * ldx;
+                const float* ar = A + (int64_t)(f0 + cb + j) * lda;
+                float acc = 0.0f;
+                for (int t = 0; t < kdim; ++t) acc = fmaf(__ldg(xr + t), __ldg(ar + t), acc);
+                bits = (bits & ~(1u << j)) | ((acc >= 0.0f ? 1u : 0u) << j);
             }
         }
         obits[rl][cb >> 5] = bits;
@@ -211,7 +217,10 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
         else atomicAnd(&obits[r][j >> 5], ~(1u << (j & 31)));
     }
     __syncthreads();
-    if (p < np) {
+    if (p < np && f0 + TC_N <= nf && ((out_ld | (f0 >> 3)) & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+        // a whole 128-function tile, 16-byte aligned: one 128-bit store per row
+        *reinterpret_cast<uint4*>(out + p * out_ld + (f0 >> 3)) = make_uint4(obits[rl][0], obits[rl][1], obits[rl][2], obits[rl][3]);
+    } else if (p < np) {
 #pragma unroll
         for (int w = 0; w < TC_N / 32; ++w) {
             const uint32_t bits = obits[rl][w];

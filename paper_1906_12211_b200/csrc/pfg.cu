@@ -581,7 +581,7 @@ void launch_mc(const float* XY, int ld, int64_t npairs, const Geo& g, const uint
 }
 
 #ifndef PFG_HP_TC
-#define PFG_HP_TC 0   // 1: SimHash bits / sketches on tcgen05 (3xTF32 + exact band, kernels_tc.cuh)
+#define PFG_HP_TC 1   // SimHash bits / sketches on tcgen05 (3xTF32 + exact band, kernels_tc.cuh); 0: the SIMT GEMM
 #endif
 void hp_bits(const float* X, int64_t np, int ldx, const float* A, int nf, int lda, int kdim, uint8_t* out,
              int64_t out_ld, cudaStream_t st) {
