@@ -543,6 +543,23 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
         // 16 KB of traffic for a small set)
         uint4* hsv = reinterpret_cast<uint4*>(rs.hsave + q * (int64_t)kHC);
         const bool saved = (fl & kFlagSaved) != 0;
+        // k_scan left the passing candidates of tile t at [t*kTile, t*kTile + tcnt[t]), in order;
+        // a batch is kCPre/4 consecutive tiles.  The tile counts (at most 64 tiles) are read once,
+        // and a batch's candidate words are read whole (the buffer is Ccap long; positions beyond
+        // a tile's count are masked after the load), the next batch's while this one is processed
+        constexpr int kTPB = kCPre * 32 / kTile;
+        const uint32_t* tcnt = rs.tcnt + q * (int64_t)(rs.Ccap / kTile);
+        const uint32_t tw0 = lane < ntl ? tcnt[lane] : 0u;
+        const uint32_t tw1 = lane + 32 < ntl ? tcnt[lane + 32] : 0u;
+        uint32_t vn[kCPre];
+        auto load_batch = [&](uint32_t t0) {
+#pragma unroll
+            for (int u = 0; u < kCPre; ++u) {
+                const uint32_t t = t0 + u / (kTile / 32);
+                vn[u] = t < ntl ? cand[t * kTile + (u % (kTile / 32)) * 32 + lane] : kEmpty;
+            }
+        };
+        load_batch(0);
         if (!saved) {
             for (int t = lane; t < kHC / 4; t += 32) reinterpret_cast<uint4*>(c->hs)[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
             __syncwarp();
@@ -573,31 +590,24 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
         __syncwarp();
         uint32_t ns = 0;
         bool overflow = false;
-        // k_scan left the passing candidates of tile t at [t*kTile, t*kTile + tcnt[t]), in order;
-        // a batch is kCPre/4 consecutive tiles
-        constexpr int kTPB = kCPre * 32 / kTile;
-        const uint32_t* tcnt = rs.tcnt + q * (int64_t)(rs.Ccap / kTile);
         for (uint32_t t0 = 0; t0 < ntl && !overflow; t0 += kTPB) {
             uint32_t v[kCPre], h[kCPre];
-            int rr[kCPre];
             bool found[kCPre];
             uint32_t tc[kTPB];
             int trep[kTPB];
 #pragma unroll
+            for (int u = 0; u < kCPre; ++u) v[u] = vn[u];
+            if (t0 + kTPB < ntl) load_batch(t0 + kTPB);
+#pragma unroll
             for (int b = 0; b < kTPB; ++b) {
-                const uint32_t w = (t0 + b < ntl) ? tcnt[t0 + b] : 0u;
-                tc[b] = w & 0xffffu;
+                const uint32_t t = t0 + b;   // warp-uniform
+                const uint32_t w = t < 32 ? __shfl_sync(kFull, tw0, t & 31) : __shfl_sync(kFull, tw1, t & 31);
+                tc[b] = t < ntl ? (w & 0xffffu) : 0u;
                 trep[b] = (int)(w >> 16);
             }
 #pragma unroll
-            for (int u = 0; u < kCPre; ++u) {
-                const int b = u / (kTile / 32);
-                const uint32_t o = (u % (kTile / 32)) * 32 + lane;
-                const bool live = o < tc[b];
-                const uint32_t g = (t0 + b) * kTile + o;
-                v[u] = live ? cand[g] : kEmpty;
-                rr[u] = live ? trep[b] : -1;
-            }
+            for (int u = 0; u < kCPre; ++u)
+                if ((u % (kTile / 32)) * 32 + lane >= tc[u / (kTile / 32)]) v[u] = kEmpty;
             // membership in the set as it stands before this batch: independent read-only probes
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
@@ -632,13 +642,17 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                         hh = hs_next(hh);
                     }
                 }
-                if (rr[u] >= 0) {
-                    atomicAdd(&c->fcnt[rr[u]], 1u);  // passing the filter (filtered = emitted - passing)
-                    if (!fresh) atomicAdd(&c->dcnt[rr[u]], 1u);
-                }
                 const uint32_t fm = __ballot_sync(kFull, fresh);
                 if (fresh) E[nE + ns + __popc(fm & lanemask_lt())] = v[u];
                 ns += __popc(fm);
+                // the step's live lanes are positions of one tile (one repetition): its duplicates
+                // are the live lanes that claimed nothing
+                const int b = u / (kTile / 32);
+                const uint32_t live = min(32u, tc[b] - (uint32_t)((u % (kTile / 32)) * 32));
+                if (lane == 0) {
+                    if (u % (kTile / 32) == 0) c->fcnt[trep[b]] += tc[b];  // passing the filter (filtered = emitted - passing)
+                    c->dcnt[trep[b]] += live - __popc(fm);
+                }
             }
             if (nE + ns > rs.hmax) overflow = true;
         }

@@ -1549,7 +1549,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     // without host synchronisation.
     const int max_rounds = s.rounds > 0 ? s.rounds : 5;
     const int ecap = 2048;  // evaluated-list stride: kHMax committed + one batch of slack
-    const int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
+    constexpr int ccap = 8192;  // emitted positions of one query's chunk (more: the fused kernel takes it)
+    static_assert(ccap / kTile <= 64, "k_dedupe holds a chunk's tile counts in two words per lane");
     const uint32_t pool_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1 << 20, nq * 1024), (int64_t)1 << 30);
     int64_t wide_max = 0;   // visit-tag arrays this search may use
     bool want_wide = false;

@@ -20,13 +20,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--recall", type=float, default=0.9)
+ap.add_argument("--storage", default="f32", choices=["f32", "i16"])
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 dev = torch.device("cuda:0")
 data, q = synth.config_data(a.config)
 X = torch.from_numpy(data).to(dev)
 Q = torch.from_numpy(q).to(dev)
-opts = dict(strategy=c["strategy"])
+opts = dict(strategy=c["strategy"], storage=a.storage)
 if c["reps"]:
     opts["reps"] = c["reps"]
 idx = pfg.Index(X, c["budget"] or 0, c["family"], seed=1, **opts)
