@@ -608,20 +608,22 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
 #pragma unroll
             for (int u = 0; u < kCPre; ++u)
                 if ((u % (kTile / 32)) * 32 + lane >= tc[u / (kTile / 32)]) v[u] = kEmpty;
-            // membership in the set as it stands before this batch: independent read-only probes
+            // membership in the set as it stands before this batch: independent read-only probes,
+            // the home slots of the whole batch loaded first
+            uint32_t x[kCPre];
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
-                found[u] = false;
-                if ((uint32_t)((u % (kTile / 32)) * 32) >= tc[u / (kTile / 32)]) { h[u] = 0; continue; }  // empty step
                 h[u] = hs_slot(v[u]);
-                if (v[u] != kEmpty) {
-                    for (;;) {
-                        const uint32_t x = c->hs[h[u]];
-                        if (x == v[u]) { found[u] = true; break; }
-                        if (x == kEmpty) break;
+                x[u] = v[u] != kEmpty ? c->hs[h[u]] : kEmpty;
+            }
+#pragma unroll
+            for (int u = 0; u < kCPre; ++u) {
+                if (v[u] != kEmpty)
+                    while (x[u] != kEmpty && x[u] != v[u]) {
                         h[u] = hs_next(h[u]);
+                        x[u] = c->hs[h[u]];
                     }
-                }
+                found[u] = v[u] != kEmpty && x[u] == v[u];
             }
             // claims of the rest in (repetition, position) order, u in order; a later occurrence
             // of an id claimed earlier in the batch finds it in the set
