@@ -34,7 +34,7 @@ namespace pfg {
 constexpr int kHC = PFG_HC;   // per-warp shared-memory hash set of evaluated ids (slots)
 constexpr int kHMax = kHC * 3 / 4;  // beyond this many evaluated ids a query switches to the global bitmap
 constexpr int kSB = PFG_SB;   // survivor buffer (evaluated ids awaiting their similarity)
-constexpr int kRPI = 8;       // candidate rows read per warp iteration (memory-level parallelism)
+constexpr int kRPI = 16;      // candidate rows read per warp step of k_sims (rows in flight: the kernel's bound)
 constexpr int kU = 4;         // table positions per lane per scan step
 constexpr int kMaxR = 32;     // max repetitions per chunk
 constexpr int kMaxK = 256;    // max k
