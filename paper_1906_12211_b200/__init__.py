@@ -58,7 +58,7 @@ class SearchOpts(C.Structure):
                 ("rounds", C.c_int32), ("wide", C.c_int32), ("tau_rule", C.c_int32), ("rerank", C.c_int32),
                 ("loop_min", C.c_int32), ("loop_max", C.c_int32), ("wide_arrays", C.c_int32),
                 ("wide_tiles_min", C.c_int32), ("ext_codes", C.c_void_p), ("ext_reps", C.c_int32),
-                ("ext_sketches", C.c_void_p)]
+                ("ext_sketches", C.c_void_p), ("pipelines", C.c_int32)]
 
 
 class IndexInfo(C.Structure):
@@ -246,7 +246,7 @@ class Index:
     def _sopts(rep_chunk=DEFAULT_REP_CHUNK, segment=12, stop_rule=0, per_round=False, use_filter=True, eps=0.0,
                trace_cap=0, trace_ptr=None, timing=False, engine=0, uniform_chunks=False, rounds=0,
                wide=0, tau_rule=0, rerank=True, loop_min=0, loop_max=0, wide_arrays=0,
-               wide_tiles_min=False, ext_codes=None, ext_sketches=None) -> SearchOpts:
+               wide_tiles_min=False, ext_codes=None, ext_sketches=None, pipelines=0) -> SearchOpts:
         o = SearchOpts()
         o.struct_size = C.sizeof(SearchOpts)
         o.rep_chunk, o.segment, o.stop_rule = rep_chunk, segment, stop_rule
@@ -264,6 +264,7 @@ class Index:
         o.rerank = 0 if rerank else -1
         o.loop_min, o.loop_max, o.wide_arrays = int(loop_min), int(loop_max), int(wide_arrays)
         o.wide_tiles_min = int(wide_tiles_min)
+        o.pipelines = int(pipelines)
         if ext_codes is not None:   # device tensors [nq, reps] uint32 (int32 view) / [nq, M] uint64 (int64 view)
             assert _is_torch(ext_codes) and ext_codes.is_cuda and ext_codes.is_contiguous()
             o.ext_codes, o.ext_reps = ext_codes.data_ptr(), int(ext_codes.shape[1])

@@ -263,35 +263,23 @@ __global__ void __launch_bounds__(256) k_fht_rep(const float* __restrict__ X, in
 // registers; a stage h >= H pairs coordinate u of lane g with u + h of lane g + h/H (the lower lane
 // keeps a + b, the upper a - b: the oracle's butterfly, same operands, same rounding).  The argmax
 // combines the lanes' winners with ties to the lower index (R-6).
+// The concatenated FHT-CP codes of one repetition (functions sf[0 .. c), ell bits each, first most
+// significant) of the row xr (lim valid floats, zero beyond; 16-byte aligned, global or shared
+// memory) by a group of TPF lanes g = 0 .. TPF-1 (see k_fht_qcodes_g).  All lanes of the group call.
 template <int DP, int TPF>
-__global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
-                                                      int c, int K, const uint32_t* __restrict__ sg, int nreps,
-                                                      uint32_t* __restrict__ codes, int ldc,
-                                                      const uint32_t* __restrict__ qlist, int r0,
-                                                      const uint32_t* __restrict__ np_dev) {
-    // rows: qlist[0..np) if given, else 0..np-1; repetitions r0 .. r0 + nreps - 1
+__device__ __forceinline__ uint64_t fhtcp_rep_full(const float* xr, int lim, const uint32_t* __restrict__ sg_rep, int c,
+                                                   int ell, int g) {
     constexpr int H = DP / TPF, W = (DP + 31) / 32;
     static_assert(H % 32 == 0 || TPF == 1, "a lane holds whole sign words");
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int g = (int)(t % TPF);
-    int64_t item = t / TPF;
-    if (np_dev) np = min(np, (int64_t)*np_dev);   // rows counted on the device (a list's length)
-    const bool live = item < np * nreps;
-    if (__all_sync(kFull, !live)) return;  // the whole warp is past the end (grids sized for the maximum)
-    if (!live) item = 0;  // keep the group's lanes in the shuffles; nothing is stored
-    const int64_t a = item / nreps;
-    const int64_t p = qlist ? (int64_t)qlist[a] : a;
-    const int j = r0 + (int)(item % nreps);
-    const float* xr = X + p * ldx;
     uint64_t full = 0;
     for (int f = 0; f < c; ++f) {
-        const uint32_t* sf = sg + ((int64_t)j * c + f) * 3 * W;
+        const uint32_t* sf = sg_rep + (int64_t)f * 3 * W;
         float y[H];
-        // rows are ldx floats, zero beyond d (k_normalize), 16-byte aligned: 128-bit loads
+        // rows are zero beyond d (k_normalize), 16-byte aligned: 128-bit loads
 #pragma unroll
         for (int i = 0; i < H; i += 4) {
             const int u = g * H + i;
-            const float4 v = (u < ldx) ? __ldg(reinterpret_cast<const float4*>(xr + u)) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            const float4 v = (u < lim) ? *reinterpret_cast<const float4*>(xr + u) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             y[i] = v.x; y[i + 1] = v.y; y[i + 2] = v.z; y[i + 3] = v.w;
         }
 #pragma unroll 1
@@ -340,7 +328,63 @@ __global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ 
         }
         full = (full << ell) | (((uint32_t)(bv < 0.0f) << (ell - 1)) | (uint32_t)bi);
     }
+    return full;
+}
+
+template <int DP, int TPF>
+__global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
+                                                      int c, int K, const uint32_t* __restrict__ sg, int nreps,
+                                                      uint32_t* __restrict__ codes, int ldc,
+                                                      const uint32_t* __restrict__ qlist, int r0,
+                                                      const uint32_t* __restrict__ np_dev) {
+    // rows: qlist[0..np) if given, else 0..np-1; repetitions r0 .. r0 + nreps - 1
+    constexpr int W = (DP + 31) / 32;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = (int)(t % TPF);
+    int64_t item = t / TPF;
+    if (np_dev) np = min(np, (int64_t)*np_dev);   // rows counted on the device (a list's length)
+    const bool live = item < np * nreps;
+    if (__all_sync(kFull, !live)) return;  // the whole warp is past the end (grids sized for the maximum)
+    if (!live) item = 0;  // keep the group's lanes in the shuffles; nothing is stored
+    const int64_t a = item / nreps;
+    const int64_t p = qlist ? (int64_t)qlist[a] : a;
+    const int j = r0 + (int)(item % nreps);
+    const uint64_t full = fhtcp_rep_full<DP, TPF>(X + p * ldx, ldx, sg + (int64_t)j * c * 3 * W, c, ell, g);
     if (live && g == 0) codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
+}
+
+// Build-side FHT-CP repetition keys (independent strategy): a block stages RB = 128/TPF rows in
+// shared memory (coalesced; row stride S floats with S/4 odd, so the lanes' 128-bit reads do not
+// conflict) and loops over repetitions r0 .. r0 + nreps - 1, one lane group per (row, repetition):
+// the sign words are the same for the whole block (broadcast) and each repetition's keys
+// {code << 32 | p} are written coalesced.  Same arithmetic as k_fht_rep / the oracle (R-6).
+template <int DP, int TPF>
+__global__ void __launch_bounds__(128) k_fht_keys(const float* __restrict__ X, int64_t np, int ldx, int dpad, int S,
+                                                  int ell, int c, int K, const uint32_t* __restrict__ sg, int r0,
+                                                  int nreps, uint64_t* __restrict__ keys, uint32_t* __restrict__ codes,
+                                                  int ldc) {
+    constexpr int RB = 128 / TPF, W = (DP + 31) / 32;
+    extern __shared__ __align__(16) float xs[];
+    const int64_t p0 = (int64_t)blockIdx.x * RB;
+    const int q4 = dpad / 4;
+    for (int i = threadIdx.x; i < RB * q4; i += blockDim.x) {
+        const int r = i / q4, u = (i - r * q4) * 4;
+        const float4 v = p0 + r < np ? __ldg(reinterpret_cast<const float4*>(X + (p0 + r) * ldx + u))
+                                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        *reinterpret_cast<float4*>(xs + r * S + u) = v;
+    }
+    __syncthreads();
+    const int lr = threadIdx.x / TPF, g = threadIdx.x % TPF;
+    const int64_t p = p0 + lr;
+    for (int r = 0; r < nreps; ++r) {
+        const int j = r0 + r;
+        const uint64_t full = fhtcp_rep_full<DP, TPF>(xs + lr * S, dpad, sg + (int64_t)j * c * 3 * W, c, ell, g);
+        const uint32_t code = (uint32_t)(full >> (c * ell - K));
+        if (g == 0 && p < np) {
+            if (keys) keys[(int64_t)r * np + p] = ((uint64_t)code << 32) | (uint64_t)p;
+            if (codes) codes[p * ldc + j] = code;
+        }
+    }
 }
 
 // FHT-CP codes of the m pool functions for every row: out [p][m] (uint16)

@@ -1243,6 +1243,15 @@ __global__ void k_split(QueryParams p, int par, uint32_t lmin, uint32_t lmax) {
         push(rs.fused, &rs.ctl->nfused, q);
     }
 }
+// two round pipelines (pfg.cu pipeline_params): pipeline 1's control-block counters added to
+// pipeline 0's, which the host reads back as the search's
+__global__ void k_ctl_fold(RoundCtl* c) {
+    RoundCtl& a = c[0];
+    const RoundCtl& b = c[1];
+    a.nfused += b.nfused; a.nfused2 += b.nfused2; a.wnext += b.wnext; a.wdefer += b.wdefer;
+    a.round = max(a.round, b.round);
+    a.evsum += b.evsum; a.emsum += b.emsum; a.sims_rows += b.sims_rows; a.sims_rows_blind += b.sims_rows_blind;
+}
 // loop condition: queries left, and either a wide one among them or at least lmin
 __device__ __forceinline__ bool loop_more(const RoundCtl* c, int par, uint32_t lmin) {
     const uint32_t n = c->nact[par];

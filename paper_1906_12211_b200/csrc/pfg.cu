@@ -358,6 +358,7 @@ struct SearchCfg {
     int tau_rule = 0;   // 0: binomial quantile (R-26), 1: (1 + eps) x expected distance (R-15)
     int rerank = 1;     // PFG_STORAGE_I16: re-score each query's top-k in fp32
     int loop_min = 0, loop_max = 0, wide_arrays = 0, wide_tiles_min = 0;  // device-side loop policy (tests)
+    int pipelines = 0;  // engine 0: round pipelines (0 = automatic, 1, 2)
     ExtHash ext;        // precomputed query codes / sketches (SURVEY 8(e) distributed preparation)
     float eps = 0.0f;
     uint32_t* trace_ids = nullptr;
@@ -406,6 +407,8 @@ pfg_status resolve_sopts(const pfg_search_opts* o, SearchCfg& s) {
     if (s.tau_rule != 0 && s.tau_rule != 1) return fail(PFG_E_ARG, "tau_rule must be 0 (quantile) or 1 (expected distance)");
     s.uniform = z.uniform_chunks;
     if (s.uniform != 0 && s.uniform != 1) return fail(PFG_E_ARG, "uniform_chunks must be 0 or 1");
+    s.pipelines = z.pipelines;
+    if (s.pipelines < 0 || s.pipelines > 2) return fail(PFG_E_ARG, "pipelines must be 0 (automatic), 1 or 2");
     if (s.trace_cap < 0 || (s.trace_cap > 0 && !s.trace_ids)) return fail(PFG_E_ARG, "trace_cap > 0 needs trace_ids");
     return PFG_OK;
 }
@@ -456,6 +459,8 @@ struct pfg_index {
     int qb_depth = 64;           // level-K match ranges precomputed per query (non-lazy families; tuned)
     cudaStream_t aux = nullptr;  // second stream: query sketches run beside the query hashing
     cudaStream_t aux2 = nullptr; // third stream: codes and ranges of the later eager repetitions
+    cudaStream_t st1 = nullptr;  // the second round pipeline (the upper half of the batch)
+    cudaEvent_t ev_h1start = nullptr, ev_h1end = nullptr;  // fork to / join from st1
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_late = nullptr;
     bool late_pending = false;   // codes/ranges of repetitions [split, eager) still on aux2
     cudaEvent_t ev_mid = nullptr;
@@ -511,6 +516,9 @@ struct pfg_index {
         if (ev_join) cudaEventDestroy(ev_join);
         if (aux) cudaStreamDestroy(aux);
         if (aux2) cudaStreamDestroy(aux2);
+        if (st1) cudaStreamDestroy(st1);
+        for (cudaEvent_t e : {ev_h1start, ev_h1end})
+            if (e) cudaEventDestroy(e);
         if (ev_late) cudaEventDestroy(ev_late);
         if (ev_mid) cudaEventDestroy(ev_mid);
         if (ev_zmin) cudaEventDestroy(ev_zmin);
@@ -531,7 +539,7 @@ void tl_mark(pfg_index* I, const char* name, cudaStream_t st);
 constexpr int kQBMax = 96;     // level-K match ranges precomputed for at most this many repetitions
 constexpr int kExtReps = 32;   // repetitions hashed in bulk for the queries the fused kernel resumes
 pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
-                     const uint32_t* nrows_dev = nullptr);
+                     const uint32_t* nrows_dev = nullptr, int64_t q0 = 0);
 #ifndef PFG_QTPF
 #define PFG_QTPF 1   // threads per function of the eager FHT-CP query hashing at d' = 128
 #endif
@@ -543,8 +551,29 @@ void launch_fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uin
     const int blocks = (int)((warps * 32 + 255) / 256);
     k_fht_rep<EPL><<<blocks, 256, 0, st>>>(X, np, ldx, g.d, g.dp, g.ell, g.c, g.K, sg, r0, nreps, keys, codes, ldc);
 }
+template <int DP, int TPF>
+void launch_fht_keys(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps,
+                     uint64_t* keys, uint32_t* codes, int ldc, cudaStream_t st) {
+    constexpr int RB = 128 / TPF;
+    const int S = (g.dpad / 4) % 2 ? g.dpad : g.dpad + 4;   // S/4 odd: conflict-free 128-bit reads
+    const size_t sm = (size_t)RB * S * 4;
+    set_smem((const void*)k_fht_keys<DP, TPF>, sm);
+    k_fht_keys<DP, TPF><<<(unsigned)((np + RB - 1) / RB), 128, sm, st>>>(X, np, ldx, g.dpad, S, g.ell, g.c, g.K, sg, r0,
+                                                                         nreps, keys, codes, ldc);
+}
 void fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps, uint64_t* keys,
              uint32_t* codes, int ldc, int num_sms, cudaStream_t st) {
+    // d' = 32 .. 1024: a lane group of max(1, d'/128) lanes (16 at 1024) per (row, repetition), rows staged in
+    // shared memory (k_fht_keys); otherwise one warp per row
+    switch (g.dp) {
+        case 32: return launch_fht_keys<32, 1>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, st);
+        case 64: return launch_fht_keys<64, 1>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, st);
+        case 128: return launch_fht_keys<128, 1>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, st);
+        case 256: return launch_fht_keys<256, 2>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, st);
+        case 512: return launch_fht_keys<512, 4>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, st);
+        case 1024: return launch_fht_keys<1024, 16>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, st);
+        default: break;
+    }
     switch (std::max(1, g.dp / 32)) {
         case 1: launch_fht_rep<1>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
         case 2: launch_fht_rep<2>(X, np, ldx, g, sg, r0, nreps, keys, codes, ldc, num_sms, st); break;
@@ -1019,6 +1048,9 @@ pfg_status ensure_streams(pfg_index* I) {
     if (I->aux) return PFG_OK;
     PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
     PFG_CUDA(cudaStreamCreateWithFlags(&I->aux2, cudaStreamNonBlocking));
+    PFG_CUDA(cudaStreamCreateWithFlags(&I->st1, cudaStreamNonBlocking));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_h1start, cudaEventDisableTiming));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_h1end, cudaEventDisableTiming));
     PFG_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
     PFG_CUDA(cudaEventCreateWithFlags(&I->ev_join, cudaEventDisableTiming));
     PFG_CUDA(cudaEventCreateWithFlags(&I->ev_late, cudaEventDisableTiming));
@@ -1149,14 +1181,15 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
 // FHT-CP query codes of repetitions [r0, r0 + nreps) for rows qlist[0..nrows) (or 0..nrows-1),
 // one thread per (row, repetition), into qcodes [q][ld]
 pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
-                     const uint32_t* nrows_dev) {
+                     const uint32_t* nrows_dev, int64_t q0) {
+    // q0: rows (and qlist entries) relative to query q0 (a round pipeline's part of the batch)
     const Geo& g = I->g;
     const int64_t threads = nrows * nreps;
     if (threads == 0) return PFG_OK;
     const unsigned blocks = (unsigned)((threads + 127) / 128);
     const uint32_t* sg = I->sg.as<uint32_t>();
-    uint32_t* qc = I->qcodes.as<uint32_t>();
-    const float* X = I->qx.as<float>();
+    uint32_t* qc = I->qcodes.as<uint32_t>() + q0 * ld;
+    const float* X = I->qx.as<float>() + q0 * g.dpad;
     if (g.dp == 32) k_fht_qcodes_g<32, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
     else if (g.dp == 64) k_fht_qcodes_g<64, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
     else k_fht_qcodes_g<128, PFG_QTPF><<<(unsigned)((PFG_QTPF * threads + 127) / 128), 128, 0, st>>>(
@@ -1281,6 +1314,43 @@ pfg_status late_join(pfg_index* I, cudaStream_t st) {
         I->late_pending = false;
     }
     return PFG_OK;
+}
+
+// The parameters of round pipeline h, which runs queries [q0, q0 + nh) of the batch as a search
+// of its own: every per-query array is offset to row q0 (query ids in the lists are relative to
+// q0), and the per-round shared state (control block, survivor pool, work counter, the fused
+// kernel's bitmap slots) is pipeline h's share.  The two pipelines touch disjoint memory.
+QueryParams pipeline_params(const QueryParams& p, int64_t q0, int64_t nh, int h, int64_t slots_h) {
+    QueryParams s = p;
+    s.nq = nh;
+    s.qx = p.qx + q0 * p.dpad;
+    if (p.qx16) s.qx16 = p.qx16 + q0 * p.dpad16;
+    if (p.qsk) s.qsk = p.qsk + q0 * p.M;
+    if (p.qcodes) s.qcodes = p.qcodes + q0 * p.qc_ld;
+    if (p.qbnd) s.qbnd = p.qbnd + q0 * p.qb_ld;
+    s.qzero = p.qzero + q0;
+    s.cur = p.cur + q0 * p.L;
+    s.out_ids = p.out_ids + q0 * p.k;
+    s.out_sims = p.out_sims + q0 * p.k;
+    if (p.stats) s.stats = p.stats + q0;
+    if (p.trace_ids) s.trace_ids = p.trace_ids + q0 * p.trace_cap;
+    s.work = p.work + h;
+    s.bitmap = p.bitmap + h * slots_h * p.bm_words;
+    s.claims = p.claims + h * slots_h * (int64_t)p.claim_cap;
+    RoundState& r = s.rs;
+    const RoundState& a = p.rs;
+    r.lvl = a.lvl + q0; r.c0 = a.c0 + q0; r.flags = a.flags + q0; r.tn = a.tn + q0;
+    r.cnt = a.cnt + q0 * kCnt; r.T = a.T + q0 * p.kt; r.E = a.E + q0 * a.Ecap; r.pend = a.pend + q0 * kMaxR;
+    r.cand = a.cand + q0 * a.Ccap; r.tcnt = a.tcnt + q0 * (a.Ccap / kTile); r.hsave = a.hsave + q0 * kHC;
+    r.rinfo = a.rinfo + q0; r.tiles = a.tiles + q0 * (a.Ccap / kTile) * 2; r.repcnt = a.repcnt + q0 * kMaxR * 3;
+    r.poff = a.poff + q0; r.pn = a.pn + q0;
+    r.act[0] = a.act[0] + q0; r.act[1] = a.act[1] + q0; r.dord[0] = a.dord[0] + q0; r.dord[1] = a.dord[1] + q0;
+    r.fused = a.fused + q0; r.fused2 = a.fused2 + q0; r.wslot = a.wslot + q0; r.rtile = a.rtile + q0 * (kMaxR + 1);
+    r.pool_cap = a.pool_cap / 2;
+    r.pool_id = a.pool_id + h * (int64_t)r.pool_cap; r.pool_q = a.pool_q + h * (int64_t)r.pool_cap;
+    r.pool_key = a.pool_key + h * (int64_t)r.pool_cap;
+    r.ctl = a.ctl + h;
+    return s;
 }
 
 template <int EPL>
@@ -1566,7 +1636,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         // it fills the next)
         PFG_TRY(I->rs_pool_id.ensure((size_t)pool_cap * 8, "pool")); PFG_TRY(I->rs_pool_q.ensure((size_t)pool_cap * 8, "pool"));
         PFG_TRY(I->rs_pool_key.ensure((size_t)pool_cap * 16, "pool"));
-        PFG_TRY(I->rs_ctl.ensure(sizeof(RoundCtl), "rs control")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
+        PFG_TRY(I->rs_ctl.ensure(2 * sizeof(RoundCtl), "rs control")); PFG_TRY(I->rs_poff.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_pn.ensure(N * 4, "rs")); PFG_TRY(I->rs_act0.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_act1.ensure(N * 4, "rs")); PFG_TRY(I->rs_fused.ensure(N * 4, "rs"));
         PFG_TRY(I->rs_cand.ensure(N * ccap * 4, "rs candidates"));
@@ -1624,8 +1694,15 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             }
         }
     }
-    PFG_TRY(I->work.ensure(8, "work counter"));
-    PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 8, st));
+    PFG_TRY(I->work.ensure(16, "work counters"));
+    PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 16, st));
+    // two round pipelines (pipelines option): the lower and the upper half of the batch run as two
+    // searches of their own on st and st1, so that one half's latency-bound control phases overlap
+    // the other half's candidate-row reads.  Not with wide queries / the device-side loop (the
+    // loop graph is per search) or exact CP's partial eager hashing (bulk codes per fused list).
+    const int64_t lmax_cfg = s.loop_max > 0 ? s.loop_max : (I->loop_heavy ? 1 : 0);
+    const bool halves = rounds && !chunk_eng && s.engine == 0 && !want_wide && lmax_cfg == 0 && cp_eager == 0 &&
+                        (s.pipelines == 2 ? nq >= 2 : (s.pipelines == 0 && nq >= 4096));
 
     const bool ids_dev = is_device_ptr(out_ids), sims_dev = is_device_ptr(out_sims);
     const bool stats_dev = stats ? is_device_ptr(stats) : true;
@@ -1749,10 +1826,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         r.wcap = wide_on ? (uint32_t)I->wc_cap : 0u;
         r.hmax = s.wide > 0 ? (uint32_t)s.wide : (uint32_t)kHMax;
         r.pool_stride = chunk_eng ? pool_cap : 0u;
-        PFG_CUDA(cudaMemsetAsync(r.ctl, 0, sizeof(RoundCtl), st));
-        k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, (uint32_t)(0xFFFEu - I->wepoch) << 16);
+        PFG_CUDA(cudaMemsetAsync(r.ctl, 0, 2 * sizeof(RoundCtl), st));
+        if (!halves) {
+            k_rinit<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(p, (uint32_t)(0xFFFEu - I->wepoch) << 16);
+            I->launches += 1;
+        }
         PFG_CUDA(cudaGetLastError());
-        I->launches += 1;
     }
     if (chunk_eng) {
         // the chunk engine: per round k_chunk (CTA per query: merge, expand, scan, dedupe) and
@@ -1861,15 +1940,20 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         // device-side counts, so no host synchronisation is needed between rounds)
         const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * 16));
         const unsigned qb_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nq + 3) / 4, (int64_t)I->num_sms * std::max(1, docc)));
-        const unsigned qb_m = qb_e;
+        const unsigned qb_m = qb_e;   // (the loop graph's key)
         const unsigned tb_s = (unsigned)(I->num_sms * 8);
         const unsigned sb = (unsigned)(I->num_sms * PFG_SIMS_MINB);
         int round = 0;
         const bool tm = s.timing == 2;
         const bool ksims_timed = s.timing == 3;
         // one round: expand, scan, dedupe, sims, merge of list `par` (phase events unless captured)
-        auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp) -> pfg_status {
+        // blind: a round outside the captured loop (counted in sims_rows_blind, timed with timing = 3);
+        // m: the queries of the pipeline (grid sizes)
+        auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp, bool blind, int64_t m) -> pfg_status {
             using PP = decltype(pp);
+            const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 3) / 4, (int64_t)I->num_sms * 16));
+            const unsigned qb_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 3) / 4, (int64_t)I->num_sms * std::max(1, docc)));
+            const unsigned qb_m = qb_e;
             PFG_TRY(phase_mark(I, marks, kPhExpand, rst));
             switch (epl) {
                 case 1: k_expand<1, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
@@ -1879,16 +1963,16 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 case 16: k_expand<16, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
                 default: k_expand<32, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
             }
-            if (rst == st) { PFG_TRY(dbg_sync("k_expand")); tl_mark(I, "k_expand", st); }
+            if (blind) { PFG_TRY(dbg_sync("k_expand")); tl_mark(I, "k_expand", rst); }
             PFG_TRY(phase_mark(I, marks, kPhScan, rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_scan<PP, true><<<tb_s, 256, 0, rst>>>(pp, par);
             else k_scan<PP, false><<<tb_s, 256, 0, rst>>>(pp, par);
-            if (rst == st) { PFG_TRY(dbg_sync("k_scan")); tl_mark(I, "k_scan", st); }
+            if (blind) { PFG_TRY(dbg_sync("k_scan")); tl_mark(I, "k_scan", rst); }
             PFG_TRY(phase_mark(I, marks, kPhDedupe, rst));
             k_dedupe<PP><<<qb_d, 128, dsm, rst>>>(pp, par);
-            if (rst == st) { PFG_TRY(dbg_sync("k_dedupe")); tl_mark(I, "k_dedupe", st); }
+            if (blind) { PFG_TRY(dbg_sync("k_dedupe")); tl_mark(I, "k_dedupe", rst); }
             PFG_TRY(phase_mark(I, marks, kPhSims, rst));
-            const bool kt = ksims_timed && rst == st;
+            const bool kt = ksims_timed && blind;
             if (kt) {
                 if ((int64_t)I->kev.size() < 2 * (I->kev_n + 1)) {
                     // fold the pairs recorded so far (all earlier on this stream) before reusing them
@@ -1901,7 +1985,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 }
                 PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n], rst));
             }
-            const int sflags = rst == st ? 2 : 0;   // blind rounds (outside the captured loop)
+            const int sflags = blind ? 2 : 0;
             if (g.storage == PFG_STORAGE_I16) k_sims<PP, true><<<sb, 256, 0, rst>>>(pp, par, sflags);
             else k_sims<PP, false><<<sb, 256, 0, rst>>>(pp, par, sflags);
             if (kt) PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n++ + 1], rst));
@@ -1910,21 +1994,97 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 if (g.storage == PFG_STORAGE_I16) k_wsims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
                 else k_wsims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
             }
-            if (rst == st) { PFG_TRY(dbg_sync("k_sims")); tl_mark(I, "k_sims", st); }
+            if (blind) { PFG_TRY(dbg_sync("k_sims")); tl_mark(I, "k_sims", rst); }
             PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_merge<PP, true><<<qb_m, 128, msm, rst>>>(pp, par);
             else k_merge<PP, false><<<qb_m, 128, msm, rst>>>(pp, par);
-            if (rst == st) { PFG_TRY(dbg_sync("k_merge")); tl_mark(I, "k_merge", st); }
+            if (blind) { PFG_TRY(dbg_sync("k_merge")); tl_mark(I, "k_merge", rst); }
             PFG_TRY(phase_mark(I, marks, kPhOther, rst));
             PFG_CUDA(cudaGetLastError());
             return PFG_OK;
         };
+        if (halves) {
+            // two round pipelines: queries [0, n0) on st, [n0, nq) on st1, each a search of its own
+            // (pipeline_params); the fused kernel of each takes its stragglers with half the grid
+            const int64_t n0 = nq / 2;
+            const int64_t qh0[2] = {0, n0}, nh[2] = {n0, nq - n0};
+            const int64_t slots_h = (max_blocks / 2) * 4;
+            const QueryParams ph[2] = {pipeline_params(p, 0, n0, 0, slots_h), pipeline_params(p, n0, nq - n0, 1, slots_h)};
+            const cudaStream_t sh[2] = {st, I->st1};
+            for (int h = 0; h < 2; ++h)
+                k_rinit<<<(unsigned)((nh[h] + 255) / 256), 256, 0, st>>>(ph[h], (uint32_t)(0xFFFEu - I->wepoch) << 16);
+            PFG_CUDA(cudaGetLastError());
+            I->launches += 2;
+            PFG_CUDA(cudaEventRecord(I->ev_h1start, st));
+            PFG_CUDA(cudaStreamWaitEvent(I->st1, I->ev_h1start, 0));
+            // the side streams' joins, on both pipelines' streams
+            auto join_both = [&](bool late) -> pfg_status {
+                const bool mp = I->mid_pending, lp = I->late_pending;
+                for (int h = 0; h < 2; ++h) {
+                    I->mid_pending = mp;
+                    I->late_pending = lp;
+                    PFG_TRY(join_sketches(I, sh[h]));
+                    PFG_TRY(late ? late_join(I, sh[h]) : mid_join(I, sh[h]));
+                }
+                return PFG_OK;
+            };
+            for (; round < max_rounds; ++round) {
+                if (round == 1) PFG_TRY(join_both(false));
+                if (round == 2) PFG_TRY(join_both(true));
+                for (int h = 0; h < 2; ++h) PFG_TRY(launch_round(round & 1, sh[h], tm && h == 0, ph[h], true, nh[h]));
+                I->launches += 10;
+            }
+            PFG_TRY(join_both(true));
+            const int P = round & 1;
+            for (int h = 0; h < 2; ++h) {
+                const cudaStream_t hs = sh[h];
+                const QueryParams& q = ph[h];
+                k_presplit<<<1, 1, 0, hs>>>(q, P);
+                k_split<<<(unsigned)((nh[h] + 255) / 256), 256, 0, hs>>>(q, P, 64u, 0u);
+                PFG_CUDA(cudaGetLastError());
+                I->launches += 2;
+                QueryParams p1 = q;
+                p1.qlist = q.rs.fused;
+                p1.nq_dev = &q.rs.ctl->nfused;
+                p1.resume = 1;
+                if (lazy && I->qc_n > 0 && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+                    const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
+                    PFG_TRY(fht_codes(I, nh[h], q.rs.fused, r0, nr, I->qc_ld, hs, &q.rs.ctl->nfused, qh0[h]));
+                    const int64_t thr_n = nh[h] * (int64_t)nr;
+                    k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, hs>>>(p1, I->qbnd.as<uint4>() + qh0[h] * p.qb_ld,
+                                                                            q.rs.fused, nh[h], r0, nr, &q.rs.ctl->nfused);
+                    PFG_CUDA(cudaGetLastError());
+                    I->launches += 2;
+                    p1.qc_n = p1.qb_n = I->qc_ld;
+                }
+                PFG_CUDA(cudaMemsetAsync(p1.work, 0, 8, hs));
+                const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((nh[h] + 3) / 4, max_blocks / 2));
+                switch (epl) {
+                    case 1: PFG_TRY(launch_query_t<1>(p1, (int)blocks, smem, hs, I->num_sms)); break;
+                    case 2: PFG_TRY(launch_query_t<2>(p1, (int)blocks, smem, hs, I->num_sms)); break;
+                    case 4: PFG_TRY(launch_query_t<4>(p1, (int)blocks, smem, hs, I->num_sms)); break;
+                    case 8: PFG_TRY(launch_query_t<8>(p1, (int)blocks, smem, hs, I->num_sms)); break;
+                    case 16: PFG_TRY(launch_query_t<16>(p1, (int)blocks, smem, hs, I->num_sms)); break;
+                    default: PFG_TRY(launch_query_t<32>(p1, (int)blocks, smem, hs, I->num_sms)); break;
+                }
+                I->launches += 1;
+                PFG_TRY(dbg_sync("fused (pipeline)"));
+                tl_mark(I, h ? "k_query (fused, pipeline 1)" : "k_query (fused, pipeline 0)", hs);
+            }
+            PFG_CUDA(cudaEventRecord(I->ev_h1end, I->st1));
+            PFG_CUDA(cudaStreamWaitEvent(st, I->ev_h1end, 0));
+            k_ctl_fold<<<1, 1, 0, st>>>(r.ctl);
+            PFG_CUDA(cudaGetLastError());
+            I->launches += 1;
+            fused_n = 0;
+            I->last_rounds = round;
+        } else {
         while (round < max_rounds) {
             // round 0 is the single repetition 0 with tau = 64 (no sketches read); round 1 reaches
             // repetitions < 1 + R; later rounds may reach every eager repetition
             if (round == 1) { PFG_TRY(join_sketches(I, st)); PFG_TRY(mid_join(I, st)); }
             if (round == 2) PFG_TRY(late_join(I, st));
-            PFG_TRY(launch_round(round & 1, st, tm, p));
+            PFG_TRY(launch_round(round & 1, st, tm, p, true, nq));
             I->launches += 5;
             ++round;
         }
@@ -2032,8 +2192,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 PFG_CUDA(cudaGraphAddNode(&cn, gr, &n0, 1, &cp));
                 cudaGraph_t body = cp.conditional.phGraph_out[0];
                 PFG_CUDA(cudaStreamBeginCaptureToGraph(I->cap_st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-                pfg_status ls = launch_round(P ^ 1, I->cap_st, false, dp);
-                if (ls == PFG_OK) ls = launch_round(P, I->cap_st, false, dp);
+                pfg_status ls = launch_round(P ^ 1, I->cap_st, false, dp, false, nq);
+                if (ls == PFG_OK) ls = launch_round(P, I->cap_st, false, dp, false, nq);
                 k_loop_cond<<<1, 1, 0, I->cap_st>>>(r.ctl, P ^ 1, h, lmin, cap);
                 cudaGraph_t body_out = body;
                 const cudaError_t ce = cudaStreamEndCapture(I->cap_st, &body_out);
@@ -2063,6 +2223,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         p.resume = 1;
         if (lmax == 0) fused_n = 0;
         I->last_rounds = round;
+        }
     }
     PFG_TRY(join_sketches(I, st));
     PFG_TRY(late_join(I, st));

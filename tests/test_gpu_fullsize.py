@@ -72,6 +72,9 @@ def test_config2_full_sampled():
     # the bench's launch: all 10 000 queries in one call; compare a sample of 200 (every 50th)
     cap = 1 << 13
     ids, sims, st, tr = g.search(torch.from_numpy(q).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
+    # two round pipelines (the automatic choice at this batch size) equal one pipeline
+    ids1, sims1, st1 = g.search(torch.from_numpy(q).to(DEV), c["k"], c["recall"], stats=True, pipelines=1)
+    assert torch.equal(ids1, ids) and torch.equal(sims1, sims) and np.array_equal(st1, st)
     sel = np.arange(0, len(q), 50)
     sub = (ids[sel], sims[sel], st[sel], tr[sel])
     orr = o.search(q[sel], c["k"], c["recall"], rep_chunk=pfg.DEFAULT_REP_CHUNK, trace_cap=cap, threads=1)
@@ -169,12 +172,12 @@ def test_config34_full(cfg):
         sids, ssims, sst, tr = g.search(torch.from_numpy(q[esel]).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
     orr = o.search(q[esel], c["k"], c["recall"], rep_chunk=pfg.DEFAULT_REP_CHUNK, trace_cap=cap, threads=8)
     _search_equal((sids, ssims, sst, tr), orr, cap)
-    assert np.array_equal(sids.cpu().numpy(), ids[sel]) and np.array_equal(sst["j_stop"], st["j_stop"][sel])
-    xn, qn = O.normalize(data), O.normalize(q[sel])
-    for r in range(len(sel)):
+    assert np.array_equal(sids.cpu().numpy(), ids[esel]) and np.array_equal(sst["j_stop"], st["j_stop"][esel])
+    xn, qn = O.normalize(data), O.normalize(q[esel])
+    for r in range(len(esel)):
         ev = tr[r, :min(cap, int(sst["evaluated"][r]))]
         assert len(set(ev.tolist())) == len(ev)
         if sst["evaluated"][r] <= cap:
             s = np.array([O.sim(qn[r], xn[e]) for e in ev], np.float32)
             order = np.lexsort((ev, -s))[:c["k"]]
-            assert np.array_equal(ev[order].astype(np.int64), ids[sel[r]]), r
+            assert np.array_equal(ev[order].astype(np.int64), ids[esel[r]]), r

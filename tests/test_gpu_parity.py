@@ -88,6 +88,22 @@ def test_build_arrays_bit_exact(cases, name):
         assert np.array_equal(g.export_prefix(j), o.prefix_table(j)), j
 
 
+@pytest.mark.parametrize("d", [20, 32, 40, 100, 130, 300, 700])
+def test_fht_tables_every_width(d):
+    # FHT-CP independent tables at d' = 32 .. 1024 (k_fht_keys: lane groups of max(1, d'/128) lanes,
+    # rows staged in shared memory; d' < 32: one warp per row), against the oracle's codes
+    rng = np.random.default_rng(d)
+    n = 2500 + d
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    g = pfg.Index(_cuda(data), 0, "fht_cp", seed=d, reps=5)
+    o = O.OracleIndex(data, O.FHTCP, L=5, seed=d)
+    for j in range(5):
+        tab = g.export_table(j)
+        codes, ids = o.rep(j)
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
+
+
 @pytest.mark.parametrize("name", ["fht", "fht_pool"])
 def test_cp_table_bit_exact(cases, name):
     c = cases[name]
@@ -171,6 +187,30 @@ def _compare(c, k, recall, gpu_kw, orc_kw, trace=True):
 def test_search_parity(cases, name, R, recall, engine):
     c = cases[name]
     _compare(c, 10, recall, dict(rep_chunk=R, engine=engine), dict(rep_chunk=R))
+
+
+@pytest.mark.parametrize("name", ALL + ["fht_long", "fht_d40", "cp"])
+@pytest.mark.parametrize("recall", [0.5, 0.9, 0.99])
+@pytest.mark.parametrize("rounds", [0, 1, 3])
+def test_search_parity_two_pipelines(cases, name, recall, rounds):
+    # pipelines = 2: the two halves of the batch as two searches on two streams (pfg.cu
+    # pipeline_params), each with its own fused tail
+    c = cases[name]
+    _compare(c, 10, recall, dict(rep_chunk=16, engine=0, pipelines=2, rounds=rounds), dict(rep_chunk=16))
+
+
+def test_two_pipelines_equal_one_pipeline():
+    # a batch large enough for the automatic choice (two pipelines): identical to one pipeline, odd nq
+    data, q = synth.config_data(2, n=60000, nq=4999)
+    g = pfg.Index(_cuda(data), 0, "fht_cp", seed=5, reps=48)
+    res = []
+    for pl in (1, 0, 2):
+        ids, sims, st = g.search(_cuda(q), 10, 0.9, stats=True, pipelines=pl)
+        res.append((ids.cpu().numpy(), sims.cpu().numpy(), st))
+    for ids, sims, st in res[1:]:
+        assert np.array_equal(ids, res[0][0]) and np.array_equal(sims.view(np.uint32), res[0][1].view(np.uint32))
+        for f in st.dtype.names:
+            assert np.array_equal(st[f], res[0][2][f]), f
 
 
 @pytest.mark.parametrize("name", ["hp_tensor", "fht_tensor", "hp_tensor64"])

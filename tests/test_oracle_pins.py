@@ -804,3 +804,22 @@ def test_int16_rerank_scores_in_fp32():
         assert np.array_equal(b_s[r], np.array(want, np.float32))
         keys = [(-s, i) for s, i in zip(b_s[r].tolist(), b_ids[r].tolist())]
         assert keys == sorted(keys)
+
+
+def test_fhtcp_recall_over_seeds_config2_shape():
+    # Lemma 1 with the FHT cross-polytope family: the
+    # stop rule's collision probabilities P_i come from the FHT-CP branch of or_P (Monte-Carlo table,
+    # prefix composition T_ell^floor(i/ell) T_(i mod ell), R-14), so a mistake there (too large P_i:
+    # early stops) shows as recall below the target.  Config 2's shape (100-d Gaussian mixture),
+    # 10 000 points, L = 32, recall target .9, index seeds 1..30: mean recall >= .9 with the filter off
+    # (the proven setting) and with the default quantile filter (R-26).
+    data, q = synth.config_data(2, n=10000, nq=60)
+    bi, _ = O.bruteforce(O.normalize(data), O.normalize(q), 10)
+    rec = {"off": [], "quantile": []}
+    for seed in range(1, 31):
+        X = O.OracleIndex(data, O.FHTCP, L=32, seed=seed, lazy=True, cp_draws=1000)
+        for name, kw in (("off", dict(use_filter=False)), ("quantile", dict())):
+            ids, _, _ = X.search(q, 10, 0.9, rep_chunk=16, threads=8, **kw)
+            rec[name].append(np.mean([len(set(a) & set(b)) / 10 for a, b in zip(ids.tolist(), bi.tolist())]))
+    assert np.mean(rec["off"]) >= 0.9, np.mean(rec["off"])
+    assert np.mean(rec["quantile"]) >= 0.9, np.mean(rec["quantile"])

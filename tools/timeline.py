@@ -21,6 +21,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--recall", type=float, default=0.9)
 ap.add_argument("--storage", default="f32", choices=["f32", "i16"])
+ap.add_argument("--pipelines", type=int, default=0)
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 dev = torch.device("cuda:0")
@@ -32,8 +33,8 @@ if c["reps"]:
     opts["reps"] = c["reps"]
 idx = pfg.Index(X, c["budget"] or 0, c["family"], seed=1, **opts)
 for _ in range(3):
-    idx.search(Q, c["k"], a.recall, engine=a.engine)
+    idx.search(Q, c["k"], a.recall, engine=a.engine, pipelines=a.pipelines, rep_chunk=16)
 torch.cuda.synchronize()
 print(f"== config {a.config} engine {a.engine}", file=sys.stderr, flush=True)
-idx.search(Q, c["k"], a.recall, engine=a.engine, timing=4)
+idx.search(Q, c["k"], a.recall, engine=a.engine, pipelines=a.pipelines, rep_chunk=16, timing=4)
 torch.cuda.synchronize()
