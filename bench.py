@@ -289,7 +289,7 @@ def main():
     ap.add_argument("--engine", type=int, default=0, help="0 = phase-split rounds + fused kernel, 1 = fused kernel only, 2 = chunk rounds + fused kernel")
     ap.add_argument("--uniform-chunks", action="store_true", help="first chunk R repetitions long (R-17 option)")
     ap.add_argument("--rounds", type=int, default=0, help="bulk rounds before the fused kernel (0 = library default)")
-    ap.add_argument("--pipelines", type=int, default=0, help="engine 0 round pipelines: 0 = library default (two from 4 096 queries), 1, 2")
+    ap.add_argument("--pipelines", type=int, default=0, help="engine 0 round pipelines: 0 = library default (one), 1, 2")
     ap.add_argument("--tau-rule", type=int, default=0, help="0 = quantile filter threshold (R-26), 1 = expected distance (R-15)")
     ap.add_argument("--parallel", default="data", choices=["data", "queries"],
                     help="N > 1: data-sharded (the default, SURVEY 8(e): each GPU indexes n/N rows -- 12.5M rows per GPU "
@@ -521,7 +521,7 @@ def main():
                        "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "storage": args.storage,
                        "tau_rule": ["quantile (R-26)", "expected distance (R-15)"][args.tau_rule],
                        "engine": args.engine, "rounds": args.rounds or 5,
-                       "pipelines": args.pipelines or (2 if args.engine == 0 and nq >= 4096 else 1),
+                       "pipelines": args.pipelines or 1,
                        "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": (f"data-sharded x{world}" if sharded else
                                        f"query replicas x{world} (every GPU builds the whole index and answers a batch "

@@ -160,12 +160,11 @@ typedef struct {
                                       (later repetitions are hashed in the kernels as usual) */
     int32_t ext_reps;
     const uint64_t* ext_sketches;  /* [nq][M] query sketches */
-    int32_t pipelines;        /* [0] engine 0: 1 = one round pipeline over the batch; 2 = two pipelines, the
-                                 lower and the upper half of the batch as two searches of their own on two
-                                 streams, so that one half's control phases overlap the other half's
-                                 candidate-row reads (used only without wide queries or the device-side
-                                 loop, and for exact cross-polytope only when every repetition is hashed
-                                 eagerly); 0 = automatic: two from 4 096 queries.  Results are identical. */
+    int32_t pipelines;        /* [0] engine 0: 0 or 1 = one round pipeline over the batch; 2 = two pipelines,
+                                 the lower and the upper half of the batch as two searches of their own on
+                                 two streams, each kernel with half its resident grid (not with wide
+                                 queries, the device-side loop, or exact cross-polytope's partial eager
+                                 hashing; then one).  Results are identical; measured slower on config 2. */
 } pfg_search_opts;
 
 /* per-query counters (optional output of pfg_search) */

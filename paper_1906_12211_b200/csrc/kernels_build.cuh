@@ -6,7 +6,9 @@
 //                canonical sequential fmaf chain over t (R-2), so bits equal the oracle's;
 //                also produces the 64-bit sketch words
 //  k_codes_from_bits  repetition codes from HP bits (independent or pool selection)
-//  k_fht_rep     a3: FHT cross-polytope repetition codes, warp per row
+//  k_fht_keys    a3: FHT cross-polytope repetition keys / codes, a lane group
+//                per (row, repetition), the transform in registers, rows staged in shared memory
+//  k_fht_rep     the same, one warp per row (d' < 32 or > 1024)
 //  k_fht_funcs   FHT-CP codes of pool functions (pool strategy)
 //  k_pool_codes  repetition codes from pooled FHT-CP function codes
 //  k_prefix      a5: 13-bit prefix tabulation of a sorted repetition
@@ -353,16 +355,18 @@ __global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ 
     if (live && g == 0) codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
 }
 
-// Build-side FHT-CP repetition keys (independent strategy): a block stages RB = 128/TPF rows in
+// FHT-CP repetition keys / codes (independent strategy): a block stages RB = 128/TPF rows in
 // shared memory (coalesced; row stride S floats with S/4 odd, so the lanes' 128-bit reads do not
-// conflict) and loops over repetitions r0 .. r0 + nreps - 1, one lane group per (row, repetition):
-// the sign words are the same for the whole block (broadcast) and each repetition's keys
-// {code << 32 | p} are written coalesced.  Same arithmetic as k_fht_rep / the oracle (R-6).
+// conflict) and loops over its repetitions (block column y: repetitions r0 + y*rpb .. + rpb - 1 of
+// r0 .. r0 + nreps - 1), one lane group per (row, repetition): the sign words are the same for the
+// whole block (broadcast) and each repetition's keys {code << 32 | p} are written coalesced.  Same
+// arithmetic as k_fht_rep / the oracle (R-6).  The index build takes every repetition in one
+// column; a query batch splits them over columns (few rows, many blocks).
 template <int DP, int TPF>
 __global__ void __launch_bounds__(128) k_fht_keys(const float* __restrict__ X, int64_t np, int ldx, int dpad, int S,
                                                   int ell, int c, int K, const uint32_t* __restrict__ sg, int r0,
                                                   int nreps, uint64_t* __restrict__ keys, uint32_t* __restrict__ codes,
-                                                  int ldc) {
+                                                  int ldc, int rpb) {
     constexpr int RB = 128 / TPF, W = (DP + 31) / 32;
     extern __shared__ __align__(16) float xs[];
     const int64_t p0 = (int64_t)blockIdx.x * RB;
@@ -376,7 +380,8 @@ __global__ void __launch_bounds__(128) k_fht_keys(const float* __restrict__ X, i
     __syncthreads();
     const int lr = threadIdx.x / TPF, g = threadIdx.x % TPF;
     const int64_t p = p0 + lr;
-    for (int r = 0; r < nreps; ++r) {
+    const int rb = blockIdx.y * rpb, re = min(nreps, rb + rpb);
+    for (int r = rb; r < re; ++r) {
         const int j = r0 + r;
         const uint64_t full = fhtcp_rep_full<DP, TPF>(xs + lr * S, dpad, sg + (int64_t)j * c * 3 * W, c, ell, g);
         const uint32_t code = (uint32_t)(full >> (c * ell - K));

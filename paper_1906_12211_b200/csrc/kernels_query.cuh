@@ -548,6 +548,36 @@ __device__ __forceinline__ uint32_t hs_next(uint32_t h) {
     return h + 1 == (uint32_t)kHC ? 0u : h + 1;
 }
 
+// Read-only lookup of id v (not kEmpty) in a hash set of kHC slots (16-byte aligned): the linear
+// probe sequence h, h + 1, ... read four slots at a time (one 128-bit shared load per aligned
+// quad), the same probe order and answer as slot-by-slot probing.  Returns true if v is present;
+// h ends at v's slot, or at the first empty slot (where an insertion of v starts probing).
+// one quad w (slots b .. b + 3, b = h & ~3) of the probe sequence from h: true if the probe ends in
+// it (then h = the ending slot and found = whether it holds v); else h = the next quad's first slot
+__device__ __forceinline__ bool hs_quad(const uint4 w, uint32_t v, uint32_t& h, bool& found) {
+    const uint32_t b = h & ~3u;
+    const uint32_t from = (0xfu << (h & 3u)) & 0xfu;   // slots h .. b + 3
+    const uint32_t eq = ((uint32_t)(w.x == v) | (uint32_t)(w.y == v) << 1 | (uint32_t)(w.z == v) << 2 |
+                         (uint32_t)(w.w == v) << 3) & from;
+    const uint32_t em = ((uint32_t)(w.x == kEmpty) | (uint32_t)(w.y == kEmpty) << 1 | (uint32_t)(w.z == kEmpty) << 2 |
+                         (uint32_t)(w.w == kEmpty) << 3) & from;
+    const uint32_t stop = eq | em;
+    if (stop) {
+        const uint32_t i = __ffs(stop) - 1;
+        h = b + i;
+        found = (eq >> i) & 1u;
+        return true;
+    }
+    h = (b + 4) & (uint32_t)(kHC - 1);
+    return false;
+}
+__device__ __forceinline__ bool hs_lookup4(const uint32_t* hs, uint32_t v, uint32_t& h) {
+    static_assert(kHCPow2 && kHC % 4 == 0, "quad probing needs a power-of-two set of whole quads");
+    bool found = false;
+    while (!hs_quad(*reinterpret_cast<const uint4*>(hs + (h & ~3u)), v, h, found)) {}
+    return found;
+}
+
 // claim id for evaluation: true if it was not evaluated before (called by one lane per distinct id)
 __device__ __forceinline__ bool claim(const WarpSmem& w, const QState& st, uint32_t* bm, uint32_t id) {
     if (st.bitmap_mode) {

@@ -609,21 +609,18 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
             for (int u = 0; u < kCPre; ++u)
                 if ((u % (kTile / 32)) * 32 + lane >= tc[u / (kTile / 32)]) v[u] = kEmpty;
             // membership in the set as it stands before this batch: independent read-only probes,
-            // the home slots of the whole batch loaded first
-            uint32_t x[kCPre];
+            // four slots per shared load (hs_lookup4); h[u] ends at the id's slot or the first empty
+            // (the home quads of the whole batch loaded first)
+            uint4 w4[kCPre];
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
                 h[u] = hs_slot(v[u]);
-                x[u] = v[u] != kEmpty ? c->hs[h[u]] : kEmpty;
+                w4[u] = v[u] != kEmpty ? *reinterpret_cast<const uint4*>(c->hs + (h[u] & ~3u)) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
-                if (v[u] != kEmpty)
-                    while (x[u] != kEmpty && x[u] != v[u]) {
-                        h[u] = hs_next(h[u]);
-                        x[u] = c->hs[h[u]];
-                    }
-                found[u] = v[u] != kEmpty && x[u] == v[u];
+                found[u] = false;
+                if (v[u] != kEmpty && !hs_quad(w4[u], v[u], h[u], found[u])) found[u] = hs_lookup4(c->hs, v[u], h[u]);
             }
             // claims of the rest in (repetition, position) order, u in order; a later occurrence
             // of an id claimed earlier in the batch finds it in the set
@@ -935,6 +932,10 @@ __device__ __forceinline__ void push_fused(const RoundState& rs, uint32_t q) {
 #ifndef PFG_MERGE_MINB
 #define PFG_MERGE_MINB 10
 #endif
+#ifndef PFG_MERGE_SORTMIN
+#define PFG_MERGE_SORTMIN 8
+#endif
+constexpr int kMergeSortMin = PFG_MERGE_SORTMIN;  // keys above the k-th from which k_merge sorts a batch
 template <typename PP, bool WIDE>
 __global__ void __launch_bounds__(128, WIDE ? 8 : PFG_MERGE_MINB) k_merge(PP pp, int par) {
     const QueryParams& p = deref(pp);
@@ -1046,6 +1047,24 @@ __global__ void __launch_bounds__(128, WIDE ? 8 : PFG_MERGE_MINB) k_merge(PP pp,
                         p.trace_ids[q * p.trace_cap + nE + idx] = key_id(cur);
                     uint64_t kth = (tn == p.k_eff) ? __shfl_sync(kFull, tv, p.k_eff - 1) : 0ull;
                     uint32_t mk = __ballot_sync(kFull, mine && cur > kth);
+                    if (__popc(mk) >= kMergeSortMin) {
+                        // many keys above the k-th (early in a search): sort them and merge the two
+                        // sorted lists at once (bitonic: max of the batch and the reversed list holds
+                        // the top 32 of the union, then a half-cleaner sort); the top k of a set of
+                        // distinct keys does not depend on the insertion order
+                        uint64_t kv = ((mk >> lane) & 1u) ? cur : 0ull;
+                        kv = warp_sort_desc(kv, lane);
+                        uint64_t mv = __shfl_sync(kFull, tv, 31 - lane);
+                        mv = kv > mv ? kv : mv;
+#pragma unroll
+                        for (int h = 16; h >= 1; h >>= 1) {
+                            const uint64_t o = __shfl_xor_sync(kFull, mv, h);
+                            mv = (lane & h) ? (mv < o ? mv : o) : (mv > o ? mv : o);
+                        }
+                        tv = lane < p.k_eff ? mv : 0ull;
+                        tn = min(p.k_eff, tn + __popc(mk));
+                        mk = 0;
+                    }
                     while (mk) {
                         const int l = __ffs(mk) - 1;
                         mk &= mk - 1;

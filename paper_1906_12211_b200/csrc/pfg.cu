@@ -553,13 +553,17 @@ void launch_fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uin
 }
 template <int DP, int TPF>
 void launch_fht_keys(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps,
-                     uint64_t* keys, uint32_t* codes, int ldc, cudaStream_t st) {
+                     uint64_t* keys, uint32_t* codes, int ldc, cudaStream_t st, int num_sms = 148) {
     constexpr int RB = 128 / TPF;
     const int S = (g.dpad / 4) % 2 ? g.dpad : g.dpad + 4;   // S/4 odd: conflict-free 128-bit reads
     const size_t sm = (size_t)RB * S * 4;
     set_smem((const void*)k_fht_keys<DP, TPF>, sm);
-    k_fht_keys<DP, TPF><<<(unsigned)((np + RB - 1) / RB), 128, sm, st>>>(X, np, ldx, g.dpad, S, g.ell, g.c, g.K, sg, r0,
-                                                                         nreps, keys, codes, ldc);
+    // repetitions per block: all of them, unless the rows alone give fewer than 4 blocks per SM
+    const int64_t rows_b = (np + RB - 1) / RB;
+    const int cols = (int)std::min<int64_t>(nreps, std::max<int64_t>(1, (4 * (int64_t)num_sms + rows_b - 1) / rows_b));
+    const int rpb = (nreps + cols - 1) / cols;
+    const dim3 grid((unsigned)rows_b, (unsigned)((nreps + rpb - 1) / rpb));
+    k_fht_keys<DP, TPF><<<grid, 128, sm, st>>>(X, np, ldx, g.dpad, S, g.ell, g.c, g.K, sg, r0, nreps, keys, codes, ldc, rpb);
 }
 void fht_rep(const float* X, int64_t np, int ldx, const Geo& g, const uint32_t* sg, int r0, int nreps, uint64_t* keys,
              uint32_t* codes, int ldc, int num_sms, cudaStream_t st) {
@@ -964,9 +968,11 @@ pfg_status hash_reps(pfg_index* I, const float* X, int64_t np, int r0, int nb, u
 }
 
 pfg_status normalize_rows(const float* src, int64_t n, int d, float* dst, int dpad, uint8_t* zflag,
-                          unsigned long long* zmin_dev, int64_t* zrow, cudaStream_t st) {
+                          unsigned long long* zmin_dev, int64_t* zrow, cudaStream_t st, int num_sms = 148) {
     PFG_CUDA(cudaMemsetAsync(zmin_dev, 0xff, 8, st));
-    const int rb = std::max(1, std::min(32, 12288 / d));   // rows per block staged in shared memory
+    // rows per block staged in shared memory; a small batch (a query batch) takes fewer per block so
+    // that every SM gets about eight blocks (the per-thread loops are latency-bound)
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(32, 12288 / d), n / (8 * (int64_t)num_sms)));
     k_normalize<<<(unsigned)((n + rb - 1) / rb), 128, (size_t)rb * d * 4, st>>>(src, n, d, d, dst, dpad, zflag, zmin_dev, rb);
     PFG_CUDA(cudaGetLastError());
     if (!zrow) return PFG_OK;  // asynchronous: the caller reads zmin_dev later
@@ -1073,7 +1079,7 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     PFG_TRY(I->qzero.ensure((size_t)nq, "query zero flags"));
     PFG_TRY(I->zmin.ensure(8, "zmin"));
     PFG_TRY(normalize_rows(qsrc, nq, g.d, I->qx.as<float>(), g.dpad, I->qzero.as<uint8_t>(),
-                           I->zmin.as<unsigned long long>(), zrow, st));
+                           I->zmin.as<unsigned long long>(), zrow, st, I->num_sms));
     tl_mark(I, "normalize", st);
     if (g.storage == PFG_STORAGE_I16) {
         // R-25: the queries' fixed-point rows for the inner products
@@ -1696,13 +1702,15 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     }
     PFG_TRY(I->work.ensure(16, "work counters"));
     PFG_CUDA(cudaMemsetAsync(I->work.p, 0, 16, st));
-    // two round pipelines (pipelines option): the lower and the upper half of the batch run as two
-    // searches of their own on st and st1, so that one half's latency-bound control phases overlap
-    // the other half's candidate-row reads.  Not with wide queries / the device-side loop (the
-    // loop graph is per search) or exact CP's partial eager hashing (bulk codes per fused list).
+    // two round pipelines (pipelines = 2): the lower and the upper half of the batch run as two
+    // searches of their own on st and st1, each kernel with half the resident grid, meant to overlap
+    // one half's latency-bound control phases with the other half's candidate-row reads.  Measured
+    // slower on config 2 (1.89 vs 1.84 ms/step): the halves fall into lock-step
+    // and k_sims at half its grid leaves HBM under-used.  Not with wide queries / the device-side
+    // loop (the loop graph is per search) or exact CP's partial eager hashing.
     const int64_t lmax_cfg = s.loop_max > 0 ? s.loop_max : (I->loop_heavy ? 1 : 0);
     const bool halves = rounds && !chunk_eng && s.engine == 0 && !want_wide && lmax_cfg == 0 && cp_eager == 0 &&
-                        (s.pipelines == 2 ? nq >= 2 : (s.pipelines == 0 && nq >= 4096));
+                        s.pipelines == 2 && nq >= 2;
 
     const bool ids_dev = is_device_ptr(out_ids), sims_dev = is_device_ptr(out_sims);
     const bool stats_dev = stats ? is_device_ptr(stats) : true;
@@ -1934,6 +1942,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(set_smem((const void*)k_dedupe<QueryParams>, dsm));
         PFG_CUDA(set_smem((const void*)k_merge<const QueryParams*, true>, msm));
         PFG_CUDA(set_smem((const void*)k_dedupe<const QueryParams*>, dsm));
+
         int docc = 1;
         PFG_CUDA(occupancy(&docc, (const void*)k_dedupe<QueryParams>, 128, dsm));
         // grids: warp per active query (at most one resident wave; the kernels stride over the
@@ -1949,11 +1958,20 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         // one round: expand, scan, dedupe, sims, merge of list `par` (phase events unless captured)
         // blind: a round outside the captured loop (counted in sims_rows_blind, timed with timing = 3);
         // m: the queries of the pipeline (grid sizes)
-        auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp, bool blind, int64_t m) -> pfg_status {
+        // share = 2 (two round pipelines): every grid is half of what stays resident, so that the
+        // other pipeline's kernel of another phase finds registers and shared memory beside it
+        int occ_e = 1, occ_s = 1, occ_m = 1;
+        PFG_CUDA(occupancy(&occ_e, (const void*)k_expand<1, QueryParams>, 128, esm));
+        PFG_CUDA(occupancy(&occ_s, (const void*)k_scan<QueryParams, false>, 256, 0));
+        PFG_CUDA(occupancy(&occ_m, (const void*)k_merge<QueryParams, false>, 128, msm));
+        auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp, bool blind, int64_t m, int share) -> pfg_status {
             using PP = decltype(pp);
-            const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 3) / 4, (int64_t)I->num_sms * 16));
-            const unsigned qb_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 3) / 4, (int64_t)I->num_sms * std::max(1, docc)));
-            const unsigned qb_m = qb_e;
+            const int64_t qw = (m + 3) / 4, ns = I->num_sms;
+            const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>(qw, share > 1 ? ns * std::max(1, occ_e / share) : ns * 16));
+            const unsigned qb_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>(qw, ns * std::max(1, docc / share)));
+            const unsigned qb_m = share > 1 ? (unsigned)std::max<int64_t>(1, std::min<int64_t>(qw, ns * std::max(1, occ_m / share))) : qb_e;
+            const unsigned tb_s = share > 1 ? (unsigned)(ns * std::max(1, occ_s / share)) : (unsigned)(ns * 8);
+            const unsigned sb = (unsigned)(ns * std::max(1, PFG_SIMS_MINB / share));
             PFG_TRY(phase_mark(I, marks, kPhExpand, rst));
             switch (epl) {
                 case 1: k_expand<1, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
@@ -2031,7 +2049,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             for (; round < max_rounds; ++round) {
                 if (round == 1) PFG_TRY(join_both(false));
                 if (round == 2) PFG_TRY(join_both(true));
-                for (int h = 0; h < 2; ++h) PFG_TRY(launch_round(round & 1, sh[h], tm && h == 0, ph[h], true, nh[h]));
+                for (int h = 0; h < 2; ++h) PFG_TRY(launch_round(round & 1, sh[h], tm && h == 0, ph[h], true, nh[h], 2));
                 I->launches += 10;
             }
             PFG_TRY(join_both(true));
@@ -2084,7 +2102,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             // repetitions < 1 + R; later rounds may reach every eager repetition
             if (round == 1) { PFG_TRY(join_sketches(I, st)); PFG_TRY(mid_join(I, st)); }
             if (round == 2) PFG_TRY(late_join(I, st));
-            PFG_TRY(launch_round(round & 1, st, tm, p, true, nq));
+            PFG_TRY(launch_round(round & 1, st, tm, p, true, nq, 1));
             I->launches += 5;
             ++round;
         }
@@ -2192,8 +2210,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 PFG_CUDA(cudaGraphAddNode(&cn, gr, &n0, 1, &cp));
                 cudaGraph_t body = cp.conditional.phGraph_out[0];
                 PFG_CUDA(cudaStreamBeginCaptureToGraph(I->cap_st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-                pfg_status ls = launch_round(P ^ 1, I->cap_st, false, dp, false, nq);
-                if (ls == PFG_OK) ls = launch_round(P, I->cap_st, false, dp, false, nq);
+                pfg_status ls = launch_round(P ^ 1, I->cap_st, false, dp, false, nq, 1);
+                if (ls == PFG_OK) ls = launch_round(P, I->cap_st, false, dp, false, nq, 1);
                 k_loop_cond<<<1, 1, 0, I->cap_st>>>(r.ctl, P ^ 1, h, lmin, cap);
                 cudaGraph_t body_out = body;
                 const cudaError_t ce = cudaStreamEndCapture(I->cap_st, &body_out);

@@ -72,8 +72,8 @@ def test_config2_full_sampled():
     # the bench's launch: all 10 000 queries in one call; compare a sample of 200 (every 50th)
     cap = 1 << 13
     ids, sims, st, tr = g.search(torch.from_numpy(q).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
-    # two round pipelines (the automatic choice at this batch size) equal one pipeline
-    ids1, sims1, st1 = g.search(torch.from_numpy(q).to(DEV), c["k"], c["recall"], stats=True, pipelines=1)
+    # two round pipelines equal one pipeline (the default)
+    ids1, sims1, st1 = g.search(torch.from_numpy(q).to(DEV), c["k"], c["recall"], stats=True, pipelines=2)
     assert torch.equal(ids1, ids) and torch.equal(sims1, sims) and np.array_equal(st1, st)
     sel = np.arange(0, len(q), 50)
     sub = (ids[sel], sims[sel], st[sel], tr[sel])

@@ -200,7 +200,7 @@ def test_search_parity_two_pipelines(cases, name, recall, rounds):
 
 
 def test_two_pipelines_equal_one_pipeline():
-    # a batch large enough for the automatic choice (two pipelines): identical to one pipeline, odd nq
+    # a larger batch (odd nq): two pipelines identical to one
     data, q = synth.config_data(2, n=60000, nq=4999)
     g = pfg.Index(_cuda(data), 0, "fht_cp", seed=5, reps=48)
     res = []
