@@ -757,6 +757,57 @@ __device__ __forceinline__ float sims_step(const QueryParams& p, uint32_t myid, 
 #ifndef PFG_I16_NR
 #define PFG_I16_NR 16
 #endif
+// 16-bit rows of at most 128 coordinates (16 chunks of 16 bytes): each half-warp takes 16 rows of a
+// 32-row step (lane l reads chunk l & 15 of the rows of half l >> 4), so every lane loads and a
+// step keeps twice the bytes in flight; the sums are exact int32 (R-25), so the reduction order
+// does not matter.  Lane r < 32 holds row r's id (myid) and query (myq); lane l ends with row l.
+template <bool ONEQ>
+__device__ __forceinline__ int sims_step_i16_half(const QueryParams& p, uint32_t myid, uint32_t myq, int lane) {
+    const uint32_t nch = (uint32_t)(p.dpad16 >> 3);
+    const int half = lane >> 4, c = lane & 15;
+    const int4* x4 = reinterpret_cast<const int4*>(p.x16);
+    const int4* q4 = reinterpret_cast<const int4*>(p.qx16);
+    uint32_t roff[16], qoff[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        // every lane takes part in the shuffles; lanes of half 1 keep the second set
+        const uint32_t i0 = __shfl_sync(kFull, myid, r), i1 = __shfl_sync(kFull, myid, 16 + r);
+        roff[r] = (half ? i1 : i0) * nch;
+        if (!ONEQ) {
+            const uint32_t q0 = __shfl_sync(kFull, myq, r), q1 = __shfl_sync(kFull, myq, 16 + r);
+            qoff[r] = (half ? q1 : q0) * nch;
+        }
+    }
+    const uint32_t qo = ONEQ ? __shfl_sync(kFull, myq, 0) * nch : 0u;
+    int acc[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc[r] = 0;
+    if ((uint32_t)c < nch) {
+        int4 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = __ldg(x4 + roff[r] + c);
+        const int4 qv0 = __ldg(q4 + qo + c);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) acc[r] = dot8_i16(v[r], ONEQ ? qv0 : __ldg(q4 + qoff[r] + c));
+    }
+    // transposed halving within the half-warp: lane l ends with the sum of row l & 15 of its half
+    int m = 16;
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+        const int hm = m >> 1;
+        const bool up = lane & h;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k < hm) {
+                const int send = up ? acc[k] : acc[k + hm];
+                const int keep = up ? acc[k + hm] : acc[k];
+                acc[k] = keep + __shfl_xor_sync(kFull, send, h);
+            }
+        }
+        m = hm;
+    }
+    return acc[0];
+}
 // flags bit 0 (the chunk engine, kernels_chunk.cuh): the pool of parity par starts at
 // par * pool_stride, and the kernel resets the counters the next round's k_chunk starts from (its
 // active list's successor, its pool, its work counter), none of which this launch reads;
@@ -790,6 +841,30 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par, int
             qq = pool_q[e];
         }
     };
+    if constexpr (I16) {
+        if (p.dpad16 <= 128) {
+            // 32 rows per step, a half-warp per 16 (sims_step_i16_half)
+            auto fetch32 = [&](int64_t b, uint32_t& id, uint32_t& qq) {
+                if (b < top) {
+                    const int64_t e = b + lane < (int64_t)top ? b + lane : (int64_t)top - 1;
+                    id = pool_id[e];
+                    qq = pool_q[e];
+                }
+            };
+            int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+            uint32_t nid = 0, nq_ = 0;
+            fetch32(b, nid, nq_);
+            for (; b < top; b += nw * 32) {
+                const uint32_t myid = nid, myq = nq_;
+                fetch32(b + nw * 32, nid, nq_);
+                const bool oneq = __shfl_sync(kFull, myq, 0) == __shfl_sync(kFull, myq, 31);
+                const int t = oneq ? sims_step_i16_half<true>(p, myid, myq, lane) : sims_step_i16_half<false>(p, myid, myq, lane);
+                // lane l holds row (l >> 4) * 16 + (l & 15) = l
+                if (b + lane < (int64_t)top) pool_key[b + lane] = make_key(sim_of_i16(t), myid);
+            }
+            return;
+        }
+    }
     int64_t b = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NR;
     uint32_t nid = 0, nq_ = 0;
     fetch(b, nid, nq_);

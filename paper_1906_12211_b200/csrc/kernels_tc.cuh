@@ -114,16 +114,17 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
     uint32_t phase = 0;
     const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    for (int k0 = 0; k0 < kdim; k0 += TC_KC) {
+    // operand tiles: tf32 hi / lo parts in the canonical layout (a 16-byte core-matrix row holds 4
+    // consecutive k of one row); columns beyond kc are zero.  Thread t stages row t of both tiles
+    // (8 chunks of 4 k), so the 8 lanes of a quarter warp write one contiguous 128-byte core matrix
+    // (no bank conflicts).  The next chunk's 16 loads are issued while the tensor core multiplies
+    // the current one (registers), so only the first chunk's load latency is exposed.
+    static_assert(TC_M == 128 && TC_N == 128, "thread t stages row t");
+    constexpr int kIt = TC_KC / 4;
+    float4 xv[kIt], av[kIt];
+    const bool xr_ok = p0 + tid < np, ar_ok = f0 + tid < nf;
+    auto load_chunk = [&](int k0) {
         const int kc = min(TC_KC, kdim - k0);
-        // operand tiles: tf32 hi / lo parts in the canonical layout (a 16-byte core-matrix row holds
-        // 4 consecutive k of one row); columns beyond kc are zero.  Thread t stages row t of both
-        // tiles (8 chunks of 4 k), so the 8 lanes of a quarter warp write one contiguous 128-byte
-        // core matrix (no bank conflicts); all 16 loads are issued before any is converted.
-        static_assert(TC_M == 128 && TC_N == 128, "thread t stages row t");
-        constexpr int kIt = TC_KC / 4;
-        float4 xv[kIt], av[kIt];
-        const bool xr_ok = p0 + tid < np, ar_ok = f0 + tid < nf;
         const float* xrow = X + (p0 + tid) * ldx + k0;
         const float* arow = A + (int64_t)(f0 + tid) * lda + k0;
 #pragma unroll
@@ -131,6 +132,10 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
             xv[u] = (xr_ok && 4 * u < kc) ? __ldg(reinterpret_cast<const float4*>(xrow + 4 * u)) : z4;
             av[u] = (ar_ok && 4 * u < kc) ? __ldg(reinterpret_cast<const float4*>(arow + 4 * u)) : z4;
         }
+    };
+    load_chunk(0);
+    for (int k0 = 0; k0 < kdim; k0 += TC_KC) {
+        const int kc = min(TC_KC, kdim - k0);
         float sq = 0.0f;
 #pragma unroll
         for (int u = 0; u < kIt; ++u) {
@@ -156,6 +161,7 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
                              tc_smem_addr(&mbar))
                          : "memory");
         }
+        if (k0 + TC_KC < kdim) load_chunk(k0 + TC_KC);
         // the MMAs read the tiles: wait for them before the next chunk overwrites them
         tc_mbar_wait(tc_smem_addr(&mbar), phase);
         phase ^= 1;
@@ -233,6 +239,188 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_N));
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Exact cross-polytope codes on tcgen05: value = argmax_i |<a_i, x>| over
+// the d hyperplanes of function f (ties to the lowest i), sign as the most significant of ell bits;
+// each <a_i, x> is decided by the sequential fmaf chain c_i over t (R-2), as in k_cp_funcs.  The
+// tensor cores give v_i (3xTF32, TMEM) with |v_i - c_i| <= B_i = 4 (kdim + 8) 2^-22 ||a_i||_2 (the
+// bound of k_hp_bits_tc).  With L = max_j (|v_j| - B_j), every i with |v_i| + B_i < L has
+// |c_i| < L <= |c_i*| for the i* attaining L, so only the candidates {i : |v_i| + B_i >= L} can be
+// the argmax: a single candidate with |v| > B is the answer (sign of v = sign of c); otherwise the
+// chains of the candidates are evaluated and compared exactly.  Codes equal k_cp_funcs' (the
+// oracle's) by construction.
+//
+// CTA: 128 rows x one function (NT = 128 or 256 hyperplane columns, d <= NT), K in chunks of 32.
+// The hyperplanes are stored transposed, AT[f][t][i] (i padded to d32): thread t stages hyperplane
+// t (and t + 128) with one coalesced scalar load per k.
+template <int NT>
+__global__ void __launch_bounds__(128, 1) k_cp_tc(const float* __restrict__ X, int64_t np, int ldx,
+                                                 const float* __restrict__ AT, int nfun, int d, int d32, int ell,
+                                                 uint16_t* __restrict__ out) {
+    extern __shared__ __align__(1024) unsigned char tc_sm[];
+    unsigned char* Xhi = tc_sm;
+    unsigned char* Xlo = Xhi + TC_M * TC_KC * 4;
+    unsigned char* Ahi = Xlo + TC_M * TC_KC * 4;
+    unsigned char* Alo = Ahi + NT * TC_KC * 4;
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    __shared__ float bnd[NT];   // ||a_i||^2, then the bound B_i
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t p0 = (int64_t)blockIdx.x * TC_M;
+    const int f = blockIdx.y;
+    const int kdim = (d + 7) & ~7;
+    const float* A = AT + (int64_t)f * d * d32;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem_addr(&tmem_base)),
+                     "r"(NT));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem_addr(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+    uint32_t phase = 0;
+    constexpr int kIt = TC_KC / 4, NH = NT / 128;
+    const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    const bool xr_ok = p0 + tid < np;
+    float4 xv[kIt], av[NH][kIt];
+    float sq[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) sq[h] = 0.0f;
+    auto load_chunk = [&](int k0) {
+        const float* xrow = X + (p0 + tid) * ldx + k0;
+#pragma unroll
+        for (int u = 0; u < kIt; ++u) xv[u] = (xr_ok && k0 + 4 * u < kdim) ? __ldg(reinterpret_cast<const float4*>(xrow + 4 * u)) : z4;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            const int i = tid + 128 * h;
+#pragma unroll
+            for (int u = 0; u < kIt; ++u) {
+                float e[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const int t = k0 + 4 * u + w;
+                    e[w] = (i < d32 && t < d) ? __ldg(A + (int64_t)t * d32 + i) : 0.0f;
+                }
+                av[h][u] = make_float4(e[0], e[1], e[2], e[3]);
+            }
+        }
+    };
+    load_chunk(0);
+    for (int k0 = 0; k0 < kdim; k0 += TC_KC) {
+        const int kc = min(TC_KC, kdim - k0);
+#pragma unroll
+        for (int u = 0; u < kIt; ++u) {
+            tc_split_store(Xhi, Xlo, tc_off(tid, 4 * u, TC_M), xv[u]);
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                tc_split_store(Ahi, Alo, tc_off(tid + 128 * h, 4 * u, NT), av[h][u]);
+                sq[h] += av[h][u].x * av[h][u].x + av[h][u].y * av[h][u].y + av[h][u].z * av[h][u].z + av[h][u].w * av[h][u].w;
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t xh = tc_smem_addr(Xhi), xl = tc_smem_addr(Xlo), ah = tc_smem_addr(Ahi), al = tc_smem_addr(Alo);
+            for (int s = 0; s < kc / 8; ++s) {
+                const uint32_t ox = s * 2 * (TC_M / 8) * 128, oa = s * 2 * (NT / 8) * 128;
+                const uint64_t dxh = tc_desc(xh + ox, TC_M), dxl = tc_desc(xl + ox, TC_M);
+                const uint64_t dah = tc_desc(ah + oa, NT), dal = tc_desc(al + oa, NT);
+                tc_mma(tmem, dxh, dah, idesc, (k0 > 0 || s > 0) ? 1u : 0u);
+                tc_mma(tmem, dxh, dal, idesc, 1u);
+                tc_mma(tmem, dxl, dah, idesc, 1u);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             tc_smem_addr(&mbar))
+                         : "memory");
+        }
+        if (k0 + TC_KC < kdim) load_chunk(k0 + TC_KC);
+        tc_mbar_wait(tc_smem_addr(&mbar), phase);
+        phase ^= 1;
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+    for (int h = 0; h < NH; ++h) bnd[tid + 128 * h] = 4.0f * (float)(kdim + 8) * 2.384185791015625e-07f * sqrtf(sq[h]);
+    __syncthreads();
+    // epilogue: thread = row 32 warp + lane; pass 1: L = max (|v_i| - B_i); pass 2: the candidates
+    const int rl = 32 * warp + lane;
+    const int64_t p = p0 + rl;
+    auto tld = [&](int cb, uint32_t (&v)[32]) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+            "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+              "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+              "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)cb));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    };
+    float L = -INFINITY;
+    for (int cb = 0; cb < NT; cb += 32) {
+        uint32_t v[32];
+        tld(cb, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (cb + j < d) L = fmaxf(L, fabsf(__uint_as_float(v[j])) - bnd[cb + j]);
+    }
+    constexpr int kCand = 4;   // candidates kept (in index order); more: every hyperplane's chain
+    int ncand = 0;
+    int ci[kCand] = {0, 0, 0, 0};
+    float bv = 0.0f;
+    for (int cb = 0; cb < NT; cb += 32) {
+        uint32_t v[32];
+        tld(cb, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float a = __uint_as_float(v[j]);
+            if (cb + j < d && fabsf(a) + bnd[cb + j] >= L) {
+                if (ncand == 0) bv = a;
+#pragma unroll
+                for (int c = 0; c < kCand; ++c)
+                    if (ncand == c) ci[c] = cb + j;
+                ++ncand;
+            }
+        }
+    }
+    if (p < np) {
+        uint32_t code;
+        if (ncand == 1 && fabsf(bv) > bnd[ci[0]]) {
+            code = ((bv < 0.0f ? 1u : 0u) << (ell - 1)) | (uint32_t)ci[0];
+        } else {
+            // near tie (or a tiny maximum): the candidates' chains compared exactly (R-2), in index
+            // order so that ties go to the lowest index
+            const float* xr = X + p * ldx;
+            float best = -1.0f, bc = 0.0f;
+            int bidx = 0;
+            const int nc = ncand <= kCand ? ncand : d;
+            for (int c = 0; c < nc; ++c) {
+                int i = c;
+                if (ncand <= kCand) {
+#pragma unroll
+                    for (int u = 0; u < kCand; ++u)
+                        if (u == c) i = ci[u];
+                }
+                float acc = 0.0f;
+                for (int t = 0; t < d; ++t) acc = fmaf(__ldg(A + (int64_t)t * d32 + i), __ldg(xr + t), acc);
+                if (fabsf(acc) > best) { best = fabsf(acc); bidx = i; bc = acc; }
+            }
+            code = ((bc < 0.0f ? 1u : 0u) << (ell - 1)) | (uint32_t)bidx;
+        }
+        out[p * nfun + f] = (uint16_t)code;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NT));
 }
 
 }  // namespace pfg

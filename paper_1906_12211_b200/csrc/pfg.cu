@@ -613,6 +613,9 @@ void launch_mc(const float* XY, int ld, int64_t npairs, const Geo& g, const uint
     k_mc_codes<EPL><<<blocks, 256, 0, st>>>(XY, ld, npairs, g.d, g.dp, g.ell, g.cp_draws, sg, cnt);
 }
 
+#ifndef PFG_CP_TC
+#define PFG_CP_TC 1   // exact cross-polytope codes on tcgen05 (kernels_tc.cuh k_cp_tc); 0: the SIMT k_cp_funcs
+#endif
 #ifndef PFG_HP_TC
 #define PFG_HP_TC 1   // SimHash bits / sketches on tcgen05 (3xTF32 + exact band, kernels_tc.cuh); 0: the SIMT GEMM
 #endif
@@ -892,6 +895,19 @@ pfg_status cp_values(pfg_index* I, const float* X, int64_t np, const uint32_t* q
 #define PFG_CP_RW 8
 #endif
     constexpr int RW = PFG_CP_RW;   // rows per warp (register tile RW x NI)
+    if (!qlist && !np_dev && PFG_CP_TC && (g.dpad % 4) == 0 && ((uintptr_t)X % 16) == 0) {
+        // tcgen05 (kernels_tc.cuh k_cp_tc): 3xTF32 values, the exact chains only for near ties
+        const int nt = g.d <= 128 ? 128 : 256;
+        const size_t sm = (size_t)(2 * TC_M * TC_KC + 2 * nt * TC_KC) * 4;
+        const void* fn = nt == 128 ? (const void*)k_cp_tc<128> : (const void*)k_cp_tc<256>;
+        if (set_smem(fn, sm) == cudaSuccess) {
+            const dim3 grid((unsigned)((np + TC_M - 1) / TC_M), (unsigned)nf);
+            if (nt == 128) k_cp_tc<128><<<grid, 128, sm, st>>>(X, np, g.dpad, AT, nf, g.d, d32, g.ell, out);
+            else k_cp_tc<256><<<grid, 128, sm, st>>>(X, np, g.dpad, AT, nf, g.d, d32, g.ell, out);
+            PFG_CUDA(cudaGetLastError());
+            return PFG_OK;
+        }
+    }
     switch (d32 / 32) {
 #define PFG_CP_CASE(NI)                                                                                        \
     case NI: {                                                                                                 \

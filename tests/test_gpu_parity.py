@@ -104,6 +104,26 @@ def test_fht_tables_every_width(d):
         assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
 
 
+@pytest.mark.parametrize("d", [3, 16, 33, 100, 150, 256])
+def test_exact_cp_tables_and_codes_every_width(d):
+    # exact cross-polytope codes on tcgen05 (k_cp_tc: 3xTF32 values, exact chains for near ties;
+    # 128 or 256 hyperplane columns) against the oracle's sequential chains: tables and query codes
+    rng = np.random.default_rng(100 + d)
+    n = 2000 + d
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    q = rng.standard_normal((300, d)).astype(np.float32)
+    g = pfg.Index(_cuda(data), 0, "cp", seed=d, reps=4, cp_draws=200)
+    o = O.OracleIndex(data, O.CP, L=4, seed=d, cp_draws=200)
+    for j in range(4):
+        tab = g.export_table(j)
+        codes, ids = o.rep(j)
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), ids), j
+    gc, _ = g.hash_queries(q)
+    oc, _ = o.hash(q)
+    assert np.array_equal(gc, oc)
+
+
 @pytest.mark.parametrize("name", ["fht", "fht_pool"])
 def test_cp_table_bit_exact(cases, name):
     c = cases[name]
