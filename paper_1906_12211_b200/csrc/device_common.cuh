@@ -31,6 +31,11 @@ __device__ __forceinline__ uint64_t make_key(float sim, uint32_t id) {
 __device__ __forceinline__ uint32_t key_id(uint64_t k) { return ~(uint32_t)k; }
 __device__ __forceinline__ float key_sim(uint64_t k) { return ord2f((uint32_t)(k >> 32)); }
 
+// programmatic dependent launch: a kernel launched with programmatic stream serialisation may start
+// while its predecessor on the stream drains; it waits here (first statement) until the
+// predecessor has completed and its writes are visible.  A no-op for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

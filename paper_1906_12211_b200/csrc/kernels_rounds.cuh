@@ -178,6 +178,7 @@ template <int EPL, typename PP>
 #define PFG_EXPAND_MINB 6
 #endif
 __global__ void __launch_bounds__(128, PFG_EXPAND_MINB) k_expand(PP pp, int par, int lazy) {
+    pdl_wait();
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -444,6 +445,7 @@ __device__ __forceinline__ void scan_wide_tiles(const QueryParams& p, int64_t aw
 #endif
 template <typename PP, bool WIDE>
 __global__ void __launch_bounds__(256, WIDE ? 1 : PFG_SCAN_MINB) k_scan(PP pp, int par) {
+    pdl_wait();
     const QueryParams& p = deref(pp);
     const int lane = threadIdx.x & 31;
     const RoundState& rs = p.rs;
@@ -520,6 +522,7 @@ static_assert(kHC % 128 == 0, "k_dedupe moves the hash set in whole warp steps o
 
 template <typename PP>
 __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
+    pdl_wait();
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -814,6 +817,7 @@ __device__ __forceinline__ int sims_step_i16_half(const QueryParams& p, uint32_t
 // bit 1: a launch outside the device-side loop (its rows are also counted in sims_rows_blind)
 template <typename PP, bool I16>
 __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par, int flags) {
+    pdl_wait();
     const int chunk = flags & 1;
     const QueryParams& p = deref(pp);
     constexpr int NR = I16 ? PFG_I16_NR : kRPI;   // int16 rows are half as long: more rows in flight
@@ -884,6 +888,7 @@ __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_sims(PP pp, int par, int
 // its register budget for the pool):
 template <typename PP, bool I16>
 __global__ void __launch_bounds__(256, PFG_SIMS_MINB) k_wsims(PP pp, int par) {
+    pdl_wait();
     const QueryParams& p = deref(pp);
     constexpr int NR = I16 ? PFG_I16_NR : kRPI;
     constexpr int kSh = NR == 32 ? 0 : NR == 16 ? 1 : NR == 8 ? 2 : 3;
@@ -1013,6 +1018,7 @@ __device__ __forceinline__ void push_fused(const RoundState& rs, uint32_t q) {
 constexpr int kMergeSortMin = PFG_MERGE_SORTMIN;  // keys above the k-th from which k_merge sorts a batch
 template <typename PP, bool WIDE>
 __global__ void __launch_bounds__(128, WIDE ? 8 : PFG_MERGE_MINB) k_merge(PP pp, int par) {
+    pdl_wait();
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

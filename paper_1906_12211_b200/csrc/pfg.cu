@@ -540,6 +540,9 @@ constexpr int kQBMax = 96;     // level-K match ranges precomputed for at most t
 constexpr int kExtReps = 32;   // repetitions hashed in bulk for the queries the fused kernel resumes
 pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
                      const uint32_t* nrows_dev = nullptr, int64_t q0 = 0);
+#ifndef PFG_PDL
+#define PFG_PDL 1   // programmatic dependent launch between the blind rounds' kernels
+#endif
 #ifndef PFG_QTPF
 #define PFG_QTPF 1   // threads per function of the eager FHT-CP query hashing at d' = 128
 #endif
@@ -1982,6 +1985,20 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(occupancy(&occ_m, (const void*)k_merge<QueryParams, false>, 128, msm));
         auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp, bool blind, int64_t m, int share) -> pfg_status {
             using PP = decltype(pp);
+            // the round's kernels start while their predecessor drains (programmatic dependent
+            // launch; each waits in pdl_wait), outside the captured loop graph
+            auto go = [&](auto kern, unsigned grid, unsigned block, size_t sm, auto... args) -> cudaError_t {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(block);
+                cfg.dynamicSmemBytes = sm;
+                cfg.stream = rst;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[0].val.programmaticStreamSerializationAllowed = 1;
+                if (blind && PFG_PDL) { cfg.attrs = at; cfg.numAttrs = 1; }
+                return cudaLaunchKernelEx(&cfg, kern, args...);
+            };
             const int64_t qw = (m + 3) / 4, ns = I->num_sms;
             const unsigned qb_e = (unsigned)std::max<int64_t>(1, std::min<int64_t>(qw, share > 1 ? ns * std::max(1, occ_e / share) : ns * 16));
             const unsigned qb_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>(qw, ns * std::max(1, docc / share)));
@@ -1990,20 +2007,20 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             const unsigned sb = (unsigned)(ns * std::max(1, PFG_SIMS_MINB / share));
             PFG_TRY(phase_mark(I, marks, kPhExpand, rst));
             switch (epl) {
-                case 1: k_expand<1, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
-                case 2: k_expand<2, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
-                case 4: k_expand<4, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
-                case 8: k_expand<8, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
-                case 16: k_expand<16, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
-                default: k_expand<32, PP><<<qb_e, 128, esm, rst>>>(pp, par, lazy ? 1 : 0); break;
+                case 1: PFG_CUDA(go(k_expand<1, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                case 2: PFG_CUDA(go(k_expand<2, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                case 4: PFG_CUDA(go(k_expand<4, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                case 8: PFG_CUDA(go(k_expand<8, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                case 16: PFG_CUDA(go(k_expand<16, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                default: PFG_CUDA(go(k_expand<32, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
             }
             if (blind) { PFG_TRY(dbg_sync("k_expand")); tl_mark(I, "k_expand", rst); }
             PFG_TRY(phase_mark(I, marks, kPhScan, rst));
-            if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_scan<PP, true><<<tb_s, 256, 0, rst>>>(pp, par);
-            else k_scan<PP, false><<<tb_s, 256, 0, rst>>>(pp, par);
+            if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) PFG_CUDA(go(k_scan<PP, true>, tb_s, 256, 0, pp, par));
+            else PFG_CUDA(go(k_scan<PP, false>, tb_s, 256, 0, pp, par));
             if (blind) { PFG_TRY(dbg_sync("k_scan")); tl_mark(I, "k_scan", rst); }
             PFG_TRY(phase_mark(I, marks, kPhDedupe, rst));
-            k_dedupe<PP><<<qb_d, 128, dsm, rst>>>(pp, par);
+            PFG_CUDA(go(k_dedupe<PP>, qb_d, 128, dsm, pp, par));
             if (blind) { PFG_TRY(dbg_sync("k_dedupe")); tl_mark(I, "k_dedupe", rst); }
             PFG_TRY(phase_mark(I, marks, kPhSims, rst));
             const bool kt = ksims_timed && blind;
@@ -2020,18 +2037,18 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n], rst));
             }
             const int sflags = blind ? 2 : 0;
-            if (g.storage == PFG_STORAGE_I16) k_sims<PP, true><<<sb, 256, 0, rst>>>(pp, par, sflags);
-            else k_sims<PP, false><<<sb, 256, 0, rst>>>(pp, par, sflags);
+            if (g.storage == PFG_STORAGE_I16) PFG_CUDA(go(k_sims<PP, true>, sb, 256, 0, pp, par, sflags));
+            else PFG_CUDA(go(k_sims<PP, false>, sb, 256, 0, pp, par, sflags));
             if (kt) PFG_CUDA(cudaEventRecord(I->kev[2 * I->kev_n++ + 1], rst));
             if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) {
                 // wide tiles of the round (tag checks, compaction, similarities)
-                if (g.storage == PFG_STORAGE_I16) k_wsims<PP, true><<<sb, 256, 0, rst>>>(pp, par);
-                else k_wsims<PP, false><<<sb, 256, 0, rst>>>(pp, par);
+                if (g.storage == PFG_STORAGE_I16) PFG_CUDA(go(k_wsims<PP, true>, sb, 256, 0, pp, par));
+                else PFG_CUDA(go(k_wsims<PP, false>, sb, 256, 0, pp, par));
             }
             if (blind) { PFG_TRY(dbg_sync("k_sims")); tl_mark(I, "k_sims", rst); }
             PFG_TRY(phase_mark(I, marks, kPhMerge, rst));
-            if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) k_merge<PP, true><<<qb_m, 128, msm, rst>>>(pp, par);
-            else k_merge<PP, false><<<qb_m, 128, msm, rst>>>(pp, par);
+            if (r.wslots > 0 || !std::is_same<PP, QueryParams>::value) PFG_CUDA(go(k_merge<PP, true>, qb_m, 128, msm, pp, par));
+            else PFG_CUDA(go(k_merge<PP, false>, qb_m, 128, msm, pp, par));
             if (blind) { PFG_TRY(dbg_sync("k_merge")); tl_mark(I, "k_merge", rst); }
             PFG_TRY(phase_mark(I, marks, kPhOther, rst));
             PFG_CUDA(cudaGetLastError());
