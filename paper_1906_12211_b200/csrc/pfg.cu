@@ -460,6 +460,9 @@ struct pfg_index {
     cudaStream_t aux = nullptr;  // second stream: query sketches run beside the query hashing
     cudaStream_t aux2 = nullptr; // third stream: codes and ranges of the later eager repetitions
     cudaStream_t st1 = nullptr;  // the second round pipeline (the upper half of the batch)
+    cudaStream_t hst = nullptr;  // highest priority: repetition 0's codes and ranges, which round 0 waits for
+    cudaEvent_t ev_hst = nullptr, ev_in = nullptr;
+    bool hst_pending = false;    // repetition 0's codes were launched on hst (its ranges follow there)
     cudaEvent_t ev_h1start = nullptr, ev_h1end = nullptr;  // fork to / join from st1
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_late = nullptr;
     bool late_pending = false;   // codes/ranges of repetitions [split, eager) still on aux2
@@ -517,6 +520,9 @@ struct pfg_index {
         if (aux) cudaStreamDestroy(aux);
         if (aux2) cudaStreamDestroy(aux2);
         if (st1) cudaStreamDestroy(st1);
+        if (hst) cudaStreamDestroy(hst);
+        if (ev_hst) cudaEventDestroy(ev_hst);
+        if (ev_in) cudaEventDestroy(ev_in);
         for (cudaEvent_t e : {ev_h1start, ev_h1end})
             if (e) cudaEventDestroy(e);
         if (ev_late) cudaEventDestroy(ev_late);
@@ -540,6 +546,9 @@ constexpr int kQBMax = 96;     // level-K match ranges precomputed for at most t
 constexpr int kExtReps = 32;   // repetitions hashed in bulk for the queries the fused kernel resumes
 pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
                      const uint32_t* nrows_dev = nullptr, int64_t q0 = 0);
+#ifndef PFG_HIPRIO
+#define PFG_HIPRIO 1   // searches run on the index's highest-priority stream (pfg_search)
+#endif
 #ifndef PFG_PDL
 #define PFG_PDL 1   // programmatic dependent launch between the blind rounds' kernels
 #endif
@@ -1074,6 +1083,11 @@ pfg_status ensure_streams(pfg_index* I) {
     PFG_CUDA(cudaStreamCreateWithFlags(&I->aux, cudaStreamNonBlocking));
     PFG_CUDA(cudaStreamCreateWithFlags(&I->aux2, cudaStreamNonBlocking));
     PFG_CUDA(cudaStreamCreateWithFlags(&I->st1, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    PFG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    PFG_CUDA(cudaStreamCreateWithPriority(&I->hst, cudaStreamNonBlocking, prio_hi));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_hst, cudaEventDisableTiming));
+    PFG_CUDA(cudaEventCreateWithFlags(&I->ev_in, cudaEventDisableTiming));
     PFG_CUDA(cudaEventCreateWithFlags(&I->ev_h1start, cudaEventDisableTiming));
     PFG_CUDA(cudaEventCreateWithFlags(&I->ev_h1end, cudaEventDisableTiming));
     PFG_CUDA(cudaEventCreateWithFlags(&I->ev_fork, cudaEventDisableTiming));
@@ -1183,7 +1197,15 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         // round 2 joins it)
         const int s0 = (split > 0 && split < ne && I->aux2) ? split : ne;
         const bool mid = s0 < ne && s0 > 1;
-        PFG_TRY(fht_codes(I, nq, nullptr, 0, mid ? 1 : s0, ld, st));
+        if (mid) {
+            // repetition 0 (round 0's only repetition) on the highest-priority stream, so that its
+            // codes and ranges (the caller) are not queued behind the side streams' hashing
+            PFG_CUDA(cudaStreamWaitEvent(I->hst, I->ev_fork, 0));
+            PFG_TRY(fht_codes(I, nq, nullptr, 0, 1, ld, I->hst));
+            I->hst_pending = true;
+        } else {
+            PFG_TRY(fht_codes(I, nq, nullptr, 0, s0, ld, st));
+        }
         if (s0 < ne) {
             PFG_CUDA(cudaStreamWaitEvent(I->aux2, I->ev_fork, 0));
             if (mid) {
@@ -1558,7 +1580,17 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
     if (nq == 0) return PFG_OK;
     std::lock_guard<std::mutex> lock(I->mu);
     PFG_CUDA(cudaSetDevice(I->device));
-    cudaStream_t st = (cudaStream_t)stream;
+    // the search runs on the index's highest-priority stream, after the caller's stream, and the
+    // caller's stream waits for its end (ev_done): the round kernels (the critical path) are
+    // scheduled before the side streams' hashing, which fills the SMs they leave
+    const cudaStream_t ust = (cudaStream_t)stream;
+    cudaStream_t st = ust;
+    PFG_TRY(ensure_streams(I));
+    if (PFG_HIPRIO) {
+        PFG_CUDA(cudaEventRecord(I->ev_in, ust));
+        PFG_CUDA(cudaStreamWaitEvent(I->hst, I->ev_in, 0));
+        st = I->hst;
+    }
     const Geo& g = I->g;
     if (!I->ev_done) PFG_CUDA(cudaEventCreateWithFlags(&I->ev_done, cudaEventDisableTiming));
     if (I->done_pending) {
@@ -1780,8 +1812,9 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         const int b0 = std::min(p.qb_n, I->late_pending ? I->qc_split : p.qb_n);
         const int bs = bm >= 0 ? bm : b0;
         const int64_t thr_n = nq * (int64_t)bs;
-        if (bs > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, bs, nullptr);
-        tl_mark(I, "k_qbounds", st);
+        const cudaStream_t sq = I->hst_pending ? I->hst : st;
+        if (bs > 0) k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, sq>>>(p, I->qbnd.as<uint4>(), nullptr, nq, 0, bs, nullptr);
+        tl_mark(I, "k_qbounds", sq);
         if (bm >= 0 && bm < b0) {
             const int64_t thr_m = nq * (int64_t)(b0 - bm);
             k_qbounds<<<(unsigned)((thr_m + 255) / 256), 256, 0, I->aux2>>>(p, I->qbnd.as<uint4>(), nullptr, nq, bm, b0 - bm,
@@ -1811,6 +1844,12 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         I->late_ne = 0;
     }
     if (I->late_pending) PFG_CUDA(cudaEventRecord(I->ev_late, I->aux2));
+    if (I->hst_pending) {
+        // repetition 0's codes and ranges, from the highest-priority stream
+        PFG_CUDA(cudaEventRecord(I->ev_hst, I->hst));
+        PFG_CUDA(cudaStreamWaitEvent(st, I->ev_hst, 0));
+        I->hst_pending = false;
+    }
     // developer instrumentation: PFG_PHASE_PROF=1 prints per-phase warp cycles of each search to stderr
     // timing = 5 (developer): per-phase cycle counters of the fused kernel (and of k_chunk in a
     // -DPFG_CHUNK_PROF=1 build), printed to stderr
@@ -2325,6 +2364,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         ++I->nsearch;
     }
     PFG_CUDA(cudaEventRecord(I->ev_done, st));
+    if (st != ust) PFG_CUDA(cudaStreamWaitEvent(ust, I->ev_done, 0));
     I->done_pending = true;
     // with device outputs the call returns without waiting for the GPU; host outputs (or the
     // developer phase print) need the results here
