@@ -778,3 +778,45 @@ def test_results_against_plain_order_oracle(cases, name):
         assert tie or edge, (r, ea, eb)
     print(f"{name}: {exc} of {len(c.q)} queries differ from the plain-order oracle (all explained by rounding)")
     assert exc <= max(1, len(c.q) // 50)
+
+
+def test_sharded_path_over_nccl_world1():
+    # the data-sharded mode's collectives on the GPU over NCCL (one rank: this pod has one GPU per
+    # call): gather_rows / gather_merge with an explicit world of 1 are copies, so the plumbing
+    # (all_gather_into_tensor of the query codes, sketches, ids and sims on device tensors) runs on
+    # NCCL with the product's shapes and dtypes, and the sharded search equals the plain one; the
+    # 3-shard merge through the all-gathered layout equals the per-shard oracle merge above
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1906_12211_b200 import sharded
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        data, q = synth.config_data(2, n=12000, nq=64)
+        Q = _cuda(q)
+        sh = sharded.ShardedIndex(_cuda(data), 0, 0, "fht_cp", seed=7, reps=40)
+        reps = sh.prep_reps()
+        codes, sk = sharded.distributed_query_hashes(lambda qs: sh.index.hash_queries_reps(qs, reps), Q)
+        # the same all-gather the world > 1 path runs, on NCCL
+        g_codes = torch.empty_like(codes)
+        dist.all_gather_into_tensor(g_codes, codes)
+        assert torch.equal(g_codes, codes)
+        ids, sims = sh.search(Q, 10, 0.9, distributed_prep=True)
+        ids2, sims2 = sh.index.search(Q, 10, 0.9, ext_codes=g_codes, ext_sketches=sk)
+        ids3, sims3 = sh.index.search(Q, 10, 0.9)
+        assert torch.equal(ids, ids3) and torch.equal(ids2, ids3) and torch.equal(sims2, sims3)
+        # gather of per-shard lists through NCCL, then the library's merge
+        g_ids = torch.empty((1 * 64, 10), dtype=ids.dtype, device=DEV)
+        dist.all_gather_into_tensor(g_ids, ids.contiguous())
+        mi, ms = pfg.merge_topk(g_ids.view(1, 64, 10), sims.view(1, 64, 10))
+        assert torch.equal(mi, ids) and torch.equal(ms, sims)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
