@@ -173,11 +173,13 @@ constexpr int kTile = PFG_TILE;   // emitted positions per scan tile
 #endif
 constexpr int kDedupeLong = PFG_DLONG;  // emitted positions from which k_dedupe schedules a chunk first
 
-template <int EPL, typename PP>
+// LZ = false: a round whose repetitions all have precomputed codes (the host knows the largest
+// repetition a round can reach), compiled without the lazy hashing (fewer registers, more warps)
+template <int EPL, typename PP, bool LZ = true>
 #ifndef PFG_EXPAND_MINB
 #define PFG_EXPAND_MINB 6
 #endif
-__global__ void __launch_bounds__(128, PFG_EXPAND_MINB) k_expand(PP pp, int par, int lazy) {
+__global__ void __launch_bounds__(128, LZ ? PFG_EXPAND_MINB : 8) k_expand(PP pp, int par, int lazy) {
     pdl_wait();
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(128, PFG_EXPAND_MINB) k_expand(PP pp, int par,
         uint32_t probes = 0;
         if (i == p.K) {
             if (lane < nr && c0 + lane < p.qc_n) c->qc[lane] = __ldg(p.qcodes + q * p.qc_ld + c0 + lane);
-            if (c0 + nr > p.qc_n) {
+            if (LZ && c0 + nr > p.qc_n) {
                 for (int t = lane; t < p.dpad; t += 32) qrow[t] = p.qx[q * p.dpad + t];
                 __syncwarp();
                 group_rep_codes<EPL>(qrow, p.d, p.dp, p.ell, p.c, p.K, p.sg, c0, max(0, p.qc_n - c0), nr, c->qc, lane);

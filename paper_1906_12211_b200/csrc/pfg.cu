@@ -2022,7 +2022,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(occupancy(&occ_e, (const void*)k_expand<1, QueryParams>, 128, esm));
         PFG_CUDA(occupancy(&occ_s, (const void*)k_scan<QueryParams, false>, 256, 0));
         PFG_CUDA(occupancy(&occ_m, (const void*)k_merge<QueryParams, false>, 128, msm));
-        auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp, bool blind, int64_t m, int share) -> pfg_status {
+        auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp, bool blind, int64_t m, int share,
+                                bool lz = true) -> pfg_status {
             using PP = decltype(pp);
             // the round's kernels start while their predecessor drains (programmatic dependent
             // launch; each waits in pdl_wait), outside the captured loop graph
@@ -2045,13 +2046,18 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             const unsigned tb_s = share > 1 ? (unsigned)(ns * std::max(1, occ_s / share)) : (unsigned)(ns * 8);
             const unsigned sb = (unsigned)(ns * std::max(1, PFG_SIMS_MINB / share));
             PFG_TRY(phase_mark(I, marks, kPhExpand, rst));
-            switch (epl) {
-                case 1: PFG_CUDA(go(k_expand<1, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
-                case 2: PFG_CUDA(go(k_expand<2, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
-                case 4: PFG_CUDA(go(k_expand<4, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
-                case 8: PFG_CUDA(go(k_expand<8, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
-                case 16: PFG_CUDA(go(k_expand<16, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
-                default: PFG_CUDA(go(k_expand<32, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+            if (!lz && std::is_same<PP, QueryParams>::value) {
+                // every repetition this round can reach has its code: no lazy hashing compiled in
+                PFG_CUDA(go(k_expand<1, PP, false>, qb_e, 128, esm, pp, par, lazy ? 1 : 0));
+            } else {
+                switch (epl) {
+                    case 1: PFG_CUDA(go(k_expand<1, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                    case 2: PFG_CUDA(go(k_expand<2, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                    case 4: PFG_CUDA(go(k_expand<4, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                    case 8: PFG_CUDA(go(k_expand<8, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                    case 16: PFG_CUDA(go(k_expand<16, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                    default: PFG_CUDA(go(k_expand<32, PP>, qb_e, 128, esm, pp, par, lazy ? 1 : 0)); break;
+                }
             }
             if (blind) { PFG_TRY(dbg_sync("k_expand")); tl_mark(I, "k_expand", rst); }
             PFG_TRY(phase_mark(I, marks, kPhScan, rst));
@@ -2169,12 +2175,30 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             fused_n = 0;
             I->last_rounds = round;
         } else {
+        const int qb_n0 = p.qb_n;   // (the fused tail extends the codes of its own list from here)
         while (round < max_rounds) {
             // round 0 is the single repetition 0 with tau = 64 (no sketches read); round 1 reaches
             // repetitions < 1 + R; later rounds may reach every eager repetition
             if (round == 1) { PFG_TRY(join_sketches(I, st)); PFG_TRY(mid_join(I, st)); }
             if (round == 2) PFG_TRY(late_join(I, st));
-            PFG_TRY(launch_round(round & 1, st, tm, p, true, nq, 1));
+            // the largest repetition this round can reach (one chunk per round; a level's chunks
+            // restart at repetition 0)
+            const int64_t reach = s.uniform ? (int64_t)s.R * (round + 1) : 1 + (int64_t)s.R * round;
+            if (round >= 3 && reach > p.qc_n && lazy && I->qc_n > 0 && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+                // the few queries still running after three rounds: codes and level-K ranges of the
+                // next kExtReps repetitions in bulk (one thread per query and repetition) instead of
+                // one lane group per query inside k_expand; the fused tail reuses them
+                RoundState& r = p.rs;
+                const int par = round & 1, r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
+                PFG_TRY(fht_codes(I, nq, r.act[par], r0, nr, I->qc_ld, st, &r.ctl->nact[par]));
+                const int64_t thr_n = nq * (int64_t)nr;
+                k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.act[par], nq, r0, nr,
+                                                                         &r.ctl->nact[par]);
+                PFG_CUDA(cudaGetLastError());
+                I->launches += 2;
+                p.qc_n = p.qb_n = I->qc_ld;
+            }
+            PFG_TRY(launch_round(round & 1, st, tm, p, true, nq, 1, !(reach <= p.qc_n)));
             I->launches += 5;
             ++round;
         }
@@ -2218,7 +2242,8 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 I->launches += 2;
                 p1.qc_n = g.L;
             }
-            if (lazy && I->qc_n > 0 && I->qc_ld > I->qc_n && p.qb_n == I->qc_n) {
+            // (every query handed to the fused kernel, also those handed off before round 3)
+            if (lazy && I->qc_n > 0 && I->qc_ld > I->qc_n && qb_n0 == I->qc_n) {
                 const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
                 PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, I->aux, &r.ctl->nfused));
                 const int64_t thr_n = nq * (int64_t)nr;

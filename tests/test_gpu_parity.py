@@ -258,9 +258,12 @@ def test_tensor_build_bit_exact(cases, name):
 @pytest.mark.parametrize("name", ["fht_long", "fht_d40", "fht_d20"])
 @pytest.mark.parametrize("recall", [0.9, 0.99])
 @pytest.mark.parametrize("engine", [0, 1, 2])
-def test_search_parity_lazy_hashing(cases, name, recall, engine):
+@pytest.mark.parametrize("R", [8, 16])
+def test_search_parity_lazy_hashing(cases, name, recall, engine, R):
+    # R = 16: round 3 reaches repetition 49, beyond the eager depth: the active queries' codes and
+    # ranges of the next repetitions are computed in bulk before it (engine 0)
     c = cases[name]
-    st = _compare(c, 10, recall, dict(rep_chunk=8, engine=engine), dict(rep_chunk=8))
+    st = _compare(c, 10, recall, dict(rep_chunk=R, engine=engine), dict(rep_chunk=R))
     if recall == 0.99:
         assert np.any(st["j_stop"] > 32) or np.any(st["i_stop"] < 24), "no query reached the lazily hashed repetitions"
 
