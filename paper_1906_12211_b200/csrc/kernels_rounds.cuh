@@ -628,7 +628,11 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                 if (v[u] != kEmpty && !hs_quad(w4[u], v[u], h[u], found[u])) found[u] = hs_lookup4(c->hs, v[u], h[u]);
             }
             // claims of the rest in (repetition, position) order, u in order; a later occurrence
-            // of an id claimed earlier in the batch finds it in the set
+            // of an id claimed earlier in the batch finds it in the set.  The per-tile duplicate
+            // counts are kept in registers and added to the repetition's count once per tile.
+            uint32_t dsum[kTPB];
+#pragma unroll
+            for (int b = 0; b < kTPB; ++b) dsum[b] = 0;
 #pragma unroll
             for (int u = 0; u < kCPre; ++u) {
                 if ((uint32_t)((u % (kTile / 32)) * 32) >= tc[u / (kTile / 32)]) continue;  // empty step (warp-uniform)
@@ -653,10 +657,15 @@ __global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
                 // are the live lanes that claimed nothing
                 const int b = u / (kTile / 32);
                 const uint32_t live = min(32u, tc[b] - (uint32_t)((u % (kTile / 32)) * 32));
-                if (lane == 0) {
-                    if (u % (kTile / 32) == 0) c->fcnt[trep[b]] += tc[b];  // passing the filter (filtered = emitted - passing)
-                    c->dcnt[trep[b]] += live - __popc(fm);
-                }
+                dsum[b] += live - __popc(fm);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int b = 0; b < kTPB; ++b)
+                    if (tc[b]) {
+                        c->fcnt[trep[b]] += tc[b];   // passing the filter (filtered = emitted - passing)
+                        c->dcnt[trep[b]] += dsum[b];
+                    }
             }
             if (nE + ns > rs.hmax) overflow = true;
         }
