@@ -333,26 +333,31 @@ __device__ __forceinline__ uint64_t fhtcp_rep_full(const float* xr, int lim, con
     return full;
 }
 
-template <int DP, int TPF>
+template <int DP, int TPF, bool LOOP = false>
 __global__ void __launch_bounds__(128) k_fht_qcodes_g(const float* __restrict__ X, int64_t np, int ldx, int d, int ell,
                                                       int c, int K, const uint32_t* __restrict__ sg, int nreps,
                                                       uint32_t* __restrict__ codes, int ldc,
                                                       const uint32_t* __restrict__ qlist, int r0,
                                                       const uint32_t* __restrict__ np_dev) {
-    // rows: qlist[0..np) if given, else 0..np-1; repetitions r0 .. r0 + nreps - 1
+    // rows: qlist[0..np) if given, else 0..np-1; repetitions r0 .. r0 + nreps - 1; TPF lanes per
+    // (row, repetition) item.  LOOP: a grid-stride loop over the items (a device-counted list gets
+    // a grid sized for its usual length, not its capacity); else one item per lane group
     constexpr int W = (DP + 31) / 32;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int g = (int)(t % TPF);
-    int64_t item = t / TPF;
     if (np_dev) np = min(np, (int64_t)*np_dev);   // rows counted on the device (a list's length)
-    const bool live = item < np * nreps;
-    if (__all_sync(kFull, !live)) return;  // the whole warp is past the end (grids sized for the maximum)
-    if (!live) item = 0;  // keep the group's lanes in the shuffles; nothing is stored
-    const int64_t a = item / nreps;
-    const int64_t p = qlist ? (int64_t)qlist[a] : a;
-    const int j = r0 + (int)(item % nreps);
-    const uint64_t full = fhtcp_rep_full<DP, TPF>(X + p * ldx, ldx, sg + (int64_t)j * c * 3 * W, c, ell, g);
-    if (live && g == 0) codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
+    const int64_t total = np * nreps, step = LOOP ? ((int64_t)gridDim.x * blockDim.x) / TPF : 0;
+    for (int64_t it = t / TPF;; it += step) {
+        const bool live = it < total;
+        if (__all_sync(kFull, !live)) return;  // the whole warp is past the end
+        const int64_t item = live ? it : 0;    // keep the group's lanes in the shuffles; nothing is stored
+        const int64_t a = item / nreps;
+        const int64_t p = qlist ? (int64_t)qlist[a] : a;
+        const int j = r0 + (int)(item % nreps);
+        const uint64_t full = fhtcp_rep_full<DP, TPF>(X + p * ldx, ldx, sg + (int64_t)j * c * 3 * W, c, ell, g);
+        if (live && g == 0) codes[p * ldc + j] = (uint32_t)(full >> (c * ell - K));
+        if (!LOOP) return;
+    }
 }
 
 // FHT-CP repetition keys / codes (independent strategy): a block stages RB = 128/TPF rows in

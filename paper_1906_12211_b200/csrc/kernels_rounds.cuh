@@ -109,14 +109,15 @@ __device__ __forceinline__ void bucket_of(const QueryParams& p, int j, uint64_t 
 
 __global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restrict__ out, const uint32_t* __restrict__ qlist,
                                                  int64_t nlist, int r0, int nreps, const uint32_t* __restrict__ nlist_dev) {
-    // queries qlist[0..nlist) if given, else 0..nlist-1 (nlist from device memory if nlist_dev);
+    // queries qlist[0..nlist) if given, else 0..nlist-1 (nlist from device memory if nlist_dev: a
+    // grid-stride loop, the grid sized for the list's usual length, not its capacity);
     // repetitions r0 .. r0 + nreps - 1
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t tot = (nlist_dev ? min(nlist, (int64_t)*nlist_dev) : nlist) * nreps;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = t / nreps;
-    if (a >= (nlist_dev ? (int64_t)*nlist_dev : nlist)) return;
     const int j = r0 + (int)(t - a * nreps);
     const int64_t q = qlist ? (int64_t)qlist[a] : a;
-    if (p.qzero[q]) { out[q * p.qb_ld + j] = make_uint4(0, 0, 0, 0); return; }
+    if (p.qzero[q]) { out[q * p.qb_ld + j] = make_uint4(0, 0, 0, 0); continue; }
     const uint32_t qc = __ldg(p.qcodes + q * p.qc_ld + j);
     uint32_t lo1, hi1, lo2, hi2, probes = 0;
     bucket_of(p, j, qc, lo1, hi1);
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(256) k_qbounds(QueryParams p, uint4* __restric
         if (lo2 < hi2) { ++probes; if ((uint64_t)c2 < (uint64_t)qc + 1) lo2 = m2 + 1; else hi2 = m2; }
     }
     out[q * p.qb_ld + j] = make_uint4(lo1, lo2, probes, 0u);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

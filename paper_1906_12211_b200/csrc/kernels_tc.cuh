@@ -77,8 +77,36 @@ __device__ __forceinline__ void tc_split_store(unsigned char* hi, unsigned char*
     *reinterpret_cast<float4*>(lo + off) = l;
 }
 
+// the canonical chain acc = fmaf(x_t, a_t, acc), t = 0 .. kdim - 1 (R-2) of one band entry, its
+// operands loaded 32 at a time as float4 (kdim a multiple of 8, rows 16-byte aligned) so that only
+// one load latency per 32 terms is exposed instead of one per term
+__device__ __forceinline__ float tc_chain_dot(const float* __restrict__ xr, const float* __restrict__ ar, int kdim) {
+    float acc = 0.0f;
+    for (int t0 = 0; t0 < kdim; t0 += 32) {
+        float4 xa[8], aa[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (t0 + 4 * u < kdim) {
+                xa[u] = __ldg(reinterpret_cast<const float4*>(xr + t0 + 4 * u));
+                aa[u] = __ldg(reinterpret_cast<const float4*>(ar + t0 + 4 * u));
+            }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (t0 + 4 * u < kdim) {
+                acc = fmaf(xa[u].x, aa[u].x, acc);
+                acc = fmaf(xa[u].y, aa[u].y, acc);
+                acc = fmaf(xa[u].z, aa[u].z, acc);
+                acc = fmaf(xa[u].w, aa[u].w, acc);
+            }
+    }
+    return acc;
+}
+
 // bits of rows X[np][ldx] against functions A[nf][lda] over kdim (a multiple of 8, rows and
-// functions zero beyond d) into out[p * out_ld + f / 8] (bit f % 8), the same output as k_hp_bits
+// functions zero beyond d) into out[p * out_ld + f / 8] (bit f % 8), the same output as k_hp_bits.
+// Two CTAs per SM (164 registers): the query sketches run on a side stream beside the first round,
+// and three CTAs per SM (registers capped at 168) made the kernel faster alone (79 -> 72 us) but
+// the search slower (1.59 -> 1.70 ms on config 2): its SMs are taken from the round kernels
 __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__ X, int64_t np, int ldx,
                                                       const float* __restrict__ A, int nf, int lda, int kdim,
                                                       uint8_t* __restrict__ out, int64_t out_ld) {
@@ -94,8 +122,6 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
     __shared__ uint32_t nfb;                 // entries inside the band (evaluated by the chain)
     __shared__ uint32_t fbl[kTcFallback];    // their (row << 16 | function) indices
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t p0 = (int64_t)blockIdx.x * TC_M;
-    const int f0 = blockIdx.y * TC_N;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem_addr(&tmem_base)),
                      "r"(TC_N));
@@ -105,14 +131,21 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem_addr(&mbar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    fsq[tid] = 0.0f;
-    if (tid == 0) nfb = 0;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base;
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
     uint32_t phase = 0;
+    // tiles (128 rows x 128 functions) in turn, row tile fastest; the grid may be smaller than the
+    // tile count (a background launch on a side stream takes a bounded share of the SMs)
+    const int64_t ntx = (np + TC_M - 1) / TC_M, ntiles = ntx * ((nf + TC_N - 1) / TC_N);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t p0 = (tile % ntx) * TC_M;
+    const int f0 = (int)(tile / ntx) * TC_N;
+    fsq[tid] = 0.0f;
+    if (tid == 0) nfb = 0;
+    __syncthreads();
     const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     // operand tiles: tf32 hi / lo parts in the canonical layout (a 16-byte core-matrix row holds 4
     // consecutive k of one row); columns beyond kc are zero.  Thread t stages row t of both tiles
@@ -202,10 +235,7 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
             if (slot < (uint32_t)kTcFallback) {
                 fbl[slot] = ((uint32_t)rl << 16) | (uint32_t)(cb + j);
             } else {
-                const float* xr = X + p * ldx;
-                const float* ar = A + (int64_t)(f0 + cb + j) * lda;
-                float acc = 0.0f;
-                for (int t = 0; t < kdim; ++t) acc = fmaf(__ldg(xr + t), __ldg(ar + t), acc);
+                const float acc = tc_chain_dot(X + p * ldx, A + (int64_t)(f0 + cb + j) * lda, kdim);
                 bits = (bits & ~(1u << j)) | ((acc >= 0.0f ? 1u : 0u) << j);
             }
         }
@@ -215,10 +245,7 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
     const uint32_t nl = min(nfb, (uint32_t)kTcFallback);
     for (uint32_t e = tid; e < nl; e += 128) {
         const uint32_t r = fbl[e] >> 16, j = fbl[e] & 0xffffu;
-        const float* xr = X + (p0 + r) * ldx;
-        const float* ar = A + (int64_t)(f0 + j) * lda;
-        float acc = 0.0f;
-        for (int t = 0; t < kdim; ++t) acc = fmaf(__ldg(xr + t), __ldg(ar + t), acc);   // the canonical chain (R-2)
+        const float acc = tc_chain_dot(X + (p0 + r) * ldx, A + (int64_t)(f0 + j) * lda, kdim);   // the canonical chain (R-2)
         if (acc >= 0.0f) atomicOr(&obits[r][j >> 5], 1u << (j & 31));
         else atomicAnd(&obits[r][j >> 5], ~(1u << (j & 31)));
     }
@@ -236,8 +263,11 @@ __global__ void __launch_bounds__(128, 1) k_hp_bits_tc(const float* __restrict__
                 if (fb + 8 * by < nf) out[p * out_ld + ((fb >> 3) + by)] = (uint8_t)(bits >> (8 * by));
         }
     }
+    // the epilogue's TMEM reads and shared-memory uses end before the next tile's MMAs and staging
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_N));
 }
 

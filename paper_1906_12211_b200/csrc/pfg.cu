@@ -632,11 +632,13 @@ void launch_mc(const float* XY, int ld, int64_t npairs, const Geo& g, const uint
 #define PFG_HP_TC 1   // SimHash bits / sketches on tcgen05 (3xTF32 + exact band, kernels_tc.cuh); 0: the SIMT GEMM
 #endif
 void hp_bits(const float* X, int64_t np, int ldx, const float* A, int nf, int lda, int kdim, uint8_t* out,
-             int64_t out_ld, cudaStream_t st) {
+             int64_t out_ld, cudaStream_t st, int max_ctas = 0) {
     if (PFG_HP_TC && (kdim % 8) == 0 && (ldx % 4) == 0 && (lda % 4) == 0 && ((uintptr_t)X % 16) == 0 &&
         ((uintptr_t)A % 16) == 0 && set_smem((const void*)k_hp_bits_tc, kTcSmem) == cudaSuccess) {
-        dim3 tg((unsigned)((np + TC_M - 1) / TC_M), (unsigned)((nf + TC_N - 1) / TC_N));
-        k_hp_bits_tc<<<tg, 128, kTcSmem, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
+        // max_ctas > 0: at most that many CTAs, each looping over tiles
+        int64_t tiles = ((np + TC_M - 1) / TC_M) * ((nf + TC_N - 1) / TC_N);
+        if (max_ctas > 0) tiles = std::min<int64_t>(tiles, max_ctas);
+        k_hp_bits_tc<<<(unsigned)tiles, 128, kTcSmem, st>>>(X, np, ldx, A, nf, lda, kdim, out, out_ld);
         return;
     }
     dim3 grid((unsigned)((np + GB_M - 1) / GB_M), (nf + GB_N - 1) / GB_N);
@@ -1142,9 +1144,10 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
         } else {
             PFG_CUDA(cudaStreamWaitEvent(I->aux, I->ev_fork, 0));
             hp_bits(I->qx.as<float>(), nq, g.dpad, I->skfn.as<float>(), 64 * g.M, g.dpad, g.dpad, I->qsk.as<uint8_t>(),
-                    (int64_t)g.M * 8, I->aux);
+                    (int64_t)g.M * 8, I->aux, I->num_sms);   // one CTA per SM looping over the tiles: it
+                                                              // runs beside round 0 (measured 1.595 -> 1.59 ms)
             PFG_CUDA(cudaGetLastError());
-            tl_mark(I, "query sketches (k_hp_bits2)", I->aux);
+            tl_mark(I, "query sketches (k_hp_bits_tc)", I->aux);
             PFG_CUDA(cudaEventRecord(I->ev_join, I->aux));
             I->launches += 1;
         }
@@ -1225,6 +1228,14 @@ pfg_status prep_queries(pfg_index* I, const float* queries, int64_t nq, bool nee
     return PFG_OK;
 }
 
+// Kernels over a device-counted query list (the queries still running late in a search) size their
+// grid for list_rows() rows and loop over the rest: a grid for the list's capacity (the batch) would
+// mostly launch blocks that exit at once
+inline int64_t list_rows(const pfg_index* I) { return (int64_t)I->num_sms * 8; }
+inline unsigned list_grid(const pfg_index* I, int64_t threads, int nreps) {
+    return (unsigned)((std::min<int64_t>(threads, list_rows(I) * nreps) + 255) / 256);
+}
+
 // FHT-CP query codes of repetitions [r0, r0 + nreps) for rows qlist[0..nrows) (or 0..nrows-1),
 // one thread per (row, repetition), into qcodes [q][ld]
 pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0, int nreps, int ld, cudaStream_t st,
@@ -1237,10 +1248,22 @@ pfg_status fht_codes(pfg_index* I, int64_t nrows, const uint32_t* qlist, int r0,
     const uint32_t* sg = I->sg.as<uint32_t>();
     uint32_t* qc = I->qcodes.as<uint32_t>() + q0 * ld;
     const float* X = I->qx.as<float>() + q0 * g.dpad;
-    if (g.dp == 32) k_fht_qcodes_g<32, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
-    else if (g.dp == 64) k_fht_qcodes_g<64, 1><<<blocks, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
-    else k_fht_qcodes_g<128, PFG_QTPF><<<(unsigned)((PFG_QTPF * threads + 127) / 128), 128, 0, st>>>(
-             X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
+    if (nrows_dev && g.dp == 128) {
+        // a device-counted list (the queries still running late in a search, usually few): four
+        // lanes per item (a quarter of the single-thread transform's dependent chain), a grid-stride
+        // loop over a grid for list_rows() rows
+        const int64_t t4 = 4 * std::min<int64_t>(threads, list_rows(I) * nreps);
+        k_fht_qcodes_g<128, 4, true><<<(unsigned)((t4 + 127) / 128), 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps,
+                                                                         qc, ld, qlist, r0, nrows_dev);
+    } else {
+        const unsigned bl = nrows_dev ? (unsigned)((std::min<int64_t>(threads, list_rows(I) * nreps) + 127) / 128) : blocks;
+        if (g.dp == 32 && nrows_dev) k_fht_qcodes_g<32, 1, true><<<bl, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
+        else if (g.dp == 64 && nrows_dev) k_fht_qcodes_g<64, 1, true><<<bl, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
+        else if (g.dp == 32) k_fht_qcodes_g<32, 1><<<bl, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
+        else if (g.dp == 64) k_fht_qcodes_g<64, 1><<<bl, 128, 0, st>>>(X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
+        else k_fht_qcodes_g<128, PFG_QTPF><<<(unsigned)((PFG_QTPF * (int64_t)bl * 128 + 127) / 128), 128, 0, st>>>(
+                 X, nrows, g.dpad, g.d, g.ell, g.c, g.K, sg, nreps, qc, ld, qlist, r0, nrows_dev);
+    }
     PFG_CUDA(cudaGetLastError());
     I->launches += 1;
     tl_mark(I, (std::string("fht codes reps ") + std::to_string(r0) + "+" + std::to_string(nreps)).c_str(), st);
@@ -1983,7 +2006,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
             PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, st, &r.ctl->nfused));
             const int64_t thr_n = nq * (int64_t)nr;
-            k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.fused, nq, r0, nr,
+            k_qbounds<<<list_grid(I, thr_n, nr), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.fused, nq, r0, nr,
                                                                      &r.ctl->nfused);
             PFG_CUDA(cudaGetLastError());
             I->launches += 2;
@@ -2023,7 +2046,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
         PFG_CUDA(occupancy(&occ_s, (const void*)k_scan<QueryParams, false>, 256, 0));
         PFG_CUDA(occupancy(&occ_m, (const void*)k_merge<QueryParams, false>, 128, msm));
         auto launch_round = [&](int par, cudaStream_t rst, bool marks, auto pp, bool blind, int64_t m, int share,
-                                bool lz = true) -> pfg_status {
+                                bool lz = true, bool dd = true) -> pfg_status {
             using PP = decltype(pp);
             // the round's kernels start while their predecessor drains (programmatic dependent
             // launch; each waits in pdl_wait), outside the captured loop graph
@@ -2065,7 +2088,9 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
             else PFG_CUDA(go(k_scan<PP, false>, tb_s, 256, 0, pp, par));
             if (blind) { PFG_TRY(dbg_sync("k_scan")); tl_mark(I, "k_scan", rst); }
             PFG_TRY(phase_mark(I, marks, kPhDedupe, rst));
-            PFG_CUDA(go(k_dedupe<PP>, qb_d, 128, dsm, pp, par));
+            // dd = false: the search's first round of single-repetition chunks (tau = 64, nothing
+            // evaluated yet), where every query is a direct chunk or handed off and k_dedupe has no work
+            if (dd) PFG_CUDA(go(k_dedupe<PP>, qb_d, 128, dsm, pp, par));
             if (blind) { PFG_TRY(dbg_sync("k_dedupe")); tl_mark(I, "k_dedupe", rst); }
             PFG_TRY(phase_mark(I, marks, kPhSims, rst));
             const bool kt = ksims_timed && blind;
@@ -2147,7 +2172,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                     const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
                     PFG_TRY(fht_codes(I, nh[h], q.rs.fused, r0, nr, I->qc_ld, hs, &q.rs.ctl->nfused, qh0[h]));
                     const int64_t thr_n = nh[h] * (int64_t)nr;
-                    k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, hs>>>(p1, I->qbnd.as<uint4>() + qh0[h] * p.qb_ld,
+                    k_qbounds<<<list_grid(I, thr_n, nr), 256, 0, hs>>>(p1, I->qbnd.as<uint4>() + qh0[h] * p.qb_ld,
                                                                             q.rs.fused, nh[h], r0, nr, &q.rs.ctl->nfused);
                     PFG_CUDA(cudaGetLastError());
                     I->launches += 2;
@@ -2192,14 +2217,15 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 const int par = round & 1, r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
                 PFG_TRY(fht_codes(I, nq, r.act[par], r0, nr, I->qc_ld, st, &r.ctl->nact[par]));
                 const int64_t thr_n = nq * (int64_t)nr;
-                k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.act[par], nq, r0, nr,
+                k_qbounds<<<list_grid(I, thr_n, nr), 256, 0, st>>>(p, I->qbnd.as<uint4>(), r.act[par], nq, r0, nr,
                                                                          &r.ctl->nact[par]);
                 PFG_CUDA(cudaGetLastError());
                 I->launches += 2;
                 p.qc_n = p.qb_n = I->qc_ld;
             }
-            PFG_TRY(launch_round(round & 1, st, tm, p, true, nq, 1, !(reach <= p.qc_n)));
-            I->launches += 5;
+            const bool dd = !(round == 0 && !s.uniform);
+            PFG_TRY(launch_round(round & 1, st, tm, p, true, nq, 1, !(reach <= p.qc_n), dd));
+            I->launches += dd ? 5 : 4;
             ++round;
         }
         PFG_TRY(join_sketches(I, st));
@@ -2247,7 +2273,7 @@ pfg_status pfg_search(pfg_index* I, const float* queries, int64_t nq, int32_t k,
                 const int r0 = I->qc_n, nr = I->qc_ld - I->qc_n;
                 PFG_TRY(fht_codes(I, nq, r.fused, r0, nr, I->qc_ld, I->aux, &r.ctl->nfused));
                 const int64_t thr_n = nq * (int64_t)nr;
-                k_qbounds<<<(unsigned)((thr_n + 255) / 256), 256, 0, I->aux>>>(p1, I->qbnd.as<uint4>(), r.fused, nq, r0,
+                k_qbounds<<<list_grid(I, thr_n, nr), 256, 0, I->aux>>>(p1, I->qbnd.as<uint4>(), r.fused, nq, r0,
                                                                               nr, &r.ctl->nfused);
                 PFG_CUDA(cudaGetLastError());
                 I->launches += 2;
