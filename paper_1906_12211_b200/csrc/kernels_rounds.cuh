@@ -525,7 +525,7 @@ constexpr int kCPre = PFG_CPRE;   // candidate ids loaded per lane per batch
 static_assert(kHC % 128 == 0, "k_dedupe moves the hash set in whole warp steps of 128 slots");
 
 template <typename PP>
-__global__ void __launch_bounds__(128) k_dedupe(PP pp, int par) {
+__global__ void __launch_bounds__(128, 6) k_dedupe(PP pp, int par) {   // 6 blocks: the shared-memory limit
     pdl_wait();
     const QueryParams& p = deref(pp);
     extern __shared__ __align__(16) unsigned char smem_raw[];
