@@ -343,6 +343,50 @@ def test_search_parity_options(cases, name, kw, engine):
     _compare(c, 10, 0.9, dict(kw, engine=engine), okw)
 
 
+def _per_level_emitted(runs, K):
+    """emitted positions per (query, level) from searches that differ only in the recall target: with
+    the filter off and the stop rule checked once per level (stop_granularity 1) the positions a query
+    retrieves down to a level do not depend on the target, so the totals of two runs that stop at
+    levels i and i + 1 differ by exactly what level i emitted; level K's count is the total of a run
+    that stops there.  runs: [(i_stop[nq], emitted[nq])]; returns {(query, level): count}"""
+    nq = len(runs[0][0])
+    out = {}
+    for r in range(nq):
+        tot = {}
+        for i_stop, emitted in runs:
+            i, e = int(i_stop[r]), int(emitted[r])
+            assert tot.setdefault(i, e) == e, "the total at a stop level depends on the recall target"
+        for i, e in tot.items():
+            if i == K:
+                out[(r, i)] = e
+            elif i + 1 in tot:
+                assert e >= tot[i + 1]
+                out[(r, i)] = e - tot[i + 1]
+    return out
+
+
+@pytest.mark.parametrize("name", ["hp", "fht", "hp_pool"])
+@pytest.mark.parametrize("engine", [0, 1])
+def test_emitted_per_level(cases, name, engine):
+    # SURVEY 8(c) parity object "emitted-position count per level", reconstructed on each side from
+    # its own totals along a ladder of recall targets and compared cell by cell
+    c = cases[name]
+    K = 24
+    ladder = [0.05, 0.2, 0.35, 0.5, 0.65, 0.8, 0.9, 0.95, 0.98, 0.995, 0.999]
+    g_runs, o_runs = [], []
+    for recall in ladder:
+        _, _, st = c.gpu.search(_cuda(c.q), 10, recall, stats=True, rep_chunk=8, engine=engine, use_filter=False,
+                                per_round=True)
+        _, _, otr = c.orc.search(c.q, 10, recall, rep_chunk=8, use_filter=False, per_round=True)
+        assert np.array_equal(st["j_stop"][st["i_stop"] > 0], np.full(int((st["i_stop"] > 0).sum()), c.orc.L))
+        g_runs.append((st["i_stop"].copy(), st["emitted"].copy()))
+        o_runs.append((otr[:, 0].copy(), otr[:, 2].astype(np.uint32)))
+    g, o = _per_level_emitted(g_runs, K), _per_level_emitted(o_runs, K)
+    assert g == o
+    levels = {lv for _, lv in g}
+    assert len(g) >= len(c.q) and len(levels) >= 3, (len(g), sorted(levels))
+
+
 @pytest.mark.parametrize("k", [1, 33, 100])
 @pytest.mark.parametrize("engine", [0, 1, 2])
 def test_search_parity_k(cases, k, engine):
