@@ -2,9 +2,12 @@
 config 1 completely, config 2 (1M x 100, FHT cross-polytope, 4 GiB budget -> L = 241) on sampled
 outputs the oracle computes one by one -- three whole repetition tables, the normalised data, and
 the complete searches of 200 queries (the oracle builds only the repetitions they touch); configs
-3, 4 and 6 (1M x 300 planted, 1M x 960 pooled with k = 100, the paper's SYNTHETIC set) with whole
-tables, every query's codes and sketches, properties of every query's result, and the complete
-searches of 16 (8) sampled queries element by element."""
+3, 4 and 6 (1M x 300 planted, 1M x 960 pooled with k = 100, the paper's SYNTHETIC set) in two parts:
+the configured index with the normalised data, slots, pool selections, (config 3) two whole tables,
+every query's codes and sketches and the properties of every query's result; then, on an index of
+the same 1M points with 48 repetitions (pooled: a 768-bit pool, 8 sketch words -- what the plain-C
+oracle can hash within the suite's time limit), two whole tables and the complete searches of 16
+(8) sampled queries element by element."""
 import numpy as np
 import pytest
 
@@ -122,33 +125,47 @@ def _recall(x_t, q_t, ids, k):
     return float(np.mean(ex >= kth[:, None] - 1e-5))
 
 
+# reduced index of the element-wise comparison at n = 1M (the oracle hashes every point for every
+# repetition / pool function and sketch word it needs, in plain C: the configured L = 458 / 830 / 459
+# repetitions, 3 072 pool bits and 32 sketch words cost 4-5 Tflop per config, most of a 20-minute
+# suite): 48 repetitions (beyond the eager hashing depth and the third round), for the pooled
+# configs a 768-bit pool and 8 sketch words
+_REDUCED = {3: dict(reps=48), 4: dict(reps=48, pool_bits=768, sketch_words=8), 6: dict(reps=48, pool_bits=768, sketch_words=8)}
+
+
 @pytest.mark.parametrize("cfg", [3, 4, 6])
 def test_config34_full(cfg):
     c = synth.CONFIGS[cfg]
     data, q = synth.config_data(cfg)
     x_t = torch.from_numpy(data).to(DEV)
     q_t = torch.from_numpy(q).to(DEV)
+    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
+    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
+    pooled = strat == O.POOL
+
+    # ---- part A: the configured index (budget -> L), the launch bench.py times
     g = pfg.Index(x_t, c["budget"], c["family"], seed=1, strategy=c["strategy"])
     L = g.info["reps"]
     assert L == pfg.derive_reps(c["n"], c["d"], c["family"], c["budget"], strategy=c["strategy"])[0]
-    strat = O.POOL if c["strategy"] == "pool" else O.INDEPENDENT
-    fam = {"simhash": O.HP, "fht_cp": O.FHTCP, "cp": O.CP}[c["family"]]
-    o = O.OracleIndex(data, fam, L=L, seed=1, strategy=strat, lazy=True)
-    # build side: data, slots, pool selections, two whole repetition tables with their inline
-    # sketch words, prefix tables
-    assert np.array_equal(g.export_data().view(np.uint32), o.data().view(np.uint32))
+    # the functions (slots, pool selections, query codes and sketches, the stop rule) do not depend on
+    # the data: for the pooled configs the oracle of part A holds the first 2 000 points only (its
+    # tables are not used); the independent config 3 builds the two tables compared below lazily
+    o = O.OracleIndex(data if not pooled else data[:2000], fam, L=L, seed=1, strategy=strat, lazy=True)
+    xn = O.normalize(data)
+    assert np.array_equal(g.export_data().view(np.uint32), xn.view(np.uint32))
     assert np.array_equal(g.export_slots(), o.slots())
-    if strat == O.POOL:
+    if pooled:
         assert np.array_equal(g.export_pool_sel(), o.pool_sel())
-    osk = o.sketches()
-    slots = o.slots()
-    for j in (0, L - 1):
-        tab = g.export_table(j)
-        codes, oid = o.rep(j)
-        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
-        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), oid), j
-        assert np.array_equal(tab[:, 1], osk[oid, slots[j]]), j
-        assert np.array_equal(g.export_prefix(j), o.prefix_table(j)), j
+    else:
+        osk = o.sketches()
+        slots = o.slots()
+        for j in (0, L - 1):
+            tab = g.export_table(j)
+            codes, oid = o.rep(j)
+            assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+            assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), oid), j
+            assert np.array_equal(tab[:, 1], osk[oid, slots[j]]), j
+            assert np.array_equal(g.export_prefix(j), o.prefix_table(j)), j
     # query side: codes and sketches of every query bit-exact
     gc, gs = g.hash_queries(q)
     oc, os_ = o.hash(q)
@@ -162,22 +179,40 @@ def test_config34_full(cfg):
     sel = np.arange(0, len(q), max(1, len(q) // 16))
     cap = 1 << 15
     sids, ssims, sst, tr = g.search(torch.from_numpy(q[sel]).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
-    # element by element against the oracle on the sampled queries (16; 8 for config 6, whose queries
-    # evaluate ~94 % of the points): the oracle's repetition tables are built first (in parallel over
-    # the points; the pooled configs 4 and 6 evaluate each pool function once per point)
-    for j in range(L):
-        o.prefix_table(j)
-    esel = sel if cfg != 6 else sel[::2]
-    if cfg == 6:
-        sids, ssims, sst, tr = g.search(torch.from_numpy(q[esel]).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
-    orr = o.search(q[esel], c["k"], c["recall"], rep_chunk=pfg.DEFAULT_REP_CHUNK, trace_cap=cap, threads=8)
-    _search_equal((sids, ssims, sst, tr), orr, cap)
-    assert np.array_equal(sids.cpu().numpy(), ids[esel]) and np.array_equal(sst["j_stop"], st["j_stop"][esel])
-    xn, qn = O.normalize(data), O.normalize(q[esel])
-    for r in range(len(esel)):
+    assert np.array_equal(sids.cpu().numpy(), ids[sel]) and np.array_equal(sst["j_stop"], st["j_stop"][sel])
+    qn = O.normalize(q[sel])
+    for r in range(len(sel)):
         ev = tr[r, :min(cap, int(sst["evaluated"][r]))]
         assert len(set(ev.tolist())) == len(ev)
         if sst["evaluated"][r] <= cap:
-            s = np.array([O.sim(qn[r], xn[e]) for e in ev], np.float32)
-            order = np.lexsort((ev, -s))[:c["k"]]
-            assert np.array_equal(ev[order].astype(np.int64), ids[esel[r]]), r
+            sv = np.array([O.sim(qn[r], xn[e]) for e in ev], np.float32)
+            order = np.lexsort((ev, -sv))[:c["k"]]
+            assert np.array_equal(ev[order].astype(np.int64), ids[sel[r]]), r
+    del g, o
+
+    # ---- part B: element by element against the oracle at n = 1M on the reduced index (_REDUCED):
+    # two whole tables with their inline sketch words and prefix tables, then the complete searches
+    # of 16 sampled queries (8 for config 6, whose queries evaluate most of the points): counters,
+    # stop points, evaluated sets, ids, similarities.  With 48 repetitions the queries descend
+    # further than under the configured L (more levels, the bitmap / visit-tag modes, k = 100)
+    rd = _REDUCED[cfg]
+    Lb, pb, Mb = rd["reps"], rd.get("pool_bits", 3072), rd.get("sketch_words", 32)
+    g = pfg.Index(x_t, 0, c["family"], seed=1, strategy=c["strategy"], reps=Lb, pool_bits=pb, sketch_words=Mb)
+    o = O.OracleIndex(data, fam, L=Lb, seed=1, strategy=strat, pool_bits=pb, M=Mb)
+    osk = o.sketches()
+    slots = o.slots()
+    for j in (0, Lb - 1):
+        tab = g.export_table(j)
+        codes, oid = o.rep(j)
+        assert np.array_equal((tab[:, 0] >> np.uint64(32)).astype(np.uint32), codes), j
+        assert np.array_equal((tab[:, 0] & np.uint64(0xFFFFFFFF)).astype(np.uint32), oid), j
+        assert np.array_equal(tab[:, 1], osk[oid, slots[j]]), j
+        assert np.array_equal(g.export_prefix(j), o.prefix_table(j)), j
+    esel = sel if cfg != 6 else sel[::2]
+    gres = g.search(torch.from_numpy(q[esel]).to(DEV), c["k"], c["recall"], stats=True, trace_cap=cap)
+    orr = o.search(q[esel], c["k"], c["recall"], rep_chunk=pfg.DEFAULT_REP_CHUNK, trace_cap=cap, threads=8)
+    _search_equal(gres, orr, cap)
+    # the same queries inside the whole batch (the bench's launch shape): identical results
+    ids_b, sims_b, st_b = g.search(q_t, c["k"], c["recall"], stats=True)
+    assert np.array_equal(ids_b.cpu().numpy()[esel], gres[0].cpu().numpy())
+    assert np.array_equal(st_b["j_stop"][esel], gres[2]["j_stop"]) and np.array_equal(st_b["evaluated"][esel], gres[2]["evaluated"])
