@@ -198,6 +198,27 @@ def oracle_recall(X, qs, ids, k):
     return float(np.mean([len(set(a) & set(b)) / k for a, b in zip(ids.tolist(), bi.tolist())]))
 
 
+def config_record(args, c, n, nq, reps, world=1, sharded=False, replicas=False):
+    """the `config` object of the JSON line: the workload and the search options, the same for the
+    product arm and the reference arm (which runs the oracle on this workload with these options;
+    engine / rounds / pipelines / l2 describe the product's launch and are carried verbatim)"""
+    weak = "shard_n" in c
+    return {"workload": f"config{args.config}: {c['name']}" + WORKLOAD_NOTE.get(args.config, "")
+            + (" [int16 fixed-point rows, R-25]" if args.storage == "i16" else "")
+            + (f" ({c['shard_n']} rows per GPU)" if weak else ""),
+            "n": n, "d": c["d"], "nq": nq, "k": c["k"], "recall_target": args.recall, "family": c["family"],
+            "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": reps,
+            "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "storage": args.storage,
+            "tau_rule": ["quantile (R-26)", "expected distance (R-15)"][args.tau_rule],
+            "engine": args.engine, "rounds": args.rounds or 5,
+            "pipelines": args.pipelines or 1,
+            "l2": "flushed (512 MiB write) between timed steps",
+            "parallelism": (f"data-sharded x{world}" if sharded else
+                            f"query replicas x{world} (every GPU builds the whole index and answers a batch "
+                            f"of {nq} queries independently; no collective on the data path)" if replicas
+                            else "single GPU")}
+
+
 def run_reference(args):
     """The CPU oracle as it stands (test infrastructure), timed on all host cores (OpenMP over the
     queries), each step a bounded sample of the workload's queries."""
@@ -211,12 +232,14 @@ def run_reference(args):
     X, q = oracle_index(args.config)
     sample = args.ref_sample
     qs = q[:sample]
-    X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk)   # builds the repetitions it touches
+    X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk, tau_rule=args.tau_rule,
+             uniform_chunks=args.uniform_chunks)   # builds the repetitions it touches
     setup = time.time() - t0
     times = []
     for s in range(args.warmup + args.steps):
         t = time.perf_counter()
-        ids, sims, tr = X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk, threads=cores)
+        ids, sims, tr = X.search(qs, c["k"], args.recall, rep_chunk=args.rep_chunk, threads=cores, tau_rule=args.tau_rule,
+                                  uniform_chunks=args.uniform_chunks)
         el = time.perf_counter() - t
         if s >= args.warmup:
             times.append(el)
@@ -225,11 +248,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"config{args.config}: {c['name']}" + WORKLOAD_NOTE.get(args.config, ""),
-                   "n": c["n"], "d": c["d"], "nq": nq, "k": c["k"],
-                   "recall_target": args.recall, "family": c["family"], "reps": c["reps"] or c["L"],
-                   "rep_chunk": args.rep_chunk},
+        "higher_is_better": True,
+        "scaling": "weak" if ("shard_n" in c or args.parallel == "queries") else "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_record(args, c, c.get("shard_n", c["n"]), nq, c["reps"] or c["L"]),
         "recall": oracle_recall(X, qs, ids, c["k"]),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
                          "cpu_model": cpu_model(),
@@ -513,20 +535,7 @@ def main():
             "vs_baseline": None,
             "dtype": "f32" if args.storage == "f32" else "i16 rows (int32 dot), f32 hashing",
             "data": "synthetic",
-            "config": {"workload": f"config{args.config}: {c['name']}" + WORKLOAD_NOTE.get(args.config, "")
-                       + (" [int16 fixed-point rows, R-25]" if args.storage == "i16" else "")
-                       + (f" ({c['shard_n']} rows per GPU)" if weak else ""),
-                       "n": n, "d": d, "nq": nq, "k": k, "recall_target": args.recall, "family": c["family"],
-                       "strategy": c["strategy"], "budget_bytes_per_gpu": c["budget"], "reps": info["reps"],
-                       "rep_chunk": args.rep_chunk, "uniform_chunks": args.uniform_chunks, "storage": args.storage,
-                       "tau_rule": ["quantile (R-26)", "expected distance (R-15)"][args.tau_rule],
-                       "engine": args.engine, "rounds": args.rounds or 5,
-                       "pipelines": args.pipelines or 1,
-                       "l2": "flushed (512 MiB write) between timed steps",
-                       "parallelism": (f"data-sharded x{world}" if sharded else
-                                       f"query replicas x{world} (every GPU builds the whole index and answers a batch "
-                                       f"of {nq} queries independently; no collective on the data path)" if replicas
-                                       else "single GPU")},
+            "config": config_record(args, c, n, nq, info["reps"], world, sharded, replicas),
             "recall": rec,
             "build_s": build_s,
             "roofline": ksims_roofline,
