@@ -5,7 +5,7 @@ PAPER.md:504-532), the memory budget (Fig. 3) and the segment 
 PAPER.md:920-934).  For each setting: queries/s (CUDA events around the search, inputs resident,
 median of 5), measured recall@k against the exact top-k, and the per-query counters.
 
-  python tools/paper_sweeps.py [--out profiles/r01/sweeps_config2.jsonl]
+  python tools/paper_sweeps.py [--out profiles/r02/sweeps_config2.jsonl]
 """
 import argparse
 import json
@@ -24,7 +24,7 @@ import synth  # noqa: E402
 from bench import ground_truth, recall_of  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "sweeps_config2.jsonl"))
+ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02", "sweeps_config2.jsonl"))
 ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
 
@@ -63,9 +63,11 @@ def run(idx, label, recall, **sopts):
 
 idx = pfg.Index(X, c["budget"], c["family"], seed=1)
 for rec in (0.5, 0.9, 0.99):
-    run(idx, "recall", rec)
+    run(idx, "recall", rec)                           # the default quantile filter (R-26)
+for rec in (0.5, 0.9, 0.99):
+    run(idx, "recall_expected_distance", rec, tau_rule=1)
 for eps in (-0.2, 0.0, 0.2, 0.5):
-    run(idx, "eps", 0.9, eps=eps)
+    run(idx, "eps", 0.9, eps=eps, tau_rule=1)         # the paper's (1 + eps) x expected distance (R-15)
 run(idx, "filter_off", 0.9, use_filter=False)
 for B in (1, 4, 12, 24):
     run(idx, "segment", 0.9, segment=B)
